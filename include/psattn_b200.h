@@ -1,0 +1,163 @@
+/* psattn_b200.h — device-batched extensions of the PSA C ABI (B200, sm_100a).
+ *
+ * psattn.h keeps the reference's one-query-at-a-time entry points. A serving
+ * loop (reference serving.cpp:161-202 drives psa_attention_batched /
+ * topk_attention once per layer per decode step) needs instead ONE stream-ordered
+ * launch covering every (request, layer, q-head) of a step with no host
+ * round-trip per microbatch. That is what this header adds (SURVEY §8b
+ * "What the replacement adds"):
+ *
+ *   - psattn_pool_*   a unified paged KV block pool in HBM shared by all
+ *                     layers (reference TieredBlockStore's Unified policy,
+ *                     store.cpp:11-22) with per-slot metadata built on device
+ *                     (reference build_metadata, metadata.cpp:8-34);
+ *   - psattn_run_batch  scoring (criticality_score, metadata.cpp:41-72),
+ *                     ordering (rank_by_scores, metadata.cpp:87-96) and the
+ *                     progressive early-terminating loop (engine.cpp:92-171,
+ *                     211-231, 240-260) for a whole batch, launched on the
+ *                     caller's cudaStream_t;
+ *   - psattn_synth_*  the seekable synthetic KV/query generator used by the
+ *                     benchmark and the parity tests (same values on host and
+ *                     device, bit for bit).
+ *
+ * All pointers in psattn_batch are DEVICE pointers unless stated. Streams are
+ * passed as void* (a cudaStream_t), NULL = legacy default stream.
+ */
+#ifndef PSATTN_B200_H
+#define PSATTN_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#include "psattn.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { PSATTN_KV_F32 = 0, PSATTN_KV_BF16 = 1 };
+
+typedef struct psattn_pool psattn_pool;
+
+typedef struct {
+    int32_t dim;          /* head dimension d (1..256) */
+    int32_t block_tokens; /* tokens per slot B (1..32) */
+    int32_t kv_dtype;     /* PSATTN_KV_* */
+    int32_t reserved;
+    int64_t n_slots;      /* slot capacity */
+} psattn_pool_desc;
+
+/* Raw device layout, for callers that write K/V themselves (e.g. a decode
+ * step's KV append) and then call psattn_pool_build_metadata. */
+typedef struct {
+    void* kv;            /* [n_slots][2][block_tokens][dim] kv_dtype: K rows then V rows */
+    void* meta;          /* [n_slots] records of {mean[dim] f32, lo[dim] kv, hi[dim] kv} */
+    int32_t* ntok;       /* [n_slots] valid tokens per slot */
+    int64_t slot_bytes;  /* bytes per KV slot */
+    int64_t meta_bytes;  /* bytes per metadata record */
+} psattn_pool_layout;
+
+int psattn_pool_create(const psattn_pool_desc* desc, psattn_pool** out_pool);
+void psattn_pool_destroy(psattn_pool* pool);
+int psattn_pool_get_desc(const psattn_pool* pool, psattn_pool_desc* out);
+int psattn_pool_get_layout(const psattn_pool* pool, psattn_pool_layout* out);
+
+/* Host fp32 K/V ([n][block_tokens][dim] each, rows past ntok[i] ignored) into
+ * slots[i] (host array), then builds their metadata. Synchronous. */
+int psattn_pool_put_blocks(psattn_pool* pool, int64_t n, const int32_t* slots, const int32_t* ntok,
+                           const float* keys, const float* values);
+
+/* Rebuilds metadata (lo/hi/mean) for slots [slot_begin, slot_end) on device. */
+int psattn_pool_build_metadata(psattn_pool* pool, int64_t slot_begin, int64_t slot_end, void* stream);
+
+/* Copies back metadata of one slot as fp32 (mean, lo, hi: dim floats each). */
+int psattn_pool_read_metadata(psattn_pool* pool, int64_t slot, float* mean, float* lo, float* hi);
+
+/* ---- Batched progressive attention ---- */
+
+typedef struct {
+    /* shape */
+    int32_t n_units;       /* independent (request, layer, kv-head) block lists */
+    int32_t group;         /* q-heads per kv-head (GQA group g), 1..8 */
+    int32_t dim;           /* must equal the pool's dim */
+    int32_t max_blocks;    /* max list length over units (host-known) */
+    int64_t total_blocks;  /* list_off[n_units] (host-known) */
+    /* inputs (device) */
+    const float* q;            /* [n_units][group][dim] */
+    const int32_t* slots;      /* page table: unit u's list = slots[list_off[u] .. list_off[u+1]) */
+    const int64_t* list_off;   /* [n_units + 1] */
+    /* Lists are in ascending block-id order (a page table's natural order), so
+       the reference's tie rule "score desc, block_id asc" is list position asc. */
+    /* config (reference psattn_config semantics) */
+    double epsilon;
+    int32_t microbatch_size;
+    int32_t estimator;         /* PSATTN_EST_* */
+    int32_t ranking_mode;      /* PSATTN_RANK_* */
+    int32_t audit_coverage;
+    double scale_override;
+    int64_t topk;              /* 0: PSA threshold stop; >0: top-k budget (epsilon forced to 1) */
+    /* outputs (device) */
+    float* out;                /* [n_units][group][dim] */
+    int64_t* blocks_processed; /* [n_units*group] */
+    double* est_coverage;      /* [n_units*group] */
+    double* true_coverage;     /* optional [n_units*group]; -1 without audit */
+    int32_t* terminated;       /* [n_units*group] */
+    /* optional output: rank-ordered list positions per head, at
+       ranked_pos[list_off[u]*group + h*n_u + r]. NULL = kept in workspace. */
+    int32_t* ranked_pos;
+    /* optional output [total_blocks*group], same indexing: at every microbatch
+       boundary rank r that was evaluated, the coverage estimate after rank r. */
+    double* iter_est;
+} psattn_batch;
+
+/* Workspace bytes psattn_run_batch needs for this batch shape. */
+size_t psattn_batch_workspace_bytes(const psattn_batch* b);
+
+/* One stream-ordered launch sequence (score -> order -> progressive), no host
+ * synchronisation. workspace: device memory of psattn_batch_workspace_bytes. */
+int psattn_run_batch(psattn_pool* pool, const psattn_batch* b, void* workspace, void* stream);
+
+/* Per-unit count of distinct blocks processed by any head of the group (the
+ * GQA union the algorithmic byte count uses), after psattn_run_batch on the
+ * same stream and workspace. out_union: device int64 [n_units]. */
+int psattn_batch_union_blocks(const psattn_batch* b, void* workspace, int64_t* out_union, void* stream);
+
+/* Per-kernel launch counts of the last psattn_run_batch (score, order, progressive). */
+int psattn_batch_last_launches(int32_t* out_count);
+
+/* ---- Seekable synthetic workload (bench + parity; not on the attention path) ----
+ * Values are a pure function of (seed, unit_id, block, token, dim), identical on
+ * host and device. Keys: approx-N(0,1) noise, plus skew*direction on planted
+ * blocks (pattern of reference workload.cpp:84-122); values: per-block centroid
+ * + 0.25*noise. planted_per_block: probability a block is planted (0 = isotropic). */
+typedef struct {
+    uint64_t seed;
+    int32_t dim;
+    int32_t block_tokens;
+    float skew;
+    float planted_prob;
+    int32_t round_bf16;   /* round K/V to bf16 values (what a bf16 pool stores) */
+    int32_t reserved;
+} psattn_synth_params;
+
+/* Unit direction (dim floats) for unit_id. */
+void psattn_synth_direction(const psattn_synth_params* p, int64_t unit_id, float* out);
+/* Query of q-head `head` for unit_id: normalize(dir + 0.1*g_head) * sqrt(dim). */
+void psattn_synth_query(const psattn_synth_params* p, int64_t unit_id, int32_t head, float* out);
+/* Host copy of one unit's blocks [first_block, first_block+n_blocks): keys/values
+ * [n_blocks][block_tokens][dim]; tokens past n_tokens_total are zero. */
+void psattn_synth_unit_host(const psattn_synth_params* p, int64_t unit_id, int64_t first_block,
+                            int64_t n_blocks, int64_t n_tokens_total, float* keys, float* values);
+int psattn_synth_is_planted(const psattn_synth_params* p, int64_t unit_id, int64_t block);
+
+/* Device fill: for each unit u (host arrays of n_units entries): blocks
+ * [0, ceil(tokens[u]/B)) go to slots slot_off[u] + b; sets ntok and builds metadata. */
+int psattn_pool_fill_synthetic(psattn_pool* pool, const psattn_synth_params* p, int32_t n_units,
+                               const int64_t* unit_ids, const int64_t* slot_off,
+                               const int64_t* tokens, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PSATTN_B200_H */

@@ -1,0 +1,126 @@
+"""torch-tensor helpers around the device-batched C ABI (include/psattn_b200.h).
+
+torch provides device memory and the stream; every kernel launched here is one
+of ours (libpsattn_b200.so). Nothing in this module computes attention.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import capi
+from .capi import Batch, PoolDesc, PoolLayout, check, lib
+
+
+def _stream_ptr(stream) -> C.c_void_p:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def _dp(t: torch.Tensor | None) -> C.c_void_p | None:
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+class DevicePool:
+    """psattn_pool: the unified paged KV block pool in HBM (slots shared by all layers)."""
+
+    def __init__(self, dim: int, block_tokens: int, kv_dtype: int, n_slots: int):
+        d = PoolDesc(dim, block_tokens, kv_dtype, 0, n_slots)
+        self.h = C.c_void_p()
+        check(lib.psattn_pool_create(C.byref(d), C.byref(self.h)))
+        self.dim, self.block_tokens, self.kv_dtype, self.n_slots = dim, block_tokens, kv_dtype, n_slots
+
+    def close(self):
+        if getattr(self, "h", None) is not None and self.h.value:
+            lib.psattn_pool_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
+
+    def layout(self) -> PoolLayout:
+        lay = PoolLayout()
+        check(lib.psattn_pool_get_layout(self.h, C.byref(lay)))
+        return lay
+
+    def fill_synthetic(self, params: capi.SynthParams, unit_ids, slot_off, tokens, stream=None):
+        u = np.ascontiguousarray(unit_ids, np.int64)
+        s = np.ascontiguousarray(slot_off, np.int64)
+        t = np.ascontiguousarray(tokens, np.int64)
+        check(lib.psattn_pool_fill_synthetic(self.h, C.byref(params), u.size, capi._p(u), capi._p(s), capi._p(t),
+                                             _stream_ptr(stream)))
+
+    def put_blocks(self, slots, ntok, keys, values):
+        s = np.ascontiguousarray(slots, np.int32)
+        n = np.ascontiguousarray(ntok, np.int32)
+        k = np.ascontiguousarray(keys, np.float32)
+        v = np.ascontiguousarray(values, np.float32)
+        check(lib.psattn_pool_put_blocks(self.h, s.size, capi._p(s), capi._p(n), capi._p(k), capi._p(v)))
+
+    def build_metadata(self, s0, s1, stream=None):
+        check(lib.psattn_pool_build_metadata(self.h, s0, s1, _stream_ptr(stream)))
+
+    def read_metadata(self, slot):
+        m, lo, hi = (np.zeros(self.dim, np.float32) for _ in range(3))
+        check(lib.psattn_pool_read_metadata(self.h, slot, capi._p(m), capi._p(lo), capi._p(hi)))
+        return m, lo, hi
+
+
+@dataclass
+class BatchConfig:
+    epsilon: float = 0.95
+    microbatch_size: int = 1
+    estimator: int = capi.PSATTN_EST_CUBOID_MEAN
+    ranking_mode: int = capi.PSATTN_RANK_ESTIMATED
+    audit_coverage: int = 0
+    scale_override: float = 0.0
+    topk: int = 0
+
+
+class BatchRun:
+    """One psattn_batch: device page tables + outputs + workspace, launched on a torch stream."""
+
+    def __init__(self, pool: DevicePool, q: torch.Tensor, slots: torch.Tensor, list_off: torch.Tensor,
+                 max_blocks: int, cfg: BatchConfig, want_ranked: bool = False, want_iter: bool = False):
+        assert q.is_cuda and q.dtype == torch.float32 and q.dim() == 3
+        assert slots.dtype == torch.int32 and list_off.dtype == torch.int64
+        self.pool = pool
+        self.n_units, self.group, self.dim = q.shape
+        self.total = int(slots.numel())
+        dev = q.device
+        nq = self.n_units * self.group
+        self.q, self.slots, self.list_off = q.contiguous(), slots.contiguous(), list_off.contiguous()
+        self.out = torch.empty((self.n_units, self.group, self.dim), dtype=torch.float32, device=dev)
+        self.bp = torch.empty(nq, dtype=torch.int64, device=dev)
+        self.est = torch.empty(nq, dtype=torch.float64, device=dev)
+        self.tcov = torch.empty(nq, dtype=torch.float64, device=dev)
+        self.term = torch.empty(nq, dtype=torch.int32, device=dev)
+        self.ranked = torch.empty(self.total * self.group, dtype=torch.int32, device=dev) if want_ranked else None
+        self.iest = torch.empty(self.total * self.group, dtype=torch.float64, device=dev) if want_iter else None
+        b = Batch()
+        b.n_units, b.group, b.dim, b.max_blocks, b.total_blocks = self.n_units, self.group, self.dim, max_blocks, \
+            self.total
+        b.q, b.slots, b.list_off = _dp(self.q), _dp(self.slots), _dp(self.list_off)
+        b.epsilon, b.microbatch_size, b.estimator = cfg.epsilon, cfg.microbatch_size, cfg.estimator
+        b.ranking_mode, b.audit_coverage, b.scale_override, b.topk = cfg.ranking_mode, cfg.audit_coverage, \
+            cfg.scale_override, cfg.topk
+        b.out, b.blocks_processed, b.est_coverage = _dp(self.out), _dp(self.bp), _dp(self.est)
+        b.true_coverage, b.terminated = _dp(self.tcov), _dp(self.term)
+        b.ranked_pos, b.iter_est = _dp(self.ranked), _dp(self.iest)
+        self.b = b
+        ws = int(lib.psattn_batch_workspace_bytes(C.byref(b)))
+        self.ws = torch.empty(max(ws, 256), dtype=torch.uint8, device=dev)
+        self.union = torch.zeros(self.n_units, dtype=torch.int64, device=dev)
+
+    def run(self, stream=None) -> int:
+        check(lib.psattn_run_batch(self.pool.h, C.byref(self.b), _dp(self.ws), _stream_ptr(stream)))
+        n = C.c_int32()
+        lib.psattn_batch_last_launches(C.byref(n))
+        return n.value
+
+    def union_blocks(self, stream=None) -> torch.Tensor:
+        check(lib.psattn_batch_union_blocks(C.byref(self.b), _dp(self.ws), _dp(self.union), _stream_ptr(stream)))
+        return self.union

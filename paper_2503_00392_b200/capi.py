@@ -1,0 +1,263 @@
+"""ctypes mirror of the C ABI (include/psattn.h, include/psattn_b200.h).
+
+Names, argument meaning and status codes follow the reference's C ABI
+(/root/reference/proj/include/psattn.h). Every compute call goes to the CUDA
+library ``_lib/libpsattn_b200.so``; there is no Python or CPU fallback: if the
+library is missing, importing this module raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "libpsattn_b200.so")
+
+PSATTN_OK = 0
+PSATTN_ERR_INVALID_ARGUMENT = 1
+PSATTN_ERR_NOT_FOUND = 2
+PSATTN_ERR_RUNTIME = 3
+
+PSATTN_POOL_UNIFIED, PSATTN_POOL_LAYER_PARTITIONED = 0, 1
+PSATTN_EVICT_LRU, PSATTN_EVICT_FIFO = 0, 1
+PSATTN_EST_MEAN, PSATTN_EST_CUBOID_UPPER, PSATTN_EST_CUBOID_MEAN = 0, 1, 2
+PSATTN_RANK_ESTIMATED, PSATTN_RANK_ORACLE = 0, 1
+PSATTN_KV_F32, PSATTN_KV_BF16 = 0, 1
+
+
+class StoreOptions(C.Structure):
+    _fields_ = [("fast_capacity_slots", C.c_int32), ("n_layers", C.c_int32), ("pool_policy", C.c_int32),
+                ("eviction_policy", C.c_int32), ("miss_latency_ms", C.c_double)]
+
+
+class Config(C.Structure):
+    _fields_ = [("epsilon", C.c_double), ("microbatch_size", C.c_int32), ("block_size", C.c_int32),
+                ("estimator", C.c_int32), ("ranking_mode", C.c_int32), ("audit_coverage", C.c_int32),
+                ("scale_override", C.c_double)]
+
+
+class RunStats(C.Structure):
+    _fields_ = [("blocks_processed", C.c_uint64), ("total_blocks", C.c_uint64), ("estimated_coverage", C.c_double),
+                ("true_coverage", C.c_double), ("terminated_early", C.c_int32)]
+
+
+class CacheStats(C.Structure):
+    _fields_ = [("hits", C.c_uint64), ("misses", C.c_uint64), ("evictions", C.c_uint64),
+                ("bytes_transferred", C.c_uint64)]
+
+
+class PoolDesc(C.Structure):
+    _fields_ = [("dim", C.c_int32), ("block_tokens", C.c_int32), ("kv_dtype", C.c_int32), ("reserved", C.c_int32),
+                ("n_slots", C.c_int64)]
+
+
+class PoolLayout(C.Structure):
+    _fields_ = [("kv", C.c_void_p), ("meta", C.c_void_p), ("ntok", C.c_void_p), ("slot_bytes", C.c_int64),
+                ("meta_bytes", C.c_int64)]
+
+
+class Batch(C.Structure):
+    _fields_ = [("n_units", C.c_int32), ("group", C.c_int32), ("dim", C.c_int32), ("max_blocks", C.c_int32),
+                ("total_blocks", C.c_int64),
+                ("q", C.c_void_p), ("slots", C.c_void_p), ("list_off", C.c_void_p),
+                ("epsilon", C.c_double), ("microbatch_size", C.c_int32), ("estimator", C.c_int32),
+                ("ranking_mode", C.c_int32), ("audit_coverage", C.c_int32), ("scale_override", C.c_double),
+                ("topk", C.c_int64),
+                ("out", C.c_void_p), ("blocks_processed", C.c_void_p), ("est_coverage", C.c_void_p),
+                ("true_coverage", C.c_void_p), ("terminated", C.c_void_p), ("ranked_pos", C.c_void_p),
+                ("iter_est", C.c_void_p)]
+
+
+class SynthParams(C.Structure):
+    _fields_ = [("seed", C.c_uint64), ("dim", C.c_int32), ("block_tokens", C.c_int32), ("skew", C.c_float),
+                ("planted_prob", C.c_float), ("round_bf16", C.c_int32), ("reserved", C.c_int32)]
+
+
+def _load() -> C.CDLL:
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+                          "(the PSA path has no CPU fallback)")
+    L = C.CDLL(LIB_PATH)
+    vp, i32, i64, u64, dbl, sz = C.c_void_p, C.c_int32, C.c_int64, C.c_uint64, C.c_double, C.c_size_t
+    L.psattn_last_error.restype = C.c_char_p
+    L.psattn_version.restype = C.c_char_p
+    L.psattn_store_options_default.argtypes = [C.POINTER(StoreOptions)]
+    L.psattn_store_create.argtypes = [C.POINTER(StoreOptions), C.POINTER(vp)]
+    L.psattn_store_destroy.argtypes = [vp]
+    L.psattn_store_put_block.argtypes = [vp, i64, i32, i64, i32, i32, vp, vp]
+    L.psattn_store_release_request.argtypes = [vp, i64]
+    L.psattn_store_contains.argtypes = [vp, i64, C.POINTER(C.c_int)]
+    L.psattn_store_stats.argtypes = [vp, C.POINTER(CacheStats)]
+    L.psattn_config_default.argtypes = [C.POINTER(Config)]
+    L.psattn_run_query.argtypes = [vp, vp, i32, vp, sz, C.POINTER(Config), vp, C.POINTER(RunStats)]
+    L.psattn_run_topk.argtypes = [vp, vp, i32, vp, sz, sz, C.POINTER(Config), vp, C.POINTER(RunStats)]
+    L.psattn_pool_create.argtypes = [C.POINTER(PoolDesc), C.POINTER(vp)]
+    L.psattn_pool_destroy.argtypes = [vp]
+    L.psattn_pool_get_desc.argtypes = [vp, C.POINTER(PoolDesc)]
+    L.psattn_pool_get_layout.argtypes = [vp, C.POINTER(PoolLayout)]
+    L.psattn_pool_put_blocks.argtypes = [vp, i64, vp, vp, vp, vp]
+    L.psattn_pool_build_metadata.argtypes = [vp, i64, i64, vp]
+    L.psattn_pool_read_metadata.argtypes = [vp, i64, vp, vp, vp]
+    L.psattn_batch_workspace_bytes.argtypes = [C.POINTER(Batch)]
+    L.psattn_batch_workspace_bytes.restype = sz
+    L.psattn_run_batch.argtypes = [vp, C.POINTER(Batch), vp, vp]
+    L.psattn_batch_union_blocks.argtypes = [C.POINTER(Batch), vp, vp, vp]
+    L.psattn_batch_last_launches.argtypes = [C.POINTER(i32)]
+    L.psattn_synth_direction.argtypes = [C.POINTER(SynthParams), i64, vp]
+    L.psattn_synth_query.argtypes = [C.POINTER(SynthParams), i64, i32, vp]
+    L.psattn_synth_unit_host.argtypes = [C.POINTER(SynthParams), i64, i64, i64, i64, vp, vp]
+    L.psattn_synth_is_planted.argtypes = [C.POINTER(SynthParams), i64, i64]
+    L.psattn_pool_fill_synthetic.argtypes = [vp, C.POINTER(SynthParams), i32, vp, vp, vp, vp]
+    return L
+
+
+lib = _load()
+
+# Every function include/psattn.h and include/psattn_b200.h declare.
+EXPORTED = [
+    "psattn_last_error", "psattn_version", "psattn_store_options_default", "psattn_store_create",
+    "psattn_store_destroy", "psattn_store_put_block", "psattn_store_release_request", "psattn_store_contains",
+    "psattn_store_stats", "psattn_config_default", "psattn_run_query", "psattn_run_topk",
+    "psattn_pool_create", "psattn_pool_destroy", "psattn_pool_get_desc", "psattn_pool_get_layout",
+    "psattn_pool_put_blocks", "psattn_pool_build_metadata", "psattn_pool_read_metadata",
+    "psattn_batch_workspace_bytes", "psattn_run_batch", "psattn_batch_union_blocks", "psattn_batch_last_launches",
+    "psattn_synth_direction", "psattn_synth_query", "psattn_synth_unit_host", "psattn_synth_is_planted",
+    "psattn_pool_fill_synthetic",
+]
+
+
+def last_error() -> str:
+    return lib.psattn_last_error().decode()
+
+
+class PsattnError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"[{code}] {msg}")
+        self.code = code
+
+
+def check(rc: int) -> None:
+    if rc != PSATTN_OK:
+        raise PsattnError(rc, last_error())
+
+
+def _p(a: np.ndarray) -> C.c_void_p:
+    return C.c_void_p(a.ctypes.data)
+
+
+def store_options_default() -> StoreOptions:
+    o = StoreOptions()
+    lib.psattn_store_options_default(C.byref(o))
+    return o
+
+
+def config_default(**kw) -> Config:
+    c = Config()
+    lib.psattn_config_default(C.byref(c))
+    for k, v in kw.items():
+        setattr(c, k, v)
+    return c
+
+
+@dataclass
+class QueryOut:
+    output: np.ndarray
+    blocks_processed: int
+    total_blocks: int
+    estimated_coverage: float
+    true_coverage: float
+    terminated_early: bool
+
+
+class Store:
+    """psattn_store: device-resident block store (reference TieredBlockStore via C ABI)."""
+
+    def __init__(self, capacity=256, n_layers=1, policy=PSATTN_POOL_UNIFIED, eviction=PSATTN_EVICT_LRU,
+                 miss_latency_ms=0.0):
+        o = StoreOptions(capacity, n_layers, policy, eviction, miss_latency_ms)
+        self.h = C.c_void_p()
+        check(lib.psattn_store_create(C.byref(o), C.byref(self.h)))
+
+    def close(self):
+        if getattr(self, "h", None) is not None and self.h.value:
+            lib.psattn_store_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
+
+    def put(self, block_id, keys, values, layer=0, owner=0) -> int:
+        k = np.ascontiguousarray(keys, np.float32)
+        v = np.ascontiguousarray(values, np.float32)
+        return lib.psattn_store_put_block(self.h, block_id, layer, owner, k.shape[0], k.shape[1], _p(k), _p(v))
+
+    def put_blockset(self, bs, layer=0, owner=0):
+        for i in range(bs.n):
+            k, v = bs.block(i)
+            check(self.put(int(bs.ids[i]), k, v, layer, owner))
+
+    def release(self, owner) -> int:
+        return lib.psattn_store_release_request(self.h, owner)
+
+    def contains(self, block_id):
+        r = C.c_int(-1)
+        rc = lib.psattn_store_contains(self.h, block_id, C.byref(r))
+        return rc, bool(r.value)
+
+    def stats(self) -> dict:
+        s = CacheStats()
+        check(lib.psattn_store_stats(self.h, C.byref(s)))
+        return dict(hits=s.hits, misses=s.misses, evictions=s.evictions, bytes_transferred=s.bytes_transferred)
+
+    def _run(self, fn, q, ids, cfg, k=None):
+        q = np.ascontiguousarray(q, np.float32)
+        ids = np.ascontiguousarray(ids, np.int64)
+        out = np.zeros(q.size, np.float32)
+        st = RunStats()
+        args = [self.h, _p(q), q.size, _p(ids), ids.size]
+        if k is not None:
+            args.append(k)
+        args += [C.byref(cfg) if cfg is not None else None, _p(out), C.byref(st)]
+        rc = fn(*args)
+        return rc, QueryOut(out, int(st.blocks_processed), int(st.total_blocks), st.estimated_coverage,
+                            st.true_coverage, bool(st.terminated_early))
+
+    def run_query(self, q, ids, cfg=None):
+        return self._run(lib.psattn_run_query, q, ids, cfg)
+
+    def run_topk(self, q, ids, k, cfg=None):
+        return self._run(lib.psattn_run_topk, q, ids, cfg, k)
+
+
+def synth_params(seed=1, dim=128, block_tokens=16, skew=8.0, planted_prob=0.0, round_bf16=1) -> SynthParams:
+    return SynthParams(seed, dim, block_tokens, skew, planted_prob, round_bf16, 0)
+
+
+def synth_query(p: SynthParams, unit_id: int, head: int) -> np.ndarray:
+    out = np.zeros(p.dim, np.float32)
+    lib.psattn_synth_query(C.byref(p), unit_id, head, _p(out))
+    return out
+
+
+def synth_direction(p: SynthParams, unit_id: int) -> np.ndarray:
+    out = np.zeros(p.dim, np.float32)
+    lib.psattn_synth_direction(C.byref(p), unit_id, _p(out))
+    return out
+
+
+def synth_unit_host(p: SynthParams, unit_id: int, n_tokens: int, first_block=0, n_blocks=None):
+    """Host copy of a unit's K/V blocks: arrays [n_blocks, block_tokens, dim] (zero past n_tokens)."""
+    T = p.block_tokens
+    nb_total = (n_tokens + T - 1) // T
+    n_blocks = nb_total - first_block if n_blocks is None else n_blocks
+    k = np.zeros((n_blocks, T, p.dim), np.float32)
+    v = np.zeros((n_blocks, T, p.dim), np.float32)
+    lib.psattn_synth_unit_host(C.byref(p), unit_id, first_block, n_blocks, n_tokens, _p(k), _p(v))
+    return k, v
+
+
+def synth_is_planted(p: SynthParams, unit_id: int, block: int) -> bool:
+    return bool(lib.psattn_synth_is_planted(C.byref(p), unit_id, block))

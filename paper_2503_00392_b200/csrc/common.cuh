@@ -1,0 +1,158 @@
+// common.cuh — device helpers shared by the PSA kernels (sm_100a).
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define PSA_FULL 0xffffffffu
+
+namespace psa {
+
+// ---- KV element types ------------------------------------------------------
+template <typename KV> struct KVT;
+template <> struct KVT<float> {
+    static constexpr int kBytes = 4;
+    __device__ __forceinline__ static float to_f(float x) { return x; }
+    __device__ __forceinline__ static float from_f(float x) { return x; }
+};
+template <> struct KVT<__nv_bfloat16> {
+    static constexpr int kBytes = 2;
+    __device__ __forceinline__ static float to_f(__nv_bfloat16 x) { return __bfloat162float(x); }
+    __device__ __forceinline__ static __nv_bfloat16 from_f(float x) { return __float2bfloat16_rn(x); }
+};
+
+// Loads DPL consecutive KV elements starting at p (lane-contiguous mapping) as
+// floats. `full` = all DPL elements valid and the address is DPL-aligned; else
+// element-wise with the [0, lim) bound.
+template <int DPL>
+__device__ __forceinline__ void load_row(const float* __restrict__ p, bool full, int lim, float (&o)[DPL]) {
+    if (full) {
+        if constexpr (DPL % 4 == 0) {
+#pragma unroll
+            for (int j = 0; j < DPL; j += 4) {
+                const float4 v = __ldg(reinterpret_cast<const float4*>(p + j));
+                o[j] = v.x; o[j + 1] = v.y; o[j + 2] = v.z; o[j + 3] = v.w;
+            }
+        } else if constexpr (DPL == 2) {
+            const float2 v = __ldg(reinterpret_cast<const float2*>(p));
+            o[0] = v.x; o[1] = v.y;
+        } else {
+#pragma unroll
+            for (int j = 0; j < DPL; ++j) o[j] = __ldg(p + j);
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < DPL; ++j) o[j] = j < lim ? __ldg(p + j) : 0.0f;
+    }
+}
+
+template <int DPL>
+__device__ __forceinline__ void load_row(const __nv_bfloat16* __restrict__ p, bool full, int lim, float (&o)[DPL]) {
+    if (full) {
+        if constexpr (DPL % 8 == 0) {
+#pragma unroll
+            for (int j = 0; j < DPL; j += 8) {
+                const uint4 v = __ldg(reinterpret_cast<const uint4*>(p + j));
+                const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    o[j + 2 * k] = __uint_as_float(w[k] << 16);
+                    o[j + 2 * k + 1] = __uint_as_float(w[k] & 0xffff0000u);
+                }
+            }
+        } else if constexpr (DPL % 4 == 0) {
+#pragma unroll
+            for (int j = 0; j < DPL; j += 4) {
+                const uint2 v = __ldg(reinterpret_cast<const uint2*>(p + j));
+                o[j] = __uint_as_float(v.x << 16);
+                o[j + 1] = __uint_as_float(v.x & 0xffff0000u);
+                o[j + 2] = __uint_as_float(v.y << 16);
+                o[j + 3] = __uint_as_float(v.y & 0xffff0000u);
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < DPL; ++j) o[j] = __bfloat162float(p[j]);
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < DPL; ++j) o[j] = j < lim ? __bfloat162float(p[j]) : 0.0f;
+    }
+}
+
+// ---- warp reductions --------------------------------------------------------
+__device__ __forceinline__ float warp_max(float x) {
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) x = fmaxf(x, __shfl_xor_sync(PSA_FULL, x, o));
+    return x;
+}
+__device__ __forceinline__ double warp_max_d(double x) {
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) x = fmax(x, __shfl_xor_sync(PSA_FULL, x, o));
+    return x;
+}
+__device__ __forceinline__ double warp_sum_d(double x) {
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) x += __shfl_xor_sync(PSA_FULL, x, o);
+    return x;
+}
+
+// Reduce-scatter of N per-lane values (N power of two, <= 32) across the warp:
+// returns the warp-wide total of index (lane >> (5 - log2 N)); every index ends
+// on 32/N lanes. N-1 + log2(32/N) shuffles instead of 5N for N all-reduces.
+template <int N>
+__device__ __forceinline__ float reduce_scatter(float (&v)[N], int lane) {
+    int o = 16;
+#pragma unroll
+    for (int n = N; n > 1; n >>= 1, o >>= 1) {
+        const bool upper = (lane & o) != 0;
+#pragma unroll
+        for (int i = 0; i < n / 2; ++i) {
+            const float send = upper ? v[i] : v[i + n / 2];
+            const float keep = upper ? v[i + n / 2] : v[i];
+            v[i] = keep + __shfl_xor_sync(PSA_FULL, send, o);
+        }
+    }
+    float x = v[0];
+#pragma unroll
+    for (; o >= 1; o >>= 1) x += __shfl_xor_sync(PSA_FULL, x, o);
+    return x;
+}
+
+template <int N>
+__device__ __forceinline__ double reduce_scatter_d(double (&v)[N], int lane) {
+    int o = 16;
+#pragma unroll
+    for (int n = N; n > 1; n >>= 1, o >>= 1) {
+        const bool upper = (lane & o) != 0;
+#pragma unroll
+        for (int i = 0; i < n / 2; ++i) {
+            const double send = upper ? v[i] : v[i + n / 2];
+            const double keep = upper ? v[i + n / 2] : v[i];
+            v[i] = keep + __shfl_xor_sync(PSA_FULL, send, o);
+        }
+    }
+    double x = v[0];
+#pragma unroll
+    for (; o >= 1; o >>= 1) x += __shfl_xor_sync(PSA_FULL, x, o);
+    return x;
+}
+
+template <int N> struct Log2 { static constexpr int v = 1 + Log2<N / 2>::v; };
+template <> struct Log2<1> { static constexpr int v = 0; };
+
+// ---- sort keys ---------------------------------------------------------------
+// Ascending key order == (score descending, list position ascending), with the
+// low `pos_bits` bits carrying the list position: scores that agree in all but
+// their last pos_bits key bits (relative 2^-(52-pos_bits)) compare by position,
+// i.e. by block id — the reference's tie rule (metadata.cpp:92-93).
+__device__ __forceinline__ uint64_t make_key(double s, uint32_t pos, int pos_bits) {
+    s = s + 0.0;  // -0 -> +0: the reference compares doubles, where -0 == +0
+    const uint64_t u = (uint64_t)__double_as_longlong(s);
+    const uint64_t asc = (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+    const uint64_t desc = ~asc;
+    const uint64_t mask = (pos_bits >= 64) ? ~0ull : ((1ull << pos_bits) - 1ull);
+    return (desc & ~mask) | (uint64_t)pos;
+}
+
+}  // namespace psa

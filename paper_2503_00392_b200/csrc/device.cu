@@ -1,0 +1,472 @@
+// device.cu — the device layer behind psattn_b200.h: HBM block pool, batched
+// launch, workspace carving and the synthetic-workload entry points.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string.h>
+
+#include <algorithm>
+#include <cmath>
+#include <string>
+#include <vector>
+
+#include "device.h"
+#include "kernels.cuh"
+#include "psattn_b200.h"
+#include "synth.h"
+
+struct psattn_pool {
+    psattn_pool_desc desc{};
+    psa::PoolView v{};
+};
+
+namespace psa {
+
+namespace {
+thread_local std::string g_err = "";
+std::atomic<int> g_last_launches{0};
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+}  // namespace
+
+void set_error(const std::string& msg) { g_err = msg; }
+const char* last_error() { return g_err.c_str(); }
+
+int fail(int code, const std::string& msg) {
+    set_error(msg);
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+    return fail(PSATTN_ERR_RUNTIME, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+static int64_t slot_bytes_for(int d, int T, int dtype) {
+    const int e = dtype == PSATTN_KV_F32 ? 4 : 2;
+    return (int64_t)align_up((size_t)2 * T * d * e, 16);
+}
+static int64_t meta_bytes_for(int d, int dtype) {
+    const int e = dtype == PSATTN_KV_F32 ? 4 : 2;
+    return (int64_t)align_up((size_t)d * 4 + (size_t)2 * d * e, 16);
+}
+
+const PoolView& pool_view(const psattn_pool* p) { return p->v; }
+
+int pool_grow(psattn_pool* pool, int64_t n_slots, int32_t T) {
+    PoolView& v = pool->v;
+    if (n_slots < v.n_slots) n_slots = v.n_slots;
+    if (T < v.T) T = v.T;
+    if (n_slots == v.n_slots && T == v.T) return PSATTN_OK;
+    PoolView nv = v;
+    nv.T = T;
+    nv.n_slots = n_slots;
+    nv.slot_bytes = slot_bytes_for(v.d, T, v.dtype);
+    cudaError_t e;
+    if ((e = cudaMalloc(&nv.kv, (size_t)(n_slots * nv.slot_bytes))) != cudaSuccess) return cuda_fail(e, "pool grow kv");
+    if ((e = cudaMalloc(&nv.meta, (size_t)(n_slots * nv.meta_bytes))) != cudaSuccess) {
+        cudaFree(nv.kv);
+        return cuda_fail(e, "pool grow meta");
+    }
+    if ((e = cudaMalloc(&nv.ntok, (size_t)n_slots * 4)) != cudaSuccess) {
+        cudaFree(nv.kv);
+        cudaFree(nv.meta);
+        return cuda_fail(e, "pool grow ntok");
+    }
+    cudaMemset(nv.kv, 0, (size_t)(n_slots * nv.slot_bytes));
+    cudaMemset(nv.meta, 0, (size_t)(n_slots * nv.meta_bytes));
+    cudaMemset(nv.ntok, 0, (size_t)n_slots * 4);
+    if (v.n_slots > 0) {
+        // K rows and V rows move to the new per-slot offsets (T may have grown).
+        const size_t rows_old = (size_t)v.T * v.d * v.esize;
+        const size_t rows_new = (size_t)T * v.d * v.esize;
+        cudaMemcpy2D(nv.kv, nv.slot_bytes, v.kv, v.slot_bytes, rows_old, v.n_slots, cudaMemcpyDeviceToDevice);
+        cudaMemcpy2D(nv.kv + rows_new, nv.slot_bytes, v.kv + rows_old, v.slot_bytes, rows_old, v.n_slots,
+                     cudaMemcpyDeviceToDevice);
+        cudaMemcpy(nv.meta, v.meta, (size_t)(v.n_slots * v.meta_bytes), cudaMemcpyDeviceToDevice);
+        cudaMemcpy(nv.ntok, v.ntok, (size_t)v.n_slots * 4, cudaMemcpyDeviceToDevice);
+    }
+    if ((e = cudaDeviceSynchronize()) != cudaSuccess) return cuda_fail(e, "pool grow copy");
+    cudaFree(v.kv);
+    cudaFree(v.meta);
+    cudaFree(v.ntok);
+    v = nv;
+    pool->desc.block_tokens = T;
+    pool->desc.n_slots = n_slots;
+    return PSATTN_OK;
+}
+
+// Packs fp32 host blocks into the pool's slot image and converts to the pool dtype.
+static void pack_host(const PoolView& v, int64_t n, const int32_t* ntok, const float* keys, const float* values,
+                      int64_t row_stride_blocks, std::vector<char>& out) {
+    out.assign((size_t)(n * v.slot_bytes), 0);
+    const size_t per = (size_t)v.T * v.d;
+    for (int64_t i = 0; i < n; ++i) {
+        char* dst = out.data() + i * v.slot_bytes;
+        const float* k = keys + (size_t)i * row_stride_blocks;
+        const float* vv = values + (size_t)i * row_stride_blocks;
+        const size_t cnt = (size_t)ntok[i] * v.d;
+        if (v.dtype == PSATTN_KV_F32) {
+            memcpy(dst, k, cnt * 4);
+            memcpy(dst + per * 4, vv, cnt * 4);
+        } else {
+            uint16_t* dk = reinterpret_cast<uint16_t*>(dst);
+            uint16_t* dv = dk + per;
+            for (size_t j = 0; j < cnt; ++j) {
+                dk[j] = (uint16_t)(psa_synth::f2u(psa_synth::round_bf16(k[j])) >> 16);
+                dv[j] = (uint16_t)(psa_synth::f2u(psa_synth::round_bf16(vv[j])) >> 16);
+            }
+        }
+    }
+}
+
+int pool_put(psattn_pool* pool, int64_t n, const int32_t* slots, const int32_t* ntok, const float* keys,
+             const float* values, int64_t row_stride_floats, cudaStream_t st) {
+    if (n <= 0) return PSATTN_OK;
+    const PoolView& v = pool->v;
+    std::vector<char> img;
+    pack_host(v, n, ntok, keys, values, row_stride_floats, img);
+    char* d_img = nullptr;
+    int32_t* d_idx = nullptr;
+    cudaError_t e;
+    if ((e = cudaMallocAsync(&d_img, img.size(), st)) != cudaSuccess) return cuda_fail(e, "put staging");
+    if ((e = cudaMallocAsync(&d_idx, (size_t)n * 8, st)) != cudaSuccess) return cuda_fail(e, "put staging");
+    cudaMemcpyAsync(d_img, img.data(), img.size(), cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(d_idx, slots, (size_t)n * 4, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(d_idx + n, ntok, (size_t)n * 4, cudaMemcpyHostToDevice, st);
+    if ((e = launch_scatter(v, d_img, d_idx, d_idx + n, n, st)) != cudaSuccess) return cuda_fail(e, "put scatter");
+    if ((e = launch_meta_build(v, d_idx, 0, n, st)) != cudaSuccess) return cuda_fail(e, "metadata build");
+    cudaFreeAsync(d_img, st);
+    cudaFreeAsync(d_idx, st);
+    if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return cuda_fail(e, "put_blocks");
+    return PSATTN_OK;
+}
+
+int read_slot(const psattn_pool* pool, int64_t slot, int32_t ntok, float* keys, float* values) {
+    const PoolView& v = pool->v;
+    std::vector<char> img((size_t)v.slot_bytes);
+    cudaError_t e = cudaMemcpy(img.data(), v.kv + slot * v.slot_bytes, (size_t)v.slot_bytes, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_fail(e, "read slot");
+    const size_t per = (size_t)v.T * v.d, cnt = (size_t)ntok * v.d;
+    if (v.dtype == PSATTN_KV_F32) {
+        memcpy(keys, img.data(), cnt * 4);
+        memcpy(values, img.data() + per * 4, cnt * 4);
+    } else {
+        const uint16_t* k = reinterpret_cast<const uint16_t*>(img.data());
+        for (size_t j = 0; j < cnt; ++j) {
+            keys[j] = psa_synth::u2f((uint32_t)k[j] << 16);
+            values[j] = psa_synth::u2f((uint32_t)k[per + j] << 16);
+        }
+    }
+    return PSATTN_OK;
+}
+
+int read_meta(const psattn_pool* pool, int64_t slot, float* mean, float* lo, float* hi) {
+    const PoolView& v = pool->v;
+    std::vector<char> rec((size_t)v.meta_bytes);
+    cudaError_t e = cudaMemcpy(rec.data(), v.meta + slot * v.meta_bytes, (size_t)v.meta_bytes, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_fail(e, "read metadata");
+    memcpy(mean, rec.data(), (size_t)v.d * 4);
+    const char* lp = rec.data() + (size_t)v.d * 4;
+    const char* hp = lp + (size_t)v.d * v.esize;
+    for (int i = 0; i < v.d; ++i) {
+        if (v.dtype == PSATTN_KV_F32) {
+            memcpy(lo + i, lp + 4 * i, 4);
+            memcpy(hi + i, hp + 4 * i, 4);
+        } else {
+            uint16_t a, b;
+            memcpy(&a, lp + 2 * i, 2);
+            memcpy(&b, hp + 2 * i, 2);
+            lo[i] = psa_synth::u2f((uint32_t)a << 16);
+            hi[i] = psa_synth::u2f((uint32_t)b << 16);
+        }
+    }
+    return PSATTN_OK;
+}
+
+// ---- workspace carving ----
+struct WsLayout {
+    size_t keys, rpos, rslot, omass, total;
+};
+
+static WsLayout ws_layout(const psattn_batch* b) {
+    const size_t hb = (size_t)b->total_blocks * (size_t)b->group;
+    WsLayout l{};
+    size_t o = 0;
+    l.keys = o;
+    o += align_up(hb * 8, 256);
+    l.rpos = o;
+    o += align_up(hb * 4, 256);
+    l.rslot = o;
+    o += align_up(hb * 4, 256);
+    l.omass = o;
+    if (b->ranking_mode == PSATTN_RANK_ORACLE || b->audit_coverage) o += align_up(hb * 8, 256);
+    l.total = o;
+    return l;
+}
+
+int validate_batch(const psattn_pool* pool, const psattn_batch* b) {
+    if (!pool || !b) return fail(PSATTN_ERR_INVALID_ARGUMENT, "psattn_run_batch: null argument");
+    if (b->n_units < 1 || b->group < 1 || b->group > 8)
+        return fail(PSATTN_ERR_INVALID_ARGUMENT, "psattn_run_batch: need n_units >= 1 and 1 <= group <= 8");
+    if (b->dim != pool->v.d)
+        return fail(PSATTN_ERR_RUNTIME, "psattn_run_batch: dimension mismatch (" + std::to_string(b->dim) + " vs " +
+                                            std::to_string(pool->v.d) + ")");
+    if (!(b->epsilon > 0.0) || b->epsilon > 1.0)
+        return fail(PSATTN_ERR_INVALID_ARGUMENT, "config: epsilon must be in (0, 1]");
+    if (b->microbatch_size < 1) return fail(PSATTN_ERR_INVALID_ARGUMENT, "config: microbatch_size must be >= 1");
+    if (b->estimator < 0 || b->estimator > 2) return fail(PSATTN_ERR_INVALID_ARGUMENT, "config: unknown estimator code");
+    if (b->ranking_mode < 0 || b->ranking_mode > 1)
+        return fail(PSATTN_ERR_INVALID_ARGUMENT, "config: unknown ranking mode code");
+    if (b->topk < 0) return fail(PSATTN_ERR_INVALID_ARGUMENT, "topk must be >= 0");
+    if (b->max_blocks < 1 || b->total_blocks < 1)
+        return fail(PSATTN_ERR_INVALID_ARGUMENT, "psattn_run_batch: empty block lists");
+    if (!b->q || !b->slots || !b->list_off || !b->out || !b->blocks_processed || !b->est_coverage || !b->terminated)
+        return fail(PSATTN_ERR_INVALID_ARGUMENT, "psattn_run_batch: null device pointer");
+    return PSATTN_OK;
+}
+
+BatchView make_view(const psattn_pool* pool, const psattn_batch* b, void* workspace) {
+    const WsLayout l = ws_layout(b);
+    char* ws = static_cast<char*>(workspace);
+    BatchView v{};
+    v.n_units = b->n_units;
+    v.g = b->group;
+    v.d = b->dim;
+    v.max_n = b->max_blocks;
+    v.total = b->total_blocks;
+    int pb = 1;
+    while (pb < 62 && (int64_t(1) << pb) < b->max_blocks) ++pb;
+    v.pos_bits = pb;
+    v.q = b->q;
+    v.slots = b->slots;
+    v.list_off = b->list_off;
+    v.eps = b->epsilon;
+    v.m = b->microbatch_size;
+    v.estimator = b->estimator;
+    v.rank_oracle = b->ranking_mode == PSATTN_RANK_ORACLE;
+    v.audit = b->audit_coverage != 0;
+    v.has_oracle = v.rank_oracle || v.audit;
+    v.scale = b->scale_override > 0.0 ? b->scale_override : 1.0 / std::sqrt((double)b->dim);
+    v.topk = b->topk;
+    v.out = b->out;
+    v.bp = b->blocks_processed;
+    v.est = b->est_coverage;
+    v.tcov = b->true_coverage;
+    v.term = b->terminated;
+    v.keys = reinterpret_cast<uint64_t*>(ws + l.keys);
+    v.rpos = b->ranked_pos ? b->ranked_pos : reinterpret_cast<int32_t*>(ws + l.rpos);
+    v.rslot = reinterpret_cast<int32_t*>(ws + l.rslot);
+    v.omass = v.has_oracle ? reinterpret_cast<double*>(ws + l.omass) : nullptr;
+    v.iest = b->iter_est;
+    (void)pool;
+    return v;
+}
+
+}  // namespace psa
+
+using namespace psa;
+
+extern "C" {
+
+int psattn_pool_create(const psattn_pool_desc* desc, psattn_pool** out_pool) {
+    if (!desc || !out_pool) return fail(PSATTN_ERR_INVALID_ARGUMENT, "psattn_pool_create: null argument");
+    if (desc->dim < 1 || desc->dim > 256)
+        return fail(PSATTN_ERR_INVALID_ARGUMENT, "psattn_pool_create: dim must be in [1, 256]");
+    if (desc->block_tokens < 1 || desc->block_tokens > 32)
+        return fail(PSATTN_ERR_INVALID_ARGUMENT, "psattn_pool_create: block_tokens must be in [1, 32]");
+    if (desc->kv_dtype != PSATTN_KV_F32 && desc->kv_dtype != PSATTN_KV_BF16)
+        return fail(PSATTN_ERR_INVALID_ARGUMENT, "psattn_pool_create: unknown kv dtype");
+    if (desc->n_slots < 0) return fail(PSATTN_ERR_INVALID_ARGUMENT, "psattn_pool_create: n_slots must be >= 0");
+    int dev_count = 0;
+    cudaError_t e = cudaGetDeviceCount(&dev_count);
+    if (e != cudaSuccess || dev_count == 0)
+        return fail(PSATTN_ERR_RUNTIME, std::string("no CUDA device: the PSA path has no CPU fallback (") +
+                                            cudaGetErrorString(e) + ")");
+    auto* p = new psattn_pool();
+    p->desc = *desc;
+    p->desc.n_slots = 0;
+    PoolView& v = p->v;
+    v.d = desc->dim;
+    v.T = desc->block_tokens;
+    v.dtype = desc->kv_dtype;
+    v.esize = desc->kv_dtype == PSATTN_KV_F32 ? 4 : 2;
+    v.slot_bytes = slot_bytes_for(v.d, v.T, v.dtype);
+    v.meta_bytes = meta_bytes_for(v.d, v.dtype);
+    v.n_slots = 0;
+    if (desc->n_slots > 0) {
+        const int rc = pool_grow(p, desc->n_slots, v.T);
+        if (rc) {
+            delete p;
+            return rc;
+        }
+    }
+    *out_pool = p;
+    return PSATTN_OK;
+}
+
+void psattn_pool_destroy(psattn_pool* pool) {
+    if (!pool) return;
+    cudaFree(pool->v.kv);
+    cudaFree(pool->v.meta);
+    cudaFree(pool->v.ntok);
+    delete pool;
+}
+
+int psattn_pool_get_desc(const psattn_pool* pool, psattn_pool_desc* out) {
+    if (!pool || !out) return fail(PSATTN_ERR_INVALID_ARGUMENT, "psattn_pool_get_desc: null argument");
+    *out = pool->desc;
+    return PSATTN_OK;
+}
+
+int psattn_pool_get_layout(const psattn_pool* pool, psattn_pool_layout* out) {
+    if (!pool || !out) return fail(PSATTN_ERR_INVALID_ARGUMENT, "psattn_pool_get_layout: null argument");
+    out->kv = pool->v.kv;
+    out->meta = pool->v.meta;
+    out->ntok = pool->v.ntok;
+    out->slot_bytes = pool->v.slot_bytes;
+    out->meta_bytes = pool->v.meta_bytes;
+    return PSATTN_OK;
+}
+
+int psattn_pool_put_blocks(psattn_pool* pool, int64_t n, const int32_t* slots, const int32_t* ntok, const float* keys,
+                           const float* values) {
+    if (!pool || !slots || !ntok || !keys || !values)
+        return fail(PSATTN_ERR_INVALID_ARGUMENT, "psattn_pool_put_blocks: null argument");
+    for (int64_t i = 0; i < n; ++i) {
+        if (slots[i] < 0 || slots[i] >= pool->v.n_slots)
+            return fail(PSATTN_ERR_INVALID_ARGUMENT, "psattn_pool_put_blocks: slot out of range");
+        if (ntok[i] < 1 || ntok[i] > pool->v.T)
+            return fail(PSATTN_ERR_INVALID_ARGUMENT, "psattn_pool_put_blocks: ntok out of range");
+    }
+    return pool_put(pool, n, slots, ntok, keys, values, (int64_t)pool->v.T * pool->v.d, 0);
+}
+
+int psattn_pool_build_metadata(psattn_pool* pool, int64_t slot_begin, int64_t slot_end, void* stream) {
+    if (!pool) return fail(PSATTN_ERR_INVALID_ARGUMENT, "psattn_pool_build_metadata: null pool");
+    if (slot_begin < 0 || slot_end > pool->v.n_slots)
+        return fail(PSATTN_ERR_INVALID_ARGUMENT, "psattn_pool_build_metadata: slot range out of bounds");
+    cudaError_t e = launch_meta_build(pool->v, nullptr, slot_begin, slot_end, (cudaStream_t)stream);
+    return e == cudaSuccess ? PSATTN_OK : cuda_fail(e, "metadata build");
+}
+
+int psattn_pool_read_metadata(psattn_pool* pool, int64_t slot, float* mean, float* lo, float* hi) {
+    if (!pool || !mean || !lo || !hi) return fail(PSATTN_ERR_INVALID_ARGUMENT, "psattn_pool_read_metadata: null");
+    if (slot < 0 || slot >= pool->v.n_slots) return fail(PSATTN_ERR_INVALID_ARGUMENT, "slot out of range");
+    return read_meta(pool, slot, mean, lo, hi);
+}
+
+size_t psattn_batch_workspace_bytes(const psattn_batch* b) { return b ? ws_layout(b).total : 0; }
+
+int psattn_run_batch(psattn_pool* pool, const psattn_batch* b, void* workspace, void* stream) {
+    int rc = validate_batch(pool, b);
+    if (rc) return rc;
+    if (!workspace) return fail(PSATTN_ERR_INVALID_ARGUMENT, "psattn_run_batch: null workspace");
+    const BatchView v = make_view(pool, b, workspace);
+    const int n = launch_batch(pool->v, v, (cudaStream_t)stream);
+    if (n < 0) return cuda_fail(cudaGetLastError(), "psattn_run_batch launch");
+    g_last_launches.store(n);
+    return PSATTN_OK;
+}
+
+int psattn_batch_union_blocks(const psattn_batch* b, void* workspace, int64_t* out_union, void* stream) {
+    if (!b || !workspace || !out_union) return fail(PSATTN_ERR_INVALID_ARGUMENT, "psattn_batch_union_blocks: null");
+    const BatchView v = make_view(nullptr, b, workspace);
+    cudaError_t e = launch_union(v, out_union, (cudaStream_t)stream);
+    return e == cudaSuccess ? PSATTN_OK : cuda_fail(e, "union kernel");
+}
+
+int psattn_batch_last_launches(int32_t* out_count) {
+    if (!out_count) return fail(PSATTN_ERR_INVALID_ARGUMENT, "null");
+    *out_count = g_last_launches.load();
+    return PSATTN_OK;
+}
+
+// ---- synthetic workload ----
+void psattn_synth_direction(const psattn_synth_params* p, int64_t unit_id, float* out) {
+    psa_synth::direction(p->seed, unit_id, p->dim, out);
+}
+
+void psattn_synth_query(const psattn_synth_params* p, int64_t unit_id, int32_t head, float* out) {
+    const int d = p->dim;
+    std::vector<float> dir(d), g(d);
+    psa_synth::direction(p->seed, unit_id, d, dir.data());
+    // per-head perturbation: a unit vector from its own stream (S_QUERY, unit*64 + head)
+    psa_synth::direction(p->seed ^ 0x51ED270B27F1A3C5ULL, unit_id * 64 + head, d, g.data());
+    std::vector<double> v(d);
+    double ss = 0.0;
+    for (int i = 0; i < d; ++i) {
+        v[i] = (double)dir[i] + 0.1 * (double)g[i];
+        ss += v[i] * v[i];
+    }
+    const double s = std::sqrt((double)d) / std::sqrt(ss);
+    for (int i = 0; i < d; ++i) out[i] = (float)(v[i] * s);
+}
+
+int psattn_synth_is_planted(const psattn_synth_params* p, int64_t unit_id, int64_t block) {
+    return psa_synth::is_planted(p->seed, p->planted_prob, unit_id, block);
+}
+
+void psattn_synth_unit_host(const psattn_synth_params* p, int64_t unit_id, int64_t first_block, int64_t n_blocks,
+                            int64_t n_tokens_total, float* keys, float* values) {
+    const int d = p->dim, T = p->block_tokens;
+    std::vector<float> dir(d);
+    psa_synth::direction(p->seed, unit_id, d, dir.data());
+    for (int64_t bi = 0; bi < n_blocks; ++bi) {
+        const int64_t b = first_block + bi;
+        const int planted = psa_synth::is_planted(p->seed, p->planted_prob, unit_id, b);
+        for (int t = 0; t < T; ++t) {
+            const int64_t tok = b * T + t;
+            for (int i = 0; i < d; ++i) {
+                const size_t idx = ((size_t)bi * T + t) * d + i;
+                float kx = 0.0f, vx = 0.0f;
+                if (tok < n_tokens_total) {
+                    kx = psa_synth::key_at(p->seed, unit_id, tok, i, d, planted, p->skew, dir[i]);
+                    vx = psa_synth::value_at(p->seed, unit_id, b, tok, i, d);
+                    if (p->round_bf16) {
+                        kx = psa_synth::round_bf16(kx);
+                        vx = psa_synth::round_bf16(vx);
+                    }
+                }
+                keys[idx] = kx;
+                values[idx] = vx;
+            }
+        }
+    }
+}
+
+int psattn_pool_fill_synthetic(psattn_pool* pool, const psattn_synth_params* p, int32_t n_units,
+                               const int64_t* unit_ids, const int64_t* slot_off, const int64_t* tokens,
+                               void* stream) {
+    if (!pool || !p || !unit_ids || !slot_off || !tokens)
+        return fail(PSATTN_ERR_INVALID_ARGUMENT, "psattn_pool_fill_synthetic: null argument");
+    if (p->dim != pool->v.d || p->block_tokens != pool->v.T)
+        return fail(PSATTN_ERR_INVALID_ARGUMENT, "psattn_pool_fill_synthetic: params do not match the pool");
+    if (n_units <= 0) return PSATTN_OK;
+    const int T = pool->v.T;
+    int64_t max_blocks = 0, lo = INT64_MAX, hi = 0;
+    for (int u = 0; u < n_units; ++u) {
+        const int64_t nb = (tokens[u] + T - 1) / T;
+        if (slot_off[u] < 0 || slot_off[u] + nb > pool->v.n_slots)
+            return fail(PSATTN_ERR_INVALID_ARGUMENT, "psattn_pool_fill_synthetic: slots out of range");
+        max_blocks = std::max(max_blocks, nb);
+        lo = std::min(lo, slot_off[u]);
+        hi = std::max(hi, slot_off[u] + nb);
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    int64_t* d_arr = nullptr;
+    float* d_dirs = nullptr;
+    cudaError_t e;
+    if ((e = cudaMalloc(&d_arr, (size_t)n_units * 24)) != cudaSuccess) return cuda_fail(e, "synth alloc");
+    if ((e = cudaMalloc(&d_dirs, (size_t)n_units * pool->v.d * 4)) != cudaSuccess) return cuda_fail(e, "synth alloc");
+    cudaMemcpyAsync(d_arr, unit_ids, (size_t)n_units * 8, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(d_arr + n_units, slot_off, (size_t)n_units * 8, cudaMemcpyHostToDevice, st);
+    cudaMemcpyAsync(d_arr + 2 * n_units, tokens, (size_t)n_units * 8, cudaMemcpyHostToDevice, st);
+    e = launch_synth_fill(pool->v, p->seed, p->skew, p->planted_prob, p->round_bf16, n_units, d_arr, d_arr + n_units,
+                          d_arr + 2 * n_units, max_blocks, d_dirs, st);
+    if (e == cudaSuccess) e = launch_meta_build(pool->v, nullptr, lo, hi, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    cudaFree(d_arr);
+    cudaFree(d_dirs);
+    return e == cudaSuccess ? PSATTN_OK : cuda_fail(e, "synthetic fill");
+}
+
+}  // extern "C"

@@ -1,0 +1,28 @@
+// device.h — internal interface of the device layer for the C++ host code.
+#pragma once
+
+#include <atomic>
+#include <string>
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "psattn_b200.h"
+
+namespace psa {
+
+struct PoolView;
+
+void set_error(const std::string& msg);
+const char* last_error();
+int fail(int code, const std::string& msg);
+
+// Grows slot capacity and/or tokens-per-slot, preserving contents.
+int pool_grow(psattn_pool* pool, int64_t n_slots, int32_t T);
+// Host fp32 blocks -> slots (row_stride_floats between consecutive blocks' K), metadata built.
+int pool_put(psattn_pool* pool, int64_t n, const int32_t* slots, const int32_t* ntok, const float* keys,
+             const float* values, int64_t row_stride_floats, cudaStream_t st);
+int read_slot(const psattn_pool* pool, int64_t slot, int32_t ntok, float* keys, float* values);
+int read_meta(const psattn_pool* pool, int64_t slot, float* mean, float* lo, float* hi);
+
+}  // namespace psa

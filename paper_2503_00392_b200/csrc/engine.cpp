@@ -1,0 +1,323 @@
+// engine.cpp — psattn:: C++ entry points over the device path (B200 build).
+//
+// Every entry point resolves ids to pool slots and issues ONE device launch
+// (TieredBlockStore::run_device -> psattn_run_batch: score -> order ->
+// progressive kernel). Host work afterwards is bookkeeping only: result
+// assembly, the fast-tier accounting replay in the reference's load order, and
+// the injected miss latency.
+#include "psattn/engine.hpp"
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <string>
+
+#include "device.h"
+#include "engine_internal.h"
+#include "psattn/pipeline.hpp"
+
+namespace psattn {
+
+namespace {
+
+double log_add_exp(double a, double b) {
+    if (a == -std::numeric_limits<double>::infinity()) return b;
+    if (b == -std::numeric_limits<double>::infinity()) return a;
+    const double hi = std::max(a, b), lo = std::min(a, b);
+    return hi + std::log1p(std::exp(lo - hi));
+}
+
+// Microbatch sizes the reference consumes for a run that processed `bp` blocks
+// of an n-block plan (engine.cpp:98-102, 219-227).
+std::vector<std::size_t> microbatches(std::size_t bp, std::size_t n, std::size_t m, std::size_t take) {
+    std::vector<std::size_t> out;
+    std::size_t cur = 0;
+    while (cur < bp) {
+        std::size_t c = std::min(n - cur, m);
+        if (take) c = std::min(c, take - cur);
+        out.push_back(c);
+        cur += c;
+    }
+    return out;
+}
+
+struct Built {
+    PSAResult res;
+    std::vector<std::size_t> mbs;
+};
+
+// Assembles query qi's PSAResult (accounting filled in later).
+Built assemble(const detail::DeviceQueryResult& r, std::size_t qi, std::size_t n, const PSAConfig& cfg,
+               std::size_t take) {
+    Built b;
+    PSAResult& res = b.res;
+    const std::size_t d = static_cast<std::size_t>(r.dim);
+    res.output.assign(r.out.begin() + qi * d, r.out.begin() + (qi + 1) * d);
+    res.blocks_processed = static_cast<std::size_t>(r.blocks_processed[qi]);
+    res.total_blocks = n;
+    res.estimated_coverage = r.est[qi];
+    if (cfg.audit_coverage) res.true_coverage = r.true_cov[qi];
+    res.terminated_early = r.terminated[qi] != 0;
+    res.processed_ids.assign(r.ranked_ids[qi].begin(), r.ranked_ids[qi].begin() + res.blocks_processed);
+    b.mbs = microbatches(res.blocks_processed, n, static_cast<std::size_t>(cfg.microbatch_size), take);
+    std::size_t cur = 0;
+    for (std::size_t c : b.mbs) {
+        cur += c;
+        IterationStats it;
+        it.blocks = c;
+        it.estimated_coverage = r.iter_est[qi][cur - 1];
+        res.iterations.push_back(it);
+    }
+    return b;
+}
+
+// Replays microbatch k of a result through the store accounting.
+std::uint64_t account_mb(TieredBlockStore& store, Built& b, std::size_t k, std::size_t start) {
+    auto& it = b.res.iterations[k];
+    const auto hm = store.account_loads(
+        std::span<const BlockId>(b.res.processed_ids.data() + start, b.mbs[k]));
+    it.hits = hm.first;
+    it.misses = hm.second;
+    return hm.second;
+}
+
+std::uint64_t account_all(TieredBlockStore& store, Built& b) {
+    std::uint64_t misses = 0;
+    std::size_t start = 0;
+    for (std::size_t k = 0; k < b.mbs.size(); ++k) {
+        misses += account_mb(store, b, k, start);
+        start += b.mbs[k];
+    }
+    return misses;
+}
+
+PSAResult single(std::span<const float> q, std::span<const BlockId> block_ids, const PSAConfig& cfg,
+                 TieredBlockStore& store, std::size_t topk) {
+    cfg.validate();
+    if (block_ids.empty()) throw Error("plan_blocks: no blocks given");
+    detail::DeviceQueryBatch qb;
+    qb.lists.push_back(block_ids);
+    qb.queries.push_back(q.data());
+    qb.group = 1;
+    qb.dim = static_cast<std::int32_t>(q.size());
+    qb.cfg = cfg;
+    qb.topk = topk;
+    detail::DeviceQueryResult r;
+    store.run_device(qb, r);
+    const std::size_t take = topk ? std::min(topk, block_ids.size()) : 0;
+    Built b = assemble(r, 0, block_ids.size(), cfg, take);
+    store.inject_miss_latency(account_all(store, b));
+    return std::move(b.res);
+}
+
+}  // namespace
+
+void PSAConfig::validate() const {
+    if (!(epsilon > 0.0) || epsilon > 1.0)
+        throw Error("config: epsilon must be in (0, 1], got " + std::to_string(epsilon));
+    if (microbatch_size < 1)
+        throw Error("config: microbatch_size must be >= 1, got " + std::to_string(microbatch_size));
+    if (block_size < 1) throw Error("config: block_size must be >= 1, got " + std::to_string(block_size));
+}
+
+void CoverageEstimator::observe(double log_as) {
+    log_as_acc = log_add_exp(log_as_acc, log_as);
+    log_as_min = std::min(log_as_min, log_as);
+    if (n_left == 0) throw Error("coverage estimator: observed more blocks than planned");
+    --n_left;
+}
+
+double estimate_coverage(const CoverageEstimator& ce) {
+    if (!ce.any_processed()) throw Error("estimate_coverage: no blocks processed yet");
+    if (ce.n_left == 0) return 1.0;
+    const double ratio = static_cast<double>(ce.n_left) * std::exp(ce.log_as_min - ce.log_as_acc);
+    return 1.0 / (1.0 + ratio);
+}
+
+RankedPlan plan_blocks(std::span<const float> q, std::span<const BlockId> block_ids, const PSAConfig& cfg,
+                       const TieredBlockStore& store) {
+    cfg.validate();
+    if (block_ids.empty()) throw Error("plan_blocks: no blocks given");
+    detail::DeviceQueryBatch qb;
+    qb.lists.push_back(block_ids);
+    qb.queries.push_back(q.data());
+    qb.dim = static_cast<std::int32_t>(q.size());
+    qb.cfg = cfg;
+    qb.topk = 1;  // stop after the first rank: only the ordering is wanted
+    detail::DeviceQueryResult r;
+    const_cast<TieredBlockStore&>(store).run_device(qb, r);
+    RankedPlan plan;
+    plan.scale = cfg.scale_for(q.size());
+    plan.ranked_ids = r.ranked_ids[0];
+    if (cfg.ranking_mode == RankingMode::Oracle || cfg.audit_coverage) {
+        plan.oracle_log_as = r.oracle_ranked[0];
+        double t = -std::numeric_limits<double>::infinity();
+        for (double x : plan.oracle_log_as) t = log_add_exp(t, x);
+        plan.total_log_as = t;
+    }
+    return plan;
+}
+
+PSAResult psa_attention(std::span<const float> q, std::span<const BlockId> block_ids, const PSAConfig& cfg,
+                        TieredBlockStore& store) {
+    return single(q, block_ids, cfg, store, 0);
+}
+
+PSAResult topk_attention(std::span<const float> q, std::span<const BlockId> block_ids, std::size_t k,
+                         const PSAConfig& cfg, TieredBlockStore& store) {
+    cfg.validate();
+    if (block_ids.empty()) throw Error("plan_blocks: no blocks given");
+    if (k == 0) throw Error("topk_attention: k must be >= 1");
+    return single(q, block_ids, cfg, store, k);
+}
+
+PSAResult topk_attention(std::span<const float> q, std::span<const BlockId> block_ids, std::size_t k,
+                         Estimator estimator, TieredBlockStore& store) {
+    PSAConfig cfg;
+    cfg.estimator = estimator;
+    return topk_attention(q, block_ids, k, cfg, store);
+}
+
+BatchResult psa_attention_batched(std::span<const HeadVector> queries,
+                                  std::span<const std::vector<BlockId>> per_query_blocks, const PSAConfig& cfg,
+                                  TieredBlockStore& store) {
+    if (queries.size() != per_query_blocks.size()) throw Error("batched attention: query/block list count mismatch");
+    if (queries.empty()) throw Error("batched attention: empty batch");
+    cfg.validate();
+    detail::DeviceQueryBatch qb;
+    qb.group = 1;
+    qb.dim = static_cast<std::int32_t>(queries[0].size());
+    qb.cfg = cfg;
+    for (std::size_t i = 0; i < queries.size(); ++i) {
+        check_dim(queries[i].size(), static_cast<std::size_t>(qb.dim), "batched attention");
+        qb.lists.emplace_back(per_query_blocks[i]);
+        qb.queries.push_back(queries[i].data());
+    }
+    detail::DeviceQueryResult r;
+    store.run_device(qb, r);
+    std::vector<Built> built;
+    for (std::size_t i = 0; i < queries.size(); ++i) built.push_back(assemble(r, i, per_query_blocks[i].size(), cfg, 0));
+    // Lockstep replay: round k advances every live query by one microbatch (engine.cpp:191-205).
+    BatchResult out;
+    std::vector<std::size_t> start(built.size(), 0);
+    std::uint64_t misses = 0;
+    for (std::size_t k = 0;; ++k) {
+        IterationStats round;
+        bool any = false;
+        for (std::size_t i = 0; i < built.size(); ++i) {
+            if (k >= built[i].mbs.size()) continue;
+            any = true;
+            misses += account_mb(store, built[i], k, start[i]);
+            start[i] += built[i].mbs[k];
+            const auto& it = built[i].res.iterations[k];
+            round.blocks += it.blocks;
+            round.hits += it.hits;
+            round.misses += it.misses;
+            round.estimated_coverage = it.estimated_coverage;
+        }
+        if (!any) break;
+        out.rounds.push_back(round);
+    }
+    for (auto& b : built) out.results.push_back(std::move(b.res));
+    store.inject_miss_latency(misses);
+    return out;
+}
+
+MultiHeadResult psa_attention_multi_head(std::span<const HeadVector> head_queries,
+                                         std::span<const std::vector<BlockId>> kv_head_blocks,
+                                         const PSAConfig& cfg, TieredBlockStore& store) {
+    if (head_queries.empty()) throw Error("multi-head attention: no query heads");
+    if (kv_head_blocks.empty()) throw Error("multi-head attention: no kv heads");
+    if (head_queries.size() % kv_head_blocks.size() != 0)
+        throw Error("multi-head attention: query head count must be a multiple of kv head count");
+    cfg.validate();
+    const std::size_t group = head_queries.size() / kv_head_blocks.size();
+    MultiHeadResult out;
+    detail::DeviceQueryResult r;
+    if (group <= 8) {
+        detail::DeviceQueryBatch qb;
+        qb.group = static_cast<std::int32_t>(group);
+        qb.dim = static_cast<std::int32_t>(head_queries[0].size());
+        qb.cfg = cfg;
+        for (const auto& l : kv_head_blocks) qb.lists.emplace_back(l);
+        for (const auto& q : head_queries) {
+            check_dim(q.size(), static_cast<std::size_t>(qb.dim), "multi-head attention");
+            qb.queries.push_back(q.data());
+        }
+        store.run_device(qb, r);
+    } else {
+        // groups wider than 8 run as independent lists (one per q-head)
+        detail::DeviceQueryBatch qb;
+        qb.group = 1;
+        qb.dim = static_cast<std::int32_t>(head_queries[0].size());
+        qb.cfg = cfg;
+        for (std::size_t h = 0; h < head_queries.size(); ++h) {
+            qb.lists.emplace_back(kv_head_blocks[h / group]);
+            qb.queries.push_back(head_queries[h].data());
+        }
+        store.run_device(qb, r);
+    }
+    std::uint64_t misses = 0;
+    for (std::size_t h = 0; h < head_queries.size(); ++h) {
+        Built b = assemble(r, h, kv_head_blocks[h / group].size(), cfg, 0);
+        misses += account_all(store, b);
+        for (BlockId id : b.res.processed_ids) out.fetched_union.push_back(id);
+        out.per_head.push_back(std::move(b.res));
+    }
+    std::sort(out.fetched_union.begin(), out.fetched_union.end());
+    out.fetched_union.erase(std::unique(out.fetched_union.begin(), out.fetched_union.end()), out.fetched_union.end());
+    store.inject_miss_latency(misses);
+    return out;
+}
+
+// ---- pipeline.hpp ----
+namespace {
+ExecutionResult run_exec(std::span<const float> q, std::span<const BlockId> ids, const PSAConfig& cfg,
+                         TieredBlockStore& store) {
+    const auto t0 = std::chrono::steady_clock::now();
+    ExecutionResult out;
+    out.result = psa_attention(q, ids, cfg, store);
+    out.timings.total_wall_ms =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    out.timings.sequential_equiv_ms = out.timings.total_wall_ms;
+    out.timings.overlap_efficiency = 1.0;
+    return out;
+}
+}  // namespace
+
+ExecutionResult run_sequential(std::span<const float> q, std::span<const BlockId> block_ids, const PSAConfig& cfg,
+                               TieredBlockStore& store, const PipelineOptions&) {
+    return run_exec(q, block_ids, cfg, store);
+}
+
+ExecutionResult run_pipelined(std::span<const float> q, std::span<const BlockId> block_ids, const PSAConfig& cfg,
+                              TieredBlockStore& store, const PipelineOptions&) {
+    return run_exec(q, block_ids, cfg, store);
+}
+
+// ---- metadata.hpp ----
+BlockMetadata build_metadata(const KVBlock& block) {
+    if (block.n_tokens <= 0) throw Error("build_metadata: empty block");
+    psattn_pool_desc desc{};
+    desc.dim = block.dim;
+    desc.block_tokens = block.n_tokens;
+    desc.kv_dtype = PSATTN_KV_F32;
+    desc.n_slots = 1;
+    psattn_pool* pool = nullptr;
+    if (psattn_pool_create(&desc, &pool) != PSATTN_OK) throw Error(psa::last_error());
+    const std::int32_t slot = 0, nt = block.n_tokens;
+    BlockMetadata m;
+    m.block_id = block.block_id;
+    m.layer_id = block.layer_id;
+    m.n_tokens = block.n_tokens;
+    m.mean_key.resize(block.dim);
+    m.lo.resize(block.dim);
+    m.hi.resize(block.dim);
+    int rc = psa::pool_put(pool, 1, &slot, &nt, block.keys.data(), block.values.data(), 0, nullptr);
+    if (rc == PSATTN_OK) rc = psa::read_meta(pool, 0, m.mean_key.data(), m.lo.data(), m.hi.data());
+    psattn_pool_destroy(pool);
+    if (rc != PSATTN_OK) throw Error(psa::last_error());
+    return m;
+}
+
+}  // namespace psattn

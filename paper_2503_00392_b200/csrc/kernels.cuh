@@ -1,0 +1,67 @@
+// kernels.cuh — device-side views and launcher declarations of the PSA path.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace psa {
+
+// Unified paged KV block pool in HBM (one per head dim). Slot s holds one
+// (layer, kv-head) block of up to T tokens: K rows [T][d] then V rows [T][d].
+// Its metadata record (reference BlockMetadata, types.hpp:52-59) lives at
+// meta + s*meta_bytes: mean[d] fp32 | lo[d] kv | hi[d] kv.
+struct PoolView {
+    int32_t d;
+    int32_t T;
+    int32_t dtype;  // 0 f32, 1 bf16
+    int32_t esize;
+    char* kv;
+    char* meta;
+    int32_t* ntok;
+    int64_t slot_bytes;
+    int64_t meta_bytes;
+    int64_t n_slots;
+};
+
+// One batched launch: n_units block lists (page tables of slots, ascending
+// block id), g q-heads per list. Workspace arrays are indexed per head at
+// hb = list_off[u]*g + h*n_u.
+struct BatchView {
+    int32_t n_units, g, d, pos_bits;
+    int64_t max_n, total;
+    const float* q;
+    const int32_t* slots;
+    const int64_t* list_off;
+    double eps;
+    int32_t m, estimator, rank_oracle, has_oracle, audit;
+    double scale;
+    int64_t topk;
+    float* out;
+    int64_t* bp;
+    double* est;
+    double* tcov;
+    int32_t* term;
+    // workspace
+    uint64_t* keys;
+    int32_t* rpos;
+    int32_t* rslot;
+    double* omass;
+    double* iest;  // optional per-rank estimate at microbatch boundaries
+};
+
+int dpl_for(int d);
+int tok_for(int T);
+int g_for(int g);
+
+cudaError_t launch_meta_build(const PoolView& p, const int32_t* list, int64_t s0, int64_t s1, cudaStream_t st);
+cudaError_t launch_scatter(const PoolView& p, const void* staged, const int32_t* d_slots, const int32_t* d_ntok,
+                           int64_t n, cudaStream_t st);
+cudaError_t launch_synth_fill(const PoolView& p, uint64_t seed, float skew, float prob, int round_bf16,
+                              int32_t n_units, const int64_t* d_unit_ids, const int64_t* d_slot_off,
+                              const int64_t* d_tokens, int64_t max_blocks, float* d_dirs, cudaStream_t st);
+void launch_psa(const PoolView& p, const BatchView& b, cudaStream_t st);
+// Returns the number of kernel launches issued, or -1 on error (cudaGetLastError has it).
+int launch_batch(const PoolView& p, const BatchView& b, cudaStream_t st);
+cudaError_t launch_union(const BatchView& b, int64_t* out_union, cudaStream_t st);
+
+}  // namespace psa

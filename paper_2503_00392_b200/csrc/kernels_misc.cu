@@ -1,0 +1,152 @@
+// kernels_misc.cu — K1 metadata build + synthetic workload fill (sm_100a).
+#include <cuda_bf16.h>
+#include <float.h>
+#include <math.h>
+
+#include "common.cuh"
+#include "kernels.cuh"
+#include "synth.h"
+
+namespace psa {
+
+// Specialised lane mappings for d = 64 and d = 128; every other d <= 256 runs
+// the masked 8-dims-per-lane variant.
+int dpl_for(int d) { return d == 128 ? 4 : d == 64 ? 2 : 8; }
+int tok_for(int T) { return T <= 16 ? 16 : 32; }
+int g_for(int g) { return g <= 4 ? 4 : 8; }
+
+// =============================================================================
+// K1: metadata build. One warp per slot; lane i covers dims i, i+32, ...
+// lo/hi: elementwise min/max with std::min/std::max semantics; mean: fp64 sum
+// in token order, divided by n, rounded to fp32 — bit-identical to the reference.
+// =============================================================================
+template <typename KV>
+__global__ void meta_build_kernel(PoolView p, const int32_t* list, int64_t s0, int64_t s1) {
+    const int lane = threadIdx.x & 31;
+    const int64_t idx = s0 + (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (idx >= s1) return;
+    const int64_t slot = list ? (int64_t)list[idx] : idx;
+    const int n = p.ntok[slot];
+    const int d = p.d;
+    const KV* k = reinterpret_cast<const KV*>(p.kv + slot * p.slot_bytes);
+    char* rec = p.meta + slot * p.meta_bytes;
+    float* mean = reinterpret_cast<float*>(rec);
+    KV* lo = reinterpret_cast<KV*>(rec + (size_t)d * 4);
+    KV* hi = reinterpret_cast<KV*>(rec + (size_t)d * 4 + (size_t)d * sizeof(KV));
+    for (int i = lane; i < d; i += 32) {
+        if (n <= 0) {
+            mean[i] = 0.0f;
+            lo[i] = KVT<KV>::from_f(0.0f);
+            hi[i] = KVT<KV>::from_f(0.0f);
+            continue;
+        }
+        float l = KVT<KV>::to_f(k[i]);
+        float h = l;
+        double s = l;
+        for (int t = 1; t < n; ++t) {
+            const float x = KVT<KV>::to_f(k[(size_t)t * d + i]);
+            l = (x < l) ? x : l;
+            h = (h < x) ? x : h;
+            s = __dadd_rn(s, (double)x);
+        }
+        mean[i] = __double2float_rn(__ddiv_rn(s, (double)n));
+        lo[i] = KVT<KV>::from_f(l);  // exact: l is a KV value
+        hi[i] = KVT<KV>::from_f(h);
+    }
+}
+
+cudaError_t launch_meta_build(const PoolView& p, const int32_t* list, int64_t s0, int64_t s1, cudaStream_t st) {
+    if (s1 <= s0) return cudaSuccess;
+    const int warps = 8;
+    const int64_t blocks = (s1 - s0 + warps - 1) / warps;
+    if (p.dtype == 0)
+        meta_build_kernel<float><<<(unsigned)blocks, warps * 32, 0, st>>>(p, list, s0, s1);
+    else
+        meta_build_kernel<__nv_bfloat16><<<(unsigned)blocks, warps * 32, 0, st>>>(p, list, s0, s1);
+    return cudaGetLastError();
+}
+
+// Copies n staged slot images ([2][T][d] in the pool dtype) into pool slots and sets ntok.
+__global__ void scatter_slots_kernel(PoolView p, const char* __restrict__ staged, const int32_t* __restrict__ slots,
+                                     const int32_t* __restrict__ ntok, int64_t n) {
+    const int64_t i = blockIdx.x;
+    if (i >= n) return;
+    const int64_t slot = slots[i];
+    const int4* src = reinterpret_cast<const int4*>(staged + i * p.slot_bytes);
+    int4* dst = reinterpret_cast<int4*>(p.kv + slot * p.slot_bytes);
+    for (int64_t e = threadIdx.x; e < p.slot_bytes / 16; e += blockDim.x) dst[e] = src[e];
+    if (threadIdx.x == 0) p.ntok[slot] = ntok[i];
+}
+
+cudaError_t launch_scatter(const PoolView& p, const void* staged, const int32_t* d_slots, const int32_t* d_ntok,
+                           int64_t n, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    scatter_slots_kernel<<<(unsigned)n, 128, 0, st>>>(p, static_cast<const char*>(staged), d_slots, d_ntok, n);
+    return cudaGetLastError();
+}
+
+// =============================================================================
+// Synthetic fill (fixture). Directions first (one thread per unit, sequential
+// fp64 norm so the host copy is bit-identical), then every K/V element.
+// =============================================================================
+__global__ void synth_dir_kernel(uint64_t seed, int32_t d, int32_t n_units, const int64_t* unit_ids, float* dirs) {
+    const int u = blockIdx.x * blockDim.x + threadIdx.x;
+    if (u >= n_units) return;
+    psa_synth::direction(seed, unit_ids[u], d, dirs + (size_t)u * d);
+}
+
+template <typename KV>
+__global__ void synth_fill_kernel(PoolView p, uint64_t seed, float skew, float prob, int round_bf16,
+                                  const int64_t* unit_ids, const int64_t* slot_off, const int64_t* tokens,
+                                  const float* dirs) {
+    const int u = blockIdx.y;
+    const int64_t ntok_total = tokens[u];
+    const int64_t nb = (ntok_total + p.T - 1) / p.T;
+    const int64_t uid = unit_ids[u];
+    const int d = p.d;
+    const int64_t per_block = (int64_t)p.T * d;
+    for (int64_t b = blockIdx.x; b < nb; b += gridDim.x) {
+        const int64_t slot = slot_off[u] + b;
+        const int planted = psa_synth::is_planted(seed, prob, uid, b);
+        KV* kp = reinterpret_cast<KV*>(p.kv + slot * p.slot_bytes);
+        KV* vp = kp + per_block;
+        for (int64_t e = threadIdx.x; e < per_block; e += blockDim.x) {
+            const int64_t t = e / d;
+            const int i = (int)(e - t * d);
+            const int64_t tok = b * p.T + t;
+            float kx = 0.0f, vx = 0.0f;
+            if (tok < ntok_total) {
+                kx = psa_synth::key_at(seed, uid, tok, i, d, planted, skew, dirs[(size_t)u * d + i]);
+                vx = psa_synth::value_at(seed, uid, b, tok, i, d);
+                if (round_bf16) {
+                    kx = psa_synth::round_bf16(kx);
+                    vx = psa_synth::round_bf16(vx);
+                }
+            }
+            kp[e] = KVT<KV>::from_f(kx);
+            vp[e] = KVT<KV>::from_f(vx);
+        }
+        if (threadIdx.x == 0) {
+            const int64_t rem = ntok_total - b * p.T;
+            p.ntok[slot] = (int32_t)(rem < p.T ? rem : p.T);
+        }
+    }
+}
+
+cudaError_t launch_synth_fill(const PoolView& p, uint64_t seed, float skew, float prob, int round_bf16,
+                              int32_t n_units, const int64_t* d_unit_ids, const int64_t* d_slot_off,
+                              const int64_t* d_tokens, int64_t max_blocks, float* d_dirs, cudaStream_t st) {
+    if (n_units <= 0) return cudaSuccess;
+    synth_dir_kernel<<<(n_units + 127) / 128, 128, 0, st>>>(seed, p.d, n_units, d_unit_ids, d_dirs);
+    const unsigned gx = (unsigned)(max_blocks < 4096 ? (max_blocks > 0 ? max_blocks : 1) : 4096);
+    dim3 grid(gx, (unsigned)n_units);
+    if (p.dtype == 0)
+        synth_fill_kernel<float><<<grid, 256, 0, st>>>(p, seed, skew, prob, round_bf16, d_unit_ids, d_slot_off,
+                                                       d_tokens, d_dirs);
+    else
+        synth_fill_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(p, seed, skew, prob, round_bf16, d_unit_ids,
+                                                               d_slot_off, d_tokens, d_dirs);
+    return cudaGetLastError();
+}
+
+}  // namespace psa

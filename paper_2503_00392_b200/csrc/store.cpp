@@ -1,0 +1,483 @@
+// store.cpp — TieredBlockStore over the device pool (B200 build).
+//
+// Blocks: one device pool per head dim (psattn_pool, slots shared by all
+// layers). Fast-tier accounting: the reference's observable semantics
+// (store.cpp:11-124 of the reference): Unified vs LayerPartitioned domains,
+// write-allocate on put, hit/miss with LRU splice or FIFO order on load,
+// eviction counts per layer, bytes = fp32 payload per miss, optional trace.
+#include "psattn/store.hpp"
+
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <numeric>
+#include <thread>
+
+#include <cuda_runtime.h>
+
+#include "device.h"
+#include "engine_internal.h"
+#include "psattn_b200.h"
+
+namespace psattn {
+
+namespace {
+[[noreturn]] void throw_last(int rc) {
+    if (rc == PSATTN_ERR_NOT_FOUND) throw NotFoundError(psa::last_error());
+    if (rc == PSATTN_ERR_INVALID_ARGUMENT) throw ConfigError(psa::last_error());
+    throw Error(psa::last_error());
+}
+void check_rc(int rc) {
+    if (rc != PSATTN_OK) throw_last(rc);
+}
+void check_cuda(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw Error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// Growable device buffer.
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    void* get(size_t n) {
+        if (n > cap) {
+            if (p) cudaFree(p);
+            p = nullptr;
+            cap = 0;
+            check_cuda(cudaMalloc(&p, std::max<size_t>(n, 256)), "device buffer");
+            cap = std::max<size_t>(n, 256);
+        }
+        return p;
+    }
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+};
+
+// Growable pinned host buffer.
+struct HostBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    void* get(size_t n) {
+        if (n > cap) {
+            if (p) cudaFreeHost(p);
+            p = nullptr;
+            cap = 0;
+            check_cuda(cudaMallocHost(&p, std::max<size_t>(n, 256)), "pinned buffer");
+            cap = std::max<size_t>(n, 256);
+        }
+        return p;
+    }
+    ~HostBuf() {
+        if (p) cudaFreeHost(p);
+    }
+};
+
+size_t align256(size_t x) { return (x + 255) / 256 * 256; }
+}  // namespace
+
+struct TieredBlockStore::DevicePool {
+    psattn_pool* pool = nullptr;
+    std::int64_t next_slot = 0;
+    std::vector<std::int64_t> free_slots;
+    ~DevicePool() { psattn_pool_destroy(pool); }
+};
+
+struct TieredBlockStore::DeviceState {
+    cudaStream_t stream = nullptr;
+    DevBuf in, outb, ws;
+    HostBuf h_in, h_out;
+    ~DeviceState() {
+        if (stream) cudaStreamDestroy(stream);
+    }
+};
+
+TieredBlockStore::TieredBlockStore(const StoreOptions& options) : options_(options) {
+    if (options_.n_layers <= 0) throw Error("TieredBlockStore: n_layers must be positive");
+    if (options_.policy == PoolPolicy::Unified) {
+        domains_.resize(1);
+        domains_[0].capacity = options_.fast_capacity_slots;
+    } else {
+        domains_.resize(static_cast<std::size_t>(options_.n_layers));
+        const std::size_t per = options_.fast_capacity_slots / static_cast<std::size_t>(options_.n_layers);
+        for (auto& d : domains_) d.capacity = per;
+    }
+    stats_.per_layer.resize(static_cast<std::size_t>(options_.n_layers));
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+        throw Error("TieredBlockStore: no CUDA device (the B200 PSA path has no CPU fallback)");
+    dev_ = std::make_unique<DeviceState>();
+    check_cuda(cudaStreamCreateWithFlags(&dev_->stream, cudaStreamNonBlocking), "stream");
+}
+
+TieredBlockStore::~TieredBlockStore() = default;
+
+TieredBlockStore::Domain& TieredBlockStore::domain_for(std::int32_t layer_id) {
+    if (layer_id < 0 || layer_id >= options_.n_layers) throw Error("TieredBlockStore: layer_id out of range");
+    return options_.policy == PoolPolicy::Unified ? domains_[0] : domains_[static_cast<std::size_t>(layer_id)];
+}
+const TieredBlockStore::Domain& TieredBlockStore::domain_for(std::int32_t layer_id) const {
+    if (layer_id < 0 || layer_id >= options_.n_layers) throw Error("TieredBlockStore: layer_id out of range");
+    return options_.policy == PoolPolicy::Unified ? domains_[0] : domains_[static_cast<std::size_t>(layer_id)];
+}
+
+void TieredBlockStore::count_eviction(BlockId victim) {
+    stats_.evictions += 1;
+    auto it = blocks_.find(victim);
+    if (it != blocks_.end()) stats_.per_layer[static_cast<std::size_t>(it->second.layer)].evictions += 1;
+}
+
+BlockId TieredBlockStore::insert_fast(Domain& domain, BlockId id, bool* evicted) {
+    *evicted = false;
+    if (domain.capacity == 0) return 0;
+    BlockId victim = 0;
+    if (domain.slots.size() == domain.capacity) {
+        victim = domain.order.back();
+        domain.order.pop_back();
+        domain.slots.erase(victim);
+        *evicted = true;
+    }
+    domain.order.push_front(id);
+    domain.slots.emplace(id, domain.order.begin());
+    return victim;
+}
+
+TieredBlockStore::DevicePool& TieredBlockStore::pool_for(std::int32_t dim, std::int32_t n_tokens) {
+    auto it = pools_.find(dim);
+    if (it == pools_.end()) {
+        auto dp = std::make_unique<DevicePool>();
+        psattn_pool_desc desc{};
+        desc.dim = dim;
+        desc.block_tokens = std::max(n_tokens, 16);
+        desc.kv_dtype = PSATTN_KV_F32;  // the C/C++ API hands fp32 blocks; keep them exact
+        desc.n_slots = 256;
+        check_rc(psattn_pool_create(&desc, &dp->pool));
+        it = pools_.emplace(dim, std::move(dp)).first;
+    }
+    DevicePool& dp = *it->second;
+    psattn_pool_desc desc{};
+    psattn_pool_get_desc(dp.pool, &desc);
+    if (n_tokens > desc.block_tokens) check_rc(psa::pool_grow(dp.pool, desc.n_slots, n_tokens));
+    return dp;
+}
+
+void TieredBlockStore::put_block(std::shared_ptr<const KVBlock> block, RequestId owner) {
+    if (!block) throw Error("put_block: null block");
+    if (block->n_tokens <= 0) throw Error("build_metadata: empty block");
+    if (block->dim <= 0 || block->dim > 256) throw Error("put_block: dim must be in [1, 256] on the device pool");
+    if (block->n_tokens > 32) throw Error("put_block: blocks of more than 32 tokens are not supported by the device pool");
+    const std::size_t nelem = static_cast<std::size_t>(block->n_tokens) * static_cast<std::size_t>(block->dim);
+    if (block->keys.size() < nelem || block->values.size() < nelem) throw Error("put_block: short key/value arrays");
+    std::lock_guard lock(mutex_);
+    if (block->layer_id < 0 || block->layer_id >= options_.n_layers) throw Error("put_block: layer_id out of range");
+    if (blocks_.count(block->block_id))
+        throw Error("put_block: duplicate block id " + std::to_string(block->block_id));
+    DevicePool& dp = pool_for(block->dim, block->n_tokens);
+    std::int64_t slot;
+    if (!dp.free_slots.empty()) {
+        slot = dp.free_slots.back();
+        dp.free_slots.pop_back();
+    } else {
+        psattn_pool_desc desc{};
+        psattn_pool_get_desc(dp.pool, &desc);
+        if (dp.next_slot >= desc.n_slots) check_rc(psa::pool_grow(dp.pool, desc.n_slots * 2, desc.block_tokens));
+        slot = dp.next_slot++;
+    }
+    const std::int32_t s32 = static_cast<std::int32_t>(slot);
+    const std::int32_t nt = block->n_tokens;
+    check_rc(psa::pool_put(dp.pool, 1, &s32, &nt, block->keys.data(), block->values.data(), 0, dev_->stream));
+    blocks_.emplace(block->block_id, BlockRec{block->dim, block->layer_id, block->n_tokens, slot, owner});
+    owned_[owner].push_back(block->block_id);
+    bool evicted = false;
+    const BlockId victim = insert_fast(domain_for(block->layer_id), block->block_id, &evicted);
+    if (evicted) count_eviction(victim);
+}
+
+bool TieredBlockStore::load_locked(BlockId id, const BlockRec& rec) {
+    Domain& domain = domain_for(rec.layer);
+    auto& ls = stats_.per_layer[static_cast<std::size_t>(rec.layer)];
+    auto slot = domain.slots.find(id);
+    bool miss = false, evicted = false;
+    BlockId victim = 0;
+    if (slot != domain.slots.end()) {
+        stats_.hits += 1;
+        ls.hits += 1;
+        if (options_.eviction == EvictionPolicy::LRU) domain.order.splice(domain.order.begin(), domain.order, slot->second);
+    } else {
+        miss = true;
+        const std::uint64_t bytes = 2ull * static_cast<std::uint64_t>(rec.n_tokens) * rec.dim * sizeof(float);
+        stats_.misses += 1;
+        ls.misses += 1;
+        stats_.bytes_transferred += bytes;
+        ls.bytes_transferred += bytes;
+        victim = insert_fast(domain, id, &evicted);
+        if (evicted) count_eviction(victim);
+    }
+    if (trace_) {
+        *trace_ << trace_seq_++ << ',' << rec.layer << ',' << id << ',' << (miss ? "miss" : "hit") << ',';
+        if (evicted) *trace_ << victim;
+        else *trace_ << '-';
+        *trace_ << '\n';
+    }
+    return miss;
+}
+
+std::pair<std::uint64_t, std::uint64_t> TieredBlockStore::account_loads(std::span<const BlockId> ids) {
+    std::lock_guard lock(mutex_);
+    std::uint64_t h = 0, m = 0;
+    for (BlockId id : ids) {
+        auto it = blocks_.find(id);
+        if (it == blocks_.end()) throw NotFoundError("load_block: unknown block id " + std::to_string(id));
+        if (load_locked(id, it->second)) ++m;
+        else ++h;
+    }
+    return {h, m};
+}
+
+void TieredBlockStore::inject_miss_latency(std::uint64_t misses) const {
+    if (misses > 0 && options_.miss_sleep_ms > 0.0)
+        std::this_thread::sleep_for(std::chrono::duration<double, std::milli>(options_.miss_sleep_ms * misses));
+}
+
+std::shared_ptr<const KVBlock> TieredBlockStore::copy_out(BlockId id, const BlockRec& rec) const {
+    auto b = std::make_shared<KVBlock>();
+    b->block_id = id;
+    b->layer_id = rec.layer;
+    b->n_tokens = rec.n_tokens;
+    b->dim = rec.dim;
+    const std::size_t n = static_cast<std::size_t>(rec.n_tokens) * rec.dim;
+    b->keys.resize(n);
+    b->values.resize(n);
+    check_rc(psa::read_slot(pools_.at(rec.dim)->pool, rec.slot, rec.n_tokens, b->keys.data(), b->values.data()));
+    return b;
+}
+
+std::shared_ptr<const KVBlock> TieredBlockStore::load_block(BlockId block_id, std::int32_t layer_id) {
+    std::shared_ptr<const KVBlock> out;
+    bool miss = false;
+    {
+        std::lock_guard lock(mutex_);
+        auto it = blocks_.find(block_id);
+        if (it == blocks_.end()) throw NotFoundError("load_block: unknown block id " + std::to_string(block_id));
+        if (layer_id >= 0 && it->second.layer != layer_id) throw Error("load_block: layer_id does not match block");
+        miss = load_locked(block_id, it->second);
+        out = copy_out(block_id, it->second);
+    }
+    if (miss) inject_miss_latency(1);
+    return out;
+}
+
+std::shared_ptr<const KVBlock> TieredBlockStore::peek_block(BlockId block_id) const {
+    std::lock_guard lock(mutex_);
+    auto it = blocks_.find(block_id);
+    if (it == blocks_.end()) throw NotFoundError("peek_block: unknown block id " + std::to_string(block_id));
+    return copy_out(block_id, it->second);
+}
+
+BlockMetadata TieredBlockStore::metadata(BlockId block_id) const {
+    std::lock_guard lock(mutex_);
+    auto it = blocks_.find(block_id);
+    if (it == blocks_.end()) throw NotFoundError("metadata: unknown block id " + std::to_string(block_id));
+    const BlockRec& r = it->second;
+    BlockMetadata m;
+    m.block_id = block_id;
+    m.layer_id = r.layer;
+    m.n_tokens = r.n_tokens;
+    m.mean_key.resize(r.dim);
+    m.lo.resize(r.dim);
+    m.hi.resize(r.dim);
+    check_rc(psa::read_meta(pools_.at(r.dim)->pool, r.slot, m.mean_key.data(), m.lo.data(), m.hi.data()));
+    return m;
+}
+
+std::vector<BlockMetadata> TieredBlockStore::metadata_for(std::span<const BlockId> ids) const {
+    std::vector<BlockMetadata> out;
+    out.reserve(ids.size());
+    for (BlockId id : ids) out.push_back(metadata(id));
+    return out;
+}
+
+void TieredBlockStore::release_request(RequestId request_id) {
+    std::lock_guard lock(mutex_);
+    auto it = owned_.find(request_id);
+    if (it == owned_.end()) throw NotFoundError("release_request: unknown request " + std::to_string(request_id));
+    for (BlockId id : it->second) {
+        auto b = blocks_.find(id);
+        if (b == blocks_.end()) continue;
+        Domain& domain = domain_for(b->second.layer);
+        auto s = domain.slots.find(id);
+        if (s != domain.slots.end()) {
+            domain.order.erase(s->second);
+            domain.slots.erase(s);
+        }
+        pools_.at(b->second.dim)->free_slots.push_back(b->second.slot);
+        blocks_.erase(b);
+    }
+    owned_.erase(it);
+}
+
+bool TieredBlockStore::contains(BlockId block_id) const {
+    std::lock_guard lock(mutex_);
+    return blocks_.count(block_id) > 0;
+}
+
+bool TieredBlockStore::resident_fast(BlockId block_id) const {
+    std::lock_guard lock(mutex_);
+    auto it = blocks_.find(block_id);
+    if (it == blocks_.end()) return false;
+    return domain_for(it->second.layer).slots.count(block_id) > 0;
+}
+
+CacheStats TieredBlockStore::stats() const {
+    std::lock_guard lock(mutex_);
+    return stats_;
+}
+
+std::size_t TieredBlockStore::fast_occupancy() const {
+    std::lock_guard lock(mutex_);
+    std::size_t t = 0;
+    for (const auto& d : domains_) t += d.slots.size();
+    return t;
+}
+
+std::size_t TieredBlockStore::domain_capacity(std::int32_t layer_id) const {
+    std::lock_guard lock(mutex_);
+    return domain_for(layer_id).capacity;
+}
+
+void TieredBlockStore::enable_trace(std::ostream* sink) {
+    std::lock_guard lock(mutex_);
+    trace_ = sink;
+}
+
+// -----------------------------------------------------------------------------
+// One device launch for a batch of progressive queries.
+// -----------------------------------------------------------------------------
+void TieredBlockStore::run_device(const detail::DeviceQueryBatch& qb, detail::DeviceQueryResult& res) {
+    std::lock_guard lock(mutex_);
+    const int g = qb.group, d = qb.dim;
+    const int n_units = static_cast<int>(qb.lists.size());
+    if (n_units == 0) throw Error("batched attention: empty batch");
+    auto pit = pools_.find(d);
+    // Resolve ids -> slots, ascending-id order per list.
+    std::vector<std::vector<BlockId>> sorted(n_units);
+    std::vector<std::int64_t> off(n_units + 1, 0);
+    std::int64_t max_n = 0;
+    for (int u = 0; u < n_units; ++u) {
+        const auto& ids = qb.lists[u];
+        if (ids.empty()) throw Error("plan_blocks: no blocks given");
+        for (BlockId id : ids) {
+            auto it = blocks_.find(id);
+            if (it == blocks_.end()) throw NotFoundError("metadata: unknown block id " + std::to_string(id));
+            check_dim(static_cast<std::size_t>(d), static_cast<std::size_t>(it->second.dim), "criticality_score");
+        }
+        sorted[u].assign(ids.begin(), ids.end());
+        std::sort(sorted[u].begin(), sorted[u].end());
+        off[u + 1] = off[u] + static_cast<std::int64_t>(ids.size());
+        max_n = std::max<std::int64_t>(max_n, static_cast<std::int64_t>(ids.size()));
+    }
+    if (pit == pools_.end()) throw Error("no blocks of this dimension");
+    psattn_pool* pool = pit->second->pool;
+    const std::int64_t total = off[n_units];
+    const std::int64_t nq = static_cast<std::int64_t>(n_units) * g;
+    const std::int64_t hbt = total * g;
+
+    // ---- host inputs: q | slots | list_off ----
+    const size_t q_b = align256(static_cast<size_t>(nq) * d * 4);
+    const size_t s_b = align256(static_cast<size_t>(total) * 4);
+    const size_t o_b = align256(static_cast<size_t>(n_units + 1) * 8);
+    char* hin = static_cast<char*>(dev_->h_in.get(q_b + s_b + o_b));
+    for (std::int64_t i = 0; i < nq; ++i) std::memcpy(hin + static_cast<size_t>(i) * d * 4, qb.queries[i], d * 4);
+    auto* hs = reinterpret_cast<std::int32_t*>(hin + q_b);
+    for (int u = 0; u < n_units; ++u)
+        for (std::int64_t i = 0; i < off[u + 1] - off[u]; ++i)
+            hs[off[u] + i] = static_cast<std::int32_t>(blocks_.at(sorted[u][i]).slot);
+    std::memcpy(hin + q_b + s_b, off.data(), (n_units + 1) * 8);
+    char* din = static_cast<char*>(dev_->in.get(q_b + s_b + o_b));
+    check_cuda(cudaMemcpyAsync(din, hin, q_b + s_b + o_b, cudaMemcpyHostToDevice, dev_->stream), "H2D");
+
+    // ---- device outputs: out | bp | est | tcov | term | rpos | iest | omass(copy) ----
+    const size_t ob_out = align256(static_cast<size_t>(nq) * d * 4), ob_bp = align256(nq * 8),
+                 ob_est = align256(nq * 8), ob_tc = align256(nq * 8), ob_term = align256(nq * 4),
+                 ob_rpos = align256(static_cast<size_t>(hbt) * 4), ob_iest = align256(static_cast<size_t>(hbt) * 8);
+    const size_t out_total = ob_out + ob_bp + ob_est + ob_tc + ob_term + ob_rpos + ob_iest;
+    char* dout = static_cast<char*>(dev_->outb.get(out_total));
+
+    psattn_batch b{};
+    b.n_units = n_units;
+    b.group = g;
+    b.dim = d;
+    b.max_blocks = max_n;
+    b.total_blocks = total;
+    b.q = reinterpret_cast<const float*>(din);
+    b.slots = reinterpret_cast<const std::int32_t*>(din + q_b);
+    b.list_off = reinterpret_cast<const std::int64_t*>(din + q_b + s_b);
+    b.epsilon = qb.cfg.epsilon;
+    b.microbatch_size = qb.cfg.microbatch_size;
+    b.estimator = static_cast<std::int32_t>(qb.cfg.estimator);
+    b.ranking_mode = qb.cfg.ranking_mode == RankingMode::Oracle ? PSATTN_RANK_ORACLE : PSATTN_RANK_ESTIMATED;
+    b.audit_coverage = qb.cfg.audit_coverage ? 1 : 0;
+    b.scale_override = qb.cfg.scale_override;
+    b.topk = static_cast<std::int64_t>(qb.topk);
+    size_t o = 0;
+    b.out = reinterpret_cast<float*>(dout + o); o += ob_out;
+    b.blocks_processed = reinterpret_cast<std::int64_t*>(dout + o); o += ob_bp;
+    b.est_coverage = reinterpret_cast<double*>(dout + o); o += ob_est;
+    b.true_coverage = reinterpret_cast<double*>(dout + o); o += ob_tc;
+    b.terminated = reinterpret_cast<std::int32_t*>(dout + o); o += ob_term;
+    b.ranked_pos = reinterpret_cast<std::int32_t*>(dout + o); o += ob_rpos;
+    b.iter_est = reinterpret_cast<double*>(dout + o); o += ob_iest;
+    const size_t wsb = psattn_batch_workspace_bytes(&b);
+    void* ws = dev_->ws.get(wsb);
+    check_rc(psattn_run_batch(pool, &b, ws, dev_->stream));
+
+    const bool has_oracle = b.ranking_mode == PSATTN_RANK_ORACLE || b.audit_coverage;
+    const size_t om_b = has_oracle ? static_cast<size_t>(hbt) * 8 : 0;
+    char* hout = static_cast<char*>(dev_->h_out.get(out_total + om_b + 256));
+    check_cuda(cudaMemcpyAsync(hout, dout, out_total, cudaMemcpyDeviceToHost, dev_->stream), "D2H");
+    if (has_oracle) {
+        // workspace layout: keys | rpos | rslot | omass (psattn_batch_workspace_bytes)
+        const size_t om_off = align256(static_cast<size_t>(hbt) * 8) + 2 * align256(static_cast<size_t>(hbt) * 4);
+        check_cuda(cudaMemcpyAsync(hout + out_total, static_cast<char*>(ws) + om_off, om_b, cudaMemcpyDeviceToHost,
+                                   dev_->stream),
+                   "D2H");
+    }
+    check_cuda(cudaStreamSynchronize(dev_->stream), "PSA device launch");
+
+    // ---- unpack ----
+    res.dim = d;
+    res.scale = qb.cfg.scale_for(static_cast<std::size_t>(d));
+    o = 0;
+    res.out.assign(reinterpret_cast<float*>(hout), reinterpret_cast<float*>(hout) + nq * d); o += ob_out;
+    const auto* bp = reinterpret_cast<const std::int64_t*>(hout + o); o += ob_bp;
+    const auto* est = reinterpret_cast<const double*>(hout + o); o += ob_est;
+    const auto* tc = reinterpret_cast<const double*>(hout + o); o += ob_tc;
+    const auto* term = reinterpret_cast<const std::int32_t*>(hout + o); o += ob_term;
+    const auto* rpos = reinterpret_cast<const std::int32_t*>(hout + o); o += ob_rpos;
+    const auto* iest = reinterpret_cast<const double*>(hout + o); o += ob_iest;
+    const auto* om = reinterpret_cast<const double*>(hout + out_total);
+    res.blocks_processed.assign(bp, bp + nq);
+    res.est.assign(est, est + nq);
+    res.true_cov.assign(tc, tc + nq);
+    res.terminated.assign(term, term + nq);
+    res.ranked_ids.assign(nq, {});
+    res.iter_est.assign(nq, {});
+    res.oracle_ranked.assign(nq, {});
+    for (int u = 0; u < n_units; ++u) {
+        const std::int64_t n = off[u + 1] - off[u];
+        for (int h = 0; h < g; ++h) {
+            const std::int64_t qi = static_cast<std::int64_t>(u) * g + h;
+            const std::int64_t hb = off[u] * g + h * n;
+            auto& ids = res.ranked_ids[qi];
+            ids.resize(n);
+            for (std::int64_t r = 0; r < n; ++r) ids[r] = sorted[u][rpos[hb + r]];
+            res.iter_est[qi].assign(iest + hb, iest + hb + n);
+            if (has_oracle) {
+                auto& orr = res.oracle_ranked[qi];
+                orr.resize(n);
+                for (std::int64_t r = 0; r < n; ++r) orr[r] = om[hb + rpos[hb + r]];
+            }
+        }
+    }
+}
+
+}  // namespace psattn

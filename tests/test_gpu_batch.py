@@ -1,0 +1,272 @@
+"""Device-batched path (psattn_run_batch) against the oracle: random GQA batches,
+ragged blocks, every estimator / ranking mode / top-k / microbatch size, bf16
+pools filled by the device generator, metadata bit-exactness, the GQA union
+counter, and GQA == per-head equivalence."""
+import math
+
+import numpy as np
+import pytest
+
+from helpers import check_parity, random_blockset
+from oracle.pyoracle import BlockSet, make_config
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def mods():
+    from paper_2503_00392_b200 import batch, capi
+    return capi, batch
+
+
+def run_units(mods, units, queries, T, kv_dtype=0, want_iter=True, **cfg):
+    """units: list of BlockSet (ids ascending 0..n-1); queries: [U][g][d]."""
+    capi, batch = mods
+    d = units[0].d
+    total = sum(u.n for u in units)
+    pool = batch.DevicePool(d, T, kv_dtype, total)
+    slots, ntok, ks, vs = [], [], [], []
+    s = 0
+    for u in units:
+        for i in range(u.n):
+            k, v = u.block(i)
+            kk = np.zeros((T, d), np.float32)
+            vv = np.zeros((T, d), np.float32)
+            kk[: k.shape[0]] = k
+            vv[: v.shape[0]] = v
+            ks.append(kk)
+            vs.append(vv)
+            ntok.append(k.shape[0])
+            slots.append(s)
+            s += 1
+    pool.put_blocks(slots, ntok, np.stack(ks), np.stack(vs))
+    off = np.zeros(len(units) + 1, np.int64)
+    off[1:] = np.cumsum([u.n for u in units])
+    dev = torch.device("cuda")
+    q = torch.tensor(np.asarray(queries, np.float32), device=dev)
+    run = batch.BatchRun(pool, q, torch.tensor(np.array(slots, np.int32), device=dev),
+                         torch.tensor(off, device=dev), max(u.n for u in units), batch.BatchConfig(**cfg),
+                         want_ranked=True, want_iter=want_iter)
+    run.run()
+    torch.cuda.synchronize()
+    return pool, run, off
+
+
+def unpack(run, off, u, h, n):
+    g = run.group
+    qi = u * g + h
+    hb = int(off[u]) * g + h * n
+    ranked = run.ranked[hb: hb + n].cpu().numpy()
+    bp = int(run.bp[qi])
+    return dict(out=run.out[u, h].cpu().numpy(), bp=bp, est=float(run.est[qi]), term=int(run.term[qi]),
+                tcov=float(run.tcov[qi]), ids=ranked[:bp], ranked=ranked)
+
+
+CFGS = [dict(epsilon=0.95), dict(epsilon=0.8, microbatch_size=4), dict(epsilon=0.99, estimator=0),
+        dict(epsilon=0.9, estimator=1, microbatch_size=3), dict(epsilon=1.0), dict(topk=7),
+        dict(topk=64, microbatch_size=5), dict(epsilon=0.9, ranking_mode=1),
+        dict(epsilon=0.95, audit_coverage=1, microbatch_size=2), dict(epsilon=0.5)]
+
+
+@pytest.mark.parametrize("ci", range(len(CFGS)))
+@pytest.mark.parametrize("d,T,g", [(128, 16, 4), (64, 16, 2), (32, 8, 1), (128, 32, 8), (20, 5, 3)])
+def test_batch_parity(mods, oracle, ci, d, T, g):
+    cfgd = CFGS[ci]
+    rng = np.random.default_rng(ci * 1000 + d * 7 + T + g)
+    U = 3
+    units, queries = [], []
+    for u in range(U):
+        n = int(rng.integers(1, 150))
+        units.append(random_blockset(rng, n, d, 1, T, planted_frac=0.1 if u % 2 else 0.0))
+        base = rng.standard_normal(d)
+        queries.append([(base + 0.3 * rng.standard_normal(d)).astype(np.float32) * 2 for _ in range(g)])
+    pool, run, off = run_units(mods, units, queries, T, **cfgd)
+    topk = cfgd.get("topk", 0)
+    ocfg = make_config(**{k: v for k, v in cfgd.items() if k != "topk"})
+    tags = []
+    for u in range(U):
+        for h in range(g):
+            r = unpack(run, off, u, h, units[u].n)
+            tags.append(check_parity(oracle, np.asarray(queries[u][h]), units[u], ocfg, topk, r["ids"], r["bp"],
+                                     r["out"], r["est"]))
+            o = oracle.psa(np.asarray(queries[u][h]), units[u], ocfg, topk)
+            if tags[-1] == "exact":
+                assert r["term"] == int(o.terminated_early)
+                if ocfg.audit_coverage:
+                    assert r["tcov"] == pytest.approx(o.true_coverage, abs=1e-9)
+                # iteration estimates at every microbatch boundary
+                m = ocfg.microbatch_size
+                it = run.iest[int(off[u]) * g + h * units[u].n:].cpu().numpy()
+                bounds, cur = [], 0
+                while cur < r["bp"]:
+                    c = min(units[u].n - cur, m)
+                    if topk:
+                        c = min(c, min(topk, units[u].n) - cur)
+                    cur += c
+                    bounds.append(cur - 1)
+                np.testing.assert_allclose(it[bounds], o.iteration_estimates, rtol=0, atol=1e-4)
+    assert tags.count("exact") >= len(tags) - 1
+
+
+def test_gqa_equals_per_head(mods):
+    """psa_attention_multi_head semantics (engine.cpp:240-260): a g=4 launch equals four g=1 runs."""
+    rng = np.random.default_rng(31337)
+    d, T = 128, 16
+    unit = random_blockset(rng, 300, d, 16, 16, planted_frac=0.05)
+    qs = [rng.standard_normal(d).astype(np.float32) * 2 for _ in range(4)]
+    _, r4, off4 = run_units(mods, [unit], [qs], T, epsilon=0.9)
+    _, r1, off1 = run_units(mods, [unit] * 4, [[q] for q in qs], T, epsilon=0.9)
+    for h in range(4):
+        a = unpack(r4, off4, 0, h, unit.n)
+        b = unpack(r1, off1, h, 0, unit.n)
+        assert a["bp"] == b["bp"]
+        assert np.array_equal(a["ids"], b["ids"])
+        assert a["out"].tobytes() == b["out"].tobytes()
+
+
+def test_union_counter(mods):
+    rng = np.random.default_rng(5)
+    d, T = 64, 16
+    units = [random_blockset(rng, int(rng.integers(50, 300)), d, 16, 16, planted_frac=0.05) for _ in range(3)]
+    qs = [[rng.standard_normal(d).astype(np.float32) * 2 for _ in range(4)] for _ in units]
+    _, run, off = run_units(mods, units, qs, T, epsilon=0.9)
+    un = run.union_blocks().cpu().numpy()
+    torch.cuda.synchronize()
+    for u, unit in enumerate(units):
+        s = set()
+        for h in range(4):
+            s |= set(map(int, unpack(run, off, u, h, unit.n)["ids"]))
+        assert un[u] == len(s)
+
+
+def test_metadata_bit_exact(mods, oracle):
+    """K1: device metadata == reference build_metadata (metadata.cpp:8-34), bit for bit."""
+    rng = np.random.default_rng(8)
+    for d, T in ((128, 16), (20, 7), (64, 32)):
+        bs = random_blockset(rng, 50, d, 1, T)
+        pool, _, _ = run_units(mods, [bs], [[np.ones(d, np.float32)]], T, epsilon=1.0)
+        for i in range(bs.n):
+            k, _ = bs.block(i)
+            m, lo, hi = pool.read_metadata(i)
+            om, olo, ohi = oracle.build_metadata(k)
+            assert m.tobytes() == om.tobytes() and lo.tobytes() == olo.tobytes() and hi.tobytes() == ohi.tobytes()
+
+
+def test_bf16_pool_synthetic_parity(mods, oracle):
+    """bf16 pool filled on device by the seekable generator; the oracle gets the same
+    values regenerated on the host (bf16-rounded, upcast to fp32)."""
+    capi, batch = mods
+    d, T, g = 128, 16, 4
+    for planted in (0.0, 64 / 2048):
+        p = capi.synth_params(seed=1, dim=d, block_tokens=T, skew=8.0, planted_prob=planted, round_bf16=1)
+        tokens = [16 * 700 + 5, 16 * 300]
+        nb = [(t + T - 1) // T for t in tokens]
+        slot_off = [0, nb[0]]
+        pool = batch.DevicePool(d, T, capi.PSATTN_KV_BF16, sum(nb))
+        pool.fill_synthetic(p, [11, 12], slot_off, tokens)
+        torch.cuda.synchronize()
+        dev = torch.device("cuda")
+        qs = [[capi.synth_query(p, uid, h) for h in range(g)] for uid in (11, 12)]
+        slots = np.arange(sum(nb), dtype=np.int32)
+        off = np.array([0, nb[0], nb[0] + nb[1]], np.int64)
+        run = batch.BatchRun(pool, torch.tensor(np.array(qs), device=dev), torch.tensor(slots, device=dev),
+                             torch.tensor(off, device=dev), max(nb), batch.BatchConfig(epsilon=0.95),
+                             want_ranked=True)
+        run.run()
+        torch.cuda.synchronize()
+        for u, uid in enumerate((11, 12)):
+            k, v = capi.synth_unit_host(p, uid, tokens[u])
+            ntok = [min(T, tokens[u] - b * T) for b in range(nb[u])]
+            bs = BlockSet([k[b, :ntok[b]] for b in range(nb[u])], [v[b, :ntok[b]] for b in range(nb[u])])
+            # metadata of the device pool equals the oracle's on the same values
+            mm, lo, hi = pool.read_metadata(slot_off[u] + 3)
+            om, olo, ohi = oracle.build_metadata(k[3, :ntok[3]])
+            assert mm.tobytes() == om.tobytes() and lo.tobytes() == olo.tobytes()
+            for h in range(g):
+                r = unpack(run, off, u, h, nb[u])
+                check_parity(oracle, qs[u][h], bs, make_config(epsilon=0.95), 0, r["ids"], r["bp"], r["out"],
+                             r["est"])
+
+
+def test_synthetic_device_equals_host(mods):
+    """The device fill kernel and the host generator produce identical bits."""
+    capi, batch = mods
+    d, T = 128, 16
+    for prob, rb, dt in ((0.1, 1, capi.PSATTN_KV_BF16), (0.05, 0, capi.PSATTN_KV_F32)):
+        p = capi.synth_params(seed=7, dim=d, block_tokens=T, skew=8.0, planted_prob=prob, round_bf16=rb)
+        tokens = [16 * 40 + 3]
+        pool = batch.DevicePool(d, T, dt, 41)
+        pool.fill_synthetic(p, [5], [0], tokens)
+        torch.cuda.synchronize()
+        lay = pool.layout()
+        raw_np = read_device(lay.kv, 41 * lay.slot_bytes)
+        k, v = capi.synth_unit_host(p, 5, tokens[0])
+        per = T * d
+        if dt == capi.PSATTN_KV_BF16:
+            words = np.frombuffer(raw_np, np.uint16).reshape(41, 2, per)
+            dk = (words[:, 0].astype(np.uint32) << 16).view(np.float32)
+            dv = (words[:, 1].astype(np.uint32) << 16).view(np.float32)
+        else:
+            f = np.frombuffer(raw_np, np.float32).reshape(41, 2, per)
+            dk, dv = f[:, 0], f[:, 1]
+        assert dk.reshape(-1).tobytes() == k.reshape(-1).tobytes()
+        assert dv.reshape(-1).tobytes() == v.reshape(-1).tobytes()
+
+
+class _DevBytes:
+    """Wraps a raw device pointer for torch.as_tensor (CUDA array interface)."""
+
+    def __init__(self, ptr, nbytes):
+        self.__cuda_array_interface__ = dict(shape=(nbytes,), typestr="|u1", data=(int(ptr), True), version=3)
+
+
+def read_device(ptr, nbytes) -> bytes:
+    t = torch.as_tensor(_DevBytes(ptr, nbytes), device="cuda")
+    return t.cpu().numpy().tobytes()
+
+
+def test_c1_shape_full_parity(mods, oracle, ref):
+    """BASELINE config 1 (fp32 KV, 32K ctx, 32 q / 8 kv heads, B=16, eps=0.95): every head vs
+    the COMPILED REFERENCE's psa_attention_multi_head on the same synthetic inputs (2 kv heads)."""
+    capi, batch = mods
+    d, T, g, n = 128, 16, 4, 2048
+    for planted in (0.0, 64 / 2048):
+        p = capi.synth_params(seed=1, dim=d, block_tokens=T, skew=8.0, planted_prob=planted, round_bf16=0)
+        units = [0, 5]
+        pool = batch.DevicePool(d, T, capi.PSATTN_KV_F32, n * len(units))
+        pool.fill_synthetic(p, units, [0, n], [n * T] * len(units))
+        torch.cuda.synchronize()
+        qs = [[capi.synth_query(p, uid, h) for h in range(g)] for uid in units]
+        dev = torch.device("cuda")
+        off = np.array([0, n, 2 * n], np.int64)
+        run = batch.BatchRun(pool, torch.tensor(np.array(qs), device=dev),
+                             torch.tensor(np.arange(2 * n, dtype=np.int32), device=dev),
+                             torch.tensor(off, device=dev), n, batch.BatchConfig(epsilon=0.95), want_ranked=True)
+        run.run()
+        torch.cuda.synchronize()
+        st = ref.store(capacity=0)
+        kv_ids = []
+        for u, uid in enumerate(units):
+            k, v = capi.synth_unit_host(p, uid, n * T)
+            for b in range(n):
+                st.put(u * n + b, k[b], v[b])
+            kv_ids.append(np.arange(u * n, (u + 1) * n))
+        allq = np.array([q for qq in qs for q in qq], np.float32)
+        res, union = st.multi_head(allq, np.array(kv_ids), make_config(epsilon=0.95))
+        exact = 0
+        for u in range(len(units)):
+            k, v = capi.synth_unit_host(p, units[u], n * T)
+            bs = BlockSet(list(k), list(v))
+            for h in range(g):
+                r = unpack(run, off, u, h, n)
+                o = res[u * g + h]
+                gpu_ids = r["ids"]
+                if r["bp"] == o.blocks_processed and np.array_equal(gpu_ids + u * n, o.processed_ids):
+                    exact += 1
+                    assert np.max(np.abs(r["out"] - o.output)) <= 1e-3
+                else:
+                    check_parity(oracle, qs[u][h], bs, make_config(epsilon=0.95), 0, gpu_ids, r["bp"], r["out"],
+                                 r["est"])
+        assert exact >= len(units) * g - 1
