@@ -1,0 +1,385 @@
+#!/usr/bin/env python3
+"""PSA decode-attention benchmark (BASELINE.json config 2 on one B200, weak-scaled over N GPUs).
+
+Workload ("step"): one decode step of Llama-3.1-8B at 128K context for a batch of
+8 requests — every (request, layer, q-head) query = 8 x 32 x 32 = 8192 progressive
+sparse attention queries over 2048 kv-head block lists of 8192 blocks (B=16, d=128,
+bf16 KV in the unified HBM pool, eps=0.95, microbatch 1, CuboidMean). Synthetic data
+from the seekable generator (planted pattern of the reference workload: skew 8,
+P(planted)=1/32, i.e. 64 planted blocks per 2048; --dist iso for isotropic keys).
+The pool (~144 GiB) is far larger than L2, so no explicit flush is needed.
+
+`value`  = queries/s over the whole job, inputs resident in HBM (device-timed, max over ranks).
+`e2e`    = same metric through the C ABI batch call with per-step H2D of the queries from
+           pinned host memory and D2H of outputs + stats inside the timed region.
+`--impl reference` times the reference's own CPU implementation (compiled from
+/root/reference into oracle/_ref) on the host cores on a bounded sample.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "PSA decode-attn queries/s, Llama-3.1-8B 128K ctx; HBM GB/s vs peak; KV bytes read"
+UNIT = "queries/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--dist", default="planted", choices=["planted", "iso"])
+    ap.add_argument("--requests", type=int, default=8)
+    ap.add_argument("--layers", type=int, default=32)
+    ap.add_argument("--ctx", type=int, default=131072)
+    ap.add_argument("--hq", type=int, default=32)
+    ap.add_argument("--hkv", type=int, default=8)
+    ap.add_argument("--dim", type=int, default=128)
+    ap.add_argument("--block", type=int, default=16)
+    ap.add_argument("--eps", type=float, default=0.95)
+    ap.add_argument("--microbatch", type=int, default=1)
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--cpu-seconds", type=float, default=20.0, help="budget of the CPU baseline sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def synth(args):
+    from paper_2503_00392_b200 import capi
+    prob = 1.0 / 32.0 if args.dist == "planted" else 0.0
+    return capi.synth_params(seed=args.seed, dim=args.dim, block_tokens=args.block, skew=8.0, planted_prob=prob,
+                             round_bf16=1)
+
+
+# ----------------------------------------------------------------------------------------------
+# Reference CPU arm: the unmodified reference library (oracle/_ref) on the host cores.
+# ----------------------------------------------------------------------------------------------
+class ReferenceCPU:
+    """psattn::psa_attention_multi_head (reference engine.cpp:240-260) of the unmodified reference
+    library on kv-head units of the same workload shape (n = ctx/B blocks, GQA group hq/hkv, same
+    synthetic bf16 values upcast to fp32), one TieredBlockStore per host thread (a shared store
+    serialises on its mutex, reference store.hpp:112)."""
+
+    def __init__(self, args, rank_offset=0):
+        from oracle.pyoracle import RefDriver, make_config
+        from paper_2503_00392_b200 import capi
+        drv = RefDriver()
+        p = synth(args)
+        self.g = args.hq // args.hkv
+        self.n = args.ctx // args.block
+        self.threads = max(1, min(os.cpu_count() or 1, 64))
+        self.stores, self.qs = [None] * self.threads, [None] * self.threads
+        self.cfg = make_config(epsilon=args.eps, microbatch_size=args.microbatch)
+        self.ids = np.arange(self.n, dtype=np.int64)[None, :]
+        self.args = args
+
+        def setup(t):
+            uid = 10_000_000 + rank_offset + t
+            k, v = capi.synth_unit_host(p, uid, args.ctx)
+            st = drv.store(capacity=0)
+            st.put_many(0, k, v)
+            self.stores[t] = st
+            self.qs[t] = np.array([capi.synth_query(p, uid, h) for h in range(self.g)], np.float32)
+            st.multi_head(self.qs[t], self.ids, self.cfg, want_ids=False)  # warm
+
+        ths = [threading.Thread(target=setup, args=(t,)) for t in range(self.threads)]
+        [th.start() for th in ths]
+        [th.join() for th in ths]
+
+    def sample(self, seconds):
+        """Every thread runs whole GQA groups until the window closes; returns queries/s."""
+        counts = [0] * self.threads
+        t0 = time.perf_counter()
+        stop_at = t0 + seconds
+
+        def work(t):
+            while True:
+                self.stores[t].multi_head(self.qs[t], self.ids, self.cfg, want_ids=False)
+                counts[t] += self.g
+                if time.perf_counter() >= stop_at:
+                    break
+
+        ths = [threading.Thread(target=work, args=(t,)) for t in range(self.threads)]
+        [th.start() for th in ths]
+        [th.join() for th in ths]
+        el = time.perf_counter() - t0
+        desc = (f"{self.threads} host threads, each on its own kv-head unit of {self.n} blocks "
+                f"(ctx {self.args.ctx}, GQA group {self.g}) via psa_attention_multi_head, eps {self.args.eps}; "
+                f"{sum(counts)} queries in {el:.1f}s")
+        return sum(counts) / el, desc
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    K, W = args.steps, args.warmup
+    per_step = max(args.cpu_seconds / max(K + W, 1), 0.5)
+    ref = ReferenceCPU(args)
+    vals = []
+    desc, threads = "", ref.threads
+    for i in range(W + K):
+        qps, desc = ref.sample(per_step)
+        if i >= W:
+            vals.append(qps)
+    v = float(np.median(vals))
+    cpu = os.popen("lscpu | grep 'Model name' | head -1").read().strip().split(":")[-1].strip()
+    line = dict(metric=METRIC, value=v, unit=UNIT, n_gpus=args.gpus, steps=K, warmup=W, ms_per_step=None,
+                higher_is_better=True, scaling="weak", vs_baseline=None, dtype="f32", data="synthetic",
+                impl="reference",
+                config=dict(workload="config2 sample: Llama-3.1-8B shape kv-head units, 128K ctx, "
+                                     f"{args.dist} keys", ctx=args.ctx, group=args.hq // args.hkv, eps=args.eps,
+                            microbatch=args.microbatch),
+                cpu_baseline=dict(value=v, unit=UNIT, cores=threads, kind="reference", sample=desc, cpu=cpu),
+                e2e=dict(value=v, unit=UNIT, h2d_bytes_per_step=0, d2h_bytes_per_step=0))
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------------------------
+# Our arm
+# ----------------------------------------------------------------------------------------------
+class ClockSampler:
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = f"/tmp/psa_clocks_{os.getpid()}.csv"
+
+    def start(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f,
+                                         stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return dict(sm_mhz=None, sm_max_mhz=None, reasons=["nvidia-smi unavailable"])
+        self.proc.terminate()
+        self.proc.wait()
+        self.f.close()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[3:7]):
+                if val.lower() == "active":
+                    reasons.add(nm)
+        return dict(sm_mhz=float(np.median(sm)) if sm else None, sm_max_mhz=mx, reasons=sorted(reasons),
+                    samples=len(sm))
+
+
+def measured_peak():
+    try:
+        mp = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        return float(mp["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def ncu_traffic(stage):
+    """dram bytes per launch of the stage's kernel from the committed ncu summary, if any."""
+    try:
+        s = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
+        return s["kernels"][stage]["dram_bytes_per_launch"]
+    except Exception:
+        return None
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    from paper_2503_00392_b200 import batch, capi
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    p = synth(args)
+    g = args.hq // args.hkv
+    n = args.ctx // args.block
+    U = args.requests * args.layers * args.hkv
+    nq = U * g
+    # ---- unified pool: every (request, layer, kv-head) list is n consecutive slots ----
+    pool = batch.DevicePool(args.dim, args.block, capi.PSATTN_KV_BF16, U * n)
+    unit_ids = np.arange(U, dtype=np.int64) + rank * U  # distinct requests per rank (weak scaling)
+    t0 = time.time()
+    pool.fill_synthetic(p, unit_ids, np.arange(U, dtype=np.int64) * n, np.full(U, args.ctx, np.int64))
+    torch.cuda.synchronize()
+    fill_s = time.time() - t0
+    q_host = np.zeros((U, g, args.dim), np.float32)
+    for u in range(U):
+        for h in range(g):
+            q_host[u, h] = capi.synth_query(p, int(unit_ids[u]), h)
+    q_dev = torch.tensor(q_host, device=dev)
+    slots = torch.arange(U * n, dtype=torch.int32, device=dev)
+    off = torch.arange(U + 1, dtype=torch.int64, device=dev) * n
+    cfg = batch.BatchConfig(epsilon=args.eps, microbatch_size=args.microbatch)
+    run = batch.BatchRun(pool, q_dev, slots, off, n, cfg, want_ranked=True)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if ws > 1:
+            dist.barrier()
+
+    # ---- device-timed region (inputs resident) ----
+    for _ in range(args.warmup):
+        launches_per_step = run.run()
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    capi.lib.psattn_profile_read(None, None, 1)
+    capi.lib.psattn_profile_enable(1)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        launches_per_step = run.run()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    capi.lib.psattn_profile_enable(0)
+    barrier()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    stage_ms = np.zeros(4, np.float64)
+    stage_n = np.zeros(4, np.int64)
+    capi.lib.psattn_profile_read(stage_ms.ctypes.data, stage_n.ctypes.data, 1)
+    if ws > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_per_step = ms / args.steps
+    value = nq * ws * args.steps / (ms / 1e3)
+
+    # ---- algorithmic bytes ----
+    un = run.union_blocks().cpu().numpy()
+    bp = run.bp.cpu().numpy()
+    torch.cuda.synchronize()
+    lay = pool.layout()
+    meta_b = U * n * lay.meta_bytes
+    kv_union_b = int(un.sum()) * lay.slot_bytes
+    kv_sum_b = int(bp.sum()) * lay.slot_bytes
+    qo_b = 2 * nq * args.dim * 4
+    step_bytes = meta_b + kv_union_b + qo_b
+    kv_full_b = U * n * lay.slot_bytes
+    stage_names = ["oracle", "score", "order", "progressive"]
+    per_launch_ms = {s: stage_ms[i] / max(stage_n[i], 1) for i, s in enumerate(stage_names) if stage_n[i] > 0}
+    stage_bytes = {"score": meta_b + nq * args.dim * 4, "progressive": kv_union_b + qo_b,
+                   "order": None, "oracle": None}
+    dom = max(per_launch_ms, key=per_launch_ms.get)
+    peak, peak_kind = measured_peak()
+    ach = (stage_bytes[dom] / (per_launch_ms[dom] / 1e3) / 1e9) if stage_bytes.get(dom) else None
+    roofline = dict(bound="hbm", kernel=dom, achieved=ach, peak=peak, peak_kind=peak_kind, unit="GB/s",
+                    frac=(ach / peak) if ach else None, traffic=ncu_traffic(dom),
+                    algorithmic_bytes_per_launch=stage_bytes.get(dom), launch_ms=per_launch_ms[dom])
+    step_gbs = step_bytes / (ms_per_step / 1e3) / 1e9
+
+    # ---- e2e through the C ABI batch call, host buffers, copies inside the timed region ----
+    q_pin = torch.from_numpy(q_host).pin_memory()
+    out_pin = torch.empty(run.out.shape, dtype=torch.float32).pin_memory()
+    bp_pin = torch.empty(nq, dtype=torch.int64).pin_memory()
+    est_pin = torch.empty(nq, dtype=torch.float64).pin_memory()
+    term_pin = torch.empty(nq, dtype=torch.int32).pin_memory()
+    h2d = q_pin.numel() * 4
+    d2h = out_pin.numel() * 4 + nq * (8 + 8 + 4)
+
+    def e2e_step():
+        run.q.copy_(q_pin, non_blocking=True)
+        run.run()
+        out_pin.copy_(run.out, non_blocking=True)
+        bp_pin.copy_(run.bp, non_blocking=True)
+        est_pin.copy_(run.est, non_blocking=True)
+        term_pin.copy_(run.term, non_blocking=True)
+
+    for _ in range(args.warmup):
+        e2e_step()
+    torch.cuda.synchronize()
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        e2e_step()
+        stream.synchronize()  # the caller consumes each step's outputs on the host
+    e2e_s = time.perf_counter() - t0
+    if ws > 1:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_val = nq * ws * args.steps / e2e_s
+
+    # ---- CPU baseline (rank 0, N=1 only) ----
+    cpu_base = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        try:
+            ref = ReferenceCPU(args)
+            v, desc = ref.sample(args.cpu_seconds)
+            cpu_base = dict(value=v, unit=UNIT, cores=ref.threads, kind="reference", sample=desc)
+        except Exception as e:  # noqa: BLE001
+            cpu_base = dict(value=None, unit=UNIT, cores=0, kind="reference", sample=f"unavailable: {e}")
+
+    if rank == 0:
+        line = dict(
+            metric=METRIC, value=value, unit=UNIT, n_gpus=ws, steps=args.steps, warmup=args.warmup,
+            ms_per_step=ms_per_step, higher_is_better=True, scaling="weak", vs_baseline=None, dtype="bf16",
+            data=f"synthetic ({args.dist} keys, seekable generator, seed {args.seed})",
+            config=dict(workload="config2: Llama-3.1-8B shape, 32 layers, batch 8 decode, 128K ctx, eps 0.95",
+                        requests_per_gpu=args.requests, layers=args.layers, ctx=args.ctx, hq=args.hq,
+                        hkv=args.hkv, dim=args.dim, block=args.block, eps=args.eps, microbatch=args.microbatch,
+                        queries_per_step=nq * ws, kv_dtype="bf16", l2="inputs (~144 GiB/GPU) >> 126 MB L2; no flush",
+                        parallelism=f"request sharding x{ws}, no collective"),
+            roofline=roofline,
+            step_roofline=dict(achieved=step_gbs, peak=peak, frac=step_gbs / peak, unit="GB/s",
+                               bytes_per_step=step_bytes, meta_bytes=meta_b, kv_union_bytes=kv_union_b,
+                               qo_bytes=qo_b),
+            kv_fraction_read=kv_union_b / kv_full_b, kv_fraction_per_head_sum=kv_sum_b / (kv_full_b * g),
+            mean_blocks_processed=float(bp.mean()),
+            stage_ms_per_step={k: v for k, v in per_launch_ms.items()},
+            cpu_baseline=cpu_base,
+            e2e=dict(value=e2e_val, unit=UNIT, h2d_bytes_per_step=h2d, d2h_bytes_per_step=d2h),
+            gpu_launches=int(launches_per_step) * args.steps,
+            clocks=clk, setup=dict(fill_seconds=fill_s, pool_gib=(U * n * (lay.slot_bytes + lay.meta_bytes)) / 2**30),
+        )
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

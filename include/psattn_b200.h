@@ -122,8 +122,16 @@ int psattn_run_batch(psattn_pool* pool, const psattn_batch* b, void* workspace, 
  * same stream and workspace. out_union: device int64 [n_units]. */
 int psattn_batch_union_blocks(const psattn_batch* b, void* workspace, int64_t* out_union, void* stream);
 
-/* Per-kernel launch counts of the last psattn_run_batch (score, order, progressive). */
+/* Number of kernels the last psattn_run_batch launched on this process. */
 int psattn_batch_last_launches(int32_t* out_count);
+
+/* Stage timing (benchmark instrumentation). While enabled, psattn_run_batch
+ * records CUDA events around each kernel on its own stream (no host sync).
+ * psattn_profile_read waits for the recorded events and returns accumulated
+ * milliseconds and launch counts per stage [oracle-mass, score, order,
+ * progressive]; reset != 0 clears the accumulators. */
+int psattn_profile_enable(int32_t enable);
+int psattn_profile_read(double* ms, int64_t* count, int32_t reset);
 
 /* ---- Seekable synthetic workload (bench + parity; not on the attention path) ----
  * Values are a pure function of (seed, unit_id, block, token, dim), identical on

@@ -230,6 +230,8 @@ class RefDriver:
         L.refdrv_put.argtypes = [C.c_void_p, C.c_int64, C.c_int32, C.c_int64, C.c_int32, C.c_int32, C.c_void_p,
                                  C.c_void_p]
         L.refdrv_release.argtypes = [C.c_void_p, C.c_int64]
+        L.refdrv_put_many.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_int32, C.c_int64, C.c_int32, C.c_int32,
+                                      C.c_void_p, C.c_void_p]
         L.refdrv_stats.argtypes = [C.c_void_p, C.c_void_p]
         L.refdrv_layer_stats.argtypes = [C.c_void_p, C.c_int32, C.c_void_p]
         L.refdrv_contains.argtypes = [C.c_void_p, C.c_int64, C.POINTER(C.c_int32)]
@@ -278,6 +280,14 @@ class RefStore:
         k = np.ascontiguousarray(keys, np.float32)
         v = np.ascontiguousarray(values, np.float32)
         st = self.L.refdrv_put(self.h, block_id, layer, owner, k.shape[0], k.shape[1], _p(k), _p(v))
+        if st:
+            raise RuntimeError(f"status {st}: {self.drv.error()}")
+
+    def put_many(self, first_id, keys, values, layer=0, owner=0):
+        """keys/values [n, ntok, d] fp32."""
+        k = np.ascontiguousarray(keys, np.float32)
+        v = np.ascontiguousarray(values, np.float32)
+        st = self.L.refdrv_put_many(self.h, k.shape[0], first_id, layer, owner, k.shape[1], k.shape[2], _p(k), _p(v))
         if st:
             raise RuntimeError(f"status {st}: {self.drv.error()}")
 

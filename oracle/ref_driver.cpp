@@ -128,6 +128,17 @@ int refdrv_put(void* s, int64_t id, int32_t layer, int64_t owner, int32_t ntok, 
     });
 }
 
+// n blocks of ntok x d each, ids first_id.., keys/values [n][ntok][d] (setup helper).
+int refdrv_put_many(void* s, int64_t n, int64_t first_id, int32_t layer, int64_t owner, int32_t ntok, int32_t d,
+                    const float* k, const float* v) {
+    const std::size_t per = static_cast<std::size_t>(ntok) * static_cast<std::size_t>(d);
+    for (int64_t i = 0; i < n; ++i) {
+        const int rc = refdrv_put(s, first_id + i, layer, owner, ntok, d, k + per * i, v + per * i);
+        if (rc) return rc;
+    }
+    return 0;
+}
+
 int refdrv_release(void* s, int64_t owner) {
     return guarded([&] {
         static_cast<Store*>(s)->impl.release_request(owner);

@@ -5,6 +5,8 @@
 #include <string.h>
 
 #include <algorithm>
+#include <array>
+#include <mutex>
 #include <cmath>
 #include <string>
 #include <vector>
@@ -24,6 +26,17 @@ namespace psa {
 namespace {
 thread_local std::string g_err = "";
 std::atomic<int> g_last_launches{0};
+
+// Stage timing (benchmark instrumentation): events recorded around each kernel
+// of psattn_run_batch on the launching stream; read back on request.
+struct Profiler {
+    std::mutex mu;
+    bool on = false;
+    std::vector<std::array<cudaEvent_t, 5>> pending;
+    double ms[4] = {0, 0, 0, 0};
+    int64_t count[4] = {0, 0, 0, 0};
+};
+Profiler g_prof;
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 }  // namespace
@@ -361,9 +374,57 @@ int psattn_run_batch(psattn_pool* pool, const psattn_batch* b, void* workspace, 
     if (rc) return rc;
     if (!workspace) return fail(PSATTN_ERR_INVALID_ARGUMENT, "psattn_run_batch: null workspace");
     const BatchView v = make_view(pool, b, workspace);
-    const int n = launch_batch(pool->v, v, (cudaStream_t)stream);
+    std::array<cudaEvent_t, 5> ev{};
+    bool prof = false;
+    {
+        std::lock_guard<std::mutex> lk(g_prof.mu);
+        prof = g_prof.on;
+    }
+    if (prof)
+        for (auto& e : ev) cudaEventCreate(&e);
+    const int n = launch_batch(pool->v, v, (cudaStream_t)stream, prof ? ev.data() : nullptr);
     if (n < 0) return cuda_fail(cudaGetLastError(), "psattn_run_batch launch");
+    if (prof) {
+        std::lock_guard<std::mutex> lk(g_prof.mu);
+        g_prof.pending.push_back(ev);
+        g_prof.count[1] += v.rank_oracle ? 0 : 1;
+        g_prof.count[0] += v.has_oracle ? 1 : 0;
+        g_prof.count[2] += 1;
+        g_prof.count[3] += 1;
+    }
     g_last_launches.store(n);
+    return PSATTN_OK;
+}
+
+int psattn_profile_enable(int32_t enable) {
+    std::lock_guard<std::mutex> lk(g_prof.mu);
+    g_prof.on = enable != 0;
+    return PSATTN_OK;
+}
+
+int psattn_profile_read(double* ms, int64_t* count, int32_t reset) {
+    std::lock_guard<std::mutex> lk(g_prof.mu);
+    for (auto& ev : g_prof.pending) {
+        cudaError_t e = cudaEventSynchronize(ev[4]);
+        if (e != cudaSuccess) return cuda_fail(e, "profile read");
+        for (int s = 0; s < 4; ++s) {
+            float t = 0.f;
+            cudaEventElapsedTime(&t, ev[s], ev[s + 1]);
+            g_prof.ms[s] += t;
+        }
+        for (auto& x : ev) cudaEventDestroy(x);
+    }
+    g_prof.pending.clear();
+    for (int s = 0; s < 4; ++s) {
+        if (ms) ms[s] = g_prof.ms[s];
+        if (count) count[s] = g_prof.count[s];
+    }
+    if (reset) {
+        for (int s = 0; s < 4; ++s) {
+            g_prof.ms[s] = 0;
+            g_prof.count[s] = 0;
+        }
+    }
     return PSATTN_OK;
 }
 

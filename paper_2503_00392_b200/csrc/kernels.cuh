@@ -61,7 +61,7 @@ cudaError_t launch_synth_fill(const PoolView& p, uint64_t seed, float skew, floa
                               const int64_t* d_tokens, int64_t max_blocks, float* d_dirs, cudaStream_t st);
 void launch_psa(const PoolView& p, const BatchView& b, cudaStream_t st);
 // Returns the number of kernel launches issued, or -1 on error (cudaGetLastError has it).
-int launch_batch(const PoolView& p, const BatchView& b, cudaStream_t st);
+int launch_batch(const PoolView& p, const BatchView& b, cudaStream_t st, cudaEvent_t* marks = nullptr);
 cudaError_t launch_union(const BatchView& b, int64_t* out_union, cudaStream_t st);
 
 }  // namespace psa

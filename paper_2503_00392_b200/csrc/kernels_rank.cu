@@ -238,8 +238,10 @@ static void launch_oracle(const PoolView& p, const BatchView& b, dim3 grid, cuda
     }
 }
 
-int launch_batch(const PoolView& p, const BatchView& b, cudaStream_t st) {
+int launch_batch(const PoolView& p, const BatchView& b, cudaStream_t st, cudaEvent_t* marks) {
+    // marks (optional, 5 events): start | oracle | score | order | progressive
     int launches = 0;
+    if (marks) cudaEventRecord(marks[0], st);
     const int64_t chunks = (b.max_n + kScoreWarps - 1) / kScoreWarps;
     dim3 grid((unsigned)(chunks < 65535 ? (chunks > 0 ? chunks : 1) : 65535), (unsigned)b.n_units);
     if (b.has_oracle) {
@@ -247,19 +249,23 @@ int launch_batch(const PoolView& p, const BatchView& b, cudaStream_t st) {
         else launch_oracle<__nv_bfloat16>(p, b, grid, st);
         ++launches;
     }
+    if (marks) cudaEventRecord(marks[1], st);
     if (!b.rank_oracle) {
         if (p.dtype == 0) launch_score<float>(p, b, grid, st);
         else launch_score<__nv_bfloat16>(p, b, grid, st);
         ++launches;
     }
+    if (marks) cudaEventRecord(marks[2], st);
     const int nq = b.n_units * b.g;
     const size_t smem = (size_t)(b.max_n <= kSmemSortMax ? b.max_n : 0) * sizeof(uint64_t);
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     sort_kernel<<<nq, kSortThreads, smem, st>>>(b);
     ++launches;
+    if (marks) cudaEventRecord(marks[3], st);
     launch_psa(p, b, st);
     ++launches;
+    if (marks) cudaEventRecord(marks[4], st);
     if (cudaPeekAtLastError() != cudaSuccess) return -1;
     return launches;
 }

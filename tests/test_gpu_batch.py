@@ -219,7 +219,7 @@ class _DevBytes:
     """Wraps a raw device pointer for torch.as_tensor (CUDA array interface)."""
 
     def __init__(self, ptr, nbytes):
-        self.__cuda_array_interface__ = dict(shape=(nbytes,), typestr="|u1", data=(int(ptr), True), version=3)
+        self.__cuda_array_interface__ = dict(shape=(nbytes,), typestr="|u1", data=(int(ptr), False), version=3)
 
 
 def read_device(ptr, nbytes) -> bytes:
