@@ -197,7 +197,7 @@ int read_meta(const psattn_pool* pool, int64_t slot, float* mean, float* lo, flo
 
 // ---- workspace carving ----
 struct WsLayout {
-    size_t keys, rpos, rslot, omass, total;
+    size_t keys, rpos, omass, total;
 };
 
 static WsLayout ws_layout(const psattn_batch* b) {
@@ -207,8 +207,6 @@ static WsLayout ws_layout(const psattn_batch* b) {
     l.keys = o;
     o += align_up(hb * 8, 256);
     l.rpos = o;
-    o += align_up(hb * 4, 256);
-    l.rslot = o;
     o += align_up(hb * 4, 256);
     l.omass = o;
     if (b->ranking_mode == PSATTN_RANK_ORACLE || b->audit_coverage) o += align_up(hb * 8, 256);
@@ -267,7 +265,6 @@ BatchView make_view(const psattn_pool* pool, const psattn_batch* b, void* worksp
     v.term = b->terminated;
     v.keys = reinterpret_cast<uint64_t*>(ws + l.keys);
     v.rpos = b->ranked_pos ? b->ranked_pos : reinterpret_cast<int32_t*>(ws + l.rpos);
-    v.rslot = reinterpret_cast<int32_t*>(ws + l.rslot);
     v.omass = v.has_oracle ? reinterpret_cast<double*>(ws + l.omass) : nullptr;
     v.iest = b->iter_est;
     (void)pool;

@@ -44,7 +44,6 @@ struct BatchView {
     // workspace
     uint64_t* keys;
     int32_t* rpos;
-    int32_t* rslot;
     double* omass;
     double* iest;  // optional per-rank estimate at microbatch boundaries
 };

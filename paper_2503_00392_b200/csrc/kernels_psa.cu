@@ -1,4 +1,5 @@
-// kernels_psa.cu — K4/K5 progressive attention kernel (sm_100a).
+// kernels_psa.cu — K3 ordering (lazy tranche selection) fused with K4/K5, the
+// persistent progressive attention kernel (sm_100a).
 #include <cuda_bf16.h>
 #include <float.h>
 #include <math.h>
@@ -9,11 +10,20 @@
 namespace psa {
 
 // =============================================================================
-// K4/K5: progressive attention. One CTA (4 warps) per (unit, q-head) query.
-// The ranked list is consumed in chunks of 32 ranks:
-//   1. K pass  — each warp scores 8 blocks of the chunk: fp32 q.k*scale per token
+// One CTA (8 warps) per (unit, q-head) query. Two interleaved loops:
+//
+// ORDER (K3, rank_by_scores, reference metadata.cpp:87-96) — lazily, in
+// tranches: the next C <= 1024 ranks are the C smallest sort keys above the
+// last consumed key (keys from score_kernel encode score desc / block id asc).
+// A bucket select over the head's n keys (min/max, 2048-bin histogram,
+// refinement) finds the cut, the survivors are gathered and bitonic-sorted in
+// shared memory. The first tranche targets 512 ranks — enough for most planted
+// queries — so a head that stops early never pays for a full sort of n keys.
+//
+// PROGRESS (K4/K5, ProgressiveRun::consume + psa_attention / topk_attention,
+// reference engine.cpp:104-127, 162-171, 211-231) over chunks of 32 ranks:
+//   1. K pass  — each warp scores 4 blocks: fp32 q.k*scale per token
 //                (attention.hpp:41-46), block max, exp-sum, log_as (:50-75);
-//                per-token weights are staged in shared memory;
 //   2. decide  — warp 0 scans the chunk in rank order in fp64: running
 //                log-sum-exp and min of the block masses (CoverageEstimator,
 //                engine.cpp:38-55), evaluates the estimate at every microbatch
@@ -21,15 +31,185 @@ namespace psa {
 //                (engine.cpp:125) or the top-k budget (engine.cpp:221-227);
 //   3. V pass  — only ranks before the stop point read V and are merged
 //                (online softmax, attention.hpp:83-102).
-// No host round trip: the stop decision lives in shared memory. K bytes of at
-// most one partial chunk past the stop point are the speculative waste.
+// The stop decision never leaves shared memory: no host round trip. K bytes of
+// at most one partial chunk past the stop point are the speculative waste.
 // =============================================================================
-constexpr int kPsaWarps = 4;
+constexpr int kPsaWarps = 8;
+constexpr int kPsaThreads = kPsaWarps * 32;
 constexpr int kChunk = 32;
 constexpr int kBpw = kChunk / kPsaWarps;
+constexpr int kTCap = 1024;
+constexpr int kBins = 2048;
+constexpr int kFirstTranche = 512;
+
+template <int TOK>
+struct PsaSmem {
+    uint64_t tb[kTCap];       // sorted keys of the current tranche
+    int32_t tslot[kTCap];     // their pool slots
+    uint32_t hist[kBins];     // bucket-select histogram; reused for the final merge
+    float w[kPsaWarps][kBpw][TOK];
+    float mb[kPsaWarps][kBpw], lb[kPsaWarps][kBpw];
+    float la[kChunk];
+    unsigned long long red_min, red_max;
+    unsigned int red_cnt, gcount, excl;
+    int bstar;
+    int commit, fin;
+    double est, acc;
+    float m[kPsaWarps], l[kPsaWarps];
+};
+
+__device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long x) {
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+        const unsigned long long y = __shfl_xor_sync(PSA_FULL, x, o);
+        x = y < x ? y : x;
+    }
+    return x;
+}
+__device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long x) {
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+        const unsigned long long y = __shfl_xor_sync(PSA_FULL, x, o);
+        x = y > x ? y : x;
+    }
+    return x;
+}
+
+// All-ascending bitonic network on a[0, n) in shared memory (indices >= n act as +inf).
+__device__ __forceinline__ void bitonic_smem(uint64_t* a, int n) {
+    int n2 = 1;
+    while (n2 < n) n2 <<= 1;
+    for (int k = 2; k <= n2; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < (n2 >> 1); i += blockDim.x) {
+                const int lo = ((i / j) * 2 * j) + (i % j);
+                const int hi = (j == (k >> 1)) ? (lo ^ (k - 1)) : (lo + j);
+                if (hi < n) {
+                    const uint64_t x = a[lo], y = a[hi];
+                    if (x > y) {
+                        a[lo] = y;
+                        a[hi] = x;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// Next tranche: the C (<= kTCap, ~target) smallest keys greater than `last` (all keys if first).
+template <int TOK>
+__device__ int select_tranche(PsaSmem<TOK>& s, const uint64_t* __restrict__ keys, int64_t n, uint64_t last,
+                              bool first, unsigned target) {
+    const int tid = threadIdx.x, lane = tid & 31;
+    unsigned long long lmin = ~0ull, lmax = 0;
+    unsigned lcnt = 0;
+    for (int64_t i = tid; i < n; i += kPsaThreads) {
+        const unsigned long long k = keys[i];
+        if (first || k > last) {
+            lmin = k < lmin ? k : lmin;
+            lmax = k > lmax ? k : lmax;
+            ++lcnt;
+        }
+    }
+    if (tid == 0) {
+        s.red_min = ~0ull;
+        s.red_max = 0;
+        s.red_cnt = 0;
+        s.gcount = 0;
+    }
+    __syncthreads();
+    lmin = warp_min_u64(lmin);
+    lmax = warp_max_u64(lmax);
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) lcnt += __shfl_xor_sync(PSA_FULL, lcnt, o);
+    if (lane == 0) {
+        atomicMin(&s.red_min, lmin);
+        atomicMax(&s.red_max, lmax);
+        atomicAdd(&s.red_cnt, lcnt);
+    }
+    __syncthreads();
+    const uint64_t kmax = s.red_max;
+    uint64_t tau = kmax;
+    if (s.red_cnt > (unsigned)kTCap) {
+        uint64_t lo = s.red_min, hi = kmax;
+        unsigned need = target, before = 0;
+        for (int it = 0; it < 10; ++it) {
+            const uint64_t span = hi - lo;
+            const int bits = 64 - __clzll((long long)span);
+            const int sh = bits > 11 ? bits - 11 : 0;
+            for (int i = tid; i < kBins; i += kPsaThreads) s.hist[i] = 0;
+            __syncthreads();
+            for (int64_t i = tid; i < n; i += kPsaThreads) {
+                const uint64_t k = keys[i];
+                if ((first || k > last) && k >= lo && k <= hi) atomicAdd(&s.hist[(k - lo) >> sh], 1u);
+            }
+            __syncthreads();
+            // first bin b with cum(b) >= need: each thread owns 8 consecutive bins
+            constexpr int per = kBins / kPsaThreads;
+            unsigned loc = 0;
+#pragma unroll
+            for (int j = 0; j < per; ++j) loc += s.hist[tid * per + j];
+            unsigned inc = loc;  // inclusive warp scan
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned y = __shfl_up_sync(PSA_FULL, inc, o);
+                if (lane >= o) inc += y;
+            }
+            __shared__ unsigned wsum[kPsaWarps];
+            if (lane == 31) wsum[tid >> 5] = inc;
+            __syncthreads();
+            unsigned wbase = 0;
+            for (int w = 0; w < (tid >> 5); ++w) wbase += wsum[w];
+            unsigned cum = wbase + inc - loc;  // exclusive prefix of this thread's bins
+            if (cum < need && need <= cum + loc) {
+#pragma unroll 1
+                for (int j = 0; j < per; ++j) {
+                    const unsigned c = s.hist[tid * per + j];
+                    if (need <= cum + c) {
+                        s.bstar = tid * per + j;
+                        s.excl = cum;
+                        break;
+                    }
+                    cum += c;
+                }
+            }
+            __syncthreads();
+            const int bs = s.bstar;
+            const unsigned ex = s.excl, incl = ex + s.hist[bs];
+            const uint64_t width_m1 = (sh >= 64) ? ~0ull : ((1ull << sh) - 1ull);
+            const uint64_t bin_lo = lo + ((uint64_t)bs << sh);
+            if (before + incl <= (unsigned)kTCap) {
+                tau = (hi - bin_lo <= width_m1) ? hi : bin_lo + width_m1;
+                break;
+            }
+            if (before + ex >= 32) {
+                tau = bin_lo - 1;  // take the bins below bs
+                break;
+            }
+            before += ex;
+            need -= ex;
+            lo = bin_lo;
+            if (hi - lo > width_m1) hi = lo + width_m1;
+            __syncthreads();
+        }
+    }
+    for (int64_t i = tid; i < n; i += kPsaThreads) {
+        const uint64_t k = keys[i];
+        if ((first || k > last) && k <= tau) {
+            const unsigned idx = atomicAdd(&s.gcount, 1u);
+            if (idx < (unsigned)kTCap) s.tb[idx] = k;
+        }
+    }
+    __syncthreads();
+    const int C = (int)min(s.gcount, (unsigned)kTCap);
+    bitonic_smem(s.tb, C);
+    return C;
+}
 
 template <typename KV, int DPL, int TOK>
-__global__ void __launch_bounds__(kPsaWarps * 32) psa_kernel(PoolView p, BatchView b) {
+__global__ void __launch_bounds__(kPsaThreads, 3) psa_kernel(PoolView p, BatchView b) {
+    __shared__ PsaSmem<TOK> s;
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const int qi = blockIdx.x;
@@ -37,7 +217,7 @@ __global__ void __launch_bounds__(kPsaWarps * 32) psa_kernel(PoolView p, BatchVi
     const int64_t off = b.list_off[u];
     const int64_t n = b.list_off[u + 1] - off;
     const int64_t hb = off * b.g + (int64_t)h * n;
-    const int32_t* __restrict__ rslot = b.rslot + hb;
+    const uint64_t* keys = b.keys + hb;
     const int64_t limit = b.topk > 0 ? (b.topk < n ? b.topk : n) : n;
     const double eps = b.topk > 0 ? 1.0 : b.eps;
     const int d = b.d;
@@ -47,39 +227,46 @@ __global__ void __launch_bounds__(kPsaWarps * 32) psa_kernel(PoolView p, BatchVi
     const float fscale = (float)b.scale;  // engine.cpp:113
     constexpr int TSH = 5 - Log2<TOK>::v;  // lanes per token after reduce-scatter = 1 << TSH
     const int my_tok = lane >> TSH;
-
-    __shared__ __align__(16) float s_w[kPsaWarps][kBpw][TOK];  // per-token weights exp(s - m_b)
-    __shared__ float s_mb[kPsaWarps][kBpw], s_lb[kPsaWarps][kBpw];
-    __shared__ float s_la[kChunk];
-    __shared__ int s_commit, s_final;
-    __shared__ double s_est, s_acc;
-    __shared__ float s_m[kPsaWarps], s_l[kPsaWarps];
-    __shared__ float s_o[kPsaWarps][256];
+    const uint64_t pmask = (b.pos_bits >= 64) ? ~0ull : ((1ull << b.pos_bits) - 1ull);
 
     float q[DPL];
     load_row<DPL>(b.q + ((size_t)u * b.g + h) * d + base, full, lim, q);
 
-    // warp-local online-softmax state
-    float M = -INFINITY, L = 0.0f, O[DPL];
+    float M = -INFINITY, L = 0.0f, O[DPL];  // warp-local online-softmax state
 #pragma unroll
     for (int j = 0; j < DPL; ++j) O[j] = 0.0f;
-    // coverage state (warp 0, lane-uniform)
-    double acc = -INFINITY, mn = INFINITY;
+    double acc = -INFINITY, mn = INFINITY;  // coverage state (warp 0, lane-uniform)
 
     const double* omass = b.has_oracle ? (b.omass + hb) : nullptr;
-    const int32_t* rpos = b.rpos + hb;
     const KV* kv = reinterpret_cast<const KV*>(p.kv);
     const int64_t slot_elems = p.slot_bytes / (int64_t)sizeof(KV);
     const int64_t v_off = (int64_t)p.T * d;
 
-    for (int64_t cb = 0;; cb += kChunk) {
-        const int cnt = (int)((limit - cb) < kChunk ? (limit - cb) : kChunk);
+    int64_t tr0 = 0;  // global rank of s.tb[0]
+    int tc = 0;       // ranks in the current tranche
+    uint64_t last = 0;
+    for (int64_t cb = 0;;) {
+        if (cb >= tr0 + tc) {  // ---- ORDER: next tranche ----
+            tr0 += tc;
+            tc = select_tranche(s, keys, n, last, tr0 == 0, tr0 == 0 ? kFirstTranche : kTCap);
+            last = s.tb[tc - 1];
+            for (int i = threadIdx.x; i < tc; i += kPsaThreads) {
+                const int32_t pos = (int32_t)(s.tb[i] & pmask);
+                b.rpos[hb + tr0 + i] = pos;
+                s.tslot[i] = b.slots[off + pos];
+            }
+            __syncthreads();
+        }
+        const int64_t room = tr0 + tc - cb;
+        int cnt = (int)((limit - cb) < kChunk ? (limit - cb) : kChunk);
+        if (room < cnt) cnt = (int)room;
+        const int ci = (int)(cb - tr0);
         // ---- 1. K pass ----
 #pragma unroll 1
         for (int j = 0; j < kBpw; ++j) {
             const int rl = warp * kBpw + j;
             if (rl >= cnt) break;
-            const int32_t slot = rslot[cb + rl];
+            const int32_t slot = s.tslot[ci + rl];
             const int nt = p.ntok[slot];
             const KV* kp = kv + (int64_t)slot * slot_elems + base;
             float part[TOK];
@@ -97,18 +284,18 @@ __global__ void __launch_bounds__(kPsaWarps * 32) psa_kernel(PoolView p, BatchVi
                 for (int jj = 0; jj < DPL; ++jj) a = fmaf(q[jj], kr[jj], a);
                 part[t] = a;
             }
-            float s = reduce_scatter<TOK>(part, lane) * fscale;
-            s = my_tok < nt ? s : -INFINITY;
-            const float mb = warp_max(s);
-            const float w = my_tok < nt ? expf(s - mb) : 0.0f;
+            float sc = reduce_scatter<TOK>(part, lane) * fscale;
+            sc = my_tok < nt ? sc : -INFINITY;
+            const float mb = warp_max(sc);
+            const float w = my_tok < nt ? expf(sc - mb) : 0.0f;
             float lb = w;
 #pragma unroll
             for (int o = 16; o >= (1 << TSH); o >>= 1) lb += __shfl_xor_sync(PSA_FULL, lb, o);
-            if ((lane & ((1 << TSH) - 1)) == 0) s_w[warp][j][my_tok] = w;
+            if ((lane & ((1 << TSH) - 1)) == 0) s.w[warp][j][my_tok] = w;
             if (lane == 0) {
-                s_mb[warp][j] = mb;
-                s_lb[warp][j] = lb;
-                s_la[rl] = mb + logf(lb);
+                s.mb[warp][j] = mb;
+                s.lb[warp][j] = lb;
+                s.la[rl] = mb + logf(lb);
             }
         }
         __syncthreads();
@@ -117,7 +304,7 @@ __global__ void __launch_bounds__(kPsaWarps * 32) psa_kernel(PoolView p, BatchVi
             const bool valid = lane < cnt;
             const int64_t r = cb + lane;
             double x = -INFINITY;
-            if (valid) x = omass ? omass[rpos[r]] : (double)s_la[lane];
+            if (valid) x = omass ? omass[s.tb[ci + lane] & pmask] : (double)s.la[lane];
             double mx = warp_max_d(x);
             mx = fmax(mx, acc);
             double e = valid ? exp(x - mx) : 0.0;
@@ -145,21 +332,21 @@ __global__ void __launch_bounds__(kPsaWarps * 32) psa_kernel(PoolView p, BatchVi
             mn = __shfl_sync(PSA_FULL, mn_i, f);
             const double e_f = __shfl_sync(PSA_FULL, est_i, f);
             if (lane == 0) {
-                s_commit = f + 1;
-                s_final = bal ? 1 : 0;
-                s_est = e_f;
-                s_acc = acc;
+                s.commit = f + 1;
+                s.fin = bal ? 1 : 0;
+                s.est = e_f;
+                s.acc = acc;
             }
         }
         __syncthreads();
-        const int commit = s_commit;
-        const int fin = s_final;
+        const int commit = s.commit;
+        const int fin = s.fin;
         // ---- 3. V pass over committed ranks ----
 #pragma unroll 1
         for (int j = 0; j < kBpw; ++j) {
             const int rl = warp * kBpw + j;
             if (rl >= commit) break;
-            const int32_t slot = rslot[cb + rl];
+            const int32_t slot = s.tslot[ci + rl];
             const int nt = p.ntok[slot];
             const KV* vp = kv + (int64_t)slot * slot_elems + v_off + base;
             float ob[DPL];
@@ -168,77 +355,79 @@ __global__ void __launch_bounds__(kPsaWarps * 32) psa_kernel(PoolView p, BatchVi
 #pragma unroll
             for (int t = 0; t < TOK; ++t) {
                 if (t < nt) {
-                    const float wt = s_w[warp][j][t];
+                    const float wt = s.w[warp][j][t];
                     float vr[DPL];
                     load_row<DPL>(vp + (size_t)t * d, full, lim, vr);
 #pragma unroll
                     for (int jj = 0; jj < DPL; ++jj) ob[jj] = fmaf(wt, vr[jj], ob[jj]);
                 }
             }
-            const float mbj = s_mb[warp][j];
+            const float mbj = s.mb[warp][j];
             const float mnew = fmaxf(M, mbj);
             const float a = expf(M - mnew);
             const float c = expf(mbj - mnew);
 #pragma unroll
             for (int jj = 0; jj < DPL; ++jj) O[jj] = O[jj] * a + ob[jj] * c;
-            L = L * a + s_lb[warp][j] * c;
+            L = L * a + s.lb[warp][j] * c;
             M = mnew;
         }
         if (fin) {
             if (threadIdx.x == 0) {
                 const int64_t bp = cb + commit;
                 b.bp[qi] = bp;
-                b.est[qi] = s_est;
+                b.est[qi] = s.est;
                 b.term[qi] = b.topk > 0 ? (limit < n) : (bp < n);
             }
             break;
         }
-        __syncthreads();  // s_w / s_la are rewritten by the next chunk's K pass
+        cb += cnt;
+        __syncthreads();  // s.w / s.la / s.tb are rewritten next
     }
     // ---- finalize: merge the warps' states (finalize, attention.hpp:104-110) ----
+    float* so = reinterpret_cast<float*>(s.hist);  // [kPsaWarps][256]
     if (lane == 0) {
-        s_m[warp] = M;
-        s_l[warp] = L;
+        s.m[warp] = M;
+        s.l[warp] = L;
     }
 #pragma unroll
     for (int jj = 0; jj < DPL; ++jj)
-        if (base + jj < d) s_o[warp][base + jj] = O[jj];
+        if (base + jj < d) so[warp * 256 + base + jj] = O[jj];
     __syncthreads();
     float Mt = -INFINITY;
 #pragma unroll
-    for (int w = 0; w < kPsaWarps; ++w) Mt = fmaxf(Mt, s_m[w]);
+    for (int w = 0; w < kPsaWarps; ++w) Mt = fmaxf(Mt, s.m[w]);
     float Lt = 0.0f, sc[kPsaWarps];
 #pragma unroll
     for (int w = 0; w < kPsaWarps; ++w) {
-        sc[w] = s_l[w] > 0.0f ? expf(s_m[w] - Mt) : 0.0f;
-        Lt += s_l[w] * sc[w];
+        sc[w] = s.l[w] > 0.0f ? expf(s.m[w] - Mt) : 0.0f;
+        Lt += s.l[w] * sc[w];
     }
-    for (int i = threadIdx.x; i < d; i += blockDim.x) {
+    for (int i = threadIdx.x; i < d; i += kPsaThreads) {
         float o = 0.0f;
 #pragma unroll
-        for (int w = 0; w < kPsaWarps; ++w) o += sc[w] > 0.0f ? s_o[w][i] * sc[w] : 0.0f;
+        for (int w = 0; w < kPsaWarps; ++w) o += sc[w] > 0.0f ? so[w * 256 + i] * sc[w] : 0.0f;
         b.out[(size_t)qi * d + i] = o / Lt;
     }
     if (b.tcov && threadIdx.x == 0) {
-        double tc = -1.0;
+        double tc2 = -1.0;
         if (b.audit) {
             // total mass over all n blocks (engine.cpp:88 total_log_as)
             double mx = -INFINITY;
             for (int64_t i = 0; i < n; ++i) mx = fmax(mx, omass[i]);
-            double s = 0.0;
-            for (int64_t i = 0; i < n; ++i) s += exp(omass[i] - mx);
-            tc = exp(s_acc - (mx + log(s)));
+            double sm = 0.0;
+            for (int64_t i = 0; i < n; ++i) sm += exp(omass[i] - mx);
+            tc2 = exp(s.acc - (mx + log(sm)));
         }
-        b.tcov[qi] = tc;
+        b.tcov[qi] = tc2;
     }
 }
 
 template <typename KV, int TOK>
 static void launch_psa_t(const PoolView& p, const BatchView& b, int nq, cudaStream_t st) {
     switch (dpl_for(b.d)) {
-        case 2: psa_kernel<KV, 2, TOK><<<nq, kPsaWarps * 32, 0, st>>>(p, b); break;
-        case 4: psa_kernel<KV, 4, TOK><<<nq, kPsaWarps * 32, 0, st>>>(p, b); break;
-        default: psa_kernel<KV, 8, TOK><<<nq, kPsaWarps * 32, 0, st>>>(p, b); break;
+        case 2: psa_kernel<KV, 2, TOK><<<nq, kPsaThreads, 0, st>>>(p, b); break;
+        case 4: psa_kernel<KV, 4, TOK><<<nq, kPsaThreads, 0, st>>>(p, b); break;
+        default: psa_kernel<KV, 8, TOK><<<nq, kPsaThreads, 0, st>>>(p, b); break;
     }
 }
 

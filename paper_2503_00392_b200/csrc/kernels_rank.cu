@@ -1,25 +1,106 @@
-// kernels_rank.cu — K2 scoring, K6 oracle masses, K3 ordering, GQA union, batch dispatch.
+// kernels_rank.cu — K2 criticality scoring, K6 oracle masses, GQA union, batch dispatch.
 #include <cuda_bf16.h>
 #include <float.h>
 #include <math.h>
 
 #include "common.cuh"
 #include "kernels.cuh"
-#include "synth.h"
 
 namespace psa {
 
+static int num_sms() {
+    static int n = 0;
+    if (n == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
 // =============================================================================
-// K2: criticality scoring. Grid (x: block chunks, y: unit). One warp scores one
-// metadata record against all G q-heads of the GQA group, so each record is read
-// from HBM once per kv-head. Lane owns DPL contiguous dims. fp64 products of
-// fp32 operands are exact; only the summation order differs from the
-// reference's sequential loop (~1e-16 relative).
+// K2: criticality scoring (criticality_score, reference metadata.cpp:41-72).
+// Grid (x: warps sharing a unit, y: unit). A warp scores kRecs CONSECUTIVE list
+// positions per iteration against all G q-heads of the GQA group: every
+// metadata record (mean f32 | lo kv | hi kv, 1 KB for d=128 bf16) is read from
+// HBM once per kv-head, the loads of all kRecs records are issued before any
+// math, and the G*kRecs fp64 dot products are finished with ONE reduce-scatter
+// so the keys of each head land as one contiguous 32 B store.
+//
+// Arithmetic (fp64, like the reference): products of fp32 operands are exact in
+// fp64; only the summation order differs from the reference's sequential loop
+// (~1e-16 relative). Two rewrites keep the FP64/XU pipes below the HBM rate:
+//  * no F2F: an fp32 (or bf16) bit pattern u becomes the double x*2^-896 with two
+//    integer ops ((int)u >> 3 & 0x8FFFFFFF | u << 29 — same exponent field, no
+//    rebias; exact for every finite input incl. zero/denormals) and q carries
+//    the compensating 2^896, so q'*x' == q*x exactly;
+//  * max(q*lo, q*hi) == q*c + |q|*r with c = (lo+hi)/2, r = (hi-lo)/2 (hi >= lo),
+//    so the per-head select disappears and c, r are shared by the G heads.
 // =============================================================================
 constexpr int kScoreWarps = 8;
+// records per warp iteration: 4 for the d=128 / g<=4 path, fewer where registers would spill
+template <int G, int DPL> struct RecsPer {
+    static constexpr int v = (G * DPL <= 16) ? 4 : (G * DPL <= 32) ? 2 : 1;
+};
+
+__device__ __forceinline__ double f32_scaled(uint32_t u) {  // = float(u) * 2^-896, exact
+    return __hiloint2double((int)(((uint32_t)((int32_t)u >> 3)) & 0x8FFFFFFFu), (int)(u << 29));
+}
+
+template <typename KV> struct MetaRow;
+template <> struct MetaRow<float> {
+    template <int DPL> __host__ __device__ static constexpr int words() { return DPL; }
+    template <int DPL>
+    __device__ __forceinline__ static void load(const float* p, bool full, int lim, uint32_t (&w)[DPL]) {
+        float f[DPL];
+        load_row<DPL>(p, full, lim, f);
+#pragma unroll
+        for (int j = 0; j < DPL; ++j) w[j] = __float_as_uint(f[j]);
+    }
+    template <int W>
+    __device__ __forceinline__ static double get(const uint32_t (&w)[W], int j) { return f32_scaled(w[j]); }
+};
+template <> struct MetaRow<__nv_bfloat16> {
+    template <int DPL> __host__ __device__ static constexpr int words() { return (DPL + 1) / 2; }
+    template <int DPL>
+    __device__ __forceinline__ static void load(const __nv_bfloat16* p, bool full, int lim,
+                                                uint32_t (&w)[(DPL + 1) / 2]) {
+        if (full && DPL % 8 == 0) {
+#pragma unroll
+            for (int j = 0; j < DPL / 8; ++j) {
+                const uint4 v = __ldg(reinterpret_cast<const uint4*>(p) + j);
+                w[4 * j] = v.x; w[4 * j + 1] = v.y; w[4 * j + 2] = v.z; w[4 * j + 3] = v.w;
+            }
+        } else if (full && DPL % 4 == 0) {
+#pragma unroll
+            for (int j = 0; j < DPL / 4; ++j) {
+                const uint2 v = __ldg(reinterpret_cast<const uint2*>(p) + j);
+                w[2 * j] = v.x; w[2 * j + 1] = v.y;
+            }
+        } else {
+            const unsigned short* ps = reinterpret_cast<const unsigned short*>(p);
+#pragma unroll
+            for (int j = 0; j < (DPL + 1) / 2; ++j) {
+                const uint32_t a = (2 * j < lim) ? ps[2 * j] : 0u;
+                const uint32_t c = (2 * j + 1 < lim && 2 * j + 1 < DPL) ? ps[2 * j + 1] : 0u;
+                w[j] = a | (c << 16);
+            }
+        }
+    }
+    template <int W>
+    __device__ __forceinline__ static double get(const uint32_t (&w)[W], int j) {
+        const uint32_t x = w[j >> 1];
+        return f32_scaled((j & 1) ? (x & 0xFFFF0000u) : (x << 16));
+    }
+};
 
 template <typename KV, int G, int DPL>
-__global__ void __launch_bounds__(kScoreWarps * 32) score_kernel(PoolView p, BatchView b) {
+__global__ void __launch_bounds__(kScoreWarps * 32, 2) score_kernel(PoolView p, BatchView b) {
+    constexpr int kRecs = RecsPer<G, DPL>::v;
+    constexpr int N = G * kRecs;
+    constexpr int SH = 5 - Log2<N>::v;  // lanes per value after reduce-scatter = 1 << SH
+    constexpr int WKV = MetaRow<KV>::template words<DPL>();
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const int u = blockIdx.y;
@@ -30,7 +111,7 @@ __global__ void __launch_bounds__(kScoreWarps * 32) score_kernel(PoolView p, Bat
     const int lim = d - base;
     const bool full = (d == 32 * DPL);
 
-    double qd[G][DPL];
+    double qd[G][DPL];  // q * 2^896 (compensates the scaled metadata)
 #pragma unroll
     for (int h = 0; h < G; ++h) {
         float qf[DPL];
@@ -40,37 +121,69 @@ __global__ void __launch_bounds__(kScoreWarps * 32) score_kernel(PoolView p, Bat
 #pragma unroll
             for (int j = 0; j < DPL; ++j) qf[j] = 0.0f;
 #pragma unroll
-        for (int j = 0; j < DPL; ++j) qd[h][j] = (double)qf[j];
+        for (int j = 0; j < DPL; ++j) qd[h][j] = (double)qf[j] * 0x1p896;
     }
     const int est = b.estimator;
     const double scale = b.scale;
-    const int gsh = 5 - Log2<G>::v;  // lanes per head after reduce-scatter = 1 << gsh
-    const int my_h = lane >> gsh;
+    const int my_idx = lane >> SH;  // value index this lane owns after the reduce-scatter
+    const int my_h = my_idx / kRecs, my_j = my_idx % kRecs;
+    const bool writer = (lane & ((1 << SH) - 1)) == 0 && my_h < b.g;
+    uint64_t* keys = b.keys + off * b.g + (int64_t)my_h * n;
 
-    for (int64_t pos = (int64_t)blockIdx.x * kScoreWarps + warp; pos < n; pos += (int64_t)gridDim.x * kScoreWarps) {
-        const int32_t slot = b.slots[off + pos];
-        const char* rec = p.meta + (int64_t)slot * p.meta_bytes;
-        float mf[DPL], lf[DPL], hf[DPL];
-        load_row<DPL>(reinterpret_cast<const float*>(rec) + base, full, lim, mf);
-        load_row<DPL>(reinterpret_cast<const KV*>(rec + (size_t)d * 4) + base, full, lim, lf);
-        load_row<DPL>(reinterpret_cast<const KV*>(rec + (size_t)d * 4 + (size_t)d * sizeof(KV)) + base, full, lim, hf);
-        double acc[G];
+    const int64_t ngroups = (n + kRecs - 1) / kRecs;
+    const int64_t nwarps = (int64_t)gridDim.x * kScoreWarps;
+    for (int64_t grp = (int64_t)blockIdx.x * kScoreWarps + warp; grp < ngroups; grp += nwarps) {
+        const int64_t p0 = grp * kRecs;
+        const int32_t my_slot = (lane < kRecs && p0 + lane < n) ? b.slots[off + p0 + lane] : -1;
+        uint32_t mw[kRecs][DPL], lw[kRecs][WKV], hw[kRecs][WKV];
 #pragma unroll
-        for (int h = 0; h < G; ++h) acc[h] = 0.0;
+        for (int j = 0; j < kRecs; ++j) {
+            const int32_t slot = __shfl_sync(PSA_FULL, my_slot, j);
+            if (slot >= 0) {
+                const char* rec = p.meta + (int64_t)slot * p.meta_bytes;
+                MetaRow<float>::load<DPL>(reinterpret_cast<const float*>(rec) + base, full, lim, mw[j]);
+                MetaRow<KV>::template load<DPL>(reinterpret_cast<const KV*>(rec + (size_t)d * 4) + base, full, lim,
+                                                lw[j]);
+                MetaRow<KV>::template load<DPL>(
+                    reinterpret_cast<const KV*>(rec + (size_t)d * 4 + (size_t)d * sizeof(KV)) + base, full, lim, hw[j]);
+            } else {
 #pragma unroll
-        for (int j = 0; j < DPL; ++j) {
-            const double md = (double)mf[j], ld = (double)lf[j], hd = (double)hf[j];
+                for (int jj = 0; jj < DPL; ++jj) mw[j][jj] = 0u;
 #pragma unroll
-            for (int h = 0; h < G; ++h) {
-                const double qv = qd[h][j];
-                if (est != 1) acc[h] = fma(qv, md, acc[h]);                 // mean_score
-                if (est != 0) acc[h] = fma(qv, qv >= 0.0 ? hd : ld, acc[h]); // max(q*lo, q*hi)
+                for (int jj = 0; jj < WKV; ++jj) lw[j][jj] = hw[j][jj] = 0u;
             }
         }
-        const double tot = reduce_scatter_d<G>(acc, lane);
-        if ((lane & ((1 << gsh) - 1)) == 0 && my_h < b.g) {
+        double acc[N];
+#pragma unroll
+        for (int i = 0; i < N; ++i) acc[i] = 0.0;
+#pragma unroll
+        for (int j = 0; j < kRecs; ++j) {
+#pragma unroll
+            for (int jj = 0; jj < DPL; ++jj) {
+                const double m = MetaRow<float>::get(mw[j], jj);
+                const double lo = MetaRow<KV>::get(lw[j], jj);
+                const double hi = MetaRow<KV>::get(hw[j], jj);
+                double A, B = 0.0;
+                if (est == 0) {
+                    A = m;  // mean_score
+                } else {
+                    const double c2 = lo + hi;          // exact
+                    B = (hi - lo) * 0.5;                // r, exact
+                    A = est == 2 ? fma(0.5, c2, m) : c2 * 0.5;  // m + c  |  c
+                }
+#pragma unroll
+                for (int h = 0; h < G; ++h) {
+                    const double qv = qd[h][jj];
+                    double a = fma(qv, A, acc[h * kRecs + j]);
+                    if (est != 0) a = fma(fabs(qv), B, a);  // + |q| r  ==  max(q lo, q hi) - q c
+                    acc[h * kRecs + j] = a;
+                }
+            }
+        }
+        const double tot = reduce_scatter_d<N>(acc, lane);
+        if (writer && p0 + my_j < n) {
             const double s = est == 2 ? 0.5 * (tot * scale) : tot * scale;
-            b.keys[off * b.g + (int64_t)my_h * n + pos] = make_key(s, (uint32_t)pos, b.pos_bits);
+            keys[p0 + my_j] = make_key(s, (uint32_t)(p0 + my_j), b.pos_bits);
         }
     }
 }
@@ -78,6 +191,7 @@ __global__ void __launch_bounds__(kScoreWarps * 32) score_kernel(PoolView p, Bat
 // =============================================================================
 // K6: fp64 block masses log(sum_t exp(q.k_t*scale)) for Oracle ranking and the
 // coverage audit (reference engine.cpp:64-72 computes these in plan_blocks).
+// Test/audit mode only; not on the benchmarked path.
 // =============================================================================
 template <typename KV, int DPL>
 __global__ void __launch_bounds__(kScoreWarps * 32) oracle_mass_kernel(PoolView p, BatchView b) {
@@ -118,58 +232,6 @@ __global__ void __launch_bounds__(kScoreWarps * 32) oracle_mass_kernel(PoolView 
                 if (b.rank_oracle) b.keys[idx] = make_key(la, (uint32_t)pos, b.pos_bits);
             }
         }
-    }
-}
-
-// =============================================================================
-// K3: ordering. One CTA per (unit, head): all-ascending bitonic network (the
-// "flip" formulation, every compare-exchange puts the min at the lower index),
-// so indices >= n behave as +inf and need no padding. Keys are unique (they
-// carry the position), so the result is THE (score desc, id asc) order.
-// Emits rank-ordered list positions and the matching pool slots.
-// =============================================================================
-constexpr int kSortThreads = 1024;
-constexpr int kSmemSortMax = 16384;  // keys per head sorted in shared memory (128 KB)
-
-__device__ __forceinline__ void bitonic_ascending(uint64_t* a, int64_t n, int64_t n2) {
-    for (int64_t k = 2; k <= n2; k <<= 1) {
-        for (int64_t j = k >> 1; j > 0; j >>= 1) {
-            for (int64_t i = threadIdx.x; i < (n2 >> 1); i += blockDim.x) {
-                const int64_t lo = ((i / j) * 2 * j) + (i % j);
-                const int64_t hi = (j == (k >> 1)) ? (lo ^ (k - 1)) : (lo + j);
-                if (hi < n) {
-                    const uint64_t x = a[lo], y = a[hi];
-                    if (x > y) {
-                        a[lo] = y;
-                        a[hi] = x;
-                    }
-                }
-            }
-            __syncthreads();
-        }
-    }
-}
-
-__global__ void __launch_bounds__(kSortThreads) sort_kernel(BatchView b) {
-    extern __shared__ uint64_t skeys[];
-    const int qi = blockIdx.x;
-    const int u = qi / b.g, h = qi % b.g;
-    const int64_t off = b.list_off[u];
-    const int64_t n = b.list_off[u + 1] - off;
-    const int64_t hb = off * b.g + (int64_t)h * n;
-    int64_t n2 = 1;
-    while (n2 < n) n2 <<= 1;
-    const bool in_smem = b.max_n <= kSmemSortMax;  // smem sized for max_n by the launcher
-    uint64_t* a = in_smem ? skeys : (b.keys + hb);
-    if (in_smem)
-        for (int64_t i = threadIdx.x; i < n; i += blockDim.x) a[i] = b.keys[hb + i];
-    __syncthreads();
-    bitonic_ascending(a, n, n2);
-    const uint64_t mask = (b.pos_bits >= 64) ? ~0ull : ((1ull << b.pos_bits) - 1ull);
-    for (int64_t r = threadIdx.x; r < n; r += blockDim.x) {
-        const int32_t pos = (int32_t)(a[r] & mask);
-        b.rpos[hb + r] = pos;
-        b.rslot[hb + r] = b.slots[off + pos];
     }
 }
 
@@ -239,29 +301,31 @@ static void launch_oracle(const PoolView& p, const BatchView& b, dim3 grid, cuda
 }
 
 int launch_batch(const PoolView& p, const BatchView& b, cudaStream_t st, cudaEvent_t* marks) {
-    // marks (optional, 5 events): start | oracle | score | order | progressive
+    // marks (optional, 5 events): start | oracle | score | order | progressive. Ordering is
+    // fused into the progressive kernel (lazy tranche selection), so the "order" stage is empty.
     int launches = 0;
     if (marks) cudaEventRecord(marks[0], st);
-    const int64_t chunks = (b.max_n + kScoreWarps - 1) / kScoreWarps;
-    dim3 grid((unsigned)(chunks < 65535 ? (chunks > 0 ? chunks : 1) : 65535), (unsigned)b.n_units);
     if (b.has_oracle) {
+        const int64_t chunks = (b.max_n + kScoreWarps - 1) / kScoreWarps;
+        dim3 grid((unsigned)(chunks < 65535 ? (chunks > 0 ? chunks : 1) : 65535), (unsigned)b.n_units);
         if (p.dtype == 0) launch_oracle<float>(p, b, grid, st);
         else launch_oracle<__nv_bfloat16>(p, b, grid, st);
         ++launches;
     }
     if (marks) cudaEventRecord(marks[1], st);
     if (!b.rank_oracle) {
+        // enough CTAs for ~2 waves of 2 CTAs/SM, never more warps than record groups
+        const int64_t groups = (b.max_n + 3) / 4;
+        int64_t gx = (2LL * 2 * num_sms() + b.n_units - 1) / b.n_units;
+        const int64_t gx_max = (groups + kScoreWarps - 1) / kScoreWarps;
+        if (gx > gx_max) gx = gx_max;
+        if (gx < 1) gx = 1;
+        dim3 grid((unsigned)gx, (unsigned)b.n_units);
         if (p.dtype == 0) launch_score<float>(p, b, grid, st);
         else launch_score<__nv_bfloat16>(p, b, grid, st);
         ++launches;
     }
     if (marks) cudaEventRecord(marks[2], st);
-    const int nq = b.n_units * b.g;
-    const size_t smem = (size_t)(b.max_n <= kSmemSortMax ? b.max_n : 0) * sizeof(uint64_t);
-    if (smem > 48 * 1024)
-        cudaFuncSetAttribute(sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    sort_kernel<<<nq, kSortThreads, smem, st>>>(b);
-    ++launches;
     if (marks) cudaEventRecord(marks[3], st);
     launch_psa(p, b, st);
     ++launches;

@@ -435,8 +435,8 @@ void TieredBlockStore::run_device(const detail::DeviceQueryBatch& qb, detail::De
     char* hout = static_cast<char*>(dev_->h_out.get(out_total + om_b + 256));
     check_cuda(cudaMemcpyAsync(hout, dout, out_total, cudaMemcpyDeviceToHost, dev_->stream), "D2H");
     if (has_oracle) {
-        // workspace layout: keys | rpos | rslot | omass (psattn_batch_workspace_bytes)
-        const size_t om_off = align256(static_cast<size_t>(hbt) * 8) + 2 * align256(static_cast<size_t>(hbt) * 4);
+        // workspace layout: keys | rpos | omass (psattn_batch_workspace_bytes)
+        const size_t om_off = align256(static_cast<size_t>(hbt) * 8) + align256(static_cast<size_t>(hbt) * 4);
         check_cuda(cudaMemcpyAsync(hout + out_total, static_cast<char*>(ws) + om_off, om_b, cudaMemcpyDeviceToHost,
                                    dev_->stream),
                    "D2H");
