@@ -48,7 +48,10 @@ typedef struct {
 } psattn_pool_desc;
 
 /* Raw device layout, for callers that write K/V themselves (e.g. a decode
- * step's KV append) and then call psattn_pool_build_metadata. */
+ * step's KV append) and then call psattn_pool_build_metadata. Rows past a
+ * slot's ntok must hold finite values (the pool is zero-initialised and every
+ * put writes zero padding): the progressive kernel loads all rows of a slot
+ * and masks by ntok. */
 typedef struct {
     void* kv;            /* [n_slots][2][block_tokens][dim] kv_dtype: K rows then V rows */
     void* meta;          /* [n_slots] records of {mean[dim] f32, lo[dim] kv, hi[dim] kv} */

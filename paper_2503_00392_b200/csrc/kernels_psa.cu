@@ -46,6 +46,7 @@ template <int TOK>
 struct PsaSmem {
     uint64_t tb[kTCap];       // sorted keys of the current tranche
     int32_t tslot[kTCap];     // their pool slots
+    uint8_t tntok[kTCap];     // their valid token counts
     uint32_t hist[kBins];     // bucket-select histogram; reused for the final merge
     float w[kPsaWarps][kBpw][TOK];
     float mb[kPsaWarps][kBpw], lb[kPsaWarps][kBpw];
@@ -97,6 +98,23 @@ __device__ __forceinline__ void bitonic_smem(uint64_t* a, int n) {
     }
 }
 
+// Calls f(key) for every key of the head; 8 independent loads in flight per thread.
+template <typename F>
+__device__ __forceinline__ void scan_keys(const uint64_t* __restrict__ keys, int64_t n, F&& f) {
+    constexpr int U = 8;
+    for (int64_t i0 = threadIdx.x; i0 < n; i0 += (int64_t)U * kPsaThreads) {
+        uint64_t k[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t i = i0 + (int64_t)u * kPsaThreads;
+            k[u] = i < n ? __ldg(reinterpret_cast<const unsigned long long*>(keys) + i) : ~0ull;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (i0 + (int64_t)u * kPsaThreads < n) f(k[u]);
+    }
+}
+
 // Next tranche: the C (<= kTCap, ~target) smallest keys greater than `last` (all keys if first).
 template <int TOK>
 __device__ int select_tranche(PsaSmem<TOK>& s, const uint64_t* __restrict__ keys, int64_t n, uint64_t last,
@@ -104,14 +122,13 @@ __device__ int select_tranche(PsaSmem<TOK>& s, const uint64_t* __restrict__ keys
     const int tid = threadIdx.x, lane = tid & 31;
     unsigned long long lmin = ~0ull, lmax = 0;
     unsigned lcnt = 0;
-    for (int64_t i = tid; i < n; i += kPsaThreads) {
-        const unsigned long long k = keys[i];
+    scan_keys(keys, n, [&](uint64_t k) {
         if (first || k > last) {
             lmin = k < lmin ? k : lmin;
             lmax = k > lmax ? k : lmax;
             ++lcnt;
         }
-    }
+    });
     if (tid == 0) {
         s.red_min = ~0ull;
         s.red_max = 0;
@@ -140,10 +157,9 @@ __device__ int select_tranche(PsaSmem<TOK>& s, const uint64_t* __restrict__ keys
             const int sh = bits > 11 ? bits - 11 : 0;
             for (int i = tid; i < kBins; i += kPsaThreads) s.hist[i] = 0;
             __syncthreads();
-            for (int64_t i = tid; i < n; i += kPsaThreads) {
-                const uint64_t k = keys[i];
+            scan_keys(keys, n, [&](uint64_t k) {
                 if ((first || k > last) && k >= lo && k <= hi) atomicAdd(&s.hist[(k - lo) >> sh], 1u);
-            }
+            });
             __syncthreads();
             // first bin b with cum(b) >= need: each thread owns 8 consecutive bins
             constexpr int per = kBins / kPsaThreads;
@@ -194,20 +210,26 @@ __device__ int select_tranche(PsaSmem<TOK>& s, const uint64_t* __restrict__ keys
             __syncthreads();
         }
     }
-    for (int64_t i = tid; i < n; i += kPsaThreads) {
-        const uint64_t k = keys[i];
-        if ((first || k > last) && k <= tau) {
-            const unsigned idx = atomicAdd(&s.gcount, 1u);
+    // gather the survivors (warp-aggregated slot reservation)
+    scan_keys(keys, n, [&](uint64_t k) {
+        const bool take = (first || k > last) && k <= tau;
+        const unsigned m = __ballot_sync(__activemask(), take);
+        if (take) {
+            const int leader = __ffs(m) - 1;
+            unsigned basei = 0;
+            if (lane == leader) basei = atomicAdd(&s.gcount, (unsigned)__popc(m));
+            basei = __shfl_sync(m, basei, leader);
+            const unsigned idx = basei + __popc(m & ((1u << lane) - 1u));
             if (idx < (unsigned)kTCap) s.tb[idx] = k;
         }
-    }
+    });
     __syncthreads();
     const int C = (int)min(s.gcount, (unsigned)kTCap);
     bitonic_smem(s.tb, C);
     return C;
 }
 
-template <typename KV, int DPL, int TOK>
+template <typename KV, int DPL, int TOK, bool FULL>
 __global__ void __launch_bounds__(kPsaThreads, 3) psa_kernel(PoolView p, BatchView b) {
     __shared__ PsaSmem<TOK> s;
     const int lane = threadIdx.x & 31;
@@ -223,7 +245,7 @@ __global__ void __launch_bounds__(kPsaThreads, 3) psa_kernel(PoolView p, BatchVi
     const int d = b.d;
     const int base = lane * DPL;
     const int lim = d - base;
-    const bool full = (d == 32 * DPL);
+    constexpr bool full = FULL;  // d == 32*DPL: vector loads, no bounds
     const float fscale = (float)b.scale;  // engine.cpp:113
     constexpr int TSH = 5 - Log2<TOK>::v;  // lanes per token after reduce-scatter = 1 << TSH
     const int my_tok = lane >> TSH;
@@ -241,6 +263,7 @@ __global__ void __launch_bounds__(kPsaThreads, 3) psa_kernel(PoolView p, BatchVi
     const KV* kv = reinterpret_cast<const KV*>(p.kv);
     const int64_t slot_elems = p.slot_bytes / (int64_t)sizeof(KV);
     const int64_t v_off = (int64_t)p.T * d;
+    const int T = p.T;
 
     int64_t tr0 = 0;  // global rank of s.tb[0]
     int tc = 0;       // ranks in the current tranche
@@ -253,7 +276,9 @@ __global__ void __launch_bounds__(kPsaThreads, 3) psa_kernel(PoolView p, BatchVi
             for (int i = threadIdx.x; i < tc; i += kPsaThreads) {
                 const int32_t pos = (int32_t)(s.tb[i] & pmask);
                 b.rpos[hb + tr0 + i] = pos;
-                s.tslot[i] = b.slots[off + pos];
+                const int32_t sl = b.slots[off + pos];
+                s.tslot[i] = sl;
+                s.tntok[i] = (uint8_t)p.ntok[sl];
             }
             __syncthreads();
         }
@@ -267,18 +292,16 @@ __global__ void __launch_bounds__(kPsaThreads, 3) psa_kernel(PoolView p, BatchVi
             const int rl = warp * kBpw + j;
             if (rl >= cnt) break;
             const int32_t slot = s.tslot[ci + rl];
-            const int nt = p.ntok[slot];
+            const int nt = s.tntok[ci + rl];
             const KV* kp = kv + (int64_t)slot * slot_elems + base;
             float part[TOK];
 #pragma unroll
             for (int t = 0; t < TOK; ++t) {
+                // Branch-free: rows in [ntok, T) are zero-filled in the pool and rows >= T
+                // (TOK > T) re-read row T-1, so all TOK loads issue before the first use;
+                // tokens >= ntok are masked below.
                 float kr[DPL];
-                if (t < nt) {
-                    load_row<DPL>(kp + (size_t)t * d, full, lim, kr);
-                } else {
-#pragma unroll
-                    for (int jj = 0; jj < DPL; ++jj) kr[jj] = 0.0f;
-                }
+                load_row<DPL>(kp + (size_t)(t < T ? t : T - 1) * d, full, lim, kr);
                 float a = 0.0f;
 #pragma unroll
                 for (int jj = 0; jj < DPL; ++jj) a = fmaf(q[jj], kr[jj], a);
@@ -347,20 +370,18 @@ __global__ void __launch_bounds__(kPsaThreads, 3) psa_kernel(PoolView p, BatchVi
             const int rl = warp * kBpw + j;
             if (rl >= commit) break;
             const int32_t slot = s.tslot[ci + rl];
-            const int nt = p.ntok[slot];
+            const int nt = s.tntok[ci + rl];
             const KV* vp = kv + (int64_t)slot * slot_elems + v_off + base;
             float ob[DPL];
 #pragma unroll
             for (int jj = 0; jj < DPL; ++jj) ob[jj] = 0.0f;
 #pragma unroll
             for (int t = 0; t < TOK; ++t) {
-                if (t < nt) {
-                    const float wt = s.w[warp][j][t];
-                    float vr[DPL];
-                    load_row<DPL>(vp + (size_t)t * d, full, lim, vr);
+                const float wt = s.w[warp][j][t];  // 0 for t >= ntok (and hence for t >= T)
+                float vr[DPL];
+                load_row<DPL>(vp + (size_t)(t < T ? t : T - 1) * d, full, lim, vr);
 #pragma unroll
-                    for (int jj = 0; jj < DPL; ++jj) ob[jj] = fmaf(wt, vr[jj], ob[jj]);
-                }
+                for (int jj = 0; jj < DPL; ++jj) ob[jj] = fmaf(wt, vr[jj], ob[jj]);
             }
             const float mbj = s.mb[warp][j];
             const float mnew = fmaxf(M, mbj);
@@ -424,10 +445,13 @@ __global__ void __launch_bounds__(kPsaThreads, 3) psa_kernel(PoolView p, BatchVi
 
 template <typename KV, int TOK>
 static void launch_psa_t(const PoolView& p, const BatchView& b, int nq, cudaStream_t st) {
-    switch (dpl_for(b.d)) {
-        case 2: psa_kernel<KV, 2, TOK><<<nq, kPsaThreads, 0, st>>>(p, b); break;
-        case 4: psa_kernel<KV, 4, TOK><<<nq, kPsaThreads, 0, st>>>(p, b); break;
-        default: psa_kernel<KV, 8, TOK><<<nq, kPsaThreads, 0, st>>>(p, b); break;
+    switch (dpl_for(b.d)) {  // d=64 and d=128 are always "full"; other d use the masked 8-dim path
+        case 2: psa_kernel<KV, 2, TOK, true><<<nq, kPsaThreads, 0, st>>>(p, b); break;
+        case 4: psa_kernel<KV, 4, TOK, true><<<nq, kPsaThreads, 0, st>>>(p, b); break;
+        default:
+            if (b.d == 256) psa_kernel<KV, 8, TOK, true><<<nq, kPsaThreads, 0, st>>>(p, b);
+            else psa_kernel<KV, 8, TOK, false><<<nq, kPsaThreads, 0, st>>>(p, b);
+            break;
     }
 }
 

@@ -95,7 +95,7 @@ template <> struct MetaRow<__nv_bfloat16> {
     }
 };
 
-template <typename KV, int G, int DPL>
+template <typename KV, int G, int DPL, bool FULL>
 __global__ void __launch_bounds__(kScoreWarps * 32, 2) score_kernel(PoolView p, BatchView b) {
     constexpr int kRecs = RecsPer<G, DPL>::v;
     constexpr int N = G * kRecs;
@@ -109,7 +109,7 @@ __global__ void __launch_bounds__(kScoreWarps * 32, 2) score_kernel(PoolView p, 
     const int d = b.d;
     const int base = lane * DPL;
     const int lim = d - base;
-    const bool full = (d == 32 * DPL);
+    constexpr bool full = FULL;  // d == 32*DPL: vector loads, no bounds
 
     double qd[G][DPL];  // q * 2^896 (compensates the scaled metadata)
 #pragma unroll
@@ -132,26 +132,27 @@ __global__ void __launch_bounds__(kScoreWarps * 32, 2) score_kernel(PoolView p, 
 
     const int64_t ngroups = (n + kRecs - 1) / kRecs;
     const int64_t nwarps = (int64_t)gridDim.x * kScoreWarps;
-    for (int64_t grp = (int64_t)blockIdx.x * kScoreWarps + warp; grp < ngroups; grp += nwarps) {
+    int64_t grp = (int64_t)blockIdx.x * kScoreWarps + warp;
+    // slot ids of the next group are fetched one iteration ahead (lanes 0..kRecs-1)
+    int32_t nxt = (lane < kRecs && grp * kRecs + lane < n) ? b.slots[off + grp * kRecs + lane] : -1;
+    for (; grp < ngroups; grp += nwarps) {
         const int64_t p0 = grp * kRecs;
-        const int32_t my_slot = (lane < kRecs && p0 + lane < n) ? b.slots[off + p0 + lane] : -1;
+        const int32_t my_slot = nxt;
+        const int64_t pn = (grp + nwarps) * kRecs;
+        nxt = (lane < kRecs && pn + lane < n) ? b.slots[off + pn + lane] : -1;
+        const int32_t slot0 = __shfl_sync(PSA_FULL, my_slot, 0);  // p0 < n: always valid
         uint32_t mw[kRecs][DPL], lw[kRecs][WKV], hw[kRecs][WKV];
+        // Branch-free: a record past the end re-reads record 0 (its key is never written),
+        // so all 3*kRecs loads issue back to back before the first use.
 #pragma unroll
         for (int j = 0; j < kRecs; ++j) {
-            const int32_t slot = __shfl_sync(PSA_FULL, my_slot, j);
-            if (slot >= 0) {
-                const char* rec = p.meta + (int64_t)slot * p.meta_bytes;
-                MetaRow<float>::load<DPL>(reinterpret_cast<const float*>(rec) + base, full, lim, mw[j]);
-                MetaRow<KV>::template load<DPL>(reinterpret_cast<const KV*>(rec + (size_t)d * 4) + base, full, lim,
-                                                lw[j]);
-                MetaRow<KV>::template load<DPL>(
-                    reinterpret_cast<const KV*>(rec + (size_t)d * 4 + (size_t)d * sizeof(KV)) + base, full, lim, hw[j]);
-            } else {
-#pragma unroll
-                for (int jj = 0; jj < DPL; ++jj) mw[j][jj] = 0u;
-#pragma unroll
-                for (int jj = 0; jj < WKV; ++jj) lw[j][jj] = hw[j][jj] = 0u;
-            }
+            int32_t slot = __shfl_sync(PSA_FULL, my_slot, j);
+            slot = slot >= 0 ? slot : slot0;
+            const char* rec = p.meta + (int64_t)slot * p.meta_bytes;
+            MetaRow<float>::load<DPL>(reinterpret_cast<const float*>(rec) + base, full, lim, mw[j]);
+            MetaRow<KV>::template load<DPL>(reinterpret_cast<const KV*>(rec + (size_t)d * 4) + base, full, lim, lw[j]);
+            MetaRow<KV>::template load<DPL>(reinterpret_cast<const KV*>(rec + (size_t)d * 4 + (size_t)d * sizeof(KV)) +
+                                                base, full, lim, hw[j]);
         }
         double acc[N];
 #pragma unroll
@@ -278,10 +279,13 @@ cudaError_t launch_union(const BatchView& b, int64_t* out, cudaStream_t st) {
 // =============================================================================
 template <typename KV, int G>
 static void launch_score_g(const PoolView& p, const BatchView& b, dim3 grid, cudaStream_t st) {
-    switch (dpl_for(b.d)) {
-        case 2: score_kernel<KV, G, 2><<<grid, kScoreWarps * 32, 0, st>>>(p, b); break;
-        case 4: score_kernel<KV, G, 4><<<grid, kScoreWarps * 32, 0, st>>>(p, b); break;
-        default: score_kernel<KV, G, 8><<<grid, kScoreWarps * 32, 0, st>>>(p, b); break;
+    switch (dpl_for(b.d)) {  // d=64 and d=128 are always "full"; other d use the masked 8-dim path
+        case 2: score_kernel<KV, G, 2, true><<<grid, kScoreWarps * 32, 0, st>>>(p, b); break;
+        case 4: score_kernel<KV, G, 4, true><<<grid, kScoreWarps * 32, 0, st>>>(p, b); break;
+        default:
+            if (b.d == 256) score_kernel<KV, G, 8, true><<<grid, kScoreWarps * 32, 0, st>>>(p, b);
+            else score_kernel<KV, G, 8, false><<<grid, kScoreWarps * 32, 0, st>>>(p, b);
+            break;
     }
 }
 
