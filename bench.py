@@ -35,7 +35,7 @@ UNIT = "queries/s"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--dist", default="planted", choices=["planted", "iso"])
@@ -168,7 +168,7 @@ class ClockSampler:
         try:
             self.f = open(self.path, "w")
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"], stdout=self.f,
+                                          "--format=csv,noheader,nounits", "-lms", "50"], stdout=self.f,
                                          stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
@@ -217,7 +217,7 @@ def ncu_traffic(stage):
 def run_ours(args):
     import torch
     import torch.distributed as dist
-    from paper_2503_00392_b200 import batch, capi
+    from paper_2503_00392_b200 import batch, capi, shard
 
     ws, rank, local = dist_env()
     if ws > 1:
@@ -231,7 +231,9 @@ def run_ours(args):
     nq = U * g
     # ---- unified pool: every (request, layer, kv-head) list is n consecutive slots ----
     pool = batch.DevicePool(args.dim, args.block, capi.PSATTN_KV_BF16, U * n)
-    unit_ids = np.arange(U, dtype=np.int64) + rank * U  # distinct requests per rank (weak scaling)
+    # weak scaling: requests_per_gpu x N requests in total, each rank owns its own (no collective)
+    unit_ids = shard.unit_ids(shard.shard_requests(args.requests * ws, ws, rank), args.layers, args.hkv)
+    assert unit_ids.size == U
     t0 = time.time()
     pool.fill_synthetic(p, unit_ids, np.arange(U, dtype=np.int64) * n, np.full(U, args.ctx, np.int64))
     torch.cuda.synchronize()
@@ -252,13 +254,14 @@ def run_ours(args):
             dist.barrier()
 
     # ---- device-timed region (inputs resident) ----
+    # nvidia-smi samples every 50 ms from the start of the warm-up through the timed region
+    clocks = ClockSampler(local)
+    clocks.start()
     for _ in range(args.warmup):
         launches_per_step = run.run()
     torch.cuda.synchronize()
     barrier()
     torch.cuda.synchronize()
-    clocks = ClockSampler(local)
-    clocks.start()
     capi.lib.psattn_profile_read(None, None, 1)
     capi.lib.psattn_profile_enable(1)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -274,10 +277,7 @@ def run_ours(args):
     stage_ms = np.zeros(4, np.float64)
     stage_n = np.zeros(4, np.int64)
     capi.lib.psattn_profile_read(stage_ms.ctypes.data, stage_n.ctypes.data, 1)
-    if ws > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = shard.max_over_ranks(ms, dev)
     ms_per_step = ms / args.steps
     value = nq * ws * args.steps / (ms / 1e3)
 
@@ -330,10 +330,7 @@ def run_ours(args):
         e2e_step()
         stream.synchronize()  # the caller consumes each step's outputs on the host
     e2e_s = time.perf_counter() - t0
-    if ws > 1:
-        t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
+    e2e_s = shard.max_over_ranks(e2e_s, dev)
     e2e_val = nq * ws * args.steps / e2e_s
 
     # ---- CPU baseline (rank 0, N=1 only) ----

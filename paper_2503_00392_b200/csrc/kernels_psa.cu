@@ -83,7 +83,7 @@ __device__ __forceinline__ void bitonic_smem(uint64_t* a, int n) {
     for (int k = 2; k <= n2; k <<= 1) {
         for (int j = k >> 1; j > 0; j >>= 1) {
             for (int i = threadIdx.x; i < (n2 >> 1); i += blockDim.x) {
-                const int lo = ((i / j) * 2 * j) + (i % j);
+                const int lo = ((i & ~(j - 1)) << 1) | (i & (j - 1));  // j is a power of two
                 const int hi = (j == (k >> 1)) ? (lo ^ (k - 1)) : (lo + j);
                 if (hi < n) {
                     const uint64_t x = a[lo], y = a[hi];
@@ -242,7 +242,7 @@ __global__ void __launch_bounds__(kPsaThreads, 3) psa_kernel(PoolView p, BatchVi
     const uint64_t* keys = b.keys + hb;
     const int64_t limit = b.topk > 0 ? (b.topk < n ? b.topk : n) : n;
     const double eps = b.topk > 0 ? 1.0 : b.eps;
-    const int d = b.d;
+    const int d = FULL ? 32 * DPL : b.d;  // compile-time on the full-row paths: row offsets fold to immediates
     const int base = lane * DPL;
     const int lim = d - base;
     constexpr bool full = FULL;  // d == 32*DPL: vector loads, no bounds
@@ -294,18 +294,30 @@ __global__ void __launch_bounds__(kPsaThreads, 3) psa_kernel(PoolView p, BatchVi
             const int32_t slot = s.tslot[ci + rl];
             const int nt = s.tntok[ci + rl];
             const KV* kp = kv + (int64_t)slot * slot_elems + base;
+            // Branch-free: rows in [ntok, T) are zero-filled in the pool and rows >= T
+            // (TOK > T) re-read row T-1, so all TOK loads issue before the first use;
+            // tokens >= ntok are masked below.
             float part[TOK];
+            if (T == TOK) {
 #pragma unroll
-            for (int t = 0; t < TOK; ++t) {
-                // Branch-free: rows in [ntok, T) are zero-filled in the pool and rows >= T
-                // (TOK > T) re-read row T-1, so all TOK loads issue before the first use;
-                // tokens >= ntok are masked below.
-                float kr[DPL];
-                load_row<DPL>(kp + (size_t)(t < T ? t : T - 1) * d, full, lim, kr);
-                float a = 0.0f;
+                for (int t = 0; t < TOK; ++t) {
+                    float kr[DPL];
+                    load_row<DPL>(kp + t * d, full, lim, kr);
+                    float a = 0.0f;
 #pragma unroll
-                for (int jj = 0; jj < DPL; ++jj) a = fmaf(q[jj], kr[jj], a);
-                part[t] = a;
+                    for (int jj = 0; jj < DPL; ++jj) a = fmaf(q[jj], kr[jj], a);
+                    part[t] = a;
+                }
+            } else {
+#pragma unroll
+                for (int t = 0; t < TOK; ++t) {
+                    float kr[DPL];
+                    load_row<DPL>(kp + (size_t)(t < T ? t : T - 1) * d, full, lim, kr);
+                    float a = 0.0f;
+#pragma unroll
+                    for (int jj = 0; jj < DPL; ++jj) a = fmaf(q[jj], kr[jj], a);
+                    part[t] = a;
+                }
             }
             float sc = reduce_scatter<TOK>(part, lane) * fscale;
             sc = my_tok < nt ? sc : -INFINITY;
@@ -375,13 +387,24 @@ __global__ void __launch_bounds__(kPsaThreads, 3) psa_kernel(PoolView p, BatchVi
             float ob[DPL];
 #pragma unroll
             for (int jj = 0; jj < DPL; ++jj) ob[jj] = 0.0f;
+            if (T == TOK) {
 #pragma unroll
-            for (int t = 0; t < TOK; ++t) {
-                const float wt = s.w[warp][j][t];  // 0 for t >= ntok (and hence for t >= T)
-                float vr[DPL];
-                load_row<DPL>(vp + (size_t)(t < T ? t : T - 1) * d, full, lim, vr);
+                for (int t = 0; t < TOK; ++t) {
+                    const float wt = s.w[warp][j][t];  // 0 for t >= ntok
+                    float vr[DPL];
+                    load_row<DPL>(vp + t * d, full, lim, vr);
 #pragma unroll
-                for (int jj = 0; jj < DPL; ++jj) ob[jj] = fmaf(wt, vr[jj], ob[jj]);
+                    for (int jj = 0; jj < DPL; ++jj) ob[jj] = fmaf(wt, vr[jj], ob[jj]);
+                }
+            } else {
+#pragma unroll
+                for (int t = 0; t < TOK; ++t) {
+                    const float wt = s.w[warp][j][t];  // 0 for t >= ntok (and hence for t >= T)
+                    float vr[DPL];
+                    load_row<DPL>(vp + (size_t)(t < T ? t : T - 1) * d, full, lim, vr);
+#pragma unroll
+                    for (int jj = 0; jj < DPL; ++jj) ob[jj] = fmaf(wt, vr[jj], ob[jj]);
+                }
             }
             const float mbj = s.mb[warp][j];
             const float mnew = fmaxf(M, mbj);

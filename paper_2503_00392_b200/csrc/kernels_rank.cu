@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(kScoreWarps * 32, 2) score_kernel(PoolView p, 
     const int u = blockIdx.y;
     const int64_t off = b.list_off[u];
     const int64_t n = b.list_off[u + 1] - off;
-    const int d = b.d;
+    const int d = FULL ? 32 * DPL : b.d;  // compile-time on the full-row paths
     const int base = lane * DPL;
     const int lim = d - base;
     constexpr bool full = FULL;  // d == 32*DPL: vector loads, no bounds
