@@ -189,6 +189,158 @@ __global__ void __launch_bounds__(kScoreWarps * 32, 2) score_kernel(PoolView p, 
     }
 }
 
+// -----------------------------------------------------------------------------
+// K2 for d = 128 (the production shape): same arithmetic, but the metadata
+// records are staged through shared memory with 1-D TMA bulk copies
+// (cp.async.bulk + mbarrier transaction counts). Each warp owns a ring of S
+// stages of kRecs records; lanes 0..kRecs-1 each issue one record copy (1 KB bf16
+// / 1.5 KB fp32, L2 evict-first: metadata is streamed once per step) S groups
+// ahead of the math, so memory-level parallelism no longer costs registers.
+// -----------------------------------------------------------------------------
+template <typename KV, int G>
+__global__ void __launch_bounds__(kScoreWarps * 32, 2) score_kernel_tma(PoolView p, BatchView b) {
+    constexpr int DPL = 4, D = 128;
+    constexpr int kRecs = RecsPer<G, DPL>::v;
+    constexpr int N = G * kRecs;
+    constexpr int SH = 5 - Log2<N>::v;
+    constexpr int MB = D * 4 + 2 * D * (int)sizeof(KV);  // metadata record bytes (meta_bytes)
+    constexpr int STAGE = kRecs * MB;
+    constexpr int S = (12288 / STAGE) < 2 ? 2 : ((12288 / STAGE) > 4 ? 4 : (12288 / STAGE));
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    unsigned char* wbuf = smem + 128 + (size_t)warp * S * STAGE;
+    uint64_t* wbar = bars + warp * S;
+    if (lane == 0)
+        for (int i = 0; i < S; ++i) mbar_init(&wbar[i], 1);
+    fence_mbar_init();
+    __syncwarp();
+
+    const int u = blockIdx.y;
+    const int64_t off = b.list_off[u];
+    const int64_t n = b.list_off[u + 1] - off;
+    const int base = lane * DPL;
+    double qd[G][DPL];  // q * 2^896 (compensates the scaled metadata)
+#pragma unroll
+    for (int h = 0; h < G; ++h) {
+        float qf[DPL];
+        if (h < b.g)
+            load_row<DPL>(b.q + ((size_t)u * b.g + h) * D + base, true, DPL, qf);
+        else
+#pragma unroll
+            for (int j = 0; j < DPL; ++j) qf[j] = 0.0f;
+#pragma unroll
+        for (int j = 0; j < DPL; ++j) qd[h][j] = (double)qf[j] * 0x1p896;
+    }
+    const int est = b.estimator;
+    const double scale = b.scale;
+    const int my_idx = lane >> SH;
+    const int my_h = my_idx / kRecs, my_j = my_idx % kRecs;
+    const bool writer = (lane & ((1 << SH) - 1)) == 0 && my_h < b.g;
+    uint64_t* keys = b.keys + off * b.g + (int64_t)my_h * n;
+    const uint64_t pol = policy_evict_first();
+
+    const int64_t ngroups = (n + kRecs - 1) / kRecs;
+    const int64_t nwarps = (int64_t)gridDim.x * kScoreWarps;
+    const int64_t grp0 = (int64_t)blockIdx.x * kScoreWarps + warp;
+    auto issue = [&](int64_t grp, int stage, int32_t slot) {
+        const int64_t p0 = grp * kRecs;
+        const int cnt = (int)((n - p0) < kRecs ? (n - p0) : kRecs);
+        if (lane == 0) mbar_arrive_expect_tx(&wbar[stage], (uint32_t)(cnt * MB));
+        __syncwarp();
+        if (lane < cnt) tma_load_1d(wbuf + stage * STAGE + lane * MB, p.meta + (int64_t)slot * MB, MB, &wbar[stage], pol);
+    };
+    // prologue: S groups in flight
+#pragma unroll 1
+    for (int st = 0; st < S; ++st) {
+        const int64_t g = grp0 + st * nwarps;
+        if (g < ngroups) {
+            const int32_t sl = (lane < kRecs && g * kRecs + lane < n) ? b.slots[off + g * kRecs + lane] : 0;
+            issue(g, st, sl);
+        }
+    }
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int64_t grp = grp0; grp < ngroups; grp += nwarps) {
+        const int64_t gn = grp + S * nwarps;  // group that refills this stage
+        const int32_t nslot = (gn < ngroups && lane < kRecs && gn * kRecs + lane < n) ? b.slots[off + gn * kRecs + lane] : 0;
+        mbar_wait(&wbar[stage], phase);
+        const unsigned char* sb = wbuf + stage * STAGE;
+        double acc[N];
+#pragma unroll
+        for (int i = 0; i < N; ++i) acc[i] = 0.0;
+#pragma unroll
+        for (int j = 0; j < kRecs; ++j) {
+            const unsigned char* rec = sb + j * MB;
+            const uint4 mv = *reinterpret_cast<const uint4*>(rec + lane * 16);
+            const uint32_t mw[4] = {mv.x, mv.y, mv.z, mv.w};
+            uint32_t lw[4], hw[4];
+            if constexpr (sizeof(KV) == 2) {
+                const uint2 lv = *reinterpret_cast<const uint2*>(rec + D * 4 + lane * 8);
+                const uint2 hv = *reinterpret_cast<const uint2*>(rec + D * 4 + D * 2 + lane * 8);
+                lw[0] = lv.x << 16; lw[1] = lv.x & 0xFFFF0000u; lw[2] = lv.y << 16; lw[3] = lv.y & 0xFFFF0000u;
+                hw[0] = hv.x << 16; hw[1] = hv.x & 0xFFFF0000u; hw[2] = hv.y << 16; hw[3] = hv.y & 0xFFFF0000u;
+            } else {
+                const uint4 lv = *reinterpret_cast<const uint4*>(rec + D * 4 + lane * 16);
+                const uint4 hv = *reinterpret_cast<const uint4*>(rec + D * 8 + lane * 16);
+                lw[0] = lv.x; lw[1] = lv.y; lw[2] = lv.z; lw[3] = lv.w;
+                hw[0] = hv.x; hw[1] = hv.y; hw[2] = hv.z; hw[3] = hv.w;
+            }
+#pragma unroll
+            for (int jj = 0; jj < DPL; ++jj) {
+                const double m = f32_scaled(mw[jj]);
+                const double lo = f32_scaled(lw[jj]);
+                const double hi = f32_scaled(hw[jj]);
+                double A, B = 0.0;
+                if (est == 0) {
+                    A = m;
+                } else {
+                    const double c2 = lo + hi;
+                    B = (hi - lo) * 0.5;
+                    A = est == 2 ? fma(0.5, c2, m) : c2 * 0.5;
+                }
+#pragma unroll
+                for (int h = 0; h < G; ++h) {
+                    const double qv = qd[h][jj];
+                    double a = fma(qv, A, acc[h * kRecs + j]);
+                    if (est != 0) a = fma(fabs(qv), B, a);
+                    acc[h * kRecs + j] = a;
+                }
+            }
+        }
+        // every lane's shared-memory reads of this stage precede the refill (generic -> async proxy)
+        fence_proxy_async();
+        __syncwarp();
+        if (gn < ngroups) issue(gn, stage, nslot);
+        const double tot = reduce_scatter_d<N>(acc, lane);
+        const int64_t p0 = grp * kRecs;
+        if (writer && p0 + my_j < n) {
+            const double sc = est == 2 ? 0.5 * (tot * scale) : tot * scale;
+            keys[p0 + my_j] = make_key(sc, (uint32_t)(p0 + my_j), b.pos_bits);
+        }
+        if (++stage == S) {
+            stage = 0;
+            phase ^= 1u;
+        }
+    }
+}
+
+template <typename KV, int G>
+static size_t tma_smem_bytes() {
+    constexpr int kRecs = RecsPer<G, 4>::v;
+    constexpr int STAGE = kRecs * (128 * 4 + 2 * 128 * (int)sizeof(KV));
+    constexpr int S = (12288 / STAGE) < 2 ? 2 : ((12288 / STAGE) > 4 ? 4 : (12288 / STAGE));
+    return 128 + (size_t)kScoreWarps * S * STAGE;
+}
+
+template <typename KV, int G>
+static void launch_score_tma(const PoolView& p, const BatchView& b, dim3 grid, cudaStream_t st) {
+    const size_t smem = tma_smem_bytes<KV, G>();
+    cudaFuncSetAttribute(score_kernel_tma<KV, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    score_kernel_tma<KV, G><<<grid, kScoreWarps * 32, smem, st>>>(p, b);
+}
+
 // =============================================================================
 // K6: fp64 block masses log(sum_t exp(q.k_t*scale)) for Oracle ranking and the
 // coverage audit (reference engine.cpp:64-72 computes these in plan_blocks).
@@ -291,6 +443,11 @@ static void launch_score_g(const PoolView& p, const BatchView& b, dim3 grid, cud
 
 template <typename KV>
 static void launch_score(const PoolView& p, const BatchView& b, dim3 grid, cudaStream_t st) {
+    if (b.d == 128 && p.meta_bytes == 128 * 4 + 2 * 128 * (int64_t)sizeof(KV)) {  // TMA-staged production path
+        if (g_for(b.g) == 4) launch_score_tma<KV, 4>(p, b, grid, st);
+        else launch_score_tma<KV, 8>(p, b, grid, st);
+        return;
+    }
     if (g_for(b.g) == 4) launch_score_g<KV, 4>(p, b, grid, st);
     else launch_score_g<KV, 8>(p, b, grid, st);
 }
