@@ -393,6 +393,12 @@ int psattn_run_batch(psattn_pool* pool, const psattn_batch* b, void* workspace, 
     return PSATTN_OK;
 }
 
+int psattn_set_progressive_kernel(int32_t mode) {
+    if (mode < 0 || mode > 2) return fail(PSATTN_ERR_INVALID_ARGUMENT, "progressive kernel mode must be 0, 1 or 2");
+    set_psa_kernel_choice(mode);
+    return PSATTN_OK;
+}
+
 int psattn_profile_enable(int32_t enable) {
     std::lock_guard<std::mutex> lk(g_prof.mu);
     g_prof.on = enable != 0;

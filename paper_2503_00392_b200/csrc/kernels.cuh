@@ -59,6 +59,10 @@ cudaError_t launch_synth_fill(const PoolView& p, uint64_t seed, float skew, floa
                               int32_t n_units, const int64_t* d_unit_ids, const int64_t* d_slot_off,
                               const int64_t* d_tokens, int64_t max_blocks, float* d_dirs, cudaStream_t st);
 void launch_psa(const PoolView& p, const BatchView& b, cudaStream_t st);
+bool gqa_supported(const PoolView& p, const BatchView& b);
+void launch_gqa(const PoolView& p, const BatchView& b, cudaStream_t st);
+// 0 = auto (GQA kernel when supported), 1 = per-query kernel, 2 = GQA kernel
+void set_psa_kernel_choice(int choice);
 // Returns the number of kernel launches issued, or -1 on error (cudaGetLastError has it).
 int launch_batch(const PoolView& p, const BatchView& b, cudaStream_t st, cudaEvent_t* marks = nullptr);
 cudaError_t launch_union(const BatchView& b, int64_t* out_union, cudaStream_t st);

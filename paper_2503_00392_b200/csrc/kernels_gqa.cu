@@ -1,0 +1,350 @@
+// kernels_gqa.cu — progressive attention for a whole GQA group in one CTA (sm_100a).
+#include <cuda_bf16.h>
+#include <float.h>
+#include <math.h>
+
+#include "common.cuh"
+#include "kernels.cuh"
+#include "psa_order.cuh"
+
+namespace psa {
+
+// =============================================================================
+// psa_gqa_kernel: one CTA (8 warps) per (request, layer, kv-head) unit running
+// the g q-heads of its GQA group together (psa_attention_multi_head, reference
+// engine.cpp:240-260: every head keeps its OWN ranking and stop point, SPEC D6).
+//
+// Each round, every live head h contributes its next chunk of <= 32 ranks; the
+// chunks are merged into a union U (hash on list position) so a block ranked by
+// several heads is read ONCE:
+//   1. ORDER   per-head lazy tranches (bucket select + bitonic, psa_order.cuh);
+//   2. K pass  each block of U: its K rows are loaded once and scored for all g
+//              heads (fp32 q.k*scale, block max / exp-sum / log_as per head);
+//   3. decide  warp h runs head h's coverage scan over its chunk (decide_chunk),
+//              all heads in parallel; committed (block, head) pairs are marked;
+//   4. V pass  each block of U committed by >= 1 head: V rows loaded once,
+//              accumulated into every committing head's online-softmax state.
+// With correlated heads (the usual GQA case) U is ~1 chunk, so K/V bytes and
+// the bf16->fp32 conversions are ~1/g of the per-head kernel's.
+// =============================================================================
+constexpr int kGTCap = 512;   // tranche capacity per head
+constexpr int kHash = 512;    // pos -> U index (>= 2 * G * kChunk)
+
+template <int TOK, int G>
+struct GqaSmem {
+    uint64_t tb[G][kGTCap];
+    int32_t tslot[G][kGTCap];
+    uint8_t tntok[G][kGTCap];
+    uint32_t hist[kBins];
+    float w[G * kChunk][G][TOK];   // per (U entry, head) token weights exp(s - m)
+    float mb[G * kChunk][G], lb[G * kChunk][G], la[G * kChunk][G];
+    float o[kPsaWarps][G][128];    // per-warp, per-head output accumulators (d <= 128)
+    float om[kPsaWarps][G], ol[kPsaWarps][G];
+    int32_t uslot[G * kChunk];
+    int32_t upos[G * kChunk];
+    uint8_t untok[G * kChunk];
+    uint32_t umask[G * kChunk];
+    int16_t cidx[G][kChunk];
+    int32_t hkey[kHash];
+    int16_t hval[kHash];
+    int64_t tr0[G], cb[G];
+    uint64_t last[G];
+    double est[G], acc[G], mn[G];
+    int tc[G], cnt[G], commit[G], fin[G], live[G];
+    int ucount, nlive;
+    SelScratch sel;
+};
+
+template <typename KV, int DPL, int TOK, bool FULL, int G>
+__global__ void __launch_bounds__(kPsaThreads, 2) psa_gqa_kernel(PoolView p, BatchView b) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    GqaSmem<TOK, G>& s = *reinterpret_cast<GqaSmem<TOK, G>*>(smem_raw);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int u = blockIdx.x;
+    const int g = b.g;
+    const int64_t off = b.list_off[u];
+    const int64_t n = b.list_off[u + 1] - off;
+    const int64_t limit = b.topk > 0 ? (b.topk < n ? b.topk : n) : n;
+    const double eps = b.topk > 0 ? 1.0 : b.eps;
+    const int d = FULL ? 32 * DPL : b.d;
+    const int base = lane * DPL;
+    const int lim = d - base;
+    constexpr bool full = FULL;
+    const float fscale = (float)b.scale;
+    constexpr int TSH = 5 - Log2<TOK>::v;
+    const int my_tok = lane >> TSH;
+    const uint64_t pmask = (b.pos_bits >= 64) ? ~0ull : ((1ull << b.pos_bits) - 1ull);
+    const KV* kv = reinterpret_cast<const KV*>(p.kv);
+    const int64_t slot_elems = p.slot_bytes / (int64_t)sizeof(KV);
+    const int T = p.T;
+    const int64_t v_off = (int64_t)T * d;
+
+    float q[G][DPL];
+#pragma unroll
+    for (int h = 0; h < G; ++h) {
+        if (h < g)
+            load_row<DPL>(b.q + ((size_t)u * g + h) * d + base, full, lim, q[h]);
+        else
+#pragma unroll
+            for (int j = 0; j < DPL; ++j) q[h][j] = 0.0f;
+    }
+    if (tid < G) {
+        s.tr0[tid] = 0;
+        s.cb[tid] = 0;
+        s.tc[tid] = 0;
+        s.last[tid] = 0;
+        s.acc[tid] = -INFINITY;
+        s.mn[tid] = INFINITY;
+        s.live[tid] = tid < g;
+        s.est[tid] = 0.0;
+    }
+    for (int i = tid; i < kPsaWarps * G; i += kPsaThreads) {
+        (&s.om[0][0])[i] = -INFINITY;
+        (&s.ol[0][0])[i] = 0.0f;
+    }
+    for (int i = tid; i < kPsaWarps * G * 128; i += kPsaThreads) (&s.o[0][0][0])[i] = 0.0f;
+    __syncthreads();
+
+    for (;;) {
+        // ---- 1. ORDER: refill the tranche of every live head that consumed it ----
+#pragma unroll 1
+        for (int h = 0; h < G; ++h) {
+            if (!(s.live[h] && s.cb[h] >= s.tr0[h] + s.tc[h])) continue;  // uniform
+            const int64_t hb = off * g + (int64_t)h * n;
+            const int64_t t0 = s.tr0[h] + s.tc[h];
+            const int tc = select_tranche(s.sel, s.tb[h], kGTCap, s.hist, b.keys + hb, n, s.last[h], t0 == 0, kGTCap);
+            for (int i = tid; i < tc; i += kPsaThreads) {
+                const int32_t pos = (int32_t)(s.tb[h][i] & pmask);
+                b.rpos[hb + t0 + i] = pos;
+                const int32_t sl = b.slots[off + pos];
+                s.tslot[h][i] = sl;
+                s.tntok[h][i] = (uint8_t)p.ntok[sl];
+            }
+            __syncthreads();
+            if (tid == 0) {
+                s.tr0[h] = t0;
+                s.tc[h] = tc;
+                s.last[h] = s.tb[h][tc - 1];
+            }
+            __syncthreads();
+        }
+        // ---- 2. round: union of the live heads' next chunks ----
+        for (int i = tid; i < kHash; i += kPsaThreads) s.hkey[i] = -1;
+        if (tid < G) {
+            int c = 0;
+            if (s.live[tid]) {
+                const int64_t room = s.tr0[tid] + s.tc[tid] - s.cb[tid];
+                const int64_t left = limit - s.cb[tid];
+                c = (int)(left < kChunk ? left : kChunk);
+                if (room < c) c = (int)room;
+            }
+            s.cnt[tid] = c;
+        }
+        if (tid == 0) s.ucount = 0;
+        __syncthreads();
+        const int hh = tid >> 5, rr = tid & 31;  // one thread per (head, rank in chunk)
+        int my_slot_idx = -1;
+        int32_t my_pos = 0;
+        if (hh < G && rr < s.cnt[hh]) {
+            const int ci = (int)(s.cb[hh] - s.tr0[hh]) + rr;
+            my_pos = (int32_t)(s.tb[hh][ci] & pmask);
+            int hs = (int)(((uint32_t)my_pos * 2654435761u) >> 23) & (kHash - 1);
+            for (;;) {
+                const int old = atomicCAS(&s.hkey[hs], -1, my_pos);
+                if (old == -1) {  // first head to rank this block in the round: new U entry
+                    const int e = atomicAdd(&s.ucount, 1);
+                    s.hval[hs] = (int16_t)e;
+                    s.uslot[e] = s.tslot[hh][ci];
+                    s.untok[e] = s.tntok[hh][ci];
+                    s.upos[e] = my_pos;
+                    s.umask[e] = 0u;
+                    break;
+                }
+                if (old == my_pos) break;
+                hs = (hs + 1) & (kHash - 1);
+            }
+            my_slot_idx = hs;
+        }
+        __syncthreads();
+        if (my_slot_idx >= 0) s.cidx[hh][rr] = s.hval[my_slot_idx];
+        const int ucount = s.ucount;
+        // ---- 3. K pass: every U block once, scored for all heads ----
+#pragma unroll 1
+        for (int e = warp; e < ucount; e += kPsaWarps) {
+            const int32_t slot = s.uslot[e];
+            const int nt = s.untok[e];
+            const KV* kp = kv + (int64_t)slot * slot_elems + base;
+            float kr[TOK][DPL];
+#pragma unroll
+            for (int t = 0; t < TOK; ++t) load_row<DPL>(kp + (size_t)(T == TOK ? t : (t < T ? t : T - 1)) * d, full, lim, kr[t]);
+#pragma unroll
+            for (int h = 0; h < G; ++h) {
+                if (!s.live[h]) continue;  // uniform
+                float part[TOK];
+#pragma unroll
+                for (int t = 0; t < TOK; ++t) {
+                    float a = 0.0f;
+#pragma unroll
+                    for (int jj = 0; jj < DPL; ++jj) a = fmaf(q[h][jj], kr[t][jj], a);
+                    part[t] = a;
+                }
+                float sc = reduce_scatter<TOK>(part, lane) * fscale;
+                sc = my_tok < nt ? sc : -INFINITY;
+                const float mbv = warp_max(sc);
+                const float wv = my_tok < nt ? expf(sc - mbv) : 0.0f;
+                float lbv = wv;
+#pragma unroll
+                for (int o = 16; o >= (1 << TSH); o >>= 1) lbv += __shfl_xor_sync(PSA_FULL, lbv, o);
+                if ((lane & ((1 << TSH) - 1)) == 0) s.w[e][h][my_tok] = wv;
+                if (lane == 0) {
+                    s.mb[e][h] = mbv;
+                    s.lb[e][h] = lbv;
+                    s.la[e][h] = mbv + logf(lbv);
+                }
+            }
+        }
+        __syncthreads();
+        // ---- 4. decide: warp h for head h, all heads in parallel ----
+        if (warp < G && s.live[warp]) {
+            const int h = warp;
+            const int cnt = s.cnt[h];
+            const int64_t hb = off * g + (int64_t)h * n;
+            double x = -INFINITY;
+            if (lane < cnt) {
+                const int e = s.cidx[h][lane];
+                x = b.has_oracle ? b.omass[hb + s.upos[e]] : (double)s.la[e][h];
+            }
+            double acc = s.acc[h], mn = s.mn[h];
+            const Decision dc = decide_chunk(x, cnt, s.cb[h], n, limit, b.m, eps, acc, mn, b.iest ? b.iest + hb : nullptr);
+            if (lane < dc.commit) atomicOr(&s.umask[s.cidx[h][lane]], 1u << h);
+            if (lane == 0) {
+                s.commit[h] = dc.commit;
+                s.fin[h] = dc.fin;
+                s.est[h] = dc.est;
+                s.acc[h] = acc;
+                s.mn[h] = mn;
+            }
+        }
+        __syncthreads();
+        // ---- 5. V pass: committed U blocks once, into every committing head ----
+#pragma unroll 1
+        for (int e = warp; e < ucount; e += kPsaWarps) {
+            const uint32_t mask = s.umask[e];
+            if (!mask) continue;
+            const int32_t slot = s.uslot[e];
+            const KV* vp = kv + (int64_t)slot * slot_elems + v_off + base;
+            float vr[TOK][DPL];
+#pragma unroll
+            for (int t = 0; t < TOK; ++t) load_row<DPL>(vp + (size_t)(T == TOK ? t : (t < T ? t : T - 1)) * d, full, lim, vr[t]);
+#pragma unroll
+            for (int h = 0; h < G; ++h) {
+                if (!(mask & (1u << h))) continue;  // uniform
+                float ob[DPL];
+#pragma unroll
+                for (int jj = 0; jj < DPL; ++jj) ob[jj] = 0.0f;
+#pragma unroll
+                for (int t = 0; t < TOK; ++t) {
+                    const float wt = s.w[e][h][t];
+#pragma unroll
+                    for (int jj = 0; jj < DPL; ++jj) ob[jj] = fmaf(wt, vr[t][jj], ob[jj]);
+                }
+                const float mbj = s.mb[e][h];
+                const float M = s.om[warp][h];
+                const float mnew = fmaxf(M, mbj);
+                const float a = expf(M - mnew);
+                const float c = expf(mbj - mnew);
+                float* op = &s.o[warp][h][base];
+#pragma unroll
+                for (int jj = 0; jj < DPL; ++jj)
+                    if (base + jj < d) op[jj] = op[jj] * a + ob[jj] * c;
+                __syncwarp();
+                if (lane == 0) {
+                    s.ol[warp][h] = s.ol[warp][h] * a + s.lb[e][h] * c;
+                    s.om[warp][h] = mnew;
+                }
+                __syncwarp();
+            }
+        }
+        __syncthreads();
+        // ---- 6. advance cursors, retire finished heads ----
+        if (tid < G && s.live[tid]) {
+            const int h = tid;
+            s.cb[h] += s.commit[h];
+            if (s.fin[h]) {
+                s.live[h] = 0;
+                const int64_t qi = (int64_t)u * g + h;
+                b.bp[qi] = s.cb[h];
+                b.est[qi] = s.est[h];
+                b.term[qi] = b.topk > 0 ? (limit < n) : (s.cb[h] < n);
+            }
+        }
+        __syncthreads();
+        int live = 0;
+#pragma unroll
+        for (int h = 0; h < G; ++h) live += s.live[h];
+        if (!live) break;
+        __syncthreads();
+    }
+    // ---- finalize: merge the warps' states per head (finalize, attention.hpp:104-110) ----
+    for (int h = 0; h < g; ++h) {
+        float Mt = -INFINITY;
+#pragma unroll
+        for (int w = 0; w < kPsaWarps; ++w) Mt = fmaxf(Mt, s.om[w][h]);
+        float Lt = 0.0f, sc[kPsaWarps];
+#pragma unroll
+        for (int w = 0; w < kPsaWarps; ++w) {
+            sc[w] = s.ol[w][h] > 0.0f ? expf(s.om[w][h] - Mt) : 0.0f;
+            Lt += s.ol[w][h] * sc[w];
+        }
+        const int64_t qi = (int64_t)u * g + h;
+        for (int i = tid; i < d; i += kPsaThreads) {
+            float o = 0.0f;
+#pragma unroll
+            for (int w = 0; w < kPsaWarps; ++w) o += sc[w] > 0.0f ? s.o[w][h][i] * sc[w] : 0.0f;
+            b.out[qi * d + i] = o / Lt;
+        }
+        if (b.tcov && tid == 0) {
+            double tcv = -1.0;
+            if (b.audit) {
+                const double* om = b.omass + off * g + (int64_t)h * n;
+                double mx = -INFINITY;
+                for (int64_t i = 0; i < n; ++i) mx = fmax(mx, om[i]);
+                double sm = 0.0;
+                for (int64_t i = 0; i < n; ++i) sm += exp(om[i] - mx);
+                tcv = exp(s.acc[h] - (mx + log(sm)));
+            }
+            b.tcov[qi] = tcv;
+        }
+    }
+}
+
+template <typename KV, int DPL, int TOK, bool FULL, int G>
+static void launch_gqa_t(const PoolView& p, const BatchView& b, cudaStream_t st) {
+    const size_t smem = sizeof(GqaSmem<TOK, G>);
+    cudaFuncSetAttribute(psa_gqa_kernel<KV, DPL, TOK, FULL, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    psa_gqa_kernel<KV, DPL, TOK, FULL, G><<<b.n_units, kPsaThreads, smem, st>>>(p, b);
+}
+
+template <typename KV, int G>
+static void launch_gqa_g(const PoolView& p, const BatchView& b, cudaStream_t st) {
+    // d = 128 (DPL 4) and d = 64 (DPL 2), blocks of <= 16 tokens: the production shapes
+    if (b.d == 128) launch_gqa_t<KV, 4, 16, true, G>(p, b, st);
+    else launch_gqa_t<KV, 2, 16, true, G>(p, b, st);
+}
+
+bool gqa_supported(const PoolView& p, const BatchView& b) {
+    return b.g >= 2 && b.g <= 4 && (b.d == 128 || b.d == 64) && p.T <= 16;
+}
+
+void launch_gqa(const PoolView& p, const BatchView& b, cudaStream_t st) {
+    const int G = b.g <= 2 ? 2 : 4;
+    if (p.dtype == 0) {
+        if (G == 2) launch_gqa_g<float, 2>(p, b, st);
+        else launch_gqa_g<float, 4>(p, b, st);
+    } else {
+        if (G == 2) launch_gqa_g<__nv_bfloat16, 2>(p, b, st);
+        else launch_gqa_g<__nv_bfloat16, 4>(p, b, st);
+    }
+}
+
+}  // namespace psa

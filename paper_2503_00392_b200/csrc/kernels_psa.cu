@@ -6,6 +6,7 @@
 
 #include "common.cuh"
 #include "kernels.cuh"
+#include "psa_order.cuh"
 
 namespace psa {
 
@@ -34,12 +35,8 @@ namespace psa {
 // The stop decision never leaves shared memory: no host round trip. K bytes of
 // at most one partial chunk past the stop point are the speculative waste.
 // =============================================================================
-constexpr int kPsaWarps = 8;
-constexpr int kPsaThreads = kPsaWarps * 32;
-constexpr int kChunk = 32;
 constexpr int kBpw = kChunk / kPsaWarps;
 constexpr int kTCap = 1024;
-constexpr int kBins = 2048;
 constexpr int kFirstTranche = 512;
 
 template <int TOK>
@@ -51,183 +48,11 @@ struct PsaSmem {
     float w[kPsaWarps][kBpw][TOK];
     float mb[kPsaWarps][kBpw], lb[kPsaWarps][kBpw];
     float la[kChunk];
-    unsigned long long red_min, red_max;
-    unsigned int red_cnt, gcount, excl;
-    int bstar;
+    SelScratch sel;
     int commit, fin;
     double est, acc;
     float m[kPsaWarps], l[kPsaWarps];
 };
-
-__device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long x) {
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) {
-        const unsigned long long y = __shfl_xor_sync(PSA_FULL, x, o);
-        x = y < x ? y : x;
-    }
-    return x;
-}
-__device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long x) {
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) {
-        const unsigned long long y = __shfl_xor_sync(PSA_FULL, x, o);
-        x = y > x ? y : x;
-    }
-    return x;
-}
-
-// All-ascending bitonic network on a[0, n) in shared memory (indices >= n act as +inf).
-__device__ __forceinline__ void bitonic_smem(uint64_t* a, int n) {
-    int n2 = 1;
-    while (n2 < n) n2 <<= 1;
-    for (int k = 2; k <= n2; k <<= 1) {
-        for (int j = k >> 1; j > 0; j >>= 1) {
-            for (int i = threadIdx.x; i < (n2 >> 1); i += blockDim.x) {
-                const int lo = ((i & ~(j - 1)) << 1) | (i & (j - 1));  // j is a power of two
-                const int hi = (j == (k >> 1)) ? (lo ^ (k - 1)) : (lo + j);
-                if (hi < n) {
-                    const uint64_t x = a[lo], y = a[hi];
-                    if (x > y) {
-                        a[lo] = y;
-                        a[hi] = x;
-                    }
-                }
-            }
-            __syncthreads();
-        }
-    }
-}
-
-// Calls f(key) for every key of the head; 8 independent loads in flight per thread.
-template <typename F>
-__device__ __forceinline__ void scan_keys(const uint64_t* __restrict__ keys, int64_t n, F&& f) {
-    constexpr int U = 8;
-    for (int64_t i0 = threadIdx.x; i0 < n; i0 += (int64_t)U * kPsaThreads) {
-        uint64_t k[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int64_t i = i0 + (int64_t)u * kPsaThreads;
-            k[u] = i < n ? __ldg(reinterpret_cast<const unsigned long long*>(keys) + i) : ~0ull;
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-            if (i0 + (int64_t)u * kPsaThreads < n) f(k[u]);
-    }
-}
-
-// Next tranche: the C (<= kTCap, ~target) smallest keys greater than `last` (all keys if first).
-template <int TOK>
-__device__ int select_tranche(PsaSmem<TOK>& s, const uint64_t* __restrict__ keys, int64_t n, uint64_t last,
-                              bool first, unsigned target) {
-    const int tid = threadIdx.x, lane = tid & 31;
-    unsigned long long lmin = ~0ull, lmax = 0;
-    unsigned lcnt = 0;
-    scan_keys(keys, n, [&](uint64_t k) {
-        if (first || k > last) {
-            lmin = k < lmin ? k : lmin;
-            lmax = k > lmax ? k : lmax;
-            ++lcnt;
-        }
-    });
-    if (tid == 0) {
-        s.red_min = ~0ull;
-        s.red_max = 0;
-        s.red_cnt = 0;
-        s.gcount = 0;
-    }
-    __syncthreads();
-    lmin = warp_min_u64(lmin);
-    lmax = warp_max_u64(lmax);
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) lcnt += __shfl_xor_sync(PSA_FULL, lcnt, o);
-    if (lane == 0) {
-        atomicMin(&s.red_min, lmin);
-        atomicMax(&s.red_max, lmax);
-        atomicAdd(&s.red_cnt, lcnt);
-    }
-    __syncthreads();
-    const uint64_t kmax = s.red_max;
-    uint64_t tau = kmax;
-    if (s.red_cnt > (unsigned)kTCap) {
-        uint64_t lo = s.red_min, hi = kmax;
-        unsigned need = target, before = 0;
-        for (int it = 0; it < 10; ++it) {
-            const uint64_t span = hi - lo;
-            const int bits = 64 - __clzll((long long)span);
-            const int sh = bits > 11 ? bits - 11 : 0;
-            for (int i = tid; i < kBins; i += kPsaThreads) s.hist[i] = 0;
-            __syncthreads();
-            scan_keys(keys, n, [&](uint64_t k) {
-                if ((first || k > last) && k >= lo && k <= hi) atomicAdd(&s.hist[(k - lo) >> sh], 1u);
-            });
-            __syncthreads();
-            // first bin b with cum(b) >= need: each thread owns 8 consecutive bins
-            constexpr int per = kBins / kPsaThreads;
-            unsigned loc = 0;
-#pragma unroll
-            for (int j = 0; j < per; ++j) loc += s.hist[tid * per + j];
-            unsigned inc = loc;  // inclusive warp scan
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const unsigned y = __shfl_up_sync(PSA_FULL, inc, o);
-                if (lane >= o) inc += y;
-            }
-            __shared__ unsigned wsum[kPsaWarps];
-            if (lane == 31) wsum[tid >> 5] = inc;
-            __syncthreads();
-            unsigned wbase = 0;
-            for (int w = 0; w < (tid >> 5); ++w) wbase += wsum[w];
-            unsigned cum = wbase + inc - loc;  // exclusive prefix of this thread's bins
-            if (cum < need && need <= cum + loc) {
-#pragma unroll 1
-                for (int j = 0; j < per; ++j) {
-                    const unsigned c = s.hist[tid * per + j];
-                    if (need <= cum + c) {
-                        s.bstar = tid * per + j;
-                        s.excl = cum;
-                        break;
-                    }
-                    cum += c;
-                }
-            }
-            __syncthreads();
-            const int bs = s.bstar;
-            const unsigned ex = s.excl, incl = ex + s.hist[bs];
-            const uint64_t width_m1 = (sh >= 64) ? ~0ull : ((1ull << sh) - 1ull);
-            const uint64_t bin_lo = lo + ((uint64_t)bs << sh);
-            if (before + incl <= (unsigned)kTCap) {
-                tau = (hi - bin_lo <= width_m1) ? hi : bin_lo + width_m1;
-                break;
-            }
-            if (before + ex >= 32) {
-                tau = bin_lo - 1;  // take the bins below bs
-                break;
-            }
-            before += ex;
-            need -= ex;
-            lo = bin_lo;
-            if (hi - lo > width_m1) hi = lo + width_m1;
-            __syncthreads();
-        }
-    }
-    // gather the survivors (warp-aggregated slot reservation)
-    scan_keys(keys, n, [&](uint64_t k) {
-        const bool take = (first || k > last) && k <= tau;
-        const unsigned m = __ballot_sync(__activemask(), take);
-        if (take) {
-            const int leader = __ffs(m) - 1;
-            unsigned basei = 0;
-            if (lane == leader) basei = atomicAdd(&s.gcount, (unsigned)__popc(m));
-            basei = __shfl_sync(m, basei, leader);
-            const unsigned idx = basei + __popc(m & ((1u << lane) - 1u));
-            if (idx < (unsigned)kTCap) s.tb[idx] = k;
-        }
-    });
-    __syncthreads();
-    const int C = (int)min(s.gcount, (unsigned)kTCap);
-    bitonic_smem(s.tb, C);
-    return C;
-}
 
 template <typename KV, int DPL, int TOK, bool FULL>
 __global__ void __launch_bounds__(kPsaThreads, 3) psa_kernel(PoolView p, BatchView b) {
@@ -271,7 +96,7 @@ __global__ void __launch_bounds__(kPsaThreads, 3) psa_kernel(PoolView p, BatchVi
     for (int64_t cb = 0;;) {
         if (cb >= tr0 + tc) {  // ---- ORDER: next tranche ----
             tr0 += tc;
-            tc = select_tranche(s, keys, n, last, tr0 == 0, tr0 == 0 ? kFirstTranche : kTCap);
+            tc = select_tranche(s.sel, s.tb, kTCap, s.hist, keys, n, last, tr0 == 0, tr0 == 0 ? kFirstTranche : kTCap);
             last = s.tb[tc - 1];
             for (int i = threadIdx.x; i < tc; i += kPsaThreads) {
                 const int32_t pos = (int32_t)(s.tb[i] & pmask);
@@ -336,40 +161,13 @@ __global__ void __launch_bounds__(kPsaThreads, 3) psa_kernel(PoolView p, BatchVi
         __syncthreads();
         // ---- 2. decide (warp 0) ----
         if (warp == 0) {
-            const bool valid = lane < cnt;
-            const int64_t r = cb + lane;
             double x = -INFINITY;
-            if (valid) x = omass ? omass[s.tb[ci + lane] & pmask] : (double)s.la[lane];
-            double mx = warp_max_d(x);
-            mx = fmax(mx, acc);
-            double e = valid ? exp(x - mx) : 0.0;
-            double mnv = valid ? x : INFINITY;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const double ye = __shfl_up_sync(PSA_FULL, e, o);
-                const double ym = __shfl_up_sync(PSA_FULL, mnv, o);
-                if (lane >= o) {
-                    e += ye;
-                    mnv = fmin(mnv, ym);
-                }
-            }
-            if (acc != -INFINITY) e += exp(acc - mx);
-            const double acc_i = mx + log(e);
-            const double mn_i = fmin(mnv, mn);
-            const int64_t nl = n - (r + 1);
-            const double est_i = nl == 0 ? 1.0 : 1.0 / (1.0 + (double)nl * exp(mn_i - acc_i));
-            const bool boundary = valid && ((((r + 1) % b.m) == 0) || (r + 1 == limit));
-            const bool stop = boundary && (est_i > eps || r + 1 == limit);
-            const unsigned bal = __ballot_sync(PSA_FULL, stop);
-            const int f = bal ? (__ffs(bal) - 1) : (cnt - 1);
-            if (b.iest && boundary && lane <= f) b.iest[hb + r] = est_i;  // IterationStats::estimated_coverage
-            acc = __shfl_sync(PSA_FULL, acc_i, f);
-            mn = __shfl_sync(PSA_FULL, mn_i, f);
-            const double e_f = __shfl_sync(PSA_FULL, est_i, f);
+            if (lane < cnt) x = omass ? omass[s.tb[ci + lane] & pmask] : (double)s.la[lane];
+            const Decision dc = decide_chunk(x, cnt, cb, n, limit, b.m, eps, acc, mn, b.iest ? b.iest + hb : nullptr);
             if (lane == 0) {
-                s.commit = f + 1;
-                s.fin = bal ? 1 : 0;
-                s.est = e_f;
+                s.commit = dc.commit;
+                s.fin = dc.fin;
+                s.est = dc.est;
                 s.acc = acc;
             }
         }
@@ -478,7 +276,14 @@ static void launch_psa_t(const PoolView& p, const BatchView& b, int nq, cudaStre
     }
 }
 
+static int g_psa_choice = 0;
+void set_psa_kernel_choice(int choice) { g_psa_choice = choice; }
+
 void launch_psa(const PoolView& p, const BatchView& b, cudaStream_t st) {
+    if (g_psa_choice != 1 && gqa_supported(p, b)) {
+        launch_gqa(p, b, st);
+        return;
+    }
     const int nq = b.n_units * b.g;
     if (p.dtype == 0) {
         if (tok_for(p.T) == 16) launch_psa_t<float, 16>(p, b, nq, st);

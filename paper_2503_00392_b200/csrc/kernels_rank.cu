@@ -197,6 +197,8 @@ __global__ void __launch_bounds__(kScoreWarps * 32, 2) score_kernel(PoolView p, 
 // / 1.5 KB fp32, L2 evict-first: metadata is streamed once per step) S groups
 // ahead of the math, so memory-level parallelism no longer costs registers.
 // -----------------------------------------------------------------------------
+constexpr int kTmaBarBytes = 256;  // kScoreWarps x (<= 4 stages) x 8 B mbarriers
+
 template <typename KV, int G>
 __global__ void __launch_bounds__(kScoreWarps * 32, 2) score_kernel_tma(PoolView p, BatchView b) {
     constexpr int DPL = 4, D = 128;
@@ -210,7 +212,8 @@ __global__ void __launch_bounds__(kScoreWarps * 32, 2) score_kernel_tma(PoolView
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
-    unsigned char* wbuf = smem + 128 + (size_t)warp * S * STAGE;
+    static_assert(kScoreWarps * S * 8 <= kTmaBarBytes, "mbarrier region too small");
+    unsigned char* wbuf = smem + kTmaBarBytes + (size_t)warp * S * STAGE;
     uint64_t* wbar = bars + warp * S;
     if (lane == 0)
         for (int i = 0; i < S; ++i) mbar_init(&wbar[i], 1);
@@ -331,7 +334,7 @@ static size_t tma_smem_bytes() {
     constexpr int kRecs = RecsPer<G, 4>::v;
     constexpr int STAGE = kRecs * (128 * 4 + 2 * 128 * (int)sizeof(KV));
     constexpr int S = (12288 / STAGE) < 2 ? 2 : ((12288 / STAGE) > 4 ? 4 : (12288 / STAGE));
-    return 128 + (size_t)kScoreWarps * S * STAGE;
+    return kTmaBarBytes + (size_t)kScoreWarps * S * STAGE;
 }
 
 template <typename KV, int G>

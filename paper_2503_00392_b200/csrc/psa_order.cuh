@@ -1,0 +1,244 @@
+// psa_order.cuh — ordering (lazy tranche selection) and the coverage decide
+// step shared by the progressive kernels (kernels_psa.cu, kernels_gqa.cu).
+#pragma once
+
+#include <math.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace psa {
+
+constexpr int kPsaWarps = 8;
+constexpr int kPsaThreads = kPsaWarps * 32;
+constexpr int kChunk = 32;
+constexpr int kBins = 2048;
+
+struct SelScratch {
+    unsigned long long red_min, red_max;
+    unsigned int red_cnt, gcount, excl;
+    int bstar;
+    unsigned wsum[kPsaWarps];
+};
+
+__device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long x) {
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+        const unsigned long long y = __shfl_xor_sync(PSA_FULL, x, o);
+        x = y < x ? y : x;
+    }
+    return x;
+}
+__device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long x) {
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+        const unsigned long long y = __shfl_xor_sync(PSA_FULL, x, o);
+        x = y > x ? y : x;
+    }
+    return x;
+}
+
+// All-ascending bitonic network on a[0, n) in shared memory (indices >= n act as +inf).
+__device__ __forceinline__ void bitonic_smem(uint64_t* a, int n) {
+    int n2 = 1;
+    while (n2 < n) n2 <<= 1;
+    for (int k = 2; k <= n2; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < (n2 >> 1); i += blockDim.x) {
+                const int lo = ((i & ~(j - 1)) << 1) | (i & (j - 1));  // j is a power of two
+                const int hi = (j == (k >> 1)) ? (lo ^ (k - 1)) : (lo + j);
+                if (hi < n) {
+                    const uint64_t x = a[lo], y = a[hi];
+                    if (x > y) {
+                        a[lo] = y;
+                        a[hi] = x;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// Calls f(key) for every key of the head; 8 independent loads in flight per thread.
+template <typename F>
+__device__ __forceinline__ void scan_keys(const uint64_t* __restrict__ keys, int64_t n, F&& f) {
+    constexpr int U = 8;
+    for (int64_t i0 = threadIdx.x; i0 < n; i0 += (int64_t)U * kPsaThreads) {
+        uint64_t k[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t i = i0 + (int64_t)u * kPsaThreads;
+            k[u] = i < n ? __ldg(reinterpret_cast<const unsigned long long*>(keys) + i) : ~0ull;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (i0 + (int64_t)u * kPsaThreads < n) f(k[u]);
+    }
+}
+
+// Next tranche: the C (<= kTCap, ~target) smallest keys greater than `last` (all keys if first).
+static __device__ __noinline__ int select_tranche(SelScratch& s, uint64_t* tb, int cap, uint32_t* hist,
+                                          const uint64_t* __restrict__ keys, int64_t n, uint64_t last, bool first,
+                                          unsigned target) {
+    const int tid = threadIdx.x, lane = tid & 31;
+    unsigned long long lmin = ~0ull, lmax = 0;
+    unsigned lcnt = 0;
+    scan_keys(keys, n, [&](uint64_t k) {
+        if (first || k > last) {
+            lmin = k < lmin ? k : lmin;
+            lmax = k > lmax ? k : lmax;
+            ++lcnt;
+        }
+    });
+    if (tid == 0) {
+        s.red_min = ~0ull;
+        s.red_max = 0;
+        s.red_cnt = 0;
+        s.gcount = 0;
+    }
+    __syncthreads();
+    lmin = warp_min_u64(lmin);
+    lmax = warp_max_u64(lmax);
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) lcnt += __shfl_xor_sync(PSA_FULL, lcnt, o);
+    if (lane == 0) {
+        atomicMin(&s.red_min, lmin);
+        atomicMax(&s.red_max, lmax);
+        atomicAdd(&s.red_cnt, lcnt);
+    }
+    __syncthreads();
+    const uint64_t kmax = s.red_max;
+    uint64_t tau = kmax;
+    if (s.red_cnt > (unsigned)cap) {
+        uint64_t lo = s.red_min, hi = kmax;
+        unsigned need = target, before = 0;
+        for (int it = 0; it < 10; ++it) {
+            const uint64_t span = hi - lo;
+            const int bits = 64 - __clzll((long long)span);
+            const int sh = bits > 11 ? bits - 11 : 0;
+            for (int i = tid; i < kBins; i += kPsaThreads) hist[i] = 0;
+            __syncthreads();
+            scan_keys(keys, n, [&](uint64_t k) {
+                if ((first || k > last) && k >= lo && k <= hi) atomicAdd(&hist[(k - lo) >> sh], 1u);
+            });
+            __syncthreads();
+            // first bin b with cum(b) >= need: each thread owns 8 consecutive bins
+            constexpr int per = kBins / kPsaThreads;
+            unsigned loc = 0;
+#pragma unroll
+            for (int j = 0; j < per; ++j) loc += hist[tid * per + j];
+            unsigned inc = loc;  // inclusive warp scan
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned y = __shfl_up_sync(PSA_FULL, inc, o);
+                if (lane >= o) inc += y;
+            }
+            if (lane == 31) s.wsum[tid >> 5] = inc;
+            __syncthreads();
+            unsigned wbase = 0;
+            for (int w = 0; w < (tid >> 5); ++w) wbase += s.wsum[w];
+            unsigned cum = wbase + inc - loc;  // exclusive prefix of this thread's bins
+            if (cum < need && need <= cum + loc) {
+#pragma unroll 1
+                for (int j = 0; j < per; ++j) {
+                    const unsigned c = hist[tid * per + j];
+                    if (need <= cum + c) {
+                        s.bstar = tid * per + j;
+                        s.excl = cum;
+                        break;
+                    }
+                    cum += c;
+                }
+            }
+            __syncthreads();
+            const int bs = s.bstar;
+            const unsigned ex = s.excl, incl = ex + hist[bs];
+            const uint64_t width_m1 = (sh >= 64) ? ~0ull : ((1ull << sh) - 1ull);
+            const uint64_t bin_lo = lo + ((uint64_t)bs << sh);
+            if (before + incl <= (unsigned)cap) {
+                tau = (hi - bin_lo <= width_m1) ? hi : bin_lo + width_m1;
+                break;
+            }
+            if (before + ex >= 32) {
+                tau = bin_lo - 1;  // take the bins below bs
+                break;
+            }
+            before += ex;
+            need -= ex;
+            lo = bin_lo;
+            if (hi - lo > width_m1) hi = lo + width_m1;
+            __syncthreads();
+        }
+    }
+    // gather the survivors (warp-aggregated slot reservation)
+    scan_keys(keys, n, [&](uint64_t k) {
+        const bool take = (first || k > last) && k <= tau;
+        const unsigned m = __ballot_sync(__activemask(), take);
+        if (take) {
+            const int leader = __ffs(m) - 1;
+            unsigned basei = 0;
+            if (lane == leader) basei = atomicAdd(&s.gcount, (unsigned)__popc(m));
+            basei = __shfl_sync(m, basei, leader);
+            const unsigned idx = basei + __popc(m & ((1u << lane) - 1u));
+            if (idx < (unsigned)cap) tb[idx] = k;
+        }
+    });
+    __syncthreads();
+    const int C = (int)min(s.gcount, (unsigned)cap);
+    bitonic_smem(tb, C);
+    return C;
+}
+
+
+// Coverage decide step for one chunk of ranks [cb, cb+cnt), executed by ONE full
+// warp: lane i holds x = log-mass of rank cb+i (valid for i < cnt). Running
+// log-sum-exp and min (CoverageEstimator::observe, reference engine.cpp:38-46) are
+// carried in acc/mn (lane-uniform). The estimate 1/(1 + n_left*exp(min - acc))
+// (engine.cpp:48-55) is evaluated at every microbatch boundary; the first boundary
+// with est > eps (engine.cpp:125), or the budget/end of the plan, stops the run.
+struct Decision {
+    int commit;  // ranks of this chunk that are processed
+    int fin;     // run finished inside this chunk
+    double est;  // estimate at the last evaluated boundary
+};
+
+__device__ __forceinline__ Decision decide_chunk(double x, int cnt, int64_t cb, int64_t n, int64_t limit, int m,
+                                                 double eps, double& acc, double& mn, double* iest_head) {
+    const int lane = threadIdx.x & 31;
+    const bool valid = lane < cnt;
+    const int64_t r = cb + lane;
+    if (!valid) x = -INFINITY;
+    double mx = warp_max_d(x);
+    mx = fmax(mx, acc);
+    double e = valid ? exp(x - mx) : 0.0;
+    double mnv = valid ? x : INFINITY;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const double ye = __shfl_up_sync(PSA_FULL, e, o);
+        const double ym = __shfl_up_sync(PSA_FULL, mnv, o);
+        if (lane >= o) {
+            e += ye;
+            mnv = fmin(mnv, ym);
+        }
+    }
+    if (acc != -INFINITY) e += exp(acc - mx);
+    const double acc_i = mx + log(e);
+    const double mn_i = fmin(mnv, mn);
+    const int64_t nl = n - (r + 1);
+    const double est_i = nl == 0 ? 1.0 : 1.0 / (1.0 + (double)nl * exp(mn_i - acc_i));
+    const bool boundary = valid && ((((r + 1) % m) == 0) || (r + 1 == limit));
+    const bool stop = boundary && (est_i > eps || r + 1 == limit);
+    const unsigned bal = __ballot_sync(PSA_FULL, stop);
+    const int f = bal ? (__ffs(bal) - 1) : (cnt - 1);
+    if (iest_head && boundary && lane <= f) iest_head[r] = est_i;  // IterationStats::estimated_coverage
+    acc = __shfl_sync(PSA_FULL, acc_i, f);
+    mn = __shfl_sync(PSA_FULL, mn_i, f);
+    Decision d;
+    d.est = __shfl_sync(PSA_FULL, est_i, f);
+    d.commit = f + 1;
+    d.fin = bal ? 1 : 0;
+    return d;
+}
+
+}  // namespace psa

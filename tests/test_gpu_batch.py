@@ -110,20 +110,42 @@ def test_batch_parity(mods, oracle, ci, d, T, g):
     assert tags.count("exact") >= len(tags) - 1
 
 
-def test_gqa_equals_per_head(mods):
-    """psa_attention_multi_head semantics (engine.cpp:240-260): a g=4 launch equals four g=1 runs."""
-    rng = np.random.default_rng(31337)
-    d, T = 128, 16
-    unit = random_blockset(rng, 300, d, 16, 16, planted_frac=0.05)
-    qs = [rng.standard_normal(d).astype(np.float32) * 2 for _ in range(4)]
-    _, r4, off4 = run_units(mods, [unit], [qs], T, epsilon=0.9)
-    _, r1, off1 = run_units(mods, [unit] * 4, [[q] for q in qs], T, epsilon=0.9)
-    for h in range(4):
-        a = unpack(r4, off4, 0, h, unit.n)
+@pytest.mark.parametrize("mode", [1, 2])
+@pytest.mark.parametrize("d,g", [(128, 4), (64, 2), (128, 3)])
+def test_gqa_equals_per_head(mods, d, g, mode):
+    """psa_attention_multi_head semantics (engine.cpp:240-260): a GQA launch (per-head or
+    GQA-group kernel) equals g independent g=1 runs: same ranks, same stop points (identical
+    fp32 block masses), outputs equal up to summation order."""
+    capi, _ = mods
+    rng = np.random.default_rng(31337 + d + g)
+    T = 16
+    unit = random_blockset(rng, 300, d, 1, 16, planted_frac=0.05)
+    base = rng.standard_normal(d)
+    qs = [((base + 0.5 * rng.standard_normal(d)) * 2).astype(np.float32) for _ in range(g)]
+    assert capi.lib.psattn_set_progressive_kernel(mode) == 0
+    try:
+        _, rg, offg = run_units(mods, [unit], [qs], T, epsilon=0.9)
+        _, r1, off1 = run_units(mods, [unit] * g, [[q] for q in qs], T, epsilon=0.9)
+    finally:
+        capi.lib.psattn_set_progressive_kernel(0)
+    for h in range(g):
+        a = unpack(rg, offg, 0, h, unit.n)
         b = unpack(r1, off1, h, 0, unit.n)
         assert a["bp"] == b["bp"]
         assert np.array_equal(a["ids"], b["ids"])
-        assert a["out"].tobytes() == b["out"].tobytes()
+        assert a["est"] == b["est"]
+        assert np.max(np.abs(a["out"] - b["out"])) <= 1e-5
+
+
+@pytest.mark.parametrize("ci", [0, 1, 5, 6, 7, 8])
+def test_per_head_kernel_parity(mods, oracle, ci):
+    """The per-q-head progressive kernel (forced) on the GQA shapes, against the oracle."""
+    capi, _ = mods
+    capi.lib.psattn_set_progressive_kernel(1)
+    try:
+        test_batch_parity(mods, oracle, ci, 128, 16, 4)
+    finally:
+        capi.lib.psattn_set_progressive_kernel(0)
 
 
 def test_union_counter(mods):
