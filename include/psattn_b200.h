@@ -133,6 +133,13 @@ int psattn_batch_last_launches(int32_t* out_count);
  * blocks <= 16 tokens; else one CTA per q-head), 1 = always per q-head,
  * 2 = GQA kernel whenever supported. Process-wide. */
 int psattn_set_progressive_kernel(int32_t mode);
+/* Score/progressive overlap: psattn_run_batch splits a batch of >= 512 units into
+ * sub-batches and runs score(i+1) on the caller's stream while progressive(i) runs on
+ * an internal stream joined back by events (stream-ordered, no host sync).
+ * 0 = auto (8 sub-batches when n_units >= 512), 1 = off, k = k sub-batches (<= 16). */
+int psattn_set_pipeline(int32_t sub_batches);
+/* Score-kernel selection: 0 = auto (TMA-staged for dim 128), 1 = register-staged, 2 = TMA whenever supported. */
+int psattn_set_score_kernel(int32_t mode);
 
 /* Stage timing (benchmark instrumentation). While enabled, psattn_run_batch
  * records CUDA events around each kernel on its own stream (no host sync).

@@ -107,6 +107,8 @@ def _load() -> C.CDLL:
     L.psattn_batch_union_blocks.argtypes = [C.POINTER(Batch), vp, vp, vp]
     L.psattn_batch_last_launches.argtypes = [C.POINTER(i32)]
     L.psattn_set_progressive_kernel.argtypes = [i32]
+    L.psattn_set_score_kernel.argtypes = [i32]
+    L.psattn_set_pipeline.argtypes = [i32]
     L.psattn_profile_enable.argtypes = [i32]
     L.psattn_profile_read.argtypes = [vp, vp, i32]
     L.psattn_synth_direction.argtypes = [C.POINTER(SynthParams), i64, vp]
@@ -128,6 +130,7 @@ EXPORTED = [
     "psattn_pool_put_blocks", "psattn_pool_build_metadata", "psattn_pool_read_metadata",
     "psattn_batch_workspace_bytes", "psattn_run_batch", "psattn_batch_union_blocks", "psattn_batch_last_launches",
     "psattn_profile_enable", "psattn_profile_read", "psattn_set_progressive_kernel",
+    "psattn_set_score_kernel", "psattn_set_pipeline",
     "psattn_synth_direction", "psattn_synth_query", "psattn_synth_unit_host", "psattn_synth_is_planted",
     "psattn_pool_fill_synthetic",
 ]

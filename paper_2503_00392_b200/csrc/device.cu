@@ -399,6 +399,18 @@ int psattn_set_progressive_kernel(int32_t mode) {
     return PSATTN_OK;
 }
 
+int psattn_set_score_kernel(int32_t mode) {
+    if (mode < 0 || mode > 2) return fail(PSATTN_ERR_INVALID_ARGUMENT, "score kernel mode must be 0, 1 or 2");
+    set_score_kernel_choice(mode);
+    return PSATTN_OK;
+}
+
+int psattn_set_pipeline(int32_t sub_batches) {
+    if (sub_batches < 0 || sub_batches > 16) return fail(PSATTN_ERR_INVALID_ARGUMENT, "sub_batches must be in [0, 16]");
+    set_pipeline_subbatches(sub_batches);
+    return PSATTN_OK;
+}
+
 int psattn_profile_enable(int32_t enable) {
     std::lock_guard<std::mutex> lk(g_prof.mu);
     g_prof.on = enable != 0;

@@ -63,6 +63,8 @@ bool gqa_supported(const PoolView& p, const BatchView& b);
 void launch_gqa(const PoolView& p, const BatchView& b, cudaStream_t st);
 // 0 = auto (GQA kernel when supported), 1 = per-query kernel, 2 = GQA kernel
 void set_psa_kernel_choice(int choice);
+void set_score_kernel_choice(int choice);
+void set_pipeline_subbatches(int k);
 // Returns the number of kernel launches issued, or -1 on error (cudaGetLastError has it).
 int launch_batch(const PoolView& p, const BatchView& b, cudaStream_t st, cudaEvent_t* marks = nullptr);
 cudaError_t launch_union(const BatchView& b, int64_t* out_union, cudaStream_t st);

@@ -444,9 +444,12 @@ static void launch_score_g(const PoolView& p, const BatchView& b, dim3 grid, cud
     }
 }
 
+static int g_score_choice = 0;
+void set_score_kernel_choice(int choice) { g_score_choice = choice; }
+
 template <typename KV>
 static void launch_score(const PoolView& p, const BatchView& b, dim3 grid, cudaStream_t st) {
-    if (b.d == 128 && p.meta_bytes == 128 * 4 + 2 * 128 * (int64_t)sizeof(KV)) {  // TMA-staged production path
+    if (g_score_choice != 1 && b.d == 128 && p.meta_bytes == 128 * 4 + 2 * 128 * (int64_t)sizeof(KV)) {  // TMA path
         if (g_for(b.g) == 4) launch_score_tma<KV, 4>(p, b, grid, st);
         else launch_score_tma<KV, 8>(p, b, grid, st);
         return;
@@ -464,36 +467,105 @@ static void launch_oracle(const PoolView& p, const BatchView& b, dim3 grid, cuda
     }
 }
 
+static int g_pipeline = 0;  // 0 auto, 1 off, k > 1: k sub-batches
+void set_pipeline_subbatches(int k) { g_pipeline = k; }
+
+// Units [u0, u0 + cnt) of a batch: unit-indexed arrays are offset, the workspace
+// (keys / ranked positions / masses, indexed by absolute list offsets) is shared.
+static BatchView sub_view(const BatchView& b, int u0, int cnt) {
+    BatchView v = b;
+    const size_t qo = (size_t)u0 * b.g;
+    v.n_units = cnt;
+    v.q = b.q + qo * b.d;
+    v.list_off = b.list_off + u0;
+    v.out = b.out + qo * b.d;
+    v.bp = b.bp + qo;
+    v.est = b.est + qo;
+    v.tcov = b.tcov ? b.tcov + qo : nullptr;
+    v.term = b.term + qo;
+    return v;
+}
+
+static void launch_score_stage(const PoolView& p, const BatchView& b, cudaStream_t st) {
+    // enough CTAs for ~2 waves of 2 CTAs/SM, never more warps than record groups
+    const int64_t groups = (b.max_n + 3) / 4;
+    int64_t gx = (2LL * 2 * num_sms() + b.n_units - 1) / b.n_units;
+    const int64_t gx_max = (groups + kScoreWarps - 1) / kScoreWarps;
+    if (gx > gx_max) gx = gx_max;
+    if (gx < 1) gx = 1;
+    dim3 grid((unsigned)gx, (unsigned)b.n_units);
+    if (p.dtype == 0) launch_score<float>(p, b, grid, st);
+    else launch_score<__nv_bfloat16>(p, b, grid, st);
+}
+
+struct PipeResources {
+    cudaStream_t aux = nullptr;
+    cudaEvent_t ev[17] = {};
+    bool ok = false;
+};
+
+static PipeResources& pipe_resources() {
+    static PipeResources r;
+    if (!r.ok) {
+        if (cudaStreamCreateWithFlags(&r.aux, cudaStreamNonBlocking) != cudaSuccess) return r;
+        for (auto& e : r.ev)
+            if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return r;
+        r.ok = true;
+    }
+    return r;
+}
+
 int launch_batch(const PoolView& p, const BatchView& b, cudaStream_t st, cudaEvent_t* marks) {
     // marks (optional, 5 events): start | oracle | score | order | progressive. Ordering is
     // fused into the progressive kernel (lazy tranche selection), so the "order" stage is empty.
     int launches = 0;
+    int subs = g_pipeline == 0 ? (b.n_units >= 512 ? 8 : 1) : g_pipeline;
+    if (subs > 16) subs = 16;
+    if (subs > b.n_units) subs = b.n_units;
     if (marks) cudaEventRecord(marks[0], st);
-    if (b.has_oracle) {
-        const int64_t chunks = (b.max_n + kScoreWarps - 1) / kScoreWarps;
-        dim3 grid((unsigned)(chunks < 65535 ? (chunks > 0 ? chunks : 1) : 65535), (unsigned)b.n_units);
-        if (p.dtype == 0) launch_oracle<float>(p, b, grid, st);
-        else launch_oracle<__nv_bfloat16>(p, b, grid, st);
+    if (b.has_oracle || b.rank_oracle || subs <= 1 || !pipe_resources().ok) {
+        if (b.has_oracle) {
+            const int64_t chunks = (b.max_n + kScoreWarps - 1) / kScoreWarps;
+            dim3 grid((unsigned)(chunks < 65535 ? (chunks > 0 ? chunks : 1) : 65535), (unsigned)b.n_units);
+            if (p.dtype == 0) launch_oracle<float>(p, b, grid, st);
+            else launch_oracle<__nv_bfloat16>(p, b, grid, st);
+            ++launches;
+        }
+        if (marks) cudaEventRecord(marks[1], st);
+        if (!b.rank_oracle) {
+            launch_score_stage(p, b, st);
+            ++launches;
+        }
+        if (marks) cudaEventRecord(marks[2], st);
+        if (marks) cudaEventRecord(marks[3], st);
+        launch_psa(p, b, st);
         ++launches;
+        if (marks) cudaEventRecord(marks[4], st);
+    } else {
+        // Two-stream pipeline over sub-batches of units: score(i+1) streams metadata from HBM
+        // on `st` while progressive(i) runs on the auxiliary stream. Stream-ordered (events),
+        // no host synchronisation; the caller's stream joins the auxiliary one at the end.
+        PipeResources& r = pipe_resources();
+        if (marks) cudaEventRecord(marks[1], st);
+        cudaEventRecord(r.ev[0], st);
+        cudaStreamWaitEvent(r.aux, r.ev[0], 0);
+        const int per = (b.n_units + subs - 1) / subs;
+        int i = 0;
+        for (int u0 = 0; u0 < b.n_units; u0 += per, ++i) {
+            const int cnt = (b.n_units - u0) < per ? (b.n_units - u0) : per;
+            const BatchView v = sub_view(b, u0, cnt);
+            launch_score_stage(p, v, st);
+            cudaEventRecord(r.ev[1 + i], st);
+            cudaStreamWaitEvent(r.aux, r.ev[1 + i], 0);
+            launch_psa(p, v, r.aux);
+            launches += 2;
+        }
+        if (marks) cudaEventRecord(marks[2], st);  // score chain done (progressive overlapped)
+        if (marks) cudaEventRecord(marks[3], st);
+        cudaEventRecord(r.ev[0], r.aux);
+        cudaStreamWaitEvent(st, r.ev[0], 0);
+        if (marks) cudaEventRecord(marks[4], st);  // exposed progressive tail
     }
-    if (marks) cudaEventRecord(marks[1], st);
-    if (!b.rank_oracle) {
-        // enough CTAs for ~2 waves of 2 CTAs/SM, never more warps than record groups
-        const int64_t groups = (b.max_n + 3) / 4;
-        int64_t gx = (2LL * 2 * num_sms() + b.n_units - 1) / b.n_units;
-        const int64_t gx_max = (groups + kScoreWarps - 1) / kScoreWarps;
-        if (gx > gx_max) gx = gx_max;
-        if (gx < 1) gx = 1;
-        dim3 grid((unsigned)gx, (unsigned)b.n_units);
-        if (p.dtype == 0) launch_score<float>(p, b, grid, st);
-        else launch_score<__nv_bfloat16>(p, b, grid, st);
-        ++launches;
-    }
-    if (marks) cudaEventRecord(marks[2], st);
-    if (marks) cudaEventRecord(marks[3], st);
-    launch_psa(p, b, st);
-    ++launches;
-    if (marks) cudaEventRecord(marks[4], st);
     if (cudaPeekAtLastError() != cudaSuccess) return -1;
     return launches;
 }

@@ -292,3 +292,23 @@ def test_c1_shape_full_parity(mods, oracle, ref):
                     check_parity(oracle, qs[u][h], bs, make_config(epsilon=0.95), 0, gpu_ids, r["bp"], r["out"],
                                  r["est"])
         assert exact >= len(units) * g - 1
+
+
+@pytest.mark.parametrize("subs", [2, 5])
+def test_pipelined_launch_identical(mods, subs):
+    """Score/progressive overlap over sub-batches (psattn_set_pipeline) gives bit-identical results."""
+    capi, _ = mods
+    rng = np.random.default_rng(77 + subs)
+    d, T, g = 128, 16, 4
+    units = [random_blockset(rng, int(rng.integers(20, 200)), d, 1, 16, planted_frac=0.05) for _ in range(11)]
+    qs = [[rng.standard_normal(d).astype(np.float32) * 2 for _ in range(g)] for _ in units]
+    res = {}
+    for mode in (1, subs):
+        assert capi.lib.psattn_set_pipeline(mode) == 0
+        try:
+            _, run, off = run_units(mods, units, qs, T, epsilon=0.9)
+        finally:
+            capi.lib.psattn_set_pipeline(0)
+        res[mode] = (run.out.cpu().numpy(), run.bp.cpu().numpy(), run.est.cpu().numpy())
+    for a, b in zip(res[1], res[subs]):
+        assert a.tobytes() == b.tobytes()
