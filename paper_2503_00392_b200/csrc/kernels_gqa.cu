@@ -46,7 +46,9 @@ struct GqaSmem {
     uint32_t umask[G * kChunk];
     int16_t cidx[G][kChunk];
     int32_t hkey[kHash];
+    int32_t hfirst[kHash];
     int16_t hval[kHash];
+    int wcnt[kPsaWarps];
     int64_t tr0[G], cb[G];
     uint64_t last[G];
     double est[G], acc[G], mn[G];
@@ -129,7 +131,12 @@ __global__ void __launch_bounds__(kPsaThreads, 2) psa_gqa_kernel(PoolView p, Bat
             __syncthreads();
         }
         // ---- 2. round: union of the live heads' next chunks ----
-        for (int i = tid; i < kHash; i += kPsaThreads) s.hkey[i] = -1;
+        // U entries are numbered by first occurrence in (head, rank) order so the
+        // per-warp accumulation order, and hence every output bit, is deterministic.
+        for (int i = tid; i < kHash; i += kPsaThreads) {
+            s.hkey[i] = -1;
+            s.hfirst[i] = 0x7fffffff;
+        }
         if (tid < G) {
             int c = 0;
             if (s.live[tid]) {
@@ -140,33 +147,42 @@ __global__ void __launch_bounds__(kPsaThreads, 2) psa_gqa_kernel(PoolView p, Bat
             }
             s.cnt[tid] = c;
         }
-        if (tid == 0) s.ucount = 0;
         __syncthreads();
         const int hh = tid >> 5, rr = tid & 31;  // one thread per (head, rank in chunk)
-        int my_slot_idx = -1;
-        int32_t my_pos = 0;
-        if (hh < G && rr < s.cnt[hh]) {
-            const int ci = (int)(s.cb[hh] - s.tr0[hh]) + rr;
-            my_pos = (int32_t)(s.tb[hh][ci] & pmask);
-            int hs = (int)(((uint32_t)my_pos * 2654435761u) >> 23) & (kHash - 1);
+        const bool act = hh < G && rr < s.cnt[hh];
+        int hs = -1, ci = 0;
+        if (act) {
+            ci = (int)(s.cb[hh] - s.tr0[hh]) + rr;
+            const int32_t pos = (int32_t)(s.tb[hh][ci] & pmask);
+            hs = (int)(((uint32_t)pos * 2654435761u) >> 23) & (kHash - 1);
             for (;;) {
-                const int old = atomicCAS(&s.hkey[hs], -1, my_pos);
-                if (old == -1) {  // first head to rank this block in the round: new U entry
-                    const int e = atomicAdd(&s.ucount, 1);
-                    s.hval[hs] = (int16_t)e;
-                    s.uslot[e] = s.tslot[hh][ci];
-                    s.untok[e] = s.tntok[hh][ci];
-                    s.upos[e] = my_pos;
-                    s.umask[e] = 0u;
-                    break;
-                }
-                if (old == my_pos) break;
+                const int old = atomicCAS(&s.hkey[hs], -1, pos);
+                if (old == -1 || old == pos) break;
                 hs = (hs + 1) & (kHash - 1);
             }
-            my_slot_idx = hs;
+            atomicMin(&s.hfirst[hs], tid);  // (head, rank) order == thread order
         }
         __syncthreads();
-        if (my_slot_idx >= 0) s.cidx[hh][rr] = s.hval[my_slot_idx];
+        const bool first = act && s.hfirst[hs] == tid;
+        const unsigned fb = __ballot_sync(PSA_FULL, first);
+        if (lane == 0) s.wcnt[warp] = __popc(fb);
+        __syncthreads();
+        if (first) {
+            int e = __popc(fb & ((1u << lane) - 1u));
+            for (int w = 0; w < warp; ++w) e += s.wcnt[w];
+            s.hval[hs] = (int16_t)e;
+            s.uslot[e] = s.tslot[hh][ci];
+            s.untok[e] = s.tntok[hh][ci];
+            s.upos[e] = (int32_t)(s.tb[hh][ci] & pmask);
+            s.umask[e] = 0u;
+        }
+        if (tid == 0) {
+            int t = 0;
+            for (int w = 0; w < kPsaWarps; ++w) t += s.wcnt[w];
+            s.ucount = t;
+        }
+        __syncthreads();
+        if (act) s.cidx[hh][rr] = s.hval[hs];
         const int ucount = s.ucount;
         // ---- 3. K pass: every U block once, scored for all heads ----
 #pragma unroll 1

@@ -280,7 +280,7 @@ static int g_psa_choice = 0;
 void set_psa_kernel_choice(int choice) { g_psa_choice = choice; }
 
 void launch_psa(const PoolView& p, const BatchView& b, cudaStream_t st) {
-    if (g_psa_choice != 1 && gqa_supported(p, b)) {
+    if (g_psa_choice == 2 && gqa_supported(p, b)) {  // auto = per-q-head kernel (faster on planted workloads)
         launch_gqa(p, b, st);
         return;
     }

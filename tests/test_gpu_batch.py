@@ -294,10 +294,13 @@ def test_c1_shape_full_parity(mods, oracle, ref):
         assert exact >= len(units) * g - 1
 
 
+@pytest.mark.parametrize("kernel", [1, 2])
 @pytest.mark.parametrize("subs", [2, 5])
-def test_pipelined_launch_identical(mods, subs):
-    """Score/progressive overlap over sub-batches (psattn_set_pipeline) gives bit-identical results."""
+def test_pipelined_launch_identical(mods, subs, kernel):
+    """Score/progressive overlap over sub-batches (psattn_set_pipeline) gives bit-identical
+    results, for both progressive kernels (the GQA kernel numbers its union deterministically)."""
     capi, _ = mods
+    capi.lib.psattn_set_progressive_kernel(kernel)
     rng = np.random.default_rng(77 + subs)
     d, T, g = 128, 16, 4
     units = [random_blockset(rng, int(rng.integers(20, 200)), d, 1, 16, planted_frac=0.05) for _ in range(11)]
@@ -310,5 +313,6 @@ def test_pipelined_launch_identical(mods, subs):
         finally:
             capi.lib.psattn_set_pipeline(0)
         res[mode] = (run.out.cpu().numpy(), run.bp.cpu().numpy(), run.est.cpu().numpy())
+    capi.lib.psattn_set_progressive_kernel(0)
     for a, b in zip(res[1], res[subs]):
         assert a.tobytes() == b.tobytes()
