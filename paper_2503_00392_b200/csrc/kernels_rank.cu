@@ -41,7 +41,8 @@ static int num_sms() {
 constexpr int kScoreWarps = 8;
 // records per warp iteration: 4 for the d=128 / g<=4 path, fewer where registers would spill
 template <int G, int DPL> struct RecsPer {
-    static constexpr int v = (G * DPL <= 16) ? 4 : (G * DPL <= 32) ? 2 : 1;
+    static constexpr int r = (G * DPL <= 16) ? 4 : (G * DPL <= 32) ? 2 : 1;
+    static constexpr int v = (G * r <= 16) ? r : 16 / G;  // G*v <= 16: the reduction scratch fits
 };
 
 __device__ __forceinline__ double f32_scaled(uint32_t u) {  // = float(u) * 2^-896, exact
@@ -95,6 +96,27 @@ template <> struct MetaRow<__nv_bfloat16> {
     }
 };
 
+// Cross-lane reduction of N per-lane doubles through a shared-memory transpose
+// (cheaper than a shuffle reduce-scatter: no selects, 2 wavefronts per 64-bit
+// access is optimal anyway). red: this warp's 32*N-double scratch. Returns the
+// warp total of value index lane / (32/N) (on all 32/N lanes that own it).
+template <int N>
+__device__ __forceinline__ double smem_reduce(double (&acc)[N], double* red, int lane) {
+    constexpr int P = 32 / N;  // lanes per value
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < N; i += 2)
+        *reinterpret_cast<double2*>(&red[lane * N + i]) = make_double2(acc[i], acc[i + 1]);
+    __syncwarp();
+    const int v = lane / P, part = lane % P;
+    double t = 0.0;
+#pragma unroll
+    for (int k = 0; k < N; ++k) t += red[(part * N + k) * N + v];
+#pragma unroll
+    for (int o = 1; o < P; o <<= 1) t += __shfl_xor_sync(PSA_FULL, t, o);
+    return t;
+}
+
 template <typename KV, int G, int DPL, bool FULL>
 __global__ void __launch_bounds__(kScoreWarps * 32, 2) score_kernel(PoolView p, BatchView b) {
     constexpr int kRecs = RecsPer<G, DPL>::v;
@@ -103,6 +125,8 @@ __global__ void __launch_bounds__(kScoreWarps * 32, 2) score_kernel(PoolView p, 
     constexpr int WKV = MetaRow<KV>::template words<DPL>();
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
+    __shared__ __align__(16) double red_all[kScoreWarps][32 * N];
+    double* red = red_all[warp];
     const int u = blockIdx.y;
     const int64_t off = b.list_off[u];
     const int64_t n = b.list_off[u + 1] - off;
@@ -181,7 +205,7 @@ __global__ void __launch_bounds__(kScoreWarps * 32, 2) score_kernel(PoolView p, 
                 }
             }
         }
-        const double tot = reduce_scatter_d<N>(acc, lane);
+        const double tot = smem_reduce<N>(acc, red, lane);
         if (writer && p0 + my_j < n) {
             const double s = est == 2 ? 0.5 * (tot * scale) : tot * scale;
             keys[p0 + my_j] = make_key(s, (uint32_t)(p0 + my_j), b.pos_bits);
@@ -265,9 +289,16 @@ __global__ void __launch_bounds__(kScoreWarps * 32, 2) score_kernel_tma(PoolView
     }
     int stage = 0;
     uint32_t phase = 0;
+    // slot ids of refill groups are fetched two iterations before their copies are issued
+    auto slot_of = [&](int64_t g) -> int32_t {
+        return (g < ngroups && lane < kRecs && g * kRecs + lane < n) ? b.slots[off + g * kRecs + lane] : 0;
+    };
+    int32_t pf0 = slot_of(grp0 + S * nwarps), pf1 = slot_of(grp0 + (S + 1) * nwarps);
     for (int64_t grp = grp0; grp < ngroups; grp += nwarps) {
         const int64_t gn = grp + S * nwarps;  // group that refills this stage
-        const int32_t nslot = (gn < ngroups && lane < kRecs && gn * kRecs + lane < n) ? b.slots[off + gn * kRecs + lane] : 0;
+        const int32_t nslot = pf0;
+        pf0 = pf1;
+        pf1 = slot_of(grp + (S + 2) * nwarps);
         mbar_wait(&wbar[stage], phase);
         const unsigned char* sb = wbuf + stage * STAGE;
         double acc[N];
@@ -316,7 +347,7 @@ __global__ void __launch_bounds__(kScoreWarps * 32, 2) score_kernel_tma(PoolView
         fence_proxy_async();
         __syncwarp();
         if (gn < ngroups) issue(gn, stage, nslot);
-        const double tot = reduce_scatter_d<N>(acc, lane);
+        const double tot = smem_reduce<N>(acc, reinterpret_cast<double*>(smem + kTmaBarBytes + (size_t)kScoreWarps * S * STAGE) + warp * 32 * N, lane);
         const int64_t p0 = grp * kRecs;
         if (writer && p0 + my_j < n) {
             const double sc = est == 2 ? 0.5 * (tot * scale) : tot * scale;
@@ -334,7 +365,7 @@ static size_t tma_smem_bytes() {
     constexpr int kRecs = RecsPer<G, 4>::v;
     constexpr int STAGE = kRecs * (128 * 4 + 2 * 128 * (int)sizeof(KV));
     constexpr int S = (12288 / STAGE) < 2 ? 2 : ((12288 / STAGE) > 4 ? 4 : (12288 / STAGE));
-    return kTmaBarBytes + (size_t)kScoreWarps * S * STAGE;
+    return kTmaBarBytes + (size_t)kScoreWarps * S * STAGE + (size_t)kScoreWarps * 32 * (G * kRecs) * 8;
 }
 
 template <typename KV, int G>
