@@ -73,6 +73,16 @@ int psattn_pool_put_blocks(psattn_pool* pool, int64_t n, const int32_t* slots, c
 /* Rebuilds metadata (lo/hi/mean) for slots [slot_begin, slot_end) on device. */
 int psattn_pool_build_metadata(psattn_pool* pool, int64_t slot_begin, int64_t slot_end, void* stream);
 
+/* Decode-step KV append + metadata maintenance (the step right before the path
+ * every decode step): for i < n, writes one token's K and V (device fp32 [n][dim]
+ * each) at row ntok of slot tail_slots[i] (device int32 [n]), increments ntok and
+ * rebuilds that slot's metadata on `stream` (reference put_block/build_metadata,
+ * store.cpp:59-78, metadata.cpp:8-34). A slot already holding block_tokens rows is
+ * left untouched and *status (device int32, caller-zeroed) is set to 1: the caller
+ * opens a new slot for that sequence. */
+int psattn_pool_append_tokens(psattn_pool* pool, int32_t n, const int32_t* tail_slots, const float* keys,
+                              const float* values, int32_t* status, void* stream);
+
 /* Copies back metadata of one slot as fp32 (mean, lo, hi: dim floats each). */
 int psattn_pool_read_metadata(psattn_pool* pool, int64_t slot, float* mean, float* lo, float* hi);
 

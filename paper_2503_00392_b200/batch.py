@@ -63,6 +63,15 @@ class DevicePool:
     def build_metadata(self, s0, s1, stream=None):
         check(lib.psattn_pool_build_metadata(self.h, s0, s1, _stream_ptr(stream)))
 
+    def append_tokens(self, tail_slots: torch.Tensor, keys: torch.Tensor, values: torch.Tensor, stream=None) -> int:
+        """One decode step's KV append (device tensors): int32 [n] tail slots, fp32 [n, dim] K and V.
+        Returns 1 if some tail slot was already full (that sequence's token was not written)."""
+        status = torch.zeros(1, dtype=torch.int32, device=keys.device)
+        check(lib.psattn_pool_append_tokens(self.h, int(tail_slots.numel()), _dp(tail_slots.contiguous()),
+                                            _dp(keys.contiguous()), _dp(values.contiguous()), _dp(status),
+                                            _stream_ptr(stream)))
+        return int(status.item())
+
     def read_metadata(self, slot):
         m, lo, hi = (np.zeros(self.dim, np.float32) for _ in range(3))
         check(lib.psattn_pool_read_metadata(self.h, slot, capi._p(m), capi._p(lo), capi._p(hi)))

@@ -101,6 +101,7 @@ def _load() -> C.CDLL:
     L.psattn_pool_put_blocks.argtypes = [vp, i64, vp, vp, vp, vp]
     L.psattn_pool_build_metadata.argtypes = [vp, i64, i64, vp]
     L.psattn_pool_read_metadata.argtypes = [vp, i64, vp, vp, vp]
+    L.psattn_pool_append_tokens.argtypes = [vp, i32, vp, vp, vp, vp, vp]
     L.psattn_batch_workspace_bytes.argtypes = [C.POINTER(Batch)]
     L.psattn_batch_workspace_bytes.restype = sz
     L.psattn_run_batch.argtypes = [vp, C.POINTER(Batch), vp, vp]
@@ -128,6 +129,7 @@ EXPORTED = [
     "psattn_store_stats", "psattn_config_default", "psattn_run_query", "psattn_run_topk",
     "psattn_pool_create", "psattn_pool_destroy", "psattn_pool_get_desc", "psattn_pool_get_layout",
     "psattn_pool_put_blocks", "psattn_pool_build_metadata", "psattn_pool_read_metadata",
+    "psattn_pool_append_tokens",
     "psattn_batch_workspace_bytes", "psattn_run_batch", "psattn_batch_union_blocks", "psattn_batch_last_launches",
     "psattn_profile_enable", "psattn_profile_read", "psattn_set_progressive_kernel",
     "psattn_set_score_kernel", "psattn_set_pipeline",

@@ -358,6 +358,15 @@ int psattn_pool_build_metadata(psattn_pool* pool, int64_t slot_begin, int64_t sl
     return e == cudaSuccess ? PSATTN_OK : cuda_fail(e, "metadata build");
 }
 
+int psattn_pool_append_tokens(psattn_pool* pool, int32_t n, const int32_t* tail_slots, const float* keys,
+                              const float* values, int32_t* status, void* stream) {
+    if (!pool || !tail_slots || !keys || !values || !status)
+        return fail(PSATTN_ERR_INVALID_ARGUMENT, "psattn_pool_append_tokens: null argument");
+    if (n < 0) return fail(PSATTN_ERR_INVALID_ARGUMENT, "psattn_pool_append_tokens: n must be >= 0");
+    cudaError_t e = launch_append(pool->v, n, tail_slots, keys, values, status, (cudaStream_t)stream);
+    return e == cudaSuccess ? PSATTN_OK : cuda_fail(e, "append tokens");
+}
+
 int psattn_pool_read_metadata(psattn_pool* pool, int64_t slot, float* mean, float* lo, float* hi) {
     if (!pool || !mean || !lo || !hi) return fail(PSATTN_ERR_INVALID_ARGUMENT, "psattn_pool_read_metadata: null");
     if (slot < 0 || slot >= pool->v.n_slots) return fail(PSATTN_ERR_INVALID_ARGUMENT, "slot out of range");

@@ -53,6 +53,8 @@ int tok_for(int T);
 int g_for(int g);
 
 cudaError_t launch_meta_build(const PoolView& p, const int32_t* list, int64_t s0, int64_t s1, cudaStream_t st);
+cudaError_t launch_append(const PoolView& p, int32_t n, const int32_t* slots, const float* keys,
+                          const float* values, int32_t* status, cudaStream_t st);
 cudaError_t launch_scatter(const PoolView& p, const void* staged, const int32_t* d_slots, const int32_t* d_ntok,
                            int64_t n, cudaStream_t st);
 cudaError_t launch_synth_fill(const PoolView& p, uint64_t seed, float skew, float prob, int round_bf16,

@@ -66,6 +66,67 @@ cudaError_t launch_meta_build(const PoolView& p, const int32_t* list, int64_t s0
     return cudaGetLastError();
 }
 
+// Decode-step KV append: sequence i writes one token's K and V
+// (fp32, converted to the pool dtype) at row ntok[slot] of its tail slot, then
+// the slot's metadata is rebuilt over its rows exactly like K1 (reference
+// put_block -> build_metadata, store.cpp:59-78, metadata.cpp:8-34). One warp per
+// sequence; rows past ntok stay zero so the progressive kernel's unmasked loads
+// remain finite.
+template <typename KV>
+__global__ void append_tokens_kernel(PoolView p, int32_t n, const int32_t* __restrict__ slots,
+                                     const float* __restrict__ keys, const float* __restrict__ values,
+                                     int32_t* __restrict__ status) {
+    const int lane = threadIdx.x & 31;
+    const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (i >= n) return;
+    const int64_t slot = slots[i];
+    const int d = p.d;
+    const int row = p.ntok[slot];
+    if (row >= p.T) {  // full block: the caller must open a new slot
+        if (lane == 0) atomicExch(status, 1);
+        return;
+    }
+    KV* k = reinterpret_cast<KV*>(p.kv + slot * p.slot_bytes);
+    KV* v = k + (size_t)p.T * d;
+    for (int j = lane; j < d; j += 32) {
+        k[(size_t)row * d + j] = KVT<KV>::from_f(keys[(size_t)i * d + j]);
+        v[(size_t)row * d + j] = KVT<KV>::from_f(values[(size_t)i * d + j]);
+    }
+    __syncwarp();
+    const int nt = row + 1;
+    char* rec = p.meta + slot * p.meta_bytes;
+    float* mean = reinterpret_cast<float*>(rec);
+    KV* lo = reinterpret_cast<KV*>(rec + (size_t)d * 4);
+    KV* hi = reinterpret_cast<KV*>(rec + (size_t)d * 4 + (size_t)d * sizeof(KV));
+    for (int j = lane; j < d; j += 32) {
+        float l = KVT<KV>::to_f(k[j]);
+        float h = l;
+        double sm = l;
+        for (int t = 1; t < nt; ++t) {
+            const float x = KVT<KV>::to_f(k[(size_t)t * d + j]);
+            l = (x < l) ? x : l;
+            h = (h < x) ? x : h;
+            sm = __dadd_rn(sm, (double)x);
+        }
+        mean[j] = __double2float_rn(__ddiv_rn(sm, (double)nt));
+        lo[j] = KVT<KV>::from_f(l);
+        hi[j] = KVT<KV>::from_f(h);
+    }
+    if (lane == 0) p.ntok[slot] = nt;
+}
+
+cudaError_t launch_append(const PoolView& p, int32_t n, const int32_t* slots, const float* keys,
+                          const float* values, int32_t* status, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    const int warps = 8;
+    if (p.dtype == 0)
+        append_tokens_kernel<float><<<(n + warps - 1) / warps, warps * 32, 0, st>>>(p, n, slots, keys, values, status);
+    else
+        append_tokens_kernel<__nv_bfloat16><<<(n + warps - 1) / warps, warps * 32, 0, st>>>(p, n, slots, keys, values,
+                                                                                              status);
+    return cudaGetLastError();
+}
+
 // Copies n staged slot images ([2][T][d] in the pool dtype) into pool slots and sets ntok.
 __global__ void scatter_slots_kernel(PoolView p, const char* __restrict__ staged, const int32_t* __restrict__ slots,
                                      const int32_t* __restrict__ ntok, int64_t n) {

@@ -102,16 +102,16 @@ template <> struct MetaRow<__nv_bfloat16> {
 // warp total of value index lane / (32/N) (on all 32/N lanes that own it).
 template <int N>
 __device__ __forceinline__ double smem_reduce(double (&acc)[N], double* red, int lane) {
-    constexpr int P = 32 / N;  // lanes per value
+    constexpr int P = 32 / N;   // lanes per value
+    constexpr int RS = N + 1;   // padded row: writes and reads both hit the 2-wavefront minimum
     __syncwarp();
 #pragma unroll
-    for (int i = 0; i < N; i += 2)
-        *reinterpret_cast<double2*>(&red[lane * N + i]) = make_double2(acc[i], acc[i + 1]);
+    for (int i = 0; i < N; ++i) red[lane * RS + i] = acc[i];
     __syncwarp();
     const int v = lane / P, part = lane % P;
     double t = 0.0;
 #pragma unroll
-    for (int k = 0; k < N; ++k) t += red[(part * N + k) * N + v];
+    for (int k = 0; k < N; ++k) t += red[(part * N + k) * RS + v];
 #pragma unroll
     for (int o = 1; o < P; o <<= 1) t += __shfl_xor_sync(PSA_FULL, t, o);
     return t;
@@ -125,7 +125,7 @@ __global__ void __launch_bounds__(kScoreWarps * 32, 2) score_kernel(PoolView p, 
     constexpr int WKV = MetaRow<KV>::template words<DPL>();
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
-    __shared__ __align__(16) double red_all[kScoreWarps][32 * N];
+    __shared__ __align__(16) double red_all[kScoreWarps][32 * (N + 1)];
     double* red = red_all[warp];
     const int u = blockIdx.y;
     const int64_t off = b.list_off[u];
@@ -347,7 +347,7 @@ __global__ void __launch_bounds__(kScoreWarps * 32, 2) score_kernel_tma(PoolView
         fence_proxy_async();
         __syncwarp();
         if (gn < ngroups) issue(gn, stage, nslot);
-        const double tot = smem_reduce<N>(acc, reinterpret_cast<double*>(smem + kTmaBarBytes + (size_t)kScoreWarps * S * STAGE) + warp * 32 * N, lane);
+        const double tot = smem_reduce<N>(acc, reinterpret_cast<double*>(smem + kTmaBarBytes + (size_t)kScoreWarps * S * STAGE) + warp * 32 * (N + 1), lane);
         const int64_t p0 = grp * kRecs;
         if (writer && p0 + my_j < n) {
             const double sc = est == 2 ? 0.5 * (tot * scale) : tot * scale;
@@ -365,7 +365,7 @@ static size_t tma_smem_bytes() {
     constexpr int kRecs = RecsPer<G, 4>::v;
     constexpr int STAGE = kRecs * (128 * 4 + 2 * 128 * (int)sizeof(KV));
     constexpr int S = (12288 / STAGE) < 2 ? 2 : ((12288 / STAGE) > 4 ? 4 : (12288 / STAGE));
-    return kTmaBarBytes + (size_t)kScoreWarps * S * STAGE + (size_t)kScoreWarps * 32 * (G * kRecs) * 8;
+    return kTmaBarBytes + (size_t)kScoreWarps * S * STAGE + (size_t)kScoreWarps * 32 * (G * kRecs + 1) * 8;
 }
 
 template <typename KV, int G>
