@@ -8,6 +8,8 @@
 #include "kernels.cuh"
 #include "psa_order.cuh"
 
+#include <type_traits>
+
 namespace psa {
 
 // =============================================================================
@@ -54,6 +56,74 @@ struct PsaSmem {
     float m[kPsaWarps], l[kPsaWarps];
 };
 
+// ---- tensor-core K pass (bf16 pools, d = 128, 16-token blocks) -------------
+// S[token][c] = sum_k K[token][k] * Qs[k][c] with Qs = [q1 q2 q3 0..] the exact
+// 3-term bf16 split of the fp32 query (q1 = bf16(q), q2 = bf16(q - q1),
+// q3 = bf16(q - q1 - q2), q1 + q2 + q3 == q): bf16 x bf16 products are exact in
+// the fp32 accumulator, so one mma.sync.m16n8k16 per 16 dims replaces 16x16
+// FFMAs, 64 bf16->fp32 conversions and the cross-lane reduction. Dims are
+// permuted (the sum over k is order-free) so thread (g = lane/4, t = lane%4)
+// owns dims [32t, 32t+32) of token rows g and g+8: 8 x 128-bit loads per block.
+__device__ __forceinline__ void mma_bf16_16816(float& c0, float& c1, float& c2, float& c3, uint32_t a0, uint32_t a1,
+                                               uint32_t a2, uint32_t a3, uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};\n"
+        : "+f"(c0), "+f"(c1), "+f"(c2), "+f"(c3)
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ uint32_t bf16_bits(float x) { return (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(x)); }
+
+// B fragments of the split query for the 8 k-steps: qb[s][0] = (k 2t, 2t+1), qb[s][1] = (k 2t+8, 2t+9), col g.
+__device__ __forceinline__ void build_q_frags(const float* __restrict__ qrow, int lane, uint32_t (&qb)[8][2]) {
+    const int g = lane >> 2, t = lane & 3;
+#pragma unroll
+    for (int st = 0; st < 8; ++st) {
+#pragma unroll
+        for (int hf = 0; hf < 2; ++hf) {
+            uint32_t packed = 0;
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const float x = qrow[32 * t + 4 * st + 2 * hf + e];
+                const float x1 = __bfloat162float(__float2bfloat16_rn(x));
+                const float r1 = x - x1;
+                const float x2 = __bfloat162float(__float2bfloat16_rn(r1));
+                const float r2 = r1 - x2;
+                const float part = g == 0 ? x : (g == 1 ? r1 : (g == 2 ? r2 : 0.0f));
+                packed |= bf16_bits(part) << (16 * e);
+            }
+            qb[st][hf] = packed;
+        }
+    }
+}
+
+// Scores of one 16-token block: returns (token g, token g+8) on lanes with t < 2.
+__device__ __forceinline__ void block_scores_mma(const __nv_bfloat16* __restrict__ kblk, int T, int lane,
+                                                 const uint32_t (&qb)[8][2], float& s_lo, float& s_hi) {
+    const int g = lane >> 2, t = lane & 3;
+    const int r0 = g < T ? g : T - 1, r1 = (g + 8) < T ? (g + 8) : T - 1;
+    const uint4* p0 = reinterpret_cast<const uint4*>(kblk + (size_t)r0 * 128 + 32 * t);
+    const uint4* p1 = reinterpret_cast<const uint4*>(kblk + (size_t)r1 * 128 + 32 * t);
+    uint32_t w0[16], w1[16];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const uint4 a = __ldg(p0 + i), b = __ldg(p1 + i);
+        w0[4 * i] = a.x; w0[4 * i + 1] = a.y; w0[4 * i + 2] = a.z; w0[4 * i + 3] = a.w;
+        w1[4 * i] = b.x; w1[4 * i + 1] = b.y; w1[4 * i + 2] = b.z; w1[4 * i + 3] = b.w;
+    }
+    float c0 = 0.f, c1 = 0.f, c2 = 0.f, c3 = 0.f;
+#pragma unroll
+    for (int st = 0; st < 8; ++st)
+        mma_bf16_16816(c0, c1, c2, c3, w0[2 * st], w1[2 * st], w0[2 * st + 1], w1[2 * st + 1], qb[st][0], qb[st][1]);
+    // columns 2t, 2t+1 are split terms: t=0 holds q1,q2 and t=1 holds q3 -> sum across the pair
+    float lo = c0 + c1, hi = c2 + c3;
+    lo += __shfl_xor_sync(PSA_FULL, lo, 1);
+    hi += __shfl_xor_sync(PSA_FULL, hi, 1);
+    s_lo = lo;
+    s_hi = hi;
+}
+
 template <typename KV, int DPL, int TOK, bool FULL>
 __global__ void __launch_bounds__(kPsaThreads, 3) psa_kernel(PoolView p, BatchView b) {
     __shared__ PsaSmem<TOK> s;
@@ -78,6 +148,9 @@ __global__ void __launch_bounds__(kPsaThreads, 3) psa_kernel(PoolView p, BatchVi
 
     float q[DPL];
     load_row<DPL>(b.q + ((size_t)u * b.g + h) * d + base, full, lim, q);
+    constexpr bool kMma = std::is_same<KV, __nv_bfloat16>::value && DPL == 4 && TOK == 16 && FULL;
+    uint32_t qb[8][2];
+    if constexpr (kMma) build_q_frags(b.q + ((size_t)u * b.g + h) * d, lane, qb);
 
     float M = -INFINITY, L = 0.0f, O[DPL];  // warp-local online-softmax state
 #pragma unroll
@@ -118,6 +191,31 @@ __global__ void __launch_bounds__(kPsaThreads, 3) psa_kernel(PoolView p, BatchVi
             if (rl >= cnt) break;
             const int32_t slot = s.tslot[ci + rl];
             const int nt = s.tntok[ci + rl];
+            if constexpr (kMma) {
+                float slo, shi;
+                block_scores_mma(kv + (int64_t)slot * slot_elems, T, lane, qb, slo, shi);
+                const int g8 = lane >> 2;
+                slo = (g8 < nt) ? slo * fscale : -INFINITY;
+                shi = (g8 + 8 < nt) ? shi * fscale : -INFINITY;
+                float mb = fmaxf(slo, shi);
+#pragma unroll
+                for (int o = 4; o < 32; o <<= 1) mb = fmaxf(mb, __shfl_xor_sync(PSA_FULL, mb, o));
+                const float wlo = (g8 < nt) ? expf(slo - mb) : 0.0f;
+                const float whi = (g8 + 8 < nt) ? expf(shi - mb) : 0.0f;
+                float lb = wlo + whi;
+#pragma unroll
+                for (int o = 4; o < 32; o <<= 1) lb += __shfl_xor_sync(PSA_FULL, lb, o);
+                if ((lane & 3) == 0) {
+                    s.w[warp][j][g8] = wlo;
+                    s.w[warp][j][g8 + 8] = whi;
+                }
+                if (lane == 0) {
+                    s.mb[warp][j] = mb;
+                    s.lb[warp][j] = lb;
+                    s.la[rl] = mb + logf(lb);
+                }
+                continue;
+            }
             const KV* kp = kv + (int64_t)slot * slot_elems + base;
             // Branch-free: rows in [ntok, T) are zero-filled in the pool and rows >= T
             // (TOK > T) re-read row T-1, so all TOK loads issue before the first use;

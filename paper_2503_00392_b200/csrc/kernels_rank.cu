@@ -231,7 +231,7 @@ __global__ void __launch_bounds__(kScoreWarps * 32, 2) score_kernel_tma(PoolView
     constexpr int SH = 5 - Log2<N>::v;
     constexpr int MB = D * 4 + 2 * D * (int)sizeof(KV);  // metadata record bytes (meta_bytes)
     constexpr int STAGE = kRecs * MB;
-    constexpr int S = (12288 / STAGE) < 2 ? 2 : ((12288 / STAGE) > 4 ? 4 : (12288 / STAGE));
+    constexpr int S = (8192 / STAGE) < 2 ? 2 : ((8192 / STAGE) > 4 ? 4 : (8192 / STAGE));  // 2 CTAs/SM incl. reduction scratch
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
     const int lane = threadIdx.x & 31;
@@ -364,7 +364,7 @@ template <typename KV, int G>
 static size_t tma_smem_bytes() {
     constexpr int kRecs = RecsPer<G, 4>::v;
     constexpr int STAGE = kRecs * (128 * 4 + 2 * 128 * (int)sizeof(KV));
-    constexpr int S = (12288 / STAGE) < 2 ? 2 : ((12288 / STAGE) > 4 ? 4 : (12288 / STAGE));
+    constexpr int S = (8192 / STAGE) < 2 ? 2 : ((8192 / STAGE) > 4 ? 4 : (8192 / STAGE));
     return kTmaBarBytes + (size_t)kScoreWarps * S * STAGE + (size_t)kScoreWarps * 32 * (G * kRecs + 1) * 8;
 }
 
