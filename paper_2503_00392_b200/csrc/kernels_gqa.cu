@@ -5,7 +5,10 @@
 
 #include "common.cuh"
 #include "kernels.cuh"
+#include "mma.cuh"
 #include "psa_order.cuh"
+
+#include <type_traits>
 
 namespace psa {
 
@@ -89,6 +92,32 @@ __global__ void __launch_bounds__(kPsaThreads, 2) psa_gqa_kernel(PoolView p, Bat
         else
 #pragma unroll
             for (int j = 0; j < DPL; ++j) q[h][j] = 0.0f;
+    }
+    // Tensor-core K pass (bf16 pools, d = 128, blocks <= 16 tokens): columns of the
+    // n8 tiles are (head, split) pairs, 4 per head (3 exact bf16 split terms + 0), so
+    // ONE set of 8 x NT mma.sync scores a block for the whole group.
+    constexpr bool kMma = std::is_same<KV, __nv_bfloat16>::value && DPL == 4 && TOK == 16 && FULL;
+    constexpr int NT = (G * 4 + 7) / 8;  // n8 tiles
+    uint32_t qg[8][NT][2];
+    if constexpr (kMma) {
+        const int gq = lane >> 2, tq = lane & 3;
+#pragma unroll
+        for (int tile = 0; tile < NT; ++tile) {
+            const int hq = tile * 2 + (gq >> 2), sp = gq & 3;
+            const float* qrow = b.q + ((size_t)u * g + (hq < g ? hq : 0)) * d;
+#pragma unroll
+            for (int st = 0; st < 8; ++st)
+#pragma unroll
+                for (int hf = 0; hf < 2; ++hf) {
+                    uint32_t packed = 0;
+#pragma unroll
+                    for (int e2 = 0; e2 < 2; ++e2) {
+                        const float x = hq < g ? bf16_split(qrow[32 * tq + 4 * st + 2 * hf + e2], sp) : 0.0f;
+                        packed |= bf16_bits(x) << (16 * e2);
+                    }
+                    qg[st][tile][hf] = packed;
+                }
+        }
     }
     if (tid < G) {
         s.tr0[tid] = 0;
@@ -189,6 +218,56 @@ __global__ void __launch_bounds__(kPsaThreads, 2) psa_gqa_kernel(PoolView p, Bat
         for (int e = warp; e < ucount; e += kPsaWarps) {
             const int32_t slot = s.uslot[e];
             const int nt = s.untok[e];
+            if constexpr (kMma) {
+                const int gq = lane >> 2, tq = lane & 3;
+                const __nv_bfloat16* kblk = reinterpret_cast<const __nv_bfloat16*>(kv + (int64_t)slot * slot_elems);
+                const int r0 = gq < T ? gq : T - 1, r1 = (gq + 8) < T ? (gq + 8) : T - 1;
+                const uint4* p0 = reinterpret_cast<const uint4*>(kblk + (size_t)r0 * 128 + 32 * tq);
+                const uint4* p1 = reinterpret_cast<const uint4*>(kblk + (size_t)r1 * 128 + 32 * tq);
+                uint32_t w0[16], w1[16];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const uint4 x0 = __ldg(p0 + i), x1 = __ldg(p1 + i);
+                    w0[4 * i] = x0.x; w0[4 * i + 1] = x0.y; w0[4 * i + 2] = x0.z; w0[4 * i + 3] = x0.w;
+                    w1[4 * i] = x1.x; w1[4 * i + 1] = x1.y; w1[4 * i + 2] = x1.z; w1[4 * i + 3] = x1.w;
+                }
+                float c[NT][4];
+#pragma unroll
+                for (int tile = 0; tile < NT; ++tile) c[tile][0] = c[tile][1] = c[tile][2] = c[tile][3] = 0.f;
+#pragma unroll
+                for (int st = 0; st < 8; ++st)
+#pragma unroll
+                    for (int tile = 0; tile < NT; ++tile)
+                        mma_bf16_16816(c[tile][0], c[tile][1], c[tile][2], c[tile][3], w0[2 * st], w1[2 * st],
+                                       w0[2 * st + 1], w1[2 * st + 1], qg[st][tile][0], qg[st][tile][1]);
+#pragma unroll
+                for (int tile = 0; tile < NT; ++tile) {
+                    float lo = c[tile][0] + c[tile][1], hi = c[tile][2] + c[tile][3];
+                    lo += __shfl_xor_sync(PSA_FULL, lo, 1);  // sum the split terms of (head, token)
+                    hi += __shfl_xor_sync(PSA_FULL, hi, 1);
+                    const int hq = tile * 2 + (tq >> 1);
+                    lo = (gq < nt) ? lo * fscale : -INFINITY;
+                    hi = (gq + 8 < nt) ? hi * fscale : -INFINITY;
+                    float mbv = fmaxf(lo, hi);
+#pragma unroll
+                    for (int o = 4; o < 32; o <<= 1) mbv = fmaxf(mbv, __shfl_xor_sync(PSA_FULL, mbv, o));
+                    const float wlo = (gq < nt) ? expf(lo - mbv) : 0.0f;
+                    const float whi = (gq + 8 < nt) ? expf(hi - mbv) : 0.0f;
+                    float lbv = wlo + whi;
+#pragma unroll
+                    for (int o = 4; o < 32; o <<= 1) lbv += __shfl_xor_sync(PSA_FULL, lbv, o);
+                    if ((tq & 1) == 0 && hq < G) {
+                        s.w[e][hq][gq] = wlo;
+                        s.w[e][hq][gq + 8] = whi;
+                        if (gq == 0) {
+                            s.mb[e][hq] = mbv;
+                            s.lb[e][hq] = lbv;
+                            s.la[e][hq] = mbv + logf(lbv);
+                        }
+                    }
+                }
+                continue;
+            }
             const KV* kp = kv + (int64_t)slot * slot_elems + base;
             float kr[TOK][DPL];
 #pragma unroll

@@ -6,6 +6,7 @@
 
 #include "common.cuh"
 #include "kernels.cuh"
+#include "mma.cuh"
 #include "psa_order.cuh"
 
 #include <type_traits>
@@ -64,17 +65,6 @@ struct PsaSmem {
 // FFMAs, 64 bf16->fp32 conversions and the cross-lane reduction. Dims are
 // permuted (the sum over k is order-free) so thread (g = lane/4, t = lane%4)
 // owns dims [32t, 32t+32) of token rows g and g+8: 8 x 128-bit loads per block.
-__device__ __forceinline__ void mma_bf16_16816(float& c0, float& c1, float& c2, float& c3, uint32_t a0, uint32_t a1,
-                                               uint32_t a2, uint32_t a3, uint32_t b0, uint32_t b1) {
-    asm volatile(
-        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-        "{%0,%1,%2,%3};\n"
-        : "+f"(c0), "+f"(c1), "+f"(c2), "+f"(c3)
-        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
-}
-
-__device__ __forceinline__ uint32_t bf16_bits(float x) { return (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(x)); }
-
 // B fragments of the split query for the 8 k-steps: qb[s][0] = (k 2t, 2t+1), qb[s][1] = (k 2t+8, 2t+9), col g.
 __device__ __forceinline__ void build_q_frags(const float* __restrict__ qrow, int lane, uint32_t (&qb)[8][2]) {
     const int g = lane >> 2, t = lane & 3;

@@ -1,0 +1,30 @@
+// mma.cuh — warp-level tensor-core helpers (mma.sync, bf16 in / fp32 accumulate).
+#pragma once
+
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+namespace psa {
+
+__device__ __forceinline__ void mma_bf16_16816(float& c0, float& c1, float& c2, float& c3, uint32_t a0, uint32_t a1,
+                                               uint32_t a2, uint32_t a3, uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};\n"
+        : "+f"(c0), "+f"(c1), "+f"(c2), "+f"(c3)
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ uint32_t bf16_bits(float x) { return (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(x)); }
+
+
+// Exact 3-term bf16 split of an fp32 value: x == x1 + x2 + x3 (split index 0..2; 3+ -> 0).
+__device__ __forceinline__ float bf16_split(float x, int part) {
+    const float x1 = __bfloat162float(__float2bfloat16_rn(x));
+    const float r1 = x - x1;
+    const float x2 = __bfloat162float(__float2bfloat16_rn(r1));
+    const float r2 = r1 - x2;
+    return part == 0 ? x : (part == 1 ? r1 : (part == 2 ? r2 : 0.0f));
+}
+
+}  // namespace psa
