@@ -51,9 +51,9 @@ def parse():
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--cpu-seconds", type=float, default=20.0, help="budget of the CPU baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--psa-kernel", type=int, default=1, help="0 auto, 1 per q-head, 2 GQA group")
-    ap.add_argument("--score-kernel", type=int, default=1, help="0 auto, 1 register-staged, 2 TMA-staged")
-    ap.add_argument("--pipeline", type=int, default=0, help="0 auto, 1 off, k sub-batches")
+    ap.add_argument("--psa-kernel", type=int, default=0, help="0 auto, 1 per q-head, 2 GQA group")
+    ap.add_argument("--score-kernel", type=int, default=0, help="0 auto, 1 register-staged, 2 TMA-staged")
+    ap.add_argument("--pipeline", type=int, default=1, help="0 auto, 1 off, k sub-batches")
     return ap.parse_args()
 
 

@@ -138,15 +138,16 @@ int psattn_batch_union_blocks(const psattn_batch* b, void* workspace, int64_t* o
 /* Number of kernels the last psattn_run_batch launched on this process. */
 int psattn_batch_last_launches(int32_t* out_count);
 
-/* Progressive-kernel selection (tuning/testing knob): 0 = auto (one CTA per
- * q-head), 1 = always per q-head, 2 = the GQA-group kernel (one CTA per kv-head
- * list, K/V of the group's union read once) when 2 <= group <= 4, dim in
- * {64,128} and blocks <= 16 tokens. Process-wide. */
+/* Progressive-kernel selection (tuning/testing knob): 0 = auto (the GQA-group
+ * kernel — one CTA per kv-head list, K/V of the group's union read once, tensor-core
+ * K pass — when 2 <= group <= 4, dim in {64,128} and blocks <= 16 tokens; else one
+ * CTA per q-head), 1 = always per q-head, 2 = GQA kernel whenever supported. */
 int psattn_set_progressive_kernel(int32_t mode);
 /* Score/progressive overlap: psattn_run_batch splits a batch of >= 512 units into
  * sub-batches and runs score(i+1) on the caller's stream while progressive(i) runs on
  * an internal stream joined back by events (stream-ordered, no host sync).
- * 0 = auto (8 sub-batches when n_units >= 512), 1 = off, k = k sub-batches (<= 16). */
+ * 0 = auto (currently off: measured no gain, both stages are SM-bound), 1 = off,
+ * k = k sub-batches (<= 16). */
 int psattn_set_pipeline(int32_t sub_batches);
 /* Score-kernel selection: 0 = auto (TMA-staged for dim 128), 1 = register-staged, 2 = TMA whenever supported. */
 int psattn_set_score_kernel(int32_t mode);

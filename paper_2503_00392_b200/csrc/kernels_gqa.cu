@@ -32,13 +32,14 @@ namespace psa {
 // =============================================================================
 constexpr int kGTCap = 512;   // tranche capacity per head
 constexpr int kHash = 512;    // pos -> U index (>= 2 * G * kChunk)
+constexpr int kGBins = 1024;  // bucket-select bins per head team
 
 template <int TOK, int G>
 struct GqaSmem {
     uint64_t tb[G][kGTCap];
     int32_t tslot[G][kGTCap];
     uint8_t tntok[G][kGTCap];
-    uint32_t hist[kBins];
+    uint32_t hist[G][kGBins];
     float w[G * kChunk][G][TOK];   // per (U entry, head) token weights exp(s - m)
     float mb[G * kChunk][G], lb[G * kChunk][G], la[G * kChunk][G];
     float o[kPsaWarps][G][128];    // per-warp, per-head output accumulators (d <= 128)
@@ -57,7 +58,7 @@ struct GqaSmem {
     double est[G], acc[G], mn[G];
     int tc[G], cnt[G], commit[G], fin[G], live[G];
     int ucount, nlive;
-    SelScratch sel;
+    SelScratch sel[G];
 };
 
 template <typename KV, int DPL, int TOK, bool FULL, int G>
@@ -137,22 +138,30 @@ __global__ void __launch_bounds__(kPsaThreads, 2) psa_gqa_kernel(PoolView p, Bat
     __syncthreads();
 
     for (;;) {
-        // ---- 1. ORDER: refill the tranche of every live head that consumed it ----
-#pragma unroll 1
-        for (int h = 0; h < G; ++h) {
-            if (!(s.live[h] && s.cb[h] >= s.tr0[h] + s.tc[h])) continue;  // uniform
-            const int64_t hb = off * g + (int64_t)h * n;
-            const int64_t t0 = s.tr0[h] + s.tc[h];
-            const int tc = select_tranche(s.sel, s.tb[h], kGTCap, s.hist, b.keys + hb, n, s.last[h], t0 == 0, kGTCap);
-            for (int i = tid; i < tc; i += kPsaThreads) {
-                const int32_t pos = (int32_t)(s.tb[h][i] & pmask);
-                b.rpos[hb + t0 + i] = pos;
-                const int32_t sl = b.slots[off + pos];
-                s.tslot[h][i] = sl;
-                s.tntok[h][i] = (uint8_t)p.ntok[sl];
+        // ---- 1. ORDER: refill the tranche of every live head that consumed it; the
+        //      heads' selections run concurrently, one team of kPsaWarps/G warps each ----
+        {
+            constexpr int W = kPsaWarps / G;
+            const int h = warp / W;
+            const Team tm{tid - h * W * 32, W * 32, 1 + h};
+            const bool need = s.live[h] && s.cb[h] >= s.tr0[h] + s.tc[h];
+            int tc = 0;
+            int64_t t0 = 0;
+            if (need) {
+                const int64_t hb = off * g + (int64_t)h * n;
+                t0 = s.tr0[h] + s.tc[h];
+                tc = select_tranche(s.sel[h], s.tb[h], kGTCap, s.hist[h], kGBins, b.keys + hb, n, s.last[h], t0 == 0,
+                                    kGTCap, tm);
+                for (int i = tm.tid; i < tc; i += tm.size) {
+                    const int32_t pos = (int32_t)(s.tb[h][i] & pmask);
+                    b.rpos[hb + t0 + i] = pos;
+                    const int32_t sl = b.slots[off + pos];
+                    s.tslot[h][i] = sl;
+                    s.tntok[h][i] = (uint8_t)p.ntok[sl];
+                }
             }
             __syncthreads();
-            if (tid == 0) {
+            if (need && tm.tid == 0) {
                 s.tr0[h] = t0;
                 s.tc[h] = tc;
                 s.last[h] = s.tb[h][tc - 1];

@@ -159,7 +159,8 @@ __global__ void __launch_bounds__(kPsaThreads, 3) psa_kernel(PoolView p, BatchVi
     for (int64_t cb = 0;;) {
         if (cb >= tr0 + tc) {  // ---- ORDER: next tranche ----
             tr0 += tc;
-            tc = select_tranche(s.sel, s.tb, kTCap, s.hist, keys, n, last, tr0 == 0, tr0 == 0 ? kFirstTranche : kTCap);
+            tc = select_tranche(s.sel, s.tb, kTCap, s.hist, kBins, keys, n, last, tr0 == 0, tr0 == 0 ? kFirstTranche : kTCap,
+                                cta_team());
             last = s.tb[tc - 1];
             for (int i = threadIdx.x; i < tc; i += kPsaThreads) {
                 const int32_t pos = (int32_t)(s.tb[i] & pmask);
@@ -368,7 +369,7 @@ static int g_psa_choice = 0;
 void set_psa_kernel_choice(int choice) { g_psa_choice = choice; }
 
 void launch_psa(const PoolView& p, const BatchView& b, cudaStream_t st) {
-    if (g_psa_choice == 2 && gqa_supported(p, b)) {  // auto = per-q-head kernel (faster on planted workloads)
+    if (g_psa_choice != 1 && gqa_supported(p, b)) {  // auto = GQA-group kernel where supported
         launch_gqa(p, b, st);
         return;
     }

@@ -550,7 +550,7 @@ int launch_batch(const PoolView& p, const BatchView& b, cudaStream_t st, cudaEve
     // marks (optional, 5 events): start | oracle | score | order | progressive. Ordering is
     // fused into the progressive kernel (lazy tranche selection), so the "order" stage is empty.
     int launches = 0;
-    int subs = g_pipeline == 0 ? (b.n_units >= 512 ? 8 : 1) : g_pipeline;
+    int subs = g_pipeline == 0 ? 1 : g_pipeline;  // measured: overlap does not pay (both stages are SM-bound)
     if (subs > 16) subs = 16;
     if (subs > b.n_units) subs = b.n_units;
     if (marks) cudaEventRecord(marks[0], st);

@@ -14,6 +14,19 @@ constexpr int kPsaThreads = kPsaWarps * 32;
 constexpr int kChunk = 32;
 constexpr int kBins = 2048;
 
+// A group of whole warps cooperating on one selection: the full CTA (__syncthreads)
+// or a sub-team synchronised by a named barrier (bar.sync id, size).
+struct Team {
+    int tid;   // thread index within the team
+    int size;  // threads in the team (multiple of 32)
+    int bar;   // named barrier id (0 = the CTA barrier)
+};
+__device__ __forceinline__ void team_sync(const Team& tm) {
+    if (tm.bar == 0) __syncthreads();
+    else asm volatile("bar.sync %0, %1;" ::"r"(tm.bar), "r"(tm.size) : "memory");
+}
+__device__ __forceinline__ Team cta_team() { return Team{(int)threadIdx.x, (int)blockDim.x, 0}; }
+
 struct SelScratch {
     unsigned long long red_min, red_max;
     unsigned int red_cnt, gcount, excl;
@@ -39,12 +52,12 @@ __device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long x)
 }
 
 // All-ascending bitonic network on a[0, n) in shared memory (indices >= n act as +inf).
-__device__ __forceinline__ void bitonic_smem(uint64_t* a, int n) {
+__device__ __forceinline__ void bitonic_smem(uint64_t* a, int n, const Team& tm) {
     int n2 = 1;
     while (n2 < n) n2 <<= 1;
     for (int k = 2; k <= n2; k <<= 1) {
         for (int j = k >> 1; j > 0; j >>= 1) {
-            for (int i = threadIdx.x; i < (n2 >> 1); i += blockDim.x) {
+            for (int i = tm.tid; i < (n2 >> 1); i += tm.size) {
                 const int lo = ((i & ~(j - 1)) << 1) | (i & (j - 1));  // j is a power of two
                 const int hi = (j == (k >> 1)) ? (lo ^ (k - 1)) : (lo + j);
                 if (hi < n) {
@@ -55,36 +68,36 @@ __device__ __forceinline__ void bitonic_smem(uint64_t* a, int n) {
                     }
                 }
             }
-            __syncthreads();
+            team_sync(tm);
         }
     }
 }
 
 // Calls f(key) for every key of the head; 8 independent loads in flight per thread.
 template <typename F>
-__device__ __forceinline__ void scan_keys(const uint64_t* __restrict__ keys, int64_t n, F&& f) {
+__device__ __forceinline__ void scan_keys(const uint64_t* __restrict__ keys, int64_t n, const Team& tm, F&& f) {
     constexpr int U = 8;
-    for (int64_t i0 = threadIdx.x; i0 < n; i0 += (int64_t)U * kPsaThreads) {
+    for (int64_t i0 = tm.tid; i0 < n; i0 += (int64_t)U * tm.size) {
         uint64_t k[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const int64_t i = i0 + (int64_t)u * kPsaThreads;
+            const int64_t i = i0 + (int64_t)u * tm.size;
             k[u] = i < n ? __ldg(reinterpret_cast<const unsigned long long*>(keys) + i) : ~0ull;
         }
 #pragma unroll
         for (int u = 0; u < U; ++u)
-            if (i0 + (int64_t)u * kPsaThreads < n) f(k[u]);
+            if (i0 + (int64_t)u * tm.size < n) f(k[u]);
     }
 }
 
 // Next tranche: the C (<= kTCap, ~target) smallest keys greater than `last` (all keys if first).
-static __device__ __noinline__ int select_tranche(SelScratch& s, uint64_t* tb, int cap, uint32_t* hist,
+static __device__ __noinline__ int select_tranche(SelScratch& s, uint64_t* tb, int cap, uint32_t* hist, int nbins,
                                           const uint64_t* __restrict__ keys, int64_t n, uint64_t last, bool first,
-                                          unsigned target) {
-    const int tid = threadIdx.x, lane = tid & 31;
+                                          unsigned target, Team tm) {
+    const int tid = tm.tid, lane = threadIdx.x & 31;
     unsigned long long lmin = ~0ull, lmax = 0;
     unsigned lcnt = 0;
-    scan_keys(keys, n, [&](uint64_t k) {
+    scan_keys(keys, n, tm, [&](uint64_t k) {
         if (first || k > last) {
             lmin = k < lmin ? k : lmin;
             lmax = k > lmax ? k : lmax;
@@ -97,7 +110,7 @@ static __device__ __noinline__ int select_tranche(SelScratch& s, uint64_t* tb, i
         s.red_cnt = 0;
         s.gcount = 0;
     }
-    __syncthreads();
+    team_sync(tm);
     lmin = warp_min_u64(lmin);
     lmax = warp_max_u64(lmax);
 #pragma unroll
@@ -107,7 +120,7 @@ static __device__ __noinline__ int select_tranche(SelScratch& s, uint64_t* tb, i
         atomicMax(&s.red_max, lmax);
         atomicAdd(&s.red_cnt, lcnt);
     }
-    __syncthreads();
+    team_sync(tm);
     const uint64_t kmax = s.red_max;
     uint64_t tau = kmax;
     if (s.red_cnt > (unsigned)cap) {
@@ -117,16 +130,15 @@ static __device__ __noinline__ int select_tranche(SelScratch& s, uint64_t* tb, i
             const uint64_t span = hi - lo;
             const int bits = 64 - __clzll((long long)span);
             const int sh = bits > 11 ? bits - 11 : 0;
-            for (int i = tid; i < kBins; i += kPsaThreads) hist[i] = 0;
-            __syncthreads();
-            scan_keys(keys, n, [&](uint64_t k) {
+            for (int i = tid; i < nbins; i += tm.size) hist[i] = 0;
+            team_sync(tm);
+            scan_keys(keys, n, tm, [&](uint64_t k) {
                 if ((first || k > last) && k >= lo && k <= hi) atomicAdd(&hist[(k - lo) >> sh], 1u);
             });
-            __syncthreads();
-            // first bin b with cum(b) >= need: each thread owns 8 consecutive bins
-            constexpr int per = kBins / kPsaThreads;
+            team_sync(tm);
+            // first bin b with cum(b) >= need: each thread owns nbins/size consecutive bins
+            const int per = nbins / tm.size;
             unsigned loc = 0;
-#pragma unroll
             for (int j = 0; j < per; ++j) loc += hist[tid * per + j];
             unsigned inc = loc;  // inclusive warp scan
 #pragma unroll
@@ -135,7 +147,7 @@ static __device__ __noinline__ int select_tranche(SelScratch& s, uint64_t* tb, i
                 if (lane >= o) inc += y;
             }
             if (lane == 31) s.wsum[tid >> 5] = inc;
-            __syncthreads();
+            team_sync(tm);
             unsigned wbase = 0;
             for (int w = 0; w < (tid >> 5); ++w) wbase += s.wsum[w];
             unsigned cum = wbase + inc - loc;  // exclusive prefix of this thread's bins
@@ -151,7 +163,7 @@ static __device__ __noinline__ int select_tranche(SelScratch& s, uint64_t* tb, i
                     cum += c;
                 }
             }
-            __syncthreads();
+            team_sync(tm);
             const int bs = s.bstar;
             const unsigned ex = s.excl, incl = ex + hist[bs];
             const uint64_t width_m1 = (sh >= 64) ? ~0ull : ((1ull << sh) - 1ull);
@@ -168,11 +180,11 @@ static __device__ __noinline__ int select_tranche(SelScratch& s, uint64_t* tb, i
             need -= ex;
             lo = bin_lo;
             if (hi - lo > width_m1) hi = lo + width_m1;
-            __syncthreads();
+            team_sync(tm);
         }
     }
     // gather the survivors (warp-aggregated slot reservation)
-    scan_keys(keys, n, [&](uint64_t k) {
+    scan_keys(keys, n, tm, [&](uint64_t k) {
         const bool take = (first || k > last) && k <= tau;
         const unsigned m = __ballot_sync(__activemask(), take);
         if (take) {
@@ -184,9 +196,9 @@ static __device__ __noinline__ int select_tranche(SelScratch& s, uint64_t* tb, i
             if (idx < (unsigned)cap) tb[idx] = k;
         }
     });
-    __syncthreads();
+    team_sync(tm);
     const int C = (int)min(s.gcount, (unsigned)cap);
-    bitonic_smem(tb, C);
+    bitonic_smem(tb, C, tm);
     return C;
 }
 
