@@ -120,6 +120,9 @@ __global__ void __launch_bounds__(kPsaThreads, 2) psa_gqa_kernel(PoolView p, Bat
                 }
         }
     }
+    float Oreg[16], Mreg = -INFINITY, Lreg = 0.0f;  // tensor-core V pass: head lane%4, dims [16*(lane/4), +16)
+#pragma unroll
+    for (int j = 0; j < 16; ++j) Oreg[j] = 0.0f;
     if (tid < G) {
         s.tr0[tid] = 0;
         s.cb[tid] = 0;
@@ -336,6 +339,58 @@ __global__ void __launch_bounds__(kPsaThreads, 2) psa_gqa_kernel(PoolView p, Bat
             const uint32_t mask = s.umask[e];
             if (!mask) continue;
             const int32_t slot = s.uslot[e];
+            if constexpr (kMma) {
+                // O^T[dim][(head, split)] += V^T[dim][token] * W^T[token][(head, split)]: 8 MMAs cover
+                // 128 dims x all heads; W carries a 2-term bf16 split (16-bit weight precision).
+                // Lane (g, t) owns head t, dims [16g, 16g+16): no cross-lane reduction.
+                const int gq = lane >> 2, tq = lane & 3;
+                const __nv_bfloat16* vblk =
+                    reinterpret_cast<const __nv_bfloat16*>(kv + (int64_t)slot * slot_elems + v_off);
+                uint32_t vw[4][8];
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    const int tok = 2 * tq + (r & 1) + (r >> 1) * 8;
+                    const int row = tok < T ? tok : T - 1;
+                    const uint4* pv = reinterpret_cast<const uint4*>(vblk + (size_t)row * 128 + 16 * gq);
+                    const uint4 x0 = __ldg(pv), x1 = __ldg(pv + 1);
+                    vw[r][0] = x0.x; vw[r][1] = x0.y; vw[r][2] = x0.z; vw[r][3] = x0.w;
+                    vw[r][4] = x1.x; vw[r][5] = x1.y; vw[r][6] = x1.z; vw[r][7] = x1.w;
+                }
+                const int hb = gq >> 1, sb = gq & 1;  // B column = (head, split)
+                const bool hon = hb < G && (mask >> hb) & 1u;
+                uint32_t bfr[2];
+#pragma unroll
+                for (int hf = 0; hf < 2; ++hf) {
+                    uint32_t packed = 0;
+#pragma unroll
+                    for (int e2 = 0; e2 < 2; ++e2) {
+                        const float wv = hon ? s.w[e][hb][2 * tq + e2 + 8 * hf] : 0.0f;
+                        packed |= bf16_bits(bf16_split(wv, sb)) << (16 * e2);
+                    }
+                    bfr[hf] = packed;
+                }
+                float ob[16];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    float c0 = 0.f, c1 = 0.f, c2 = 0.f, c3 = 0.f;
+                    mma_bf16_16816(c0, c1, c2, c3, __byte_perm(vw[0][i], vw[1][i], 0x5410),
+                                   __byte_perm(vw[0][i], vw[1][i], 0x7632), __byte_perm(vw[2][i], vw[3][i], 0x5410),
+                                   __byte_perm(vw[2][i], vw[3][i], 0x7632), bfr[0], bfr[1]);
+                    ob[2 * i] = c0 + c1;      // dim 16g + 2i
+                    ob[2 * i + 1] = c2 + c3;  // dim 16g + 2i + 1
+                }
+                if (tq < G && ((mask >> tq) & 1u)) {
+                    const float mbj = s.mb[e][tq];
+                    const float mnew = fmaxf(Mreg, mbj);
+                    const float a = expf(Mreg - mnew);
+                    const float c = expf(mbj - mnew);
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) Oreg[j] = Oreg[j] * a + ob[j] * c;
+                    Lreg = Lreg * a + s.lb[e][tq] * c;
+                    Mreg = mnew;
+                }
+                continue;
+            }
             const KV* vp = kv + (int64_t)slot * slot_elems + v_off + base;
             float vr[TOK][DPL];
 #pragma unroll
@@ -387,6 +442,18 @@ __global__ void __launch_bounds__(kPsaThreads, 2) psa_gqa_kernel(PoolView p, Bat
 #pragma unroll
         for (int h = 0; h < G; ++h) live += s.live[h];
         if (!live) break;
+        __syncthreads();
+    }
+    if constexpr (kMma) {  // registers -> the per-warp shared-memory accumulators
+        const int gq = lane >> 2, tq = lane & 3;
+        if (tq < G) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) s.o[warp][tq][16 * gq + j] = Oreg[j];
+            if (gq == 0) {
+                s.om[warp][tq] = Mreg;
+                s.ol[warp][tq] = Lreg;
+            }
+        }
         __syncthreads();
     }
     // ---- finalize: merge the warps' states per head (finalize, attention.hpp:104-110) ----
