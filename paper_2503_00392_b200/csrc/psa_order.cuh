@@ -129,7 +129,8 @@ static __device__ __noinline__ int select_tranche(SelScratch& s, uint64_t* tb, i
         for (int it = 0; it < 10; ++it) {
             const uint64_t span = hi - lo;
             const int bits = 64 - __clzll((long long)span);
-            const int sh = bits > 11 ? bits - 11 : 0;
+            const int bbits = 31 - __clz(nbins);  // log2(nbins): bin index (k - lo) >> sh < nbins
+            const int sh = bits > bbits ? bits - bbits : 0;
             for (int i = tid; i < nbins; i += tm.size) hist[i] = 0;
             team_sync(tm);
             scan_keys(keys, n, tm, [&](uint64_t k) {

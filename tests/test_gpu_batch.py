@@ -316,3 +316,29 @@ def test_pipelined_launch_identical(mods, subs, kernel):
     capi.lib.psattn_set_progressive_kernel(0)
     for a, b in zip(res[1], res[subs]):
         assert a.tobytes() == b.tobytes()
+
+
+@pytest.mark.parametrize("kernel", [1, 2])
+@pytest.mark.parametrize("kv_dtype", [0, 1])
+def test_long_lists_multi_tranche(mods, oracle, kernel, kv_dtype):
+    """Lists longer than one ordering tranche (GQA: 512, per-head: 1024 ranks) with eps near 1,
+    so heads consume several tranches (bucket-select refinement + histogram paths)."""
+    capi, _ = mods
+    rng = np.random.default_rng(99 + kernel + 10 * kv_dtype)
+    d, T, g, n = 128, 16, 4, 2600
+    units = [random_blockset(rng, n, d, 16, 16) for _ in range(2)]
+    if kv_dtype == 1:
+        for u in units:
+            u.keys[:] = torch.tensor(u.keys).bfloat16().float().numpy()
+            u.values[:] = torch.tensor(u.values).bfloat16().float().numpy()
+    qs = [[(rng.standard_normal(d) * 0.3).astype(np.float32) for _ in range(g)] for _ in units]
+    capi.lib.psattn_set_progressive_kernel(kernel)
+    try:
+        _, run, off = run_units(mods, units, qs, T, kv_dtype=kv_dtype, epsilon=0.99)
+    finally:
+        capi.lib.psattn_set_progressive_kernel(0)
+    for u in range(2):
+        for h in range(g):
+            r = unpack(run, off, u, h, n)
+            assert r["bp"] > 1100  # several tranches consumed
+            check_parity(oracle, qs[u][h], units[u], make_config(epsilon=0.99), 0, r["ids"], r["bp"], r["out"], r["est"])
