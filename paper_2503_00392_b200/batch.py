@@ -34,7 +34,7 @@ class DevicePool:
         self.dim, self.block_tokens, self.kv_dtype, self.n_slots = dim, block_tokens, kv_dtype, n_slots
 
     def close(self):
-        if getattr(self, "h", None) is not None and self.h.value:
+        if lib is not None and getattr(self, "h", None) is not None and self.h.value:
             lib.psattn_pool_destroy(self.h)
             self.h = None
 

@@ -191,7 +191,7 @@ class Store:
         check(lib.psattn_store_create(C.byref(o), C.byref(self.h)))
 
     def close(self):
-        if getattr(self, "h", None) is not None and self.h.value:
+        if lib is not None and getattr(self, "h", None) is not None and self.h.value:
             lib.psattn_store_destroy(self.h)
             self.h = None
 
