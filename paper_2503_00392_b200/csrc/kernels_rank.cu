@@ -117,6 +117,25 @@ __device__ __forceinline__ double smem_reduce(double (&acc)[N], double* red, int
     return t;
 }
 
+// Same reduction with XOR-swizzled 16-double rows (no padding): 32 x 16 doubles =
+// exactly 4 KB, so it fits in a consumed TMA stage buffer. Conflict-free (2 wavefronts
+// per 64-bit access, the minimum) for both the row writes and the column reads.
+__device__ __forceinline__ double smem_reduce16_swz(double (&acc)[16], double* red, int lane) {
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < 16; ++i) red[lane * 16 + (i ^ (lane & 15))] = acc[i];
+    __syncwarp();
+    const int v = lane >> 1, part = lane & 1;
+    double t = 0.0;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+        const int r = part * 16 + k;
+        t += red[r * 16 + (v ^ (r & 15))];
+    }
+    t += __shfl_xor_sync(PSA_FULL, t, 1);
+    return t;
+}
+
 template <typename KV, int G, int DPL, bool FULL>
 __global__ void __launch_bounds__(kScoreWarps * 32, 2) score_kernel(PoolView p, BatchView b) {
     constexpr int kRecs = RecsPer<G, DPL>::v;
@@ -231,7 +250,9 @@ __global__ void __launch_bounds__(kScoreWarps * 32, 2) score_kernel_tma(PoolView
     constexpr int SH = 5 - Log2<N>::v;
     constexpr int MB = D * 4 + 2 * D * (int)sizeof(KV);  // metadata record bytes (meta_bytes)
     constexpr int STAGE = kRecs * MB;
-    constexpr int S = (8192 / STAGE) < 2 ? 2 : ((8192 / STAGE) > 4 ? 4 : (8192 / STAGE));  // 2 CTAs/SM incl. reduction scratch
+    constexpr bool kReuse = (N == 16 && STAGE >= 4096);  // reduction scratch lives in the consumed stage
+    constexpr int SB = kReuse ? 12288 : 8192;
+    constexpr int S = (SB / STAGE) < 2 ? 2 : ((SB / STAGE) > 4 ? 4 : (SB / STAGE));  // 2 CTAs/SM
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
     const int lane = threadIdx.x & 31;
@@ -343,11 +364,20 @@ __global__ void __launch_bounds__(kScoreWarps * 32, 2) score_kernel_tma(PoolView
                 }
             }
         }
-        // every lane's shared-memory reads of this stage precede the refill (generic -> async proxy)
+        // The consumed stage doubles as the reduction scratch when it is large enough
+        // (N = 16 doubles x 32 lanes = 4 KB = one bf16 stage); then it is refilled.
+        double tot;
+        if constexpr (N == 16 && STAGE >= 4096) {
+            tot = smem_reduce16_swz(acc, reinterpret_cast<double*>(wbuf + stage * STAGE), lane);
+        } else {
+            tot = smem_reduce<N>(acc, reinterpret_cast<double*>(smem + kTmaBarBytes + (size_t)kScoreWarps * S * STAGE) +
+                                          warp * 32 * (N + 1),
+                                 lane);
+        }
+        // every lane's shared-memory accesses of this stage precede the refill (generic -> async proxy)
         fence_proxy_async();
         __syncwarp();
         if (gn < ngroups) issue(gn, stage, nslot);
-        const double tot = smem_reduce<N>(acc, reinterpret_cast<double*>(smem + kTmaBarBytes + (size_t)kScoreWarps * S * STAGE) + warp * 32 * (N + 1), lane);
         const int64_t p0 = grp * kRecs;
         if (writer && p0 + my_j < n) {
             const double sc = est == 2 ? 0.5 * (tot * scale) : tot * scale;
@@ -364,8 +394,11 @@ template <typename KV, int G>
 static size_t tma_smem_bytes() {
     constexpr int kRecs = RecsPer<G, 4>::v;
     constexpr int STAGE = kRecs * (128 * 4 + 2 * 128 * (int)sizeof(KV));
-    constexpr int S = (8192 / STAGE) < 2 ? 2 : ((8192 / STAGE) > 4 ? 4 : (8192 / STAGE));
-    return kTmaBarBytes + (size_t)kScoreWarps * S * STAGE + (size_t)kScoreWarps * 32 * (G * kRecs + 1) * 8;
+    constexpr int N = G * kRecs;
+    constexpr bool kReuse = (N == 16 && STAGE >= 4096);
+    constexpr int SB = kReuse ? 12288 : 8192;
+    constexpr int S = (SB / STAGE) < 2 ? 2 : ((SB / STAGE) > 4 ? 4 : (SB / STAGE));
+    return kTmaBarBytes + (size_t)kScoreWarps * S * STAGE + (kReuse ? 0 : (size_t)kScoreWarps * 32 * (N + 1) * 8);
 }
 
 template <typename KV, int G>
