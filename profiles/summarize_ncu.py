@@ -28,32 +28,45 @@ def num(x):
         return None
 
 
+UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
+        "ns": 1e-6, "us": 1e-3, "usecond": 1e-3, "msecond": 1.0, "ms": 1.0, "nsecond": 1e-6, "s": 1e3, "second": 1e3}
+
+
 def summarize(rep):
     rows = ncu_page(rep, "raw")
-    h, v = rows[0], rows[2]
-    raw = dict(zip(h, v))
+    h, units, v = rows[0], rows[1], rows[2]
+    raw = {k: (x, u) for k, u, x in zip(h, units, v)}
+
+    def g(k, to_base=False):
+        if k not in raw:
+            return None
+        x, u = raw[k]
+        val = num(x)
+        if val is None:
+            return None
+        return val * UNIT.get(u, 1.0) if to_base else val
+
     det = {}
-    for r in ncu_page(rep, "details"):
-        if len(r) >= 3:
-            det[r[-3]] = r[-1]
-    g = lambda k: num(raw.get(k))  # noqa: E731
+    for r in ncu_page(rep, "details")[1:]:
+        if len(r) >= 15:
+            det[r[12]] = (r[14], r[13])
+    d = lambda k: num(det[k][0]) if k in det else None  # noqa: E731
     stalls = {k.replace("smsp__average_warps_issue_stalled_", "").replace("_per_issue_active.ratio", ""): g(k)
               for k in h if k.startswith("smsp__average_warps_issue_stalled_") and k.endswith("per_issue_active.ratio")}
     stalls = {k: v for k, v in sorted(stalls.items(), key=lambda kv: -(kv[1] or 0)) if (v or 0) > 0.1}
-    rd, wr = g("dram__bytes_read.sum"), g("dram__bytes_write.sum")
-    unit_scale = 1.0
-    # ncu reports bytes in the unit of the column header; raw page uses plain bytes for .sum counters
+    rd, wr = g("dram__bytes_read.sum", True), g("dram__bytes_write.sum", True)
     return dict(
-        kernel=raw.get("Kernel Name", "")[:120],
-        duration_ms=(g("gpu__time_duration.sum") or 0) / 1e6,
-        dram_bytes_read=rd * unit_scale if rd is not None else None,
-        dram_bytes_write=wr * unit_scale if wr is not None else None,
+        kernel=raw.get("Kernel Name", ("",))[0][:120],
+        duration_ms=g("gpu__time_duration.sum", True),
+        dram_bytes_read=rd,
+        dram_bytes_write=wr,
         dram_bytes_per_launch=(rd or 0) + (wr or 0),
-        dram_throughput_pct=num(det.get("DRAM Throughput")),
-        sm_throughput_pct=num(det.get("Compute (SM) Throughput")),
-        ipc=num(det.get("Executed Ipc Active")),
-        achieved_occupancy_pct=num(det.get("Achieved Occupancy")),
-        registers=num(det.get("Registers Per Thread")),
+        dram_throughput_pct_of_nominal=d("DRAM Throughput"),
+        sm_throughput_pct=d("Compute (SM) Throughput"),
+        ipc=d("Executed Ipc Active"),
+        achieved_occupancy_pct=d("Achieved Occupancy"),
+        registers=d("Registers Per Thread"),
+        sm_clock_ghz=d("SM Frequency"),
         pipes_pct={k.split(".")[0].replace("sm__", ""): g(k) for k in [
             "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
             "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
