@@ -30,13 +30,14 @@ static int num_sms() {
 //
 // Arithmetic (fp64, like the reference): products of fp32 operands are exact in
 // fp64; only the summation order differs from the reference's sequential loop
-// (~1e-16 relative). Two rewrites keep the FP64/XU pipes below the HBM rate:
-//  * no F2F: an fp32 (or bf16) bit pattern u becomes the double x*2^-896 with two
-//    integer ops ((int)u >> 3 & 0x8FFFFFFF | u << 29 — same exponent field, no
-//    rebias; exact for every finite input incl. zero/denormals) and q carries
-//    the compensating 2^896, so q'*x' == q*x exactly;
-//  * max(q*lo, q*hi) == q*c + |q|*r with c = (lo+hi)/2, r = (hi-lo)/2 (hi >= lo),
-//    so the per-head select disappears and c, r are shared by the G heads.
+// (~1e-16 relative). Issue slots are the limiter at the HBM rate (ncu: IPC 2.8,
+// ALU and FP64 pipes ~45%), so:
+//  * fp32/bf16 -> fp64 conversions are single F2F instructions on the XU pipe,
+//    which nothing else uses (an integer bit-construction costs ~4 ALU slots);
+//  * max(q*lo, q*hi) == q*c + |q|*r with c = (lo+hi)/2, r = (hi-lo)/2 (hi >= lo):
+//    no per-head select, and with the factor 2 folded into the final scale the
+//    shared per-dim work is lo+hi, hi-lo and 2m+(lo+hi) (3 fp64 ops), then
+//    2 DFMA per head: acc = sum q(2m + lo + hi) + |q|(hi - lo) = 4 * CuboidMean.
 // =============================================================================
 constexpr int kScoreWarps = 8;
 // records per warp iteration: 4 for the d=128 / g<=4 path, fewer where registers would spill
@@ -45,7 +46,10 @@ template <int G, int DPL> struct RecsPer {
     static constexpr int v = (G * r <= 16) ? r : 16 / G;  // G*v <= 16: the reduction scratch fits
 };
 
-__device__ __forceinline__ double f32_scaled(uint32_t u) {  // = float(u) * 2^-896, exact
+// fp32 bit pattern -> double: one F2F on the otherwise idle XU pipe (the integer
+// bit-construction alternative costs ~4 ALU/issue slots per value).
+__device__ __forceinline__ double f32_to_f64(uint32_t u) { return (double)__uint_as_float(u); }
+__device__ __forceinline__ double f32_scaled(uint32_t u) {  // = float(u) * 2^-896, exact (kept for reference)
     return __hiloint2double((int)(((uint32_t)((int32_t)u >> 3)) & 0x8FFFFFFFu), (int)(u << 29));
 }
 
@@ -60,7 +64,7 @@ template <> struct MetaRow<float> {
         for (int j = 0; j < DPL; ++j) w[j] = __float_as_uint(f[j]);
     }
     template <int W>
-    __device__ __forceinline__ static double get(const uint32_t (&w)[W], int j) { return f32_scaled(w[j]); }
+    __device__ __forceinline__ static double get(const uint32_t (&w)[W], int j) { return f32_to_f64(w[j]); }
 };
 template <> struct MetaRow<__nv_bfloat16> {
     template <int DPL> __host__ __device__ static constexpr int words() { return (DPL + 1) / 2; }
@@ -92,7 +96,7 @@ template <> struct MetaRow<__nv_bfloat16> {
     template <int W>
     __device__ __forceinline__ static double get(const uint32_t (&w)[W], int j) {
         const uint32_t x = w[j >> 1];
-        return f32_scaled((j & 1) ? (x & 0xFFFF0000u) : (x << 16));
+        return f32_to_f64((j & 1) ? (x & 0xFFFF0000u) : (x << 16));
     }
 };
 
@@ -164,7 +168,7 @@ __global__ void __launch_bounds__(kScoreWarps * 32, 2) score_kernel(PoolView p, 
 #pragma unroll
             for (int j = 0; j < DPL; ++j) qf[j] = 0.0f;
 #pragma unroll
-        for (int j = 0; j < DPL; ++j) qd[h][j] = (double)qf[j] * 0x1p896;
+        for (int j = 0; j < DPL; ++j) qd[h][j] = (double)qf[j];
     }
     const int est = b.estimator;
     const double scale = b.scale;
@@ -212,8 +216,8 @@ __global__ void __launch_bounds__(kScoreWarps * 32, 2) score_kernel(PoolView p, 
                     A = m;  // mean_score
                 } else {
                     const double c2 = lo + hi;          // exact
-                    B = (hi - lo) * 0.5;                // r, exact
-                    A = est == 2 ? fma(0.5, c2, m) : c2 * 0.5;  // m + c  |  c
+                    B = hi - lo;                        // 2r, exact
+                    A = est == 2 ? fma(2.0, m, c2) : c2;  // 2(m + c)  |  2c
                 }
 #pragma unroll
                 for (int h = 0; h < G; ++h) {
@@ -226,7 +230,8 @@ __global__ void __launch_bounds__(kScoreWarps * 32, 2) score_kernel(PoolView p, 
         }
         const double tot = smem_reduce<N>(acc, red, lane);
         if (writer && p0 + my_j < n) {
-            const double s = est == 2 ? 0.5 * (tot * scale) : tot * scale;
+            // acc = sum q(2m + lo + hi) + |q|(hi - lo) = 4 * CuboidMean / 2 * Upper; Mean: plain
+            const double s = est == 2 ? 0.25 * (tot * scale) : (est == 1 ? 0.5 * (tot * scale) : tot * scale);
             keys[p0 + my_j] = make_key(s, (uint32_t)(p0 + my_j), b.pos_bits);
         }
     }
@@ -279,7 +284,7 @@ __global__ void __launch_bounds__(kScoreWarps * 32, 2) score_kernel_tma(PoolView
 #pragma unroll
             for (int j = 0; j < DPL; ++j) qf[j] = 0.0f;
 #pragma unroll
-        for (int j = 0; j < DPL; ++j) qd[h][j] = (double)qf[j] * 0x1p896;
+        for (int j = 0; j < DPL; ++j) qd[h][j] = (double)qf[j];
     }
     const int est = b.estimator;
     const double scale = b.scale;
@@ -344,16 +349,16 @@ __global__ void __launch_bounds__(kScoreWarps * 32, 2) score_kernel_tma(PoolView
             }
 #pragma unroll
             for (int jj = 0; jj < DPL; ++jj) {
-                const double m = f32_scaled(mw[jj]);
-                const double lo = f32_scaled(lw[jj]);
-                const double hi = f32_scaled(hw[jj]);
+                const double m = f32_to_f64(mw[jj]);
+                const double lo = f32_to_f64(lw[jj]);
+                const double hi = f32_to_f64(hw[jj]);
                 double A, B = 0.0;
                 if (est == 0) {
                     A = m;
                 } else {
                     const double c2 = lo + hi;
-                    B = (hi - lo) * 0.5;
-                    A = est == 2 ? fma(0.5, c2, m) : c2 * 0.5;
+                    B = hi - lo;                          // 2r, exact
+                    A = est == 2 ? fma(2.0, m, c2) : c2;  // 2(m + c)  |  2c
                 }
 #pragma unroll
                 for (int h = 0; h < G; ++h) {
@@ -380,7 +385,7 @@ __global__ void __launch_bounds__(kScoreWarps * 32, 2) score_kernel_tma(PoolView
         if (gn < ngroups) issue(gn, stage, nslot);
         const int64_t p0 = grp * kRecs;
         if (writer && p0 + my_j < n) {
-            const double sc = est == 2 ? 0.5 * (tot * scale) : tot * scale;
+            const double sc = est == 2 ? 0.25 * (tot * scale) : (est == 1 ? 0.5 * (tot * scale) : tot * scale);
             keys[p0 + my_j] = make_key(sc, (uint32_t)(p0 + my_j), b.pos_bits);
         }
         if (++stage == S) {
