@@ -409,7 +409,7 @@ int psattn_set_progressive_kernel(int32_t mode) {
 }
 
 int psattn_set_score_kernel(int32_t mode) {
-    if (mode < 0 || mode > 2) return fail(PSATTN_ERR_INVALID_ARGUMENT, "score kernel mode must be 0, 1 or 2");
+    if (mode < 0 || mode > 3) return fail(PSATTN_ERR_INVALID_ARGUMENT, "score kernel mode must be 0..3");
     set_score_kernel_choice(mode);
     return PSATTN_OK;
 }

@@ -64,7 +64,7 @@ template <> struct MetaRow<float> {
         for (int j = 0; j < DPL; ++j) w[j] = __float_as_uint(f[j]);
     }
     template <int W>
-    __device__ __forceinline__ static double get(const uint32_t (&w)[W], int j) { return f32_to_f64(w[j]); }
+    __device__ __forceinline__ static double get(const uint32_t (&w)[W], int j) { return f32_scaled(w[j]); }
 };
 template <> struct MetaRow<__nv_bfloat16> {
     template <int DPL> __host__ __device__ static constexpr int words() { return (DPL + 1) / 2; }
@@ -96,7 +96,7 @@ template <> struct MetaRow<__nv_bfloat16> {
     template <int W>
     __device__ __forceinline__ static double get(const uint32_t (&w)[W], int j) {
         const uint32_t x = w[j >> 1];
-        return f32_to_f64((j & 1) ? (x & 0xFFFF0000u) : (x << 16));
+        return f32_scaled((j & 1) ? (x & 0xFFFF0000u) : (x << 16));
     }
 };
 
@@ -168,7 +168,7 @@ __global__ void __launch_bounds__(kScoreWarps * 32, 2) score_kernel(PoolView p, 
 #pragma unroll
             for (int j = 0; j < DPL; ++j) qf[j] = 0.0f;
 #pragma unroll
-        for (int j = 0; j < DPL; ++j) qd[h][j] = (double)qf[j];
+        for (int j = 0; j < DPL; ++j) qd[h][j] = (double)qf[j] * 0x1p896;
     }
     const int est = b.estimator;
     const double scale = b.scale;
@@ -247,7 +247,7 @@ __global__ void __launch_bounds__(kScoreWarps * 32, 2) score_kernel(PoolView p, 
 // -----------------------------------------------------------------------------
 constexpr int kTmaBarBytes = 256;  // kScoreWarps x (<= 4 stages) x 8 B mbarriers
 
-template <typename KV, int G>
+template <typename KV, int G, int CONV>
 __global__ void __launch_bounds__(kScoreWarps * 32, 2) score_kernel_tma(PoolView p, BatchView b) {
     constexpr int DPL = 4, D = 128;
     constexpr int kRecs = RecsPer<G, DPL>::v;
@@ -284,7 +284,7 @@ __global__ void __launch_bounds__(kScoreWarps * 32, 2) score_kernel_tma(PoolView
 #pragma unroll
             for (int j = 0; j < DPL; ++j) qf[j] = 0.0f;
 #pragma unroll
-        for (int j = 0; j < DPL; ++j) qd[h][j] = (double)qf[j];
+        for (int j = 0; j < DPL; ++j) qd[h][j] = (double)qf[j] * 0x1p896;
     }
     const int est = b.estimator;
     const double scale = b.scale;
@@ -349,9 +349,11 @@ __global__ void __launch_bounds__(kScoreWarps * 32, 2) score_kernel_tma(PoolView
             }
 #pragma unroll
             for (int jj = 0; jj < DPL; ++jj) {
-                const double m = f32_to_f64(mw[jj]);
-                const double lo = f32_to_f64(lw[jj]);
-                const double hi = f32_to_f64(hw[jj]);
+                // CONV 0: all three via the exact 2^-896 bit construction (ALU);
+                // CONV 1: the mean via F2F (XU pipe, rescaled by 2^-896 exactly), lo/hi via ALU.
+                const double m = CONV == 0 ? f32_scaled(mw[jj]) : f32_to_f64(mw[jj]) * 0x1p-896;
+                const double lo = f32_scaled(lw[jj]);
+                const double hi = f32_scaled(hw[jj]);
                 double A, B = 0.0;
                 if (est == 0) {
                     A = m;
@@ -406,11 +408,19 @@ static size_t tma_smem_bytes() {
     return kTmaBarBytes + (size_t)kScoreWarps * S * STAGE + (kReuse ? 0 : (size_t)kScoreWarps * 32 * (N + 1) * 8);
 }
 
+static int g_score_choice = 0;
+void set_score_kernel_choice(int choice) { g_score_choice = choice; }
+
 template <typename KV, int G>
 static void launch_score_tma(const PoolView& p, const BatchView& b, dim3 grid, cudaStream_t st) {
     const size_t smem = tma_smem_bytes<KV, G>();
-    cudaFuncSetAttribute(score_kernel_tma<KV, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    score_kernel_tma<KV, G><<<grid, kScoreWarps * 32, smem, st>>>(p, b);
+    if (g_score_choice == 3) {
+        cudaFuncSetAttribute(score_kernel_tma<KV, G, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        score_kernel_tma<KV, G, 1><<<grid, kScoreWarps * 32, smem, st>>>(p, b);
+    } else {
+        cudaFuncSetAttribute(score_kernel_tma<KV, G, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        score_kernel_tma<KV, G, 0><<<grid, kScoreWarps * 32, smem, st>>>(p, b);
+    }
 }
 
 // =============================================================================
@@ -512,9 +522,6 @@ static void launch_score_g(const PoolView& p, const BatchView& b, dim3 grid, cud
             break;
     }
 }
-
-static int g_score_choice = 0;
-void set_score_kernel_choice(int choice) { g_score_choice = choice; }
 
 template <typename KV>
 static void launch_score(const PoolView& p, const BatchView& b, dim3 grid, cudaStream_t st) {
