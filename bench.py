@@ -269,6 +269,8 @@ def run_ours(args):
     barrier()
     torch.cuda.synchronize()
     capi.lib.psattn_profile_read(None, None, 1)
+    phases = np.zeros(12, np.uint64)
+    prof_build = capi.lib.psattn_debug_gqa_phases(phases.ctypes.data) == 0  # PROF=1 development build only
     capi.lib.psattn_profile_enable(1)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
@@ -283,6 +285,16 @@ def run_ours(args):
     stage_ms = np.zeros(4, np.float64)
     stage_n = np.zeros(4, np.int64)
     capi.lib.psattn_profile_read(stage_ms.ctypes.data, stage_n.ctypes.data, 1)
+    if prof_build:
+        capi.lib.psattn_debug_gqa_phases(phases.ctypes.data)
+        names = ["init", "order", "union", "k_pass", "decide", "v_pass", "advance", "finalize"]
+        tot = float(phases[:8].sum())
+        print(json.dumps({"gqa_phase_share": {k: round(float(phases[i]) / tot, 4) for i, k in enumerate(names)},
+                          "rounds_per_cta": float(phases[8]) / (U * args.steps),
+                          "cycles_per_cta": tot / (U * args.steps),
+                          "warp0_decide_chunk": round(float(phases[9]) / tot, 4),
+                          "warp0_k_work": round(float(phases[10]) / tot, 4),
+                          "warp0_v_work": round(float(phases[11]) / tot, 4)}), file=sys.stderr)
     ms = shard.max_over_ranks(ms, dev)
     ms_per_step = ms / args.steps
     value = nq * ws * args.steps / (ms / 1e3)

@@ -14,7 +14,7 @@ from dataclasses import dataclass
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libpsattn_b200.so")
+LIB_PATH = os.environ.get("PSATTN_B200_LIB") or os.path.join(_HERE, "_lib", "libpsattn_b200.so")
 
 PSATTN_OK = 0
 PSATTN_ERR_INVALID_ARGUMENT = 1

@@ -61,6 +61,23 @@ struct GqaSmem {
     SelScratch sel[G];
 };
 
+#ifdef PSA_GQA_PROF
+// Development-only phase timer (make PROF=1): SM cycles per phase summed over CTAs.
+__device__ unsigned long long g_gqa_prof[12];
+#define GQA_MARK(k)                                \
+    do {                                           \
+        if (tid == 0) {                            \
+            const long long t_ = clock64();        \
+            pc[k] += t_ - pt;                      \
+            pt = t_;                               \
+        }                                          \
+    } while (0)
+#else
+#define GQA_MARK(k) \
+    do {            \
+    } while (0)
+#endif
+
 template <typename KV, int DPL, int TOK, bool FULL, int G>
 __global__ void __launch_bounds__(kPsaThreads, 2) psa_gqa_kernel(PoolView p, BatchView b) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -84,6 +101,9 @@ __global__ void __launch_bounds__(kPsaThreads, 2) psa_gqa_kernel(PoolView p, Bat
     const int64_t slot_elems = p.slot_bytes / (int64_t)sizeof(KV);
     const int T = p.T;
     const int64_t v_off = (int64_t)T * d;
+#ifdef PSA_GQA_PROF
+    long long pt = clock64(), pc[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+#endif
 
     float q[G][DPL];
 #pragma unroll
@@ -139,6 +159,7 @@ __global__ void __launch_bounds__(kPsaThreads, 2) psa_gqa_kernel(PoolView p, Bat
     }
     for (int i = tid; i < kPsaWarps * G * 128; i += kPsaThreads) (&s.o[0][0][0])[i] = 0.0f;
     __syncthreads();
+    GQA_MARK(0);
 
     for (;;) {
         // ---- 1. ORDER: refill the tranche of every live head that consumed it; the
@@ -155,13 +176,7 @@ __global__ void __launch_bounds__(kPsaThreads, 2) psa_gqa_kernel(PoolView p, Bat
                 t0 = s.tr0[h] + s.tc[h];
                 tc = select_tranche(s.sel[h], s.tb[h], kGTCap, s.hist[h], kGBins, b.keys + hb, n, s.last[h], t0 == 0,
                                     kGTCap, tm);
-                for (int i = tm.tid; i < tc; i += tm.size) {
-                    const int32_t pos = (int32_t)(s.tb[h][i] & pmask);
-                    b.rpos[hb + t0 + i] = pos;
-                    const int32_t sl = b.slots[off + pos];
-                    s.tslot[h][i] = sl;
-                    s.tntok[h][i] = (uint8_t)p.ntok[sl];
-                }
+                fill_tranche(s.tb[h], tc, pmask, b.rpos + hb + t0, b.slots + off, p.ntok, s.tslot[h], s.tntok[h], tm);
             }
             __syncthreads();
             if (need && tm.tid == 0) {
@@ -171,6 +186,10 @@ __global__ void __launch_bounds__(kPsaThreads, 2) psa_gqa_kernel(PoolView p, Bat
             }
             __syncthreads();
         }
+        GQA_MARK(1);
+#ifdef PSA_GQA_PROF
+        pc[8] += 1;
+#endif
         // ---- 2. round: union of the live heads' next chunks ----
         // U entries are numbered by first occurrence in (head, rank) order so the
         // per-warp accumulation order, and hence every output bit, is deterministic.
@@ -225,6 +244,7 @@ __global__ void __launch_bounds__(kPsaThreads, 2) psa_gqa_kernel(PoolView p, Bat
         __syncthreads();
         if (act) s.cidx[hh][rr] = s.hval[hs];
         const int ucount = s.ucount;
+        GQA_MARK(2);
         // ---- 3. K pass: every U block once, scored for all heads ----
 #pragma unroll 1
         for (int e = warp; e < ucount; e += kPsaWarps) {
@@ -310,7 +330,11 @@ __global__ void __launch_bounds__(kPsaThreads, 2) psa_gqa_kernel(PoolView p, Bat
                 }
             }
         }
+#ifdef PSA_GQA_PROF
+        if (tid == 0) pc[10] += clock64() - pt;  // warp 0's own K-pass work (rest = imbalance)
+#endif
         __syncthreads();
+        GQA_MARK(3);
         // ---- 4. decide: warp h for head h, all heads in parallel ----
         if (warp < G && s.live[warp]) {
             const int h = warp;
@@ -322,7 +346,13 @@ __global__ void __launch_bounds__(kPsaThreads, 2) psa_gqa_kernel(PoolView p, Bat
                 x = b.has_oracle ? b.omass[hb + s.upos[e]] : (double)s.la[e][h];
             }
             double acc = s.acc[h], mn = s.mn[h];
+#ifdef PSA_GQA_PROF
+            const long long d0_ = clock64();
+#endif
             const Decision dc = decide_chunk(x, cnt, s.cb[h], n, limit, b.m, eps, acc, mn, b.iest ? b.iest + hb : nullptr);
+#ifdef PSA_GQA_PROF
+            if (tid == 0) pc[9] += clock64() - d0_;
+#endif
             if (lane < dc.commit) atomicOr(&s.umask[s.cidx[h][lane]], 1u << h);
             if (lane == 0) {
                 s.commit[h] = dc.commit;
@@ -333,6 +363,7 @@ __global__ void __launch_bounds__(kPsaThreads, 2) psa_gqa_kernel(PoolView p, Bat
             }
         }
         __syncthreads();
+        GQA_MARK(4);
         // ---- 5. V pass: committed U blocks once, into every committing head ----
 #pragma unroll 1
         for (int e = warp; e < ucount; e += kPsaWarps) {
@@ -361,13 +392,9 @@ __global__ void __launch_bounds__(kPsaThreads, 2) psa_gqa_kernel(PoolView p, Bat
                 uint32_t bfr[2];
 #pragma unroll
                 for (int hf = 0; hf < 2; ++hf) {
-                    uint32_t packed = 0;
-#pragma unroll
-                    for (int e2 = 0; e2 < 2; ++e2) {
-                        const float wv = hon ? s.w[e][hb][2 * tq + e2 + 8 * hf] : 0.0f;
-                        packed |= bf16_bits(bf16_split(wv, sb)) << (16 * e2);
-                    }
-                    bfr[hf] = packed;
+                    const float2 wv = hon ? *reinterpret_cast<const float2*>(&s.w[e][hb][2 * tq + 8 * hf])
+                                          : make_float2(0.0f, 0.0f);
+                    bfr[hf] = pack_bf16x2_split(wv.x, wv.y, sb);
                 }
                 float ob[16];
 #pragma unroll
@@ -424,7 +451,11 @@ __global__ void __launch_bounds__(kPsaThreads, 2) psa_gqa_kernel(PoolView p, Bat
                 __syncwarp();
             }
         }
+#ifdef PSA_GQA_PROF
+        if (tid == 0) pc[11] += clock64() - pt;
+#endif
         __syncthreads();
+        GQA_MARK(5);
         // ---- 6. advance cursors, retire finished heads ----
         if (tid < G && s.live[tid]) {
             const int h = tid;
@@ -441,6 +472,7 @@ __global__ void __launch_bounds__(kPsaThreads, 2) psa_gqa_kernel(PoolView p, Bat
         int live = 0;
 #pragma unroll
         for (int h = 0; h < G; ++h) live += s.live[h];
+        GQA_MARK(6);
         if (!live) break;
         __syncthreads();
     }
@@ -487,6 +519,11 @@ __global__ void __launch_bounds__(kPsaThreads, 2) psa_gqa_kernel(PoolView p, Bat
             b.tcov[qi] = tcv;
         }
     }
+#ifdef PSA_GQA_PROF
+    GQA_MARK(7);
+    if (tid == 0)
+        for (int k = 0; k < 12; ++k) atomicAdd(&g_gqa_prof[k], (unsigned long long)pc[k]);
+#endif
 }
 
 template <typename KV, int DPL, int TOK, bool FULL, int G>
@@ -519,3 +556,17 @@ void launch_gqa(const PoolView& p, const BatchView& b, cudaStream_t st) {
 }
 
 }  // namespace psa
+
+// Reads (and zeroes) the phase timer: init, order, union, K pass, decide, V pass,
+// advance, finalize cycles and the round count. -1 when built without PROF=1.
+extern "C" int psattn_debug_gqa_phases(unsigned long long* out12) {
+#ifdef PSA_GQA_PROF
+    if (cudaMemcpyFromSymbol(out12, psa::g_gqa_prof, sizeof(unsigned long long) * 12) != cudaSuccess) return -1;
+    static const unsigned long long z[12] = {};
+    cudaMemcpyToSymbol(psa::g_gqa_prof, z, sizeof(z));
+    return 0;
+#else
+    (void)out12;
+    return -1;
+#endif
+}

@@ -162,13 +162,7 @@ __global__ void __launch_bounds__(kPsaThreads, 3) psa_kernel(PoolView p, BatchVi
             tc = select_tranche(s.sel, s.tb, kTCap, s.hist, kBins, keys, n, last, tr0 == 0, tr0 == 0 ? kFirstTranche : kTCap,
                                 cta_team());
             last = s.tb[tc - 1];
-            for (int i = threadIdx.x; i < tc; i += kPsaThreads) {
-                const int32_t pos = (int32_t)(s.tb[i] & pmask);
-                b.rpos[hb + tr0 + i] = pos;
-                const int32_t sl = b.slots[off + pos];
-                s.tslot[i] = sl;
-                s.tntok[i] = (uint8_t)p.ntok[sl];
-            }
+            fill_tranche(s.tb, tc, pmask, b.rpos + hb + tr0, b.slots + off, p.ntok, s.tslot, s.tntok, cta_team());
             __syncthreads();
         }
         const int64_t room = tr0 + tc - cb;

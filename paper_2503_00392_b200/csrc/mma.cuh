@@ -17,6 +17,18 @@ __device__ __forceinline__ void mma_bf16_16816(float& c0, float& c1, float& c2, 
 
 __device__ __forceinline__ uint32_t bf16_bits(float x) { return (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(x)); }
 
+// Two fp32 -> packed bf16x2 (round to nearest even), element a in the low half: one cvt.
+__device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
+    const __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<const uint32_t*>(&v);
+}
+// Packed 2-term split of a pair: part 0 = rn(x), part 1 = rn(x - rn(x)) (as bf16_split(x, 0/1)).
+__device__ __forceinline__ uint32_t pack_bf16x2_split(float a, float b, int part) {
+    const uint32_t p = pack_bf16x2(a, b);
+    if (part == 0) return p;
+    return pack_bf16x2(a - __uint_as_float(p << 16), b - __uint_as_float(p & 0xFFFF0000u));
+}
+
 
 // Exact 3-term bf16 split of an fp32 value: x == x1 + x2 + x3 (split index 0..2; 3+ -> 0).
 __device__ __forceinline__ float bf16_split(float x, int part) {

@@ -73,20 +73,32 @@ __device__ __forceinline__ void bitonic_smem(uint64_t* a, int n, const Team& tm)
     }
 }
 
-// Calls f(key) for every key of the head; 8 independent loads in flight per thread.
+// Calls f(key) for every key of the head: 16-byte loads (two keys), 8 in flight per
+// thread (the scan is latency-bound: a team of 64 threads keeps 8 KB in flight).
+// Scalar head/tail keys are handled by team thread 0, so f must tolerate a partial warp.
 template <typename F>
 __device__ __forceinline__ void scan_keys(const uint64_t* __restrict__ keys, int64_t n, const Team& tm, F&& f) {
     constexpr int U = 8;
-    for (int64_t i0 = tm.tid; i0 < n; i0 += (int64_t)U * tm.size) {
-        uint64_t k[U];
+    const int64_t head = ((reinterpret_cast<uintptr_t>(keys) & 15) && n > 0) ? 1 : 0;
+    const ulonglong2* k2 = reinterpret_cast<const ulonglong2*>(keys + head);
+    const int64_t n2 = (n - head) >> 1;
+    for (int64_t i0 = tm.tid; i0 < n2; i0 += (int64_t)U * tm.size) {
+        ulonglong2 k[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int64_t i = i0 + (int64_t)u * tm.size;
-            k[u] = i < n ? __ldg(reinterpret_cast<const unsigned long long*>(keys) + i) : ~0ull;
+            k[u] = i < n2 ? __ldg(k2 + i) : make_ulonglong2(~0ull, ~0ull);
         }
 #pragma unroll
         for (int u = 0; u < U; ++u)
-            if (i0 + (int64_t)u * tm.size < n) f(k[u]);
+            if (i0 + (int64_t)u * tm.size < n2) {
+                f(k[u].x);
+                f(k[u].y);
+            }
+    }
+    if (tm.tid == 0) {
+        if (head) f(__ldg(reinterpret_cast<const unsigned long long*>(keys)));
+        if ((n - head) & 1) f(__ldg(reinterpret_cast<const unsigned long long*>(keys) + n - 1));
     }
 }
 
@@ -204,6 +216,38 @@ static __device__ __noinline__ int select_tranche(SelScratch& s, uint64_t* tb, i
 }
 
 
+// Tranche page-table fill: ranked positions -> rpos output, slots and token counts into
+// shared memory. The two dependent gathers (slot, then its token count) are batched
+// 8 per thread so one thread keeps 8 loads in flight instead of 2 serial misses per entry.
+__device__ __forceinline__ void fill_tranche(const uint64_t* tb, int tc, uint64_t pmask, int32_t* rpos_out,
+                                             const int32_t* __restrict__ slots, const int32_t* ntok, int32_t* tslot,
+                                             uint8_t* tntok, const Team& tm) {
+    constexpr int U = 8;
+    for (int i0 = tm.tid; i0 < tc; i0 += U * tm.size) {
+        int32_t sl[U], nt[U];
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            const int i = i0 + k * tm.size;
+            sl[k] = 0;
+            if (i < tc) {
+                const int32_t pos = (int32_t)(tb[i] & pmask);
+                rpos_out[i] = pos;
+                sl[k] = slots[pos];
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < U; ++k) nt[k] = (i0 + k * tm.size < tc) ? ntok[sl[k]] : 0;
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            const int i = i0 + k * tm.size;
+            if (i < tc) {
+                tslot[i] = sl[k];
+                tntok[i] = (uint8_t)nt[k];
+            }
+        }
+    }
+}
+
 // Coverage decide step for one chunk of ranks [cb, cb+cnt), executed by ONE full
 // warp: lane i holds x = log-mass of rank cb+i (valid for i < cnt). Running
 // log-sum-exp and min (CoverageEstimator::observe, reference engine.cpp:38-46) are
@@ -225,6 +269,7 @@ __device__ __forceinline__ Decision decide_chunk(double x, int cnt, int64_t cb, 
     double mx = warp_max_d(x);
     mx = fmax(mx, acc);
     double e = valid ? exp(x - mx) : 0.0;
+    const double e0 = acc != -INFINITY ? exp(acc - mx) : 0.0;  // independent of the scan
     double mnv = valid ? x : INFINITY;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -235,12 +280,15 @@ __device__ __forceinline__ Decision decide_chunk(double x, int cnt, int64_t cb, 
             mnv = fmin(mnv, ym);
         }
     }
-    if (acc != -INFINITY) e += exp(acc - mx);
-    const double acc_i = mx + log(e);
+    e += e0;  // S = sum exp(mass - mx) over everything observed up to this rank
     const double mn_i = fmin(mnv, mn);
     const int64_t nl = n - (r + 1);
-    const double est_i = nl == 0 ? 1.0 : 1.0 / (1.0 + (double)nl * exp(mn_i - acc_i));
-    const bool boundary = valid && ((((r + 1) % m) == 0) || (r + 1 == limit));
+    // est = 1 / (1 + nl * exp(min - acc)) with acc = mx + log S, i.e. S / (S + nl * exp(min - mx)):
+    // the exp and the log (for the carried acc) are independent, so their latencies overlap.
+    const double t = exp(mn_i - mx);
+    const double acc_i = mx + log(e);
+    const double est_i = nl == 0 ? 1.0 : (e > 0.0 ? e / fma((double)nl, t, e) : 0.0);
+    const bool boundary = valid && (m == 1 || (((r + 1) % m) == 0) || (r + 1 == limit));
     const bool stop = boundary && (est_i > eps || r + 1 == limit);
     const unsigned bal = __ballot_sync(PSA_FULL, stop);
     const int f = bal ? (__ffs(bal) - 1) : (cnt - 1);
