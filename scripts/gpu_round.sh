@@ -1,0 +1,28 @@
+#!/bin/bash
+# One GPU session: parity tests, smoke, bench line, ncu launch list + full captures of the two hot kernels.
+# usage (from the repo root, on the GPU box): bash scripts/gpu_round.sh <tag> [tests|bench|ncu|all]
+tag=${1:-r01}; what=${2:-all}
+mkdir -p gpurun_out
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/gpu_$tag.txt 2>&1
+if [[ $what == all || $what == tests ]]; then
+  timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu_$tag.log 2>&1; echo "pytest rc=$?"
+  tail -3 gpurun_out/pytest_gpu_$tag.log
+  timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_$tag.log 2>&1; echo "smoke rc=$?"
+  tail -2 gpurun_out/smoke_$tag.log
+fi
+if [[ $what == all || $what == bench ]]; then
+  timeout 600 python bench.py > gpurun_out/bench_$tag.log 2>&1; echo "bench rc=$?"
+  tail -1 gpurun_out/bench_$tag.log
+  timeout 300 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref_$tag.log 2>&1; echo "ref rc=$?"
+  tail -1 gpurun_out/bench_ref_$tag.log | cut -c1-300
+fi
+if [[ $what == all || $what == ncu ]]; then
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+     --log-file gpurun_out/launches_$tag.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline \
+     > gpurun_out/ncu_launch_bench_$tag.log 2>&1; echo "ncu launches rc=$?"
+  for k in score_kernel psa_gqa_kernel; do
+    timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k --launch-skip 2 -c 1 \
+       -o gpurun_out/${tag}_$k -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline \
+       > gpurun_out/ncu_full_${k}_$tag.log 2>&1; echo "ncu $k rc=$?"
+  done
+fi
