@@ -244,6 +244,17 @@ __global__ void __launch_bounds__(kPsaThreads, 2) psa_gqa_kernel(PoolView p, Bat
         __syncthreads();
         if (act) s.cidx[hh][rr] = s.hval[hs];
         const int ucount = s.ucount;
+#ifndef PSA_PF
+#define PSA_PF 1
+#endif
+        if constexpr (kMma && PSA_PF >= 1) {
+            // Bulk L2 prefetch of every U block's K (threads 0..) and V (threads 128..): the K pass
+            // below then walks L2-resident blocks, and the V pass finds committed blocks in L2.
+            const int e = tid & (G * kChunk - 1);
+            if (e < ucount && tid < 2 * G * kChunk)
+                prefetch_l2_bulk(kv + (int64_t)s.uslot[e] * slot_elems + (tid >= G * kChunk ? v_off : 0),
+                                 (uint32_t)(T * 128 * sizeof(KV)));
+        }
         GQA_MARK(2);
         // ---- 3. K pass: every U block once, scored for all heads ----
 #pragma unroll 1
@@ -363,6 +374,18 @@ __global__ void __launch_bounds__(kPsaThreads, 2) psa_gqa_kernel(PoolView p, Bat
             }
         }
         __syncthreads();
+        if constexpr (kMma && PSA_PF >= 2) {
+            // next round's chunk of every continuing head, while this round's V pass runs
+            const int h = tid >> 5, r = tid & 31;
+            if (h < G && s.live[h] && !s.fin[h]) {
+                const int64_t idx = s.cb[h] + s.commit[h] - s.tr0[h] + r;
+                if (idx < s.tc[h]) {
+                    const KV* bp0 = kv + (int64_t)s.tslot[h][idx] * slot_elems;
+                    prefetch_l2_bulk(bp0, (uint32_t)(T * 128 * sizeof(KV)));
+                    prefetch_l2_bulk(bp0 + v_off, (uint32_t)(T * 128 * sizeof(KV)));
+                }
+            }
+        }
         GQA_MARK(4);
         // ---- 5. V pass: committed U blocks once, into every committing head ----
 #pragma unroll 1

@@ -2,6 +2,7 @@
 #include <cuda_bf16.h>
 #include <float.h>
 #include <math.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -408,10 +409,15 @@ static size_t tma_smem_bytes() {
 
 static int g_score_choice = 0;
 void set_score_kernel_choice(int choice) { g_score_choice = choice; }
+// Dynamic shared memory floor of the score kernel. In the two-stream pipeline the score
+// kernel is held to ONE CTA per SM (its ~98 KB ring padded past half of the SM's 228 KB)
+// so a progressive CTA (~105 KB, 128 regs x 256) can be co-resident on every SM.
+static size_t g_score_smem_floor = 0;
 
 template <typename KV, int G>
 static void launch_score_tma(const PoolView& p, const BatchView& b, dim3 grid, cudaStream_t st) {
-    const size_t smem = tma_smem_bytes<KV, G>();
+    size_t smem = tma_smem_bytes<KV, G>();
+    if (smem < g_score_smem_floor) smem = g_score_smem_floor;
     auto go = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         kern<<<grid, kScoreWarps * 32, smem, st>>>(p, b);
@@ -620,6 +626,11 @@ int launch_batch(const PoolView& p, const BatchView& b, cudaStream_t st, cudaEve
         // on `st` while progressive(i) runs on the auxiliary stream. Stream-ordered (events),
         // no host synchronisation; the caller's stream joins the auxiliary one at the end.
         PipeResources& r = pipe_resources();
+        static const size_t floor_env = [] {
+            const char* e = getenv("PSA_SCORE_SMEM_FLOOR");
+            return e ? (size_t)atol(e) : (size_t)(116 * 1024);
+        }();
+        g_score_smem_floor = floor_env;
         if (marks) cudaEventRecord(marks[1], st);
         cudaEventRecord(r.ev[0], st);
         cudaStreamWaitEvent(r.aux, r.ev[0], 0);
@@ -634,6 +645,7 @@ int launch_batch(const PoolView& p, const BatchView& b, cudaStream_t st, cudaEve
             launch_psa(p, v, r.aux);
             launches += 2;
         }
+        g_score_smem_floor = 0;
         if (marks) cudaEventRecord(marks[2], st);  // score chain done (progressive overlapped)
         if (marks) cudaEventRecord(marks[3], st);
         cudaEventRecord(r.ev[0], r.aux);
