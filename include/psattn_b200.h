@@ -160,6 +160,33 @@ int psattn_set_score_kernel(int32_t mode);
 int psattn_profile_enable(int32_t enable);
 int psattn_profile_read(double* ms, int64_t* count, int32_t reset);
 
+/* ---- Oracle / audit tooling (test and report mode; reads every block of every list) ---- */
+
+/* fp64 exact attention over every block of each list, in list order
+ * (exact_attention_blocks, reference attention.cpp:36-63): out = device double
+ * [n_units][group][dim]. Uses the batch's shape, q, slots, list_off, dim <= 256, scale. */
+int psattn_exact_attention(psattn_pool* pool, const psattn_batch* b, double* out, void* stream);
+
+/* run_tradeoff (reference scenario.cpp:451-545, TradeoffReport scenario.hpp) for the
+ * batch's queries: fp64 block masses and coverage curves in mass order, the smallest
+ * uniform top-k whose coverage meets `target` for every query (bisection), and PSA at
+ * epsilon = target with the coverage audit (the batch's estimator, ranking mode and
+ * microbatch; its epsilon/topk/audit fields are ignored). Synchronous on `stream`. */
+typedef struct {
+    double target_coverage;
+    int64_t n_queries;
+    int64_t max_blocks;
+    int64_t k_min;
+    double worst_coverage_at_kmin;
+    double worst_coverage_below_kmin;
+    double psa_mean_blocks;
+    double psa_p99_blocks;
+    double psa_mean_coverage;
+    double block_access_ratio;
+} psattn_tradeoff_report;
+int psattn_tradeoff(psattn_pool* pool, const psattn_batch* b, double target, psattn_tradeoff_report* out,
+                    void* stream);
+
 /* ---- Seekable synthetic workload (bench + parity; not on the attention path) ----
  * Values are a pure function of (seed, unit_id, block, token, dim), identical on
  * host and device. Keys: approx-N(0,1) noise, plus skew*direction on planted

@@ -263,6 +263,63 @@ class RefDriver:
     def store(self, capacity=256, n_layers=1, partitioned=0, fifo=0, miss_ms=0.0) -> "RefStore":
         return RefStore(self, capacity, n_layers, partitioned, fifo, miss_ms)
 
+    def workload(self, **spec) -> "RefWorkload":
+        """The reference's generate_workload (workload.cpp:49-153) with a WorkloadSpec's fields."""
+        return RefWorkload(self, **spec)
+
+
+class RefWorkload:
+    """Requests of the reference's synthetic workload generator: blocks (ids, layers, n_tokens, K/V
+    zero-padded to block_size), per-layer block lists and per-step queries."""
+
+    FIELDS = ("n_requests", "dim", "block_size", "n_layers", "context_min", "context_max", "decode_steps", "rho",
+              "skew", "planted_blocks", "planted_blocks_alt", "seed")
+
+    def __init__(self, drv: RefDriver, **spec):
+        L = drv.L
+        L.refdrv_workload_create.argtypes = [C.c_int32] * 7 + [C.c_double, C.c_double, C.c_int32, C.c_int32,
+                                                              C.c_uint64]
+        L.refdrv_workload_create.restype = C.c_void_p
+        L.refdrv_workload_destroy.argtypes = [C.c_void_p]
+        L.refdrv_workload_n_requests.argtypes = [C.c_void_p]
+        L.refdrv_workload_request.argtypes = [C.c_void_p, C.c_int32, C.c_void_p]
+        L.refdrv_workload_blocks.argtypes = [C.c_void_p, C.c_int32, C.c_int32] + [C.c_void_p] * 5
+        L.refdrv_workload_layer_list.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]
+        L.refdrv_workload_query.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p]
+        sp = dict(n_requests=1, dim=64, block_size=32, n_layers=1, context_min=1024, context_max=1024,
+                  decode_steps=8, rho=0.0, skew=0.0, planted_blocks=0, planted_blocks_alt=0, seed=1)
+        sp.update(spec)
+        self.spec = sp
+        self.L = L
+        self.h = L.refdrv_workload_create(*[sp[k] for k in self.FIELDS])
+        if not self.h:
+            raise RuntimeError(drv.error())
+        self.requests = []
+        d, B = sp["dim"], sp["block_size"]
+        for r in range(L.refdrv_workload_n_requests(self.h)):
+            info = np.zeros(5, np.int64)
+            L.refdrv_workload_request(self.h, r, _p(info))
+            nb = int(info[3])
+            ids, lay, nt = np.zeros(nb, np.int64), np.zeros(nb, np.int32), np.zeros(nb, np.int32)
+            k, v = np.zeros((nb, B, d), np.float32), np.zeros((nb, B, d), np.float32)
+            L.refdrv_workload_blocks(self.h, r, B, _p(ids), _p(lay), _p(nt), _p(k), _p(v))
+            lists = []
+            for l in range(sp["n_layers"]):
+                li = np.zeros(int(info[4]), np.int64)
+                L.refdrv_workload_layer_list(self.h, r, l, _p(li))
+                lists.append(li)
+            qs = np.zeros((int(info[2]), sp["n_layers"], d), np.float32)
+            for t in range(int(info[2])):
+                for l in range(sp["n_layers"]):
+                    L.refdrv_workload_query(self.h, r, t, l, _p(qs[t, l]))
+            self.requests.append(dict(request_id=int(info[0]), context=int(info[1]), steps=int(info[2]), ids=ids,
+                                      layers=lay, ntok=nt, keys=k, values=v, lists=lists, queries=qs))
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.L.refdrv_workload_destroy(self.h)
+            self.h = None
+
 
 class RefStore:
     def __init__(self, drv: RefDriver, capacity, n_layers, partitioned, fifo, miss_ms):

@@ -25,6 +25,7 @@
 #include "psattn/pipeline.hpp"
 #include "psattn/scenario.hpp"
 #include "psattn/store.hpp"
+#include "psattn/workload.hpp"
 
 namespace {
 
@@ -319,6 +320,75 @@ double refdrv_block_log_as_oracle(const float* q, int32_t d, int32_t ntok, const
     b.values.assign(b.keys.size(), 0.0f);
     return psattn::block_log_as_oracle(std::span<const float>(q, static_cast<std::size_t>(d)), b,
                                        scale);
+}
+
+// ---- Reference workload generator (workload.cpp:49-153), exported so the GPU path can be fed the
+// exact inputs of the reference's own scenarios (tradeoff / serving golden reports in proj/out).
+void* refdrv_workload_create(int32_t n_requests, int32_t dim, int32_t block_size, int32_t n_layers,
+                             int32_t context_min, int32_t context_max, int32_t decode_steps, double rho,
+                             double skew, int32_t planted, int32_t planted_alt, uint64_t seed) {
+    try {
+        psattn::WorkloadSpec w;
+        w.n_requests = n_requests;
+        w.dim = dim;
+        w.block_size = block_size;
+        w.n_layers = n_layers;
+        w.context_min = context_min;
+        w.context_max = context_max;
+        w.decode_steps = decode_steps;
+        w.rho = rho;
+        w.skew = skew;
+        w.planted_blocks = planted;
+        w.planted_blocks_alt = planted_alt;
+        w.seed = seed;
+        return new std::vector<psattn::Request>(psattn::generate_workload(w));
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return nullptr;
+    }
+}
+void refdrv_workload_destroy(void* w) { delete static_cast<std::vector<psattn::Request>*>(w); }
+int32_t refdrv_workload_n_requests(void* w) {
+    return static_cast<int32_t>(static_cast<std::vector<psattn::Request>*>(w)->size());
+}
+// info[0..3] = request_id, context_tokens, decode_steps, n_blocks (all layers); info[4] = blocks per layer
+int refdrv_workload_request(void* w, int32_t r, int64_t* info) {
+    const auto& q = static_cast<std::vector<psattn::Request>*>(w)->at(static_cast<std::size_t>(r));
+    info[0] = q.request_id;
+    info[1] = q.context_tokens;
+    info[2] = q.decode_steps;
+    info[3] = static_cast<int64_t>(q.blocks.size());
+    info[4] = static_cast<int64_t>(q.blocks_per_layer());
+    return 0;
+}
+// Blocks in the request's put order: ids, layers, n_tokens, K/V [n][block_size][dim] zero-padded.
+int refdrv_workload_blocks(void* w, int32_t r, int32_t block_size, int64_t* ids, int32_t* layers,
+                           int32_t* ntok, float* keys, float* values) {
+    const auto& q = static_cast<std::vector<psattn::Request>*>(w)->at(static_cast<std::size_t>(r));
+    for (std::size_t i = 0; i < q.blocks.size(); ++i) {
+        const auto& b = *q.blocks[i];
+        ids[i] = b.block_id;
+        layers[i] = b.layer_id;
+        ntok[i] = b.n_tokens;
+        const std::size_t stride = static_cast<std::size_t>(block_size) * b.dim;
+        std::memset(keys + i * stride, 0, stride * sizeof(float));
+        std::memset(values + i * stride, 0, stride * sizeof(float));
+        std::memcpy(keys + i * stride, b.keys.data(), b.keys.size() * sizeof(float));
+        std::memcpy(values + i * stride, b.values.data(), b.values.size() * sizeof(float));
+    }
+    return 0;
+}
+int refdrv_workload_layer_list(void* w, int32_t r, int32_t layer, int64_t* ids) {
+    const auto& q = static_cast<std::vector<psattn::Request>*>(w)->at(static_cast<std::size_t>(r));
+    const auto& l = q.layer_blocks.at(static_cast<std::size_t>(layer));
+    std::memcpy(ids, l.data(), l.size() * sizeof(int64_t));
+    return 0;
+}
+int refdrv_workload_query(void* w, int32_t r, int32_t step, int32_t layer, float* out) {
+    const auto& q = static_cast<std::vector<psattn::Request>*>(w)->at(static_cast<std::size_t>(r));
+    const auto& v = q.step_queries.at(static_cast<std::size_t>(step)).at(static_cast<std::size_t>(layer));
+    std::memcpy(out, v.data(), v.size() * sizeof(float));
+    return 0;
 }
 
 }  // extern "C"

@@ -133,3 +133,15 @@ class BatchRun:
     def union_blocks(self, stream=None) -> torch.Tensor:
         check(lib.psattn_batch_union_blocks(C.byref(self.b), _dp(self.ws), _dp(self.union), _stream_ptr(stream)))
         return self.union
+
+    def exact_attention(self, stream=None) -> torch.Tensor:
+        """fp64 exact attention over every block of each list (reference exact_attention_blocks)."""
+        out = torch.empty((self.n_units, self.group, self.dim), dtype=torch.float64, device=self.q.device)
+        check(lib.psattn_exact_attention(self.pool.h, C.byref(self.b), _dp(out), _stream_ptr(stream)))
+        return out
+
+    def tradeoff(self, target: float, stream=None) -> dict:
+        """Reference run_tradeoff on device: k_min of a uniform top-k vs PSA at epsilon = target."""
+        rep = capi.TradeoffReport()
+        check(lib.psattn_tradeoff(self.pool.h, C.byref(self.b), target, C.byref(rep), _stream_ptr(stream)))
+        return rep.as_dict()

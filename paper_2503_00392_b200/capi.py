@@ -71,6 +71,17 @@ class Batch(C.Structure):
                 ("iter_est", C.c_void_p)]
 
 
+class TradeoffReport(C.Structure):
+    _fields_ = [("target_coverage", C.c_double), ("n_queries", C.c_int64), ("max_blocks", C.c_int64),
+                ("k_min", C.c_int64), ("worst_coverage_at_kmin", C.c_double),
+                ("worst_coverage_below_kmin", C.c_double), ("psa_mean_blocks", C.c_double),
+                ("psa_p99_blocks", C.c_double), ("psa_mean_coverage", C.c_double),
+                ("block_access_ratio", C.c_double)]
+
+    def as_dict(self) -> dict:
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
 class SynthParams(C.Structure):
     _fields_ = [("seed", C.c_uint64), ("dim", C.c_int32), ("block_tokens", C.c_int32), ("skew", C.c_float),
                 ("planted_prob", C.c_float), ("round_bf16", C.c_int32), ("reserved", C.c_int32)]
@@ -117,6 +128,8 @@ def _load() -> C.CDLL:
     L.psattn_synth_unit_host.argtypes = [C.POINTER(SynthParams), i64, i64, i64, i64, vp, vp]
     L.psattn_synth_is_planted.argtypes = [C.POINTER(SynthParams), i64, i64]
     L.psattn_pool_fill_synthetic.argtypes = [vp, C.POINTER(SynthParams), i32, vp, vp, vp, vp]
+    L.psattn_exact_attention.argtypes = [vp, C.POINTER(Batch), vp, vp]
+    L.psattn_tradeoff.argtypes = [vp, C.POINTER(Batch), dbl, C.POINTER(TradeoffReport), vp]
     return L
 
 
@@ -134,7 +147,7 @@ EXPORTED = [
     "psattn_profile_enable", "psattn_profile_read", "psattn_set_progressive_kernel",
     "psattn_set_score_kernel", "psattn_set_pipeline",
     "psattn_synth_direction", "psattn_synth_query", "psattn_synth_unit_host", "psattn_synth_is_planted",
-    "psattn_pool_fill_synthetic",
+    "psattn_pool_fill_synthetic", "psattn_exact_attention", "psattn_tradeoff",
 ]
 
 

@@ -214,6 +214,9 @@ static WsLayout ws_layout(const psattn_batch* b) {
     return l;
 }
 
+size_t ws_omass_offset(const psattn_batch* b) { return ws_layout(b).omass; }
+size_t ws_rpos_offset(const psattn_batch* b) { return ws_layout(b).rpos; }
+
 int validate_batch(const psattn_pool* pool, const psattn_batch* b) {
     if (!pool || !b) return fail(PSATTN_ERR_INVALID_ARGUMENT, "psattn_run_batch: null argument");
     if (b->n_units < 1 || b->group < 1 || b->group > 8)

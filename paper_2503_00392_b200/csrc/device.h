@@ -24,5 +24,11 @@ int pool_put(psattn_pool* pool, int64_t n, const int32_t* slots, const int32_t* 
              const float* values, int64_t row_stride_floats, cudaStream_t st);
 int read_slot(const psattn_pool* pool, int64_t slot, int32_t ntok, float* keys, float* values);
 int read_meta(const psattn_pool* pool, int64_t slot, float* mean, float* lo, float* hi);
+int cuda_fail(cudaError_t e, const char* what);
+// psattn_run_batch internals shared with the audit/tradeoff tooling (tradeoff.cu).
+int validate_batch(const psattn_pool* pool, const psattn_batch* b);
+size_t ws_omass_offset(const psattn_batch* b);
+size_t ws_rpos_offset(const psattn_batch* b);
+const PoolView& pool_view(const psattn_pool* pool);
 
 }  // namespace psa
