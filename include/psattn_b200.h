@@ -160,6 +160,49 @@ int psattn_set_score_kernel(int32_t mode);
 int psattn_profile_enable(int32_t enable);
 int psattn_profile_read(double* ms, int64_t* count, int32_t reset);
 
+/* ---- Two-tier KV block store: pinned host backing tier + HBM fast tier ----
+ * The paper's KV-cache manager with the reference TieredBlockStore's observable semantics
+ * (store.hpp:16-120, store.cpp:11-205): every block's K/V lives in pinned, device-mapped
+ * host memory; `fast_slots` HBM slots form one Unified LRU/FIFO domain shared by all
+ * layers or LayerPartitioned floor(fast_slots / n_layers) slots per layer; metadata of
+ * every block stays resident in HBM. Blocks are named by their index in [0, n_blocks). */
+typedef struct psattn_tier psattn_tier;
+typedef struct {
+    int32_t dim;
+    int32_t block_tokens;
+    int32_t kv_dtype;        /* PSATTN_KV_* */
+    int32_t n_layers;
+    int64_t n_blocks;        /* backing-tier capacity (logical blocks) */
+    int64_t fast_slots;      /* HBM fast-tier capacity (reference fast_capacity_slots) */
+    int32_t pool_policy;     /* PSATTN_POOL_* */
+    int32_t eviction_policy; /* PSATTN_EVICT_* */
+} psattn_tier_desc;
+
+int psattn_tier_create(const psattn_tier_desc* desc, psattn_tier** out);
+void psattn_tier_destroy(psattn_tier* t);
+/* put_block (reference store.cpp:59-78) for n blocks: host fp32 K/V [n][block_tokens][dim]
+ * (rows past ntok ignored) into the host tier, metadata built in HBM, then write-allocated
+ * into the fast tier (evictions counted, installed into HBM). owners may be NULL (owner 0).
+ * Duplicate index / bad layer / empty block -> PSATTN_ERR_RUNTIME. Synchronous. */
+int psattn_tier_put_blocks(psattn_tier* t, int64_t n, const int64_t* blocks, const int32_t* layers,
+                           const int32_t* ntok, const int64_t* owners, const float* keys, const float* values);
+/* release_request (reference store.cpp:152-170): drops the owner's blocks from both tiers. */
+int psattn_tier_release_request(psattn_tier* t, int64_t owner);
+/* psattn_run_batch over block indices (b->slots): fast-tier blocks are read from HBM, the others
+ * zero-copy from the host tier; then the loads are accounted in psa_attention_batched's order
+ * (reference engine.cpp:173-209: lockstep rounds over the batch's queries, one microbatch of
+ * ranks each) through the LRU/FIFO domains, and blocks that entered the fast tier are installed
+ * into HBM on `stream`. Synchronous (the accounting needs the processed ranks). */
+int psattn_tier_run_batch(psattn_tier* t, const psattn_batch* b, void* workspace, void* stream);
+/* Reference CacheStats semantics (bytes = fp32 payload 2*n*d*4 per miss); layer -1 = totals. */
+int psattn_tier_stats(psattn_tier* t, int32_t layer, psattn_cache_stats* out);
+/* HBM slot of a block (-1: host tier only). */
+int psattn_tier_resident(psattn_tier* t, int64_t block, int32_t* out_slot);
+/* Bytes actually installed host -> HBM so far (pool dtype, whole slots). */
+int psattn_tier_h2d_bytes(psattn_tier* t, uint64_t* out);
+/* The tier's device pool (metadata, ntok and layout; for psattn_batch_workspace_bytes users). */
+psattn_pool* psattn_tier_pool(psattn_tier* t);
+
 /* ---- Oracle / audit tooling (test and report mode; reads every block of every list) ---- */
 
 /* fp64 exact attention over every block of each list, in list order

@@ -458,5 +458,44 @@ class RefStore:
                 for i in range(nq)], int(rounds.value)
 
 
+def _batched_ragged(self, qs, ids, off, cfg: Config):
+    """psa_attention_batched over ragged lists ids[off[i]:off[i+1]]; returns (results with processed ids, rounds)."""
+    L = self.L
+    L.refdrv_batched_ragged.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
+                                        C.POINTER(Config), C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                        C.c_void_p, C.POINTER(C.c_uint64)]
+    qs = np.ascontiguousarray(qs, np.float32)
+    ids = np.ascontiguousarray(ids, np.int64)
+    off = np.ascontiguousarray(off, np.int64)
+    nq, d = qs.shape
+    outs = np.zeros((nq, d), np.float32)
+    su = np.zeros((nq, 3), np.uint64)
+    sf = np.zeros((nq, 2), np.float64)
+    term = np.zeros(nq, np.int32)
+    pids = np.zeros(ids.size, np.int64)
+    rounds = C.c_uint64()
+    st = L.refdrv_batched_ragged(self.h, _p(qs), nq, d, _p(ids), _p(off), C.byref(cfg), _p(outs), _p(su), _p(sf),
+                                 _p(term), _p(pids), C.byref(rounds))
+    if st:
+        raise RuntimeError(self.drv.error())
+    return [QueryResult(outs[i], int(su[i, 0]), int(su[i, 1]), float(sf[i, 0]),
+                        None if sf[i, 1] < 0 else float(sf[i, 1]), bool(term[i]),
+                        pids[off[i]: off[i] + int(su[i, 0])].copy()) for i in range(nq)], int(rounds.value)
+
+
+RefStore.batched_ragged = _batched_ragged
+
+
+def _load_ids(self, ids):
+    self.L.refdrv_load_ids.argtypes = [C.c_void_p, C.c_void_p, C.c_int64]
+    ids = np.ascontiguousarray(ids, np.int64)
+    st = self.L.refdrv_load_ids(self.h, _p(ids), ids.size)
+    if st:
+        raise RuntimeError(self.drv.error())
+
+
+RefStore.load_ids = _load_ids
+
+
 def ref_available() -> bool:
     return os.path.exists(REFDRV_SO)

@@ -282,6 +282,42 @@ int refdrv_batched(void* s, const float* qs, int32_t nq, int32_t d, const int64_
     });
 }
 
+// store.load_block for each id in order (cache accounting replay of a given load sequence).
+int refdrv_load_ids(void* s, const int64_t* ids, int64_t n) {
+    return guarded([&] {
+        auto& store = static_cast<Store*>(s)->impl;
+        for (int64_t i = 0; i < n; ++i) store.load_block(ids[i]);
+        return 0;
+    });
+}
+
+// psa_attention_batched over ragged lists: query i's blocks are ids[off[i] .. off[i+1]);
+// processed ids of query i go to pids[off[i] ..] (count = blocks_processed).
+int refdrv_batched_ragged(void* s, const float* qs, int32_t nq, int32_t d, const int64_t* ids, const int64_t* off,
+                          const psattn_config* cfg, float* outs, uint64_t* stats_u64, double* stats_f64,
+                          int32_t* terminated, int64_t* pids, uint64_t* n_rounds) {
+    return guarded([&] {
+        const psattn::PSAConfig c = to_cpp(*cfg);
+        std::vector<psattn::HeadVector> qv(static_cast<std::size_t>(nq));
+        std::vector<std::vector<psattn::BlockId>> lists(static_cast<std::size_t>(nq));
+        for (int32_t i = 0; i < nq; ++i) {
+            const std::size_t ii = static_cast<std::size_t>(i);
+            qv[ii].assign(qs + ii * d, qs + (ii + 1) * d);
+            lists[ii].assign(ids + off[i], ids + off[i + 1]);
+        }
+        auto& store = static_cast<Store*>(s)->impl;
+        const psattn::BatchResult r = psattn::psa_attention_batched(qv, lists, c, store);
+        for (int32_t i = 0; i < nq; ++i) {
+            const std::size_t ii = static_cast<std::size_t>(i);
+            write_result(r.results[ii], {outs + ii * d, stats_u64 + ii * 3, stats_f64 + ii * 2,
+                                         terminated + ii, nullptr, nullptr});
+            std::copy(r.results[ii].processed_ids.begin(), r.results[ii].processed_ids.end(), pids + off[i]);
+        }
+        *n_rounds = r.rounds.size();
+        return 0;
+    });
+}
+
 // Reference metadata for one block (metadata.cpp:8-34).
 int refdrv_build_metadata(int32_t ntok, int32_t d, const float* k, float* mean, float* lo,
                           float* hi) {

@@ -78,6 +78,55 @@ class DevicePool:
         return m, lo, hi
 
 
+class DeviceTier:
+    """psattn_tier: pinned-host backing tier + HBM fast tier (LRU/FIFO, unified or layer-partitioned)
+    with the reference TieredBlockStore's accounting. Batches over it take block indices as slots."""
+
+    def __init__(self, dim, block_tokens, kv_dtype, n_layers, n_blocks, fast_slots,
+                 policy=capi.PSATTN_POOL_UNIFIED, eviction=capi.PSATTN_EVICT_LRU):
+        d = capi.TierDesc(dim, block_tokens, kv_dtype, n_layers, n_blocks, fast_slots, policy, eviction)
+        self.t = C.c_void_p()
+        check(lib.psattn_tier_create(C.byref(d), C.byref(self.t)))
+        self.h = C.c_void_p(lib.psattn_tier_pool(self.t))
+        self.dim, self.block_tokens, self.n_layers = dim, block_tokens, n_layers
+
+    def close(self):
+        if lib is not None and getattr(self, "t", None) is not None and self.t.value:
+            lib.psattn_tier_destroy(self.t)
+            self.t = None
+
+    def __del__(self):
+        self.close()
+
+    def put_blocks(self, blocks, layers, ntok, keys, values, owners=None):
+        b = np.ascontiguousarray(blocks, np.int64)
+        ly = np.ascontiguousarray(layers, np.int32)
+        nt = np.ascontiguousarray(ntok, np.int32)
+        ow = None if owners is None else np.ascontiguousarray(owners, np.int64)
+        k = np.ascontiguousarray(keys, np.float32)
+        v = np.ascontiguousarray(values, np.float32)
+        check(lib.psattn_tier_put_blocks(self.t, b.size, capi._p(b), capi._p(ly), capi._p(nt),
+                                         None if ow is None else capi._p(ow), capi._p(k), capi._p(v)))
+
+    def release(self, owner):
+        check(lib.psattn_tier_release_request(self.t, owner))
+
+    def stats(self, layer=-1) -> dict:
+        s = capi.CacheStats()
+        check(lib.psattn_tier_stats(self.t, layer, C.byref(s)))
+        return dict(hits=s.hits, misses=s.misses, evictions=s.evictions, bytes_transferred=s.bytes_transferred)
+
+    def resident_slot(self, block) -> int:
+        out = C.c_int32()
+        check(lib.psattn_tier_resident(self.t, block, C.byref(out)))
+        return out.value
+
+    def h2d_bytes(self) -> int:
+        out = C.c_uint64()
+        check(lib.psattn_tier_h2d_bytes(self.t, C.byref(out)))
+        return out.value
+
+
 @dataclass
 class BatchConfig:
     epsilon: float = 0.95
@@ -125,7 +174,10 @@ class BatchRun:
         self.union = torch.zeros(self.n_units, dtype=torch.int64, device=dev)
 
     def run(self, stream=None) -> int:
-        check(lib.psattn_run_batch(self.pool.h, C.byref(self.b), _dp(self.ws), _stream_ptr(stream)))
+        if isinstance(self.pool, DeviceTier):
+            check(lib.psattn_tier_run_batch(self.pool.t, C.byref(self.b), _dp(self.ws), _stream_ptr(stream)))
+        else:
+            check(lib.psattn_run_batch(self.pool.h, C.byref(self.b), _dp(self.ws), _stream_ptr(stream)))
         n = C.c_int32()
         lib.psattn_batch_last_launches(C.byref(n))
         return n.value

@@ -82,6 +82,12 @@ class TradeoffReport(C.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
+class TierDesc(C.Structure):
+    _fields_ = [("dim", C.c_int32), ("block_tokens", C.c_int32), ("kv_dtype", C.c_int32), ("n_layers", C.c_int32),
+                ("n_blocks", C.c_int64), ("fast_slots", C.c_int64), ("pool_policy", C.c_int32),
+                ("eviction_policy", C.c_int32)]
+
+
 class SynthParams(C.Structure):
     _fields_ = [("seed", C.c_uint64), ("dim", C.c_int32), ("block_tokens", C.c_int32), ("skew", C.c_float),
                 ("planted_prob", C.c_float), ("round_bf16", C.c_int32), ("reserved", C.c_int32)]
@@ -130,6 +136,16 @@ def _load() -> C.CDLL:
     L.psattn_pool_fill_synthetic.argtypes = [vp, C.POINTER(SynthParams), i32, vp, vp, vp, vp]
     L.psattn_exact_attention.argtypes = [vp, C.POINTER(Batch), vp, vp]
     L.psattn_tradeoff.argtypes = [vp, C.POINTER(Batch), dbl, C.POINTER(TradeoffReport), vp]
+    L.psattn_tier_create.argtypes = [C.POINTER(TierDesc), C.POINTER(vp)]
+    L.psattn_tier_destroy.argtypes = [vp]
+    L.psattn_tier_put_blocks.argtypes = [vp, i64, vp, vp, vp, vp, vp, vp]
+    L.psattn_tier_release_request.argtypes = [vp, i64]
+    L.psattn_tier_run_batch.argtypes = [vp, C.POINTER(Batch), vp, vp]
+    L.psattn_tier_stats.argtypes = [vp, i32, C.POINTER(CacheStats)]
+    L.psattn_tier_resident.argtypes = [vp, i64, C.POINTER(i32)]
+    L.psattn_tier_h2d_bytes.argtypes = [vp, C.POINTER(u64)]
+    L.psattn_tier_pool.argtypes = [vp]
+    L.psattn_tier_pool.restype = vp
     return L
 
 
@@ -148,6 +164,8 @@ EXPORTED = [
     "psattn_set_score_kernel", "psattn_set_pipeline",
     "psattn_synth_direction", "psattn_synth_query", "psattn_synth_unit_host", "psattn_synth_is_planted",
     "psattn_pool_fill_synthetic", "psattn_exact_attention", "psattn_tradeoff",
+    "psattn_tier_create", "psattn_tier_destroy", "psattn_tier_put_blocks", "psattn_tier_release_request",
+    "psattn_tier_run_batch", "psattn_tier_stats", "psattn_tier_resident", "psattn_tier_h2d_bytes", "psattn_tier_pool",
 ]
 
 

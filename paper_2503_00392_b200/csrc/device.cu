@@ -19,6 +19,9 @@
 struct psattn_pool {
     psattn_pool_desc desc{};
     psa::PoolView v{};
+    // two-tier pools only (psattn_tier): pinned host backing tier + HBM location table
+    char* host_kv = nullptr;
+    int32_t* loc = nullptr;
 };
 
 namespace psa {
@@ -128,6 +131,57 @@ static void pack_host(const PoolView& v, int64_t n, const int32_t* ntok, const f
                 dv[j] = (uint16_t)(psa_synth::f2u(psa_synth::round_bf16(vv[j])) >> 16);
             }
         }
+    }
+}
+
+// Two-tier pool: metadata + ntok for n_blocks logical blocks in HBM, K/V of every block in
+// pinned mapped host memory, `fast_slots` HBM K/V slots, loc[] = -1 (nothing resident).
+int pool_create_tiered(const psattn_pool_desc* desc, int64_t n_blocks, int64_t fast_slots, psattn_pool** out) {
+    psattn_pool_desc d = *desc;
+    d.n_slots = 0;
+    int rc = psattn_pool_create(&d, out);
+    if (rc) return rc;
+    psattn_pool* p = *out;
+    PoolView& v = p->v;
+    cudaError_t e;
+    auto bail = [&](cudaError_t err, const char* what) {
+        psattn_pool_destroy(p);
+        *out = nullptr;
+        return cuda_fail(err, what);
+    };
+    if ((e = cudaMalloc(&v.kv, (size_t)std::max<int64_t>(fast_slots, 1) * v.slot_bytes)) != cudaSuccess)
+        return bail(e, "tier HBM slots");
+    if ((e = cudaMalloc(&v.meta, (size_t)n_blocks * v.meta_bytes)) != cudaSuccess) return bail(e, "tier metadata");
+    if ((e = cudaMalloc(&v.ntok, (size_t)n_blocks * 4)) != cudaSuccess) return bail(e, "tier ntok");
+    if ((e = cudaMalloc(&p->loc, (size_t)n_blocks * 4)) != cudaSuccess) return bail(e, "tier location table");
+    if ((e = cudaHostAlloc(&p->host_kv, (size_t)n_blocks * v.slot_bytes, cudaHostAllocMapped)) != cudaSuccess)
+        return bail(e, "tier host backing store");
+    void* dev_alias = nullptr;
+    if ((e = cudaHostGetDevicePointer(&dev_alias, p->host_kv, 0)) != cudaSuccess) return bail(e, "tier host mapping");
+    memset(p->host_kv, 0, (size_t)n_blocks * v.slot_bytes);
+    cudaMemset(v.kv, 0, (size_t)std::max<int64_t>(fast_slots, 1) * v.slot_bytes);
+    cudaMemset(v.meta, 0, (size_t)n_blocks * v.meta_bytes);
+    cudaMemset(v.ntok, 0, (size_t)n_blocks * 4);
+    cudaMemset(p->loc, 0xff, (size_t)n_blocks * 4);
+    if ((e = cudaDeviceSynchronize()) != cudaSuccess) return bail(e, "tier init");
+    v.n_slots = n_blocks;
+    v.loc = p->loc;
+    v.host_kv = static_cast<const char*>(dev_alias);
+    p->desc.n_slots = n_blocks;
+    return PSATTN_OK;
+}
+int32_t* pool_loc(psattn_pool* pool) { return pool->loc; }
+char* pool_host_kv(psattn_pool* pool) { return pool->host_kv; }
+
+// Packs host fp32 blocks (rows past ntok zero) into the host backing tier in the pool dtype.
+void pool_pack_into(const psattn_pool* pool, int64_t n, const int64_t* blocks, const int32_t* ntok, const float* keys,
+                    const float* values) {
+    const PoolView& v = pool->v;
+    const size_t stride = (size_t)v.T * v.d;
+    for (int64_t i = 0; i < n; ++i) {
+        std::vector<char> img;
+        pack_host(v, 1, ntok + i, keys + i * stride, values + i * stride, (int64_t)stride, img);
+        memcpy(pool->host_kv + blocks[i] * v.slot_bytes, img.data(), (size_t)v.slot_bytes);
     }
 }
 
@@ -318,6 +372,8 @@ int psattn_pool_create(const psattn_pool_desc* desc, psattn_pool** out_pool) {
 
 void psattn_pool_destroy(psattn_pool* pool) {
     if (!pool) return;
+    if (pool->host_kv) cudaFreeHost(pool->host_kv);
+    if (pool->loc) cudaFree(pool->loc);
     cudaFree(pool->v.kv);
     cudaFree(pool->v.meta);
     cudaFree(pool->v.ntok);

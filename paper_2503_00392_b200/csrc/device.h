@@ -30,5 +30,11 @@ int validate_batch(const psattn_pool* pool, const psattn_batch* b);
 size_t ws_omass_offset(const psattn_batch* b);
 size_t ws_rpos_offset(const psattn_batch* b);
 const PoolView& pool_view(const psattn_pool* pool);
+// Two-tier pools (tier.cpp).
+int pool_create_tiered(const psattn_pool_desc* desc, int64_t n_blocks, int64_t fast_slots, psattn_pool** out);
+int32_t* pool_loc(psattn_pool* pool);
+char* pool_host_kv(psattn_pool* pool);
+void pool_pack_into(const psattn_pool* pool, int64_t n, const int64_t* blocks, const int32_t* ntok, const float* keys,
+                    const float* values);
 
 }  // namespace psa

@@ -21,7 +21,28 @@ struct PoolView {
     int64_t slot_bytes;
     int64_t meta_bytes;
     int64_t n_slots;
+    // Two-tier pools (psattn_tier): slot indices name LOGICAL blocks (metadata, ntok);
+    // loc[s] >= 0 is the HBM slot holding block s's K/V, loc[s] < 0 means it is read
+    // from the pinned host backing tier at host_kv + s*slot_bytes (zero-copy over
+    // PCIe/C2C). loc == nullptr: the plain HBM pool, K/V of slot s at kv + s*slot_bytes.
+    const int32_t* loc;
+    const char* host_kv;
 };
+
+#ifdef __CUDACC__
+// K rows (then V rows at + T*d) of block s.
+template <typename KV>
+__device__ __forceinline__ const KV* kv_block(const PoolView& p, int64_t s) {
+    if (p.loc) {
+        const int32_t l = __ldg(p.loc + s);
+        if (l < 0) return reinterpret_cast<const KV*>(p.host_kv + s * p.slot_bytes);
+        s = l;
+    }
+    return reinterpret_cast<const KV*>(p.kv + s * p.slot_bytes);
+}
+// HBM-resident (bulk L2 prefetch is issued only for device memory).
+__device__ __forceinline__ bool kv_resident(const PoolView& p, int64_t s) { return !p.loc || __ldg(p.loc + s) >= 0; }
+#endif
 
 // One batched launch: n_units block lists (page tables of slots, ascending
 // block id), g q-heads per list. Workspace arrays are indexed per head at
@@ -55,6 +76,8 @@ int g_for(int g);
 cudaError_t launch_meta_build(const PoolView& p, const int32_t* list, int64_t s0, int64_t s1, cudaStream_t st);
 cudaError_t launch_append(const PoolView& p, int32_t n, const int32_t* slots, const float* keys,
                           const float* values, int32_t* status, cudaStream_t st);
+cudaError_t launch_install(const PoolView& p, const int64_t* d_blocks, const int32_t* d_dst, int64_t n,
+                           cudaStream_t st);
 cudaError_t launch_scatter(const PoolView& p, const void* staged, const int32_t* d_slots, const int32_t* d_ntok,
                            int64_t n, cudaStream_t st);
 cudaError_t launch_synth_fill(const PoolView& p, uint64_t seed, float skew, float prob, int round_bf16,

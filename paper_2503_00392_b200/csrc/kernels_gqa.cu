@@ -97,8 +97,6 @@ __global__ void __launch_bounds__(kPsaThreads, 2) psa_gqa_kernel(PoolView p, Bat
     constexpr int TSH = 5 - Log2<TOK>::v;
     const int my_tok = lane >> TSH;
     const uint64_t pmask = (b.pos_bits >= 64) ? ~0ull : ((1ull << b.pos_bits) - 1ull);
-    const KV* kv = reinterpret_cast<const KV*>(p.kv);
-    const int64_t slot_elems = p.slot_bytes / (int64_t)sizeof(KV);
     const int T = p.T;
     const int64_t v_off = (int64_t)T * d;
 #ifdef PSA_GQA_PROF
@@ -251,8 +249,8 @@ __global__ void __launch_bounds__(kPsaThreads, 2) psa_gqa_kernel(PoolView p, Bat
             // Bulk L2 prefetch of every U block's K (threads 0..) and V (threads 128..): the K pass
             // below then walks L2-resident blocks, and the V pass finds committed blocks in L2.
             const int e = tid & (G * kChunk - 1);
-            if (e < ucount && tid < 2 * G * kChunk)
-                prefetch_l2_bulk(kv + (int64_t)s.uslot[e] * slot_elems + (tid >= G * kChunk ? v_off : 0),
+            if (e < ucount && tid < 2 * G * kChunk && kv_resident(p, s.uslot[e]))
+                prefetch_l2_bulk(kv_block<KV>(p, s.uslot[e]) + (tid >= G * kChunk ? v_off : 0),
                                  (uint32_t)(T * 128 * sizeof(KV)));
         }
         GQA_MARK(2);
@@ -263,7 +261,7 @@ __global__ void __launch_bounds__(kPsaThreads, 2) psa_gqa_kernel(PoolView p, Bat
             const int nt = s.untok[e];
             if constexpr (kMma) {
                 const int gq = lane >> 2, tq = lane & 3;
-                const __nv_bfloat16* kblk = reinterpret_cast<const __nv_bfloat16*>(kv + (int64_t)slot * slot_elems);
+                const __nv_bfloat16* kblk = reinterpret_cast<const __nv_bfloat16*>(kv_block<KV>(p, slot));
                 const int r0 = gq < T ? gq : T - 1, r1 = (gq + 8) < T ? (gq + 8) : T - 1;
                 const uint4* p0 = reinterpret_cast<const uint4*>(kblk + (size_t)r0 * 128 + 32 * tq);
                 const uint4* p1 = reinterpret_cast<const uint4*>(kblk + (size_t)r1 * 128 + 32 * tq);
@@ -311,7 +309,7 @@ __global__ void __launch_bounds__(kPsaThreads, 2) psa_gqa_kernel(PoolView p, Bat
                 }
                 continue;
             }
-            const KV* kp = kv + (int64_t)slot * slot_elems + base;
+            const KV* kp = kv_block<KV>(p, slot) + base;
             float kr[TOK][DPL];
 #pragma unroll
             for (int t = 0; t < TOK; ++t) load_row<DPL>(kp + (size_t)(T == TOK ? t : (t < T ? t : T - 1)) * d, full, lim, kr[t]);
@@ -379,8 +377,8 @@ __global__ void __launch_bounds__(kPsaThreads, 2) psa_gqa_kernel(PoolView p, Bat
             const int h = tid >> 5, r = tid & 31;
             if (h < G && s.live[h] && !s.fin[h]) {
                 const int64_t idx = s.cb[h] + s.commit[h] - s.tr0[h] + r;
-                if (idx < s.tc[h]) {
-                    const KV* bp0 = kv + (int64_t)s.tslot[h][idx] * slot_elems;
+                if (idx < s.tc[h] && kv_resident(p, s.tslot[h][idx])) {
+                    const KV* bp0 = kv_block<KV>(p, s.tslot[h][idx]);
                     prefetch_l2_bulk(bp0, (uint32_t)(T * 128 * sizeof(KV)));
                     prefetch_l2_bulk(bp0 + v_off, (uint32_t)(T * 128 * sizeof(KV)));
                 }
@@ -399,7 +397,7 @@ __global__ void __launch_bounds__(kPsaThreads, 2) psa_gqa_kernel(PoolView p, Bat
                 // Lane (g, t) owns head t, dims [16g, 16g+16): no cross-lane reduction.
                 const int gq = lane >> 2, tq = lane & 3;
                 const __nv_bfloat16* vblk =
-                    reinterpret_cast<const __nv_bfloat16*>(kv + (int64_t)slot * slot_elems + v_off);
+                    reinterpret_cast<const __nv_bfloat16*>(kv_block<KV>(p, slot) + v_off);
                 uint32_t vw[4][8];
 #pragma unroll
                 for (int r = 0; r < 4; ++r) {
@@ -441,7 +439,7 @@ __global__ void __launch_bounds__(kPsaThreads, 2) psa_gqa_kernel(PoolView p, Bat
                 }
                 continue;
             }
-            const KV* vp = kv + (int64_t)slot * slot_elems + v_off + base;
+            const KV* vp = kv_block<KV>(p, slot) + v_off + base;
             float vr[TOK][DPL];
 #pragma unroll
             for (int t = 0; t < TOK; ++t) load_row<DPL>(vp + (size_t)(T == TOK ? t : (t < T ? t : T - 1)) * d, full, lim, vr[t]);

@@ -28,7 +28,7 @@ __global__ void meta_build_kernel(PoolView p, const int32_t* list, int64_t s0, i
     const int64_t slot = list ? (int64_t)list[idx] : idx;
     const int n = p.ntok[slot];
     const int d = p.d;
-    const KV* k = reinterpret_cast<const KV*>(p.kv + slot * p.slot_bytes);
+    const KV* k = kv_block<KV>(p, slot);
     char* rec = p.meta + slot * p.meta_bytes;
     float* mean = reinterpret_cast<float*>(rec);
     KV* lo = reinterpret_cast<KV*>(rec + (size_t)d * 4);
@@ -137,6 +137,24 @@ __global__ void scatter_slots_kernel(PoolView p, const char* __restrict__ staged
     int4* dst = reinterpret_cast<int4*>(p.kv + slot * p.slot_bytes);
     for (int64_t e = threadIdx.x; e < p.slot_bytes / 16; e += blockDim.x) dst[e] = src[e];
     if (threadIdx.x == 0) p.ntok[slot] = ntok[i];
+}
+
+// Two-tier pools: installs blocks[i] from the pinned host backing tier into HBM slot dst[i]
+// (reads over PCIe/C2C, 16-byte vectors; one CTA per block).
+__global__ void install_blocks_kernel(PoolView p, const int64_t* __restrict__ blocks, const int32_t* __restrict__ dst,
+                                      int64_t n) {
+    const int64_t i = blockIdx.x;
+    if (i >= n) return;
+    const int4* src = reinterpret_cast<const int4*>(p.host_kv + blocks[i] * p.slot_bytes);
+    int4* out = reinterpret_cast<int4*>(p.kv + (int64_t)dst[i] * p.slot_bytes);
+    for (int64_t e = threadIdx.x; e < p.slot_bytes / 16; e += blockDim.x) out[e] = src[e];
+}
+
+cudaError_t launch_install(const PoolView& p, const int64_t* d_blocks, const int32_t* d_dst, int64_t n,
+                           cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    install_blocks_kernel<<<(unsigned)n, 256, 0, st>>>(p, d_blocks, d_dst, n);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_scatter(const PoolView& p, const void* staged, const int32_t* d_slots, const int32_t* d_ntok,

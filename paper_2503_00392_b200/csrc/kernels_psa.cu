@@ -148,8 +148,6 @@ __global__ void __launch_bounds__(kPsaThreads, 3) psa_kernel(PoolView p, BatchVi
     double acc = -INFINITY, mn = INFINITY;  // coverage state (warp 0, lane-uniform)
 
     const double* omass = b.has_oracle ? (b.omass + hb) : nullptr;
-    const KV* kv = reinterpret_cast<const KV*>(p.kv);
-    const int64_t slot_elems = p.slot_bytes / (int64_t)sizeof(KV);
     const int64_t v_off = (int64_t)p.T * d;
     const int T = p.T;
 
@@ -178,7 +176,7 @@ __global__ void __launch_bounds__(kPsaThreads, 3) psa_kernel(PoolView p, BatchVi
             const int nt = s.tntok[ci + rl];
             if constexpr (kMma) {
                 float slo, shi;
-                block_scores_mma(kv + (int64_t)slot * slot_elems, T, lane, qb, slo, shi);
+                block_scores_mma(kv_block<KV>(p, slot), T, lane, qb, slo, shi);
                 const int g8 = lane >> 2;
                 slo = (g8 < nt) ? slo * fscale : -INFINITY;
                 shi = (g8 + 8 < nt) ? shi * fscale : -INFINITY;
@@ -201,7 +199,7 @@ __global__ void __launch_bounds__(kPsaThreads, 3) psa_kernel(PoolView p, BatchVi
                 }
                 continue;
             }
-            const KV* kp = kv + (int64_t)slot * slot_elems + base;
+            const KV* kp = kv_block<KV>(p, slot) + base;
             // Branch-free: rows in [ntok, T) are zero-filled in the pool and rows >= T
             // (TOK > T) re-read row T-1, so all TOK loads issue before the first use;
             // tokens >= ntok are masked below.
@@ -264,7 +262,7 @@ __global__ void __launch_bounds__(kPsaThreads, 3) psa_kernel(PoolView p, BatchVi
             if (rl >= commit) break;
             const int32_t slot = s.tslot[ci + rl];
             const int nt = s.tntok[ci + rl];
-            const KV* vp = kv + (int64_t)slot * slot_elems + v_off + base;
+            const KV* vp = kv_block<KV>(p, slot) + v_off + base;
             float ob[DPL];
 #pragma unroll
             for (int jj = 0; jj < DPL; ++jj) ob[jj] = 0.0f;

@@ -446,7 +446,7 @@ __global__ void __launch_bounds__(kScoreWarps * 32) oracle_mass_kernel(PoolView 
     for (int64_t pos = (int64_t)blockIdx.x * kScoreWarps + warp; pos < n; pos += (int64_t)gridDim.x * kScoreWarps) {
         const int32_t slot = b.slots[off + pos];
         const int nt = p.ntok[slot];
-        const KV* k = reinterpret_cast<const KV*>(p.kv + (int64_t)slot * p.slot_bytes) + base;
+        const KV* k = kv_block<KV>(p, slot) + base;
         for (int h = 0; h < b.g; ++h) {
             float qf[DPL];
             load_row<DPL>(b.q + ((size_t)u * b.g + h) * d + base, full, lim, qf);

@@ -44,8 +44,6 @@ __global__ void __launch_bounds__(kExactThreads) exact_attention_kernel(PoolView
     const int d = b.d;
     const int64_t off = b.list_off[u], n = b.list_off[u + 1] - off;
     const float* q = b.q + (size_t)qi * d;
-    const KV* kv = reinterpret_cast<const KV*>(p.kv);
-    const int64_t se = p.slot_bytes / (int64_t)sizeof(KV);
     const int64_t voff = (int64_t)p.T * d;
     double qd[8];
 #pragma unroll
@@ -61,7 +59,7 @@ __global__ void __launch_bounds__(kExactThreads) exact_attention_kernel(PoolView
     for (int64_t i = 0; i < n; ++i) {
         const int32_t slot = b.slots[off + i];
         const int nt = p.ntok[slot];
-        for (int t = warp; t < nt; t += W) mx = fmax(mx, score(kv + slot * se + (int64_t)t * d));
+        for (int t = warp; t < nt; t += W) mx = fmax(mx, score(kv_block<KV>(p, slot) + (int64_t)t * d));
     }
     if (lane == 0) red[warp] = mx;
     __syncthreads();
@@ -79,9 +77,9 @@ __global__ void __launch_bounds__(kExactThreads) exact_attention_kernel(PoolView
         const int32_t slot = b.slots[off + i];
         const int nt = p.ntok[slot];
         for (int t = warp; t < nt; t += W) {
-            const double w = exp(score(kv + slot * se + (int64_t)t * d) - mx);
+            const double w = exp(score(kv_block<KV>(p, slot) + (int64_t)t * d) - mx);
             es += w;
-            const KV* vrow = kv + slot * se + voff + (int64_t)t * d;
+            const KV* vrow = kv_block<KV>(p, slot) + voff + (int64_t)t * d;
 #pragma unroll
             for (int j = 0; j < 8; ++j)
                 if (lane + 32 * j < d) o[j] = fma(w, (double)KVT<KV>::to_f(vrow[lane + 32 * j]), o[j]);

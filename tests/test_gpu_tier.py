@@ -1,0 +1,200 @@
+"""Two-tier KV store (psattn_tier) and BASELINE config 4.
+
+* Cache semantics equal the reference TieredBlockStore (store.cpp:11-205) driven by the
+  reference's psa_attention_batched (engine.cpp:173-209): same per-layer hits / misses /
+  evictions / bytes for Unified and LayerPartitioned pools under LRU and FIFO, across
+  consecutive decode steps, with the same processed blocks and outputs.
+* Config 4: a mixed-length batch (8K-128K context, ragged last blocks) over layers with uneven
+  attention budgets (planted blocks per layer 2 / 16 / 128 / isotropic) through a fast tier
+  smaller than the KV: results are independent of placement (== the all-HBM pool), the
+  accounting equals the reference store replaying the same loads, and the unified pool's
+  hit count is reported against the layer-partitioned one.
+"""
+import numpy as np
+import pytest
+
+from helpers import check_parity
+from oracle.pyoracle import BlockSet, make_config
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def mods():
+    from paper_2503_00392_b200 import batch, capi
+    return capi, batch
+
+
+def lockstep_loads(ranked_ids, bp, m):
+    """Load order of psa_attention_batched: rounds over the queries, one microbatch each."""
+    cur = [0] * len(bp)
+    out = []
+    live = True
+    while live:
+        live = False
+        for i in range(len(bp)):
+            e = min(cur[i] + m, bp[i])
+            out.extend(ranked_ids[i][cur[i]:e])
+            cur[i] = e
+            live |= e < bp[i]
+    return np.array(out, np.int64)
+
+
+def tier_batch(mods, tier, qs, lists, cfg, dev):
+    """qs [U][g][d]; lists: per-unit arrays of block indices (ascending)."""
+    capi, batch = mods
+    off = np.zeros(len(lists) + 1, np.int64)
+    off[1:] = np.cumsum([len(x) for x in lists])
+    return batch.BatchRun(tier, torch.tensor(np.asarray(qs, np.float32), device=dev),
+                          torch.tensor(np.concatenate(lists).astype(np.int32), device=dev),
+                          torch.tensor(off, device=dev), max(len(x) for x in lists), cfg, want_ranked=True), off
+
+
+def ranked_of(run, off, u, h):
+    n = int(off[u + 1] - off[u])
+    hb = int(off[u]) * run.group + h * n
+    return run.ranked[hb: hb + n].cpu().numpy()
+
+
+@pytest.mark.parametrize("policy", [0, 1])
+@pytest.mark.parametrize("eviction", [0, 1])
+def test_tier_matches_reference_store(mods, ref, policy, eviction):
+    capi, batch = mods
+    rng = np.random.default_rng(10 + 2 * policy + eviction)
+    d, T, L = 32, 8, 3
+    # 4 requests x 3 layers, ragged lists (blocks of the layer, ascending id), ragged last blocks
+    blocks, layers, ntok, owners, lists = [], [], [], [], []
+    bid = 0
+    for r in range(4):
+        for l in range(L):
+            n = int(rng.integers(20, 60))
+            ids = []
+            for i in range(n):
+                blocks.append(bid)
+                layers.append(l)
+                ntok.append(T if i < n - 1 else int(rng.integers(1, T + 1)))
+                owners.append(r)
+                ids.append(bid)
+                bid += 1
+            lists.append(np.array(ids, np.int64))
+    nb = len(blocks)
+    K = rng.standard_normal((nb, T, d)).astype(np.float32)
+    V = rng.standard_normal((nb, T, d)).astype(np.float32)
+    bias = rng.standard_normal(d).astype(np.float32) * 2.5
+    planted = rng.random(nb) < 0.1
+    K[planted] += bias
+    for i in range(nb):
+        K[i, ntok[i]:] = 0
+        V[i, ntok[i]:] = 0
+    cap = 90
+    tier = batch.DeviceTier(d, T, capi.PSATTN_KV_F32, L, nb, cap, policy, eviction)
+    tier.put_blocks(blocks, layers, ntok, K, V, owners)
+    st = ref.store(capacity=cap, n_layers=L, partitioned=policy, fifo=eviction)
+    for i in range(nb):
+        st.put(i, K[i, :ntok[i]], V[i, :ntok[i]], layers[i], owners[i])
+    assert tier.stats() == st.stats()
+    dev = torch.device("cuda")
+    g = 2
+    for step in range(3):
+        cfg = dict(epsilon=[0.9, 0.95, 0.8][step], microbatch_size=[1, 3, 2][step])
+        qs = rng.standard_normal((len(lists), g, d)).astype(np.float32) + bias * 0.3
+        run, off = tier_batch(mods, tier, qs, lists, batch.BatchConfig(**cfg), dev)
+        run.run()
+        torch.cuda.synchronize()
+        allq = qs.reshape(-1, d)
+        rlists = [lists[i // g] for i in range(len(allq))]
+        roff = np.zeros(len(rlists) + 1, np.int64)
+        roff[1:] = np.cumsum([len(x) for x in rlists])
+        res, _ = st.batched_ragged(allq, np.concatenate(rlists), roff, make_config(**cfg))
+        for u in range(len(lists)):
+            for h in range(g):
+                o = res[u * g + h]
+                bp = int(run.bp[u * g + h])
+                ids = lists[u][ranked_of(run, off, u, h)[:bp]]
+                assert bp == o.blocks_processed and np.array_equal(ids, o.processed_ids), (step, u, h)
+                assert np.max(np.abs(run.out[u, h].cpu().numpy() - o.output)) <= 1e-3
+        assert tier.stats() == st.stats(), step
+        for l in range(L):
+            assert tier.stats(l) == st.layer_stats(l), (step, l)
+        # the fast tier holds exactly the reference's resident set, in distinct HBM slots
+        slots = [tier.resident_slot(i) for i in range(nb)]
+        used = [s for s in slots if s >= 0]
+        assert len(used) == len(set(used)) and len(used) <= cap
+        assert [s >= 0 for s in slots] == [bool(st.contains(i)) for i in range(nb)]
+    # release drops a request from both tiers
+    tier.release(1)
+    st.release(1)
+    assert tier.stats() == st.stats()
+
+
+def test_config4_mixed_lengths_uneven_layers(mods, oracle, ref):
+    capi, batch = mods
+    d, T, g = 128, 16, 4
+    ctxs = [8192 + 5, 40960 + 3, 131072]
+    planted_per_layer = [2 / 2048, 16 / 2048, 128 / 2048, 0.0]
+    L = len(planted_per_layer)
+    units = []  # (request, layer, unit_id, tokens)
+    for r, c in enumerate(ctxs):
+        for l in range(L):
+            units.append((r, l, 1000 + 10 * r + l, c))
+    blocks, layers, ntok, lists, K, V, qs, bsets = [], [], [], [], [], [], [], []
+    base = 0
+    for r, l, uid, c in units:
+        p = capi.synth_params(seed=4, dim=d, block_tokens=T, skew=8.0, planted_prob=planted_per_layer[l],
+                              round_bf16=1)
+        k, v = capi.synth_unit_host(p, uid, c)
+        n = k.shape[0]
+        nt = [min(T, c - i * T) for i in range(n)]
+        blocks.extend(range(base, base + n))
+        layers.extend([l] * n)
+        ntok.extend(nt)
+        K.append(k)
+        V.append(v)
+        lists.append(np.arange(base, base + n, dtype=np.int64))
+        qs.append([capi.synth_query(p, uid, h) for h in range(g)])
+        bsets.append((k, v, nt))
+        base += n
+    K, V = np.concatenate(K), np.concatenate(V)
+    nb = base
+    cap = nb // 4
+    dev = torch.device("cuda")
+    cfg = batch.BatchConfig(epsilon=0.95)
+    # all-HBM reference placement: the plain pool
+    pool = batch.DevicePool(d, T, capi.PSATTN_KV_BF16, nb)
+    pool.put_blocks(np.arange(nb, dtype=np.int32), ntok, K, V)
+    base_run, off = tier_batch(mods, pool, qs, lists, cfg, dev)
+    base_run.run()
+    torch.cuda.synchronize()
+    hits = {}
+    for policy in (0, 1):
+        tier = batch.DeviceTier(d, T, capi.PSATTN_KV_BF16, L, nb, cap, policy, 0)
+        tier.put_blocks(blocks, layers, ntok, K, V)
+        st = ref.store(capacity=cap, n_layers=L, partitioned=policy, fifo=0)
+        for i in range(nb):
+            st.put(i, K[i, :ntok[i]], V[i, :ntok[i]], layers[i], 0)
+        for step in range(2):
+            run, off = tier_batch(mods, tier, qs, lists, cfg, dev)
+            run.run()
+            torch.cuda.synchronize()
+            # placement never changes results: bit-identical to the all-HBM pool
+            assert torch.equal(run.out, base_run.out) and torch.equal(run.bp, base_run.bp)
+            bp = run.bp.cpu().numpy()
+            ranked = [lists[u][ranked_of(run, off, u, h)[:bp[u * g + h]]] for u in range(len(lists)) for h in range(g)]
+            st.load_ids(lockstep_loads(ranked, bp, cfg.microbatch_size))
+            assert tier.stats() == st.stats(), (policy, step)
+            for l in range(L):
+                assert tier.stats(l) == st.layer_stats(l), (policy, step, l)
+        hits[policy] = tier.stats()["hits"]
+        assert tier.h2d_bytes() > 0
+    # uneven budgets: the unified pool serves at least as many loads from HBM
+    assert hits[0] >= hits[1], hits
+    # parity of the base run against the C oracle on one head of every unit
+    for u, (k, v, nt) in enumerate(bsets):
+        bs = BlockSet([k[i, :nt[i]] for i in range(len(nt))], [v[i, :nt[i]] for i in range(len(nt))])
+        h = u % g
+        bpq = int(base_run.bp[u * g + h])
+        ids = ranked_of(base_run, off, u, h)[:bpq]
+        check_parity(oracle, qs[u][h], bs, make_config(epsilon=0.95), 0, ids, bpq,
+                     base_run.out[u, h].cpu().numpy(), float(base_run.est[u * g + h]))
