@@ -203,6 +203,46 @@ int psattn_tier_h2d_bytes(psattn_tier* t, uint64_t* out);
 /* The tier's device pool (metadata, ntok and layout; for psattn_batch_workspace_bytes users). */
 psattn_pool* psattn_tier_pool(psattn_tier* t);
 
+/* ---- Batched serving loop on the GPU path (reference run_serving,
+ * serving.cpp:100-229). FCFS head-only admission while one microbatch per live (request,
+ * layer) fits the fast tier; every decode step runs ONE device batch per layer over the live
+ * requests through a fresh two-tier store (psattn_tier); finished requests are released.
+ * The reference's simulated TBT cost model (ServingConfig, serving.hpp:26-34; simulate_pipeline,
+ * pipeline.cpp:153-175) is evaluated on the device run's hit/miss series, so the report rows
+ * (scenario.cpp:303-341) compare with the reference's exactly; gpu_ms is measured device time. */
+typedef struct psattn_serving psattn_serving;
+typedef struct {
+    double miss_cost_ms;
+    double hit_cost_ms;
+    double compute_cost_ms;
+    int32_t overlap;
+    int32_t reserved;
+} psattn_serving_cost;
+typedef struct {
+    /* reference ReportRow (scenario.cpp:303-341) */
+    double mean_blocks, p99_blocks, kv_fraction, mean_coverage, min_coverage, hit_ratio;
+    double tbt_p50_ms, tbt_p99_ms, overlap_eff;
+    psattn_cache_stats store_stats;
+    int64_t n_calls, n_steps, completed_requests, device_batches;
+    double sim_time_ms;
+    double gpu_ms; /* device time of the per-layer batches (CUDA events) */
+} psattn_serving_report;
+enum { PSATTN_METHOD_PSA = 0, PSATTN_METHOD_TOPK = 1, PSATTN_METHOD_EXACT = 2 };
+/* store: the fast tier (dim, block_tokens, kv_dtype, n_layers, fast_slots, policies; n_blocks
+ * is derived from the requests); engine: reference psattn_config. */
+int psattn_serving_create(const psattn_tier_desc* store, const psattn_config* engine, const psattn_serving_cost* cost,
+                          psattn_serving** out);
+void psattn_serving_destroy(psattn_serving* s);
+/* One request (reference workload Request, workload.hpp:36-50): layer_blocks [n_layers][blocks_per_layer]
+ * ids in sequence order; blocks (ids, layers, ntok, fp32 K/V [n_blocks][block_tokens][dim]);
+ * queries [decode_steps][n_layers][dim]. Copied. */
+int psattn_serving_add_request(psattn_serving* s, int64_t request_id, double arrival_s, int32_t decode_steps,
+                               int32_t n_layers, int64_t blocks_per_layer, const int64_t* layer_blocks,
+                               int64_t n_blocks, const int64_t* block_ids, const int32_t* block_layers,
+                               const int32_t* ntok, const float* keys, const float* values, const float* queries);
+/* Runs every added request to completion with method PSATTN_METHOD_* (epsilon for PSA, k for top-k). */
+int psattn_serving_run(psattn_serving* s, int32_t method, double epsilon, int64_t k, psattn_serving_report* out);
+
 /* ---- Oracle / audit tooling (test and report mode; reads every block of every list) ---- */
 
 /* fp64 exact attention over every block of each list, in list order

@@ -26,6 +26,7 @@ PSATTN_EVICT_LRU, PSATTN_EVICT_FIFO = 0, 1
 PSATTN_EST_MEAN, PSATTN_EST_CUBOID_UPPER, PSATTN_EST_CUBOID_MEAN = 0, 1, 2
 PSATTN_RANK_ESTIMATED, PSATTN_RANK_ORACLE = 0, 1
 PSATTN_KV_F32, PSATTN_KV_BF16 = 0, 1
+PSATTN_METHOD_PSA, PSATTN_METHOD_TOPK, PSATTN_METHOD_EXACT = 0, 1, 2
 
 
 class StoreOptions(C.Structure):
@@ -88,6 +89,27 @@ class TierDesc(C.Structure):
                 ("eviction_policy", C.c_int32)]
 
 
+class ServingCost(C.Structure):
+    _fields_ = [("miss_cost_ms", C.c_double), ("hit_cost_ms", C.c_double), ("compute_cost_ms", C.c_double),
+                ("overlap", C.c_int32), ("reserved", C.c_int32)]
+
+
+class ServingReport(C.Structure):
+    _fields_ = [("mean_blocks", C.c_double), ("p99_blocks", C.c_double), ("kv_fraction", C.c_double),
+                ("mean_coverage", C.c_double), ("min_coverage", C.c_double), ("hit_ratio", C.c_double),
+                ("tbt_p50_ms", C.c_double), ("tbt_p99_ms", C.c_double), ("overlap_eff", C.c_double),
+                ("store_stats", CacheStats), ("n_calls", C.c_int64), ("n_steps", C.c_int64),
+                ("completed_requests", C.c_int64), ("device_batches", C.c_int64), ("sim_time_ms", C.c_double),
+                ("gpu_ms", C.c_double)]
+
+    def as_dict(self) -> dict:
+        d = {k: getattr(self, k) for k, _ in self._fields_ if k != "store_stats"}
+        s = self.store_stats
+        d["store_stats"] = dict(hits=s.hits, misses=s.misses, evictions=s.evictions,
+                                bytes_transferred=s.bytes_transferred)
+        return d
+
+
 class SynthParams(C.Structure):
     _fields_ = [("seed", C.c_uint64), ("dim", C.c_int32), ("block_tokens", C.c_int32), ("skew", C.c_float),
                 ("planted_prob", C.c_float), ("round_bf16", C.c_int32), ("reserved", C.c_int32)]
@@ -146,6 +168,10 @@ def _load() -> C.CDLL:
     L.psattn_tier_h2d_bytes.argtypes = [vp, C.POINTER(u64)]
     L.psattn_tier_pool.argtypes = [vp]
     L.psattn_tier_pool.restype = vp
+    L.psattn_serving_create.argtypes = [C.POINTER(TierDesc), C.POINTER(Config), C.POINTER(ServingCost), C.POINTER(vp)]
+    L.psattn_serving_destroy.argtypes = [vp]
+    L.psattn_serving_add_request.argtypes = [vp, i64, dbl, i32, i32, i64, vp, i64, vp, vp, vp, vp, vp, vp]
+    L.psattn_serving_run.argtypes = [vp, i32, dbl, i64, C.POINTER(ServingReport)]
     return L
 
 
@@ -166,6 +192,7 @@ EXPORTED = [
     "psattn_pool_fill_synthetic", "psattn_exact_attention", "psattn_tradeoff",
     "psattn_tier_create", "psattn_tier_destroy", "psattn_tier_put_blocks", "psattn_tier_release_request",
     "psattn_tier_run_batch", "psattn_tier_stats", "psattn_tier_resident", "psattn_tier_h2d_bytes", "psattn_tier_pool",
+    "psattn_serving_create", "psattn_serving_destroy", "psattn_serving_add_request", "psattn_serving_run",
 ]
 
 
@@ -301,3 +328,36 @@ def synth_unit_host(p: SynthParams, unit_id: int, n_tokens: int, first_block=0, 
 
 def synth_is_planted(p: SynthParams, unit_id: int, block: int) -> bool:
     return bool(lib.psattn_synth_is_planted(C.byref(p), unit_id, block))
+
+
+class Serving:
+    """psattn_serving: the batched FCFS serving loop over the two-tier store (reference run_serving)."""
+
+    def __init__(self, store: TierDesc, engine: Config, cost: ServingCost):
+        self.h = C.c_void_p()
+        check(lib.psattn_serving_create(C.byref(store), C.byref(engine), C.byref(cost), C.byref(self.h)))
+
+    def close(self):
+        if lib is not None and getattr(self, "h", None) is not None and self.h.value:
+            lib.psattn_serving_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
+
+    def add_request(self, request_id, arrival_s, steps, layer_blocks, block_ids, block_layers, ntok, keys, values,
+                    queries):
+        lb = np.ascontiguousarray(layer_blocks, np.int64)
+        ids = np.ascontiguousarray(block_ids, np.int64)
+        ly = np.ascontiguousarray(block_layers, np.int32)
+        nt = np.ascontiguousarray(ntok, np.int32)
+        k = np.ascontiguousarray(keys, np.float32)
+        v = np.ascontiguousarray(values, np.float32)
+        q = np.ascontiguousarray(queries, np.float32)
+        check(lib.psattn_serving_add_request(self.h, request_id, arrival_s, steps, lb.shape[0], lb.shape[1], _p(lb),
+                                             ids.size, _p(ids), _p(ly), _p(nt), _p(k), _p(v), _p(q)))
+
+    def run(self, method: int, epsilon: float = 0.95, k: int = 0) -> dict:
+        rep = ServingReport()
+        check(lib.psattn_serving_run(self.h, method, epsilon, k, C.byref(rep)))
+        return rep.as_dict()

@@ -16,7 +16,9 @@
 // reference counts them — and the blocks that entered the fast tier are installed into
 // their HBM slots by one copy kernel on the caller's stream.
 #include <algorithm>
+#include <cmath>
 #include <cstring>
+#include <limits>
 #include <list>
 #include <mutex>
 #include <string>
@@ -247,11 +249,21 @@ int psattn_tier_release_request(psattn_tier* t, int64_t owner) {
     return install_pending(t, nullptr);
 }
 
-int psattn_tier_run_batch(psattn_tier* t, const psattn_batch* b, void* workspace, void* stream) {
-    if (!t || !b) return fail(PSATTN_ERR_INVALID_ARGUMENT, "psattn_tier_run_batch: null argument");
-    std::lock_guard<std::mutex> lk(t->mu);
-    cudaStream_t st = (cudaStream_t)stream;
-    int rc = psattn_run_batch(t->pool, b, workspace, stream);
+}  // extern "C"
+
+namespace psa {
+
+// One microbatch load's accounting (reference IterationStats, engine.hpp:57-62).
+struct TierIter {
+    int64_t blocks = 0, hits = 0, misses = 0;
+};
+
+// psattn_run_batch on the tier, then the load accounting. lockstep: psa_attention_batched's
+// rounds (engine.cpp:173-209; one TierIter per round with blocks > 0); otherwise query by
+// query like consecutive psa_attention / topk_attention calls (one TierIter per microbatch).
+int tier_run_account(psattn_tier* t, const psattn_batch* b, void* workspace, cudaStream_t st, bool lockstep,
+                     std::vector<TierIter>* iters) {
+    int rc = psattn_run_batch(t->pool, b, workspace, st);
     if (rc) return rc;
     const int64_t nq = (int64_t)b->n_units * b->group;
     const int64_t hbt = b->total_blocks * b->group;
@@ -269,22 +281,50 @@ int psattn_tier_run_batch(psattn_tier* t, const psattn_batch* b, void* workspace
     for (int32_t s : slots)
         if (s < 0 || s >= t->desc.n_blocks || t->layer[(size_t)s] < 0)
             return fail(PSATTN_ERR_NOT_FOUND, "load_block: unknown block id " + std::to_string(s));
-    // lockstep rounds (psa_attention_batched): every live query loads its next microbatch
     const int64_t m = std::max<int32_t>(b->microbatch_size, 1);
     std::vector<int64_t> cur((size_t)nq, 0);
-    for (bool live = true; live;) {
-        live = false;
-        for (int64_t qi = 0; qi < nq; ++qi) {
-            const int64_t u = qi / b->group, h = qi % b->group;
-            const int64_t n = off[(size_t)u + 1] - off[(size_t)u];
-            const int64_t end = std::min(cur[(size_t)qi] + m, bp[(size_t)qi]);
-            const int64_t hb = off[(size_t)u] * b->group + h * n;
-            for (int64_t r = cur[(size_t)qi]; r < end; ++r) load(t, slots[(size_t)(off[(size_t)u] + rpos[(size_t)(hb + r)])]);
-            cur[(size_t)qi] = end;
-            if (end < bp[(size_t)qi]) live = true;
+    auto load_mb = [&](int64_t qi, TierIter& it) {  // next microbatch of query qi
+        const int64_t u = qi / b->group, h = qi % b->group;
+        const int64_t n = off[(size_t)u + 1] - off[(size_t)u];
+        const int64_t end = std::min(cur[(size_t)qi] + m, bp[(size_t)qi]);
+        const int64_t hb = off[(size_t)u] * b->group + h * n;
+        for (int64_t r = cur[(size_t)qi]; r < end; ++r) {
+            const uint64_t h0 = t->total.hits;
+            load(t, slots[(size_t)(off[(size_t)u] + rpos[(size_t)(hb + r)])]);
+            if (t->total.hits != h0) ++it.hits;
+            else ++it.misses;
+            ++it.blocks;
         }
+        cur[(size_t)qi] = end;
+        return end < bp[(size_t)qi];
+    };
+    if (lockstep) {
+        for (bool live = true; live;) {
+            live = false;
+            TierIter round;
+            for (int64_t qi = 0; qi < nq; ++qi)
+                if (cur[(size_t)qi] < bp[(size_t)qi]) live |= load_mb(qi, round);
+            if (iters && round.blocks > 0) iters->push_back(round);
+        }
+    } else {
+        for (int64_t qi = 0; qi < nq; ++qi)
+            for (bool more = cur[(size_t)qi] < bp[(size_t)qi]; more;) {
+                TierIter it;
+                more = load_mb(qi, it);
+                if (iters) iters->push_back(it);
+            }
     }
     return install_pending(t, st);
+}
+
+}  // namespace psa
+
+extern "C" {
+
+int psattn_tier_run_batch(psattn_tier* t, const psattn_batch* b, void* workspace, void* stream) {
+    if (!t || !b) return fail(PSATTN_ERR_INVALID_ARGUMENT, "psattn_tier_run_batch: null argument");
+    std::lock_guard<std::mutex> lk(t->mu);
+    return psa::tier_run_account(t, b, workspace, (cudaStream_t)stream, true, nullptr);
 }
 
 int psattn_tier_stats(psattn_tier* t, int32_t layer, psattn_cache_stats* out) {
@@ -312,5 +352,309 @@ int psattn_tier_h2d_bytes(psattn_tier* t, uint64_t* out) {
 }
 
 psattn_pool* psattn_tier_pool(psattn_tier* t) { return t ? t->pool : nullptr; }
+
+}  // extern "C"
+
+// =============================================================================
+// Batched serving loop on the GPU path (reference run_serving,
+// serving.cpp:100-229): FCFS head-only admission while one microbatch per live
+// (request, layer) fits the fast tier, then one decode step for every live request
+// layer by layer — each layer ONE device batch over the live requests through the
+// two-tier store — retirement and release. The simulated TBT cost model
+// (iteration_costs + simulate_pipeline, serving.cpp:85-96, pipeline.cpp:153-175)
+// is reproduced from the device run's hit/miss series, so the reports compare with
+// the reference's byte for byte; the device time of the attention launches is
+// measured alongside (CUDA events).
+// =============================================================================
+namespace {
+
+struct ServeRequest {
+    int64_t id = 0;
+    double arrival_s = 0.0;
+    int32_t steps = 0;
+    std::vector<std::vector<int64_t>> layer_blocks;  // per layer, block ids in sequence order
+    std::vector<int64_t> ids;
+    std::vector<int32_t> layers, ntok;
+    std::vector<float> keys, values;  // [nb][B][d]
+    std::vector<float> queries;       // [steps][L][d]
+};
+
+struct DevScratch {
+    void* p = nullptr;
+    size_t cap = 0;
+    void* get(size_t n) {
+        if (n > cap) {
+            cudaFree(p);
+            p = nullptr;
+            cap = 0;
+            if (cudaMalloc(&p, n) != cudaSuccess) return nullptr;
+            cap = n;
+        }
+        return p;
+    }
+    ~DevScratch() { cudaFree(p); }
+};
+
+double percentile_nr(std::vector<double> v, double p) {
+    std::sort(v.begin(), v.end());
+    if (p == 0.0) return v.front();
+    const auto rank = static_cast<size_t>(std::ceil(p / 100.0 * static_cast<double>(v.size())));
+    return v[rank - 1];
+}
+
+}  // namespace
+
+struct psattn_serving {
+    psattn_tier_desc store{};
+    psattn_config engine{};
+    psattn_serving_cost cost{};
+    std::vector<ServeRequest> requests;
+};
+
+extern "C" {
+
+int psattn_serving_create(const psattn_tier_desc* store, const psattn_config* engine, const psattn_serving_cost* cost,
+                          psattn_serving** out) {
+    if (!store || !engine || !cost || !out) return fail(PSATTN_ERR_INVALID_ARGUMENT, "psattn_serving_create: null argument");
+    auto* s = new psattn_serving();
+    s->store = *store;
+    s->engine = *engine;
+    s->cost = *cost;
+    *out = s;
+    return PSATTN_OK;
+}
+
+void psattn_serving_destroy(psattn_serving* s) { delete s; }
+
+int psattn_serving_add_request(psattn_serving* s, int64_t request_id, double arrival_s, int32_t decode_steps,
+                               int32_t n_layers, int64_t blocks_per_layer, const int64_t* layer_blocks,
+                               int64_t n_blocks, const int64_t* block_ids, const int32_t* block_layers,
+                               const int32_t* ntok, const float* keys, const float* values, const float* queries) {
+    if (!s || !layer_blocks || !block_ids || !block_layers || !ntok || !keys || !values || !queries)
+        return fail(PSATTN_ERR_INVALID_ARGUMENT, "psattn_serving_add_request: null argument");
+    if (n_layers != s->store.n_layers) return fail(PSATTN_ERR_RUNTIME, "serving: requests disagree on layer count");
+    ServeRequest r;
+    r.id = request_id;
+    r.arrival_s = arrival_s;
+    r.steps = decode_steps;
+    const int64_t d = s->store.dim, B = s->store.block_tokens;
+    for (int32_t l = 0; l < n_layers; ++l)
+        r.layer_blocks.emplace_back(layer_blocks + l * blocks_per_layer, layer_blocks + (l + 1) * blocks_per_layer);
+    r.ids.assign(block_ids, block_ids + n_blocks);
+    r.layers.assign(block_layers, block_layers + n_blocks);
+    r.ntok.assign(ntok, ntok + n_blocks);
+    r.keys.assign(keys, keys + n_blocks * B * d);
+    r.values.assign(values, values + n_blocks * B * d);
+    r.queries.assign(queries, queries + (int64_t)decode_steps * n_layers * d);
+    s->requests.push_back(std::move(r));
+    return PSATTN_OK;
+}
+
+int psattn_serving_run(psattn_serving* s, int32_t method, double epsilon, int64_t k, psattn_serving_report* out) {
+    if (!s || !out) return fail(PSATTN_ERR_INVALID_ARGUMENT, "psattn_serving_run: null argument");
+    if (s->requests.empty()) return fail(PSATTN_ERR_RUNTIME, "serving: empty request list");
+    if (method < 0 || method > 2) return fail(PSATTN_ERR_INVALID_ARGUMENT, "serving: unknown method");
+    if (method == 1 && k < 1) return fail(PSATTN_ERR_RUNTIME, "serving: top-k method needs k >= 1");
+    psattn_config cfg = s->engine;
+    if (method == 0) cfg.epsilon = epsilon;
+    if (method == 2) cfg.epsilon = 1.0;
+    if (!(cfg.epsilon > 0.0) || cfg.epsilon > 1.0) return fail(PSATTN_ERR_INVALID_ARGUMENT, "config: epsilon must be in (0, 1]");
+    if (cfg.microbatch_size < 1) return fail(PSATTN_ERR_INVALID_ARGUMENT, "config: microbatch_size must be >= 1");
+    const int32_t L = s->store.n_layers;
+    const int64_t d = s->store.dim;
+    // block id -> backing-tier index (every request's blocks, in request order)
+    std::unordered_map<int64_t, int64_t> index;
+    int64_t nb = 0;
+    for (const auto& r : s->requests)
+        for (int64_t id : r.ids) index.emplace(id, nb++);
+    psattn_tier_desc td = s->store;
+    td.n_blocks = nb;
+    psattn_tier* t = nullptr;
+    int rc = psattn_tier_create(&td, &t);
+    if (rc) return rc;
+    struct TierGuard {
+        psattn_tier* t;
+        ~TierGuard() { psattn_tier_destroy(t); }
+    } guard{t};
+    // Admission (serving.cpp:31-81)
+    const size_t m = (size_t)cfg.microbatch_size, cap = (size_t)td.fast_slots;
+    const bool unified = td.pool_policy == PSATTN_POOL_UNIFIED;
+    const size_t layer_cap = cap / (unified ? 1 : (size_t)L);
+    size_t reserved = 0;  // per layer in partitioned mode (all layers reserve alike)
+    auto fits = [&] { return unified ? reserved * L + m * L <= cap : reserved + m <= layer_cap; };
+    const bool solo = unified ? m * L <= cap : m <= layer_cap;
+    for (const auto& r : s->requests)
+        if (!solo)
+            return fail(PSATTN_ERR_RUNTIME, "unschedulable request " + std::to_string(r.id) +
+                                                ": one microbatch per layer does not fit the fast pool");
+    std::vector<size_t> pending;
+    for (size_t i = 0; i < s->requests.size(); ++i) pending.push_back(i);
+    size_t ph = 0;
+    struct Live {
+        size_t r;
+        int32_t step;
+    };
+    std::vector<Live> live;
+    std::vector<double> tbt, blocks, cov;
+    uint64_t blocks_sum = 0, total_sum = 0;
+    double now = 0.0, model_seq = 0.0, model_pipe = 0.0, gpu_ms = 0.0;
+    int64_t steps = 0, completed = 0, launches = 0;
+    cudaStream_t st = nullptr;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    DevScratch d_in, d_out, d_ws;
+    std::vector<char> h_in;
+    while (ph < pending.size() || !live.empty()) {
+        while (ph < pending.size() && s->requests[pending[ph]].arrival_s * 1000.0 <= now && fits()) {
+            const ServeRequest& r = s->requests[pending[ph++]];
+            reserved += m;
+            std::vector<int64_t> bi(r.ids.size()), own(r.ids.size(), r.id);
+            for (size_t i = 0; i < r.ids.size(); ++i) bi[i] = index.at(r.ids[i]);
+            if ((rc = psattn_tier_put_blocks(t, (int64_t)bi.size(), bi.data(), r.layers.data(), r.ntok.data(), own.data(),
+                                             r.keys.data(), r.values.data())))
+                return rc;
+            live.push_back({(size_t)(&r - s->requests.data()), 0});
+        }
+        if (live.empty()) {
+            if (ph >= pending.size()) break;
+            now = std::max(now, s->requests[pending[ph]].arrival_s * 1000.0);
+            continue;
+        }
+        double step_cost = 0.0;
+        for (int32_t l = 0; l < L; ++l) {
+            // one device batch: unit i = live request i's layer-l list (ascending id), its step query
+            const int32_t nu = (int32_t)live.size();
+            std::vector<std::vector<int64_t>> sorted(nu);
+            std::vector<int64_t> off(nu + 1, 0);
+            int64_t maxn = 0;
+            for (int32_t i = 0; i < nu; ++i) {
+                sorted[i] = s->requests[live[i].r].layer_blocks[l];
+                std::sort(sorted[i].begin(), sorted[i].end());
+                off[i + 1] = off[i] + (int64_t)sorted[i].size();
+                maxn = std::max<int64_t>(maxn, (int64_t)sorted[i].size());
+            }
+            const int64_t tot = off[nu];
+            const size_t qb = (size_t)nu * d * 4, sb = (size_t)tot * 4, ob = (size_t)(nu + 1) * 8;
+            h_in.resize(qb + sb + ob);
+            for (int32_t i = 0; i < nu; ++i) {
+                const ServeRequest& r = s->requests[live[i].r];
+                std::memcpy(h_in.data() + (size_t)i * d * 4, r.queries.data() + ((size_t)live[i].step * L + l) * d, d * 4);
+                for (size_t j = 0; j < sorted[i].size(); ++j)
+                    reinterpret_cast<int32_t*>(h_in.data() + qb)[off[i] + (int64_t)j] = (int32_t)index.at(sorted[i][j]);
+            }
+            std::memcpy(h_in.data() + qb + sb, off.data(), ob);
+            char* din = static_cast<char*>(d_in.get(h_in.size()));
+            const size_t oo = (size_t)nu * d * 4, o8 = (size_t)nu * 8, o4 = (size_t)nu * 4;
+            char* dout = static_cast<char*>(d_out.get(oo + 3 * o8 + o4 + (size_t)tot * 4 + 64));
+            if (!din || !dout) return fail(PSATTN_ERR_RUNTIME, "serving: device allocation failed");
+            cudaMemcpyAsync(din, h_in.data(), h_in.size(), cudaMemcpyHostToDevice, st);
+            psattn_batch b{};
+            b.n_units = nu;
+            b.group = 1;
+            b.dim = (int32_t)d;
+            b.max_blocks = (int32_t)maxn;
+            b.total_blocks = tot;
+            b.q = reinterpret_cast<const float*>(din);
+            b.slots = reinterpret_cast<const int32_t*>(din + qb);
+            b.list_off = reinterpret_cast<const int64_t*>(din + qb + sb);
+            b.epsilon = method == 1 ? 1.0 : cfg.epsilon;
+            b.microbatch_size = cfg.microbatch_size;
+            b.estimator = cfg.estimator;
+            b.ranking_mode = cfg.ranking_mode;
+            b.audit_coverage = cfg.audit_coverage;
+            b.scale_override = cfg.scale_override;
+            b.topk = method == 1 ? k : 0;
+            b.out = reinterpret_cast<float*>(dout);
+            b.blocks_processed = reinterpret_cast<int64_t*>(dout + oo);
+            b.est_coverage = reinterpret_cast<double*>(dout + oo + o8);
+            b.true_coverage = reinterpret_cast<double*>(dout + oo + 2 * o8);
+            b.terminated = reinterpret_cast<int32_t*>(dout + oo + 3 * o8);
+            b.ranked_pos = reinterpret_cast<int32_t*>(dout + oo + 3 * o8 + o4);
+            void* ws = d_ws.get(psattn_batch_workspace_bytes(&b));
+            if (!ws) return fail(PSATTN_ERR_RUNTIME, "serving: device allocation failed");
+            std::vector<psa::TierIter> iters;
+            cudaEventRecord(e0, st);
+            // top-k: consecutive topk_attention calls (serving.cpp:168-174); else psa_attention_batched
+            if ((rc = psa::tier_run_account(t, &b, ws, st, method != 1, &iters))) return rc;
+            float ms = 0.0f;
+            cudaEventRecord(e1, st);
+            cudaEventSynchronize(e1);
+            cudaEventElapsedTime(&ms, e0, e1);
+            gpu_ms += ms;  // attention launches + the (tiny) install of newly cached blocks
+            ++launches;
+            std::vector<int64_t> bp(nu);
+            std::vector<double> est(nu), tc(nu);
+            cudaMemcpy(bp.data(), b.blocks_processed, o8, cudaMemcpyDeviceToHost);
+            cudaMemcpy(est.data(), b.est_coverage, o8, cudaMemcpyDeviceToHost);
+            cudaMemcpy(tc.data(), b.true_coverage, o8, cudaMemcpyDeviceToHost);
+            // cost model (iteration_costs + simulate_pipeline)
+            double lf = 0.0, cf = 0.0, freed = 0.0, seq = 0.0;
+            for (size_t i = 0; i < iters.size(); ++i) {
+                const double load_ms = (double)iters[i].misses * s->cost.miss_cost_ms + (double)iters[i].hits * s->cost.hit_cost_ms;
+                const double comp_ms = (double)iters[i].blocks * s->cost.compute_cost_ms;
+                lf = (i == 0 ? 0.0 : freed) + load_ms;
+                const double cs = std::max(lf, cf);
+                freed = cs;
+                cf = cs + comp_ms;
+                seq += load_ms + comp_ms;
+            }
+            model_seq += seq;
+            model_pipe += cf;
+            step_cost += s->cost.overlap ? cf : seq;
+            for (int32_t i = 0; i < nu; ++i) {
+                blocks.push_back((double)bp[i]);
+                cov.push_back(cfg.audit_coverage ? tc[i] : est[i]);
+                blocks_sum += (uint64_t)bp[i];
+                total_sum += (uint64_t)(off[i + 1] - off[i]);
+            }
+        }
+        now += step_cost;
+        ++steps;
+        for (auto& lr : live) {
+            tbt.push_back(step_cost);
+            ++lr.step;
+        }
+        for (auto it = live.begin(); it != live.end();) {
+            if (it->step >= s->requests[it->r].steps) {
+                if ((rc = psattn_tier_release_request(t, s->requests[it->r].id))) return rc;
+                reserved -= m;
+                ++completed;
+                it = live.erase(it);
+            } else {
+                ++it;
+            }
+        }
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (blocks.empty()) return fail(PSATTN_ERR_RUNTIME, "serving produced no attention calls");
+    psattn_serving_report rep{};
+    double bm = 0.0, cm = 0.0, cmin = std::numeric_limits<double>::infinity();
+    for (double x : blocks) bm += x;
+    for (double x : cov) {
+        cm += x;
+        cmin = std::min(cmin, x);
+    }
+    psattn_tier_stats(t, -1, &rep.store_stats);
+    const uint64_t acc = rep.store_stats.hits + rep.store_stats.misses;
+    rep.mean_blocks = bm / (double)blocks.size();
+    rep.p99_blocks = percentile_nr(blocks, 99.0);
+    rep.kv_fraction = (double)blocks_sum / (double)total_sum;
+    rep.mean_coverage = cm / (double)cov.size();
+    rep.min_coverage = cmin;
+    rep.hit_ratio = acc ? (double)rep.store_stats.hits / (double)acc : 0.0;
+    rep.tbt_p50_ms = percentile_nr(tbt, 50.0);
+    rep.tbt_p99_ms = percentile_nr(tbt, 99.0);
+    rep.overlap_eff = model_pipe > 0.0 ? model_seq / model_pipe : 1.0;
+    rep.n_calls = (int64_t)blocks.size();
+    rep.n_steps = steps;
+    rep.completed_requests = completed;
+    rep.sim_time_ms = now;
+    rep.gpu_ms = gpu_ms;
+    rep.device_batches = launches;
+    *out = rep;
+    return PSATTN_OK;
+}
 
 }  // extern "C"
