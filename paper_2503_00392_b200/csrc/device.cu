@@ -251,7 +251,7 @@ int read_meta(const psattn_pool* pool, int64_t slot, float* mean, float* lo, flo
 
 // ---- workspace carving ----
 struct WsLayout {
-    size_t keys, rpos, omass, total;
+    size_t keys, rpos, omass, kmm, total;
 };
 
 static WsLayout ws_layout(const psattn_batch* b) {
@@ -264,6 +264,8 @@ static WsLayout ws_layout(const psattn_batch* b) {
     o += align_up(hb * 4, 256);
     l.omass = o;
     if (b->ranking_mode == PSATTN_RANK_ORACLE || b->audit_coverage) o += align_up(hb * 8, 256);
+    l.kmm = o;
+    o += align_up((size_t)b->n_units * b->group * 16, 256);
     l.total = o;
     return l;
 }
@@ -324,6 +326,7 @@ BatchView make_view(const psattn_pool* pool, const psattn_batch* b, void* worksp
     v.rpos = b->ranked_pos ? b->ranked_pos : reinterpret_cast<int32_t*>(ws + l.rpos);
     v.omass = v.has_oracle ? reinterpret_cast<double*>(ws + l.omass) : nullptr;
     v.iest = b->iter_est;
+    v.kminmax = v.rank_oracle ? nullptr : reinterpret_cast<unsigned long long*>(ws + l.kmm);
     (void)pool;
     return v;
 }

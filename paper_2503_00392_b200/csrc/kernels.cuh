@@ -67,6 +67,9 @@ struct BatchView {
     int32_t* rpos;
     double* omass;
     double* iest;  // optional per-rank estimate at microbatch boundaries
+    // optional [2][n_units*g]: per-head min / max sort key, produced by the score kernel so the
+    // first tranche selection skips its min/max scan (nullptr: the selection scans)
+    unsigned long long* kminmax;
 };
 
 int dpl_for(int d);

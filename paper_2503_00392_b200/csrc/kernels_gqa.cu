@@ -55,7 +55,7 @@ struct GqaSmem {
     int wcnt[kPsaWarps];
     int64_t tr0[G], cb[G];
     uint64_t last[G];
-    double est[G], acc[G], mn[G];
+    double est[G], acc[G], mn[G], ssum[G];  // acc: log-sum-exp (oracle masses) or running max M (fast decide)
     int tc[G], cnt[G], commit[G], fin[G], live[G];
     int ucount, nlive;
     SelScratch sel[G];
@@ -147,6 +147,7 @@ __global__ void __launch_bounds__(kPsaThreads, 2) psa_gqa_kernel(PoolView p, Bat
         s.tc[tid] = 0;
         s.last[tid] = 0;
         s.acc[tid] = -INFINITY;
+        s.ssum[tid] = 0.0;
         s.mn[tid] = INFINITY;
         s.live[tid] = tid < g;
         s.est[tid] = 0.0;
@@ -173,7 +174,8 @@ __global__ void __launch_bounds__(kPsaThreads, 2) psa_gqa_kernel(PoolView p, Bat
                 const int64_t hb = off * g + (int64_t)h * n;
                 t0 = s.tr0[h] + s.tc[h];
                 tc = select_tranche(s.sel[h], s.tb[h], kGTCap, s.hist[h], kGBins, b.keys + hb, n, s.last[h], t0 == 0,
-                                    kGTCap, tm);
+                                    kGTCap, tm, b.kminmax ? b.kminmax + (size_t)u * g + h : nullptr,
+                                    (int64_t)b.n_units * g);
                 fill_tranche(s.tb[h], tc, pmask, b.rpos + hb + t0, b.slots + off, p.ntok, s.tslot[h], s.tntok[h], tm);
             }
             __syncthreads();
@@ -354,11 +356,20 @@ __global__ void __launch_bounds__(kPsaThreads, 2) psa_gqa_kernel(PoolView p, Bat
                 const int e = s.cidx[h][lane];
                 x = b.has_oracle ? b.omass[hb + s.upos[e]] : (double)s.la[e][h];
             }
-            double acc = s.acc[h], mn = s.mn[h];
+            double acc = s.acc[h], mn = s.mn[h], ssum = s.ssum[h];
 #ifdef PSA_GQA_PROF
             const long long d0_ = clock64();
 #endif
-            const Decision dc = decide_chunk(x, cnt, s.cb[h], n, limit, b.m, eps, acc, mn, b.iest ? b.iest + hb : nullptr);
+            Decision dc;
+            if (b.has_oracle) {
+                dc = decide_chunk(x, cnt, s.cb[h], n, limit, b.m, eps, acc, mn, b.iest ? b.iest + hb : nullptr);
+            } else if (!decide_chunk_fast((float)x, cnt, s.cb[h], n, limit, b.m, eps, acc, ssum, mn,
+                                          b.iest ? b.iest + hb : nullptr, dc)) {
+                // fp64 fallback: carried (M, S) -> log-sum-exp and back (M' = lse, S' = 1)
+                acc = ssum > 0.0 ? acc + log(ssum) : -INFINITY;
+                dc = decide_chunk(x, cnt, s.cb[h], n, limit, b.m, eps, acc, mn, b.iest ? b.iest + hb : nullptr);
+                ssum = 1.0;
+            }
 #ifdef PSA_GQA_PROF
             if (tid == 0) pc[9] += clock64() - d0_;
 #endif
@@ -368,6 +379,7 @@ __global__ void __launch_bounds__(kPsaThreads, 2) psa_gqa_kernel(PoolView p, Bat
                 s.fin[h] = dc.fin;
                 s.est[h] = dc.est;
                 s.acc[h] = acc;
+                s.ssum[h] = ssum;
                 s.mn[h] = mn;
             }
         }

@@ -145,7 +145,9 @@ __global__ void __launch_bounds__(kPsaThreads, 3) psa_kernel(PoolView p, BatchVi
     float M = -INFINITY, L = 0.0f, O[DPL];  // warp-local online-softmax state
 #pragma unroll
     for (int j = 0; j < DPL; ++j) O[j] = 0.0f;
-    double acc = -INFINITY, mn = INFINITY;  // coverage state (warp 0, lane-uniform)
+    // coverage state (warp 0, lane-uniform): acc = log-sum-exp (oracle masses) or the running
+    // max M of the fast decide, whose running sum S is ssum
+    double acc = -INFINITY, mn = INFINITY, ssum = 0.0;
 
     const double* omass = b.has_oracle ? (b.omass + hb) : nullptr;
     const int64_t v_off = (int64_t)p.T * d;
@@ -158,7 +160,8 @@ __global__ void __launch_bounds__(kPsaThreads, 3) psa_kernel(PoolView p, BatchVi
         if (cb >= tr0 + tc) {  // ---- ORDER: next tranche ----
             tr0 += tc;
             tc = select_tranche(s.sel, s.tb, kTCap, s.hist, kBins, keys, n, last, tr0 == 0, tr0 == 0 ? kFirstTranche : kTCap,
-                                cta_team());
+                                cta_team(), b.kminmax ? b.kminmax + (size_t)u * b.g + h : nullptr,
+                                (int64_t)b.n_units * b.g);
             last = s.tb[tc - 1];
             fill_tranche(s.tb, tc, pmask, b.rpos + hb + tr0, b.slots + off, p.ntok, s.tslot, s.tntok, cta_team());
             __syncthreads();
@@ -244,7 +247,15 @@ __global__ void __launch_bounds__(kPsaThreads, 3) psa_kernel(PoolView p, BatchVi
         if (warp == 0) {
             double x = -INFINITY;
             if (lane < cnt) x = omass ? omass[s.tb[ci + lane] & pmask] : (double)s.la[lane];
-            const Decision dc = decide_chunk(x, cnt, cb, n, limit, b.m, eps, acc, mn, b.iest ? b.iest + hb : nullptr);
+            Decision dc;
+            if (omass) {
+                dc = decide_chunk(x, cnt, cb, n, limit, b.m, eps, acc, mn, b.iest ? b.iest + hb : nullptr);
+            } else if (!decide_chunk_fast((float)x, cnt, cb, n, limit, b.m, eps, acc, ssum, mn,
+                                          b.iest ? b.iest + hb : nullptr, dc)) {
+                acc = ssum > 0.0 ? acc + log(ssum) : -INFINITY;  // fp64 fallback (see kernels_gqa.cu)
+                dc = decide_chunk(x, cnt, cb, n, limit, b.m, eps, acc, mn, b.iest ? b.iest + hb : nullptr);
+                ssum = 1.0;
+            }
             if (lane == 0) {
                 s.commit = dc.commit;
                 s.fin = dc.fin;

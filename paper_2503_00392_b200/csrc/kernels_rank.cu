@@ -177,6 +177,7 @@ __global__ void __launch_bounds__(kScoreWarps * 32, 2) score_kernel(PoolView p, 
     const int my_h = my_idx / kRecs, my_j = my_idx % kRecs;
     const bool writer = (lane & ((1 << SH) - 1)) == 0 && my_h < b.g;
     uint64_t* keys = b.keys + off * b.g + (int64_t)my_h * n;
+    uint64_t kmin = ~0ull, kmax = 0;  // keys written by this lane (first-tranche bounds)
 
     const int64_t ngroups = (n + kRecs - 1) / kRecs;
     const int64_t nwarps = (int64_t)gridDim.x * kScoreWarps;
@@ -233,8 +234,15 @@ __global__ void __launch_bounds__(kScoreWarps * 32, 2) score_kernel(PoolView p, 
         if (writer && p0 + my_j < n) {
             // acc = sum q(2m + lo + hi) + |q|(hi - lo) = 4 * CuboidMean / 2 * Upper; Mean: plain
             const double s = est == 2 ? 0.25 * (tot * scale) : (est == 1 ? 0.5 * (tot * scale) : tot * scale);
-            keys[p0 + my_j] = make_key(s, (uint32_t)(p0 + my_j), b.pos_bits);
+            const uint64_t key = make_key(s, (uint32_t)(p0 + my_j), b.pos_bits);
+            keys[p0 + my_j] = key;
+            kmin = key < kmin ? key : kmin;
+            kmax = key > kmax ? key : kmax;
         }
+    }
+    if (b.kminmax && writer && kmax != 0) {
+        atomicMin(b.kminmax + (size_t)u * b.g + my_h, (unsigned long long)kmin);
+        atomicMax(b.kminmax + (size_t)(b.n_units + u) * b.g + my_h, (unsigned long long)kmax);
     }
 }
 
@@ -293,6 +301,7 @@ __global__ void __launch_bounds__(kScoreWarps * 32, 2) score_kernel_tma(PoolView
     const int my_h = my_idx / kRecs, my_j = my_idx % kRecs;
     const bool writer = (lane & ((1 << SH) - 1)) == 0 && my_h < b.g;
     uint64_t* keys = b.keys + off * b.g + (int64_t)my_h * n;
+    uint64_t kmin = ~0ull, kmax = 0;  // keys written by this lane (first-tranche bounds)
     const uint64_t pol = policy_evict_first();
 
     const int64_t ngroups = (n + kRecs - 1) / kRecs;
@@ -387,12 +396,19 @@ __global__ void __launch_bounds__(kScoreWarps * 32, 2) score_kernel_tma(PoolView
         const int64_t p0 = grp * kRecs;
         if (writer && p0 + my_j < n) {
             const double sc = est == 2 ? 0.25 * (tot * scale) : (est == 1 ? 0.5 * (tot * scale) : tot * scale);
-            keys[p0 + my_j] = make_key(sc, (uint32_t)(p0 + my_j), b.pos_bits);
+            const uint64_t key = make_key(sc, (uint32_t)(p0 + my_j), b.pos_bits);
+            keys[p0 + my_j] = key;
+            kmin = key < kmin ? key : kmin;
+            kmax = key > kmax ? key : kmax;
         }
         if (++stage == S) {
             stage = 0;
             phase ^= 1u;
         }
+    }
+    if (b.kminmax && writer && kmax != 0) {
+        atomicMin(b.kminmax + (size_t)u * b.g + my_h, (unsigned long long)kmin);
+        atomicMax(b.kminmax + (size_t)(b.n_units + u) * b.g + my_h, (unsigned long long)kmax);
     }
 }
 
@@ -563,6 +579,7 @@ static BatchView sub_view(const BatchView& b, int u0, int cnt) {
     v.est = b.est + qo;
     v.tcov = b.tcov ? b.tcov + qo : nullptr;
     v.term = b.term + qo;
+    v.kminmax = nullptr;  // unit-indexed [2][n_units*g]: not carved per sub-batch
     return v;
 }
 
@@ -613,6 +630,11 @@ int launch_batch(const PoolView& p, const BatchView& b, cudaStream_t st, cudaEve
         }
         if (marks) cudaEventRecord(marks[1], st);
         if (!b.rank_oracle) {
+            if (b.kminmax) {
+                const size_t nq = (size_t)b.n_units * b.g;
+                cudaMemsetAsync(b.kminmax, 0xff, nq * 8, st);
+                cudaMemsetAsync(b.kminmax + nq, 0, nq * 8, st);
+            }
             launch_score_stage(p, b, st);
             ++launches;
         }

@@ -105,17 +105,26 @@ __device__ __forceinline__ void scan_keys(const uint64_t* __restrict__ keys, int
 // Next tranche: the C (<= kTCap, ~target) smallest keys greater than `last` (all keys if first).
 static __device__ __noinline__ int select_tranche(SelScratch& s, uint64_t* tb, int cap, uint32_t* hist, int nbins,
                                           const uint64_t* __restrict__ keys, int64_t n, uint64_t last, bool first,
-                                          unsigned target, Team tm) {
+                                          unsigned target, Team tm, const unsigned long long* bounds = nullptr,
+                                          int64_t bstride = 0) {
     const int tid = tm.tid, lane = threadIdx.x & 31;
     unsigned long long lmin = ~0ull, lmax = 0;
     unsigned lcnt = 0;
-    scan_keys(keys, n, tm, [&](uint64_t k) {
-        if (first || k > last) {
-            lmin = k < lmin ? k : lmin;
-            lmax = k > lmax ? k : lmax;
-            ++lcnt;
+    if (first && bounds) {  // min / max of all keys from the score kernel: no scan
+        if (tid == 0) {
+            lmin = bounds[0];
+            lmax = bounds[bstride];
+            lcnt = (unsigned)n;
         }
-    });
+    } else {
+        scan_keys(keys, n, tm, [&](uint64_t k) {
+            if (first || k > last) {
+                lmin = k < lmin ? k : lmin;
+                lmax = k > lmax ? k : lmax;
+                ++lcnt;
+            }
+        });
+    }
     if (tid == 0) {
         s.red_min = ~0ull;
         s.red_max = 0;
@@ -300,6 +309,60 @@ __device__ __forceinline__ Decision decide_chunk(double x, int cnt, int64_t cb, 
     d.commit = f + 1;
     d.fin = bal ? 1 : 0;
     return d;
+}
+
+// Same decision with the in-chunk work in fp32 (MUFU exp, fp32 scans) and the running sum
+// carried in fp64 as (M, S): log-sum-exp of everything observed = M + log S. The estimate
+// est = S / (S + n_left * exp(min - M_i)) (the reference's 1 / (1 + n_left * exp(min - acc))
+// with both sides scaled by exp(M_i - acc)) carries ~1e-7 relative error, so a decision can
+// differ from the fp64 reference only within ~1e-7 of eps (the parity rule's tau is 1e-5).
+// Returns false, leaving every argument untouched, when a chunk mass sits > 80 below the
+// chunk maximum (fp32 exp would lose it): the caller then runs decide_chunk in fp64.
+__device__ __forceinline__ bool decide_chunk_fast(float x, int cnt, int64_t cb, int64_t n, int64_t limit, int m,
+                                                  double eps, double& M, double& S, double& mn, double* iest_head,
+                                                  Decision& d) {
+    const int lane = threadIdx.x & 31;
+    const bool valid = lane < cnt;
+    const int64_t r = cb + lane;
+    const float xf = valid ? x : -INFINITY;
+    float cmax = xf;
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) cmax = fmaxf(cmax, __shfl_xor_sync(PSA_FULL, cmax, o));
+    const float Mf = (float)M;  // M is a carried fp32 mass (or -inf)
+    const float mx = fmaxf(cmax, Mf);
+    const float dx = xf - mx;
+    if (__any_sync(PSA_FULL, valid && dx < -80.0f)) return false;
+    float e = valid ? expf(dx) : 0.0f;
+    const double scale = M == -INFINITY ? 0.0 : (double)expf(Mf - mx);
+    float mnv = valid ? xf : INFINITY;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const float ye = __shfl_up_sync(PSA_FULL, e, o);
+        const float ym = __shfl_up_sync(PSA_FULL, mnv, o);
+        if (lane >= o) {
+            e += ye;
+            mnv = fminf(mnv, ym);
+        }
+    }
+    const double Si = fma(S, scale, (double)e);  // sum exp(mass - mx) observed up to this rank
+    const float mn_i = fminf(mnv, (float)mn);
+    const int64_t nl = n - (r + 1);
+    const float t = expf(mn_i - mx);
+    const float sf = (float)Si;
+    const float est_f = nl == 0 ? 1.0f : (sf > 0.0f ? sf / fmaf((float)nl, t, sf) : 0.0f);
+    const double est_i = (double)est_f;
+    const bool boundary = valid && (m == 1 || (((r + 1) % m) == 0) || (r + 1 == limit));
+    const bool stop = boundary && (est_i > eps || r + 1 == limit);
+    const unsigned bal = __ballot_sync(PSA_FULL, stop);
+    const int f = bal ? (__ffs(bal) - 1) : (cnt - 1);
+    if (iest_head && boundary && lane <= f) iest_head[r] = est_i;
+    M = (double)mx;
+    S = __shfl_sync(PSA_FULL, Si, f);
+    mn = (double)__shfl_sync(PSA_FULL, mn_i, f);
+    d.est = __shfl_sync(PSA_FULL, est_i, f);
+    d.commit = f + 1;
+    d.fin = bal ? 1 : 0;
+    return true;
 }
 
 }  // namespace psa
