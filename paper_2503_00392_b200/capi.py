@@ -156,6 +156,7 @@ def _load() -> C.CDLL:
     L.psattn_synth_unit_host.argtypes = [C.POINTER(SynthParams), i64, i64, i64, i64, vp, vp]
     L.psattn_synth_is_planted.argtypes = [C.POINTER(SynthParams), i64, i64]
     L.psattn_pool_fill_synthetic.argtypes = [vp, C.POINTER(SynthParams), i32, vp, vp, vp, vp]
+    L.psattn_set_dense.argtypes = [i32]
     L.psattn_exact_attention.argtypes = [vp, C.POINTER(Batch), vp, vp]
     L.psattn_tradeoff.argtypes = [vp, C.POINTER(Batch), dbl, C.POINTER(TradeoffReport), vp]
     L.psattn_tier_create.argtypes = [C.POINTER(TierDesc), C.POINTER(vp)]
@@ -187,7 +188,7 @@ EXPORTED = [
     "psattn_pool_append_tokens",
     "psattn_batch_workspace_bytes", "psattn_run_batch", "psattn_batch_union_blocks", "psattn_batch_last_launches",
     "psattn_profile_enable", "psattn_profile_read", "psattn_set_progressive_kernel",
-    "psattn_set_score_kernel", "psattn_set_pipeline",
+    "psattn_set_score_kernel", "psattn_set_pipeline", "psattn_set_dense",
     "psattn_synth_direction", "psattn_synth_query", "psattn_synth_unit_host", "psattn_synth_is_planted",
     "psattn_pool_fill_synthetic", "psattn_exact_attention", "psattn_tradeoff",
     "psattn_tier_create", "psattn_tier_destroy", "psattn_tier_put_blocks", "psattn_tier_release_request",

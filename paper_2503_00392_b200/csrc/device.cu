@@ -251,7 +251,7 @@ int read_meta(const psattn_pool* pool, int64_t slot, float* mean, float* lo, flo
 
 // ---- workspace carving ----
 struct WsLayout {
-    size_t keys, rpos, omass, kmm, total;
+    size_t keys, rpos, omass, kmm, dflag, dla, dp, dthr, total;
 };
 
 static WsLayout ws_layout(const psattn_batch* b) {
@@ -266,6 +266,19 @@ static WsLayout ws_layout(const psattn_batch* b) {
     if (b->ranking_mode == PSATTN_RANK_ORACLE || b->audit_coverage) o += align_up(hb * 8, 256);
     l.kmm = o;
     o += align_up((size_t)b->n_units * b->group * 16, 256);
+    // dense hand-over scratch (GQA shapes with the estimated ranking: d = 128, group 2..4)
+    l.dflag = l.dla = l.dp = l.dthr = 0;
+    if (b->dim == 128 && b->group >= 2 && b->group <= 4 && b->ranking_mode != PSATTN_RANK_ORACLE &&
+        !b->audit_coverage && b->max_blocks <= kDenseMaxBlocks) {
+        l.dflag = o;
+        o += 256 + align_up((size_t)b->n_units * 4, 256);  // count | unit list
+        l.dla = o;
+        o += align_up(hb * 4, 256);
+        l.dp = o;
+        o += align_up(hb * 64, 256);
+        l.dthr = o;
+        o += align_up((size_t)b->n_units * b->group * 8, 256);
+    }
     l.total = o;
     return l;
 }
@@ -327,6 +340,11 @@ BatchView make_view(const psattn_pool* pool, const psattn_batch* b, void* worksp
     v.omass = v.has_oracle ? reinterpret_cast<double*>(ws + l.omass) : nullptr;
     v.iest = b->iter_est;
     v.kminmax = v.rank_oracle ? nullptr : reinterpret_cast<unsigned long long*>(ws + l.kmm);
+    v.dense_count = l.dflag ? reinterpret_cast<int32_t*>(ws + l.dflag) : nullptr;
+    v.dense_flag = l.dflag ? reinterpret_cast<int32_t*>(ws + l.dflag + 256) : nullptr;
+    v.dense_la = l.dflag ? reinterpret_cast<float*>(ws + l.dla) : nullptr;
+    v.dense_p = l.dflag ? reinterpret_cast<float*>(ws + l.dp) : nullptr;
+    v.dense_thr = l.dflag ? reinterpret_cast<unsigned long long*>(ws + l.dthr) : nullptr;
     (void)pool;
     return v;
 }
@@ -467,6 +485,12 @@ int psattn_run_batch(psattn_pool* pool, const psattn_batch* b, void* workspace, 
 int psattn_set_progressive_kernel(int32_t mode) {
     if (mode < 0 || mode > 2) return fail(PSATTN_ERR_INVALID_ARGUMENT, "progressive kernel mode must be 0, 1 or 2");
     set_psa_kernel_choice(mode);
+    return PSATTN_OK;
+}
+
+int psattn_set_dense(int32_t mode) {
+    if (mode < 0 || mode > 1) return fail(PSATTN_ERR_INVALID_ARGUMENT, "psattn_set_dense: mode must be 0 or 1");
+    set_dense_mode(mode);
     return PSATTN_OK;
 }
 

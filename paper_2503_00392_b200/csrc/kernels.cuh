@@ -70,7 +70,14 @@ struct BatchView {
     // optional [2][n_units*g]: per-head min / max sort key, produced by the score kernel so the
     // first tranche selection skips its min/max scan (nullptr: the selection scans)
     unsigned long long* kminmax;
+    // dense hand-over (kernels_dense.cu); dense_flag == nullptr disables it
+    int32_t* dense_flag;            // [n_units] list of handed-over units (dense_count entries)
+    int32_t* dense_count;
+    float* dense_la;                // [total*g] fp32 block masses
+    float* dense_p;                 // [total*g][16] normalised token weights
+    unsigned long long* dense_thr;  // [n_units*g] rank-threshold key of each head's processed set
 };
+constexpr int64_t kDenseMaxBlocks = 16384;
 
 int dpl_for(int d);
 int tok_for(int T);
@@ -86,13 +93,16 @@ cudaError_t launch_scatter(const PoolView& p, const void* staged, const int32_t*
 cudaError_t launch_synth_fill(const PoolView& p, uint64_t seed, float skew, float prob, int round_bf16,
                               int32_t n_units, const int64_t* d_unit_ids, const int64_t* d_slot_off,
                               const int64_t* d_tokens, int64_t max_blocks, float* d_dirs, cudaStream_t st);
-void launch_psa(const PoolView& p, const BatchView& b, cudaStream_t st);
+int launch_psa(const PoolView& p, const BatchView& b, cudaStream_t st);  // returns kernels launched
 bool gqa_supported(const PoolView& p, const BatchView& b);
 void launch_gqa(const PoolView& p, const BatchView& b, cudaStream_t st);
 // 0 = auto (GQA kernel when supported), 1 = per-query kernel, 2 = GQA kernel
 void set_psa_kernel_choice(int choice);
 void set_score_kernel_choice(int choice);
 void set_pipeline_subbatches(int k);
+void set_dense_mode(int mode);  // 0 auto (hand-over enabled), 1 off
+bool dense_supported(const PoolView& p, const BatchView& b);
+void launch_dense(const PoolView& p, const BatchView& b, cudaStream_t st);
 // Returns the number of kernel launches issued, or -1 on error (cudaGetLastError has it).
 int launch_batch(const PoolView& p, const BatchView& b, cudaStream_t st, cudaEvent_t* marks = nullptr);
 cudaError_t launch_union(const BatchView& b, int64_t* out_union, cudaStream_t st);

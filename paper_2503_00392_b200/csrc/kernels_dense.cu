@@ -1,0 +1,334 @@
+// kernels_dense.cu — dense mode of the GQA progressive path (bf16 pool, d = 128, blocks <= 16
+// tokens, group 2..4, estimated ranking).
+//
+// The round-based GQA kernel (kernels_gqa.cu) reads a block once per ROUND in which any head
+// of the group reaches it. When the heads need many ranks (weakly skewed attention, e.g.
+// isotropic keys: ~90% of the list at eps 0.95) their rank orders diverge and a block is
+// K-scored in up to g different rounds. psa_gqa_kernel therefore hands a unit over to this
+// path when one of its heads exhausts its first tranche (512 ranks), and the unit is redone:
+//
+//   dense_k_kernel           ONE K pass over every block of the list (tensor-core scores for
+//                            all heads at once): per (head, block) the fp32 block mass
+//                            la = m + log(l) (block_partial_attention's log_as, reference
+//                            attention.hpp:73) and the normalised token weights p_t = w_t / l;
+//   dense_decide_kernel      per head: its full rank order (bitonic sort of the head's keys in
+//                            shared memory) and Algorithm 1's sequential stop rule over the
+//                            masses in rank order (decide_chunk_fast / decide_chunk, the same
+//                            arithmetic as the round kernel) -> blocks_processed, estimate and
+//                            the rank threshold key;
+//   dense_v_kernel           ONE V pass over the union of the heads' processed sets: block b
+//                            belongs to head h's set iff key_h(b) <= threshold_h (keys are
+//                            unique and ordered), accumulated with mma.sync like the round
+//                            kernel's V pass, merged with weight exp(la - M).
+//
+// Same processed sets and stop points as the round kernel (identical masses, same decide);
+// outputs differ only by fp32 summation order.
+#include <cuda_bf16.h>
+#include <math.h>
+
+#include "common.cuh"
+#include "kernels.cuh"
+#include "mma.cuh"
+#include "psa_order.cuh"
+
+namespace psa {
+
+constexpr int kDenseWarps = 8;
+constexpr int kDensePf = 4;  // L2 prefetch distance (warp iterations)
+
+// q fragments of the K pass (see psa_gqa_kernel): columns = (head, split), 4 per head.
+template <int G>
+__device__ __forceinline__ void load_qg(const BatchView& b, int u, int lane, uint32_t (&qg)[8][(G * 4 + 7) / 8][2]) {
+    constexpr int NT = (G * 4 + 7) / 8;
+    const int gq = lane >> 2, tq = lane & 3;
+#pragma unroll
+    for (int tile = 0; tile < NT; ++tile) {
+        const int hq = tile * 2 + (gq >> 2), sp = gq & 3;
+        const float* qrow = b.q + ((size_t)u * b.g + (hq < b.g ? hq : 0)) * 128;
+#pragma unroll
+        for (int st = 0; st < 8; ++st)
+#pragma unroll
+            for (int hf = 0; hf < 2; ++hf) {
+                uint32_t packed = 0;
+#pragma unroll
+                for (int e2 = 0; e2 < 2; ++e2) {
+                    const float x = hq < b.g ? bf16_split(qrow[32 * tq + 4 * st + 2 * hf + e2], sp) : 0.0f;
+                    packed |= bf16_bits(x) << (16 * e2);
+                }
+                qg[st][tile][hf] = packed;
+            }
+    }
+}
+
+template <int G>
+__device__ __forceinline__ void dense_k_unit(const PoolView& p, const BatchView& b, int u) {
+    constexpr int NT = (G * 4 + 7) / 8;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int gq = lane >> 2, tq = lane & 3;
+    const int64_t off = b.list_off[u], n = b.list_off[u + 1] - off;
+    const float fscale = (float)b.scale;
+    const int T = p.T;
+    uint32_t qg[8][NT][2];
+    load_qg<G>(b, u, lane, qg);
+    for (int64_t e = warp; e < n; e += kDenseWarps) {
+        const int64_t ef = e + (int64_t)kDensePf * kDenseWarps;
+        if (lane == 0 && ef < n) {
+            const int32_t sf = b.slots[off + ef];
+            if (kv_resident(p, sf)) prefetch_l2_bulk(kv_block<__nv_bfloat16>(p, sf), (uint32_t)(T * 128 * 2));
+        }
+        const int32_t slot = b.slots[off + e];
+        const int nt = p.ntok[slot];
+        const __nv_bfloat16* kblk = kv_block<__nv_bfloat16>(p, slot);
+        const int r0 = gq < T ? gq : T - 1, r1 = (gq + 8) < T ? (gq + 8) : T - 1;
+        const uint4* p0 = reinterpret_cast<const uint4*>(kblk + (size_t)r0 * 128 + 32 * tq);
+        const uint4* p1 = reinterpret_cast<const uint4*>(kblk + (size_t)r1 * 128 + 32 * tq);
+        uint32_t w0[16], w1[16];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const uint4 x0 = __ldg(p0 + i), x1 = __ldg(p1 + i);
+            w0[4 * i] = x0.x; w0[4 * i + 1] = x0.y; w0[4 * i + 2] = x0.z; w0[4 * i + 3] = x0.w;
+            w1[4 * i] = x1.x; w1[4 * i + 1] = x1.y; w1[4 * i + 2] = x1.z; w1[4 * i + 3] = x1.w;
+        }
+        float c[NT][4];
+#pragma unroll
+        for (int tile = 0; tile < NT; ++tile) c[tile][0] = c[tile][1] = c[tile][2] = c[tile][3] = 0.f;
+#pragma unroll
+        for (int st = 0; st < 8; ++st)
+#pragma unroll
+            for (int tile = 0; tile < NT; ++tile)
+                mma_bf16_16816(c[tile][0], c[tile][1], c[tile][2], c[tile][3], w0[2 * st], w1[2 * st], w0[2 * st + 1],
+                               w1[2 * st + 1], qg[st][tile][0], qg[st][tile][1]);
+#pragma unroll
+        for (int tile = 0; tile < NT; ++tile) {
+            float lo = c[tile][0] + c[tile][1], hi = c[tile][2] + c[tile][3];
+            lo += __shfl_xor_sync(PSA_FULL, lo, 1);
+            hi += __shfl_xor_sync(PSA_FULL, hi, 1);
+            const int hq = tile * 2 + (tq >> 1);
+            lo = (gq < nt) ? lo * fscale : -INFINITY;
+            hi = (gq + 8 < nt) ? hi * fscale : -INFINITY;
+            float mbv = fmaxf(lo, hi);
+#pragma unroll
+            for (int o = 4; o < 32; o <<= 1) mbv = fmaxf(mbv, __shfl_xor_sync(PSA_FULL, mbv, o));
+            const float wlo = (gq < nt) ? expf(lo - mbv) : 0.0f;
+            const float whi = (gq + 8 < nt) ? expf(hi - mbv) : 0.0f;
+            float lbv = wlo + whi;
+#pragma unroll
+            for (int o = 4; o < 32; o <<= 1) lbv += __shfl_xor_sync(PSA_FULL, lbv, o);
+            if ((tq & 1) == 0 && hq < b.g) {
+                const int64_t hb = off * b.g + (int64_t)hq * n;
+                float* pw = b.dense_p + (hb + e) * 16;
+                const float inv = 1.0f / lbv;
+                pw[gq] = wlo * inv;
+                pw[gq + 8] = whi * inv;
+                if (gq == 0) b.dense_la[hb + e] = mbv + logf(lbv);
+            }
+        }
+    }
+}
+
+template <int G>
+__global__ void __launch_bounds__(kDenseWarps * 32) dense_k_kernel(PoolView p, BatchView b) {
+    for (int item = blockIdx.x; item < *b.dense_count; item += gridDim.x) dense_k_unit<G>(p, b, b.dense_flag[item]);
+}
+
+// One CTA per (flagged unit, head): the head's keys sorted in shared memory, then warp 0 runs
+// the stop rule over the masses in rank order.
+__device__ __forceinline__ void dense_decide_head(const BatchView& b, int u, int h, uint64_t* ks);
+
+__global__ void __launch_bounds__(kPsaThreads) dense_decide_kernel(BatchView b) {
+    extern __shared__ __align__(16) unsigned char dsm[];
+    uint64_t* ks = reinterpret_cast<uint64_t*>(dsm);
+    for (int item = blockIdx.x; item < *b.dense_count * b.g; item += gridDim.x) {
+        dense_decide_head(b, b.dense_flag[item / b.g], item % b.g, ks);
+        __syncthreads();
+    }
+}
+
+__device__ __forceinline__ void dense_decide_head(const BatchView& b, int u, int h, uint64_t* ks) {
+    const int qi = u * b.g + h;
+    const int64_t off = b.list_off[u], n = b.list_off[u + 1] - off;
+    const int64_t hb = off * b.g + (int64_t)h * n;
+    const uint64_t pmask = (b.pos_bits >= 64) ? ~0ull : ((1ull << b.pos_bits) - 1ull);
+    const int64_t limit = b.topk > 0 ? (b.topk < n ? b.topk : n) : n;
+    const double eps = b.topk > 0 ? 1.0 : b.eps;
+    int n2 = 1;
+    while (n2 < n) n2 <<= 1;
+    for (int64_t i = threadIdx.x; i < n2; i += blockDim.x) ks[i] = i < n ? b.keys[hb + i] : ~0ull;
+    __syncthreads();
+    bitonic_smem(ks, (int)n, cta_team());
+    if (threadIdx.x >= 32) return;  // (the caller's __syncthreads: warps 1.. arrive early)
+    const int lane = threadIdx.x;
+    double acc = -INFINITY, mn = INFINITY, ssum = 0.0;
+    int64_t cb = 0;
+    Decision dc{};
+    for (;;) {
+        const int64_t left = limit - cb;
+        const int cnt = (int)(left < 32 ? left : 32);
+        const int64_t pos = lane < cnt ? (int64_t)(ks[cb + lane] & pmask) : 0;
+        const float x = lane < cnt ? b.dense_la[hb + pos] : -INFINITY;
+        if (lane < cnt) b.rpos[hb + cb + lane] = (int32_t)pos;
+        if (!decide_chunk_fast(x, cnt, cb, n, limit, b.m, eps, acc, ssum, mn, b.iest ? b.iest + hb : nullptr, dc)) {
+            acc = ssum > 0.0 ? acc + log(ssum) : -INFINITY;
+            dc = decide_chunk((double)x, cnt, cb, n, limit, b.m, eps, acc, mn, b.iest ? b.iest + hb : nullptr);
+            ssum = 1.0;
+        }
+        cb += dc.commit;
+        if (dc.fin) break;
+    }
+    if (lane == 0) {
+        b.bp[qi] = cb;
+        b.est[qi] = dc.est;
+        b.term[qi] = b.topk > 0 ? (limit < n) : (cb < n);
+        b.dense_thr[qi] = ks[cb - 1];
+    }
+}
+
+template <int G>
+__device__ __forceinline__ void dense_v_unit(const PoolView& p, const BatchView& b, int u, float (&so)[kDenseWarps][G][128],
+                                             float (&som)[kDenseWarps][G], float (&sol)[kDenseWarps][G]);
+
+template <int G>
+__global__ void __launch_bounds__(kDenseWarps * 32) dense_v_kernel(PoolView p, BatchView b) {
+    __shared__ float so[kDenseWarps][G][128];
+    __shared__ float som[kDenseWarps][G], sol[kDenseWarps][G];
+    for (int item = blockIdx.x; item < *b.dense_count; item += gridDim.x) {
+        dense_v_unit<G>(p, b, b.dense_flag[item], so, som, sol);
+        __syncthreads();
+    }
+}
+
+template <int G>
+__device__ __forceinline__ void dense_v_unit(const PoolView& p, const BatchView& b, int u, float (&so)[kDenseWarps][G][128],
+                                             float (&som)[kDenseWarps][G], float (&sol)[kDenseWarps][G]) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, tid = threadIdx.x;
+    const int gq = lane >> 2, tq = lane & 3;
+    const int g = b.g;
+    const int64_t off = b.list_off[u], n = b.list_off[u + 1] - off;
+    const int T = p.T;
+    const int64_t v_off = (int64_t)T * 128;
+    uint64_t thr[G];
+#pragma unroll
+    for (int h = 0; h < G; ++h) thr[h] = h < g ? b.dense_thr[(size_t)u * g + h] : 0;
+    auto mask_of = [&](int64_t e) {
+        uint32_t m = 0;
+#pragma unroll
+        for (int h = 0; h < G; ++h)
+            if (h < g && b.keys[off * g + (int64_t)h * n + e] <= thr[h]) m |= 1u << h;
+        return m;
+    };
+    float Oreg[16], Mreg = -INFINITY, Lreg = 0.0f;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) Oreg[j] = 0.0f;
+    for (int64_t e = warp; e < n; e += kDenseWarps) {
+        const int64_t ef = e + (int64_t)kDensePf * kDenseWarps;
+        if (lane == 0 && ef < n && mask_of(ef)) {
+            const int32_t sf = b.slots[off + ef];
+            if (kv_resident(p, sf)) prefetch_l2_bulk(kv_block<__nv_bfloat16>(p, sf) + v_off, (uint32_t)(T * 128 * 2));
+        }
+        const uint32_t mask = mask_of(e);
+        if (!mask) continue;
+        const int32_t slot = b.slots[off + e];
+        const __nv_bfloat16* vblk = kv_block<__nv_bfloat16>(p, slot) + v_off;
+        uint32_t vw[4][8];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const int tok = 2 * tq + (r & 1) + (r >> 1) * 8;
+            const int row = tok < T ? tok : T - 1;
+            const uint4* pv = reinterpret_cast<const uint4*>(vblk + (size_t)row * 128 + 16 * gq);
+            const uint4 x0 = __ldg(pv), x1 = __ldg(pv + 1);
+            vw[r][0] = x0.x; vw[r][1] = x0.y; vw[r][2] = x0.z; vw[r][3] = x0.w;
+            vw[r][4] = x1.x; vw[r][5] = x1.y; vw[r][6] = x1.z; vw[r][7] = x1.w;
+        }
+        // B columns = (head, split): weights p_t of head hb (2-term bf16 split), zero if not committed
+        const int hbq = gq >> 1, sb = gq & 1;
+        const bool hon = hbq < g && (mask >> hbq) & 1u;
+        uint32_t bfr[2];
+#pragma unroll
+        for (int hf = 0; hf < 2; ++hf) {
+            float2 wv = make_float2(0.0f, 0.0f);
+            if (hon) wv = *reinterpret_cast<const float2*>(b.dense_p + ((off * g + (int64_t)hbq * n) + e) * 16 + 2 * tq + 8 * hf);
+            bfr[hf] = pack_bf16x2_split(wv.x, wv.y, sb);
+        }
+        float ob[16];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            float c0 = 0.f, c1 = 0.f, c2 = 0.f, c3 = 0.f;
+            mma_bf16_16816(c0, c1, c2, c3, __byte_perm(vw[0][i], vw[1][i], 0x5410), __byte_perm(vw[0][i], vw[1][i], 0x7632),
+                           __byte_perm(vw[2][i], vw[3][i], 0x5410), __byte_perm(vw[2][i], vw[3][i], 0x7632), bfr[0], bfr[1]);
+            ob[2 * i] = c0 + c1;
+            ob[2 * i + 1] = c2 + c3;
+        }
+        if (tq < g && ((mask >> tq) & 1u)) {
+            const float la = b.dense_la[off * g + (int64_t)tq * n + e];  // block weight exp(la - M), sum_t p_t = 1
+            const float mnew = fmaxf(Mreg, la);
+            const float a = expf(Mreg - mnew);
+            const float cc = expf(la - mnew);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) Oreg[j] = Oreg[j] * a + ob[j] * cc;
+            Lreg = Lreg * a + cc;
+            Mreg = mnew;
+        }
+    }
+    if (tq < G) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) so[warp][tq][16 * gq + j] = Oreg[j];
+        if (gq == 0) {
+            som[warp][tq] = Mreg;
+            sol[warp][tq] = Lreg;
+        }
+    }
+    __syncthreads();
+    for (int h = 0; h < g; ++h) {
+        float Mt = -INFINITY;
+#pragma unroll
+        for (int w = 0; w < kDenseWarps; ++w) Mt = fmaxf(Mt, som[w][h]);
+        float Lt = 0.0f, sc[kDenseWarps];
+#pragma unroll
+        for (int w = 0; w < kDenseWarps; ++w) {
+            sc[w] = sol[w][h] > 0.0f ? expf(som[w][h] - Mt) : 0.0f;
+            Lt += sol[w][h] * sc[w];
+        }
+        const int64_t qi = (int64_t)u * g + h;
+        for (int i = tid; i < 128; i += kDenseWarps * 32) {
+            float o = 0.0f;
+#pragma unroll
+            for (int w = 0; w < kDenseWarps; ++w) o += sc[w] > 0.0f ? so[w][h][i] * sc[w] : 0.0f;
+            b.out[qi * 128 + i] = o / Lt;
+        }
+    }
+}
+
+bool dense_supported(const PoolView& p, const BatchView& b) {
+    return p.dtype == 1 && b.d == 128 && p.T <= 16 && b.g >= 2 && b.g <= 4 && !b.has_oracle && b.dense_flag &&
+           b.max_n <= kDenseMaxBlocks;
+}
+
+static int dense_sms() {
+    static int n = 0;
+    if (n == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
+// Persistent grids over the hand-over list (sized to the SMs: no cost when the list is empty).
+void launch_dense(const PoolView& p, const BatchView& b, cudaStream_t st) {
+    const int G = b.g <= 2 ? 2 : 4;
+    const int units = b.n_units < 2 * dense_sms() ? b.n_units : 2 * dense_sms();
+    if (G == 2) dense_k_kernel<2><<<units, kDenseWarps * 32, 0, st>>>(p, b);
+    else dense_k_kernel<4><<<units, kDenseWarps * 32, 0, st>>>(p, b);
+    int n2 = 1;
+    while (n2 < b.max_n) n2 <<= 1;
+    const size_t smem = (size_t)n2 * 8;
+    const int per_sm = smem <= 70 * 1024 ? 3 : (smem <= 110 * 1024 ? 2 : 1);
+    const int heads = b.n_units * b.g < per_sm * dense_sms() ? b.n_units * b.g : per_sm * dense_sms();
+    cudaFuncSetAttribute(dense_decide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    dense_decide_kernel<<<heads, kPsaThreads, smem, st>>>(b);
+    if (G == 2) dense_v_kernel<2><<<units, kDenseWarps * 32, 0, st>>>(p, b);
+    else dense_v_kernel<4><<<units, kDenseWarps * 32, 0, st>>>(p, b);
+}
+
+}  // namespace psa

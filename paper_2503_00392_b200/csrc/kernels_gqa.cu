@@ -507,6 +507,20 @@ __global__ void __launch_bounds__(kPsaThreads, 2) psa_gqa_kernel(PoolView p, Bat
         for (int h = 0; h < G; ++h) live += s.live[h];
         GQA_MARK(6);
         if (!live) break;
+        if constexpr (kMma) {
+            // Dense hand-over (kernels_dense.cu): a head that exhausted its first tranche needs
+            // many ranks; the unit is redone by one K pass + per-head stop rule + one V pass.
+            if (b.dense_flag) {
+                bool handover = false;
+#pragma unroll
+                for (int h = 0; h < G; ++h)
+                    handover |= s.live[h] && s.cb[h] >= s.tr0[h] + s.tc[h] && s.tr0[h] + s.tc[h] < limit;
+                if (handover) {
+                    if (tid == 0) b.dense_flag[atomicAdd(b.dense_count, 1)] = u;
+                    return;
+                }
+            }
+        }
         __syncthreads();
     }
     if constexpr (kMma) {  // registers -> the per-warp shared-memory accumulators

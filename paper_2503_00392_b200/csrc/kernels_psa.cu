@@ -371,10 +371,19 @@ static void launch_psa_t(const PoolView& p, const BatchView& b, int nq, cudaStre
 static int g_psa_choice = 0;
 void set_psa_kernel_choice(int choice) { g_psa_choice = choice; }
 
-void launch_psa(const PoolView& p, const BatchView& b, cudaStream_t st) {
+static int g_dense_mode = 0;
+void set_dense_mode(int mode) { g_dense_mode = mode; }
+
+int launch_psa(const PoolView& p, const BatchView& b, cudaStream_t st) {
     if (g_psa_choice != 1 && gqa_supported(p, b)) {  // auto = GQA-group kernel where supported
-        launch_gqa(p, b, st);
-        return;
+        BatchView v = b;
+        const bool dense = g_dense_mode == 0 && dense_supported(p, b);
+        if (!dense) v.dense_flag = nullptr;
+        if (dense) cudaMemsetAsync(v.dense_count, 0, 4, st);
+        launch_gqa(p, v, st);
+        if (!dense) return 1;
+        launch_dense(p, v, st);  // units the GQA kernel handed over (others exit at once)
+        return 4;
     }
     const int nq = b.n_units * b.g;
     if (p.dtype == 0) {
@@ -384,6 +393,7 @@ void launch_psa(const PoolView& p, const BatchView& b, cudaStream_t st) {
         if (tok_for(p.T) == 16) launch_psa_t<__nv_bfloat16, 16>(p, b, nq, st);
         else launch_psa_t<__nv_bfloat16, 32>(p, b, nq, st);
     }
+    return 1;
 }
 
 }  // namespace psa

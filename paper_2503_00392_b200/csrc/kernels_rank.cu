@@ -580,6 +580,10 @@ static BatchView sub_view(const BatchView& b, int u0, int cnt) {
     v.tcov = b.tcov ? b.tcov + qo : nullptr;
     v.term = b.term + qo;
     v.kminmax = nullptr;  // unit-indexed [2][n_units*g]: not carved per sub-batch
+    if (b.dense_flag) {
+        v.dense_flag = nullptr;  // the hand-over list is per launch: sub-batches run the round kernel only
+        v.dense_count = nullptr;
+    }
     return v;
 }
 
@@ -640,8 +644,7 @@ int launch_batch(const PoolView& p, const BatchView& b, cudaStream_t st, cudaEve
         }
         if (marks) cudaEventRecord(marks[2], st);
         if (marks) cudaEventRecord(marks[3], st);
-        launch_psa(p, b, st);
-        ++launches;
+        launches += launch_psa(p, b, st);
         if (marks) cudaEventRecord(marks[4], st);
     } else {
         // Two-stream pipeline over sub-batches of units: score(i+1) streams metadata from HBM
@@ -664,8 +667,7 @@ int launch_batch(const PoolView& p, const BatchView& b, cudaStream_t st, cudaEve
             launch_score_stage(p, v, st);
             cudaEventRecord(r.ev[1 + i], st);
             cudaStreamWaitEvent(r.aux, r.ev[1 + i], 0);
-            launch_psa(p, v, r.aux);
-            launches += 2;
+            launches += 1 + launch_psa(p, v, r.aux);
         }
         g_score_smem_floor = 0;
         if (marks) cudaEventRecord(marks[2], st);  // score chain done (progressive overlapped)

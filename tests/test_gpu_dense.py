@@ -1,0 +1,99 @@
+"""Dense hand-over of the GQA path (kernels_dense.cu): units whose heads need more than the first
+512-rank tranche (weakly skewed / isotropic keys) are redone by one K pass, a per-head stop rule
+over the masses in rank order and one V pass. Parity with the C oracle for every head, and
+equivalence with the round kernel run to the end (psattn_set_dense(1))."""
+import numpy as np
+import pytest
+
+from helpers import check_parity
+from oracle.pyoracle import BlockSet, make_config
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def mods():
+    from paper_2503_00392_b200 import batch, capi
+    return capi, batch
+
+
+def synth_batch(mods, tokens, g, planted, cfg, seed=5):
+    capi, batch = mods
+    d, T = 128, 16
+    p = capi.synth_params(seed=seed, dim=d, block_tokens=T, skew=8.0, planted_prob=planted, round_bf16=1)
+    nb = [(t + T - 1) // T for t in tokens]
+    off = np.zeros(len(tokens) + 1, np.int64)
+    off[1:] = np.cumsum(nb)
+    uids = [40 + i for i in range(len(tokens))]
+    pool = batch.DevicePool(d, T, capi.PSATTN_KV_BF16, int(off[-1]))
+    pool.fill_synthetic(p, uids, off[:-1], tokens)
+    dev = torch.device("cuda")
+    qs = np.array([[capi.synth_query(p, uid, h) for h in range(g)] for uid in uids], np.float32)
+    run = batch.BatchRun(pool, torch.tensor(qs, device=dev), torch.arange(int(off[-1]), dtype=torch.int32, device=dev),
+                         torch.tensor(off, device=dev), max(nb), batch.BatchConfig(**cfg), want_ranked=True)
+    return p, uids, nb, off, qs, run
+
+
+def results(run, off, nb, g):
+    torch.cuda.synchronize()
+    out = []
+    for u in range(len(nb)):
+        for h in range(g):
+            qi = u * g + h
+            bp = int(run.bp[qi])
+            hb = int(off[u]) * g + h * nb[u]
+            out.append(dict(bp=bp, ids=run.ranked[hb: hb + bp].cpu().numpy(), out=run.out[u, h].cpu().numpy(),
+                            est=float(run.est[qi]), term=int(run.term[qi])))
+    return out
+
+
+@pytest.mark.parametrize("g", [4, 2])
+@pytest.mark.parametrize("cfg", [dict(epsilon=0.95), dict(epsilon=0.9, microbatch_size=4), dict(topk=1200),
+                                 dict(epsilon=0.99, estimator=0)])
+def test_dense_handover_parity(mods, oracle, g, cfg):
+    capi, _ = mods
+    tokens = [16 * 3000 + 7, 16 * 1500]  # isotropic: every head needs most of its list
+    p, uids, nb, off, qs, run = synth_batch(mods, tokens, g, 0.0, cfg)
+    assert capi.lib.psattn_set_dense(0) == 0
+    run.run()
+    dense = results(run, off, nb, g)
+    assert capi.lib.psattn_set_dense(1) == 0
+    try:
+        run.run()
+        rounds = results(run, off, nb, g)
+    finally:
+        capi.lib.psattn_set_dense(0)
+    assert max(r["bp"] for r in dense) > 512  # the hand-over was exercised
+    oc = make_config(epsilon=cfg.get("epsilon", 1.0) if not cfg.get("topk") else 1.0,
+                     microbatch_size=cfg.get("microbatch_size", 1), estimator=cfg.get("estimator", 2))
+    for u, uid in enumerate(uids):
+        k, v = capi.synth_unit_host(p, uid, tokens[u])
+        nt = [min(16, tokens[u] - i * 16) for i in range(nb[u])]
+        bs = BlockSet([k[i, :nt[i]] for i in range(nb[u])], [v[i, :nt[i]] for i in range(nb[u])])
+        for h in range(g):
+            a, b = dense[u * g + h], rounds[u * g + h]
+            check_parity(oracle, qs[u, h], bs, oc, cfg.get("topk", 0), a["ids"], a["bp"], a["out"], a["est"])
+            # identical masses and decide arithmetic: same processed sets and stop points as the round kernel
+            assert a["bp"] == b["bp"] and np.array_equal(a["ids"], b["ids"]) and a["term"] == b["term"]
+            assert abs(a["est"] - b["est"]) <= 1e-6
+            assert np.max(np.abs(a["out"] - b["out"])) <= 1e-4
+
+
+def test_planted_units_stay_on_round_kernel(mods):
+    """Sparse (planted) units finish inside their first tranche: dense on/off give identical bits."""
+    capi, _ = mods
+    tokens = [16 * 4096, 16 * 2048 + 3]
+    p, uids, nb, off, qs, run = synth_batch(mods, tokens, 4, 1 / 32, dict(epsilon=0.95))
+    run.run()
+    a = results(run, off, nb, 4)
+    assert capi.lib.psattn_set_dense(1) == 0
+    try:
+        run.run()
+        b = results(run, off, nb, 4)
+    finally:
+        capi.lib.psattn_set_dense(0)
+    assert max(r["bp"] for r in a) < 512
+    for x, y in zip(a, b):
+        assert x["bp"] == y["bp"] and np.array_equal(x["out"], y["out"])
