@@ -150,7 +150,7 @@ int psattn_set_progressive_kernel(int32_t mode);
  * k = k sub-batches (<= 16). */
 int psattn_set_pipeline(int32_t sub_batches);
 /* Dense hand-over of the GQA kernel (kernels_dense.cu): 0 = auto (a unit whose head exhausts
- * its first 512-rank tranche is redone by one K pass + per-head stop rule + one V pass),
+ * 384 ranks without stopping is redone by one K pass + per-head stop rule + one V pass),
  * 1 = off (the round kernel runs every unit to the end). Same results either way. */
 int psattn_set_dense(int32_t mode);
 /* Score-kernel selection: 0 = auto (TMA-staged for dim 128), 1 = register-staged, 2 = TMA whenever supported. */

@@ -77,7 +77,8 @@ struct BatchView {
     float* dense_p;                 // [total*g][16] normalised token weights
     unsigned long long* dense_thr;  // [n_units*g] rank-threshold key of each head's processed set
 };
-constexpr int64_t kDenseMaxBlocks = 16384;
+constexpr int64_t kDenseMaxBlocks = 16384;  // decide smem: 12 B per rank (196 KB)
+constexpr int64_t kDenseHandover = 384;     // ranks a head consumes on the round kernel before the hand-over
 
 int dpl_for(int d);
 int tok_for(int T);

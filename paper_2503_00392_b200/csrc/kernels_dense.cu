@@ -5,7 +5,8 @@
 // of the group reaches it. When the heads need many ranks (weakly skewed attention, e.g.
 // isotropic keys: ~90% of the list at eps 0.95) their rank orders diverge and a block is
 // K-scored in up to g different rounds. psa_gqa_kernel therefore hands a unit over to this
-// path when one of its heads exhausts its first tranche (512 ranks), and the unit is redone:
+// path when one of its heads has consumed kDenseHandover (384) ranks without stopping, and the unit
+// is redone:
 //
 //   dense_k_kernel           ONE K pass over every block of the list (tensor-core scores for
 //                            all heads at once): per (head, block) the fp32 block mass
@@ -156,6 +157,15 @@ __device__ __forceinline__ void dense_decide_head(const BatchView& b, int u, int
     for (int64_t i = threadIdx.x; i < n2; i += blockDim.x) ks[i] = i < n ? b.keys[hb + i] : ~0ull;
     __syncthreads();
     bitonic_smem(ks, (int)n, cta_team());
+    // every rank's list position (ranked_pos output) and mass, gathered by the whole CTA so the
+    // sequential walk below reads shared memory only
+    float* xs = reinterpret_cast<float*>(ks + n2);
+    for (int64_t r = threadIdx.x; r < limit; r += blockDim.x) {
+        const int64_t pos = (int64_t)(ks[r] & pmask);
+        b.rpos[hb + r] = (int32_t)pos;
+        xs[r] = b.dense_la[hb + pos];
+    }
+    __syncthreads();
     if (threadIdx.x >= 32) return;  // (the caller's __syncthreads: warps 1.. arrive early)
     const int lane = threadIdx.x;
     double acc = -INFINITY, mn = INFINITY, ssum = 0.0;
@@ -164,9 +174,7 @@ __device__ __forceinline__ void dense_decide_head(const BatchView& b, int u, int
     for (;;) {
         const int64_t left = limit - cb;
         const int cnt = (int)(left < 32 ? left : 32);
-        const int64_t pos = lane < cnt ? (int64_t)(ks[cb + lane] & pmask) : 0;
-        const float x = lane < cnt ? b.dense_la[hb + pos] : -INFINITY;
-        if (lane < cnt) b.rpos[hb + cb + lane] = (int32_t)pos;
+        const float x = lane < cnt ? xs[cb + lane] : -INFINITY;
         if (!decide_chunk_fast(x, cnt, cb, n, limit, b.m, eps, acc, ssum, mn, b.iest ? b.iest + hb : nullptr, dc)) {
             acc = ssum > 0.0 ? acc + log(ssum) : -INFINITY;
             dc = decide_chunk((double)x, cnt, cb, n, limit, b.m, eps, acc, mn, b.iest ? b.iest + hb : nullptr);
@@ -322,7 +330,7 @@ void launch_dense(const PoolView& p, const BatchView& b, cudaStream_t st) {
     else dense_k_kernel<4><<<units, kDenseWarps * 32, 0, st>>>(p, b);
     int n2 = 1;
     while (n2 < b.max_n) n2 <<= 1;
-    const size_t smem = (size_t)n2 * 8;
+    const size_t smem = (size_t)n2 * 12;  // sorted keys + masses in rank order
     const int per_sm = smem <= 70 * 1024 ? 3 : (smem <= 110 * 1024 ? 2 : 1);
     const int heads = b.n_units * b.g < per_sm * dense_sms() ? b.n_units * b.g : per_sm * dense_sms();
     cudaFuncSetAttribute(dense_decide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -514,7 +514,7 @@ __global__ void __launch_bounds__(kPsaThreads, 2) psa_gqa_kernel(PoolView p, Bat
                 bool handover = false;
 #pragma unroll
                 for (int h = 0; h < G; ++h)
-                    handover |= s.live[h] && s.cb[h] >= s.tr0[h] + s.tc[h] && s.tr0[h] + s.tc[h] < limit;
+                    handover |= s.live[h] && s.cb[h] >= kDenseHandover && s.cb[h] < limit;
                 if (handover) {
                     if (tid == 0) b.dense_flag[atomicAdd(b.dense_count, 1)] = u;
                     return;
