@@ -125,6 +125,29 @@ __device__ __forceinline__ double smem_reduce(double (&acc)[N], double* red, int
 // Same reduction with XOR-swizzled 16-double rows (no padding): 32 x 16 doubles =
 // exactly 4 KB, so it fits in a consumed TMA stage buffer. Conflict-free (2 wavefronts
 // per 64-bit access, the minimum) for both the row writes and the column reads.
+// Column-major variant (the TMA kernel's): value i's 32 partials are written contiguously
+// (red[i*32 + lane]: immediate offsets, conflict-free), and lane (v = lane & 15, part = lane >> 4)
+// sums the partials of lanes [16*part, 16*part + 16) of value v in the XOR order k ^ v, so the
+// 16 lanes of a half-warp hit 16 different 8-byte bank pairs; the address of read k is
+// A ^ 8k (one LOP3). Returns the total of value (lane & 15) on lanes v and v + 16.
+__device__ __forceinline__ double smem_reduce16_cm(double (&acc)[16], double* red, int lane) {
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < 16; ++i) red[i * 32 + lane] = acc[i];
+    __syncwarp();
+    const int v = lane & 15, part = lane >> 4;
+    const uint32_t a0 = smem_u32(red) + (uint32_t)(v * 256 + part * 128 + v * 8);
+    double t = 0.0;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+        double x;
+        asm volatile("ld.shared.f64 %0, [%1];" : "=d"(x) : "r"(a0 ^ (uint32_t)(8 * k)));
+        t += x;
+    }
+    t += __shfl_xor_sync(PSA_FULL, t, 16);
+    return t;
+}
+
 __device__ __forceinline__ double smem_reduce16_swz(double (&acc)[16], double* red, int lane) {
     __syncwarp();
 #pragma unroll
@@ -297,9 +320,12 @@ __global__ void __launch_bounds__(kScoreWarps * 32, 2) score_kernel_tma(PoolView
     }
     constexpr int est = EST;  // estimator as a template parameter: no per-record branches
     const double scale = b.scale;
-    const int my_idx = lane >> SH;
+    // value this lane owns after the reduction: lane & 15 (lanes 0-15 write) for the column-major
+    // 16-value reduce, else lane >> SH
+    constexpr bool kCM = (N == 16 && STAGE >= 4096);
+    const int my_idx = kCM ? (lane & 15) : (lane >> SH);
     const int my_h = my_idx / kRecs, my_j = my_idx % kRecs;
-    const bool writer = (lane & ((1 << SH) - 1)) == 0 && my_h < b.g;
+    const bool writer = (kCM ? lane < 16 : (lane & ((1 << SH) - 1)) == 0) && my_h < b.g;
     uint64_t* keys = b.keys + off * b.g + (int64_t)my_h * n;
     uint64_t kmin = ~0ull, kmax = 0;  // keys written by this lane (first-tranche bounds)
     const uint64_t pol = policy_evict_first();
@@ -383,7 +409,7 @@ __global__ void __launch_bounds__(kScoreWarps * 32, 2) score_kernel_tma(PoolView
         // (N = 16 doubles x 32 lanes = 4 KB = one bf16 stage); then it is refilled.
         double tot;
         if constexpr (N == 16 && STAGE >= 4096) {
-            tot = smem_reduce16_swz(acc, reinterpret_cast<double*>(wbuf + stage * STAGE), lane);
+            tot = smem_reduce16_cm(acc, reinterpret_cast<double*>(wbuf + stage * STAGE), lane);
         } else {
             tot = smem_reduce<N>(acc, reinterpret_cast<double*>(smem + kTmaBarBytes + (size_t)kScoreWarps * S * STAGE) +
                                           warp * 32 * (N + 1),
