@@ -54,6 +54,7 @@ def parse():
     ap.add_argument("--psa-kernel", type=int, default=0, help="0 auto, 1 per q-head, 2 GQA group")
     ap.add_argument("--score-kernel", type=int, default=0, help="0 auto, 1 register-staged, 2 TMA-staged")
     ap.add_argument("--pipeline", type=int, default=1, help="0 auto, 1 off, k sub-batches")
+    ap.add_argument("--graph", type=int, default=1, help="1: replay the step as a captured CUDA graph")
     return ap.parse_args()
 
 
@@ -253,7 +254,8 @@ def run_ours(args):
     off = torch.arange(U + 1, dtype=torch.int64, device=dev) * n
     cfg = batch.BatchConfig(epsilon=args.eps, microbatch_size=args.microbatch)
     run = batch.BatchRun(pool, q_dev, slots, off, n, cfg, want_ranked=True)
-    stream = torch.cuda.current_stream()
+    stream = torch.cuda.Stream()  # a non-default stream: graph capture and every launch/copy/event go here
+    torch.cuda.set_stream(stream)
 
     def barrier():
         if ws > 1:
@@ -268,20 +270,33 @@ def run_ours(args):
     torch.cuda.synchronize()
     barrier()
     torch.cuda.synchronize()
-    capi.lib.psattn_profile_read(None, None, 1)
+    step = run.run
+    if args.graph:
+        run.capture(stream)  # one decode step = one CUDA graph replay
+        step = run.run_graph
+        for _ in range(args.warmup):
+            step()
+        torch.cuda.synchronize()
     phases = np.zeros(12, np.uint64)
     prof_build = capi.lib.psattn_debug_gqa_phases(phases.ctypes.data) == 0  # PROF=1 development build only
-    capi.lib.psattn_profile_enable(1)
+    barrier()
+    torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(args.steps):
-        launches_per_step = run.run()
+        launches_per_step = step()
     e1.record(stream)
     torch.cuda.synchronize()
-    capi.lib.psattn_profile_enable(0)
     barrier()
     clk = clocks.stop()
     ms = e0.elapsed_time(e1)
+    # per-stage kernel times: the same steps launched directly with CUDA events between the stages
+    capi.lib.psattn_profile_read(None, None, 1)
+    capi.lib.psattn_profile_enable(1)
+    for _ in range(args.steps):
+        run.run()
+    torch.cuda.synchronize()
+    capi.lib.psattn_profile_enable(0)
     stage_ms = np.zeros(4, np.float64)
     stage_n = np.zeros(4, np.int64)
     capi.lib.psattn_profile_read(stage_ms.ctypes.data, stage_n.ctypes.data, 1)
@@ -333,7 +348,7 @@ def run_ours(args):
 
     def e2e_step():
         run.q.copy_(q_pin, non_blocking=True)
-        run.run()
+        step()
         out_pin.copy_(run.out, non_blocking=True)
         bp_pin.copy_(run.bp, non_blocking=True)
         est_pin.copy_(run.est, non_blocking=True)
@@ -350,6 +365,23 @@ def run_ours(args):
     e2e_s = time.perf_counter() - t0
     e2e_s = shard.max_over_ranks(e2e_s, dev)
     e2e_val = nq * ws * args.steps / e2e_s
+
+    # ---- optional final output gather over NCCL (N > 1; not part of `value`) ----
+    gather = None
+    if ws > 1:
+        for _ in range(2):
+            shard.gather_outputs(run.out)
+        torch.cuda.synchronize()
+        barrier()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        for _ in range(args.steps):
+            allout = shard.gather_outputs(run.out)
+        g1.record(stream)
+        torch.cuda.synchronize()
+        gms = shard.max_over_ranks(g0.elapsed_time(g1) / args.steps, dev)
+        gather = dict(ms_per_step=gms, bytes_per_step=int(allout.numel()) * 4, collective="all_gather (NCCL)",
+                      value_with_gather=nq * ws / ((ms_per_step + gms) / 1e3))
 
     # ---- CPU baseline (rank 0, N=1 only) ----
     cpu_base = None
@@ -381,6 +413,7 @@ def run_ours(args):
             cpu_baseline=cpu_base,
             e2e=dict(value=e2e_val, unit=UNIT, h2d_bytes_per_step=h2d, d2h_bytes_per_step=d2h),
             gpu_launches=int(launches_per_step) * args.steps,
+            cuda_graph=bool(args.graph), gather=gather,
             clocks=clk, setup=dict(fill_seconds=fill_s, pool_gib=(U * n * (lay.slot_bytes + lay.meta_bytes)) / 2**30),
         )
         print(json.dumps(line), flush=True)

@@ -130,6 +130,15 @@ size_t psattn_batch_workspace_bytes(const psattn_batch* b);
  * synchronisation. workspace: device memory of psattn_batch_workspace_bytes. */
 int psattn_run_batch(psattn_pool* pool, const psattn_batch* b, void* workspace, void* stream);
 
+/* CUDA-graph capture of one decode step: psattn_run_batch on (pool, b, workspace) recorded once
+ * (relaxed stream capture on `stream`, or an internal stream when NULL) and replayed by
+ * psattn_graph_launch on any stream, re-reading the same device buffers (queries, page tables)
+ * at every replay: the serving loop refreshes q / slots in place and replays. */
+typedef struct psattn_graph psattn_graph;
+int psattn_graph_create(psattn_pool* pool, const psattn_batch* b, void* workspace, void* stream, psattn_graph** out);
+int psattn_graph_launch(psattn_graph* g, void* stream);
+void psattn_graph_destroy(psattn_graph* g);
+
 /* Per-unit count of distinct blocks processed by any head of the group (the
  * GQA union the algorithmic byte count uses), after psattn_run_batch on the
  * same stream and workspace. out_union: device int64 [n_units]. */

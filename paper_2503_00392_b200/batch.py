@@ -182,6 +182,23 @@ class BatchRun:
         lib.psattn_batch_last_launches(C.byref(n))
         return n.value
 
+    def capture(self, stream=None):
+        """Records this batch's launch sequence as a CUDA graph; run_graph() replays it."""
+        self.graph = C.c_void_p()
+        check(lib.psattn_graph_create(self.pool.h, C.byref(self.b), _dp(self.ws), _stream_ptr(stream),
+                                      C.byref(self.graph)))
+
+    def run_graph(self, stream=None) -> int:
+        check(lib.psattn_graph_launch(self.graph, _stream_ptr(stream)))
+        n = C.c_int32()
+        lib.psattn_batch_last_launches(C.byref(n))
+        return n.value
+
+    def __del__(self):
+        if lib is not None and getattr(self, "graph", None) is not None and self.graph.value:
+            lib.psattn_graph_destroy(self.graph)
+            self.graph = None
+
     def union_blocks(self, stream=None) -> torch.Tensor:
         check(lib.psattn_batch_union_blocks(C.byref(self.b), _dp(self.ws), _dp(self.union), _stream_ptr(stream)))
         return self.union

@@ -157,6 +157,9 @@ def _load() -> C.CDLL:
     L.psattn_synth_is_planted.argtypes = [C.POINTER(SynthParams), i64, i64]
     L.psattn_pool_fill_synthetic.argtypes = [vp, C.POINTER(SynthParams), i32, vp, vp, vp, vp]
     L.psattn_set_dense.argtypes = [i32]
+    L.psattn_graph_create.argtypes = [vp, C.POINTER(Batch), vp, vp, C.POINTER(vp)]
+    L.psattn_graph_launch.argtypes = [vp, vp]
+    L.psattn_graph_destroy.argtypes = [vp]
     L.psattn_exact_attention.argtypes = [vp, C.POINTER(Batch), vp, vp]
     L.psattn_tradeoff.argtypes = [vp, C.POINTER(Batch), dbl, C.POINTER(TradeoffReport), vp]
     L.psattn_tier_create.argtypes = [C.POINTER(TierDesc), C.POINTER(vp)]
@@ -189,6 +192,7 @@ EXPORTED = [
     "psattn_batch_workspace_bytes", "psattn_run_batch", "psattn_batch_union_blocks", "psattn_batch_last_launches",
     "psattn_profile_enable", "psattn_profile_read", "psattn_set_progressive_kernel",
     "psattn_set_score_kernel", "psattn_set_pipeline", "psattn_set_dense",
+    "psattn_graph_create", "psattn_graph_launch", "psattn_graph_destroy",
     "psattn_synth_direction", "psattn_synth_query", "psattn_synth_unit_host", "psattn_synth_is_planted",
     "psattn_pool_fill_synthetic", "psattn_exact_attention", "psattn_tradeoff",
     "psattn_tier_create", "psattn_tier_destroy", "psattn_tier_put_blocks", "psattn_tier_release_request",

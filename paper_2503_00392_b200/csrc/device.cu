@@ -488,6 +488,60 @@ int psattn_set_progressive_kernel(int32_t mode) {
     return PSATTN_OK;
 }
 
+}  // extern "C"
+
+struct psattn_graph {
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    int launches = 0;
+};
+
+extern "C" {
+
+int psattn_graph_create(psattn_pool* pool, const psattn_batch* b, void* workspace, void* stream, psattn_graph** out) {
+    if (!out) return fail(PSATTN_ERR_INVALID_ARGUMENT, "psattn_graph_create: null output");
+    int rc = validate_batch(pool, b);
+    if (rc) return rc;
+    if (!workspace) return fail(PSATTN_ERR_INVALID_ARGUMENT, "psattn_graph_create: null workspace");
+    cudaStream_t st = (cudaStream_t)stream, own = nullptr;
+    if (!st) {
+        cudaError_t e = cudaStreamCreateWithFlags(&own, cudaStreamNonBlocking);
+        if (e != cudaSuccess) return cuda_fail(e, "psattn_graph_create: stream");
+        st = own;
+    }
+    auto* g = new psattn_graph();
+    cudaError_t e = cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed);
+    if (e == cudaSuccess) {
+        const BatchView v = make_view(pool, b, workspace);
+        g->launches = launch_batch(pool->v, v, st, nullptr);
+        e = cudaStreamEndCapture(st, &g->graph);
+        if (e == cudaSuccess && g->launches < 0) e = cudaErrorUnknown;
+    }
+    if (e == cudaSuccess) e = cudaGraphInstantiate(&g->exec, g->graph, 0);
+    if (own) cudaStreamDestroy(own);
+    if (e != cudaSuccess) {
+        psattn_graph_destroy(g);
+        return cuda_fail(e, "psattn_graph_create: capture");
+    }
+    *out = g;
+    return PSATTN_OK;
+}
+
+int psattn_graph_launch(psattn_graph* g, void* stream) {
+    if (!g) return fail(PSATTN_ERR_INVALID_ARGUMENT, "psattn_graph_launch: null graph");
+    const cudaError_t e = cudaGraphLaunch(g->exec, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "psattn_graph_launch");
+    g_last_launches.store(g->launches);
+    return PSATTN_OK;
+}
+
+void psattn_graph_destroy(psattn_graph* g) {
+    if (!g) return;
+    if (g->exec) cudaGraphExecDestroy(g->exec);
+    if (g->graph) cudaGraphDestroy(g->graph);
+    delete g;
+}
+
 int psattn_set_dense(int32_t mode) {
     if (mode < 0 || mode > 1) return fail(PSATTN_ERR_INVALID_ARGUMENT, "psattn_set_dense: mode must be 0 or 1");
     set_dense_mode(mode);

@@ -13,6 +13,8 @@ fi
 if [[ $what == all || $what == bench ]]; then
   timeout 600 python bench.py > gpurun_out/bench_$tag.log 2>&1; echo "bench rc=$?"
   tail -1 gpurun_out/bench_$tag.log
+  timeout 600 python bench.py --dist iso --steps 10 --no-cpu-baseline > gpurun_out/bench_iso_$tag.log 2>&1; echo "bench iso rc=$?"
+  timeout 600 python scripts/config3_report.py gpurun_out/config3_$tag.json > /dev/null 2>&1; echo "config3 rc=$?"
   timeout 300 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref_$tag.log 2>&1; echo "ref rc=$?"
   tail -1 gpurun_out/bench_ref_$tag.log | cut -c1-300
 fi
@@ -23,6 +25,15 @@ if [[ $what == all || $what == ncu ]]; then
   for k in score_kernel psa_gqa_kernel; do
     timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k --launch-skip 2 -c 1 \
        -o gpurun_out/${tag}_$k -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline \
+       > gpurun_out/ncu_full_${k}_$tag.log 2>&1; echo "ncu $k rc=$?"
+  done
+  # isotropic keys: the dense hand-over kernels carry the step
+  timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
+     -k regex:"psa|score|dense" --launch-skip 6 -c 6 --csv --log-file gpurun_out/launches_iso_$tag.csv \
+     python bench.py --steps 1 --warmup 3 --no-cpu-baseline --dist iso > /dev/null 2>&1; echo "ncu iso rc=$?"
+  for k in dense_k_kernel dense_v_kernel; do
+    timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k --launch-skip 1 -c 1 \
+       -o gpurun_out/${tag}_$k -f python bench.py --steps 1 --warmup 1 --no-cpu-baseline --dist iso \
        > gpurun_out/ncu_full_${k}_$tag.log 2>&1; echo "ncu $k rc=$?"
   done
 fi

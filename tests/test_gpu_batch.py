@@ -342,3 +342,38 @@ def test_long_lists_multi_tranche(mods, oracle, kernel, kv_dtype):
             r = unpack(run, off, u, h, n)
             assert r["bp"] > 1100  # several tranches consumed
             check_parity(oracle, qs[u][h], units[u], make_config(epsilon=0.99), 0, r["ids"], r["bp"], r["out"], r["est"])
+
+
+@pytest.mark.parametrize("planted", [1 / 32, 0.0])
+def test_graph_replay_identical(mods, planted):
+    """A decode step captured as a CUDA graph (psattn_graph_*) replays bit-identically to the
+    direct launch, including after the queries are refreshed in place (the serving pattern);
+    planted = 0 exercises the dense hand-over inside the graph."""
+    capi, batch = mods
+    d, T, g = 128, 16, 4
+    p = capi.synth_params(seed=3, dim=d, block_tokens=T, skew=8.0, planted_prob=planted, round_bf16=1)
+    units, n = [21, 22, 23], 1200
+    pool = batch.DevicePool(d, T, capi.PSATTN_KV_BF16, n * len(units))
+    pool.fill_synthetic(p, units, np.arange(len(units)) * n, [n * T] * len(units))
+    dev = torch.device("cuda")
+    q0 = torch.tensor(np.array([[capi.synth_query(p, u, h) for h in range(g)] for u in units], np.float32), device=dev)
+    q1 = torch.tensor(np.array([[capi.synth_query(p, u + 100, h) for h in range(g)] for u in units], np.float32),
+                      device=dev)
+    slots = torch.arange(n * len(units), dtype=torch.int32, device=dev)
+    off = torch.arange(len(units) + 1, dtype=torch.int64, device=dev) * n
+    run = batch.BatchRun(pool, q0.clone(), slots, off, n, batch.BatchConfig(epsilon=0.95), want_ranked=True)
+    stream = torch.cuda.Stream()
+    run.capture(stream)
+    for q in (q0, q1, q0):
+        run.q.copy_(q)
+        run.run()
+        torch.cuda.synchronize()
+        ref = (run.out.clone(), run.bp.clone(), run.est.clone())
+        run.out.zero_()
+        run.bp.zero_()
+        assert run.run_graph() == run.run()
+        torch.cuda.synchronize()
+        run.out.zero_()
+        run.run_graph()
+        torch.cuda.synchronize()
+        assert torch.equal(run.out, ref[0]) and torch.equal(run.bp, ref[1]) and torch.equal(run.est, ref[2])
