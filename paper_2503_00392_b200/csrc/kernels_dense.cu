@@ -13,17 +13,17 @@
 //                            la = m + log(l) (block_partial_attention's log_as, reference
 //                            attention.hpp:73) and the normalised token weights p_t = w_t / l;
 //   dense_decide_kernel      per head: its full rank order (bitonic sort of the head's keys in
-//                            shared memory) and Algorithm 1's sequential stop rule over the
-//                            masses in rank order (decide_chunk_fast / decide_chunk, the same
-//                            arithmetic as the round kernel) -> blocks_processed, estimate and
-//                            the rank threshold key;
+//                            shared memory) and Algorithm 1's stop rule over the masses in rank
+//                            order, evaluated for all ranks at once (per-thread online
+//                            log-sum-exp, block scan, second walk: the first boundary with
+//                            est > eps) -> blocks_processed, estimate, rank threshold key;
 //   dense_v_kernel           ONE V pass over the union of the heads' processed sets: block b
 //                            belongs to head h's set iff key_h(b) <= threshold_h (keys are
 //                            unique and ordered), accumulated with mma.sync like the round
 //                            kernel's V pass, merged with weight exp(la - M).
 //
-// Same processed sets and stop points as the round kernel (identical masses, same decide);
-// outputs differ only by fp32 summation order.
+// Same processed sets and stop points as the round kernel (identical masses; the estimates
+// differ only by rounding, ~1e-7); outputs differ only by fp32 summation order.
 #include <cuda_bf16.h>
 #include <math.h>
 
@@ -166,28 +166,79 @@ __device__ __forceinline__ void dense_decide_head(const BatchView& b, int u, int
         xs[r] = b.dense_la[hb + pos];
     }
     __syncthreads();
-    if (threadIdx.x >= 32) return;  // (the caller's __syncthreads: warps 1.. arrive early)
-    const int lane = threadIdx.x;
-    double acc = -INFINITY, mn = INFINITY, ssum = 0.0;
-    int64_t cb = 0;
-    Decision dc{};
-    for (;;) {
-        const int64_t left = limit - cb;
-        const int cnt = (int)(left < 32 ? left : 32);
-        const float x = lane < cnt ? xs[cb + lane] : -INFINITY;
-        if (!decide_chunk_fast(x, cnt, cb, n, limit, b.m, eps, acc, ssum, mn, b.iest ? b.iest + hb : nullptr, dc)) {
-            acc = ssum > 0.0 ? acc + log(ssum) : -INFINITY;
-            dc = decide_chunk((double)x, cnt, cb, n, limit, b.m, eps, acc, mn, b.iest ? b.iest + hb : nullptr);
-            ssum = 1.0;
+    // Algorithm 1's stop rule over all ranks at once (every mass is known): thread t owns ranks
+    // [t*seg, (t+1)*seg). (1) online log-sum-exp (running max M, fp64 sum S relative to it, min)
+    // of its segment; (2) its exclusive prefix over the other threads' triples; (3) a second walk from the
+    // prefix evaluating est = S / (S + n_left * exp(min - M)) at every microbatch boundary (the
+    // reference's 1 / (1 + n_left * exp(min - acc)), engine.cpp:48-55); (4) the first rank whose
+    // boundary has est > eps (or reaches the limit) over the block is the stop point.
+    __shared__ float tM[kPsaThreads], tmn[kPsaThreads];
+    __shared__ double tS[kPsaThreads];
+    __shared__ unsigned long long first_stop;
+    const int tid = threadIdx.x;
+    const int64_t seg = (limit + kPsaThreads - 1) / kPsaThreads;
+    const int64_t r0 = (int64_t)tid * seg, r1 = r0 + seg < limit ? r0 + seg : limit;
+    auto absorb = [](float x, float& M, double& S, float& mn) {
+        if (x > M) {
+            S = (M == -INFINITY) ? 1.0 : fma(S, (double)expf(M - x), 1.0);
+            M = x;
+        } else {
+            S += (double)expf(x - M);
         }
-        cb += dc.commit;
-        if (dc.fin) break;
+        mn = fminf(mn, x);
+    };
+    auto combine = [](float Ma, double Sa, float mna, float& M, double& S, float& mn) {  // (a) then (M, S, mn)
+        const float Mx = fmaxf(Ma, M);
+        const double sa = Ma == -INFINITY ? 0.0 : Sa * (double)expf(Ma - Mx);
+        const double sb = M == -INFINITY ? 0.0 : S * (double)expf(M - Mx);
+        M = Mx;
+        S = sa + sb;
+        mn = fminf(mna, mn);
+    };
+    float M = -INFINITY, mn = INFINITY;
+    double S = 0.0;
+    for (int64_t r = r0; r < r1; ++r) absorb(xs[r], M, S, mn);
+    // exclusive prefix of this thread: the triples of threads 0 .. tid-1, combined in order
+    tM[tid] = M;
+    tS[tid] = S;
+    tmn[tid] = mn;
+    if (tid == 0) first_stop = ~0ull;
+    __syncthreads();
+    float PM = -INFINITY, Pmn = INFINITY;
+    double PS = 0.0;
+    for (int t = 0; t < tid; ++t) {
+        float m2 = tM[t], n2v = tmn[t];
+        double s2 = tS[t];
+        combine(PM, PS, Pmn, m2, s2, n2v);
+        PM = m2;
+        PS = s2;
+        Pmn = n2v;
     }
-    if (lane == 0) {
+    // walk again from the prefix
+    int64_t stop_r = -1;
+    float stop_est = 0.0f;
+    for (int64_t r = r0; r < r1; ++r) {
+        absorb(xs[r], PM, PS, Pmn);
+        const bool boundary = b.m == 1 || ((r + 1) % b.m) == 0 || (r + 1 == limit);
+        if (!boundary) continue;
+        const int64_t nl = n - (r + 1);
+        const float sf = (float)PS;
+        const float est = nl == 0 ? 1.0f : sf / fmaf((float)nl, expf(Pmn - PM), sf);
+        if (b.iest) b.iest[hb + r] = (double)est;
+        if ((double)est > eps || r + 1 == limit) {
+            stop_r = r;
+            stop_est = est;
+            break;
+        }
+    }
+    if (stop_r >= 0) atomicMin(&first_stop, (unsigned long long)stop_r);
+    __syncthreads();
+    if (stop_r >= 0 && (unsigned long long)stop_r == first_stop) {
+        const int64_t cb = stop_r + 1;
         b.bp[qi] = cb;
-        b.est[qi] = dc.est;
+        b.est[qi] = (double)stop_est;
         b.term[qi] = b.topk > 0 ? (limit < n) : (cb < n);
-        b.dense_thr[qi] = ks[cb - 1];
+        b.dense_thr[qi] = ks[stop_r];
     }
 }
 
