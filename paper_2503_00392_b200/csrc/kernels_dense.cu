@@ -35,7 +35,10 @@
 namespace psa {
 
 constexpr int kDenseWarps = 8;
-constexpr int kDensePf = 4;  // L2 prefetch distance (warp iterations)
+#ifndef PSA_DENSE_PF
+#define PSA_DENSE_PF 2
+#endif
+constexpr int kDensePf = PSA_DENSE_PF;  // L2 prefetch distance (warp iterations)
 
 // q fragments of the K pass (see psa_gqa_kernel): columns = (head, split), 4 per head.
 template <int G>

@@ -13,6 +13,9 @@ constexpr int kPsaWarps = 8;
 constexpr int kPsaThreads = kPsaWarps * 32;
 constexpr int kChunk = 32;
 constexpr int kBins = 2048;
+#ifndef PSA_SCAN_U
+#define PSA_SCAN_U 8
+#endif
 
 // A group of whole warps cooperating on one selection: the full CTA (__syncthreads)
 // or a sub-team synchronised by a named barrier (bar.sync id, size).
@@ -78,7 +81,7 @@ __device__ __forceinline__ void bitonic_smem(uint64_t* a, int n, const Team& tm)
 // Scalar head/tail keys are handled by team thread 0, so f must tolerate a partial warp.
 template <typename F>
 __device__ __forceinline__ void scan_keys(const uint64_t* __restrict__ keys, int64_t n, const Team& tm, F&& f) {
-    constexpr int U = 8;
+    constexpr int U = PSA_SCAN_U;
     const int64_t head = ((reinterpret_cast<uintptr_t>(keys) & 15) && n > 0) ? 1 : 0;
     const ulonglong2* k2 = reinterpret_cast<const ulonglong2*>(keys + head);
     const int64_t n2 = (n - head) >> 1;
@@ -231,7 +234,7 @@ static __device__ __noinline__ int select_tranche(SelScratch& s, uint64_t* tb, i
 __device__ __forceinline__ void fill_tranche(const uint64_t* tb, int tc, uint64_t pmask, int32_t* rpos_out,
                                              const int32_t* __restrict__ slots, const int32_t* ntok, int32_t* tslot,
                                              uint8_t* tntok, const Team& tm) {
-    constexpr int U = 8;
+    constexpr int U = PSA_SCAN_U;
     for (int i0 = tm.tid; i0 < tc; i0 += U * tm.size) {
         int32_t sl[U], nt[U];
 #pragma unroll
