@@ -251,7 +251,7 @@ int read_meta(const psattn_pool* pool, int64_t slot, float* mean, float* lo, flo
 
 // ---- workspace carving ----
 struct WsLayout {
-    size_t keys, rpos, omass, kmm, dflag, dla, dp, dthr, total;
+    size_t keys, rpos, omass, kmm, dflag, dla, dp, dthr, ft, total;
 };
 
 static WsLayout ws_layout(const psattn_batch* b) {
@@ -278,6 +278,14 @@ static WsLayout ws_layout(const psattn_batch* b) {
         o += align_up(hb * 64, 256);
         l.dthr = o;
         o += align_up((size_t)b->n_units * b->group * 8, 256);
+    }
+    // first tranche of every head (GQA shapes): keys | slots | ntok | count
+    l.ft = 0;
+    if ((b->dim == 128 || b->dim == 64) && b->group >= 2 && b->group <= 4) {
+        const size_t hq = (size_t)b->n_units * b->group;
+        l.ft = o;
+        o += align_up(hq * kFirstCap * 8, 256) + align_up(hq * kFirstCap * 4, 256) + align_up(hq * kFirstCap, 256) +
+             align_up(hq * 4, 256);
     }
     l.total = o;
     return l;
@@ -345,6 +353,17 @@ BatchView make_view(const psattn_pool* pool, const psattn_batch* b, void* worksp
     v.dense_la = l.dflag ? reinterpret_cast<float*>(ws + l.dla) : nullptr;
     v.dense_p = l.dflag ? reinterpret_cast<float*>(ws + l.dp) : nullptr;
     v.dense_thr = l.dflag ? reinterpret_cast<unsigned long long*>(ws + l.dthr) : nullptr;
+    if (l.ft) {
+        const size_t hq = (size_t)b->n_units * b->group;
+        char* f = ws + l.ft;
+        v.ft_keys = reinterpret_cast<unsigned long long*>(f);
+        f += align_up(hq * kFirstCap * 8, 256);
+        v.ft_slot = reinterpret_cast<int32_t*>(f);
+        f += align_up(hq * kFirstCap * 4, 256);
+        v.ft_ntok = reinterpret_cast<uint8_t*>(f);
+        f += align_up(hq * kFirstCap, 256);
+        v.ft_count = reinterpret_cast<int32_t*>(f);
+    }
     (void)pool;
     return v;
 }

@@ -76,7 +76,14 @@ struct BatchView {
     float* dense_la;                // [total*g] fp32 block masses
     float* dense_p;                 // [total*g][16] normalised token weights
     unsigned long long* dense_thr;  // [n_units*g] rank-threshold key of each head's processed set
+    // first tranche of every head, selected up front by first_tranche_kernel (nullptr: the
+    // progressive kernel selects it itself): [n_units*g][kFirstCap] sorted keys, slots, ntok, count
+    unsigned long long* ft_keys;
+    int32_t* ft_slot;
+    uint8_t* ft_ntok;
+    int32_t* ft_count;
 };
+constexpr int kFirstCap = 512;  // == the GQA kernel's tranche capacity
 constexpr int64_t kDenseMaxBlocks = 16384;  // decide smem: 12 B per rank (196 KB)
 constexpr int64_t kDenseHandover = 384;     // ranks a head consumes on the round kernel before the hand-over
 
@@ -96,7 +103,7 @@ cudaError_t launch_synth_fill(const PoolView& p, uint64_t seed, float skew, floa
                               const int64_t* d_tokens, int64_t max_blocks, float* d_dirs, cudaStream_t st);
 int launch_psa(const PoolView& p, const BatchView& b, cudaStream_t st);  // returns kernels launched
 bool gqa_supported(const PoolView& p, const BatchView& b);
-void launch_gqa(const PoolView& p, const BatchView& b, cudaStream_t st);
+int launch_gqa(const PoolView& p, const BatchView& b, cudaStream_t st);  // returns kernels launched
 // 0 = auto (GQA kernel when supported), 1 = per-query kernel, 2 = GQA kernel
 void set_psa_kernel_choice(int choice);
 void set_score_kernel_choice(int choice);

@@ -30,7 +30,7 @@ namespace psa {
 // With correlated heads (the usual GQA case) U is ~1 chunk, so K/V bytes and
 // the bf16->fp32 conversions are ~1/g of the per-head kernel's.
 // =============================================================================
-constexpr int kGTCap = 512;   // tranche capacity per head
+constexpr int kGTCap = kFirstCap;  // tranche capacity per head
 constexpr int kHash = 512;    // pos -> U index (>= 2 * G * kChunk)
 constexpr int kGBins = 1024;  // bucket-select bins per head team
 
@@ -170,7 +170,16 @@ __global__ void __launch_bounds__(kPsaThreads, 2) psa_gqa_kernel(PoolView p, Bat
             const bool need = s.live[h] && s.cb[h] >= s.tr0[h] + s.tc[h];
             int tc = 0;
             int64_t t0 = 0;
-            if (need) {
+            if (need && b.ft_keys && s.tr0[h] + s.tc[h] == 0) {
+                // first tranche selected up front (first_tranche_kernel): copy it in
+                const size_t qi = (size_t)u * g + h;
+                tc = b.ft_count[qi];
+                for (int i = tm.tid; i < tc; i += tm.size) {
+                    s.tb[h][i] = b.ft_keys[qi * kGTCap + i];
+                    s.tslot[h][i] = b.ft_slot[qi * kGTCap + i];
+                    s.tntok[h][i] = b.ft_ntok[qi * kGTCap + i];
+                }
+            } else if (need) {
                 const int64_t hb = off * g + (int64_t)h * n;
                 t0 = s.tr0[h] + s.tc[h];
                 tc = select_tranche(s.sel[h], s.tb[h], kGTCap, s.hist[h], kGBins, b.keys + hb, n, s.last[h], t0 == 0,
@@ -587,12 +596,35 @@ static void launch_gqa_g(const PoolView& p, const BatchView& b, cudaStream_t st)
     else launch_gqa_t<KV, 2, 16, true, G>(p, b, st);
 }
 
+// First tranche of every (unit, head) up front: one CTA per head, bandwidth-parallel across the
+// batch instead of four 2-warp teams inside each progressive CTA (the same select_tranche /
+// fill_tranche, so the tranche is identical). Writes the ranked positions of the tranche too.
+__global__ void __launch_bounds__(kPsaThreads) first_tranche_kernel(PoolView p, BatchView b) {
+    __shared__ SelScratch sel;
+    __shared__ uint32_t hist[kGBins];
+    __shared__ uint64_t tb[kGTCap];
+    const int qi = blockIdx.x;
+    const int u = qi / b.g, h = qi % b.g;
+    const int64_t off = b.list_off[u], n = b.list_off[u + 1] - off;
+    const int64_t hb = off * b.g + (int64_t)h * n;
+    const uint64_t pmask = (b.pos_bits >= 64) ? ~0ull : ((1ull << b.pos_bits) - 1ull);
+    const Team tm = cta_team();
+    const int tc = select_tranche(sel, tb, kGTCap, hist, kGBins, b.keys + hb, n, 0, true, kGTCap, tm,
+                                  b.kminmax ? b.kminmax + qi : nullptr, (int64_t)b.n_units * b.g);
+    fill_tranche(tb, tc, pmask, b.rpos + hb, b.slots + off, p.ntok, b.ft_slot + (size_t)qi * kGTCap,
+                 b.ft_ntok + (size_t)qi * kGTCap, tm);
+    for (int i = threadIdx.x; i < tc; i += blockDim.x) b.ft_keys[(size_t)qi * kGTCap + i] = tb[i];
+    if (threadIdx.x == 0) b.ft_count[qi] = tc;
+}
+
 bool gqa_supported(const PoolView& p, const BatchView& b) {
     return b.g >= 2 && b.g <= 4 && (b.d == 128 || b.d == 64) && p.T <= 16;
 }
 
-void launch_gqa(const PoolView& p, const BatchView& b, cudaStream_t st) {
+int launch_gqa(const PoolView& p, const BatchView& b, cudaStream_t st) {
     const int G = b.g <= 2 ? 2 : 4;
+    if (b.ft_keys) first_tranche_kernel<<<b.n_units * b.g, kPsaThreads, 0, st>>>(p, b);
+    const int launches = b.ft_keys ? 2 : 1;
     if (p.dtype == 0) {
         if (G == 2) launch_gqa_g<float, 2>(p, b, st);
         else launch_gqa_g<float, 4>(p, b, st);
@@ -600,6 +632,7 @@ void launch_gqa(const PoolView& p, const BatchView& b, cudaStream_t st) {
         if (G == 2) launch_gqa_g<__nv_bfloat16, 2>(p, b, st);
         else launch_gqa_g<__nv_bfloat16, 4>(p, b, st);
     }
+    return launches;
 }
 
 }  // namespace psa

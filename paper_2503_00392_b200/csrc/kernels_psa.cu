@@ -380,10 +380,10 @@ int launch_psa(const PoolView& p, const BatchView& b, cudaStream_t st) {
         const bool dense = g_dense_mode == 0 && dense_supported(p, b);
         if (!dense) v.dense_flag = nullptr;
         if (dense) cudaMemsetAsync(v.dense_count, 0, 4, st);
-        launch_gqa(p, v, st);
-        if (!dense) return 1;
+        const int n = launch_gqa(p, v, st);
+        if (!dense) return n;
         launch_dense(p, v, st);  // units the GQA kernel handed over (others exit at once)
-        return 4;
+        return n + 3;
     }
     const int nq = b.n_units * b.g;
     if (p.dtype == 0) {

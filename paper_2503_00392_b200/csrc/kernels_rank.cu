@@ -610,6 +610,12 @@ static BatchView sub_view(const BatchView& b, int u0, int cnt) {
         v.dense_flag = nullptr;  // the hand-over list is per launch: sub-batches run the round kernel only
         v.dense_count = nullptr;
     }
+    if (b.ft_keys) {  // head-indexed [n_units*g][kFirstCap]: offset to the sub-batch's heads
+        v.ft_keys = b.ft_keys + qo * kFirstCap;
+        v.ft_slot = b.ft_slot + qo * kFirstCap;
+        v.ft_ntok = b.ft_ntok + qo * kFirstCap;
+        v.ft_count = b.ft_count + qo;
+    }
     return v;
 }
 
