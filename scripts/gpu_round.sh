@@ -22,14 +22,14 @@ if [[ $what == all || $what == ncu ]]; then
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
      --log-file gpurun_out/launches_$tag.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline \
      > gpurun_out/ncu_launch_bench_$tag.log 2>&1; echo "ncu launches rc=$?"
-  for k in score_kernel psa_gqa_kernel; do
+  for k in score_kernel psa_gqa_kernel first_tranche_kernel; do
     timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k --launch-skip 2 -c 1 \
        -o gpurun_out/${tag}_$k -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline \
        > gpurun_out/ncu_full_${k}_$tag.log 2>&1; echo "ncu $k rc=$?"
   done
   # isotropic keys: the dense hand-over kernels carry the step
   timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
-     -k regex:"psa|score|dense" --launch-skip 6 -c 6 --csv --log-file gpurun_out/launches_iso_$tag.csv \
+     -k regex:"psa|score|dense|first" --launch-skip 7 -c 7 --csv --log-file gpurun_out/launches_iso_$tag.csv \
      python bench.py --steps 1 --warmup 3 --no-cpu-baseline --dist iso > /dev/null 2>&1; echo "ncu iso rc=$?"
   for k in dense_k_kernel dense_v_kernel; do
     timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k --launch-skip 1 -c 1 \

@@ -1,0 +1,60 @@
+"""Small end-to-end launches of every kernel family for compute-sanitizer (memcheck / racecheck /
+synccheck): score (TMA), first tranche, GQA round kernel, dense hand-over, per-head kernel, metadata
+build, append, tier install, tradeoff/exact. Sizes are tiny: the tools replay every access."""
+import os
+import sys
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2503_00392_b200 import batch, capi  # noqa: E402
+
+dev = torch.device("cuda")
+d, T, g = 128, 16, 4
+
+
+def synth_run(tokens, planted, cfg, kv=capi.PSATTN_KV_BF16, kernel=0):
+    p = capi.synth_params(seed=2, dim=d, block_tokens=T, skew=8.0, planted_prob=planted, round_bf16=1)
+    nb = [(t + T - 1) // T for t in tokens]
+    off = np.zeros(len(tokens) + 1, np.int64)
+    off[1:] = np.cumsum(nb)
+    pool = batch.DevicePool(d, T, kv, int(off[-1]))
+    uids = list(range(7, 7 + len(tokens)))
+    pool.fill_synthetic(p, uids, off[:-1], tokens)
+    qs = np.array([[capi.synth_query(p, u, h) for h in range(g)] for u in uids], np.float32)
+    run = batch.BatchRun(pool, torch.tensor(qs, device=dev), torch.arange(int(off[-1]), dtype=torch.int32, device=dev),
+                         torch.tensor(off, device=dev), max(nb), batch.BatchConfig(**cfg), want_ranked=True)
+    capi.check(capi.lib.psattn_set_progressive_kernel(kernel))
+    run.run()
+    torch.cuda.synchronize()
+    capi.check(capi.lib.psattn_set_progressive_kernel(0))
+    return pool, run
+
+
+synth_run([16 * 900 + 3, 16 * 300], 1 / 32, dict(epsilon=0.95))            # score + first tranche + GQA
+synth_run([16 * 700 + 5], 0.0, dict(epsilon=0.95))                          # dense hand-over
+synth_run([16 * 500], 0.0, dict(epsilon=0.9), kernel=1)                     # per-head kernel
+synth_run([16 * 400 + 1], 0.05, dict(topk=64, microbatch_size=3), kv=capi.PSATTN_KV_F32)
+pool, run = synth_run([16 * 300], 0.05, dict(epsilon=0.9, audit_coverage=1, microbatch_size=2))
+run.exact_attention()
+torch.cuda.synchronize()
+# append + metadata rebuild
+tail = torch.tensor([5, 9], dtype=torch.int32, device=dev)
+pool.append_tokens(tail, torch.randn(2, d, device=dev), torch.randn(2, d, device=dev))
+torch.cuda.synchronize()
+# two-tier store: put, batch with host-resident blocks, install
+tier = batch.DeviceTier(d, T, capi.PSATTN_KV_BF16, 2, 200, 60)
+rng = np.random.default_rng(0)
+K = rng.standard_normal((200, T, d)).astype(np.float32)
+V = rng.standard_normal((200, T, d)).astype(np.float32)
+tier.put_blocks(np.arange(200), np.arange(200) % 2, np.full(200, T), K, V)
+lists = [np.arange(0, 200, 2), np.arange(1, 200, 2)]
+off = torch.tensor([0, 100, 200], dtype=torch.int64, device=dev)
+tr = batch.BatchRun(tier, torch.randn(2, g, d, device=dev), torch.tensor(np.concatenate(lists).astype(np.int32), device=dev),
+                    off, 100, batch.BatchConfig(epsilon=0.9))
+tr.run()
+tr.run()
+torch.cuda.synchronize()
+print("sanitize driver ok")
