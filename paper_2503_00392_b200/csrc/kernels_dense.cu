@@ -157,16 +157,45 @@ __device__ __forceinline__ void dense_decide_head(const BatchView& b, int u, int
     const double eps = b.topk > 0 ? 1.0 : b.eps;
     int n2 = 1;
     while (n2 < n) n2 <<= 1;
-    for (int64_t i = threadIdx.x; i < n2; i += blockDim.x) ks[i] = i < n ? b.keys[hb + i] : ~0ull;
+    {  // 8 loads in flight per thread (the loop is latency-bound otherwise)
+        constexpr int U = 8;
+        for (int64_t i0 = threadIdx.x; i0 < n2; i0 += (int64_t)U * blockDim.x) {
+            uint64_t v[U];
+#pragma unroll
+            for (int k = 0; k < U; ++k) {
+                const int64_t i = i0 + (int64_t)k * blockDim.x;
+                v[k] = i < n ? __ldg(reinterpret_cast<const unsigned long long*>(b.keys) + hb + i) : ~0ull;
+            }
+#pragma unroll
+            for (int k = 0; k < U; ++k) {
+                const int64_t i = i0 + (int64_t)k * blockDim.x;
+                if (i < n2) ks[i] = v[k];
+            }
+        }
+    }
     __syncthreads();
     bitonic_smem(ks, (int)n, cta_team());
     // every rank's list position (ranked_pos output) and mass, gathered by the whole CTA so the
     // sequential walk below reads shared memory only
     float* xs = reinterpret_cast<float*>(ks + n2);
-    for (int64_t r = threadIdx.x; r < limit; r += blockDim.x) {
-        const int64_t pos = (int64_t)(ks[r] & pmask);
-        b.rpos[hb + r] = (int32_t)pos;
-        xs[r] = b.dense_la[hb + pos];
+    {
+        constexpr int U = 8;
+        for (int64_t r0 = threadIdx.x; r0 < limit; r0 += (int64_t)U * blockDim.x) {
+            float v[U];
+#pragma unroll
+            for (int k = 0; k < U; ++k) {
+                const int64_t r = r0 + (int64_t)k * blockDim.x;
+                v[k] = r < limit ? __ldg(b.dense_la + hb + (int64_t)(ks[r] & pmask)) : 0.0f;
+            }
+#pragma unroll
+            for (int k = 0; k < U; ++k) {
+                const int64_t r = r0 + (int64_t)k * blockDim.x;
+                if (r < limit) {
+                    b.rpos[hb + r] = (int32_t)(ks[r] & pmask);
+                    xs[r] = v[k];
+                }
+            }
+        }
     }
     __syncthreads();
     // Algorithm 1's stop rule over all ranks at once (every mass is known): thread t owns ranks

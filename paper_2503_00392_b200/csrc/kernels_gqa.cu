@@ -383,6 +383,7 @@ __global__ void __launch_bounds__(kPsaThreads, 2) psa_gqa_kernel(PoolView p, Bat
             if (tid == 0) pc[9] += clock64() - d0_;
 #endif
             if (lane < dc.commit) atomicOr(&s.umask[s.cidx[h][lane]], 1u << h);
+            __syncwarp();  // every lane read the carried state above before lane 0 replaces it
             if (lane == 0) {
                 s.commit[h] = dc.commit;
                 s.fin[h] = dc.fin;
