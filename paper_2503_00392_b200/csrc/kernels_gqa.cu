@@ -254,13 +254,13 @@ __global__ void __launch_bounds__(kPsaThreads, 2) psa_gqa_kernel(PoolView p, Bat
         if (act) s.cidx[hh][rr] = s.hval[hs];
         const int ucount = s.ucount;
 #ifndef PSA_PF
-#define PSA_PF 1
+#define PSA_PF 0
 #endif
         if constexpr (kMma && PSA_PF >= 1) {
             // Bulk L2 prefetch of every U block's K (threads 0..) and V (threads 128..): the K pass
             // below then walks L2-resident blocks, and the V pass finds committed blocks in L2.
             const int e = tid & (G * kChunk - 1);
-            if (e < ucount && tid < 2 * G * kChunk && kv_resident(p, s.uslot[e]))
+            if (e < ucount && tid < (PSA_PF == 3 ? 1 : 2) * G * kChunk && kv_resident(p, s.uslot[e]))
                 prefetch_l2_bulk(kv_block<KV>(p, s.uslot[e]) + (tid >= G * kChunk ? v_off : 0),
                                  (uint32_t)(T * 128 * sizeof(KV)));
         }
