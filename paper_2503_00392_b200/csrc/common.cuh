@@ -146,13 +146,15 @@ template <> struct Log2<1> { static constexpr int v = 0; };
 // low `pos_bits` bits carrying the list position: scores that agree in all but
 // their last pos_bits key bits (relative 2^-(52-pos_bits)) compare by position,
 // i.e. by block id — the reference's tie rule (metadata.cpp:92-93).
-__device__ __forceinline__ uint64_t make_key(double s, uint32_t pos, int pos_bits) {
+__device__ __forceinline__ uint64_t make_key_masked(double s, uint32_t pos, uint64_t mask) {
     s = s + 0.0;  // -0 -> +0: the reference compares doubles, where -0 == +0
     const uint64_t u = (uint64_t)__double_as_longlong(s);
     const uint64_t asc = (u >> 63) ? ~u : (u | 0x8000000000000000ull);
     const uint64_t desc = ~asc;
-    const uint64_t mask = (pos_bits >= 64) ? ~0ull : ((1ull << pos_bits) - 1ull);
     return (desc & ~mask) | (uint64_t)pos;
+}
+__device__ __forceinline__ uint64_t make_key(double s, uint32_t pos, int pos_bits) {
+    return make_key_masked(s, pos, (pos_bits >= 64) ? ~0ull : ((1ull << pos_bits) - 1ull));
 }
 
 }  // namespace psa

@@ -319,7 +319,9 @@ __global__ void __launch_bounds__(kScoreWarps * 32, 2) score_kernel_tma(PoolView
         for (int j = 0; j < DPL; ++j) qd[h][j] = (double)qf[j] * 0x1p896;
     }
     constexpr int est = EST;  // estimator as a template parameter: no per-record branches
-    const double scale = b.scale;
+    // acc = 4 CuboidMean / 2 Upper / Mean: the power-of-two factor folded into the scale (exact)
+    const double kscale = est == 2 ? 0.25 * b.scale : (est == 1 ? 0.5 * b.scale : b.scale);
+    const uint64_t kmask = (b.pos_bits >= 64) ? ~0ull : ((1ull << b.pos_bits) - 1ull);
     // value this lane owns after the reduction: lane & 15 (lanes 0-15 write) for the column-major
     // 16-value reduce, else lane >> SH
     constexpr bool kCM = (N == 16 && STAGE >= 4096);
@@ -421,8 +423,7 @@ __global__ void __launch_bounds__(kScoreWarps * 32, 2) score_kernel_tma(PoolView
         if (gn < ngroups) issue(gn, stage, nslot);
         const int64_t p0 = grp * kRecs;
         if (writer && p0 + my_j < n) {
-            const double sc = est == 2 ? 0.25 * (tot * scale) : (est == 1 ? 0.5 * (tot * scale) : tot * scale);
-            const uint64_t key = make_key(sc, (uint32_t)(p0 + my_j), b.pos_bits);
+            const uint64_t key = make_key_masked(tot * kscale, (uint32_t)(p0 + my_j), kmask);
             keys[p0 + my_j] = key;
             kmin = key < kmin ? key : kmin;
             kmax = key > kmax ? key : kmax;
