@@ -34,21 +34,29 @@ constexpr int kGTCap = kFirstCap;  // tranche capacity per head
 constexpr int kHash = 512;    // pos -> U index (>= 2 * G * kChunk)
 constexpr int kGBins = 1024;  // bucket-select bins per head team
 
-template <int TOK, int G>
+// CH: ranks per head per round. CH = 64 (tensor-core path with the dense hand-over) halves the
+// rounds; it has no later-tranche selection (a head that exhausts its first tranche is handed
+// over) and its per-warp output accumulators alias the token weights (both fit 2 CTAs / SM).
+template <int TOK, int G, int CH = kChunk>
 struct GqaSmem {
+    static constexpr bool kWide = CH > kChunk;
     uint64_t tb[G][kGTCap];
     int32_t tslot[G][kGTCap];
     uint8_t tntok[G][kGTCap];
-    uint32_t hist[G][kGBins];
-    float w[G * kChunk][G][TOK];   // per (U entry, head) token weights exp(s - m)
-    float mb[G * kChunk][G], lb[G * kChunk][G], la[G * kChunk][G];
-    float o[kPsaWarps][G][128];    // per-warp, per-head output accumulators (d <= 128)
+    uint32_t hist[kWide ? 1 : G][kWide ? 1 : kGBins];
+    union alignas(16) {
+        float w[G * CH][G][TOK];  // per (U entry, head) token weights exp(s - m)
+        float o_alias[kWide ? kPsaWarps : 1][G][128];
+    } wo;
+    float mb[G * CH][G], lb[G * CH][G];  // block max and exp-sum (log_as = mb + log lb)
+    float o_sep[kWide ? 1 : kPsaWarps][kWide ? 1 : G][kWide ? 1 : 128];  // per-warp, per-head output accumulators
+    __device__ __forceinline__ float* o(int w_, int h_) { return kWide ? wo.o_alias[w_][h_] : o_sep[w_][h_]; }
     float om[kPsaWarps][G], ol[kPsaWarps][G];
-    int32_t uslot[G * kChunk];
-    int32_t upos[G * kChunk];
-    uint8_t untok[G * kChunk];
-    uint32_t umask[G * kChunk];
-    int16_t cidx[G][kChunk];
+    int32_t uslot[G * CH];
+    int32_t upos[G * CH];
+    uint8_t untok[G * CH];
+    uint32_t umask[G * CH];
+    int16_t cidx[G][CH];
     int32_t hkey[kHash];
     int32_t hfirst[kHash];
     int16_t hval[kHash];
@@ -78,10 +86,11 @@ __device__ unsigned long long g_gqa_prof[12];
     } while (0)
 #endif
 
-template <typename KV, int DPL, int TOK, bool FULL, int G>
+template <typename KV, int DPL, int TOK, bool FULL, int G, int CH>
 __global__ void __launch_bounds__(kPsaThreads, 2) psa_gqa_kernel(PoolView p, BatchView b) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    GqaSmem<TOK, G>& s = *reinterpret_cast<GqaSmem<TOK, G>*>(smem_raw);
+    GqaSmem<TOK, G, CH>& s = *reinterpret_cast<GqaSmem<TOK, G, CH>*>(smem_raw);
+    constexpr bool kWide = GqaSmem<TOK, G, CH>::kWide;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int u = blockIdx.x;
     const int g = b.g;
@@ -156,7 +165,8 @@ __global__ void __launch_bounds__(kPsaThreads, 2) psa_gqa_kernel(PoolView p, Bat
         (&s.om[0][0])[i] = -INFINITY;
         (&s.ol[0][0])[i] = 0.0f;
     }
-    for (int i = tid; i < kPsaWarps * G * 128; i += kPsaThreads) (&s.o[0][0][0])[i] = 0.0f;
+    if constexpr (!GqaSmem<TOK, G, CH>::kWide)
+        for (int i = tid; i < kPsaWarps * G * 128; i += kPsaThreads) (&s.o_sep[0][0][0])[i] = 0.0f;
     __syncthreads();
     GQA_MARK(0);
 
@@ -179,7 +189,7 @@ __global__ void __launch_bounds__(kPsaThreads, 2) psa_gqa_kernel(PoolView p, Bat
                     s.tslot[h][i] = b.ft_slot[qi * kGTCap + i];
                     s.tntok[h][i] = b.ft_ntok[qi * kGTCap + i];
                 }
-            } else if (need) {
+            } else if (!kWide && need) {  // (the wide variant hands the unit over instead)
                 const int64_t hb = off * g + (int64_t)h * n;
                 t0 = s.tr0[h] + s.tc[h];
                 tc = select_tranche(s.sel[h], s.tb[h], kGTCap, s.hist[h], kGBins, b.keys + hb, n, s.last[h], t0 == 0,
@@ -211,13 +221,14 @@ __global__ void __launch_bounds__(kPsaThreads, 2) psa_gqa_kernel(PoolView p, Bat
             if (s.live[tid]) {
                 const int64_t room = s.tr0[tid] + s.tc[tid] - s.cb[tid];
                 const int64_t left = limit - s.cb[tid];
-                c = (int)(left < kChunk ? left : kChunk);
+                c = (int)(left < CH ? left : CH);
                 if (room < c) c = (int)room;
             }
             s.cnt[tid] = c;
         }
         __syncthreads();
-        const int hh = tid >> 5, rr = tid & 31;  // one thread per (head, rank in chunk)
+        static_assert(G * CH <= kPsaThreads && 2 * G * CH <= kHash, "one thread per (head, rank) of the round");
+        const int hh = tid / CH, rr = tid % CH;  // one thread per (head, rank in chunk)
         const bool act = hh < G && rr < s.cnt[hh];
         int hs = -1, ci = 0;
         if (act) {
@@ -259,9 +270,9 @@ __global__ void __launch_bounds__(kPsaThreads, 2) psa_gqa_kernel(PoolView p, Bat
         if constexpr (kMma && PSA_PF >= 1) {
             // Bulk L2 prefetch of every U block's K (threads 0..) and V (threads 128..): the K pass
             // below then walks L2-resident blocks, and the V pass finds committed blocks in L2.
-            const int e = tid & (G * kChunk - 1);
-            if (e < ucount && tid < (PSA_PF == 3 ? 1 : 2) * G * kChunk && kv_resident(p, s.uslot[e]))
-                prefetch_l2_bulk(kv_block<KV>(p, s.uslot[e]) + (tid >= G * kChunk ? v_off : 0),
+            const int e = tid & (G * CH - 1);
+            if (e < ucount && tid < (PSA_PF == 3 ? 1 : 2) * G * CH && kv_resident(p, s.uslot[e]))
+                prefetch_l2_bulk(kv_block<KV>(p, s.uslot[e]) + (tid >= G * CH ? v_off : 0),
                                  (uint32_t)(T * 128 * sizeof(KV)));
         }
         GQA_MARK(2);
@@ -309,12 +320,11 @@ __global__ void __launch_bounds__(kPsaThreads, 2) psa_gqa_kernel(PoolView p, Bat
 #pragma unroll
                     for (int o = 4; o < 32; o <<= 1) lbv += __shfl_xor_sync(PSA_FULL, lbv, o);
                     if ((tq & 1) == 0 && hq < G) {
-                        s.w[e][hq][gq] = wlo;
-                        s.w[e][hq][gq + 8] = whi;
+                        s.wo.w[e][hq][gq] = wlo;
+                        s.wo.w[e][hq][gq + 8] = whi;
                         if (gq == 0) {
                             s.mb[e][hq] = mbv;
                             s.lb[e][hq] = lbv;
-                            s.la[e][hq] = mbv + logf(lbv);
                         }
                     }
                 }
@@ -342,11 +352,10 @@ __global__ void __launch_bounds__(kPsaThreads, 2) psa_gqa_kernel(PoolView p, Bat
                 float lbv = wv;
 #pragma unroll
                 for (int o = 16; o >= (1 << TSH); o >>= 1) lbv += __shfl_xor_sync(PSA_FULL, lbv, o);
-                if ((lane & ((1 << TSH) - 1)) == 0) s.w[e][h][my_tok] = wv;
+                if ((lane & ((1 << TSH) - 1)) == 0) s.wo.w[e][h][my_tok] = wv;
                 if (lane == 0) {
                     s.mb[e][h] = mbv;
                     s.lb[e][h] = lbv;
-                    s.la[e][h] = mbv + logf(lbv);
                 }
             }
         }
@@ -358,31 +367,40 @@ __global__ void __launch_bounds__(kPsaThreads, 2) psa_gqa_kernel(PoolView p, Bat
         // ---- 4. decide: warp h for head h, all heads in parallel ----
         if (warp < G && s.live[warp]) {
             const int h = warp;
-            const int cnt = s.cnt[h];
+            const int cnt_all = s.cnt[h];
             const int64_t hb = off * g + (int64_t)h * n;
-            double x = -INFINITY;
-            if (lane < cnt) {
-                const int e = s.cidx[h][lane];
-                x = b.has_oracle ? b.omass[hb + s.upos[e]] : (double)s.la[e][h];
-            }
             double acc = s.acc[h], mn = s.mn[h], ssum = s.ssum[h];
 #ifdef PSA_GQA_PROF
             const long long d0_ = clock64();
 #endif
-            Decision dc;
-            if (b.has_oracle) {
-                dc = decide_chunk(x, cnt, s.cb[h], n, limit, b.m, eps, acc, mn, b.iest ? b.iest + hb : nullptr);
-            } else if (!decide_chunk_fast((float)x, cnt, s.cb[h], n, limit, b.m, eps, acc, ssum, mn,
-                                          b.iest ? b.iest + hb : nullptr, dc)) {
-                // fp64 fallback: carried (M, S) -> log-sum-exp and back (M' = lse, S' = 1)
-                acc = ssum > 0.0 ? acc + log(ssum) : -INFINITY;
-                dc = decide_chunk(x, cnt, s.cb[h], n, limit, b.m, eps, acc, mn, b.iest ? b.iest + hb : nullptr);
-                ssum = 1.0;
+            Decision dc{};
+            int committed = 0;
+            // the head's chunk in 32-rank pieces (one piece unless CH = 64); stop at the first stop
+            for (int c0 = 0; c0 < cnt_all; c0 += 32) {
+                const int cnt = cnt_all - c0 < 32 ? cnt_all - c0 : 32;
+                double x = -INFINITY;
+                if (lane < cnt) {
+                    const int e = s.cidx[h][c0 + lane];
+                    x = b.has_oracle ? b.omass[hb + s.upos[e]] : (double)(s.mb[e][h] + logf(s.lb[e][h]));
+                }
+                const int64_t cb = s.cb[h] + c0;
+                if (b.has_oracle) {
+                    dc = decide_chunk(x, cnt, cb, n, limit, b.m, eps, acc, mn, b.iest ? b.iest + hb : nullptr);
+                } else if (!decide_chunk_fast((float)x, cnt, cb, n, limit, b.m, eps, acc, ssum, mn,
+                                              b.iest ? b.iest + hb : nullptr, dc)) {
+                    // fp64 fallback: carried (M, S) -> log-sum-exp and back (M' = lse, S' = 1)
+                    acc = ssum > 0.0 ? acc + log(ssum) : -INFINITY;
+                    dc = decide_chunk(x, cnt, cb, n, limit, b.m, eps, acc, mn, b.iest ? b.iest + hb : nullptr);
+                    ssum = 1.0;
+                }
+                if (lane < dc.commit) atomicOr(&s.umask[s.cidx[h][c0 + lane]], 1u << h);
+                committed = c0 + dc.commit;
+                if (dc.fin) break;
             }
+            dc.commit = committed;
 #ifdef PSA_GQA_PROF
             if (tid == 0) pc[9] += clock64() - d0_;
 #endif
-            if (lane < dc.commit) atomicOr(&s.umask[s.cidx[h][lane]], 1u << h);
             __syncwarp();  // every lane read the carried state above before lane 0 replaces it
             if (lane == 0) {
                 s.commit[h] = dc.commit;
@@ -435,7 +453,7 @@ __global__ void __launch_bounds__(kPsaThreads, 2) psa_gqa_kernel(PoolView p, Bat
                 uint32_t bfr[2];
 #pragma unroll
                 for (int hf = 0; hf < 2; ++hf) {
-                    const float2 wv = hon ? *reinterpret_cast<const float2*>(&s.w[e][hb][2 * tq + 8 * hf])
+                    const float2 wv = hon ? *reinterpret_cast<const float2*>(&s.wo.w[e][hb][2 * tq + 8 * hf])
                                           : make_float2(0.0f, 0.0f);
                     bfr[hf] = pack_bf16x2_split(wv.x, wv.y, sb);
                 }
@@ -473,7 +491,7 @@ __global__ void __launch_bounds__(kPsaThreads, 2) psa_gqa_kernel(PoolView p, Bat
                 for (int jj = 0; jj < DPL; ++jj) ob[jj] = 0.0f;
 #pragma unroll
                 for (int t = 0; t < TOK; ++t) {
-                    const float wt = s.w[e][h][t];
+                    const float wt = s.wo.w[e][h][t];
 #pragma unroll
                     for (int jj = 0; jj < DPL; ++jj) ob[jj] = fmaf(wt, vr[t][jj], ob[jj]);
                 }
@@ -482,7 +500,7 @@ __global__ void __launch_bounds__(kPsaThreads, 2) psa_gqa_kernel(PoolView p, Bat
                 const float mnew = fmaxf(M, mbj);
                 const float a = expf(M - mnew);
                 const float c = expf(mbj - mnew);
-                float* op = &s.o[warp][h][base];
+                float* op = s.o(warp, h) + base;
 #pragma unroll
                 for (int jj = 0; jj < DPL; ++jj)
                     if (base + jj < d) op[jj] = op[jj] * a + ob[jj] * c;
@@ -524,7 +542,8 @@ __global__ void __launch_bounds__(kPsaThreads, 2) psa_gqa_kernel(PoolView p, Bat
                 bool handover = false;
 #pragma unroll
                 for (int h = 0; h < G; ++h)
-                    handover |= s.live[h] && s.cb[h] >= kDenseHandover && s.cb[h] < limit;
+                    handover |= s.live[h] && s.cb[h] < limit &&
+                                (s.cb[h] >= kDenseHandover || (kWide && s.cb[h] >= s.tr0[h] + s.tc[h]));
                 if (handover) {
                     if (tid == 0) b.dense_flag[atomicAdd(b.dense_count, 1)] = u;
                     return;
@@ -537,7 +556,7 @@ __global__ void __launch_bounds__(kPsaThreads, 2) psa_gqa_kernel(PoolView p, Bat
         const int gq = lane >> 2, tq = lane & 3;
         if (tq < G) {
 #pragma unroll
-            for (int j = 0; j < 16; ++j) s.o[warp][tq][16 * gq + j] = Oreg[j];
+            for (int j = 0; j < 16; ++j) s.o(warp, tq)[16 * gq + j] = Oreg[j];
             if (gq == 0) {
                 s.om[warp][tq] = Mreg;
                 s.ol[warp][tq] = Lreg;
@@ -560,7 +579,7 @@ __global__ void __launch_bounds__(kPsaThreads, 2) psa_gqa_kernel(PoolView p, Bat
         for (int i = tid; i < d; i += kPsaThreads) {
             float o = 0.0f;
 #pragma unroll
-            for (int w = 0; w < kPsaWarps; ++w) o += sc[w] > 0.0f ? s.o[w][h][i] * sc[w] : 0.0f;
+            for (int w = 0; w < kPsaWarps; ++w) o += sc[w] > 0.0f ? s.o(w, h)[i] * sc[w] : 0.0f;
             b.out[qi * d + i] = o / Lt;
         }
         if (b.tcov && tid == 0) {
@@ -583,11 +602,28 @@ __global__ void __launch_bounds__(kPsaThreads, 2) psa_gqa_kernel(PoolView p, Bat
 #endif
 }
 
+template <typename KV, int DPL, int TOK, bool FULL, int G, int CH>
+static void launch_gqa_c(const PoolView& p, const BatchView& b, cudaStream_t st) {
+    const size_t smem = sizeof(GqaSmem<TOK, G, CH>);
+    cudaFuncSetAttribute(psa_gqa_kernel<KV, DPL, TOK, FULL, G, CH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    psa_gqa_kernel<KV, DPL, TOK, FULL, G, CH><<<b.n_units, kPsaThreads, smem, st>>>(p, b);
+}
+
+#ifndef PSA_WIDE_CHUNK
+#define PSA_WIDE_CHUNK 64
+#endif
 template <typename KV, int DPL, int TOK, bool FULL, int G>
 static void launch_gqa_t(const PoolView& p, const BatchView& b, cudaStream_t st) {
-    const size_t smem = sizeof(GqaSmem<TOK, G>);
-    cudaFuncSetAttribute(psa_gqa_kernel<KV, DPL, TOK, FULL, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    psa_gqa_kernel<KV, DPL, TOK, FULL, G><<<b.n_units, kPsaThreads, smem, st>>>(p, b);
+    // 64-rank rounds on the tensor-core path when the dense hand-over covers long heads
+    constexpr bool kMmaPath = std::is_same<KV, __nv_bfloat16>::value && DPL == 4 && TOK == 16 && FULL;
+    if constexpr (kMmaPath && PSA_WIDE_CHUNK > kChunk) {
+        if (b.dense_flag) {
+            launch_gqa_c<KV, DPL, TOK, FULL, G, PSA_WIDE_CHUNK>(p, b, st);
+            return;
+        }
+    }
+    launch_gqa_c<KV, DPL, TOK, FULL, G, kChunk>(p, b, st);
 }
 
 template <typename KV, int G>

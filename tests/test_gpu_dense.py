@@ -82,7 +82,8 @@ def test_dense_handover_parity(mods, oracle, g, cfg):
 
 
 def test_planted_units_stay_on_round_kernel(mods):
-    """Sparse (planted) units finish inside their first tranche: dense on/off give identical bits."""
+    """Sparse (planted) units finish inside their first tranche, never handed over: dense on (64-rank
+    rounds) and off (32-rank rounds) process the same blocks; outputs agree up to summation order."""
     capi, _ = mods
     tokens = [16 * 4096, 16 * 2048 + 3]
     p, uids, nb, off, qs, run = synth_batch(mods, tokens, 4, 1 / 32, dict(epsilon=0.95))
@@ -96,4 +97,5 @@ def test_planted_units_stay_on_round_kernel(mods):
         capi.lib.psattn_set_dense(0)
     assert max(r["bp"] for r in a) < 384
     for x, y in zip(a, b):
-        assert x["bp"] == y["bp"] and np.array_equal(x["out"], y["out"])
+        assert x["bp"] == y["bp"] and np.array_equal(x["ids"], y["ids"]) and abs(x["est"] - y["est"]) <= 1e-6
+        assert np.max(np.abs(x["out"] - y["out"])) <= 1e-5
