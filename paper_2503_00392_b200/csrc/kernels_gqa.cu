@@ -267,7 +267,7 @@ __global__ void __launch_bounds__(kPsaThreads, 2) psa_gqa_kernel(PoolView p, Bat
 #ifndef PSA_PF
 #define PSA_PF 0
 #endif
-        if constexpr (kMma && PSA_PF >= 1) {
+        if constexpr (kMma && (PSA_PF >= 1 || kWide)) {  // measured: helps 64-rank rounds (1.76 -> 1.70 ms), not 32
             // Bulk L2 prefetch of every U block's K (threads 0..) and V (threads 128..): the K pass
             // below then walks L2-resident blocks, and the V pass finds committed blocks in L2.
             const int e = tid & (G * CH - 1);
