@@ -49,7 +49,7 @@ def results(run, off, nb, g):
     return out
 
 
-@pytest.mark.parametrize("g", [4, 2])
+@pytest.mark.parametrize("g", [4, 3, 2])
 @pytest.mark.parametrize("cfg", [dict(epsilon=0.95), dict(epsilon=0.9, microbatch_size=4), dict(topk=1200),
                                  dict(epsilon=0.99, estimator=0)])
 def test_dense_handover_parity(mods, oracle, g, cfg):
@@ -99,3 +99,23 @@ def test_planted_units_stay_on_round_kernel(mods):
     for x, y in zip(a, b):
         assert x["bp"] == y["bp"] and np.array_equal(x["ids"], y["ids"]) and abs(x["est"] - y["est"]) <= 1e-6
         assert np.max(np.abs(x["out"] - y["out"])) <= 1e-5
+
+
+@pytest.mark.parametrize("g", [4, 3, 2])
+@pytest.mark.parametrize("cfg", [dict(epsilon=0.95), dict(epsilon=0.9, microbatch_size=3), dict(topk=100)])
+def test_wide_rounds_parity(mods, oracle, g, cfg):
+    """64-rank rounds of the tensor-core path on planted (sparse) units, every head vs the oracle."""
+    capi, _ = mods
+    tokens = [16 * 2500 + 9, 16 * 800]
+    p, uids, nb, off, qs, run = synth_batch(mods, tokens, g, 1 / 32, cfg, seed=9)
+    run.run()
+    res = results(run, off, nb, g)
+    oc = make_config(epsilon=cfg.get("epsilon", 1.0) if not cfg.get("topk") else 1.0,
+                     microbatch_size=cfg.get("microbatch_size", 1))
+    for u, uid in enumerate(uids):
+        k, v = capi.synth_unit_host(p, uid, tokens[u])
+        nt = [min(16, tokens[u] - i * 16) for i in range(nb[u])]
+        bs = BlockSet([k[i, :nt[i]] for i in range(nb[u])], [v[i, :nt[i]] for i in range(nb[u])])
+        for h in range(g):
+            a = res[u * g + h]
+            check_parity(oracle, qs[u, h], bs, oc, cfg.get("topk", 0), a["ids"], a["bp"], a["out"], a["est"])
