@@ -60,7 +60,7 @@ struct GqaSmem {
     int32_t hkey[kHash];
     int32_t hfirst[kHash];
     int16_t hval[kHash];
-    int wcnt[kPsaWarps];
+    alignas(16) int wcnt[kPsaWarps];  // (16-byte aligned: the prefix loop reads it with 128-bit loads)
     int64_t tr0[G], cb[G];
     uint64_t last[G];
     double est[G], acc[G], mn[G], ssum[G];  // acc: log-sum-exp (oracle masses) or running max M (fast decide)
