@@ -340,7 +340,14 @@ __global__ void __launch_bounds__(kScoreWarps * 32, 2) score_kernel_tma(PoolView
         const int cnt = (int)((n - p0) < kRecs ? (n - p0) : kRecs);
         if (lane == 0) mbar_arrive_expect_tx(&wbar[stage], (uint32_t)(cnt * MB));
         __syncwarp();
-        if (lane < cnt) tma_load_1d(wbuf + stage * STAGE + lane * MB, p.meta + (int64_t)slot * MB, MB, &wbar[stage], pol);
+        // records in consecutive slots (the usual page-table layout) move as ONE bulk copy
+        const int32_t slot0 = __shfl_sync(PSA_FULL, slot, 0);
+        if (__all_sync(PSA_FULL, lane >= cnt || slot == slot0 + lane)) {
+            if (lane == 0)
+                tma_load_1d(wbuf + stage * STAGE, p.meta + (int64_t)slot0 * MB, (uint32_t)(cnt * MB), &wbar[stage], pol);
+        } else if (lane < cnt) {
+            tma_load_1d(wbuf + stage * STAGE + lane * MB, p.meta + (int64_t)slot * MB, MB, &wbar[stage], pol);
+        }
     };
     // prologue: S groups in flight
 #pragma unroll 1
