@@ -377,3 +377,24 @@ def test_graph_replay_identical(mods, planted):
         run.run_graph()
         torch.cuda.synchronize()
         assert torch.equal(run.out, ref[0]) and torch.equal(run.bp, ref[1]) and torch.equal(run.est, ref[2])
+
+
+@pytest.mark.parametrize("T", [8, 12, 16])
+@pytest.mark.parametrize("g", [4, 2])
+@pytest.mark.parametrize("planted", [0.08, 0.0])
+def test_bf16_short_blocks_tensor_core_path(mods, oracle, T, g, planted):
+    """bf16 pools with blocks of fewer than 16 tokens and ragged blocks on the tensor-core GQA path
+    (rows past T clamp to the last row and are masked), through 64-rank rounds and — with
+    isotropic keys — the dense hand-over; every head against the oracle."""
+    rng = np.random.default_rng(int(T * 10 + g + planted * 100))
+    d, n = 128, 900
+    units = [random_blockset(rng, n, d, 1, T, planted_frac=planted, skew=2.5) for _ in range(2)]
+    for u in units:
+        u.keys[:] = torch.tensor(u.keys).bfloat16().float().numpy()
+        u.values[:] = torch.tensor(u.values).bfloat16().float().numpy()
+    qs = [[(rng.standard_normal(d) * 0.5 + 0.5).astype(np.float32) for _ in range(g)] for _ in units]
+    _, run, off = run_units(mods, units, qs, T, kv_dtype=1, epsilon=0.95)
+    for u in range(2):
+        for h in range(g):
+            r = unpack(run, off, u, h, n)
+            check_parity(oracle, qs[u][h], units[u], make_config(epsilon=0.95), 0, r["ids"], r["bp"], r["out"], r["est"])
