@@ -17,18 +17,21 @@ namespace psa {
 // the g q-heads of its GQA group together (psa_attention_multi_head, reference
 // engine.cpp:240-260: every head keeps its OWN ranking and stop point, SPEC D6).
 //
-// Each round, every live head h contributes its next chunk of <= 32 ranks; the
-// chunks are merged into a union U (hash on list position) so a block ranked by
-// several heads is read ONCE:
-//   1. ORDER   per-head lazy tranches (bucket select + bitonic, psa_order.cuh);
+// Each round, every live head h contributes its next chunk of <= CH ranks (64 on the
+// tensor-core path with the dense hand-over, else 32); the chunks are merged into a
+// union U (hash on list position) so a block ranked by several heads is read ONCE:
+//   1. ORDER   the first tranche comes from first_tranche_kernel; later tranches
+//              (32-rank variant only) by bucket select + bitonic (psa_order.cuh);
 //   2. K pass  each block of U: its K rows are loaded once and scored for all g
-//              heads (fp32 q.k*scale, block max / exp-sum / log_as per head);
-//   3. decide  warp h runs head h's coverage scan over its chunk (decide_chunk),
-//              all heads in parallel; committed (block, head) pairs are marked;
+//              heads (fp32 q.k*scale, block max / exp-sum per head);
+//   3. decide  warp h runs head h's coverage scan over its chunk in 32-rank pieces
+//              (decide_chunk_fast, fp64 fallback), all heads in parallel;
+//              committed (block, head) pairs are marked;
 //   4. V pass  each block of U committed by >= 1 head: V rows loaded once,
 //              accumulated into every committing head's online-softmax state.
 // With correlated heads (the usual GQA case) U is ~1 chunk, so K/V bytes and
-// the bf16->fp32 conversions are ~1/g of the per-head kernel's.
+// the bf16->fp32 conversions are ~1/g of the per-head kernel's. A head reaching
+// kDenseHandover ranks hands the unit over to the dense kernels (kernels_dense.cu).
 // =============================================================================
 constexpr int kGTCap = kFirstCap;  // tranche capacity per head
 constexpr int kHash = 512;    // pos -> U index (>= 2 * G * kChunk)
