@@ -251,7 +251,7 @@ int read_meta(const psattn_pool* pool, int64_t slot, float* mean, float* lo, flo
 
 // ---- workspace carving ----
 struct WsLayout {
-    size_t keys, rpos, omass, kmm, dflag, dla, dp, dthr, ft, total;
+    size_t keys, rpos, omass, kmm, dflag, dla, dp, dthr, dpart, ft, total;
 };
 
 static WsLayout ws_layout(const psattn_batch* b) {
@@ -267,7 +267,7 @@ static WsLayout ws_layout(const psattn_batch* b) {
     l.kmm = o;
     o += align_up((size_t)b->n_units * b->group * 16, 256);
     // dense hand-over scratch (GQA shapes with the estimated ranking: d = 128, group 2..4)
-    l.dflag = l.dla = l.dp = l.dthr = 0;
+    l.dflag = l.dla = l.dp = l.dthr = l.dpart = 0;
     if (b->dim == 128 && b->group >= 2 && b->group <= 4 && b->ranking_mode != PSATTN_RANK_ORACLE &&
         !b->audit_coverage && b->max_blocks <= kDenseMaxBlocks) {
         l.dflag = o;
@@ -278,6 +278,8 @@ static WsLayout ws_layout(const psattn_batch* b) {
         o += align_up(hb * 64, 256);
         l.dthr = o;
         o += align_up((size_t)b->n_units * b->group * 8, 256);
+        l.dpart = o;
+        o += align_up((size_t)b->n_units * b->group * ((b->max_blocks + kDenseSlice - 1) / kDenseSlice) * kDensePart * 4, 256);
     }
     // first tranche of every head (GQA shapes): keys | slots | ntok | count
     l.ft = 0;
@@ -353,6 +355,7 @@ BatchView make_view(const psattn_pool* pool, const psattn_batch* b, void* worksp
     v.dense_la = l.dflag ? reinterpret_cast<float*>(ws + l.dla) : nullptr;
     v.dense_p = l.dflag ? reinterpret_cast<float*>(ws + l.dp) : nullptr;
     v.dense_thr = l.dflag ? reinterpret_cast<unsigned long long*>(ws + l.dthr) : nullptr;
+    v.dense_part = l.dflag ? reinterpret_cast<float*>(ws + l.dpart) : nullptr;
     if (l.ft) {
         const size_t hq = (size_t)b->n_units * b->group;
         char* f = ws + l.ft;

@@ -76,6 +76,8 @@ struct BatchView {
     float* dense_la;                // [total*g] fp32 block masses
     float* dense_p;                 // [total*g][16] normalised token weights
     unsigned long long* dense_thr;  // [n_units*g] rank-threshold key of each head's processed set
+    float* dense_part;              // [n_units*g][slices][kDensePart] per-slice V-pass partial states
+    int64_t dense_slice;            // list positions per dense work item (set by launch_dense)
     // first tranche of every head, selected up front by first_tranche_kernel (nullptr: the
     // progressive kernel selects it itself): [n_units*g][kFirstCap] sorted keys, slots, ntok, count
     unsigned long long* ft_keys;
@@ -86,6 +88,8 @@ struct BatchView {
 constexpr int kFirstCap = 512;  // == the GQA kernel's tranche capacity
 constexpr int64_t kDenseMaxBlocks = 16384;  // decide smem: 12 B per rank (196 KB)
 constexpr int64_t kDenseHandover = 384;     // ranks a head consumes on the round kernel before the hand-over
+constexpr int64_t kDenseSlice = 512;        // list positions per dense K / V work item
+constexpr int kDensePart = 132;             // partial state: out[128], max, sum (+ pad)
 
 int dpl_for(int d);
 int tok_for(int T);

@@ -64,8 +64,12 @@ __device__ __forceinline__ void load_qg(const BatchView& b, int u, int lane, uin
     }
 }
 
+// Work items of the K and V passes: (handed-over unit, slice of kDenseSlice list positions), so a
+// few long units still spread over every SM (the V pass merges the slices' partial states).
+__device__ __forceinline__ int dense_slices(const BatchView& b) { return (int)((b.max_n + b.dense_slice - 1) / b.dense_slice); }
+
 template <int G>
-__device__ __forceinline__ void dense_k_unit(const PoolView& p, const BatchView& b, int u) {
+__device__ __forceinline__ void dense_k_unit(const PoolView& p, const BatchView& b, int u, int64_t e_begin, int64_t e_end) {
     constexpr int NT = (G * 4 + 7) / 8;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int gq = lane >> 2, tq = lane & 3;
@@ -74,9 +78,9 @@ __device__ __forceinline__ void dense_k_unit(const PoolView& p, const BatchView&
     const int T = p.T;
     uint32_t qg[8][NT][2];
     load_qg<G>(b, u, lane, qg);
-    for (int64_t e = warp; e < n; e += kDenseWarps) {
+    for (int64_t e = e_begin + warp; e < e_end; e += kDenseWarps) {
         const int64_t ef = e + (int64_t)kDensePf * kDenseWarps;
-        if (lane == 0 && ef < n) {
+        if (lane == 0 && ef < e_end) {
             const int32_t sf = b.slots[off + ef];
             if (kv_resident(p, sf)) prefetch_l2_bulk(kv_block<__nv_bfloat16>(p, sf), (uint32_t)(T * 128 * 2));
         }
@@ -132,7 +136,13 @@ __device__ __forceinline__ void dense_k_unit(const PoolView& p, const BatchView&
 
 template <int G>
 __global__ void __launch_bounds__(kDenseWarps * 32) dense_k_kernel(PoolView p, BatchView b) {
-    for (int item = blockIdx.x; item < *b.dense_count; item += gridDim.x) dense_k_unit<G>(p, b, b.dense_flag[item]);
+    const int S = dense_slices(b);
+    for (int item = blockIdx.x; item < *b.dense_count * S; item += gridDim.x) {
+        const int u = b.dense_flag[item / S];
+        const int64_t n = b.list_off[u + 1] - b.list_off[u];
+        const int64_t e0 = (int64_t)(item % S) * b.dense_slice, e1 = e0 + b.dense_slice < n ? e0 + b.dense_slice : n;
+        if (e0 < n) dense_k_unit<G>(p, b, u, e0, e1);
+    }
 }
 
 // One CTA per (flagged unit, head): the head's keys sorted in shared memory, then warp 0 runs
@@ -275,21 +285,27 @@ __device__ __forceinline__ void dense_decide_head(const BatchView& b, int u, int
 }
 
 template <int G>
-__device__ __forceinline__ void dense_v_unit(const PoolView& p, const BatchView& b, int u, float (&so)[kDenseWarps][G][128],
+__device__ __forceinline__ void dense_v_unit(const PoolView& p, const BatchView& b, int u, int slice, int64_t e_begin,
+                                             int64_t e_end, float (&so)[kDenseWarps][G][128],
                                              float (&som)[kDenseWarps][G], float (&sol)[kDenseWarps][G]);
 
 template <int G>
 __global__ void __launch_bounds__(kDenseWarps * 32) dense_v_kernel(PoolView p, BatchView b) {
     __shared__ float so[kDenseWarps][G][128];
     __shared__ float som[kDenseWarps][G], sol[kDenseWarps][G];
-    for (int item = blockIdx.x; item < *b.dense_count; item += gridDim.x) {
-        dense_v_unit<G>(p, b, b.dense_flag[item], so, som, sol);
+    const int S = dense_slices(b);
+    for (int item = blockIdx.x; item < *b.dense_count * S; item += gridDim.x) {
+        const int u = b.dense_flag[item / S];
+        const int64_t n = b.list_off[u + 1] - b.list_off[u];
+        const int64_t e0 = (int64_t)(item % S) * b.dense_slice, e1 = e0 + b.dense_slice < n ? e0 + b.dense_slice : n;
+        if (e0 < n) dense_v_unit<G>(p, b, u, item % S, e0, e1, so, som, sol);
         __syncthreads();
     }
 }
 
 template <int G>
-__device__ __forceinline__ void dense_v_unit(const PoolView& p, const BatchView& b, int u, float (&so)[kDenseWarps][G][128],
+__device__ __forceinline__ void dense_v_unit(const PoolView& p, const BatchView& b, int u, int slice, int64_t e_begin,
+                                             int64_t e_end, float (&so)[kDenseWarps][G][128],
                                              float (&som)[kDenseWarps][G], float (&sol)[kDenseWarps][G]) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, tid = threadIdx.x;
     const int gq = lane >> 2, tq = lane & 3;
@@ -310,9 +326,9 @@ __device__ __forceinline__ void dense_v_unit(const PoolView& p, const BatchView&
     float Oreg[16], Mreg = -INFINITY, Lreg = 0.0f;
 #pragma unroll
     for (int j = 0; j < 16; ++j) Oreg[j] = 0.0f;
-    for (int64_t e = warp; e < n; e += kDenseWarps) {
+    for (int64_t e = e_begin + warp; e < e_end; e += kDenseWarps) {
         const int64_t ef = e + (int64_t)kDensePf * kDenseWarps;
-        if (lane == 0 && ef < n && mask_of(ef)) {
+        if (lane == 0 && ef < e_end && mask_of(ef)) {
             const int32_t sf = b.slots[off + ef];
             if (kv_resident(p, sf)) prefetch_l2_bulk(kv_block<__nv_bfloat16>(p, sf) + v_off, (uint32_t)(T * 128 * 2));
         }
@@ -379,13 +395,43 @@ __device__ __forceinline__ void dense_v_unit(const PoolView& p, const BatchView&
             sc[w] = sol[w][h] > 0.0f ? expf(som[w][h] - Mt) : 0.0f;
             Lt += sol[w][h] * sc[w];
         }
+        // this slice's partial state of head h: (max, sum, unnormalised output), merged by dense_merge_kernel
         const int64_t qi = (int64_t)u * g + h;
+        float* part = b.dense_part + (qi * dense_slices(b) + slice) * kDensePart;
         for (int i = tid; i < 128; i += kDenseWarps * 32) {
             float o = 0.0f;
 #pragma unroll
             for (int w = 0; w < kDenseWarps; ++w) o += sc[w] > 0.0f ? so[w][h][i] * sc[w] : 0.0f;
-            b.out[qi * 128 + i] = o / Lt;
+            part[i] = o;
         }
+        if (tid == 0) {
+            part[128] = Mt;
+            part[129] = Lt;
+        }
+    }
+}
+
+// Per (handed-over unit, head): the slices' partial states merged (finalize, attention.hpp:104-110).
+__global__ void __launch_bounds__(128) dense_merge_kernel(BatchView b) {
+    const int S = dense_slices(b);
+    for (int item = blockIdx.x; item < *b.dense_count * b.g; item += gridDim.x) {
+        const int u = b.dense_flag[item / b.g], h = item % b.g;
+        const int64_t n = b.list_off[u + 1] - b.list_off[u];
+        const int ns = (int)((n + b.dense_slice - 1) / b.dense_slice);
+        const int64_t qi = (int64_t)u * b.g + h;
+        const float* part = b.dense_part + qi * S * kDensePart;
+        float Mt = -INFINITY;
+        for (int s = 0; s < ns; ++s)
+            if (part[s * kDensePart + 129] > 0.0f) Mt = fmaxf(Mt, part[s * kDensePart + 128]);
+        float Lt = 0.0f, o = 0.0f;
+        for (int s = 0; s < ns; ++s) {
+            const float L = part[s * kDensePart + 129];
+            if (!(L > 0.0f)) continue;
+            const float c = expf(part[s * kDensePart + 128] - Mt);
+            Lt += L * c;
+            o += part[s * kDensePart + threadIdx.x] * c;
+        }
+        b.out[qi * 128 + threadIdx.x] = o / Lt;
     }
 }
 
@@ -406,9 +452,13 @@ static int dense_sms() {
 }
 
 // Persistent grids over the hand-over list (sized to the SMs: no cost when the list is empty).
-void launch_dense(const PoolView& p, const BatchView& b, cudaStream_t st) {
+void launch_dense(const PoolView& p, const BatchView& b_in, cudaStream_t st) {
+    // a whole list per work item when the batch alone fills the GPU, else kDenseSlice positions
+    BatchView b = b_in;
+    b.dense_slice = b.n_units >= 2 * dense_sms() ? (b.max_n > 0 ? b.max_n : 1) : kDenseSlice;
     const int G = b.g <= 2 ? 2 : 4;
-    const int units = b.n_units < 2 * dense_sms() ? b.n_units : 2 * dense_sms();
+    const int64_t slices = (b.max_n + b.dense_slice - 1) / b.dense_slice;
+    const int units = b.n_units * slices < 2 * dense_sms() ? (int)(b.n_units * slices) : 2 * dense_sms();
     if (G == 2) dense_k_kernel<2><<<units, kDenseWarps * 32, 0, st>>>(p, b);
     else dense_k_kernel<4><<<units, kDenseWarps * 32, 0, st>>>(p, b);
     int n2 = 1;
@@ -420,6 +470,7 @@ void launch_dense(const PoolView& p, const BatchView& b, cudaStream_t st) {
     dense_decide_kernel<<<heads, kPsaThreads, smem, st>>>(b);
     if (G == 2) dense_v_kernel<2><<<units, kDenseWarps * 32, 0, st>>>(p, b);
     else dense_v_kernel<4><<<units, kDenseWarps * 32, 0, st>>>(p, b);
+    dense_merge_kernel<<<heads, 128, 0, st>>>(b);
 }
 
 }  // namespace psa
