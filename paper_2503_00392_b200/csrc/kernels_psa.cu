@@ -383,7 +383,7 @@ int launch_psa(const PoolView& p, const BatchView& b, cudaStream_t st) {
         const int n = launch_gqa(p, v, st);
         if (!dense) return n;
         launch_dense(p, v, st);  // units the GQA kernel handed over (others exit at once)
-        return n + 3;
+        return n + 4;
     }
     const int nq = b.n_units * b.g;
     if (p.dtype == 0) {
