@@ -398,3 +398,28 @@ def test_bf16_short_blocks_tensor_core_path(mods, oracle, T, g, planted):
         for h in range(g):
             r = unpack(run, off, u, h, n)
             check_parity(oracle, qs[u][h], units[u], make_config(epsilon=0.95), 0, r["ids"], r["bp"], r["out"], r["est"])
+
+
+@pytest.mark.parametrize("kv_dtype", [0, 1])
+@pytest.mark.parametrize("cfg", [dict(epsilon=0.95), dict(epsilon=1.0), dict(topk=5), dict(epsilon=0.9, microbatch_size=7)])
+def test_tiny_and_ragged_lists(mods, oracle, kv_dtype, cfg):
+    """Edge shapes on every path: lists of 1, 2 and 3 blocks, single-token blocks, top-k larger than
+    the list, microbatch larger than the list, GQA 4 at d = 128 (tensor-core path for bf16)."""
+    rng = np.random.default_rng(17 + kv_dtype)
+    d, T, g = 128, 16, 4
+    units = [random_blockset(rng, n, d, 1, T) for n in (1, 2, 3, 40)]
+    units.append(random_blockset(rng, 5, d, 1, 1))  # single-token blocks
+    if kv_dtype == 1:
+        for u in units:
+            u.keys[:] = torch.tensor(u.keys).bfloat16().float().numpy()
+            u.values[:] = torch.tensor(u.values).bfloat16().float().numpy()
+    qs = [[rng.standard_normal(d).astype(np.float32) for _ in range(g)] for _ in units]
+    _, run, off = run_units(mods, units, qs, T, kv_dtype=kv_dtype, **cfg)
+    oc = make_config(epsilon=cfg.get("epsilon", 1.0) if not cfg.get("topk") else 1.0,
+                     microbatch_size=cfg.get("microbatch_size", 1))
+    for u, bs in enumerate(units):
+        for h in range(g):
+            r = unpack(run, off, u, h, bs.n)
+            check_parity(oracle, qs[u][h], bs, oc, cfg.get("topk", 0), r["ids"], r["bp"], r["out"], r["est"])
+            if cfg.get("topk"):
+                assert r["bp"] == min(cfg["topk"], bs.n)
