@@ -76,6 +76,7 @@ def synth(args):
 # Reference CPU arm: the unmodified reference library (oracle/_ref) on the host cores.
 # ----------------------------------------------------------------------------------------------
 class ReferenceCPU:
+    kind = "reference"
     """psattn::psa_attention_multi_head (reference engine.cpp:240-260) of the unmodified reference
     library on kv-head units of the same workload shape (n = ctx/B blocks, GQA group hq/hkv, same
     synthetic bf16 values upcast to fp32), one TieredBlockStore per host thread (a shared store
@@ -130,13 +131,70 @@ class ReferenceCPU:
         return sum(counts) / el, desc
 
 
+class PortCPU(ReferenceCPU):
+    """Fallback when oracle/_ref (the compiled reference) is absent on the box: the plain-C oracle
+    port (oracle/psa_oracle.c, the reference algorithm restated) on the same units, one head at a
+    time per thread, kind "port"."""
+    kind = "port"
+
+    def __init__(self, args, rank_offset=0):
+        from oracle.pyoracle import BlockSet, COracle, make_config
+        from paper_2503_00392_b200 import capi
+        self.orc = COracle()
+        p = synth(args)
+        self.g = args.hq // args.hkv
+        self.n = args.ctx // args.block
+        self.threads = max(1, min(os.cpu_count() or 1, 64))
+        self.cfg = make_config(epsilon=args.eps, microbatch_size=args.microbatch)
+        self.args = args
+        self.units, self.qs = [None] * self.threads, [None] * self.threads
+
+        def setup(t):
+            uid = 10_000_000 + rank_offset + t
+            k, v = capi.synth_unit_host(p, uid, args.ctx)
+            self.units[t] = BlockSet(list(k), list(v))
+            self.qs[t] = np.array([capi.synth_query(p, uid, h) for h in range(self.g)], np.float32)
+
+        ths = [threading.Thread(target=setup, args=(t,)) for t in range(self.threads)]
+        [th.start() for th in ths]
+        [th.join() for th in ths]
+
+    def sample(self, seconds):
+        counts = [0] * self.threads
+        t0 = time.perf_counter()
+        stop_at = t0 + seconds
+
+        def work(t):
+            while True:
+                for h in range(self.g):
+                    self.orc.psa(self.qs[t][h], self.units[t], self.cfg)
+                counts[t] += self.g
+                if time.perf_counter() >= stop_at:
+                    break
+
+        ths = [threading.Thread(target=work, args=(t,)) for t in range(self.threads)]
+        [th.start() for th in ths]
+        [th.join() for th in ths]
+        el = time.perf_counter() - t0
+        desc = (f"{self.threads} host threads, each on its own kv-head unit of {self.n} blocks "
+                f"(ctx {self.args.ctx}, GQA group {self.g}) via the C oracle port (oracle/_ref absent), eps "
+                f"{self.args.eps}; {sum(counts)} queries in {el:.1f}s")
+        return sum(counts) / el, desc
+
+
+def cpu_reference(args):
+    """The compiled reference when present (kind "reference"), else the C oracle port."""
+    from oracle.pyoracle import ref_available
+    return ReferenceCPU(args) if ref_available() else PortCPU(args)
+
+
 def run_reference(args):
     ws, rank, _ = dist_env()
     if rank != 0:
         return
     K, W = args.steps, args.warmup
     per_step = max(args.cpu_seconds / max(K + W, 1), 0.5)
-    ref = ReferenceCPU(args)
+    ref = cpu_reference(args)
     vals = []
     desc, threads = "", ref.threads
     for i in range(W + K):
@@ -151,7 +209,8 @@ def run_reference(args):
                 config=dict(workload="config2 sample: Llama-3.1-8B shape kv-head units, 128K ctx, "
                                      f"{args.dist} keys", ctx=args.ctx, group=args.hq // args.hkv, eps=args.eps,
                             microbatch=args.microbatch),
-                cpu_baseline=dict(value=v, unit=UNIT, cores=threads, kind="reference", sample=desc, cpu=cpu),
+                cpu_baseline=dict(value=v, unit=UNIT, cores=threads, kind=getattr(ref, "kind", "reference"),
+                                  sample=desc, cpu=cpu),
                 e2e=dict(value=v, unit=UNIT, h2d_bytes_per_step=0, d2h_bytes_per_step=0))
     print(json.dumps(line), flush=True)
 
@@ -387,9 +446,9 @@ def run_ours(args):
     cpu_base = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         try:
-            ref = ReferenceCPU(args)
+            ref = cpu_reference(args)
             v, desc = ref.sample(args.cpu_seconds)
-            cpu_base = dict(value=v, unit=UNIT, cores=ref.threads, kind="reference", sample=desc)
+            cpu_base = dict(value=v, unit=UNIT, cores=ref.threads, kind=getattr(ref, "kind", "reference"), sample=desc)
         except Exception as e:  # noqa: BLE001
             cpu_base = dict(value=None, unit=UNIT, cores=0, kind="reference", sample=f"unavailable: {e}")
 
