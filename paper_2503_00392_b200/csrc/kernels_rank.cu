@@ -31,10 +31,11 @@ static int num_sms() {
 //
 // Arithmetic (fp64, like the reference): products of fp32 operands are exact in
 // fp64; only the summation order differs from the reference's sequential loop
-// (~1e-16 relative). Issue slots are the limiter at the HBM rate (ncu: IPC 2.8,
+// (~1e-16 relative). Issue slots are the limiter at the HBM rate (ncu: IPC 2.7,
 // ALU and FP64 pipes ~45%), so:
-//  * fp32/bf16 -> fp64 conversions are single F2F instructions on the XU pipe,
-//    which nothing else uses (an integer bit-construction costs ~4 ALU slots);
+//  * bf16 lo/hi -> fp64 are bit constructions scaled by 2^-896 (2-3 ALU slots); the
+//    fp32 mean takes one F2F on the otherwise idle XU pipe (all three on the XU pipe
+//    measured slower: its 16 lanes/clk become the limit);
 //  * max(q*lo, q*hi) == q*c + |q|*r with c = (lo+hi)/2, r = (hi-lo)/2 (hi >= lo):
 //    no per-head select, and with the factor 2 folded into the final scale the
 //    shared per-dim work is lo+hi, hi-lo and 2m+(lo+hi) (3 fp64 ops), then
@@ -394,7 +395,14 @@ __global__ void __launch_bounds__(kScoreWarps * 32, 2) score_kernel_tma(PoolView
             }
 #pragma unroll
             for (int jj = 0; jj < DPL; ++jj) {
-                const double m = f32_scaled(mw[jj]);
+#ifndef PSA_MEAN_F2F
+#define PSA_MEAN_F2F 1  // measured: score 3.42 -> 3.22-3.33 ms
+#endif
+                // CuboidMean with PSA_MEAN_F2F: the mean converts with one F2F on the otherwise idle
+                // XU pipe (true value) and the 2^-896 metadata scale is folded into A's DFMA
+                // (exact: a power of two, fp32 denormals stay exact fp64 values)
+                constexpr bool kF2F = PSA_MEAN_F2F && est == 2;
+                const double m = kF2F ? (double)__uint_as_float(mw[jj]) : f32_scaled(mw[jj]);
                 const double lo = f32_scaled(lw[jj]);
                 const double hi = f32_scaled(hw[jj]);
                 double A, B = 0.0;
@@ -402,8 +410,8 @@ __global__ void __launch_bounds__(kScoreWarps * 32, 2) score_kernel_tma(PoolView
                     A = m;
                 } else {
                     const double c2 = lo + hi;
-                    B = hi - lo;                          // 2r, exact
-                    A = est == 2 ? fma(2.0, m, c2) : c2;  // 2(m + c)  |  2c
+                    B = hi - lo;  // 2r, exact
+                    A = est == 2 ? fma(kF2F ? 0x1p-895 : 2.0, m, c2) : c2;  // 2(m + c)  |  2c
                 }
 #pragma unroll
                 for (int h = 0; h < G; ++h) {
