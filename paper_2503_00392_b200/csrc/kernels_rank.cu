@@ -401,17 +401,21 @@ __global__ void __launch_bounds__(kScoreWarps * 32, 2) score_kernel_tma(PoolView
                 // CuboidMean with PSA_MEAN_F2F: the mean converts with one F2F on the otherwise idle
                 // XU pipe (true value) and the 2^-896 metadata scale is folded into A's DFMA
                 // (exact: a power of two, fp32 denormals stay exact fp64 values)
+#ifndef PSA_LO_F2F
+#define PSA_LO_F2F 0
+#endif
                 constexpr bool kF2F = PSA_MEAN_F2F && est == 2;
+                constexpr bool kLoF2F = PSA_LO_F2F && est != 0;  // lo's scale folded into the c2 / B DFMAs
                 const double m = kF2F ? (double)__uint_as_float(mw[jj]) : f32_scaled(mw[jj]);
-                const double lo = f32_scaled(lw[jj]);
+                const double lo = kLoF2F ? (double)__uint_as_float(lw[jj]) : f32_scaled(lw[jj]);
                 const double hi = f32_scaled(hw[jj]);
                 double A, B = 0.0;
                 if (est == 0) {
                     A = m;
                 } else {
-                    const double c2 = lo + hi;
-                    B = hi - lo;  // 2r, exact
-                    A = est == 2 ? fma(kF2F ? 0x1p-895 : 2.0, m, c2) : c2;  // 2(m + c)  |  2c
+                    const double c2 = kLoF2F ? fma(0x1p-896, lo, hi) : lo + hi;  // exact
+                    B = kLoF2F ? fma(-0x1p-896, lo, hi) : hi - lo;             // 2r, exact
+                    A = est == 2 ? fma(kF2F ? 0x1p-895 : 2.0, m, c2) : c2;       // 2(m + c)  |  2c
                 }
 #pragma unroll
                 for (int h = 0; h < G; ++h) {
