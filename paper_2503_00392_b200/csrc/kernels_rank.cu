@@ -7,6 +7,11 @@
 #include "common.cuh"
 #include "kernels.cuh"
 
+// score-kernel conversion variants (build knobs; defaults are the measured best)
+#ifndef PSA_ALL_F2F
+#define PSA_ALL_F2F 0
+#endif
+
 namespace psa {
 
 static int num_sms() {
@@ -317,7 +322,7 @@ __global__ void __launch_bounds__(kScoreWarps * 32, 2) score_kernel_tma(PoolView
 #pragma unroll
             for (int j = 0; j < DPL; ++j) qf[j] = 0.0f;
 #pragma unroll
-        for (int j = 0; j < DPL; ++j) qd[h][j] = (double)qf[j] * 0x1p896;
+        for (int j = 0; j < DPL; ++j) qd[h][j] = (double)qf[j] * (PSA_ALL_F2F && EST == 2 ? 1.0 : 0x1p896);
     }
     constexpr int est = EST;  // estimator as a template parameter: no per-record branches
     // acc = 4 CuboidMean / 2 Upper / Mean: the power-of-two factor folded into the scale (exact)
@@ -404,18 +409,27 @@ __global__ void __launch_bounds__(kScoreWarps * 32, 2) score_kernel_tma(PoolView
 #ifndef PSA_LO_F2F
 #define PSA_LO_F2F 0
 #endif
-                constexpr bool kF2F = PSA_MEAN_F2F && est == 2;
-                constexpr bool kLoF2F = PSA_LO_F2F && est != 0;  // lo's scale folded into the c2 / B DFMAs
+                constexpr bool kAll = PSA_ALL_F2F && est == 2;  // every conversion on the XU pipe, true scale
+                constexpr bool kF2F = PSA_MEAN_F2F && est == 2 && !kAll;
+                constexpr bool kLoF2F = PSA_LO_F2F && est != 0 && !kAll;  // lo's scale folded into c2 / B
+                double A, B = 0.0;
+                if constexpr (kAll) {
+                    const double m = (double)__uint_as_float(mw[jj]);
+                    const double lo = (double)__uint_as_float(lw[jj]);
+                    const double hi = (double)__uint_as_float(hw[jj]);
+                    B = hi - lo;                 // exact (bf16 operands)
+                    A = fma(2.0, m, lo + hi);    // lo + hi exact in fp64
+                } else {
                 const double m = kF2F ? (double)__uint_as_float(mw[jj]) : f32_scaled(mw[jj]);
                 const double lo = kLoF2F ? (double)__uint_as_float(lw[jj]) : f32_scaled(lw[jj]);
                 const double hi = f32_scaled(hw[jj]);
-                double A, B = 0.0;
                 if (est == 0) {
                     A = m;
                 } else {
                     const double c2 = kLoF2F ? fma(0x1p-896, lo, hi) : lo + hi;  // exact
                     B = kLoF2F ? fma(-0x1p-896, lo, hi) : hi - lo;             // 2r, exact
                     A = est == 2 ? fma(kF2F ? 0x1p-895 : 2.0, m, c2) : c2;       // 2(m + c)  |  2c
+                }
                 }
 #pragma unroll
                 for (int h = 0; h < G; ++h) {
