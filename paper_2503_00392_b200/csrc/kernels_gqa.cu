@@ -34,6 +34,13 @@ namespace psa {
 // kDenseHandover ranks hands the unit over to the dense kernels (kernels_dense.cu).
 // =============================================================================
 constexpr int kGTCap = kFirstCap;  // tranche capacity per head
+#ifndef PSA_KUNROLL
+#define PSA_KUNROLL 1
+#endif
+#ifndef PSA_VUNROLL
+#define PSA_VUNROLL 1
+#endif
+constexpr int kKUnroll = PSA_KUNROLL, kVUnroll = PSA_VUNROLL;  // K / V pass loop unroll (build knobs)
 constexpr int kHash = 512;    // pos -> U index (>= 2 * G * kChunk)
 constexpr int kGBins = 1024;  // bucket-select bins per head team
 
@@ -280,7 +287,7 @@ __global__ void __launch_bounds__(kPsaThreads, 2) psa_gqa_kernel(PoolView p, Bat
         }
         GQA_MARK(2);
         // ---- 3. K pass: every U block once, scored for all heads ----
-#pragma unroll 1
+#pragma unroll kKUnroll
         for (int e = warp; e < ucount; e += kPsaWarps) {
             const int32_t slot = s.uslot[e];
             const int nt = s.untok[e];
@@ -429,7 +436,7 @@ __global__ void __launch_bounds__(kPsaThreads, 2) psa_gqa_kernel(PoolView p, Bat
         }
         GQA_MARK(4);
         // ---- 5. V pass: committed U blocks once, into every committing head ----
-#pragma unroll 1
+#pragma unroll kVUnroll
         for (int e = warp; e < ucount; e += kPsaWarps) {
             const uint32_t mask = s.umask[e];
             if (!mask) continue;

@@ -379,15 +379,17 @@ def test_graph_replay_identical(mods, planted):
         assert torch.equal(run.out, ref[0]) and torch.equal(run.bp, ref[1]) and torch.equal(run.est, ref[2])
 
 
+@pytest.mark.parametrize("d", [128, 64])
 @pytest.mark.parametrize("T", [8, 12, 16])
 @pytest.mark.parametrize("g", [4, 2])
 @pytest.mark.parametrize("planted", [0.08, 0.0])
-def test_bf16_short_blocks_tensor_core_path(mods, oracle, T, g, planted):
-    """bf16 pools with blocks of fewer than 16 tokens and ragged blocks on the tensor-core GQA path
-    (rows past T clamp to the last row and are masked), through 64-rank rounds and — with
-    isotropic keys — the dense hand-over; every head against the oracle."""
-    rng = np.random.default_rng(int(T * 10 + g + planted * 100))
-    d, n = 128, 900
+def test_bf16_short_blocks_tensor_core_path(mods, oracle, d, T, g, planted):
+    """bf16 pools with blocks of fewer than 16 tokens and ragged blocks on the GQA paths: d = 128
+    is the tensor-core path (rows past T clamp to the last row and are masked) through 64-rank
+    rounds and — with isotropic keys — the dense hand-over; d = 64 the FFMA GQA path with
+    32-rank rounds and later tranches. Every head against the oracle."""
+    rng = np.random.default_rng(int(T * 10 + g + planted * 100 + d))
+    n = 900
     units = [random_blockset(rng, n, d, 1, T, planted_frac=planted, skew=2.5) for _ in range(2)]
     for u in units:
         u.keys[:] = torch.tensor(u.keys).bfloat16().float().numpy()
