@@ -78,14 +78,24 @@ __device__ __forceinline__ void dense_k_unit(const PoolView& p, const BatchView&
     const int T = p.T;
     uint32_t qg[8][NT][2];
     load_qg<G>(b, u, lane, qg);
-    for (int64_t e = e_begin + warp; e < e_end; e += kDenseWarps) {
-        const int64_t ef = e + (int64_t)kDensePf * kDenseWarps;
-        if (lane == 0 && ef < e_end) {
-            const int32_t sf = b.slots[off + ef];
-            if (kv_resident(p, sf)) prefetch_l2_bulk(kv_block<__nv_bfloat16>(p, sf), (uint32_t)(T * 128 * 2));
+    // the small dependent loads (page-table slot, its ntok, the prefetch target's slot) are
+    // issued one iteration ahead so they never sit on the block's critical path
+    constexpr int64_t kPfd = (int64_t)kDensePf * kDenseWarps;
+    int64_t e = e_begin + warp;
+    int32_t slot_n = e < e_end ? b.slots[off + e] : 0;
+    int nt_n = e < e_end ? p.ntok[slot_n] : 0;
+    int32_t sf_n = e + kPfd < e_end ? b.slots[off + e + kPfd] : -1;
+    for (; e < e_end; e += kDenseWarps) {
+        const int32_t slot = slot_n, sf = sf_n;
+        const int nt = nt_n;
+        const int64_t en = e + kDenseWarps;
+        if (en < e_end) {
+            slot_n = b.slots[off + en];
+            nt_n = p.ntok[slot_n];
         }
-        const int32_t slot = b.slots[off + e];
-        const int nt = p.ntok[slot];
+        sf_n = en + kPfd < e_end ? b.slots[off + en + kPfd] : -1;
+        if (lane == 0 && sf >= 0 && kv_resident(p, sf))
+            prefetch_l2_bulk(kv_block<__nv_bfloat16>(p, sf), (uint32_t)(T * 128 * 2));
         const __nv_bfloat16* kblk = kv_block<__nv_bfloat16>(p, slot);
         const int r0 = gq < T ? gq : T - 1, r1 = (gq + 8) < T ? (gq + 8) : T - 1;
         const uint4* p0 = reinterpret_cast<const uint4*>(kblk + (size_t)r0 * 128 + 32 * tq);
@@ -326,15 +336,24 @@ __device__ __forceinline__ void dense_v_unit(const PoolView& p, const BatchView&
     float Oreg[16], Mreg = -INFINITY, Lreg = 0.0f;
 #pragma unroll
     for (int j = 0; j < 16; ++j) Oreg[j] = 0.0f;
-    for (int64_t e = e_begin + warp; e < e_end; e += kDenseWarps) {
-        const int64_t ef = e + (int64_t)kDensePf * kDenseWarps;
-        if (lane == 0 && ef < e_end && mask_of(ef)) {
-            const int32_t sf = b.slots[off + ef];
-            if (kv_resident(p, sf)) prefetch_l2_bulk(kv_block<__nv_bfloat16>(p, sf) + v_off, (uint32_t)(T * 128 * 2));
+    // membership mask, slot and prefetch target of the NEXT block are loaded one iteration ahead
+    constexpr int64_t kPfd = (int64_t)kDensePf * kDenseWarps;
+    int64_t e = e_begin + warp;
+    uint32_t mask_n = e < e_end ? mask_of(e) : 0u;
+    int32_t slot_n = e < e_end ? b.slots[off + e] : 0;
+    int32_t sf_n = e + kPfd < e_end ? b.slots[off + e + kPfd] : -1;
+    for (; e < e_end; e += kDenseWarps) {
+        const uint32_t mask = mask_n;
+        const int32_t slot = slot_n, sf = sf_n;
+        const int64_t en = e + kDenseWarps;
+        if (en < e_end) {
+            mask_n = mask_of(en);
+            slot_n = b.slots[off + en];
         }
-        const uint32_t mask = mask_of(e);
+        sf_n = en + kPfd < e_end ? b.slots[off + en + kPfd] : -1;
+        if (lane == 0 && sf >= 0 && kv_resident(p, sf))
+            prefetch_l2_bulk(kv_block<__nv_bfloat16>(p, sf) + v_off, (uint32_t)(T * 128 * 2));
         if (!mask) continue;
-        const int32_t slot = b.slots[off + e];
         const __nv_bfloat16* vblk = kv_block<__nv_bfloat16>(p, slot) + v_off;
         uint32_t vw[4][8];
 #pragma unroll
