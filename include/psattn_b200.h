@@ -256,6 +256,19 @@ int psattn_serving_add_request(psattn_serving* s, int64_t request_id, double arr
 /* Runs every added request to completion with method PSATTN_METHOD_* (epsilon for PSA, k for top-k). */
 int psattn_serving_run(psattn_serving* s, int32_t method, double epsilon, int64_t k, psattn_serving_report* out);
 
+/* ---- Per-call scoring and ranking over host metadata records (metadata_api.cu) ----
+ * The reference's criticality_score / rank_by_scores (include/psattn/metadata.hpp:27-36,
+ * src/metadata.cpp:41-96) for callers holding BlockMetadata in host memory; computed on the
+ * device. The progressive path scores and orders pool metadata inside its own kernels. */
+/* scores[i] = criticality_score(q, record i, estimator, scale), bit-identical to the
+ * reference's double. mean/lo/hi: host fp32 [n][d]; estimator 0 Mean, 1 CuboidUpperBound,
+ * 2 CuboidMean. Synchronous. */
+int psattn_criticality_scores(const float* q, int32_t d, const float* mean, const float* lo, const float* hi,
+                              int64_t n, int32_t estimator, double scale, double* scores);
+/* order[r] = index of the r-th block by descending score, ties by ascending block id
+ * (rank_by_scores). Host arrays of n entries. Synchronous. */
+int psattn_rank_by_scores(const double* scores, const int64_t* block_ids, int64_t n, int64_t* order);
+
 /* ---- Oracle / audit tooling (test and report mode; reads every block of every list) ---- */
 
 /* fp64 exact attention over every block of each list, in list order

@@ -260,6 +260,13 @@ class RefDriver:
     def error(self) -> str:
         return self.L.refdrv_last_error().decode()
 
+    def criticality(self, q, mean, lo, hi, estimator=2, scale=None):
+        """The reference's criticality_score (metadata.cpp:60-72), compiled."""
+        q = np.ascontiguousarray(q, np.float32)
+        scale = 1.0 / np.sqrt(q.size) if scale is None else scale
+        arr = [np.ascontiguousarray(a, np.float32) for a in (mean, lo, hi)]
+        return self.L.refdrv_criticality(_p(q), q.size, _p(arr[0]), _p(arr[1]), _p(arr[2]), estimator, scale)
+
     def store(self, capacity=256, n_layers=1, partitioned=0, fifo=0, miss_ms=0.0) -> "RefStore":
         return RefStore(self, capacity, n_layers, partitioned, fifo, miss_ms)
 

@@ -161,6 +161,8 @@ def _load() -> C.CDLL:
     L.psattn_graph_launch.argtypes = [vp, vp]
     L.psattn_graph_destroy.argtypes = [vp]
     L.psattn_exact_attention.argtypes = [vp, C.POINTER(Batch), vp, vp]
+    L.psattn_criticality_scores.argtypes = [vp, i32, vp, vp, vp, i64, i32, dbl, vp]
+    L.psattn_rank_by_scores.argtypes = [vp, vp, i64, vp]
     L.psattn_tradeoff.argtypes = [vp, C.POINTER(Batch), dbl, C.POINTER(TradeoffReport), vp]
     L.psattn_tier_create.argtypes = [C.POINTER(TierDesc), C.POINTER(vp)]
     L.psattn_tier_destroy.argtypes = [vp]
@@ -195,6 +197,7 @@ EXPORTED = [
     "psattn_graph_create", "psattn_graph_launch", "psattn_graph_destroy",
     "psattn_synth_direction", "psattn_synth_query", "psattn_synth_unit_host", "psattn_synth_is_planted",
     "psattn_pool_fill_synthetic", "psattn_exact_attention", "psattn_tradeoff",
+    "psattn_criticality_scores", "psattn_rank_by_scores",
     "psattn_tier_create", "psattn_tier_destroy", "psattn_tier_put_blocks", "psattn_tier_release_request",
     "psattn_tier_run_batch", "psattn_tier_stats", "psattn_tier_resident", "psattn_tier_h2d_bytes", "psattn_tier_pool",
     "psattn_serving_create", "psattn_serving_destroy", "psattn_serving_add_request", "psattn_serving_run",
@@ -302,6 +305,36 @@ class Store:
 
     def run_topk(self, q, ids, k, cfg=None):
         return self._run(lib.psattn_run_topk, q, ids, cfg, k)
+
+
+def criticality_scores(q, mean, lo, hi, estimator=2, scale=None) -> np.ndarray:
+    """criticality_score (reference src/metadata.cpp:60-72) of every record: mean/lo/hi [n, d]."""
+    q = np.ascontiguousarray(q, np.float32)
+    arr = [np.ascontiguousarray(x, np.float32).reshape(-1, q.size) for x in (mean, lo, hi)]
+    n = arr[0].shape[0]
+    scale = 1.0 / np.sqrt(q.size) if scale is None else float(scale)
+    out = np.zeros(n, np.float64)
+    check(lib.psattn_criticality_scores(_p(q), q.size, _p(arr[0]), _p(arr[1]), _p(arr[2]), n, estimator, scale,
+                                        _p(out)))
+    return out
+
+
+def rank_by_scores(scores, block_ids) -> np.ndarray:
+    """rank_by_scores (reference src/metadata.cpp:87-96): descending score, ties by block id."""
+    s = np.ascontiguousarray(scores, np.float64)
+    ids = np.ascontiguousarray(block_ids, np.int64)
+    if s.size != ids.size:
+        raise ValueError("rank_by_scores: scores and block ids differ in length")
+    out = np.zeros(s.size, np.int64)
+    check(lib.psattn_rank_by_scores(_p(s), _p(ids), s.size, _p(out)))
+    return out
+
+
+def rank_blocks(q, mean, lo, hi, block_ids, estimator=2, scale=None) -> np.ndarray:
+    """rank_blocks (reference src/metadata.cpp:74-85)."""
+    if len(block_ids) == 0:
+        raise ValueError("rank_blocks: empty metadata list")
+    return rank_by_scores(criticality_scores(q, mean, lo, hi, estimator, scale), block_ids)
 
 
 def synth_params(seed=1, dim=128, block_tokens=16, skew=8.0, planted_prob=0.0, round_bf16=1) -> SynthParams:

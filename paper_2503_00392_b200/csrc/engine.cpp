@@ -320,4 +320,50 @@ BlockMetadata build_metadata(const KVBlock& block) {
     return m;
 }
 
+namespace {
+// Device scores of every record (metadata_api.cu: psattn_criticality_scores).
+std::vector<double> device_scores(std::span<const float> q, std::span<const BlockMetadata> metas, Estimator est,
+                                  double scale, const char* what) {
+    const std::size_t d = q.size(), n = metas.size();
+    std::vector<float> mean(n * d), lo(n * d), hi(n * d);
+    for (std::size_t i = 0; i < n; ++i) {
+        check_dim(q.size(), metas[i].mean_key.size(), what);
+        check_dim(q.size(), metas[i].lo.size(), what);
+        check_dim(q.size(), metas[i].hi.size(), what);
+        std::copy(metas[i].mean_key.begin(), metas[i].mean_key.end(), mean.begin() + i * d);
+        std::copy(metas[i].lo.begin(), metas[i].lo.end(), lo.begin() + i * d);
+        std::copy(metas[i].hi.begin(), metas[i].hi.end(), hi.begin() + i * d);
+    }
+    std::vector<double> s(n);
+    if (psattn_criticality_scores(q.data(), static_cast<std::int32_t>(d), mean.data(), lo.data(), hi.data(),
+                                  static_cast<std::int64_t>(n), static_cast<std::int32_t>(est), scale,
+                                  s.data()) != PSATTN_OK)
+        throw Error(psa::last_error());
+    return s;
+}
+}  // namespace
+
+double criticality_score(std::span<const float> q, const BlockMetadata& meta, Estimator estimator, double scale) {
+    return device_scores(q, std::span<const BlockMetadata>(&meta, 1), estimator, scale, "criticality_score")[0];
+}
+
+std::vector<std::size_t> rank_by_scores(std::span<const double> scores, std::span<const BlockId> block_ids) {
+    if (scores.size() != block_ids.size()) throw Error("rank_by_scores: scores and block ids differ in length");
+    std::vector<std::int64_t> order(scores.size());
+    if (!scores.empty() &&
+        psattn_rank_by_scores(scores.data(), block_ids.data(), static_cast<std::int64_t>(scores.size()),
+                              order.data()) != PSATTN_OK)
+        throw Error(psa::last_error());
+    return std::vector<std::size_t>(order.begin(), order.end());
+}
+
+std::vector<std::size_t> rank_blocks(std::span<const float> q, std::span<const BlockMetadata> metas,
+                                     Estimator estimator, double scale) {
+    if (metas.empty()) throw Error("rank_blocks: empty metadata list");
+    const std::vector<double> s = device_scores(q, metas, estimator, scale, "criticality_score");
+    std::vector<BlockId> ids(metas.size());
+    for (std::size_t i = 0; i < metas.size(); ++i) ids[i] = metas[i].block_id;
+    return rank_by_scores(s, ids);
+}
+
 }  // namespace psattn

@@ -49,6 +49,53 @@ static StoreOptions opts(std::size_t cap, int layers = 1) {
 }
 
 int main() {
+    // --- metadata.hpp scoring / ranking (reference test_core.cpp:363-434) ---
+    {
+        KVBlock proto;
+        proto.layer_id = 0;
+        proto.n_tokens = 2;
+        proto.dim = 2;
+        proto.keys = {1.0f, 0.0f, 0.0f, 1.0f};
+        proto.values = {0.0f, 0.0f, 0.0f, 0.0f};
+        std::vector<BlockMetadata> metas;
+        for (BlockId id : {7, 3, 5}) {
+            KVBlock b = proto;
+            b.block_id = id;
+            metas.push_back(build_metadata(b));
+        }
+        const std::vector<float> q = {1.0f, 1.0f};
+        const auto order = rank_blocks(q, metas, Estimator::CuboidMean, 1.0);
+        CHECK(order.size() == 3);
+        CHECK(metas[order[0]].block_id == 3 && metas[order[1]].block_id == 5 && metas[order[2]].block_id == 7);
+        bool threw = false;
+        try {
+            (void)rank_blocks(q, std::span<const BlockMetadata>{}, Estimator::Mean, 1.0);
+        } catch (const Error&) {
+            threw = true;
+        }
+        CHECK(threw);
+        const std::vector<double> scores = {1.0, 3.0, 3.0, -2.0, 0.5};
+        const std::vector<BlockId> ids = {10, 9, 4, 2, 3};
+        const auto o2 = rank_by_scores(scores, ids);
+        CHECK(o2.size() == 5 && ids[o2[0]] == 4 && ids[o2[1]] == 9 && ids[o2[2]] == 10 && ids[o2[3]] == 3 &&
+              ids[o2[4]] == 2);
+        // the cuboid upper bound dominates every per-token score of the block
+        std::mt19937_64 rng(707);
+        for (int i = 0; i < 200; ++i) {
+            const int d = 4 + (i % 5) * 7, nt = 1 + i % 24;
+            auto blk = make_block(rng, i, 0, nt, d);
+            const BlockMetadata m = build_metadata(*blk);
+            std::vector<float> qq(static_cast<std::size_t>(d));
+            std::normal_distribution<float> nd;
+            for (auto& x : qq) x = nd(rng);
+            const double bound = criticality_score(qq, m, Estimator::CuboidUpperBound, 0.5);
+            for (int t = 0; t < nt; ++t) {
+                double s = 0.0;
+                for (int k = 0; k < d; ++k) s += (double)qq[k] * (double)blk->keys[(std::size_t)t * d + k];
+                CHECK(s * 0.5 <= bound + std::ldexp(std::max(1.0, std::abs(bound)), -48));
+            }
+        }
+    }
     // --- Fig. 4 walkthrough (reference test_engine.cpp:130-211) with iteration records ---
     {
         const std::vector<double> masses = {400, 330, 250, 55, 40, 30, 20, 14.08, 12, 10, 9, 5.848, 5, 4, 3, 2};
