@@ -37,4 +37,13 @@ char* pool_host_kv(psattn_pool* pool);
 void pool_pack_into(const psattn_pool* pool, int64_t n, const int64_t* blocks, const int32_t* ntok, const float* keys,
                     const float* values);
 
+// ProgressiveRun device state (progressive_api.cu).
+struct RunState;
+int prun_create(const float* q, int d, RunState** out);
+void prun_destroy(RunState* s);
+// Folds n host blocks (in order) into the accumulator; log_as[b] = the block's log mass.
+int prun_consume(RunState* s, float scale, int n, const int32_t* ntok, const float* const* keys,
+                 const float* const* values, float* log_as);
+int prun_result(const RunState* s, float* out);
+
 }  // namespace psa

@@ -295,6 +295,92 @@ ExecutionResult run_pipelined(std::span<const float> q, std::span<const BlockId>
     return run_exec(q, block_ids, cfg, store);
 }
 
+// ---- ProgressiveRun / load_microbatch (reference engine.cpp:92-160) ----
+namespace detail {
+struct RunHandle {
+    psa::RunState* s = nullptr;
+    ~RunHandle() { psa::prun_destroy(s); }
+};
+}  // namespace detail
+
+ProgressiveRun::ProgressiveRun(std::span<const float> q, const RankedPlan& plan, const PSAConfig& cfg)
+    : q_(q), plan_(&plan), cfg_(&cfg), dev_(std::make_shared<detail::RunHandle>()) {
+    if (psa::prun_create(q.data(), static_cast<int>(q.size()), &dev_->s) != PSATTN_OK) throw Error(psa::last_error());
+    estimator_.n_left = plan.ranked_ids.size();
+}
+
+std::size_t ProgressiveRun::next_microbatch_size() const {
+    if (finished()) return 0;
+    const std::size_t remaining = plan_->ranked_ids.size() - cursor_;
+    return std::min(remaining, static_cast<std::size_t>(cfg_->microbatch_size));
+}
+
+double ProgressiveRun::consume(std::span<const std::shared_ptr<const KVBlock>> microbatch, std::uint64_t hits,
+                               std::uint64_t misses) {
+    if (microbatch.empty()) throw Error("progressive run: empty microbatch");
+    if (cursor_ + microbatch.size() > plan_->ranked_ids.size())
+        throw Error("progressive run: more blocks fed than planned");
+    const std::size_t n = microbatch.size();
+    std::vector<std::int32_t> ntok(n);
+    std::vector<const float*> ks(n), vs(n);
+    for (std::size_t i = 0; i < n; ++i) {
+        const KVBlock& b = *microbatch[i];
+        if (b.block_id != plan_->ranked_ids[cursor_ + i]) throw Error("progressive run: block fed out of rank order");
+        if (b.n_tokens <= 0) throw Error("block_partial_attention: empty block");
+        check_dim(q_.size(), static_cast<std::size_t>(b.dim), "block_partial_attention");
+        ntok[i] = b.n_tokens;
+        ks[i] = b.keys.data();
+        vs[i] = b.values.data();
+    }
+    std::vector<float> las(n);
+    if (psa::prun_consume(dev_->s, static_cast<float>(plan_->scale), static_cast<int>(n), ntok.data(), ks.data(),
+                          vs.data(), las.data()) != PSATTN_OK)
+        throw Error(psa::last_error());
+    for (std::size_t i = 0; i < n; ++i) {
+        // oracle ranking: the stop rule uses the oracle masses (reference engine.cpp:116-121)
+        estimator_.observe(plan_->has_oracle() ? plan_->oracle_log_as[cursor_] : static_cast<double>(las[i]));
+        ++cursor_;
+    }
+    last_estimate_ = estimate_coverage(estimator_);
+    iterations_.push_back({n, hits, misses, last_estimate_});
+    if (last_estimate_ > cfg_->epsilon) stop_ = true;
+    return last_estimate_;
+}
+
+PSAResult ProgressiveRun::result() const {
+    if (cursor_ == 0) throw Error("progressive run: no blocks processed");
+    PSAResult res;
+    res.output.resize(q_.size());
+    if (psa::prun_result(dev_->s, res.output.data()) != PSATTN_OK) throw Error(psa::last_error());
+    res.blocks_processed = cursor_;
+    res.total_blocks = plan_->ranked_ids.size();
+    res.estimated_coverage = last_estimate_;
+    res.terminated_early = cursor_ < plan_->ranked_ids.size();
+    res.processed_ids.assign(plan_->ranked_ids.begin(),
+                             plan_->ranked_ids.begin() + static_cast<std::ptrdiff_t>(cursor_));
+    res.iterations = iterations_;
+    if (cfg_->audit_coverage) {
+        if (!plan_->has_oracle()) throw Error("progressive run: audit requested without oracle plan data");
+        double mx = -std::numeric_limits<double>::infinity(), s = 0.0;
+        for (std::size_t i = 0; i < cursor_; ++i) mx = std::max(mx, plan_->oracle_log_as[i]);
+        for (std::size_t i = 0; i < cursor_; ++i) s += std::exp(plan_->oracle_log_as[i] - mx);
+        res.true_coverage = std::exp(mx + std::log(s) - plan_->total_log_as);
+    }
+    return res;
+}
+
+LoadedBatch load_microbatch(TieredBlockStore& store, const RankedPlan& plan, std::size_t cursor,
+                            std::size_t count) {
+    LoadedBatch out;
+    out.blocks.reserve(count);
+    const CacheStats before = store.stats();
+    for (std::size_t i = 0; i < count; ++i) out.blocks.push_back(store.load_block(plan.ranked_ids[cursor + i]));
+    const CacheStats after = store.stats();
+    out.hits = after.hits - before.hits;
+    out.misses = after.misses - before.misses;
+    return out;
+}
+
 // ---- metadata.hpp ----
 BlockMetadata build_metadata(const KVBlock& block) {
     if (block.n_tokens <= 0) throw Error("build_metadata: empty block");

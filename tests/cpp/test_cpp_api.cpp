@@ -142,6 +142,55 @@ int main() {
         CHECK(plan.has_oracle() && plan.oracle_log_as.size() == 16);
         for (std::size_t i = 1; i < 16; ++i) CHECK(plan.oracle_log_as[i - 1] >= plan.oracle_log_as[i]);
     }
+    // --- caller-driven ProgressiveRun + load_microbatch (reference engine.cpp:162-171's loop)
+    //     reproduces psa_attention: same stop point, ids, iteration records, output ---
+    {
+        std::mt19937_64 rng(9090);
+        const int d = 32;
+        TieredBlockStore sa(opts(64)), sb(opts(64));
+        std::vector<BlockId> ids;
+        for (int i = 0; i < 40; ++i) {
+            auto blk = make_block(rng, 100 + i, 0, 1 + i % 16, d);
+            sa.put_block(blk);
+            sb.put_block(blk);
+            ids.push_back(100 + i);
+        }
+        std::normal_distribution<float> nd;
+        for (int rep = 0; rep < 2; ++rep) {
+            HeadVector q(d);
+            for (auto& x : q) x = 2.0f * nd(rng);
+            PSAConfig cfg;
+            cfg.epsilon = 0.9;
+            cfg.microbatch_size = 3;
+            cfg.audit_coverage = rep == 1;
+            if (rep == 1) cfg.ranking_mode = RankingMode::Oracle;
+            const PSAResult want = psa_attention(q, ids, cfg, sa);
+            const RankedPlan plan = plan_blocks(q, ids, cfg, sb);
+            ProgressiveRun run(q, plan, cfg);
+            while (!run.finished()) {
+                LoadedBatch lb = load_microbatch(sb, plan, run.cursor(), run.next_microbatch_size());
+                run.consume(lb.blocks, lb.hits, lb.misses);
+            }
+            const PSAResult got = run.result();
+            CHECK(got.blocks_processed == want.blocks_processed && got.processed_ids == want.processed_ids);
+            CHECK(got.terminated_early == want.terminated_early && got.iterations.size() == want.iterations.size());
+            CHECK(std::fabs(got.estimated_coverage - want.estimated_coverage) < 1e-6);
+            for (int k = 0; k < d; ++k) CHECK(std::fabs(got.output[k] - want.output[k]) < 1e-4f);
+            if (rep == 1) CHECK(got.true_coverage && std::fabs(*got.true_coverage - *want.true_coverage) < 1e-9);
+        }
+        const PSAConfig dcfg;  // (ProgressiveRun keeps references to q, plan and cfg, like the reference)
+        const HeadVector q1(d, 1.0f);
+        const RankedPlan plan = plan_blocks(q1, ids, dcfg, sb);
+        ProgressiveRun run(q1, plan, dcfg);
+        bool threw = false;
+        try {
+            std::vector<std::shared_ptr<const KVBlock>> wrong = {sb.peek_block(plan.ranked_ids[1])};
+            run.consume(wrong, 0, 0);
+        } catch (const Error&) {
+            threw = true;
+        }
+        CHECK(threw);
+    }
     // --- batched == solo (test_engine.cpp:280-327) incl. lockstep round accounting ---
     {
         std::mt19937_64 rng(4242);
