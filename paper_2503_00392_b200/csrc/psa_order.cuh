@@ -55,11 +55,20 @@ __device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long x)
 }
 
 // All-ascending bitonic network on a[0, n) in shared memory (indices >= n act as +inf).
+// Steps whose partner distance is >= 32 exchange through shared memory (one team barrier
+// each); the remaining steps of every stage (distance < 32: the partner sits in the same
+// aligned 32-element group) run in registers, one warp per group, partners by shuffle —
+// one barrier per stage instead of one per step.
+#ifndef PSA_BITONIC_WARP
+#define PSA_BITONIC_WARP 1
+#endif
 __device__ __forceinline__ void bitonic_smem(uint64_t* a, int n, const Team& tm) {
     int n2 = 1;
     while (n2 < n) n2 <<= 1;
+    const int lane = threadIdx.x & 31, wt = tm.tid >> 5, nw = tm.size >> 5;
     for (int k = 2; k <= n2; k <<= 1) {
-        for (int j = k >> 1; j > 0; j >>= 1) {
+        int j = k >> 1;
+        for (; j > 0 && (!PSA_BITONIC_WARP || j >= 32); j >>= 1) {
             for (int i = tm.tid; i < (n2 >> 1); i += tm.size) {
                 const int lo = ((i & ~(j - 1)) << 1) | (i & (j - 1));  // j is a power of two
                 const int hi = (j == (k >> 1)) ? (lo ^ (k - 1)) : (lo + j);
@@ -73,6 +82,19 @@ __device__ __forceinline__ void bitonic_smem(uint64_t* a, int n, const Team& tm)
             }
             team_sync(tm);
         }
+        if (j == 0) continue;
+        for (int g = wt; g * 32 < n2; g += nw) {
+            const int idx = g * 32 + lane;
+            unsigned long long x = idx < n ? a[idx] : ~0ull;
+            for (int jj = j; jj > 0; jj >>= 1) {
+                // the stage's first step pairs idx with idx ^ (k - 1), later ones with idx ^ jj;
+                // either way the lower index of the pair has bit jj clear and keeps the minimum
+                const unsigned long long y = __shfl_xor_sync(PSA_FULL, x, jj == (k >> 1) ? k - 1 : jj);
+                x = ((lane & jj) == 0) == (x < y) ? x : y;
+            }
+            if (idx < n) a[idx] = x;
+        }
+        team_sync(tm);
     }
 }
 
