@@ -60,14 +60,72 @@ __device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long x)
 // aligned 32-element group) run in registers, one warp per group, partners by shuffle —
 // one barrier per stage instead of one per step.
 #ifndef PSA_BITONIC_WARP
-#define PSA_BITONIC_WARP 1
+#define PSA_BITONIC_WARP 2  // 1: warp-shuffle steps; 2: + shared-memory steps grouped three at a time
 #endif
+// S consecutive shared-memory steps of one stage at once (partner masks m[0..S-1], the first
+// possibly the stage's reversal mask k-1, the rest single bits): each thread owns groups of 2^S
+// elements closed under the S partner maps, loads them once, runs the S compare-exchange
+// layers in registers and stores them once — one barrier per S steps.
+template <int S>
+__device__ __forceinline__ void bitonic_group_steps(uint64_t* a, int n, int n2, const int (&m)[3], const int (&hb)[3],
+                                                    const Team& tm) {
+    for (int i = tm.tid; i < (n2 >> S); i += tm.size) {
+        // base: i with zero bits inserted at the masks' top-bit positions (lowest first, so a
+        // later insertion never moves an earlier one)
+        int bse = i;
+#pragma unroll
+        for (int q = S - 1; q >= 0; --q) {
+            const int lowm = hb[q] - 1;
+            bse = ((bse & ~lowm) << 1) | (bse & lowm);
+        }
+        int idx[1 << S];
+        unsigned long long v[1 << S];
+#pragma unroll
+        for (int t = 0; t < (1 << S); ++t) {
+            int x = bse;
+#pragma unroll
+            for (int q = 0; q < S; ++q)
+                if (t & (1 << q)) x ^= m[q];
+            idx[t] = x;
+            v[t] = x < n ? a[x] : ~0ull;
+        }
+#pragma unroll
+        for (int q = 0; q < S; ++q)
+#pragma unroll
+            for (int t = 0; t < (1 << S); ++t)
+                if (!(t & (1 << q))) {
+                    const int u = t | (1 << q);
+                    const bool tlow = (idx[t] & hb[q]) == 0;  // the lower index keeps the minimum
+                    const unsigned long long x = v[t], y = v[u];
+                    const unsigned long long mn = x < y ? x : y, mx = x < y ? y : x;
+                    v[t] = tlow ? mn : mx;
+                    v[u] = tlow ? mx : mn;
+                }
+#pragma unroll
+        for (int t = 0; t < (1 << S); ++t)
+            if (idx[t] < n) a[idx[t]] = v[t];
+    }
+}
+
 __device__ __forceinline__ void bitonic_smem(uint64_t* a, int n, const Team& tm) {
     int n2 = 1;
     while (n2 < n) n2 <<= 1;
     const int lane = threadIdx.x & 31, wt = tm.tid >> 5, nw = tm.size >> 5;
     for (int k = 2; k <= n2; k <<= 1) {
         int j = k >> 1;
+        if (PSA_BITONIC_WARP >= 2) {
+            while (j >= 32) {
+                int m[3] = {0, 0, 0}, hb[3] = {1, 1, 1}, s = 0;
+                for (; s < 3 && j >= 32; ++s, j >>= 1) {
+                    m[s] = (j == (k >> 1)) ? k - 1 : j;
+                    hb[s] = j;
+                }
+                if (s == 3) bitonic_group_steps<3>(a, n, n2, m, hb, tm);
+                else if (s == 2) bitonic_group_steps<2>(a, n, n2, m, hb, tm);
+                else bitonic_group_steps<1>(a, n, n2, m, hb, tm);
+                team_sync(tm);
+            }
+        }
         for (; j > 0 && (!PSA_BITONIC_WARP || j >= 32); j >>= 1) {
             for (int i = tm.tid; i < (n2 >> 1); i += tm.size) {
                 const int lo = ((i & ~(j - 1)) << 1) | (i & (j - 1));  // j is a power of two
