@@ -1,6 +1,6 @@
 """Small end-to-end launches of every kernel family for compute-sanitizer (memcheck / racecheck /
 synccheck): score (TMA), first tranche, GQA round kernel, dense hand-over, per-head kernel, metadata
-build, append, tier install, tradeoff/exact. Sizes are tiny: the tools replay every access."""
+build, append, tier install, tradeoff/exact, per-call scoring/ranking. Sizes are tiny: the tools replay every access."""
 import os
 import sys
 
@@ -56,5 +56,10 @@ tr = batch.BatchRun(tier, torch.randn(2, g, d, device=dev), torch.tensor(np.conc
                     off, 100, batch.BatchConfig(epsilon=0.9))
 tr.run()
 tr.run()
+torch.cuda.synchronize()
+# per-call scoring / ranking over host records (metadata_api.cu)
+mk = rng.standard_normal((50, T, 40)).astype(np.float32)
+sc = capi.criticality_scores(rng.standard_normal(40).astype(np.float32), mk.mean(1), mk.min(1), mk.max(1), 2)
+capi.rank_by_scores(np.round(sc, 1), np.arange(50))
 torch.cuda.synchronize()
 print("sanitize driver ok")
