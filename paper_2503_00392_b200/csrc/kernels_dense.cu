@@ -159,7 +159,11 @@ __global__ void __launch_bounds__(kDenseWarps * 32) dense_k_kernel(PoolView p, B
 // the stop rule over the masses in rank order.
 __device__ __forceinline__ void dense_decide_head(const BatchView& b, int u, int h, uint64_t* ks);
 
-__global__ void __launch_bounds__(kPsaThreads) dense_decide_kernel(BatchView b) {
+#ifndef PSA_DECIDE_THREADS
+#define PSA_DECIDE_THREADS 256
+#endif
+constexpr int kDecideThreads = PSA_DECIDE_THREADS;
+__global__ void __launch_bounds__(kDecideThreads) dense_decide_kernel(BatchView b) {
     extern __shared__ __align__(16) unsigned char dsm[];
     uint64_t* ks = reinterpret_cast<uint64_t*>(dsm);
     for (int item = blockIdx.x; item < *b.dense_count * b.g; item += gridDim.x) {
@@ -224,11 +228,11 @@ __device__ __forceinline__ void dense_decide_head(const BatchView& b, int u, int
     // prefix evaluating est = S / (S + n_left * exp(min - M)) at every microbatch boundary (the
     // reference's 1 / (1 + n_left * exp(min - acc)), engine.cpp:48-55); (4) the first rank whose
     // boundary has est > eps (or reaches the limit) over the block is the stop point.
-    __shared__ float tM[kPsaThreads], tmn[kPsaThreads];
-    __shared__ double tS[kPsaThreads];
+    __shared__ float tM[kDecideThreads], tmn[kDecideThreads];
+    __shared__ double tS[kDecideThreads];
     __shared__ unsigned long long first_stop;
     const int tid = threadIdx.x;
-    const int64_t seg = (limit + kPsaThreads - 1) / kPsaThreads;
+    const int64_t seg = (limit + kDecideThreads - 1) / kDecideThreads;
     const int64_t r0 = (int64_t)tid * seg, r1 = r0 + seg < limit ? r0 + seg : limit;
     auto absorb = [](float x, float& M, double& S, float& mn) {
         if (x > M) {
@@ -486,7 +490,7 @@ void launch_dense(const PoolView& p, const BatchView& b_in, cudaStream_t st) {
     const int per_sm = smem <= 70 * 1024 ? 3 : (smem <= 110 * 1024 ? 2 : 1);
     const int heads = b.n_units * b.g < per_sm * dense_sms() ? b.n_units * b.g : per_sm * dense_sms();
     cudaFuncSetAttribute(dense_decide_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    dense_decide_kernel<<<heads, kPsaThreads, smem, st>>>(b);
+    dense_decide_kernel<<<heads, kDecideThreads, smem, st>>>(b);
     if (G == 2) dense_v_kernel<2><<<units, kDenseWarps * 32, 0, st>>>(p, b);
     else dense_v_kernel<4><<<units, kDenseWarps * 32, 0, st>>>(p, b);
     dense_merge_kernel<<<heads, 128, 0, st>>>(b);
