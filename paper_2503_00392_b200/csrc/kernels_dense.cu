@@ -172,6 +172,110 @@ __global__ void __launch_bounds__(kDecideThreads) dense_decide_kernel(BatchView 
     }
 }
 
+// Bucket sort of a head's keys in shared memory (n <= kBucketPerThread * blockDim.x): keys are
+// binned linearly in their decoded score between the head's min and max (monotone in the key,
+// so bins are ordered), scattered by a block-wide counting pass and each bin is finished by an
+// insertion sort. Returns false, leaving ks untouched, when a bin holds more than kBucketMax keys
+// (the caller then runs the bitonic network). Uses `hist` (nbins u32, nbins a power of two).
+#ifndef PSA_DECIDE_BUCKET
+#define PSA_DECIDE_BUCKET 1
+#endif
+constexpr int kBucketPerThread = 32;
+constexpr unsigned kBucketMax = 64;
+__device__ __forceinline__ double key_score(uint64_t k, uint64_t pmask) {
+    const uint64_t asc = ~k | pmask;  // make_key_masked's order-preserving image, position bits set
+    const uint64_t u = (asc >> 63) ? (asc & 0x7FFFFFFFFFFFFFFFull) : ~asc;
+    return __longlong_as_double((long long)u);
+}
+__device__ bool bucket_sort_smem(uint64_t* ks, int n, uint64_t pmask, uint32_t* hist, int nbins) {
+    __shared__ unsigned long long s_min, s_max;
+    __shared__ unsigned s_big, wsum[32];
+    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
+    uint64_t r[kBucketPerThread];
+    unsigned long long lmin = ~0ull, lmax = 0;
+#pragma unroll
+    for (int k = 0; k < kBucketPerThread; ++k) {
+        const int i = tid + k * nt;
+        r[k] = i < n ? ks[i] : ~0ull;
+        if (i < n) {
+            lmin = r[k] < lmin ? r[k] : lmin;
+            lmax = r[k] > lmax ? r[k] : lmax;
+        }
+    }
+    if (tid == 0) {
+        s_min = ~0ull;
+        s_max = 0;
+        s_big = 0;
+    }
+    for (int i = tid; i < nbins; i += nt) hist[i] = 0;
+    __syncthreads();
+    lmin = warp_min_u64(lmin);
+    lmax = warp_max_u64(lmax);
+    if (lane == 0) {
+        atomicMin(&s_min, lmin);
+        atomicMax(&s_max, lmax);
+    }
+    __syncthreads();
+    const double smax = key_score(s_min, pmask), smin = key_score(s_max, pmask);  // smallest key = top score
+    const double range = smax - smin;
+    if (!(range < 1e300)) return false;  // inf / nan scores: leave it to the bitonic network (uniform)
+    const double inv = range > 0.0 ? (double)(nbins - 1) / range : 0.0;
+    auto bin_of = [&](uint64_t k) {
+        const int bb = (int)((smax - key_score(k, pmask)) * inv);
+        return bb < 0 ? 0 : (bb >= nbins ? nbins - 1 : bb);
+    };
+#pragma unroll
+    for (int k = 0; k < kBucketPerThread; ++k)
+        if (tid + k * nt < n) atomicAdd(&hist[bin_of(r[k])], 1u);
+    __syncthreads();
+    // exclusive scan of the bin counts: thread t owns bins [t*per, (t+1)*per)
+    const int per = (nbins + nt - 1) / nt;
+    const int b0 = tid * per, b1 = b0 + per < nbins ? b0 + per : nbins;
+    unsigned loc = 0, mx = 0;
+    for (int j = b0; j < b1; ++j) {
+        const unsigned c = hist[j];
+        loc += c;
+        mx = c > mx ? c : mx;
+    }
+    unsigned inc = loc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned y = __shfl_up_sync(PSA_FULL, inc, o);
+        if (lane >= o) inc += y;
+    }
+    if (lane == 31) wsum[warp] = inc;
+    if (mx > kBucketMax) atomicOr(&s_big, 1u);
+    __syncthreads();
+    if (s_big) return false;
+    unsigned run = inc - loc;
+    for (int w = 0; w < warp; ++w) run += wsum[w];
+    for (int j = b0; j < b1; ++j) {
+        const unsigned c = hist[j];
+        hist[j] = run;
+        run += c;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kBucketPerThread; ++k)
+        if (tid + k * nt < n) ks[atomicAdd(&hist[bin_of(r[k])], 1u)] = r[k];
+    __syncthreads();
+    // hist[j] is now the end of bin j; insertion sort inside each bin
+    for (int j = tid; j < nbins; j += nt) {
+        const int s0 = j ? (int)hist[j - 1] : 0, s1 = (int)hist[j];
+        for (int i = s0 + 1; i < s1; ++i) {
+            const uint64_t x = ks[i];
+            int q = i - 1;
+            while (q >= s0 && ks[q] > x) {
+                ks[q + 1] = ks[q];
+                --q;
+            }
+            ks[q + 1] = x;
+        }
+    }
+    __syncthreads();
+    return true;
+}
+
 __device__ __forceinline__ void dense_decide_head(const BatchView& b, int u, int h, uint64_t* ks) {
     const int qi = u * b.g + h;
     const int64_t off = b.list_off[u], n = b.list_off[u + 1] - off;
@@ -198,7 +302,13 @@ __device__ __forceinline__ void dense_decide_head(const BatchView& b, int u, int
         }
     }
     __syncthreads();
-    bitonic_smem(ks, (int)n, cta_team());
+    {
+        // bins: the rank-order mass array's space (n2 floats) before it is filled
+        const int nbins = n2 < 2048 ? n2 : 2048;
+        if (!(PSA_DECIDE_BUCKET && n <= (int64_t)kBucketPerThread * blockDim.x &&
+              bucket_sort_smem(ks, (int)n, pmask, reinterpret_cast<uint32_t*>(ks + n2), nbins)))
+            bitonic_smem(ks, (int)n, cta_team());
+    }
     // every rank's list position (ranked_pos output) and mass, gathered by the whole CTA so the
     // sequential walk below reads shared memory only
     float* xs = reinterpret_cast<float*>(ks + n2);
