@@ -119,3 +119,43 @@ def test_wide_rounds_parity(mods, oracle, g, cfg):
         for h in range(g):
             a = res[u * g + h]
             check_parity(oracle, qs[u, h], bs, oc, cfg.get("topk", 0), a["ids"], a["bp"], a["out"], a["est"])
+
+
+@pytest.mark.parametrize("cfg", [dict(topk=1200), dict(epsilon=0.999)])
+def test_dense_decide_crowded_bins(mods, oracle, cfg):
+    """Hand-over units whose keys crowd one score bin (1500 identical blocks: equal scores, ties by
+    position): dense_decide_kernel's bucket sort declines and the bitonic fallback orders them. Same
+    processed sets as the round kernel, and the oracle's parity rule."""
+    capi, batch = mods
+    d, T, g, n = 128, 16, 4, 2000
+    rng = np.random.default_rng(21)
+    K = rng.standard_normal((n, T, d)).astype(np.float32)
+    K[:1500] = K[0]
+    V = rng.standard_normal((n, T, d)).astype(np.float32)
+    pool = batch.DevicePool(d, T, capi.PSATTN_KV_BF16, n)
+    pool.put_blocks(np.arange(n), np.full(n, T), K, V)
+    dev = torch.device("cuda")
+    qs = (0.3 * rng.standard_normal((1, g, d))).astype(np.float32)
+    off = np.array([0, n], np.int64)
+    run = batch.BatchRun(pool, torch.tensor(qs, device=dev), torch.arange(n, dtype=torch.int32, device=dev),
+                         torch.tensor(off, device=dev), n, batch.BatchConfig(**cfg), want_ranked=True)
+    assert capi.lib.psattn_set_dense(0) == 0
+    run.run()
+    dense = results(run, off, [n], g)
+    assert capi.lib.psattn_set_dense(1) == 0
+    try:
+        run.run()
+        rounds = results(run, off, [n], g)
+    finally:
+        capi.lib.psattn_set_dense(0)
+    assert max(r["bp"] for r in dense) > 384
+    # the pool holds bf16 K/V: the oracle sees the same rounded blocks
+    kb = torch.tensor(K).to(torch.bfloat16).float().numpy()
+    vb = torch.tensor(V).to(torch.bfloat16).float().numpy()
+    bs = BlockSet([kb[i] for i in range(n)], [vb[i] for i in range(n)])
+    oc = make_config(epsilon=cfg.get("epsilon", 1.0), microbatch_size=1, estimator=2)
+    for h in range(g):
+        a, b = dense[h], rounds[h]
+        assert a["bp"] == b["bp"] and np.array_equal(a["ids"], b["ids"]) and a["term"] == b["term"]
+        assert np.max(np.abs(a["out"] - b["out"])) <= 1e-4
+        check_parity(oracle, qs[0, h], bs, oc, cfg.get("topk", 0), a["ids"], a["bp"], a["out"], a["est"])
