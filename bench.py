@@ -65,10 +65,10 @@ def dist_env():
     return ws, rank, local
 
 
-def synth(args):
-    from paper_2503_00392_b200 import capi
+def synth_params(args):
+    from workload import synth
     prob = 1.0 / 32.0 if args.dist == "planted" else 0.0
-    return capi.synth_params(seed=args.seed, dim=args.dim, block_tokens=args.block, skew=8.0, planted_prob=prob,
+    return synth.params(seed=args.seed, dim=args.dim, block_tokens=args.block, skew=8.0, planted_prob=prob,
                              round_bf16=1)
 
 
@@ -84,9 +84,9 @@ class ReferenceCPU:
 
     def __init__(self, args, rank_offset=0):
         from oracle.pyoracle import RefDriver, make_config
-        from paper_2503_00392_b200 import capi
+        from workload import synth
         drv = RefDriver()
-        p = synth(args)
+        p = synth_params(args)
         self.g = args.hq // args.hkv
         self.n = args.ctx // args.block
         self.threads = max(1, min(os.cpu_count() or 1, 64))
@@ -97,11 +97,11 @@ class ReferenceCPU:
 
         def setup(t):
             uid = 10_000_000 + rank_offset + t
-            k, v = capi.synth_unit_host(p, uid, args.ctx)
+            k, v = synth.unit_host(p, uid, args.ctx)
             st = drv.store(capacity=0)
             st.put_many(0, k, v)
             self.stores[t] = st
-            self.qs[t] = np.array([capi.synth_query(p, uid, h) for h in range(self.g)], np.float32)
+            self.qs[t] = np.array([synth.query(p, uid, h) for h in range(self.g)], np.float32)
             st.multi_head(self.qs[t], self.ids, self.cfg, want_ids=False)  # warm
 
         ths = [threading.Thread(target=setup, args=(t,)) for t in range(self.threads)]
@@ -139,9 +139,9 @@ class PortCPU(ReferenceCPU):
 
     def __init__(self, args, rank_offset=0):
         from oracle.pyoracle import BlockSet, COracle, make_config
-        from paper_2503_00392_b200 import capi
+        from workload import synth
         self.orc = COracle()
-        p = synth(args)
+        p = synth_params(args)
         self.g = args.hq // args.hkv
         self.n = args.ctx // args.block
         self.threads = max(1, min(os.cpu_count() or 1, 64))
@@ -151,9 +151,9 @@ class PortCPU(ReferenceCPU):
 
         def setup(t):
             uid = 10_000_000 + rank_offset + t
-            k, v = capi.synth_unit_host(p, uid, args.ctx)
+            k, v = synth.unit_host(p, uid, args.ctx)
             self.units[t] = BlockSet(list(k), list(v))
-            self.qs[t] = np.array([capi.synth_query(p, uid, h) for h in range(self.g)], np.float32)
+            self.qs[t] = np.array([synth.query(p, uid, h) for h in range(self.g)], np.float32)
 
         ths = [threading.Thread(target=setup, args=(t,)) for t in range(self.threads)]
         [th.start() for th in ths]
@@ -290,7 +290,8 @@ def run_ours(args):
     capi.check(capi.lib.psattn_set_progressive_kernel(args.psa_kernel))
     capi.check(capi.lib.psattn_set_score_kernel(args.score_kernel))
     capi.check(capi.lib.psattn_set_pipeline(args.pipeline))
-    p = synth(args)
+    from workload import synth
+    p = synth_params(args)
     g = args.hq // args.hkv
     n = args.ctx // args.block
     U = args.requests * args.layers * args.hkv
@@ -301,13 +302,13 @@ def run_ours(args):
     unit_ids = shard.unit_ids(shard.shard_requests(args.requests * ws, ws, rank), args.layers, args.hkv)
     assert unit_ids.size == U
     t0 = time.time()
-    pool.fill_synthetic(p, unit_ids, np.arange(U, dtype=np.int64) * n, np.full(U, args.ctx, np.int64))
+    synth.fill(pool, p, unit_ids, np.arange(U, dtype=np.int64) * n, np.full(U, args.ctx, np.int64))
     torch.cuda.synchronize()
     fill_s = time.time() - t0
     q_host = np.zeros((U, g, args.dim), np.float32)
     for u in range(U):
         for h in range(g):
-            q_host[u, h] = capi.synth_query(p, int(unit_ids[u]), h)
+            q_host[u, h] = synth.query(p, int(unit_ids[u]), h)
     q_dev = torch.tensor(q_host, device=dev)
     slots = torch.arange(U * n, dtype=torch.int32, device=dev)
     off = torch.arange(U + 1, dtype=torch.int64, device=dev) * n

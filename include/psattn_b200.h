@@ -15,10 +15,9 @@
  *                     ordering (rank_by_scores, metadata.cpp:87-96) and the
  *                     progressive early-terminating loop (engine.cpp:92-171,
  *                     211-231, 240-260) for a whole batch, launched on the
- *                     caller's cudaStream_t;
- *   - psattn_synth_*  the seekable synthetic KV/query generator used by the
- *                     benchmark and the parity tests (same values on host and
- *                     device, bit for bit).
+ *                     caller's cudaStream_t.
+ * The synthetic workload generator of the benchmark and the tests is a separate
+ * fixture library (workload/psattn_synth.h), not part of this one.
  *
  * All pointers in psattn_batch are DEVICE pointers unless stated. Streams are
  * passed as void* (a cudaStream_t), NULL = legacy default stream.
@@ -86,6 +85,17 @@ int psattn_pool_append_tokens(psattn_pool* pool, int32_t n, const int32_t* tail_
 /* Copies back metadata of one slot as fp32 (mean, lo, hi: dim floats each). */
 int psattn_pool_read_metadata(psattn_pool* pool, int64_t slot, float* mean, float* lo, float* hi);
 
+/* ---- Multi-head (GQA) progressive attention through the store (C form of the reference's
+ * psattn::psa_attention_multi_head, include/psattn/engine.hpp:160-170, engine.cpp:240-260) ----
+ * q: [n_q_heads][dim] host floats; q-head h reads kv-head list h / (n_q_heads / n_kv_heads);
+ * list k = block_ids[list_off[k] .. list_off[k+1]) (host arrays, n_kv_heads + 1 offsets).
+ * out: [n_q_heads][dim]; out_stats: NULL or n_q_heads entries; out_union: NULL or the number of
+ * distinct blocks fetched by any head (MultiHeadResult::fetched_union). One device launch for
+ * all heads; store accounting and miss latency as the reference's per-head calls. */
+int psattn_run_multi_head(psattn_store* store, const float* q, int32_t n_q_heads, int32_t dim,
+                          const int64_t* block_ids, const int64_t* list_off, int32_t n_kv_heads,
+                          const psattn_config* cfg, float* out, psattn_run_stats* out_stats, int64_t* out_union);
+
 /* ---- Batched progressive attention ---- */
 
 typedef struct {
@@ -116,12 +126,21 @@ typedef struct {
     double* true_coverage;     /* optional [n_units*group]; -1 without audit */
     int32_t* terminated;       /* [n_units*group] */
     /* optional output: rank-ordered list positions per head, at
-       ranked_pos[list_off[u]*group + h*n_u + r]. NULL = kept in workspace. */
+       ranked_pos[list_off[u]*group + h*n_u + r], defined for r < blocks_processed
+       (psattn_rank_batch fills every rank). NULL = kept in workspace. */
     int32_t* ranked_pos;
     /* optional output [total_blocks*group], same indexing: at every microbatch
        boundary rank r that was evaluated, the coverage estimate after rank r. */
     double* iter_est;
 } psattn_batch;
+
+/* Full ranking of every head of the batch (plan_blocks' ranked_ids, reference engine.cpp:57-90;
+ * rank_by_scores order, metadata.cpp:87-96): every n_u rank of every head into ranked_pos (or the
+ * workspace's rank array when NULL), descending score with ties by ascending block id (list
+ * position), exactly; fp64 oracle masses computed into the workspace for Oracle ranking / audit.
+ * No attention outputs are written. psattn_run_batch instead orders only the ranks it consumes:
+ * its ranked_pos / iter_est entries are defined for ranks < blocks_processed. Same workspace size. */
+int psattn_rank_batch(psattn_pool* pool, const psattn_batch* b, void* workspace, void* stream);
 
 /* Workspace bytes psattn_run_batch needs for this batch shape. */
 size_t psattn_batch_workspace_bytes(const psattn_batch* b);
@@ -295,37 +314,6 @@ typedef struct {
 } psattn_tradeoff_report;
 int psattn_tradeoff(psattn_pool* pool, const psattn_batch* b, double target, psattn_tradeoff_report* out,
                     void* stream);
-
-/* ---- Seekable synthetic workload (bench + parity; not on the attention path) ----
- * Values are a pure function of (seed, unit_id, block, token, dim), identical on
- * host and device. Keys: approx-N(0,1) noise, plus skew*direction on planted
- * blocks (pattern of reference workload.cpp:84-122); values: per-block centroid
- * + 0.25*noise. planted_per_block: probability a block is planted (0 = isotropic). */
-typedef struct {
-    uint64_t seed;
-    int32_t dim;
-    int32_t block_tokens;
-    float skew;
-    float planted_prob;
-    int32_t round_bf16;   /* round K/V to bf16 values (what a bf16 pool stores) */
-    int32_t reserved;
-} psattn_synth_params;
-
-/* Unit direction (dim floats) for unit_id. */
-void psattn_synth_direction(const psattn_synth_params* p, int64_t unit_id, float* out);
-/* Query of q-head `head` for unit_id: normalize(dir + 0.1*g_head) * sqrt(dim). */
-void psattn_synth_query(const psattn_synth_params* p, int64_t unit_id, int32_t head, float* out);
-/* Host copy of one unit's blocks [first_block, first_block+n_blocks): keys/values
- * [n_blocks][block_tokens][dim]; tokens past n_tokens_total are zero. */
-void psattn_synth_unit_host(const psattn_synth_params* p, int64_t unit_id, int64_t first_block,
-                            int64_t n_blocks, int64_t n_tokens_total, float* keys, float* values);
-int psattn_synth_is_planted(const psattn_synth_params* p, int64_t unit_id, int64_t block);
-
-/* Device fill: for each unit u (host arrays of n_units entries): blocks
- * [0, ceil(tokens[u]/B)) go to slots slot_off[u] + b; sets ntok and builds metadata. */
-int psattn_pool_fill_synthetic(psattn_pool* pool, const psattn_synth_params* p, int32_t n_units,
-                               const int64_t* unit_ids, const int64_t* slot_off,
-                               const int64_t* tokens, void* stream);
 
 #ifdef __cplusplus
 }

@@ -46,13 +46,6 @@ class DevicePool:
         check(lib.psattn_pool_get_layout(self.h, C.byref(lay)))
         return lay
 
-    def fill_synthetic(self, params: capi.SynthParams, unit_ids, slot_off, tokens, stream=None):
-        u = np.ascontiguousarray(unit_ids, np.int64)
-        s = np.ascontiguousarray(slot_off, np.int64)
-        t = np.ascontiguousarray(tokens, np.int64)
-        check(lib.psattn_pool_fill_synthetic(self.h, C.byref(params), u.size, capi._p(u), capi._p(s), capi._p(t),
-                                             _stream_ptr(stream)))
-
     def put_blocks(self, slots, ntok, keys, values):
         s = np.ascontiguousarray(slots, np.int32)
         n = np.ascontiguousarray(ntok, np.int32)

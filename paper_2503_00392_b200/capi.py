@@ -110,11 +110,6 @@ class ServingReport(C.Structure):
         return d
 
 
-class SynthParams(C.Structure):
-    _fields_ = [("seed", C.c_uint64), ("dim", C.c_int32), ("block_tokens", C.c_int32), ("skew", C.c_float),
-                ("planted_prob", C.c_float), ("round_bf16", C.c_int32), ("reserved", C.c_int32)]
-
-
 def _load() -> C.CDLL:
     if not os.path.exists(LIB_PATH):
         raise ImportError(f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
@@ -133,6 +128,7 @@ def _load() -> C.CDLL:
     L.psattn_config_default.argtypes = [C.POINTER(Config)]
     L.psattn_run_query.argtypes = [vp, vp, i32, vp, sz, C.POINTER(Config), vp, C.POINTER(RunStats)]
     L.psattn_run_topk.argtypes = [vp, vp, i32, vp, sz, sz, C.POINTER(Config), vp, C.POINTER(RunStats)]
+    L.psattn_run_multi_head.argtypes = [vp, vp, i32, i32, vp, vp, i32, C.POINTER(Config), vp, vp, vp]
     L.psattn_pool_create.argtypes = [C.POINTER(PoolDesc), C.POINTER(vp)]
     L.psattn_pool_destroy.argtypes = [vp]
     L.psattn_pool_get_desc.argtypes = [vp, C.POINTER(PoolDesc)]
@@ -144,6 +140,7 @@ def _load() -> C.CDLL:
     L.psattn_batch_workspace_bytes.argtypes = [C.POINTER(Batch)]
     L.psattn_batch_workspace_bytes.restype = sz
     L.psattn_run_batch.argtypes = [vp, C.POINTER(Batch), vp, vp]
+    L.psattn_rank_batch.argtypes = [vp, C.POINTER(Batch), vp, vp]
     L.psattn_batch_union_blocks.argtypes = [C.POINTER(Batch), vp, vp, vp]
     L.psattn_batch_last_launches.argtypes = [C.POINTER(i32)]
     L.psattn_set_progressive_kernel.argtypes = [i32]
@@ -151,11 +148,6 @@ def _load() -> C.CDLL:
     L.psattn_set_pipeline.argtypes = [i32]
     L.psattn_profile_enable.argtypes = [i32]
     L.psattn_profile_read.argtypes = [vp, vp, i32]
-    L.psattn_synth_direction.argtypes = [C.POINTER(SynthParams), i64, vp]
-    L.psattn_synth_query.argtypes = [C.POINTER(SynthParams), i64, i32, vp]
-    L.psattn_synth_unit_host.argtypes = [C.POINTER(SynthParams), i64, i64, i64, i64, vp, vp]
-    L.psattn_synth_is_planted.argtypes = [C.POINTER(SynthParams), i64, i64]
-    L.psattn_pool_fill_synthetic.argtypes = [vp, C.POINTER(SynthParams), i32, vp, vp, vp, vp]
     L.psattn_set_dense.argtypes = [i32]
     L.psattn_graph_create.argtypes = [vp, C.POINTER(Batch), vp, vp, C.POINTER(vp)]
     L.psattn_graph_launch.argtypes = [vp, vp]
@@ -195,8 +187,7 @@ EXPORTED = [
     "psattn_profile_enable", "psattn_profile_read", "psattn_set_progressive_kernel",
     "psattn_set_score_kernel", "psattn_set_pipeline", "psattn_set_dense",
     "psattn_graph_create", "psattn_graph_launch", "psattn_graph_destroy",
-    "psattn_synth_direction", "psattn_synth_query", "psattn_synth_unit_host", "psattn_synth_is_planted",
-    "psattn_pool_fill_synthetic", "psattn_exact_attention", "psattn_tradeoff",
+    "psattn_exact_attention", "psattn_tradeoff", "psattn_rank_batch", "psattn_run_multi_head",
     "psattn_criticality_scores", "psattn_rank_by_scores",
     "psattn_tier_create", "psattn_tier_destroy", "psattn_tier_put_blocks", "psattn_tier_release_request",
     "psattn_tier_run_batch", "psattn_tier_stats", "psattn_tier_resident", "psattn_tier_h2d_bytes", "psattn_tier_pool",
@@ -306,6 +297,28 @@ class Store:
     def run_topk(self, q, ids, k, cfg=None):
         return self._run(lib.psattn_run_topk, q, ids, cfg, k)
 
+    def put_many(self, first_id, keys, values, layer=0, owner=0):
+        """Blocks keys[i] / values[i] ([n, T, d]) as ids first_id + i."""
+        for i in range(keys.shape[0]):
+            check(self.put(first_id + i, keys[i], values[i], layer, owner))
+
+    def run_multi_head(self, qs, kv_ids, cfg=None):
+        """psattn_run_multi_head (reference psa_attention_multi_head): qs [Hq, d], kv_ids: list of
+        Hkv id arrays. Returns (rc, outputs [Hq, d], per-head QueryOut list, fetched-union size)."""
+        qs = np.ascontiguousarray(qs, np.float32)
+        lists = [np.ascontiguousarray(x, np.int64) for x in kv_ids]
+        ids = np.ascontiguousarray(np.concatenate(lists), np.int64)
+        off = np.zeros(len(lists) + 1, np.int64)
+        off[1:] = np.cumsum([x.size for x in lists])
+        out = np.zeros(qs.shape, np.float32)
+        st = (RunStats * qs.shape[0])()
+        un = C.c_int64(0)
+        rc = lib.psattn_run_multi_head(self.h, _p(qs), qs.shape[0], qs.shape[1], _p(ids), _p(off), len(lists),
+                                       C.byref(cfg) if cfg is not None else None, _p(out), st, C.byref(un))
+        res = [QueryOut(out[h], int(st[h].blocks_processed), int(st[h].total_blocks), st[h].estimated_coverage,
+                        st[h].true_coverage, bool(st[h].terminated_early)) for h in range(qs.shape[0])]
+        return rc, out, res, int(un.value)
+
 
 def criticality_scores(q, mean, lo, hi, estimator=2, scale=None) -> np.ndarray:
     """criticality_score (reference src/metadata.cpp:60-72) of every record: mean/lo/hi [n, d]."""
@@ -335,37 +348,6 @@ def rank_blocks(q, mean, lo, hi, block_ids, estimator=2, scale=None) -> np.ndarr
     if len(block_ids) == 0:
         raise ValueError("rank_blocks: empty metadata list")
     return rank_by_scores(criticality_scores(q, mean, lo, hi, estimator, scale), block_ids)
-
-
-def synth_params(seed=1, dim=128, block_tokens=16, skew=8.0, planted_prob=0.0, round_bf16=1) -> SynthParams:
-    return SynthParams(seed, dim, block_tokens, skew, planted_prob, round_bf16, 0)
-
-
-def synth_query(p: SynthParams, unit_id: int, head: int) -> np.ndarray:
-    out = np.zeros(p.dim, np.float32)
-    lib.psattn_synth_query(C.byref(p), unit_id, head, _p(out))
-    return out
-
-
-def synth_direction(p: SynthParams, unit_id: int) -> np.ndarray:
-    out = np.zeros(p.dim, np.float32)
-    lib.psattn_synth_direction(C.byref(p), unit_id, _p(out))
-    return out
-
-
-def synth_unit_host(p: SynthParams, unit_id: int, n_tokens: int, first_block=0, n_blocks=None):
-    """Host copy of a unit's K/V blocks: arrays [n_blocks, block_tokens, dim] (zero past n_tokens)."""
-    T = p.block_tokens
-    nb_total = (n_tokens + T - 1) // T
-    n_blocks = nb_total - first_block if n_blocks is None else n_blocks
-    k = np.zeros((n_blocks, T, p.dim), np.float32)
-    v = np.zeros((n_blocks, T, p.dim), np.float32)
-    lib.psattn_synth_unit_host(C.byref(p), unit_id, first_block, n_blocks, n_tokens, _p(k), _p(v))
-    return k, v
-
-
-def synth_is_planted(p: SynthParams, unit_id: int, block: int) -> bool:
-    return bool(lib.psattn_synth_is_planted(C.byref(p), unit_id, block))
 
 
 class Serving:

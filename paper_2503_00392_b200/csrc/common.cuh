@@ -151,7 +151,7 @@ __device__ __forceinline__ uint64_t make_key_masked(double s, uint32_t pos, uint
     const uint64_t u = (uint64_t)__double_as_longlong(s);
     const uint64_t asc = (u >> 63) ? ~u : (u | 0x8000000000000000ull);
     const uint64_t desc = ~asc;
-    return (desc & ~mask) | (uint64_t)pos;
+    return (desc & ~mask) | ((uint64_t)pos & mask);  // mask == 0: the pure score key (full rankings)
 }
 __device__ __forceinline__ uint64_t make_key(double s, uint32_t pos, int pos_bits) {
     return make_key_masked(s, pos, (pos_bits >= 64) ? ~0ull : ((1ull << pos_bits) - 1ull));

@@ -1,5 +1,5 @@
 // device.cu — the device layer behind psattn_b200.h: HBM block pool, batched
-// launch, workspace carving and the synthetic-workload entry points.
+// launch and workspace carving.
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <string.h>
@@ -14,7 +14,6 @@
 #include "device.h"
 #include "kernels.cuh"
 #include "psattn_b200.h"
-#include "synth.h"
 
 struct psattn_pool {
     psattn_pool_desc desc{};
@@ -110,6 +109,20 @@ int pool_grow(psattn_pool* pool, int64_t n_slots, int32_t T) {
     return PSATTN_OK;
 }
 
+// fp32 <-> bf16 bit patterns on the host (round to nearest even, like __float2bfloat16_rn)
+static uint16_t f32_to_bf16_bits(float x) {
+    uint32_t u;
+    memcpy(&u, &x, 4);
+    if ((u & 0x7fffffffu) > 0x7f800000u) return (uint16_t)((u >> 16) | 0x40u);  // NaN stays NaN
+    u += 0x7FFFu + ((u >> 16) & 1u);
+    return (uint16_t)(u >> 16);
+}
+static float bits_to_f32(uint32_t u) {
+    float x;
+    memcpy(&x, &u, 4);
+    return x;
+}
+
 // Packs fp32 host blocks into the pool's slot image and converts to the pool dtype.
 static void pack_host(const PoolView& v, int64_t n, const int32_t* ntok, const float* keys, const float* values,
                       int64_t row_stride_blocks, std::vector<char>& out) {
@@ -127,8 +140,8 @@ static void pack_host(const PoolView& v, int64_t n, const int32_t* ntok, const f
             uint16_t* dk = reinterpret_cast<uint16_t*>(dst);
             uint16_t* dv = dk + per;
             for (size_t j = 0; j < cnt; ++j) {
-                dk[j] = (uint16_t)(psa_synth::f2u(psa_synth::round_bf16(k[j])) >> 16);
-                dv[j] = (uint16_t)(psa_synth::f2u(psa_synth::round_bf16(vv[j])) >> 16);
+                dk[j] = (uint16_t)(f32_to_bf16_bits(k[j]));
+                dv[j] = (uint16_t)(f32_to_bf16_bits(vv[j]));
             }
         }
     }
@@ -219,8 +232,8 @@ int read_slot(const psattn_pool* pool, int64_t slot, int32_t ntok, float* keys, 
     } else {
         const uint16_t* k = reinterpret_cast<const uint16_t*>(img.data());
         for (size_t j = 0; j < cnt; ++j) {
-            keys[j] = psa_synth::u2f((uint32_t)k[j] << 16);
-            values[j] = psa_synth::u2f((uint32_t)k[per + j] << 16);
+            keys[j] = bits_to_f32((uint32_t)k[j] << 16);
+            values[j] = bits_to_f32((uint32_t)k[per + j] << 16);
         }
     }
     return PSATTN_OK;
@@ -242,8 +255,8 @@ int read_meta(const psattn_pool* pool, int64_t slot, float* mean, float* lo, flo
             uint16_t a, b;
             memcpy(&a, lp + 2 * i, 2);
             memcpy(&b, hp + 2 * i, 2);
-            lo[i] = psa_synth::u2f((uint32_t)a << 16);
-            hi[i] = psa_synth::u2f((uint32_t)b << 16);
+            lo[i] = bits_to_f32((uint32_t)a << 16);
+            hi[i] = bits_to_f32((uint32_t)b << 16);
         }
     }
     return PSATTN_OK;
@@ -504,6 +517,30 @@ int psattn_run_batch(psattn_pool* pool, const psattn_batch* b, void* workspace, 
     return PSATTN_OK;
 }
 
+int psattn_rank_batch(psattn_pool* pool, const psattn_batch* b, void* workspace, void* stream) {
+    int rc = validate_batch(pool, b);
+    if (rc) return rc;
+    if (!workspace) return fail(PSATTN_ERR_INVALID_ARGUMENT, "psattn_rank_batch: null workspace");
+    BatchView v = make_view(pool, b, workspace);
+    v.pos_bits = 0;        // compare full scores; ties fall to the stable sort (input = block-id order)
+    v.kminmax = nullptr;   // no tranche selection follows
+    const cudaStream_t st = (cudaStream_t)stream;
+    if (launch_rank_keys(pool->v, v, st) < 0) return cuda_fail(cudaGetLastError(), "psattn_rank_batch: keys");
+    const size_t hb = (size_t)b->total_blocks * (size_t)b->group;
+    void* tmp = nullptr;
+    cudaError_t e = cudaMallocAsync(&tmp, align_up(hb * 8, 256) + 2 * align_up(hb * 4, 256), st);
+    if (e != cudaSuccess) return cuda_fail(e, "psattn_rank_batch: scratch");
+    char* t = static_cast<char*>(tmp);
+    uint64_t* tk = reinterpret_cast<uint64_t*>(t);
+    int32_t* tv = reinterpret_cast<int32_t*>(t + align_up(hb * 8, 256));
+    int32_t* tv2 = reinterpret_cast<int32_t*>(t + align_up(hb * 8, 256) + align_up(hb * 4, 256));
+    e = launch_seg_sort(v.keys, nullptr, v.rpos, tk, tv, tv2, b->list_off, b->n_units, b->group, st);
+    const cudaError_t e2 = cudaFreeAsync(tmp, st);
+    if (e != cudaSuccess) return cuda_fail(e, "psattn_rank_batch: sort");
+    if (e2 != cudaSuccess) return cuda_fail(e2, "psattn_rank_batch: scratch free");
+    return PSATTN_OK;
+}
+
 int psattn_set_progressive_kernel(int32_t mode) {
     if (mode < 0 || mode > 2) return fail(PSATTN_ERR_INVALID_ARGUMENT, "progressive kernel mode must be 0, 1 or 2");
     set_psa_kernel_choice(mode);
@@ -625,95 +662,6 @@ int psattn_batch_last_launches(int32_t* out_count) {
     if (!out_count) return fail(PSATTN_ERR_INVALID_ARGUMENT, "null");
     *out_count = g_last_launches.load();
     return PSATTN_OK;
-}
-
-// ---- synthetic workload ----
-void psattn_synth_direction(const psattn_synth_params* p, int64_t unit_id, float* out) {
-    psa_synth::direction(p->seed, unit_id, p->dim, out);
-}
-
-void psattn_synth_query(const psattn_synth_params* p, int64_t unit_id, int32_t head, float* out) {
-    const int d = p->dim;
-    std::vector<float> dir(d), g(d);
-    psa_synth::direction(p->seed, unit_id, d, dir.data());
-    // per-head perturbation: a unit vector from its own stream (S_QUERY, unit*64 + head)
-    psa_synth::direction(p->seed ^ 0x51ED270B27F1A3C5ULL, unit_id * 64 + head, d, g.data());
-    std::vector<double> v(d);
-    double ss = 0.0;
-    for (int i = 0; i < d; ++i) {
-        v[i] = (double)dir[i] + 0.1 * (double)g[i];
-        ss += v[i] * v[i];
-    }
-    const double s = std::sqrt((double)d) / std::sqrt(ss);
-    for (int i = 0; i < d; ++i) out[i] = (float)(v[i] * s);
-}
-
-int psattn_synth_is_planted(const psattn_synth_params* p, int64_t unit_id, int64_t block) {
-    return psa_synth::is_planted(p->seed, p->planted_prob, unit_id, block);
-}
-
-void psattn_synth_unit_host(const psattn_synth_params* p, int64_t unit_id, int64_t first_block, int64_t n_blocks,
-                            int64_t n_tokens_total, float* keys, float* values) {
-    const int d = p->dim, T = p->block_tokens;
-    std::vector<float> dir(d);
-    psa_synth::direction(p->seed, unit_id, d, dir.data());
-    for (int64_t bi = 0; bi < n_blocks; ++bi) {
-        const int64_t b = first_block + bi;
-        const int planted = psa_synth::is_planted(p->seed, p->planted_prob, unit_id, b);
-        for (int t = 0; t < T; ++t) {
-            const int64_t tok = b * T + t;
-            for (int i = 0; i < d; ++i) {
-                const size_t idx = ((size_t)bi * T + t) * d + i;
-                float kx = 0.0f, vx = 0.0f;
-                if (tok < n_tokens_total) {
-                    kx = psa_synth::key_at(p->seed, unit_id, tok, i, d, planted, p->skew, dir[i]);
-                    vx = psa_synth::value_at(p->seed, unit_id, b, tok, i, d);
-                    if (p->round_bf16) {
-                        kx = psa_synth::round_bf16(kx);
-                        vx = psa_synth::round_bf16(vx);
-                    }
-                }
-                keys[idx] = kx;
-                values[idx] = vx;
-            }
-        }
-    }
-}
-
-int psattn_pool_fill_synthetic(psattn_pool* pool, const psattn_synth_params* p, int32_t n_units,
-                               const int64_t* unit_ids, const int64_t* slot_off, const int64_t* tokens,
-                               void* stream) {
-    if (!pool || !p || !unit_ids || !slot_off || !tokens)
-        return fail(PSATTN_ERR_INVALID_ARGUMENT, "psattn_pool_fill_synthetic: null argument");
-    if (p->dim != pool->v.d || p->block_tokens != pool->v.T)
-        return fail(PSATTN_ERR_INVALID_ARGUMENT, "psattn_pool_fill_synthetic: params do not match the pool");
-    if (n_units <= 0) return PSATTN_OK;
-    const int T = pool->v.T;
-    int64_t max_blocks = 0, lo = INT64_MAX, hi = 0;
-    for (int u = 0; u < n_units; ++u) {
-        const int64_t nb = (tokens[u] + T - 1) / T;
-        if (slot_off[u] < 0 || slot_off[u] + nb > pool->v.n_slots)
-            return fail(PSATTN_ERR_INVALID_ARGUMENT, "psattn_pool_fill_synthetic: slots out of range");
-        max_blocks = std::max(max_blocks, nb);
-        lo = std::min(lo, slot_off[u]);
-        hi = std::max(hi, slot_off[u] + nb);
-    }
-    cudaStream_t st = (cudaStream_t)stream;
-    int64_t* d_arr = nullptr;
-    float* d_dirs = nullptr;
-    cudaError_t e;
-    if ((e = cudaMalloc(&d_arr, (size_t)n_units * 24)) != cudaSuccess) return cuda_fail(e, "synth alloc");
-    if ((e = cudaMalloc(&d_dirs, (size_t)n_units * pool->v.d * 4)) != cudaSuccess) return cuda_fail(e, "synth alloc");
-    cudaMemcpyAsync(d_arr, unit_ids, (size_t)n_units * 8, cudaMemcpyHostToDevice, st);
-    cudaMemcpyAsync(d_arr + n_units, slot_off, (size_t)n_units * 8, cudaMemcpyHostToDevice, st);
-    cudaMemcpyAsync(d_arr + 2 * n_units, tokens, (size_t)n_units * 8, cudaMemcpyHostToDevice, st);
-    e = launch_synth_fill(pool->v, p->seed, p->skew, p->planted_prob, p->round_bf16, n_units, d_arr, d_arr + n_units,
-                          d_arr + 2 * n_units, max_blocks, d_dirs, st);
-    if (e == cudaSuccess) e = launch_meta_build(pool->v, nullptr, lo, hi, st);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-    cudaFree(d_arr);
-    cudaFree(d_dirs);
-    return e == cudaSuccess ? PSATTN_OK : cuda_fail(e, "synthetic fill");
 }
 
 }  // extern "C"

@@ -143,7 +143,7 @@ RankedPlan plan_blocks(std::span<const float> q, std::span<const BlockId> block_
     qb.queries.push_back(q.data());
     qb.dim = static_cast<std::int32_t>(q.size());
     qb.cfg = cfg;
-    qb.topk = 1;  // stop after the first rank: only the ordering is wanted
+    qb.rank_only = true;  // every rank ordered on the device (psattn_rank_batch), no attention
     detail::DeviceQueryResult r;
     const_cast<TieredBlockStore&>(store).run_device(qb, r);
     RankedPlan plan;
@@ -232,6 +232,7 @@ MultiHeadResult psa_attention_multi_head(std::span<const HeadVector> head_querie
         throw Error("multi-head attention: query head count must be a multiple of kv head count");
     cfg.validate();
     const std::size_t group = head_queries.size() / kv_head_blocks.size();
+    for (const auto& q : head_queries) check_dim(q.size(), head_queries[0].size(), "multi-head attention");
     MultiHeadResult out;
     detail::DeviceQueryResult r;
     if (group <= 8) {

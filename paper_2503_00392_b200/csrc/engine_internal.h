@@ -18,6 +18,7 @@ struct DeviceQueryBatch {
     std::int32_t dim = 0;
     PSAConfig cfg;
     std::size_t topk = 0;  // 0: PSA threshold stop
+    bool rank_only = false;  // plan_blocks: full ranking of every rank (psattn_rank_batch), no attention
 };
 
 struct DeviceQueryResult {
@@ -28,8 +29,8 @@ struct DeviceQueryResult {
     std::vector<double> est;
     std::vector<double> true_cov;
     std::vector<std::int32_t> terminated;
-    std::vector<std::vector<BlockId>> ranked_ids;   // per query, full rank order
-    std::vector<std::vector<double>> oracle_ranked; // per query, fp64 masses in rank order (oracle/audit)
+    std::vector<std::vector<BlockId>> ranked_ids;   // per query: ranks < blocks_processed (all with rank_only)
+    std::vector<std::vector<double>> oracle_ranked; // per query, fp64 masses of those ranks (oracle/audit)
     std::vector<std::vector<double>> iter_est;      // per query, estimate at each rank (boundaries valid)
 };
 

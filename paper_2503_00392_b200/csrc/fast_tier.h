@@ -1,0 +1,172 @@
+// fast_tier.h — fast-tier residency accounting shared by the C/C++ store (store.cpp) and the
+// two-tier HBM/host store (tier.cpp).
+//
+// Observable semantics are the reference TieredBlockStore's (store.hpp:16-120,
+// store.cpp:11-124): slot domains (one Unified domain of `capacity` slots, or
+// floor(capacity / n_layers) slots per layer), write-allocate on put, a hit refreshes recency
+// under LRU (FIFO keeps insertion order), a miss costs the block's fp32 payload in bytes and
+// admits it (evicting the oldest entry of a full domain; the eviction is charged to the
+// victim's layer), release drops entries without counting evictions.
+//
+// Representation: each domain is an intrusive doubly linked recency chain stored in one hash
+// map (id -> {older, newer} neighbour ids), with the newest / oldest ids at the ends — one
+// lookup per access, no per-entry list nodes.
+#pragma once
+
+#include <cstdint>
+#include <optional>
+#include <stdexcept>
+#include <unordered_map>
+#include <vector>
+
+namespace psa {
+
+class RecencyChain {
+public:
+    static constexpr std::int64_t kNone = INT64_MIN;
+
+    explicit RecencyChain(std::size_t capacity = 0) : cap_(capacity) {}
+    std::size_t capacity() const { return cap_; }
+    std::size_t size() const { return links_.size(); }
+    bool contains(std::int64_t id) const { return links_.count(id) != 0; }
+
+    // Moves a present id to the newest end. Returns false when absent.
+    bool refresh(std::int64_t id) {
+        auto it = links_.find(id);
+        if (it == links_.end()) return false;
+        if (newest_ != id) {
+            unlink(it->second);
+            link_newest(id, it->second);
+        }
+        return true;
+    }
+    // Inserts an absent id as newest; returns the evicted oldest id when the chain was full.
+    // A zero-capacity chain holds nothing (the id is not inserted, nothing is evicted).
+    std::optional<std::int64_t> admit(std::int64_t id) {
+        if (cap_ == 0) return std::nullopt;
+        std::optional<std::int64_t> victim;
+        if (links_.size() == cap_) {
+            victim = oldest_;
+            erase(oldest_);
+        }
+        Link& l = links_[id];
+        link_newest(id, l);
+        return victim;
+    }
+    bool erase(std::int64_t id) {
+        auto it = links_.find(id);
+        if (it == links_.end()) return false;
+        unlink(it->second);
+        links_.erase(it);
+        return true;
+    }
+
+private:
+    struct Link {
+        std::int64_t older = kNone, newer = kNone;
+    };
+    void unlink(Link& l) {
+        if (l.older != kNone) links_[l.older].newer = l.newer;
+        else oldest_ = l.newer;
+        if (l.newer != kNone) links_[l.newer].older = l.older;
+        else newest_ = l.older;
+        l.older = l.newer = kNone;
+    }
+    void link_newest(std::int64_t id, Link& l) {
+        l.older = newest_;
+        l.newer = kNone;
+        if (newest_ != kNone) links_[newest_].newer = id;
+        newest_ = id;
+        if (oldest_ == kNone) oldest_ = id;
+    }
+
+    std::size_t cap_;
+    std::unordered_map<std::int64_t, Link> links_;
+    std::int64_t newest_ = kNone, oldest_ = kNone;
+};
+
+struct TierCounters {
+    std::uint64_t hits = 0, misses = 0, evictions = 0, bytes = 0;
+};
+
+// Domains + counters of one store.
+class FastTier {
+public:
+    struct Access {
+        bool hit = false;
+        std::optional<std::int64_t> evicted;  // victim of the admission (misses only)
+    };
+
+    FastTier(std::size_t capacity, std::int32_t n_layers, bool per_layer_domains, bool lru)
+        : per_layer_domains_(per_layer_domains), lru_(lru), layers_(static_cast<std::size_t>(n_layers)) {
+        if (n_layers <= 0) throw std::invalid_argument("fast tier: n_layers must be positive");
+        if (per_layer_domains) domains_.assign(layers_.size(), RecencyChain(capacity / layers_.size()));
+        else domains_.assign(1, RecencyChain(capacity));
+    }
+
+    // put_block's write-allocate (no hit/miss). `layer_of` resolves a victim's layer.
+    template <typename LayerOf>
+    std::optional<std::int64_t> put(std::int64_t id, std::int32_t layer, LayerOf&& layer_of) {
+        auto victim = domain(layer).admit(id);
+        if (victim) charge_eviction(layer_of(*victim));
+        return victim;
+    }
+    // load_block's accounting: hit (LRU refresh) or miss (bytes + admission).
+    template <typename LayerOf>
+    Access access(std::int64_t id, std::int32_t layer, std::uint64_t payload_bytes, LayerOf&& layer_of) {
+        RecencyChain& d = domain(layer);
+        TierCounters& c = layers_.at(static_cast<std::size_t>(layer));
+        Access a;
+        if (lru_ ? d.refresh(id) : d.contains(id)) {
+            a.hit = true;
+            ++c.hits;
+            ++total_.hits;
+            return a;
+        }
+        ++c.misses;
+        ++total_.misses;
+        c.bytes += payload_bytes;
+        total_.bytes += payload_bytes;
+        a.evicted = d.admit(id);
+        if (a.evicted) charge_eviction(layer_of(*a.evicted));
+        return a;
+    }
+    bool release(std::int64_t id, std::int32_t layer) { return domain(layer).erase(id); }
+    bool resident(std::int64_t id, std::int32_t layer) const { return domain(layer).contains(id); }
+
+    std::size_t capacity(std::int32_t layer) const { return domain(layer).capacity(); }
+    std::size_t occupancy() const {
+        std::size_t n = 0;
+        for (const auto& d : domains_) n += d.size();
+        return n;
+    }
+    const TierCounters& total() const { return total_; }
+    const TierCounters& layer(std::int32_t l) const { return layers_.at(static_cast<std::size_t>(l)); }
+    std::int32_t n_layers() const { return static_cast<std::int32_t>(layers_.size()); }
+
+private:
+    RecencyChain& domain(std::int32_t layer) {
+        check(layer);
+        return domains_[per_layer_domains_ ? static_cast<std::size_t>(layer) : 0];
+    }
+    const RecencyChain& domain(std::int32_t layer) const {
+        check(layer);
+        return domains_[per_layer_domains_ ? static_cast<std::size_t>(layer) : 0];
+    }
+    void check(std::int32_t layer) const {
+        if (layer < 0 || static_cast<std::size_t>(layer) >= layers_.size())
+            throw std::out_of_range("fast tier: layer out of range");
+    }
+    void charge_eviction(std::int32_t victim_layer) {
+        ++total_.evictions;
+        if (victim_layer >= 0 && static_cast<std::size_t>(victim_layer) < layers_.size())
+            ++layers_[static_cast<std::size_t>(victim_layer)].evictions;
+    }
+
+    bool per_layer_domains_, lru_;
+    std::vector<RecencyChain> domains_;
+    std::vector<TierCounters> layers_;
+    TierCounters total_;
+};
+
+}  // namespace psa

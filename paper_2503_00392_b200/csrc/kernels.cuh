@@ -102,9 +102,6 @@ cudaError_t launch_install(const PoolView& p, const int64_t* d_blocks, const int
                            cudaStream_t st);
 cudaError_t launch_scatter(const PoolView& p, const void* staged, const int32_t* d_slots, const int32_t* d_ntok,
                            int64_t n, cudaStream_t st);
-cudaError_t launch_synth_fill(const PoolView& p, uint64_t seed, float skew, float prob, int round_bf16,
-                              int32_t n_units, const int64_t* d_unit_ids, const int64_t* d_slot_off,
-                              const int64_t* d_tokens, int64_t max_blocks, float* d_dirs, cudaStream_t st);
 int launch_psa(const PoolView& p, const BatchView& b, cudaStream_t st);  // returns kernels launched
 bool gqa_supported(const PoolView& p, const BatchView& b);
 int launch_gqa(const PoolView& p, const BatchView& b, cudaStream_t st);  // returns kernels launched
@@ -118,5 +115,8 @@ void launch_dense(const PoolView& p, const BatchView& b, cudaStream_t st);
 // Returns the number of kernel launches issued, or -1 on error (cudaGetLastError has it).
 int launch_batch(const PoolView& p, const BatchView& b, cudaStream_t st, cudaEvent_t* marks = nullptr);
 cudaError_t launch_union(const BatchView& b, int64_t* out_union, cudaStream_t st);
+int launch_rank_keys(const PoolView& p, const BatchView& b, cudaStream_t st);  // oracle masses / scores only
+cudaError_t launch_seg_sort(uint64_t* keys, const int32_t* vals_in, int32_t* vals_out, uint64_t* tk, int32_t* tv,
+                            int32_t* tv2, const int64_t* list_off, int n_units, int g, cudaStream_t st);
 
 }  // namespace psa

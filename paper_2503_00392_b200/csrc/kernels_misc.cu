@@ -1,11 +1,10 @@
-// kernels_misc.cu — K1 metadata build + synthetic workload fill (sm_100a).
+// kernels_misc.cu — K1 metadata build, KV append, slot install/scatter (sm_100a).
 #include <cuda_bf16.h>
 #include <float.h>
 #include <math.h>
 
 #include "common.cuh"
 #include "kernels.cuh"
-#include "synth.h"
 
 namespace psa {
 
@@ -161,70 +160,6 @@ cudaError_t launch_scatter(const PoolView& p, const void* staged, const int32_t*
                            int64_t n, cudaStream_t st) {
     if (n <= 0) return cudaSuccess;
     scatter_slots_kernel<<<(unsigned)n, 128, 0, st>>>(p, static_cast<const char*>(staged), d_slots, d_ntok, n);
-    return cudaGetLastError();
-}
-
-// =============================================================================
-// Synthetic fill (fixture). Directions first (one thread per unit, sequential
-// fp64 norm so the host copy is bit-identical), then every K/V element.
-// =============================================================================
-__global__ void synth_dir_kernel(uint64_t seed, int32_t d, int32_t n_units, const int64_t* unit_ids, float* dirs) {
-    const int u = blockIdx.x * blockDim.x + threadIdx.x;
-    if (u >= n_units) return;
-    psa_synth::direction(seed, unit_ids[u], d, dirs + (size_t)u * d);
-}
-
-template <typename KV>
-__global__ void synth_fill_kernel(PoolView p, uint64_t seed, float skew, float prob, int round_bf16,
-                                  const int64_t* unit_ids, const int64_t* slot_off, const int64_t* tokens,
-                                  const float* dirs) {
-    const int u = blockIdx.y;
-    const int64_t ntok_total = tokens[u];
-    const int64_t nb = (ntok_total + p.T - 1) / p.T;
-    const int64_t uid = unit_ids[u];
-    const int d = p.d;
-    const int64_t per_block = (int64_t)p.T * d;
-    for (int64_t b = blockIdx.x; b < nb; b += gridDim.x) {
-        const int64_t slot = slot_off[u] + b;
-        const int planted = psa_synth::is_planted(seed, prob, uid, b);
-        KV* kp = reinterpret_cast<KV*>(p.kv + slot * p.slot_bytes);
-        KV* vp = kp + per_block;
-        for (int64_t e = threadIdx.x; e < per_block; e += blockDim.x) {
-            const int64_t t = e / d;
-            const int i = (int)(e - t * d);
-            const int64_t tok = b * p.T + t;
-            float kx = 0.0f, vx = 0.0f;
-            if (tok < ntok_total) {
-                kx = psa_synth::key_at(seed, uid, tok, i, d, planted, skew, dirs[(size_t)u * d + i]);
-                vx = psa_synth::value_at(seed, uid, b, tok, i, d);
-                if (round_bf16) {
-                    kx = psa_synth::round_bf16(kx);
-                    vx = psa_synth::round_bf16(vx);
-                }
-            }
-            kp[e] = KVT<KV>::from_f(kx);
-            vp[e] = KVT<KV>::from_f(vx);
-        }
-        if (threadIdx.x == 0) {
-            const int64_t rem = ntok_total - b * p.T;
-            p.ntok[slot] = (int32_t)(rem < p.T ? rem : p.T);
-        }
-    }
-}
-
-cudaError_t launch_synth_fill(const PoolView& p, uint64_t seed, float skew, float prob, int round_bf16,
-                              int32_t n_units, const int64_t* d_unit_ids, const int64_t* d_slot_off,
-                              const int64_t* d_tokens, int64_t max_blocks, float* d_dirs, cudaStream_t st) {
-    if (n_units <= 0) return cudaSuccess;
-    synth_dir_kernel<<<(n_units + 127) / 128, 128, 0, st>>>(seed, p.d, n_units, d_unit_ids, d_dirs);
-    const unsigned gx = (unsigned)(max_blocks < 4096 ? (max_blocks > 0 ? max_blocks : 1) : 4096);
-    dim3 grid(gx, (unsigned)n_units);
-    if (p.dtype == 0)
-        synth_fill_kernel<float><<<grid, 256, 0, st>>>(p, seed, skew, prob, round_bf16, d_unit_ids, d_slot_off,
-                                                       d_tokens, d_dirs);
-    else
-        synth_fill_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(p, seed, skew, prob, round_bf16, d_unit_ids,
-                                                               d_slot_off, d_tokens, d_dirs);
     return cudaGetLastError();
 }
 

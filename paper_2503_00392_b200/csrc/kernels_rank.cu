@@ -746,4 +746,22 @@ int launch_batch(const PoolView& p, const BatchView& b, cudaStream_t st, cudaEve
     return launches;
 }
 
+// Sort keys of every (unit, head) for a full ranking (psattn_rank_batch): fp64 oracle masses
+// (Oracle ranking / audit) and/or criticality scores, nothing else. Returns launches or -1.
+int launch_rank_keys(const PoolView& p, const BatchView& b, cudaStream_t st) {
+    int launches = 0;
+    if (b.has_oracle) {
+        const int64_t chunks = (b.max_n + kScoreWarps - 1) / kScoreWarps;
+        dim3 grid((unsigned)(chunks < 65535 ? (chunks > 0 ? chunks : 1) : 65535), (unsigned)b.n_units);
+        if (p.dtype == 0) launch_oracle<float>(p, b, grid, st);
+        else launch_oracle<__nv_bfloat16>(p, b, grid, st);
+        ++launches;
+    }
+    if (!b.rank_oracle) {
+        launch_score_stage(p, b, st);
+        ++launches;
+    }
+    return cudaPeekAtLastError() == cudaSuccess ? launches : -1;
+}
+
 }  // namespace psa

@@ -10,14 +10,13 @@
 // (score_kernel_tma, first_tranche_kernel, dense_decide_kernel).
 #include <cuda_runtime.h>
 #include <stdint.h>
-#include <thrust/device_ptr.h>
-#include <thrust/execution_policy.h>
-#include <thrust/sequence.h>
-#include <thrust/sort.h>
 
 #include <string>
+#include <vector>
 
+#include "common.cuh"
 #include "device.h"
+#include "kernels.cuh"
 #include "psattn_b200.h"
 
 namespace psa {
@@ -47,14 +46,17 @@ __global__ void criticality_kernel(const float* __restrict__ q, int d, const flo
     out[i] = est == 0 ? ms : (est == 1 ? us : __dmul_rn(0.5, __dadd_rn(ms, us)));
 }
 
-struct ScoreOrder {
-    const double* s;
-    const int64_t* id;
-    __device__ bool operator()(int64_t a, int64_t b) const {
-        if (s[a] != s[b]) return s[a] > s[b];
-        return id[a] < id[b];
-    }
-};
+// rank_by_scores keys: pass 1 sorts by block id (signed -> order-preserving unsigned), pass 2
+// stably by descending score, so equal scores keep ascending block id (metadata.cpp:92-93).
+__global__ void id_keys_kernel(const int64_t* __restrict__ ids, int64_t n, uint64_t* __restrict__ keys) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) keys[i] = (uint64_t)ids[i] ^ 0x8000000000000000ull;
+}
+__global__ void score_keys_kernel(const double* __restrict__ s, const int32_t* __restrict__ perm, int64_t n,
+                                  uint64_t* __restrict__ keys) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) keys[i] = make_key_masked(s[perm[i]], 0u, 0ull);
+}
 
 template <typename T>
 struct DevBuf {
@@ -111,17 +113,32 @@ extern "C" int psattn_rank_by_scores(const double* scores, const int64_t* block_
     if (int rc = need_device("psattn_rank_by_scores")) return rc;
     if (n == 0) return PSATTN_OK;
     DevBuf<double> ds;
-    DevBuf<int64_t> di, dord;
+    DevBuf<int64_t> di;
     cudaError_t e;
-    if ((e = ds.alloc(n)) || (e = di.alloc(n)) || (e = dord.alloc(n))) return cuda_fail(e, "psattn_rank_by_scores: alloc");
+    if ((e = ds.alloc(n)) || (e = di.alloc(n))) return cuda_fail(e, "psattn_rank_by_scores: alloc");
     if ((e = cudaMemcpy(ds.p, scores, (size_t)n * 8, cudaMemcpyHostToDevice)) ||
         (e = cudaMemcpy(di.p, block_ids, (size_t)n * 8, cudaMemcpyHostToDevice)))
         return cuda_fail(e, "psattn_rank_by_scores: upload");
-    thrust::device_ptr<int64_t> o(dord.p);
-    thrust::sequence(thrust::device, o, o + n);
-    thrust::sort(thrust::device, o, o + n, ScoreOrder{ds.p, di.p});
-    if ((e = cudaGetLastError())) return cuda_fail(e, "psattn_rank_by_scores: sort");
-    if ((e = cudaMemcpy(order, dord.p, (size_t)n * 8, cudaMemcpyDeviceToHost)))
+    if (n > 0x7fffffffLL) return fail(PSATTN_ERR_INVALID_ARGUMENT, "psattn_rank_by_scores: too many blocks");
+    DevBuf<uint64_t> keys, tk;
+    DevBuf<int32_t> perm, ord32, tv, tv2;
+    DevBuf<int64_t> off;
+    if ((e = keys.alloc(n)) || (e = tk.alloc(n)) || (e = perm.alloc(n)) || (e = ord32.alloc(n)) || (e = tv.alloc(n)) || (e = tv2.alloc(n)) ||
+        (e = off.alloc(2)))
+        return cuda_fail(e, "psattn_rank_by_scores: alloc");
+    const int64_t hoff[2] = {0, n};
+    if ((e = cudaMemcpy(off.p, hoff, sizeof(hoff), cudaMemcpyHostToDevice)))
+        return cuda_fail(e, "psattn_rank_by_scores: upload");
+    const unsigned blocks = (unsigned)((n + 255) / 256);
+    id_keys_kernel<<<blocks, 256>>>(di.p, n, keys.p);
+    if ((e = launch_seg_sort(keys.p, nullptr, perm.p, tk.p, tv.p, tv2.p, off.p, 1, 1, 0)))
+        return cuda_fail(e, "psattn_rank_by_scores: sort by id");
+    score_keys_kernel<<<blocks, 256>>>(ds.p, perm.p, n, keys.p);
+    if ((e = launch_seg_sort(keys.p, perm.p, ord32.p, tk.p, tv.p, tv2.p, off.p, 1, 1, 0)))
+        return cuda_fail(e, "psattn_rank_by_scores: sort by score");
+    std::vector<int32_t> ord((size_t)n);
+    if ((e = cudaMemcpy(ord.data(), ord32.p, (size_t)n * 4, cudaMemcpyDeviceToHost)))
         return cuda_fail(e, "psattn_rank_by_scores: download");
+    for (int64_t i = 0; i < n; ++i) order[i] = ord[(size_t)i];
     return PSATTN_OK;
 }

@@ -1,10 +1,9 @@
 // store.cpp — TieredBlockStore over the device pool (B200 build).
 //
-// Blocks: one device pool per head dim (psattn_pool, slots shared by all
-// layers). Fast-tier accounting: the reference's observable semantics
-// (store.cpp:11-124 of the reference): Unified vs LayerPartitioned domains,
-// write-allocate on put, hit/miss with LRU splice or FIFO order on load,
-// eviction counts per layer, bytes = fp32 payload per miss, optional trace.
+// Blocks: one device pool per head dim (psattn_pool, slots shared by all layers). The
+// fast-tier hit/miss/eviction/byte accounting with the reference's observable semantics
+// (store.cpp:11-124 of the reference) is psa::FastTier (fast_tier.h), shared with the two-tier
+// store (tier.cpp); this file adds the block records, the device copies and the access trace.
 #include "psattn/store.hpp"
 
 #include <algorithm>
@@ -17,6 +16,7 @@
 
 #include "device.h"
 #include "engine_internal.h"
+#include "fast_tier.h"
 #include "psattn_b200.h"
 
 namespace psattn {
@@ -93,15 +93,9 @@ struct TieredBlockStore::DeviceState {
 
 TieredBlockStore::TieredBlockStore(const StoreOptions& options) : options_(options) {
     if (options_.n_layers <= 0) throw Error("TieredBlockStore: n_layers must be positive");
-    if (options_.policy == PoolPolicy::Unified) {
-        domains_.resize(1);
-        domains_[0].capacity = options_.fast_capacity_slots;
-    } else {
-        domains_.resize(static_cast<std::size_t>(options_.n_layers));
-        const std::size_t per = options_.fast_capacity_slots / static_cast<std::size_t>(options_.n_layers);
-        for (auto& d : domains_) d.capacity = per;
-    }
-    stats_.per_layer.resize(static_cast<std::size_t>(options_.n_layers));
+    tier_ = std::make_unique<psa::FastTier>(options_.fast_capacity_slots, options_.n_layers,
+                                            options_.policy == PoolPolicy::LayerPartitioned,
+                                            options_.eviction == EvictionPolicy::LRU);
     int n = 0;
     if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
         throw Error("TieredBlockStore: no CUDA device (the B200 PSA path has no CPU fallback)");
@@ -111,34 +105,9 @@ TieredBlockStore::TieredBlockStore(const StoreOptions& options) : options_(optio
 
 TieredBlockStore::~TieredBlockStore() = default;
 
-TieredBlockStore::Domain& TieredBlockStore::domain_for(std::int32_t layer_id) {
-    if (layer_id < 0 || layer_id >= options_.n_layers) throw Error("TieredBlockStore: layer_id out of range");
-    return options_.policy == PoolPolicy::Unified ? domains_[0] : domains_[static_cast<std::size_t>(layer_id)];
-}
-const TieredBlockStore::Domain& TieredBlockStore::domain_for(std::int32_t layer_id) const {
-    if (layer_id < 0 || layer_id >= options_.n_layers) throw Error("TieredBlockStore: layer_id out of range");
-    return options_.policy == PoolPolicy::Unified ? domains_[0] : domains_[static_cast<std::size_t>(layer_id)];
-}
-
-void TieredBlockStore::count_eviction(BlockId victim) {
-    stats_.evictions += 1;
-    auto it = blocks_.find(victim);
-    if (it != blocks_.end()) stats_.per_layer[static_cast<std::size_t>(it->second.layer)].evictions += 1;
-}
-
-BlockId TieredBlockStore::insert_fast(Domain& domain, BlockId id, bool* evicted) {
-    *evicted = false;
-    if (domain.capacity == 0) return 0;
-    BlockId victim = 0;
-    if (domain.slots.size() == domain.capacity) {
-        victim = domain.order.back();
-        domain.order.pop_back();
-        domain.slots.erase(victim);
-        *evicted = true;
-    }
-    domain.order.push_front(id);
-    domain.slots.emplace(id, domain.order.begin());
-    return victim;
+std::int32_t TieredBlockStore::layer_of(BlockId id) const {
+    auto it = blocks_.find(id);
+    return it == blocks_.end() ? -1 : it->second.layer;
 }
 
 TieredBlockStore::DevicePool& TieredBlockStore::pool_for(std::int32_t dim, std::int32_t n_tokens) {
@@ -187,38 +156,16 @@ void TieredBlockStore::put_block(std::shared_ptr<const KVBlock> block, RequestId
     check_rc(psa::pool_put(dp.pool, 1, &s32, &nt, block->keys.data(), block->values.data(), 0, dev_->stream));
     blocks_.emplace(block->block_id, BlockRec{block->dim, block->layer_id, block->n_tokens, slot, owner});
     owned_[owner].push_back(block->block_id);
-    bool evicted = false;
-    const BlockId victim = insert_fast(domain_for(block->layer_id), block->block_id, &evicted);
-    if (evicted) count_eviction(victim);
+    tier_->put(block->block_id, block->layer_id, [this](BlockId v) { return layer_of(v); });
 }
 
-bool TieredBlockStore::load_locked(BlockId id, const BlockRec& rec) {
-    Domain& domain = domain_for(rec.layer);
-    auto& ls = stats_.per_layer[static_cast<std::size_t>(rec.layer)];
-    auto slot = domain.slots.find(id);
-    bool miss = false, evicted = false;
-    BlockId victim = 0;
-    if (slot != domain.slots.end()) {
-        stats_.hits += 1;
-        ls.hits += 1;
-        if (options_.eviction == EvictionPolicy::LRU) domain.order.splice(domain.order.begin(), domain.order, slot->second);
-    } else {
-        miss = true;
-        const std::uint64_t bytes = 2ull * static_cast<std::uint64_t>(rec.n_tokens) * rec.dim * sizeof(float);
-        stats_.misses += 1;
-        ls.misses += 1;
-        stats_.bytes_transferred += bytes;
-        ls.bytes_transferred += bytes;
-        victim = insert_fast(domain, id, &evicted);
-        if (evicted) count_eviction(victim);
-    }
-    if (trace_) {
-        *trace_ << trace_seq_++ << ',' << rec.layer << ',' << id << ',' << (miss ? "miss" : "hit") << ',';
-        if (evicted) *trace_ << victim;
-        else *trace_ << '-';
-        *trace_ << '\n';
-    }
-    return miss;
+bool TieredBlockStore::account_locked(BlockId id, const BlockRec& rec) {
+    const std::uint64_t payload = 2ull * static_cast<std::uint64_t>(rec.n_tokens) * rec.dim * sizeof(float);
+    const auto a = tier_->access(id, rec.layer, payload, [this](BlockId v) { return layer_of(v); });
+    if (trace_)  // seq,layer_id,block_id,hit|miss,evicted_id|-
+        *trace_ << trace_seq_++ << ',' << rec.layer << ',' << id << ',' << (a.hit ? "hit," : "miss,")
+                << (a.evicted ? std::to_string(*a.evicted) : std::string("-")) << '\n';
+    return !a.hit;
 }
 
 std::pair<std::uint64_t, std::uint64_t> TieredBlockStore::account_loads(std::span<const BlockId> ids) {
@@ -227,7 +174,7 @@ std::pair<std::uint64_t, std::uint64_t> TieredBlockStore::account_loads(std::spa
     for (BlockId id : ids) {
         auto it = blocks_.find(id);
         if (it == blocks_.end()) throw NotFoundError("load_block: unknown block id " + std::to_string(id));
-        if (load_locked(id, it->second)) ++m;
+        if (account_locked(id, it->second)) ++m;
         else ++h;
     }
     return {h, m};
@@ -259,7 +206,7 @@ std::shared_ptr<const KVBlock> TieredBlockStore::load_block(BlockId block_id, st
         auto it = blocks_.find(block_id);
         if (it == blocks_.end()) throw NotFoundError("load_block: unknown block id " + std::to_string(block_id));
         if (layer_id >= 0 && it->second.layer != layer_id) throw Error("load_block: layer_id does not match block");
-        miss = load_locked(block_id, it->second);
+        miss = account_locked(block_id, it->second);
         out = copy_out(block_id, it->second);
     }
     if (miss) inject_miss_latency(1);
@@ -303,12 +250,7 @@ void TieredBlockStore::release_request(RequestId request_id) {
     for (BlockId id : it->second) {
         auto b = blocks_.find(id);
         if (b == blocks_.end()) continue;
-        Domain& domain = domain_for(b->second.layer);
-        auto s = domain.slots.find(id);
-        if (s != domain.slots.end()) {
-            domain.order.erase(s->second);
-            domain.slots.erase(s);
-        }
+        tier_->release(id, b->second.layer);
         pools_.at(b->second.dim)->free_slots.push_back(b->second.slot);
         blocks_.erase(b);
     }
@@ -324,24 +266,29 @@ bool TieredBlockStore::resident_fast(BlockId block_id) const {
     std::lock_guard lock(mutex_);
     auto it = blocks_.find(block_id);
     if (it == blocks_.end()) return false;
-    return domain_for(it->second.layer).slots.count(block_id) > 0;
+    return tier_->resident(block_id, it->second.layer);
 }
 
 CacheStats TieredBlockStore::stats() const {
     std::lock_guard lock(mutex_);
-    return stats_;
+    const auto& t = tier_->total();
+    CacheStats out{t.hits, t.misses, t.evictions, t.bytes, {}};
+    for (std::int32_t l = 0; l < tier_->n_layers(); ++l) {
+        const auto& c = tier_->layer(l);
+        out.per_layer.push_back(LayerCacheStats{c.hits, c.misses, c.evictions, c.bytes});
+    }
+    return out;
 }
 
 std::size_t TieredBlockStore::fast_occupancy() const {
     std::lock_guard lock(mutex_);
-    std::size_t t = 0;
-    for (const auto& d : domains_) t += d.slots.size();
-    return t;
+    return tier_->occupancy();
 }
 
 std::size_t TieredBlockStore::domain_capacity(std::int32_t layer_id) const {
     std::lock_guard lock(mutex_);
-    return domain_for(layer_id).capacity;
+    if (layer_id < 0 || layer_id >= options_.n_layers) throw Error("TieredBlockStore: layer_id out of range");
+    return tier_->capacity(layer_id);
 }
 
 void TieredBlockStore::enable_trace(std::ostream* sink) {
@@ -428,7 +375,7 @@ void TieredBlockStore::run_device(const detail::DeviceQueryBatch& qb, detail::De
     b.iter_est = reinterpret_cast<double*>(dout + o); o += ob_iest;
     const size_t wsb = psattn_batch_workspace_bytes(&b);
     void* ws = dev_->ws.get(wsb);
-    check_rc(psattn_run_batch(pool, &b, ws, dev_->stream));
+    check_rc(qb.rank_only ? psattn_rank_batch(pool, &b, ws, dev_->stream) : psattn_run_batch(pool, &b, ws, dev_->stream));
 
     const bool has_oracle = b.ranking_mode == PSATTN_RANK_ORACLE || b.audit_coverage;
     const size_t om_b = has_oracle ? static_cast<size_t>(hbt) * 8 : 0;
@@ -467,14 +414,20 @@ void TieredBlockStore::run_device(const detail::DeviceQueryBatch& qb, detail::De
         for (int h = 0; h < g; ++h) {
             const std::int64_t qi = static_cast<std::int64_t>(u) * g + h;
             const std::int64_t hb = off[u] * g + h * n;
+            // psattn_run_batch defines ranks below blocks_processed only (it orders lazily)
+            const std::int64_t nr = qb.rank_only ? n : std::clamp<std::int64_t>(bp[qi], 0, n);
             auto& ids = res.ranked_ids[qi];
-            ids.resize(n);
-            for (std::int64_t r = 0; r < n; ++r) ids[r] = sorted[u][rpos[hb + r]];
-            res.iter_est[qi].assign(iest + hb, iest + hb + n);
+            ids.resize(static_cast<std::size_t>(nr));
+            for (std::int64_t r = 0; r < nr; ++r) {
+                const std::int32_t pos = rpos[hb + r];
+                if (pos < 0 || pos >= n) throw Error("device ranking: position out of range");
+                ids[r] = sorted[u][pos];
+            }
+            if (!qb.rank_only) res.iter_est[qi].assign(iest + hb, iest + hb + nr);
             if (has_oracle) {
                 auto& orr = res.oracle_ranked[qi];
-                orr.resize(n);
-                for (std::int64_t r = 0; r < n; ++r) orr[r] = om[hb + rpos[hb + r]];
+                orr.resize(static_cast<std::size_t>(nr));
+                for (std::int64_t r = 0; r < nr; ++r) orr[r] = om[hb + rpos[hb + r]];
             }
         }
     }

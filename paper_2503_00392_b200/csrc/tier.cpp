@@ -19,7 +19,7 @@
 #include <cmath>
 #include <cstring>
 #include <limits>
-#include <list>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <unordered_map>
@@ -28,26 +28,20 @@
 #include <cuda_runtime.h>
 
 #include "device.h"
+#include "fast_tier.h"
 #include "kernels.cuh"
 #include "psattn_b200.h"
 
 struct psattn_tier {
     psattn_tier_desc desc{};
     psattn_pool* pool = nullptr;
-    struct Domain {
-        size_t capacity = 0;
-        std::list<int64_t> order;  // front = most recent
-        std::unordered_map<int64_t, std::list<int64_t>::iterator> pos;
-        std::vector<int32_t> free_slots;
-    };
-    std::vector<Domain> domains;
+    std::unique_ptr<psa::FastTier> fast;          // residency + counters (fast_tier.h)
+    std::vector<std::vector<int32_t>> free_slots;  // free HBM slots per domain
     std::vector<int32_t> loc;    // host mirror of the device location table
     std::vector<int32_t> layer;  // -1 = no such block
     std::vector<int32_t> ntok;
     std::vector<int64_t> owner;
     std::unordered_map<int64_t, std::vector<int64_t>> owned;
-    std::vector<psattn_cache_stats> per_layer;
-    psattn_cache_stats total{};
     uint64_t h2d_bytes = 0;
     std::vector<int64_t> pending;  // blocks (re)inserted into the fast tier since the last install
     std::mutex mu;
@@ -57,53 +51,43 @@ namespace {
 
 using psa::fail;
 
-psattn_tier::Domain& domain_of(psattn_tier* t, int32_t layer) {
-    return t->desc.pool_policy == PSATTN_POOL_UNIFIED ? t->domains[0] : t->domains[(size_t)layer];
+size_t domain_index(const psattn_tier* t, int32_t layer) {
+    return t->desc.pool_policy == PSATTN_POOL_UNIFIED ? 0 : (size_t)layer;
 }
 
-// insert_fast (reference store.cpp:44-57): evicts the LRU/FIFO tail when full; the new
-// block takes the victim's HBM slot (or a free one).
-void insert_fast(psattn_tier* t, int64_t id) {
-    psattn_tier::Domain& d = domain_of(t, t->layer[(size_t)id]);
-    if (d.capacity == 0) return;
+// Slot bookkeeping after an admission into the fast tier: the new block takes the victim's
+// HBM slot, or a free slot of its domain.
+void place(psattn_tier* t, int64_t id, const std::optional<int64_t>& victim) {
+    if (!t->fast->resident(id, t->layer[(size_t)id])) return;  // zero-capacity domain
     int32_t slot;
-    if (d.pos.size() == d.capacity) {
-        const int64_t victim = d.order.back();
-        d.order.pop_back();
-        d.pos.erase(victim);
-        slot = t->loc[(size_t)victim];
-        t->loc[(size_t)victim] = -1;
-        t->total.evictions += 1;
-        t->per_layer[(size_t)t->layer[(size_t)victim]].evictions += 1;
+    if (victim) {
+        slot = t->loc[(size_t)*victim];
+        t->loc[(size_t)*victim] = -1;
     } else {
-        slot = d.free_slots.back();
-        d.free_slots.pop_back();
+        auto& fl = t->free_slots[domain_index(t, t->layer[(size_t)id])];
+        slot = fl.back();
+        fl.pop_back();
     }
-    d.order.push_front(id);
-    d.pos.emplace(id, d.order.begin());
     t->loc[(size_t)id] = slot;
     t->pending.push_back(id);
 }
 
-// load_block's accounting (reference store.cpp:80-124).
-void load(psattn_tier* t, int64_t id) {
-    const int32_t l = t->layer[(size_t)id];
-    psattn_tier::Domain& d = domain_of(t, l);
-    auto& ls = t->per_layer[(size_t)l];
-    auto it = d.pos.find(id);
-    if (it != d.pos.end()) {
-        t->total.hits += 1;
-        ls.hits += 1;
-        if (t->desc.eviction_policy == PSATTN_EVICT_LRU) d.order.splice(d.order.begin(), d.order, it->second);
-        return;
-    }
-    const uint64_t bytes = 2ull * (uint64_t)t->ntok[(size_t)id] * (uint64_t)t->desc.dim * sizeof(float);
-    t->total.misses += 1;
-    ls.misses += 1;
-    t->total.bytes_transferred += bytes;
-    ls.bytes_transferred += bytes;
-    insert_fast(t, id);
+int32_t layer_lookup(const psattn_tier* t, int64_t id) { return t->layer[(size_t)id]; }
+
+// put_block's write-allocate (reference store.cpp:75-77).
+void put_fast(psattn_tier* t, int64_t id) {
+    place(t, id, t->fast->put(id, t->layer[(size_t)id], [t](int64_t v) { return layer_lookup(t, v); }));
 }
+
+// load_block's accounting (reference store.cpp:80-124); true on a hit.
+bool load(psattn_tier* t, int64_t id) {
+    const uint64_t bytes = 2ull * (uint64_t)t->ntok[(size_t)id] * (uint64_t)t->desc.dim * sizeof(float);
+    const auto a = t->fast->access(id, t->layer[(size_t)id], bytes, [t](int64_t v) { return layer_lookup(t, v); });
+    if (!a.hit) place(t, id, a.evicted);
+    return a.hit;
+}
+
+psattn_cache_stats to_c(const psa::TierCounters& c) { return psattn_cache_stats{c.hits, c.misses, c.evictions, c.bytes}; }
 
 // Installs every pending block that is still resident and publishes the location table.
 int install_pending(psattn_tier* t, cudaStream_t st) {
@@ -165,21 +149,15 @@ int psattn_tier_create(const psattn_tier_desc* desc, psattn_tier** out) {
     t->layer.assign(nb, -1);
     t->ntok.assign(nb, 0);
     t->owner.assign(nb, 0);
-    t->per_layer.assign((size_t)desc->n_layers, psattn_cache_stats{});
-    if (desc->pool_policy == PSATTN_POOL_UNIFIED) {
-        t->domains.resize(1);
-        t->domains[0].capacity = (size_t)desc->fast_slots;
-    } else {
-        t->domains.resize((size_t)desc->n_layers);
-        const size_t per = (size_t)desc->fast_slots / (size_t)desc->n_layers;
-        for (auto& d : t->domains) d.capacity = per;
-    }
+    const bool per_layer = desc->pool_policy != PSATTN_POOL_UNIFIED;
+    t->fast = std::make_unique<psa::FastTier>((size_t)desc->fast_slots, desc->n_layers, per_layer,
+                                              desc->eviction_policy == PSATTN_EVICT_LRU);
     // HBM slots: [0, cap) for the unified domain, [l*per, (l+1)*per) for layer l
-    int32_t next = 0;
-    for (auto& d : t->domains) {
-        for (size_t i = 0; i < d.capacity; ++i) d.free_slots.push_back(next + (int32_t)(d.capacity - 1 - i));
-        next += (int32_t)d.capacity;
-    }
+    const size_t n_dom = per_layer ? (size_t)desc->n_layers : 1;
+    const size_t per = per_layer ? (size_t)desc->fast_slots / (size_t)desc->n_layers : (size_t)desc->fast_slots;
+    t->free_slots.assign(n_dom, {});
+    for (size_t dd = 0; dd < n_dom; ++dd)
+        for (size_t i = 0; i < per; ++i) t->free_slots[dd].push_back((int32_t)(dd * per + per - 1 - i));
     *out = t;
     return PSATTN_OK;
 }
@@ -224,7 +202,7 @@ int psattn_tier_put_blocks(psattn_tier* t, int64_t n, const int64_t* blocks, con
     cudaError_t e2 = cudaStreamSynchronize(st);
     cudaFree(d_idx);
     if (e != cudaSuccess || e2 != cudaSuccess) return psa::cuda_fail(e != cudaSuccess ? e : e2, "tier metadata build");
-    for (int64_t i = 0; i < n; ++i) insert_fast(t, blocks[i]);  // write-allocate (store.cpp:75-77)
+    for (int64_t i = 0; i < n; ++i) put_fast(t, blocks[i]);  // write-allocate (store.cpp:75-77)
     return install_pending(t, st);
 }
 
@@ -235,12 +213,8 @@ int psattn_tier_release_request(psattn_tier* t, int64_t owner) {
     if (it == t->owned.end()) return fail(PSATTN_ERR_NOT_FOUND, "release_request: unknown request " + std::to_string(owner));
     for (int64_t id : it->second) {
         if (t->layer[(size_t)id] < 0) continue;
-        psattn_tier::Domain& d = domain_of(t, t->layer[(size_t)id]);
-        auto p = d.pos.find(id);
-        if (p != d.pos.end()) {
-            d.order.erase(p->second);
-            d.pos.erase(p);
-            d.free_slots.push_back(t->loc[(size_t)id]);
+        if (t->fast->release(id, t->layer[(size_t)id])) {
+            t->free_slots[domain_index(t, t->layer[(size_t)id])].push_back(t->loc[(size_t)id]);
             t->loc[(size_t)id] = -1;
         }
         t->layer[(size_t)id] = -1;
@@ -289,9 +263,7 @@ int tier_run_account(psattn_tier* t, const psattn_batch* b, void* workspace, cud
         const int64_t end = std::min(cur[(size_t)qi] + m, bp[(size_t)qi]);
         const int64_t hb = off[(size_t)u] * b->group + h * n;
         for (int64_t r = cur[(size_t)qi]; r < end; ++r) {
-            const uint64_t h0 = t->total.hits;
-            load(t, slots[(size_t)(off[(size_t)u] + rpos[(size_t)(hb + r)])]);
-            if (t->total.hits != h0) ++it.hits;
+            if (load(t, slots[(size_t)(off[(size_t)u] + rpos[(size_t)(hb + r)])])) ++it.hits;
             else ++it.misses;
             ++it.blocks;
         }
@@ -331,7 +303,7 @@ int psattn_tier_stats(psattn_tier* t, int32_t layer, psattn_cache_stats* out) {
     if (!t || !out) return fail(PSATTN_ERR_INVALID_ARGUMENT, "psattn_tier_stats: null argument");
     std::lock_guard<std::mutex> lk(t->mu);
     if (layer < -1 || layer >= t->desc.n_layers) return fail(PSATTN_ERR_INVALID_ARGUMENT, "psattn_tier_stats: bad layer");
-    *out = layer < 0 ? t->total : t->per_layer[(size_t)layer];
+    *out = to_c(layer < 0 ? t->fast->total() : t->fast->layer(layer));
     return PSATTN_OK;
 }
 

@@ -10,20 +10,21 @@ import torch
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from paper_2503_00392_b200 import batch, capi  # noqa: E402
+from workload import synth  # fixture: the seekable synthetic generator
 
 dev = torch.device("cuda")
 d, T, g = 128, 16, 4
 
 
 def synth_run(tokens, planted, cfg, kv=capi.PSATTN_KV_BF16, kernel=0):
-    p = capi.synth_params(seed=2, dim=d, block_tokens=T, skew=8.0, planted_prob=planted, round_bf16=1)
+    p = synth.params(seed=2, dim=d, block_tokens=T, skew=8.0, planted_prob=planted, round_bf16=1)
     nb = [(t + T - 1) // T for t in tokens]
     off = np.zeros(len(tokens) + 1, np.int64)
     off[1:] = np.cumsum(nb)
     pool = batch.DevicePool(d, T, kv, int(off[-1]))
     uids = list(range(7, 7 + len(tokens)))
-    pool.fill_synthetic(p, uids, off[:-1], tokens)
-    qs = np.array([[capi.synth_query(p, u, h) for h in range(g)] for u in uids], np.float32)
+    synth.fill(pool, p, uids, off[:-1], tokens)
+    qs = np.array([[synth.query(p, u, h) for h in range(g)] for u in uids], np.float32)
     run = batch.BatchRun(pool, torch.tensor(qs, device=dev), torch.arange(int(off[-1]), dtype=torch.int32, device=dev),
                          torch.tensor(off, device=dev), max(nb), batch.BatchConfig(**cfg), want_ranked=True)
     capi.check(capi.lib.psattn_set_progressive_kernel(kernel))

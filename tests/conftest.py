@@ -16,6 +16,15 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200); run with -m gpu")
 
 
+def _ensure_workload():
+    lib = os.path.join(ROOT, "workload", "_lib", "libpsattn_synth_host.so")
+    if not os.path.exists(lib):
+        subprocess.run(["make", "-C", os.path.join(ROOT, "workload")], check=True, stdout=subprocess.DEVNULL)
+
+
+_ensure_workload()
+
+
 def _ensure_oracle():
     so = os.path.join(ROOT, "oracle", "build", "libpsa_oracle.so")
     if not os.path.exists(so):

@@ -2,6 +2,7 @@
 // test_pipeline.cpp, test_store.cpp) against include/psattn/*.hpp, linked to
 // libpsattn_b200.so. Prints "OK <n>" and exits 0 on success. Built by
 // tests/test_gpu_cpp.py with g++ -std=c++20.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -374,6 +375,70 @@ int main() {
         CHECK(nf);
         const BlockMetadata bm = build_metadata(*blk);
         CHECK(bm.mean_key == m.mean_key && bm.lo == m.lo && bm.hi == m.hi);
+    }
+    // --- plan_blocks over a long list (> the 512/1024-rank tranches the progressive kernels order
+    //     lazily): every rank equals the reference ranking restated on the host (criticality_score
+    //     in index order, metadata.cpp:41-72; score desc, block id asc, metadata.cpp:87-96);
+    //     psa_attention on the same list agrees with the plan's prefix ---
+    {
+        std::mt19937_64 rng(4242);
+        const int d = 128, T = 16, n = 3000;
+        TieredBlockStore store(opts(0));
+        std::vector<BlockId> ids;
+        // ids deliberately not in ascending order of insertion: the tie rule is on block id
+        std::shared_ptr<KVBlock> prev;
+        for (int i = 0; i < n; ++i) {
+            const BlockId id = static_cast<BlockId>((i * 7919) % 10007);
+            auto blk = make_block(rng, id, 0, T, d);
+            if (i % 100 == 1) {  // exact copy of the previous block: equal scores, ties resolved by id
+                *blk = *prev;
+                blk->block_id = id;
+            }
+            store.put_block(blk, 1);
+            ids.push_back(id);
+            prev = blk;
+        }
+        std::normal_distribution<float> nd;
+        std::vector<float> q(d);
+        for (auto& x : q) x = nd(rng);
+        for (Estimator est : {Estimator::Mean, Estimator::CuboidUpperBound, Estimator::CuboidMean}) {
+            PSAConfig cfg;
+            cfg.estimator = est;
+            const RankedPlan plan = plan_blocks(q, ids, cfg, store);
+            CHECK(plan.ranked_ids.size() == static_cast<std::size_t>(n));
+            const double scale = 1.0 / std::sqrt(static_cast<double>(d));
+            std::vector<std::pair<double, BlockId>> ref;
+            for (BlockId id : ids) {
+                const BlockMetadata m = store.metadata(id);
+                double am = 0.0, au = 0.0;
+                for (int k = 0; k < d; ++k) {
+                    const double qd = q[k];
+                    am += qd * static_cast<double>(m.mean_key[k]);
+                    au += std::max(qd * static_cast<double>(m.lo[k]), qd * static_cast<double>(m.hi[k]));
+                }
+                const double s = est == Estimator::Mean ? am * scale
+                                 : est == Estimator::CuboidUpperBound ? au * scale
+                                                                      : 0.5 * (am * scale + au * scale);
+                ref.emplace_back(s, id);
+            }
+            std::vector<std::pair<double, BlockId>> sorted = ref;
+            std::sort(sorted.begin(), sorted.end(), [](const auto& a, const auto& b) {
+                return a.first != b.first ? a.first > b.first : a.second < b.second;
+            });
+            std::size_t mism = 0;
+            for (int r = 0; r < n; ++r)
+                if (plan.ranked_ids[r] != sorted[r].second) {
+                    // only a near-tie (fp64 summation order, ~1e-16 relative) may swap neighbours
+                    const double gap = std::fabs(sorted[r].first - (r + 1 < n ? sorted[r + 1].first : sorted[r - 1].first));
+                    CHECK(gap <= 1e-12 * std::max(1.0, std::fabs(sorted[r].first)));
+                    ++mism;
+                }
+            CHECK(mism <= 2);
+            std::set<BlockId> uniq(plan.ranked_ids.begin(), plan.ranked_ids.end());
+            CHECK(uniq.size() == static_cast<std::size_t>(n));
+            const PSAResult run = psa_attention(q, ids, cfg, store);
+            for (std::size_t r = 0; r < run.blocks_processed; ++r) CHECK(run.processed_ids[r] == plan.ranked_ids[r]);
+        }
     }
     std::printf("OK %d\n", g_checks);
     return 0;

@@ -8,6 +8,7 @@ import re
 
 import numpy as np
 import pytest
+from workload import synth  # fixture: the seekable synthetic generator
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
@@ -70,15 +71,15 @@ def test_synthetic_generator_host_properties():
     """Host copy of the seekable generator: deterministic, seekable, N(0,1)-like keys,
     bf16 rounding exact, planted blocks aligned with the unit direction."""
     from paper_2503_00392_b200 import capi
-    p = capi.synth_params(seed=1, dim=128, block_tokens=16, skew=8.0, planted_prob=0.25, round_bf16=0)
-    k1, v1 = capi.synth_unit_host(p, 3, 16 * 64)
-    k2, v2 = capi.synth_unit_host(p, 3, 16 * 64)
+    p = synth.params(seed=1, dim=128, block_tokens=16, skew=8.0, planted_prob=0.25, round_bf16=0)
+    k1, v1 = synth.unit_host(p, 3, 16 * 64)
+    k2, v2 = synth.unit_host(p, 3, 16 * 64)
     assert k1.tobytes() == k2.tobytes() and v1.tobytes() == v2.tobytes()
-    ks, vs = capi.synth_unit_host(p, 3, 16 * 64, first_block=10, n_blocks=5)  # seekable
+    ks, vs = synth.unit_host(p, 3, 16 * 64, first_block=10, n_blocks=5)  # seekable
     assert ks.tobytes() == k1[10:15].tobytes() and vs.tobytes() == v1[10:15].tobytes()
-    dirv = capi.synth_direction(p, 3)
+    dirv = synth.direction(p, 3)
     assert abs(np.linalg.norm(dirv.astype(np.float64)) - 1) < 1e-6
-    planted = [capi.synth_is_planted(p, 3, b) for b in range(64)]
+    planted = [synth.is_planted(p, 3, b) for b in range(64)]
     assert 4 <= sum(planted) <= 30
     proj = (k1 @ dirv).mean(axis=1)
     for b in range(64):
@@ -86,13 +87,13 @@ def test_synthetic_generator_host_properties():
     iso = [b for b in range(64) if not planted[b]]
     x = k1[iso].reshape(-1)
     assert abs(x.mean()) < 0.02 and abs(x.std() - 1) < 0.02
-    pb = capi.synth_params(seed=1, dim=128, block_tokens=16, skew=8.0, planted_prob=0.25, round_bf16=1)
-    kb, _ = capi.synth_unit_host(pb, 3, 16 * 64)
+    pb = synth.params(seed=1, dim=128, block_tokens=16, skew=8.0, planted_prob=0.25, round_bf16=1)
+    kb, _ = synth.unit_host(pb, 3, 16 * 64)
     assert np.all((kb.view(np.uint32) & 0xFFFF) == 0)
     assert np.max(np.abs(kb - k1)) <= np.max(np.abs(k1)) * 2 ** -8
-    q = capi.synth_query(p, 3, 0)
+    q = synth.query(p, 3, 0)
     assert abs(np.linalg.norm(q.astype(np.float64)) - np.sqrt(128)) < 1e-4
     assert float(q @ dirv) / np.sqrt(128) > 0.98
     # ragged tail: tokens past the end are zero
-    kr, _ = capi.synth_unit_host(p, 3, 16 * 3 + 5)
+    kr, _ = synth.unit_host(p, 3, 16 * 3 + 5)
     assert kr.shape == (4, 16, 128) and np.all(kr[3, 5:] == 0) and np.any(kr[3, :5] != 0)

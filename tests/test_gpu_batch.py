@@ -9,6 +9,7 @@ import pytest
 
 from helpers import check_parity, random_blockset
 from oracle.pyoracle import BlockSet, make_config
+from workload import synth  # fixture: the seekable synthetic generator
 
 pytestmark = pytest.mark.gpu
 
@@ -182,15 +183,15 @@ def test_bf16_pool_synthetic_parity(mods, oracle):
     capi, batch = mods
     d, T, g = 128, 16, 4
     for planted in (0.0, 64 / 2048):
-        p = capi.synth_params(seed=1, dim=d, block_tokens=T, skew=8.0, planted_prob=planted, round_bf16=1)
+        p = synth.params(seed=1, dim=d, block_tokens=T, skew=8.0, planted_prob=planted, round_bf16=1)
         tokens = [16 * 700 + 5, 16 * 300]
         nb = [(t + T - 1) // T for t in tokens]
         slot_off = [0, nb[0]]
         pool = batch.DevicePool(d, T, capi.PSATTN_KV_BF16, sum(nb))
-        pool.fill_synthetic(p, [11, 12], slot_off, tokens)
+        synth.fill(pool, p, [11, 12], slot_off, tokens)
         torch.cuda.synchronize()
         dev = torch.device("cuda")
-        qs = [[capi.synth_query(p, uid, h) for h in range(g)] for uid in (11, 12)]
+        qs = [[synth.query(p, uid, h) for h in range(g)] for uid in (11, 12)]
         slots = np.arange(sum(nb), dtype=np.int32)
         off = np.array([0, nb[0], nb[0] + nb[1]], np.int64)
         run = batch.BatchRun(pool, torch.tensor(np.array(qs), device=dev), torch.tensor(slots, device=dev),
@@ -199,7 +200,7 @@ def test_bf16_pool_synthetic_parity(mods, oracle):
         run.run()
         torch.cuda.synchronize()
         for u, uid in enumerate((11, 12)):
-            k, v = capi.synth_unit_host(p, uid, tokens[u])
+            k, v = synth.unit_host(p, uid, tokens[u])
             ntok = [min(T, tokens[u] - b * T) for b in range(nb[u])]
             bs = BlockSet([k[b, :ntok[b]] for b in range(nb[u])], [v[b, :ntok[b]] for b in range(nb[u])])
             # metadata of the device pool equals the oracle's on the same values
@@ -217,14 +218,14 @@ def test_synthetic_device_equals_host(mods):
     capi, batch = mods
     d, T = 128, 16
     for prob, rb, dt in ((0.1, 1, capi.PSATTN_KV_BF16), (0.05, 0, capi.PSATTN_KV_F32)):
-        p = capi.synth_params(seed=7, dim=d, block_tokens=T, skew=8.0, planted_prob=prob, round_bf16=rb)
+        p = synth.params(seed=7, dim=d, block_tokens=T, skew=8.0, planted_prob=prob, round_bf16=rb)
         tokens = [16 * 40 + 3]
         pool = batch.DevicePool(d, T, dt, 41)
-        pool.fill_synthetic(p, [5], [0], tokens)
+        synth.fill(pool, p, [5], [0], tokens)
         torch.cuda.synchronize()
         lay = pool.layout()
         raw_np = read_device(lay.kv, 41 * lay.slot_bytes)
-        k, v = capi.synth_unit_host(p, 5, tokens[0])
+        k, v = synth.unit_host(p, 5, tokens[0])
         per = T * d
         if dt == capi.PSATTN_KV_BF16:
             words = np.frombuffer(raw_np, np.uint16).reshape(41, 2, per)
@@ -255,12 +256,12 @@ def test_c1_shape_full_parity(mods, oracle, ref):
     capi, batch = mods
     d, T, g, n = 128, 16, 4, 2048
     for planted in (0.0, 64 / 2048):
-        p = capi.synth_params(seed=1, dim=d, block_tokens=T, skew=8.0, planted_prob=planted, round_bf16=0)
+        p = synth.params(seed=1, dim=d, block_tokens=T, skew=8.0, planted_prob=planted, round_bf16=0)
         units = [0, 5]
         pool = batch.DevicePool(d, T, capi.PSATTN_KV_F32, n * len(units))
-        pool.fill_synthetic(p, units, [0, n], [n * T] * len(units))
+        synth.fill(pool, p, units, [0, n], [n * T] * len(units))
         torch.cuda.synchronize()
-        qs = [[capi.synth_query(p, uid, h) for h in range(g)] for uid in units]
+        qs = [[synth.query(p, uid, h) for h in range(g)] for uid in units]
         dev = torch.device("cuda")
         off = np.array([0, n, 2 * n], np.int64)
         run = batch.BatchRun(pool, torch.tensor(np.array(qs), device=dev),
@@ -271,7 +272,7 @@ def test_c1_shape_full_parity(mods, oracle, ref):
         st = ref.store(capacity=0)
         kv_ids = []
         for u, uid in enumerate(units):
-            k, v = capi.synth_unit_host(p, uid, n * T)
+            k, v = synth.unit_host(p, uid, n * T)
             for b in range(n):
                 st.put(u * n + b, k[b], v[b])
             kv_ids.append(np.arange(u * n, (u + 1) * n))
@@ -279,7 +280,7 @@ def test_c1_shape_full_parity(mods, oracle, ref):
         res, union = st.multi_head(allq, np.array(kv_ids), make_config(epsilon=0.95))
         exact = 0
         for u in range(len(units)):
-            k, v = capi.synth_unit_host(p, units[u], n * T)
+            k, v = synth.unit_host(p, units[u], n * T)
             bs = BlockSet(list(k), list(v))
             for h in range(g):
                 r = unpack(run, off, u, h, n)
@@ -351,13 +352,13 @@ def test_graph_replay_identical(mods, planted):
     planted = 0 exercises the dense hand-over inside the graph."""
     capi, batch = mods
     d, T, g = 128, 16, 4
-    p = capi.synth_params(seed=3, dim=d, block_tokens=T, skew=8.0, planted_prob=planted, round_bf16=1)
+    p = synth.params(seed=3, dim=d, block_tokens=T, skew=8.0, planted_prob=planted, round_bf16=1)
     units, n = [21, 22, 23], 1200
     pool = batch.DevicePool(d, T, capi.PSATTN_KV_BF16, n * len(units))
-    pool.fill_synthetic(p, units, np.arange(len(units)) * n, [n * T] * len(units))
+    synth.fill(pool, p, units, np.arange(len(units)) * n, [n * T] * len(units))
     dev = torch.device("cuda")
-    q0 = torch.tensor(np.array([[capi.synth_query(p, u, h) for h in range(g)] for u in units], np.float32), device=dev)
-    q1 = torch.tensor(np.array([[capi.synth_query(p, u + 100, h) for h in range(g)] for u in units], np.float32),
+    q0 = torch.tensor(np.array([[synth.query(p, u, h) for h in range(g)] for u in units], np.float32), device=dev)
+    q1 = torch.tensor(np.array([[synth.query(p, u + 100, h) for h in range(g)] for u in units], np.float32),
                       device=dev)
     slots = torch.arange(n * len(units), dtype=torch.int32, device=dev)
     off = torch.arange(len(units) + 1, dtype=torch.int64, device=dev) * n

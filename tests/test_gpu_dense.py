@@ -7,6 +7,7 @@ import pytest
 
 from helpers import check_parity
 from oracle.pyoracle import BlockSet, make_config
+from workload import synth  # fixture: the seekable synthetic generator
 
 pytestmark = pytest.mark.gpu
 
@@ -22,15 +23,15 @@ def mods():
 def synth_batch(mods, tokens, g, planted, cfg, seed=5):
     capi, batch = mods
     d, T = 128, 16
-    p = capi.synth_params(seed=seed, dim=d, block_tokens=T, skew=8.0, planted_prob=planted, round_bf16=1)
+    p = synth.params(seed=seed, dim=d, block_tokens=T, skew=8.0, planted_prob=planted, round_bf16=1)
     nb = [(t + T - 1) // T for t in tokens]
     off = np.zeros(len(tokens) + 1, np.int64)
     off[1:] = np.cumsum(nb)
     uids = [40 + i for i in range(len(tokens))]
     pool = batch.DevicePool(d, T, capi.PSATTN_KV_BF16, int(off[-1]))
-    pool.fill_synthetic(p, uids, off[:-1], tokens)
+    synth.fill(pool, p, uids, off[:-1], tokens)
     dev = torch.device("cuda")
-    qs = np.array([[capi.synth_query(p, uid, h) for h in range(g)] for uid in uids], np.float32)
+    qs = np.array([[synth.query(p, uid, h) for h in range(g)] for uid in uids], np.float32)
     run = batch.BatchRun(pool, torch.tensor(qs, device=dev), torch.arange(int(off[-1]), dtype=torch.int32, device=dev),
                          torch.tensor(off, device=dev), max(nb), batch.BatchConfig(**cfg), want_ranked=True)
     return p, uids, nb, off, qs, run
@@ -69,7 +70,7 @@ def test_dense_handover_parity(mods, oracle, g, cfg):
     oc = make_config(epsilon=cfg.get("epsilon", 1.0) if not cfg.get("topk") else 1.0,
                      microbatch_size=cfg.get("microbatch_size", 1), estimator=cfg.get("estimator", 2))
     for u, uid in enumerate(uids):
-        k, v = capi.synth_unit_host(p, uid, tokens[u])
+        k, v = synth.unit_host(p, uid, tokens[u])
         nt = [min(16, tokens[u] - i * 16) for i in range(nb[u])]
         bs = BlockSet([k[i, :nt[i]] for i in range(nb[u])], [v[i, :nt[i]] for i in range(nb[u])])
         for h in range(g):
@@ -113,7 +114,7 @@ def test_wide_rounds_parity(mods, oracle, g, cfg):
     oc = make_config(epsilon=cfg.get("epsilon", 1.0) if not cfg.get("topk") else 1.0,
                      microbatch_size=cfg.get("microbatch_size", 1))
     for u, uid in enumerate(uids):
-        k, v = capi.synth_unit_host(p, uid, tokens[u])
+        k, v = synth.unit_host(p, uid, tokens[u])
         nt = [min(16, tokens[u] - i * 16) for i in range(nb[u])]
         bs = BlockSet([k[i, :nt[i]] for i in range(nb[u])], [v[i, :nt[i]] for i in range(nb[u])])
         for h in range(g):

@@ -15,6 +15,7 @@ import pytest
 
 from helpers import check_parity
 from oracle.pyoracle import BlockSet, make_config
+from workload import synth  # fixture: the seekable synthetic generator
 
 pytestmark = pytest.mark.gpu
 
@@ -142,9 +143,9 @@ def test_config4_mixed_lengths_uneven_layers(mods, oracle, ref):
     blocks, layers, ntok, lists, K, V, qs, bsets = [], [], [], [], [], [], [], []
     base = 0
     for r, l, uid, c in units:
-        p = capi.synth_params(seed=4, dim=d, block_tokens=T, skew=8.0, planted_prob=planted_per_layer[l],
+        p = synth.params(seed=4, dim=d, block_tokens=T, skew=8.0, planted_prob=planted_per_layer[l],
                               round_bf16=1)
-        k, v = capi.synth_unit_host(p, uid, c)
+        k, v = synth.unit_host(p, uid, c)
         n = k.shape[0]
         nt = [min(T, c - i * T) for i in range(n)]
         blocks.extend(range(base, base + n))
@@ -153,7 +154,7 @@ def test_config4_mixed_lengths_uneven_layers(mods, oracle, ref):
         K.append(k)
         V.append(v)
         lists.append(np.arange(base, base + n, dtype=np.int64))
-        qs.append([capi.synth_query(p, uid, h) for h in range(g)])
+        qs.append([synth.query(p, uid, h) for h in range(g)])
         bsets.append((k, v, nt))
         base += n
     K, V = np.concatenate(K), np.concatenate(V)

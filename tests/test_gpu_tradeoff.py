@@ -17,6 +17,7 @@ import pytest
 
 from helpers import check_parity
 from oracle.pyoracle import BlockSet, make_config
+from workload import synth  # fixture: the seekable synthetic generator
 
 pytestmark = pytest.mark.gpu
 
@@ -111,12 +112,12 @@ def config3_sweep(mods, n_kv_units=2, ctx=65536, seed=1, planted=1 / 32):
     capi, batch = mods
     d, T, g = 128, 16, 4
     n = ctx // T
-    p = capi.synth_params(seed=seed, dim=d, block_tokens=T, skew=8.0, planted_prob=planted, round_bf16=1)
+    p = synth.params(seed=seed, dim=d, block_tokens=T, skew=8.0, planted_prob=planted, round_bf16=1)
     units = list(range(100, 100 + n_kv_units))
     pool = batch.DevicePool(d, T, capi.PSATTN_KV_BF16, n * len(units))
-    pool.fill_synthetic(p, units, np.arange(len(units)) * n, [ctx] * len(units))
+    synth.fill(pool, p, units, np.arange(len(units)) * n, [ctx] * len(units))
     dev = torch.device("cuda")
-    qs = torch.tensor(np.array([[capi.synth_query(p, u, h) for h in range(g)] for u in units], np.float32),
+    qs = torch.tensor(np.array([[synth.query(p, u, h) for h in range(g)] for u in units], np.float32),
                       device=dev)
     slots = torch.arange(n * len(units), dtype=torch.int32, device=dev)
     off = torch.arange(len(units) + 1, dtype=torch.int64, device=dev) * n
@@ -150,7 +151,7 @@ def test_config3_threshold_vs_topk(mods, oracle):
     # PSA reads a fraction of the KV
     assert eps_rows[2]["kv_fraction_read"] < 0.5
     # parity of every head of the first kv-head unit against the C oracle, for every setting
-    k, v = capi.synth_unit_host(p, units[0], n * 16)
+    k, v = synth.unit_host(p, units[0], n * 16)
     bs = BlockSet(list(k), list(v))
     for (kind, val), (run, cfg) in runs.items():
         oc = make_config(epsilon=val if kind == "eps" else 1.0)
