@@ -39,7 +39,11 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--dist", default="planted", choices=["planted", "iso"])
-    ap.add_argument("--requests", type=int, default=8)
+    ap.add_argument("--requests", type=int, default=8, help="requests per GPU (weak scaling, the default)")
+    ap.add_argument("--total-requests", type=int, default=0,
+                    help="fixed total requests over all GPUs (strong scaling; config 5 = 64): requests shard "
+                         "across ranks, (request, kv head) pairs when requests < GPUs; layers beyond the HBM "
+                         "budget are not resident (a step runs the resident layers)")
     ap.add_argument("--layers", type=int, default=32)
     ap.add_argument("--ctx", type=int, default=131072)
     ap.add_argument("--hq", type=int, default=32)
@@ -55,6 +59,10 @@ def parse():
     ap.add_argument("--score-kernel", type=int, default=0, help="0 auto, 1 register-staged, 2 TMA-staged")
     ap.add_argument("--pipeline", type=int, default=1, help="0 auto, 1 off, k sub-batches")
     ap.add_argument("--graph", type=int, default=1, help="1: replay the step as a captured CUDA graph")
+    ap.add_argument("--plan-only", action="store_true",
+                    help="launcher/sharding dry run (no GPU): every rank reports its units over gloo")
+    ap.add_argument("--check", type=int, default=16,
+                    help="after timing: units of this rank's step checked against the reference (0: off)")
     return ap.parse_args()
 
 
@@ -277,6 +285,33 @@ def ncu_traffic(stage):
         return None
 
 
+def check_step(args, p, run, q_host, unit_ids, n, g):
+    """Samples `--check` units spread over this rank's step (requests x layers x kv heads) and
+    compares all g heads of each with the reference on the same synthetic data (oracle/parity.py:
+    compiled reference psa_attention_multi_head, C oracle for ties). Outside every timed region."""
+    t0 = time.time()
+    U = unit_ids.size
+    pick = np.unique(np.linspace(0, U - 1, min(args.check, U)).astype(np.int64))
+    out = run.out.cpu().numpy()
+    bp = run.bp.cpu().numpy()
+    ranked = run.ranked.cpu().numpy()
+    units = []
+    for u in pick:
+        ids = [ranked[u * n * g + h * n: u * n * g + h * n + int(bp[u * g + h])] for h in range(g)]
+        units.append(dict(uid=int(unit_ids[u]), q=q_host[u], out=out[u], bp=bp[u * g: (u + 1) * g], ids=ids))
+    try:
+        from oracle.parity import check_sampled_units
+        r = check_sampled_units(p, units, args.ctx, args.eps, args.microbatch)
+        r["ok"] = True
+    except AssertionError as e:
+        r = dict(ok=False, units=len(units), error=str(e)[:400])
+    except Exception as e:  # noqa: BLE001  (checker unavailable: say so, never claim parity)
+        r = dict(ok=None, units=len(units), error=f"checker unavailable: {e}"[:400])
+    r["sampled_units"] = [int(unit_ids[u]) for u in pick]
+    r["seconds"] = round(time.time() - t0, 1)
+    return r
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -284,7 +319,10 @@ def run_ours(args):
 
     ws, rank, local = dist_env()
     if ws > 1:
-        dist.init_process_group("nccl")
+        os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator lines show the rank count
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     capi.check(capi.lib.psattn_set_progressive_kernel(args.psa_kernel))
@@ -294,13 +332,24 @@ def run_ours(args):
     p = synth_params(args)
     g = args.hq // args.hkv
     n = args.ctx // args.block
-    U = args.requests * args.layers * args.hkv
+    # ---- units of this rank: weak scaling (requests per GPU fixed) or a fixed total (strong) ----
+    strong = args.total_requests > 0
+    total_req = args.total_requests if strong else args.requests * ws
+    unit_ids = shard.plan_units(total_req, args.layers, args.hkv, ws, rank)
+    layers_resident = args.layers
+    if strong:
+        slot_b = 2 * args.block * args.dim * 2
+        meta_b1 = args.dim * (4 + 2 * 2)
+        budget = torch.cuda.mem_get_info(dev)[0] - (10 << 30)
+        reqs_here = max(1, len(np.unique(unit_ids // (args.layers * args.hkv))))
+        layers_resident = shard.resident_layers(reqs_here, args.layers, args.hkv, n, slot_b + meta_b1, budget)
+        layers_resident = int(shard.max_over_ranks(-layers_resident, dev) * -1)  # the same on every rank
+        unit_ids = unit_ids[(unit_ids // args.hkv) % args.layers < layers_resident]
+    U = int(unit_ids.size)
     nq = U * g
+    nq_all = int(shard.sum_over_ranks(nq, dev))
     # ---- unified pool: every (request, layer, kv-head) list is n consecutive slots ----
     pool = batch.DevicePool(args.dim, args.block, capi.PSATTN_KV_BF16, U * n)
-    # weak scaling: requests_per_gpu x N requests in total, each rank owns its own (no collective)
-    unit_ids = shard.unit_ids(shard.shard_requests(args.requests * ws, ws, rank), args.layers, args.hkv)
-    assert unit_ids.size == U
     t0 = time.time()
     synth.fill(pool, p, unit_ids, np.arange(U, dtype=np.int64) * n, np.full(U, args.ctx, np.int64))
     torch.cuda.synchronize()
@@ -352,11 +401,14 @@ def run_ours(args):
     ms = e0.elapsed_time(e1)
     # per-stage kernel times: the same steps launched directly with CUDA events between the stages
     capi.lib.psattn_profile_read(None, None, 1)
+    sstats = np.zeros(4, np.uint64)
+    capi.lib.psattn_debug_stream_stats(sstats.ctypes.data)  # zero the stream kernel's fetch counters
     capi.lib.psattn_profile_enable(1)
     for _ in range(args.steps):
         run.run()
     torch.cuda.synchronize()
     capi.lib.psattn_profile_enable(0)
+    capi.lib.psattn_debug_stream_stats(sstats.ctypes.data)
     stage_ms = np.zeros(4, np.float64)
     stage_n = np.zeros(4, np.int64)
     capi.lib.psattn_profile_read(stage_ms.ctypes.data, stage_n.ctypes.data, 1)
@@ -372,7 +424,7 @@ def run_ours(args):
                           "warp0_v_work": round(float(phases[11]) / tot, 4)}), file=sys.stderr)
     ms = shard.max_over_ranks(ms, dev)
     ms_per_step = ms / args.steps
-    value = nq * ws * args.steps / (ms / 1e3)
+    value = nq_all * args.steps / (ms / 1e3)
 
     # ---- algorithmic bytes ----
     un = run.union_blocks().cpu().numpy()
@@ -385,6 +437,15 @@ def run_ours(args):
     qo_b = 2 * nq * args.dim * 4
     step_bytes = meta_b + kv_union_b + qo_b
     kv_full_b = U * n * lay.slot_bytes
+    # physical K/V tiles the stream kernel fetched vs the algorithmic union (bounded speculation)
+    fetch = None
+    if int(sstats[3]) > 0:
+        kt, vt = float(sstats[0]) / args.steps, float(sstats[1]) / args.steps
+        tile_b = lay.slot_bytes / 2
+        fetch = dict(k_tiles_per_step=kt, v_tiles_per_step=vt, union_blocks_per_step=float(un.sum()),
+                     fetched_bytes_per_step=(kt + vt) * tile_b, kv_union_bytes=kv_union_b,
+                     waste_frac=(kt + vt) * tile_b / max(kv_union_b, 1) - 1.0,
+                     rounds_per_unit=float(sstats[2]) / max(float(sstats[3]), 1.0))
     stage_names = ["oracle", "score", "order", "progressive"]
     per_launch_ms = {s: stage_ms[i] / max(stage_n[i], 1) for i, s in enumerate(stage_names) if stage_n[i] > 0}
     stage_bytes = {"score": meta_b + nq * args.dim * 4, "progressive": kv_union_b + qo_b,
@@ -424,7 +485,7 @@ def run_ours(args):
         stream.synchronize()  # the caller consumes each step's outputs on the host
     e2e_s = time.perf_counter() - t0
     e2e_s = shard.max_over_ranks(e2e_s, dev)
-    e2e_val = nq * ws * args.steps / e2e_s
+    e2e_val = nq_all * args.steps / e2e_s
 
     # ---- optional final output gather over NCCL (N > 1; not part of `value`) ----
     gather = None
@@ -441,7 +502,12 @@ def run_ours(args):
         torch.cuda.synchronize()
         gms = shard.max_over_ranks(g0.elapsed_time(g1) / args.steps, dev)
         gather = dict(ms_per_step=gms, bytes_per_step=int(allout.numel()) * 4, collective="all_gather (NCCL)",
-                      value_with_gather=nq * ws / ((ms_per_step + gms) / 1e3))
+                      value_with_gather=nq_all / ((ms_per_step + gms) / 1e3))
+
+    # ---- parity of the benchmarked step itself (after timing; the checker is the reference) ----
+    parity = None
+    if args.check > 0:
+        parity = check_step(args, p, run, q_host, unit_ids, n, g)  # every rank checks a sample of its own units
 
     # ---- CPU baseline (rank 0, N=1 only) ----
     cpu_base = None
@@ -453,24 +519,45 @@ def run_ours(args):
         except Exception as e:  # noqa: BLE001
             cpu_base = dict(value=None, unit=UNIT, cores=0, kind="reference", sample=f"unavailable: {e}")
 
+    # ---- every rank's view (device, units, parity of its own sample) gathered on rank 0 ----
+    me = dict(rank=rank, device=torch.cuda.get_device_name(dev), units=U, queries=nq, parity_ok=(parity or {}).get("ok"))
+    ranks = [me]
+    if ws > 1:
+        ranks = [None] * ws
+        dist.all_gather_object(ranks, me)
+        if parity is not None:
+            allp = [None] * ws
+            dist.all_gather_object(allp, parity)
+            parity = dict(ok=all(x.get("ok") for x in allp) if all(x.get("ok") is not None for x in allp) else None,
+                          units=sum(x.get("units", 0) for x in allp), queries=sum(x.get("queries", 0) for x in allp),
+                          exact=sum(x.get("exact", 0) for x in allp), tie=sum(x.get("tie", 0) for x in allp),
+                          per_rank=allp)
     if rank == 0:
+        if strong:
+            wl = (f"config5: {total_req} concurrent 128K-context decodes (Llama-3.1-8B shape) over {ws} GPU(s), "
+                  f"{layers_resident} of {args.layers} layers resident per step, eps {args.eps}")
+        else:
+            wl = "config2: Llama-3.1-8B shape, 32 layers, batch 8 decode, 128K ctx, eps 0.95"
         line = dict(
             metric=METRIC, value=value, unit=UNIT, n_gpus=ws, steps=args.steps, warmup=args.warmup,
-            ms_per_step=ms_per_step, higher_is_better=True, scaling="weak", vs_baseline=None, dtype="bf16",
+            ms_per_step=ms_per_step, higher_is_better=True, scaling="strong" if strong else "weak",
+            vs_baseline=None, dtype="bf16",
             data=f"synthetic ({args.dist} keys, seekable generator, seed {args.seed})",
-            config=dict(workload="config2: Llama-3.1-8B shape, 32 layers, batch 8 decode, 128K ctx, eps 0.95",
-                        requests_per_gpu=args.requests, layers=args.layers, ctx=args.ctx, hq=args.hq,
+            config=dict(workload=wl, requests_total=total_req, requests_per_gpu=None if strong else args.requests,
+                        layers=args.layers, layers_resident=layers_resident, ctx=args.ctx, hq=args.hq,
                         hkv=args.hkv, dim=args.dim, block=args.block, eps=args.eps, microbatch=args.microbatch,
-                        queries_per_step=nq * ws, kv_dtype="bf16", l2="inputs (~144 GiB/GPU) >> 126 MB L2; no flush",
-                        parallelism=f"request sharding x{ws}, no collective"),
+                        queries_per_step=nq_all, kv_dtype="bf16", l2="inputs (~144 GiB/GPU) >> 126 MB L2; no flush",
+                        parallelism=(f"request sharding x{ws}" if total_req >= ws else f"(request, kv head) sharding x{ws}")
+                        + ", no collective on the data path"),
+            world=dict(size=ws, backend="nccl" if ws > 1 else None, ranks=ranks),
             roofline=roofline,
-            step_roofline=dict(achieved=step_gbs, peak=peak, frac=step_gbs / peak, unit="GB/s",
+            step_roofline=dict(per_gpu="rank 0", achieved=step_gbs, peak=peak, frac=step_gbs / peak, unit="GB/s",
                                bytes_per_step=step_bytes, meta_bytes=meta_b, kv_union_bytes=kv_union_b,
                                qo_bytes=qo_b),
             kv_fraction_read=kv_union_b / kv_full_b, kv_fraction_per_head_sum=kv_sum_b / (kv_full_b * g),
-            mean_blocks_processed=float(bp.mean()),
+            mean_blocks_processed=float(bp.mean()), fetch=fetch,
             stage_ms_per_step={k: v for k, v in per_launch_ms.items()},
-            cpu_baseline=cpu_base,
+            cpu_baseline=cpu_base, parity=parity, parity_ok=(parity or {}).get("ok"),
             e2e=dict(value=e2e_val, unit=UNIT, h2d_bytes_per_step=h2d, d2h_bytes_per_step=d2h),
             gpu_launches=int(launches_per_step) * args.steps,
             cuda_graph=bool(args.graph), gather=gather,
@@ -481,9 +568,51 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def run_plan_only(args):
+    """What each rank would own, gathered over gloo on the host (tests the N-rank launch on CPU)."""
+    import torch.distributed as dist
+    from paper_2503_00392_b200 import shard
+    ws, rank, _ = dist_env()
+    if ws > 1:
+        dist.init_process_group("gloo")
+    total_req = args.total_requests if args.total_requests > 0 else args.requests * ws
+    units = shard.plan_units(total_req, args.layers, args.hkv, ws, rank)
+    me = dict(rank=rank, pid=os.getpid(), units=units.tolist())
+    ranks = [me]
+    if ws > 1:
+        ranks = [None] * ws
+        dist.all_gather_object(ranks, me)
+    if rank == 0:
+        print(json.dumps(dict(plan_only=True, n_gpus=args.gpus, world_size=ws, requests_total=total_req,
+                              ranks=ranks)), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+def relaunch_multi_gpu(args):
+    """`--gpus N` outside torchrun: start N ranks (one process per GPU) under torch.distributed.run
+    on 127.0.0.1 with this same command line and return their exit code."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.run(cmd).returncode
+
+
 def main():
     args = parse()
-    if args.impl == "reference":
+    ws = int(os.environ.get("WORLD_SIZE", "0"))
+    if (args.impl == "ours" or args.plan_only) and args.gpus > 1 and ws == 0:
+        sys.exit(relaunch_multi_gpu(args))
+    if ws and ws != args.gpus:
+        print(json.dumps(dict(metric=METRIC, error=f"--gpus {args.gpus} but WORLD_SIZE {ws}")), flush=True)
+        sys.exit(2)
+    if args.plan_only:
+        run_plan_only(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)

@@ -166,11 +166,25 @@ int psattn_batch_union_blocks(const psattn_batch* b, void* workspace, int64_t* o
 /* Number of kernels the last psattn_run_batch launched on this process. */
 int psattn_batch_last_launches(int32_t* out_count);
 
-/* Progressive-kernel selection (tuning/testing knob): 0 = auto (the GQA-group
- * kernel — one CTA per kv-head list, K/V of the group's union read once, tensor-core
- * K pass — when 2 <= group <= 4, dim in {64,128} and blocks <= 16 tokens; else one
- * CTA per q-head), 1 = always per q-head, 2 = GQA kernel whenever supported. */
+/* Progressive-kernel selection (tuning/testing knob): 0 = auto (the warp-specialised
+ * stream kernel on the production shape — bf16 HBM pool, dim 128, 16-token blocks,
+ * 2 <= group <= 4, dense hand-over on; else the GQA round kernel — one CTA per kv-head
+ * list, K/V of the group's union read once — when 2 <= group <= 4, dim in {64,128} and
+ * blocks <= 16 tokens; else one CTA per q-head), 1 = always per q-head, 2 = GQA round
+ * kernel whenever supported, 3 = stream kernel whenever supported. */
 int psattn_set_progressive_kernel(int32_t mode);
+/* Benchmark instrumentation of the stream kernel: K tiles fetched, V tiles fetched,
+ * rounds decided and units run since the last call (device counters; reading zeroes
+ * them). Returns 0, or -1 on a CUDA error. */
+int psattn_debug_stream_stats(unsigned long long* out4);
+/* Development builds (make PROF=1) only: SM cycles per phase of the GQA round kernel
+ * (init, order, union, K pass, decide, V pass, advance, finalize, rounds, 3 warp-0
+ * counters); reading zeroes them. -1 in normal builds. */
+int psattn_debug_gqa_phases(unsigned long long* out12);
+/* Development builds (make STREAM_DEBUG=1) only: attaches a mapped host buffer that collects
+ * stuck-wait records of the stream kernel (int[16 + 16*256]: count, then 16-int records) and
+ * returns it; nullptr in normal builds. */
+int* psattn_debug_stream_attach(void);
 /* Score/progressive overlap: psattn_run_batch splits a batch of >= 512 units into
  * sub-batches and runs score(i+1) on the caller's stream while progressive(i) runs on
  * an internal stream joined back by events (stream-ordered, no host sync).

@@ -1,5 +1,6 @@
 // device.cu — the device layer behind psattn_b200.h: HBM block pool, batched
 // launch and workspace carving.
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <string.h>
@@ -21,6 +22,8 @@ struct psattn_pool {
     // two-tier pools only (psattn_tier): pinned host backing tier + HBM location table
     char* host_kv = nullptr;
     int32_t* loc = nullptr;
+    // 2-D TMA descriptor of the K/V slots (rows of d bf16, 2T rows per slot) for the stream kernel
+    CUtensorMap kv_tmap;
 };
 
 namespace psa {
@@ -66,6 +69,38 @@ static int64_t meta_bytes_for(int d, int dtype) {
 
 const PoolView& pool_view(const psattn_pool* p) { return p->v; }
 
+// The stream kernel (kernels_stream.cu) loads K / V tiles with 2-D TMA: the pool's K/V array
+// viewed as rows of 128 bf16 (256 B), 32 rows per slot (16 K rows, then 16 V rows); boxes of
+// 64 dims x 16 rows with the 128-byte swizzle. Built for the production layout only (bf16,
+// d = 128, 16-token slots); rebuilt whenever the pool's storage moves (pool_grow).
+static void build_kv_tmap(psattn_pool* pool) {
+    PoolView& v = pool->v;
+    v.kv_tmap = nullptr;
+    if (v.dtype != PSATTN_KV_BF16 || v.d != 128 || v.T != 16 || v.n_slots <= 0 || v.slot_bytes != 2 * 16 * 128 * 2)
+        return;
+    using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    static EncodeFn fn = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return static_cast<EncodeFn>(nullptr);
+        return reinterpret_cast<EncodeFn>(f);
+    }();
+    if (!fn || (uint64_t)v.n_slots * 32 > 0xFFFFFFFFull) return;
+    const cuuint64_t dims[2] = {128, (cuuint64_t)v.n_slots * 32};
+    const cuuint64_t strides[1] = {256};
+    const cuuint32_t box[2] = {64, 16};
+    const cuuint32_t es[2] = {1, 1};
+    if (fn(&pool->kv_tmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, v.kv, dims, strides, box, es,
+           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return;
+    v.kv_tmap = &pool->kv_tmap;
+}
+
 int pool_grow(psattn_pool* pool, int64_t n_slots, int32_t T) {
     PoolView& v = pool->v;
     if (n_slots < v.n_slots) n_slots = v.n_slots;
@@ -106,6 +141,7 @@ int pool_grow(psattn_pool* pool, int64_t n_slots, int32_t T) {
     v = nv;
     pool->desc.block_tokens = T;
     pool->desc.n_slots = n_slots;
+    build_kv_tmap(pool);
     return PSATTN_OK;
 }
 
@@ -264,7 +300,7 @@ int read_meta(const psattn_pool* pool, int64_t slot, float* mean, float* lo, flo
 
 // ---- workspace carving ----
 struct WsLayout {
-    size_t keys, rpos, omass, kmm, dflag, dla, dp, dthr, dpart, ft, total;
+    size_t keys, rpos, omass, kmm, dflag, dla, dp, dthr, dpart, ft, sw, total;
 };
 
 static WsLayout ws_layout(const psattn_batch* b) {
@@ -293,6 +329,9 @@ static WsLayout ws_layout(const psattn_batch* b) {
         o += align_up((size_t)b->n_units * b->group * 8, 256);
         l.dpart = o;
         o += align_up((size_t)b->n_units * b->group * ((b->max_blocks + kDenseSlice - 1) / kDenseSlice) * kDensePart * 4, 256);
+        // stream kernel: token weights of every fetched block, [unit][kStreamEnt][4 heads][16] fp32
+        l.sw = o;
+        o += align_up((size_t)b->n_units * kStreamEnt * 4 * 16 * 4, 256);
     }
     // first tranche of every head (GQA shapes): keys | slots | ntok | count
     l.ft = 0;
@@ -369,6 +408,7 @@ BatchView make_view(const psattn_pool* pool, const psattn_batch* b, void* worksp
     v.dense_p = l.dflag ? reinterpret_cast<float*>(ws + l.dp) : nullptr;
     v.dense_thr = l.dflag ? reinterpret_cast<unsigned long long*>(ws + l.dthr) : nullptr;
     v.dense_part = l.dflag ? reinterpret_cast<float*>(ws + l.dpart) : nullptr;
+    v.stream_w = l.sw ? reinterpret_cast<float*>(ws + l.sw) : nullptr;
     if (l.ft) {
         const size_t hq = (size_t)b->n_units * b->group;
         char* f = ws + l.ft;
@@ -542,7 +582,7 @@ int psattn_rank_batch(psattn_pool* pool, const psattn_batch* b, void* workspace,
 }
 
 int psattn_set_progressive_kernel(int32_t mode) {
-    if (mode < 0 || mode > 2) return fail(PSATTN_ERR_INVALID_ARGUMENT, "progressive kernel mode must be 0, 1 or 2");
+    if (mode < 0 || mode > 3) return fail(PSATTN_ERR_INVALID_ARGUMENT, "progressive kernel mode must be 0, 1, 2 or 3");
     set_psa_kernel_choice(mode);
     return PSATTN_OK;
 }

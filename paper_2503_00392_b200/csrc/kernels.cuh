@@ -27,6 +27,9 @@ struct PoolView {
     // PCIe/C2C). loc == nullptr: the plain HBM pool, K/V of slot s at kv + s*slot_bytes.
     const int32_t* loc;
     const char* host_kv;
+    // Host pointer to the pool's CUtensorMap (2-D view of the K/V rows) or nullptr; passed by
+    // value to the stream kernel as a __grid_constant__ parameter, never read on the device.
+    const void* kv_tmap;
 };
 
 #ifdef __CUDACC__
@@ -84,8 +87,12 @@ struct BatchView {
     int32_t* ft_slot;
     uint8_t* ft_ntok;
     int32_t* ft_count;
+    // stream kernel (kernels_stream.cu): token weights of every fetched block of a unit,
+    // [n_units][kStreamEnt][4][16] fp32, bulk-copied back beside the block's V tile
+    float* stream_w;
 };
-constexpr int kFirstCap = 512;  // == the GQA kernel's tranche capacity
+constexpr int kFirstCap = 512;   // == the GQA kernel's tranche capacity
+constexpr int kStreamEnt = 512;  // distinct blocks one unit may fetch on the stream kernel (else hand-over)
 constexpr int64_t kDenseMaxBlocks = 16384;  // decide smem: 12 B per rank (196 KB)
 constexpr int64_t kDenseHandover = 384;     // ranks a head consumes on the round kernel before the hand-over
 constexpr int64_t kDenseSlice = 512;        // list positions per dense K / V work item
@@ -104,8 +111,12 @@ cudaError_t launch_scatter(const PoolView& p, const void* staged, const int32_t*
                            int64_t n, cudaStream_t st);
 int launch_psa(const PoolView& p, const BatchView& b, cudaStream_t st);  // returns kernels launched
 bool gqa_supported(const PoolView& p, const BatchView& b);
+bool stream_supported(const PoolView& p, const BatchView& b);
+void launch_stream(const PoolView& p, const BatchView& b, cudaStream_t st);  // kernels_stream.cu
 int launch_gqa(const PoolView& p, const BatchView& b, cudaStream_t st);  // returns kernels launched
-// 0 = auto (GQA kernel when supported), 1 = per-query kernel, 2 = GQA kernel
+// 0 = auto (stream kernel, else the GQA round kernel where supported), 1 = per-query kernel,
+// 2 = GQA round kernel, 3 = stream kernel (kernels_stream.cu) where supported
+int psa_kernel_choice();
 void set_psa_kernel_choice(int choice);
 void set_score_kernel_choice(int choice);
 void set_pipeline_subbatches(int k);

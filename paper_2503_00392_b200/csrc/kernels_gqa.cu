@@ -675,6 +675,10 @@ int launch_gqa(const PoolView& p, const BatchView& b, cudaStream_t st) {
 #endif
     if (b.ft_keys) first_tranche_kernel<<<b.n_units * b.g, PSA_FT_THREADS, 0, st>>>(p, b);
     const int launches = b.ft_keys ? 2 : 1;
+    if (psa_kernel_choice() != 2 && stream_supported(p, b)) {  // the production shape
+        launch_stream(p, b, st);
+        return launches;
+    }
     if (p.dtype == 0) {
         if (G == 2) launch_gqa_g<float, 2>(p, b, st);
         else launch_gqa_g<float, 4>(p, b, st);

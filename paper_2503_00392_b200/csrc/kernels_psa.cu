@@ -370,6 +370,7 @@ static void launch_psa_t(const PoolView& p, const BatchView& b, int nq, cudaStre
 
 static int g_psa_choice = 0;
 void set_psa_kernel_choice(int choice) { g_psa_choice = choice; }
+int psa_kernel_choice() { return g_psa_choice; }
 
 static int g_dense_mode = 0;
 void set_dense_mode(int mode) { g_dense_mode = mode; }

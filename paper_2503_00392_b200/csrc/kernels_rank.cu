@@ -143,15 +143,18 @@ __device__ __forceinline__ double smem_reduce16_cm(double (&acc)[16], double* re
     __syncwarp();
     const int v = lane & 15, part = lane >> 4;
     const uint32_t a0 = smem_u32(red) + (uint32_t)(v * 256 + part * 128 + v * 8);
-    double t = 0.0;
+    double x[16];
 #pragma unroll
-    for (int k = 0; k < 16; ++k) {
-        double x;
-        asm volatile("ld.shared.f64 %0, [%1];" : "=d"(x) : "r"(a0 ^ (uint32_t)(8 * k)));
-        t += x;
-    }
-    t += __shfl_xor_sync(PSA_FULL, t, 16);
-    return t;
+    for (int k = 0; k < 16; ++k) asm volatile("ld.shared.f64 %0, [%1];" : "=d"(x[k]) : "r"(a0 ^ (uint32_t)(8 * k)));
+    // x[k] is the partial of lane 16*part + (k ^ v). A balanced pairwise tree pairs indices that
+    // differ in one bit, level by level, so it is invariant under the XOR permutation by v: every
+    // value v sums its 16 partials with the same bracketing, and equal metadata records give
+    // bit-equal scores wherever they sit in a group (exact ties then fall to the block-id rule).
+#pragma unroll
+    for (int w = 1; w < 16; w <<= 1)
+#pragma unroll
+        for (int k = 0; k < 16; k += 2 * w) x[k] += x[k + w];
+    return x[0] + __shfl_xor_sync(PSA_FULL, x[0], 16);
 }
 
 __device__ __forceinline__ double smem_reduce16_swz(double (&acc)[16], double* red, int lane) {

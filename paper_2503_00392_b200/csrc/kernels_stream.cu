@@ -1,0 +1,787 @@
+// kernels_stream.cu — progressive attention of one GQA group as a warp-specialised stream
+// (sm_100a): TMA tensor loads of K/V tiles into shared-memory rings, mbarrier hand-offs,
+// tensor-core K and V passes, a per-round fp64 coverage decide.
+//
+// Replaces the round kernel (kernels_gqa.cu) on the production shape: bf16 pool, d = 128,
+// 16-token blocks, GQA group of 2..4, HBM-resident pool. Same semantics (reference
+// engine.cpp:92-147 per head, psa_attention_multi_head engine.cpp:240-260 for the group):
+// every head keeps its own ranking and stop point; a block ranked by several heads in the
+// same round is read once.
+//
+// One CTA per (request, layer, kv-head) unit, 8 warps with fixed roles:
+//   warp 0    PRODUCER  round r = the live heads' ranks [rC, rC+C) (C = 32 / G); a block is an
+//                       ENTRY the first time any head's round reaches it (unit-wide dedup: a
+//                       hash of list positions in shared memory), so its K tile is fetched once
+//                       (two 2-D TMA boxes of 64 dims x 16 tokens, 128-byte swizzle) into the K
+//                       ring, at most kLook rounds ahead of the last decided round; V tiles are
+//                       fetched for the blocks the decider releases, each once, together with the
+//                       block's token weights (1-D bulk copy) into the V ring;
+//   warp 1    DECIDER   per round, one warp-wide segmented scan (C lanes per head) of the
+//                       block masses in each head's rank order: CoverageEstimator::observe + the
+//                       estimate at microbatch boundaries (engine.cpp:38-55, 109-125) in fp64,
+//                       the first boundary with est > eps stops the head. A block is released to
+//                       the V pass once every head has decided it (committed it, or stopped
+//                       before reaching it);
+//   warps 2-4 SCORERS   K pass: ldmatrix of the swizzled K tile, mma.sync bf16 with the
+//                       query split into 3 exact bf16 terms (all heads of the group in the
+//                       N dimension); per (block, head) max / exp-sum kept in shared memory for
+//                       the whole unit, token weights written to a global scratch row;
+//   warps 5-7 V         V pass: ldmatrix.trans of the V tile, mma.sync with the weights split
+//                       into 3 exact bf16 terms (fp32-exact weights), online-softmax merge of the
+//                       block into every head that committed it (merge_partial,
+//                       attention.hpp:83-102); at the end the three warps' states merge
+//                       (finalize, attention.hpp:104-110).
+// Bytes: every block of the heads' union is fetched exactly once (K and V); speculation is
+// K-only and bounded by kLook rounds; blocks no head commits are never V-fetched. Counters of
+// fetched K / V tiles feed the benchmark's waste figure.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <float.h>
+#include <math.h>
+#include <stdint.h>
+#include <string.h>
+
+#include "common.cuh"
+#include "kernels.cuh"
+#include "mma.cuh"
+
+namespace psa {
+
+__device__ unsigned long long g_stream_stats[4];  // K tiles, V tiles, rounds, units (accumulating)
+// Development builds (make STREAM_DEBUG=1): a wait that does not complete within ~2^22 polls
+// writes the stuck warp's state into mapped host memory (readable after the trap) and traps.
+__device__ int* g_stream_dbg = nullptr;
+
+namespace stream {
+
+constexpr int kThreads = 256;
+constexpr int kNS = 3, kNV = 3;          // scorer / V warps
+constexpr int kWS0 = 2, kWV0 = 2 + kNS;  // first scorer / V warp
+#ifndef PSA_STREAM_RK
+#define PSA_STREAM_RK 9
+#endif
+#ifndef PSA_STREAM_RV
+#define PSA_STREAM_RV 9
+#endif
+#ifndef PSA_STREAM_LOOK
+#define PSA_STREAM_LOOK 2
+#endif
+constexpr int kRK = PSA_STREAM_RK;  // K ring stages (4 KB K tile)
+constexpr int kRV = PSA_STREAM_RV;  // V ring stages (4 KB V tile + the block's token weights)
+constexpr int kLR = 8;              // round slots in flight
+constexpr int kENT = kStreamEnt;    // distinct blocks per unit
+constexpr int kHash = 2 * kENT;     // list position -> entry (open addressing)
+constexpr int kLook = PSA_STREAM_LOOK;
+static_assert(kLook + 2 <= kLR, "round slots must cover the lookahead");
+// Entry e is consumed by scorer e % kNS from K stage e % kRK (V item j: V warp j % kNV, stage
+// j % kRV). With the ring a multiple of the consumer count, a stage's previous use belongs to
+// the SAME consumer, which has already waited on it: a full-barrier wait can never pass on the
+// parity of a stale phase (two uses back) while another consumer's load is still in flight.
+static_assert(kRK % kNS == 0 && kRV % kNV == 0, "each consumer warp owns its ring stages");
+
+template <int G>
+struct Smem {
+    alignas(1024) unsigned char kring[kRK][4096];
+    alignas(1024) unsigned char vring[kRV][4096];
+    alignas(16) float vw[kRV][G][16];  // token weights beside each V tile
+    float em[kENT][G];                 // block max per (entry, head)
+    float el[kENT][G];                 // block exp-sum
+    int32_t eslot[kENT];
+    int32_t epos[kENT];
+    uint32_t vmask[kENT];  // heads that committed the entry (decider)
+    uint8_t entok[kENT];
+    uint8_t queued[kENT];
+    int32_t hkey[kHash];
+    int16_t hval[kHash];
+    int16_t r_map[kLR][32];  // (head, rank-in-round) lane -> entry, -1 none
+    int32_t r_e0[kLR], r_cnt[kLR], r_flag[kLR];
+    int32_t r_live[kLR], r_vc[kLR], r_stop[kLR];  // decider -> producer, per decided round
+    int16_t vq[kENT + kNV];  // V items in creation order (entry), -1 = end
+    int32_t handover;
+    int32_t dbg_flag;
+    float mpart[kNV][G], lpart[kNV][G];
+    uint64_t kfull[kRK], kempty[kRK], vfull[kRV], vempty[kRV];
+    uint64_t rpub[kLR], rscored[kLR], rdec[kLR];
+};
+
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t phase) {
+    uint32_t ok;
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n"
+        "}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(phase)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// 2-D tiled TMA load (box 64 dims x 16 tokens, 128-byte swizzle) completing on `bar`.
+__device__ __forceinline__ void tma_tile(uint32_t dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void ldsm4(uint32_t addr, uint32_t& a0, uint32_t& a1, uint32_t& a2, uint32_t& a3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(a0), "=r"(a1), "=r"(a2), "=r"(a3)
+                 : "r"(addr));
+}
+__device__ __forceinline__ void ldsm4t(uint32_t addr, uint32_t& a0, uint32_t& a1, uint32_t& a2, uint32_t& a3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(a0), "=r"(a1), "=r"(a2), "=r"(a3)
+                 : "r"(addr));
+}
+// Byte address of the 16-byte chunk c (0..15, 8 dims each) of token row r (0..15) in a tile
+// loaded as two 64-dim boxes with the 128-byte swizzle (chunk index XOR row % 8).
+__device__ __forceinline__ uint32_t swz(uint32_t base, int r, int c) {
+    return base + (uint32_t)((c >> 3) * 2048 + r * 128 + (((c & 7) ^ (r & 7)) << 4));
+}
+// Term `part` (0..2) of the exact 3-term bf16 split of a and b, packed (a low); part 3 -> 0.
+__device__ __forceinline__ uint32_t pack_split3(float a, float b, int part) {
+    if (part >= 3) return 0u;
+    uint32_t p = pack_bf16x2(a, b);
+    for (int i = 0; i < part; ++i) {
+        a -= __uint_as_float(p << 16);
+        b -= __uint_as_float(p & 0xFFFF0000u);
+        p = pack_bf16x2(a, b);
+    }
+    return p;
+}
+
+#ifdef PSA_STREAM_DEBUG
+__device__ __noinline__ void dbg_stuck(int site, int a0, int a1, int a2, int a3, int a4, int a5, int a6, int a7) {
+    int* d = g_stream_dbg;
+    if (d) {
+        const int k = atomicAdd(d, 1);
+        if (k < 256) {
+            int* r = d + 16 + 16 * k;
+            const int v[12] = {(int)blockIdx.x, (int)(threadIdx.x >> 5), (int)(threadIdx.x & 31), site, a0, a1, a2, a3,
+                               a4, a5, a6, a7};
+            for (int i = 0; i < 12; ++i) ((volatile int*)r)[i] = v[i];
+            __threadfence_system();
+        }
+    }
+    __trap();
+}
+__device__ __noinline__ void dbg_note(int site, int a0, int a1, int a2, int a3, int a4, int a5, int a6, int a7) {
+    int* d = g_stream_dbg;
+    if (d) {
+        const int k = atomicAdd(d, 1);
+        if (k < 256) {
+            int* r = d + 16 + 16 * k;
+            const int v[12] = {(int)blockIdx.x, (int)(threadIdx.x >> 5), (int)(threadIdx.x & 31), site, a0, a1, a2, a3,
+                               a4, a5, a6, a7};
+            for (int i = 0; i < 12; ++i) ((volatile int*)r)[i] = v[i];
+            __threadfence_system();
+        }
+    }
+}
+// waits; when the producer flags a stall, a waiting lane 0 writes where it waits (once)
+#define SWAIT(bar, ph, site, a0, a1, a2, a3, a4, a5, a6, a7)                                            \
+    do {                                                                                               \
+        bool noted_ = false;                                                                           \
+        for (uint32_t it_ = 0; !mbar_try_wait((bar), (ph)); ++it_) {                                   \
+            if (!noted_ && (it_ & 255) == 0 && *(volatile int*)&s.dbg_flag && (threadIdx.x & 31) == 0) { \
+                noted_ = true;                                                                         \
+                dbg_note((site), (a0), (a1), (a2), (a3), (int)(ph), (int)*(volatile uint32_t*)(bar),     \
+                         (int)(*(volatile uint64_t*)(bar) >> 32), (a7));                               \
+            }                                                                                          \
+        }                                                                                              \
+    } while (0)
+#else
+#define SWAIT(bar, ph, site, a0, a1, a2, a3, a4, a5, a6, a7) mbar_wait((bar), (ph))
+#endif
+
+template <int G>
+__global__ void __launch_bounds__(kThreads, 2) psa_stream_kernel(const __grid_constant__ CUtensorMap kvmap,
+                                                                PoolView p, BatchView b) {
+    constexpr int C = 32 / G;  // ranks per head per round
+    constexpr int NT = G / 2;  // n8 tiles (4 columns per head: 3 split terms + 0)
+    constexpr uint32_t kWB = G * 16 * 4;  // weight bytes per entry
+    extern __shared__ unsigned char smem_raw[];
+    Smem<G>& s = *reinterpret_cast<Smem<G>*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int u = blockIdx.x;
+    const int g = b.g;
+    const int64_t off = b.list_off[u];
+    const int64_t n = b.list_off[u + 1] - off;
+    const int64_t limit = b.topk > 0 ? (b.topk < n ? b.topk : n) : n;
+    const int T2 = 2 * p.T;  // tensor-map rows per slot (K rows then V rows)
+    float* wg = b.stream_w + (size_t)u * kENT * 64;  // this unit's weights, 64 floats per entry
+
+    if (tid == 0) {
+        for (int i = 0; i < kRK; ++i) {
+            mbar_init(&s.kfull[i], 1);
+            mbar_init(&s.kempty[i], 1);
+        }
+        for (int i = 0; i < kRV; ++i) {
+            mbar_init(&s.vfull[i], 1);
+            mbar_init(&s.vempty[i], 1);
+        }
+        for (int i = 0; i < kLR; ++i) {
+            mbar_init(&s.rpub[i], 1);
+            mbar_init(&s.rscored[i], kNS);
+            mbar_init(&s.rdec[i], 1);
+        }
+        s.handover = 0;
+        s.dbg_flag = 0;
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    if (warp == 0) {
+        // ================================ PRODUCER ================================
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&kvmap)) : "memory");
+        for (int i = lane; i < kHash; i += 32) s.hkey[i] = -1;
+        __syncwarp();
+        const int h = lane / C, i = lane % C;
+        const bool hv = h < g;
+        const size_t qi = (size_t)u * g + (hv ? h : 0);
+        const int ftc = hv ? b.ft_count[qi] : 0;
+        const uint64_t pmask = (b.pos_bits >= 64) ? ~0ull : ((1ull << b.pos_bits) - 1ull);
+        int k_pub = 0, E = 0, k_issue = 0, v_seen = 0, v_issued = 0, decided = -1, lm = (1 << g) - 1;
+        bool stopped = false, closed = false;  // closed: no more rounds (entry table full)
+        auto fetch = [&](int k, int32_t& pos, int32_t& slot, int32_t& nt) {
+            const int64_t r = (int64_t)k * C + i;
+            if (hv && r < ftc && r < limit) {
+                pos = (int32_t)(b.ft_keys[qi * kFirstCap + r] & pmask);
+                slot = b.ft_slot[qi * kFirstCap + r];
+                nt = b.ft_ntok[qi * kFirstCap + r];
+            } else {
+                pos = -1;
+                slot = 0;
+                nt = 0;
+            }
+        };
+        int32_t fpos, fslot, fnt;
+        fetch(0, fpos, fslot, fnt);
+#ifdef PSA_STREAM_DEBUG
+        int idle = 0;
+#endif
+        for (;;) {
+            bool progress = false;
+            // (1) decisions, in round order
+            // (lane 0 tests, the warp follows: every lane must see the same decisions)
+            while (__shfl_sync(PSA_FULL, lane == 0 && decided + 1 < k_pub &&
+                                             mbar_test(&s.rdec[(decided + 1) % kLR], ((decided + 1) / kLR) & 1), 0)) {
+                ++decided;
+                const int rs = decided % kLR;  // values the decider published with this round
+                lm = s.r_live[rs];
+                v_seen = s.r_vc[rs];
+                if (s.r_stop[rs]) stopped = true;
+                progress = true;
+            }
+            // (2) publish the next round (speculative: heads live as of the last decided round)
+            if (!stopped && !closed && k_pub <= decided + kLook) {
+                const int rs = k_pub % kLR;
+                const bool valid = fpos >= 0 && ((lm >> h) & 1);
+                const unsigned peers = __match_any_sync(PSA_FULL, valid ? fpos : -1 - lane);
+                const int leader = __ffs(peers) - 1;
+                const bool lead = valid && leader == lane;
+                int hs = 0, ent = -1;
+                bool isnew = false;
+                if (lead) {  // unit-wide dedup: a block fetched in an earlier round is not fetched again
+                    hs = (int)(((uint32_t)fpos * 2654435761u) >> 21) & (kHash - 1);
+                    for (;;) {
+                        const int kk = s.hkey[hs];
+                        if (kk == fpos) {
+                            ent = s.hval[hs];
+                            break;
+                        }
+                        if (kk == -1) {
+                            const int old = atomicCAS(&s.hkey[hs], -1, fpos);
+                            if (old == -1) {
+                                isnew = true;
+                                break;
+                            }
+                            continue;  // another lane took the slot: look at it again
+                        }
+                        hs = (hs + 1) & (kHash - 1);
+                    }
+                }
+                const unsigned nb = __ballot_sync(PSA_FULL, isnew);
+                const int cnt = __popc(nb);
+                if (E + cnt > kENT) {
+                    // more distinct blocks than the entry table holds: the decider hands the unit
+                    // over (dense path) at this round; nothing more is published
+                    if (lane == 0) {
+                        s.r_e0[rs] = E;
+                        s.r_cnt[rs] = 0;
+                        s.r_flag[rs] = 1;
+                    }
+                    s.r_map[rs][lane] = -1;
+                    closed = true;
+                } else {
+                    if (isnew) {
+                        ent = E + __popc(nb & ((1u << lane) - 1u));
+                        s.hval[hs] = (int16_t)ent;
+                        s.eslot[ent] = fslot;
+                        s.epos[ent] = fpos;
+                        s.entok[ent] = (uint8_t)fnt;
+                        s.vmask[ent] = 0u;
+                        s.queued[ent] = 0;
+                    }
+                    const int myent = __shfl_sync(PSA_FULL, ent, leader);
+                    s.r_map[rs][lane] = (int16_t)(valid ? myent : -1);
+                    if (lane == 0) {
+                        s.r_e0[rs] = E;
+                        s.r_cnt[rs] = cnt;
+                        s.r_flag[rs] = 0;
+                    }
+                    E += cnt;
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&s.rpub[rs]);
+                ++k_pub;
+                if (!closed) fetch(k_pub, fpos, fslot, fnt);
+                progress = true;
+            }
+            // (3) K tiles of new entries, while K stages are free
+            {
+                const int e = k_issue + lane;
+                const bool ok = e < E && (e < kRK || mbar_test(&s.kempty[e % kRK], ((e / kRK) - 1) & 1));
+                const unsigned bal = __ballot_sync(PSA_FULL, ok);
+                const int pc = bal == PSA_FULL ? 32 : __ffs(~bal) - 1;
+                if (lane < pc) {
+                    const int st = e % kRK;
+                    const int y = s.eslot[e] * T2;
+                    mbar_arrive_expect_tx(&s.kfull[st], 4096);
+                    const uint32_t dst = smem_u32(s.kring[st]);
+                    tma_tile(dst, &kvmap, 0, y, &s.kfull[st]);
+                    tma_tile(dst + 2048, &kvmap, 64, y, &s.kfull[st]);
+                }
+                k_issue += pc;
+                progress |= pc > 0;
+            }
+            // (4) V tiles (+ the block's token weights) of ready items, while V stages are free
+            {
+                const int it = v_issued + lane;
+                const bool ok = it < v_seen && (it < kRV || mbar_test(&s.vempty[it % kRV], ((it / kRV) - 1) & 1));
+                const unsigned bal = __ballot_sync(PSA_FULL, ok);
+                const int pc = bal == PSA_FULL ? 32 : __ffs(~bal) - 1;
+                if (lane < pc) {
+                    const int st = it % kRV;
+                    const int e = s.vq[it];
+                    const int y = s.eslot[e] * T2 + p.T;
+                    mbar_arrive_expect_tx(&s.vfull[st], 4096 + kWB);
+                    const uint32_t dst = smem_u32(s.vring[st]);
+                    tma_tile(dst, &kvmap, 0, y, &s.vfull[st]);
+                    tma_tile(dst + 2048, &kvmap, 64, y, &s.vfull[st]);
+                    bulk_g2s(smem_u32(&s.vw[st][0][0]), wg + (size_t)e * 64, kWB, &s.vfull[st]);
+                }
+                v_issued += pc;
+                progress |= pc > 0;
+            }
+            // (5) done: every published K tile and every V item issued after the last decision
+            if (stopped && k_issue == E && v_issued == v_seen) {
+                const int rs = k_pub % kLR;  // sentinel round for the scorers
+                if (lane == 0) s.r_cnt[rs] = -1;
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&s.rpub[rs]);
+                if (lane < kNV) {  // one end item per V warp
+                    const int it = v_seen + lane;
+                    if (it >= kRV)
+                        SWAIT(&s.vempty[it % kRV], ((it / kRV) - 1) & 1, 1, it, v_seen, v_issued, E, k_issue, k_pub,
+                              decided, 0);
+                    s.vq[it] = -1;
+                    mbar_arrive(&s.vfull[it % kRV]);
+                }
+                break;
+            }
+            if (!progress) {
+                __nanosleep(64);
+#ifdef PSA_STREAM_DEBUG
+                if (++idle == (1 << 22)) {
+                    if (lane == 0) {
+                        const int st = k_issue % kRK;
+                        dbg_note(0, k_pub, E, k_issue, v_seen, v_issued, decided, (int)*(volatile uint32_t*)&s.kempty[st],
+                                 (int)(*(volatile uint64_t*)&s.kempty[st] >> 32));
+                        dbg_note(6, s.r_e0[0], s.r_e0[1], s.r_e0[2], s.r_e0[3], s.r_e0[4], s.r_e0[5], s.r_e0[6], s.r_e0[7]);
+                        dbg_note(7, s.r_cnt[0], s.r_cnt[1], s.r_cnt[2], s.r_cnt[3], s.r_cnt[4], s.r_cnt[5], s.r_cnt[6], s.r_cnt[7]);
+                        *(volatile int*)&s.dbg_flag = 1;
+                    }
+                }
+                if (idle > (1 << 22) + (1 << 16)) dbg_stuck(99, 0, 0, 0, 0, 0, 0, 0, 0);
+            } else {
+                idle = 0;
+#endif
+            }
+        }
+        if (lane == 0) {
+            atomicAdd(&g_stream_stats[0], (unsigned long long)E);
+            atomicAdd(&g_stream_stats[1], (unsigned long long)v_seen);
+            atomicAdd(&g_stream_stats[2], (unsigned long long)(decided + 1));
+            atomicAdd(&g_stream_stats[3], 1ull);
+        }
+    } else if (warp == 1) {
+        // ================================ DECIDER ================================
+        const int h = lane / C, i = lane % C;
+        const bool hv = h < g;
+        const int64_t qi = (int64_t)u * g + (hv ? h : 0);
+        const int64_t hb = off * g + (int64_t)(hv ? h : 0) * n;
+        const int ftc = hv ? b.ft_count[qi] : 0;
+        const double eps = b.topk > 0 ? 1.0 : b.eps;
+        const unsigned seg = (C == 32 ? PSA_FULL : ((1u << C) - 1u)) << (h * C);
+        const uint32_t all = (1u << g) - 1u;
+        bool live = hv;
+        int64_t cb = 0;
+        int vc = 0;  // V items created
+        double M = -INFINITY, S = 0.0, mn = INFINITY, est = 0.0;
+        for (int k = 0;; ++k) {
+            const int rs = k % kLR;
+            SWAIT(&s.rscored[rs], (k / kLR) & 1, 2, k, (int)cb, vc, (int)live, 0, 0, 0, 0);
+            const int e = s.r_map[rs][lane];
+            const int e_end = s.r_e0[rs] + s.r_cnt[rs];  // entries published up to this round
+            const bool overflow = s.r_flag[rs] == 1;
+            const int64_t r = cb + i;
+            const bool valid = live && e >= 0 && r < limit;
+            double x = -INFINITY;
+            if (valid) x = b.has_oracle ? b.omass[hb + s.epos[e]] : (double)(s.em[e][h] + logf(s.el[e][h]));
+            // segment (C lanes = one head) scan in fp64: running log-sum-exp carried as (max M, sum S)
+            double mx = x;
+#pragma unroll
+            for (int o = C / 2; o >= 1; o >>= 1) mx = fmax(mx, __shfl_xor_sync(PSA_FULL, mx, o));
+            mx = fmax(mx, M);
+            double ev = valid ? exp(x - mx) : 0.0;
+            double mnv = valid ? x : INFINITY;
+#pragma unroll
+            for (int o = 1; o < C; o <<= 1) {
+                const double ye = __shfl_up_sync(PSA_FULL, ev, o, C);
+                const double ym = __shfl_up_sync(PSA_FULL, mnv, o, C);
+                if (i >= o) {
+                    ev += ye;
+                    mnv = fmin(mnv, ym);
+                }
+            }
+            const double Si = (M == -INFINITY ? 0.0 : S * exp(M - mx)) + ev;  // sum exp(mass - mx) so far
+            const double mn_i = fmin(mnv, mn);
+            const int64_t nl = n - (r + 1);
+            const double est_i = nl == 0 ? 1.0 : (Si > 0.0 ? Si / fma((double)nl, exp(mn_i - mx), Si) : 0.0);
+            const bool boundary = valid && (b.m == 1 || ((r + 1) % b.m) == 0 || r + 1 == limit);
+            const bool stop = boundary && (est_i > eps || r + 1 == limit);
+            const unsigned sb = __ballot_sync(PSA_FULL, stop) & seg;
+            const unsigned vb = __ballot_sync(PSA_FULL, valid) & seg;
+            const int nvalid = __popc(vb);
+            const int f = sb ? (__ffs(sb) - 1 - h * C) : nvalid - 1;  // last committed lane of the head
+            const bool committed = valid && i <= f;
+            if (b.iest && boundary && i <= f) b.iest[hb + r] = est_i;  // IterationStats::estimated_coverage
+            if (committed) atomicOr(&s.vmask[e], 1u << h);
+            const int src = h * C + (f > 0 ? f : 0);
+            const double Sf = __shfl_sync(PSA_FULL, Si, src), mnf = __shfl_sync(PSA_FULL, mn_i, src);
+            const double estf = __shfl_sync(PSA_FULL, est_i, src);
+            if (nvalid > 0) {
+                M = mx;
+                S = Sf;
+                mn = mnf;
+                est = estf;
+                cb += f + 1;
+            }
+            const bool fin_now = live && sb != 0;
+            if (fin_now) {
+                live = false;
+                if (i == 0) {
+                    b.bp[qi] = cb;
+                    b.est[qi] = est;
+                    b.term[qi] = b.topk > 0 ? (limit < n) : (cb < n);
+                    if (b.tcov) {
+                        double tcv = -1.0;
+                        if (b.audit) {
+                            const double* om = b.omass + hb;
+                            double omx = -INFINITY;
+                            for (int64_t j = 0; j < n; ++j) omx = fmax(omx, om[j]);
+                            double sm = 0.0;
+                            for (int64_t j = 0; j < n; ++j) sm += exp(om[j] - omx);
+                            tcv = exp((M + log(S)) - (omx + log(sm)));
+                        }
+                        b.tcov[qi] = tcv;
+                    }
+                }
+            }
+            // a head that used up its first tranche (or kDenseHandover ranks), or a unit whose
+            // distinct blocks overflow the entry table, is handed over to the dense kernels
+            const bool ho = live && cb < limit && (cb >= kDenseHandover || cb >= ftc || overflow);
+            const bool anyho = __any_sync(PSA_FULL, ho);
+            const unsigned lb = __ballot_sync(PSA_FULL, live && i == 0);
+            uint32_t lmask = 0;
+#pragma unroll
+            for (int hh = 0; hh < G; ++hh) lmask |= ((lb >> (hh * C)) & 1u) << hh;
+            const bool done = anyho || lmask == 0;
+            __syncwarp();  // this round's vmask bits are visible to every lane
+            if (!anyho) {
+                // V items: a block goes to the V pass once every head has decided it (committed it,
+                // or stopped before reaching it), in a deterministic order
+                const uint32_t stopped = all & ~lmask;
+                const unsigned peers = __match_any_sync(PSA_FULL, committed ? e : -1 - lane);
+                const bool cand = committed && (__ffs(peers) - 1) == lane;
+                const bool ready = cand && ((s.vmask[e] | stopped) == all) && !s.queued[e];
+                const unsigned rb = __ballot_sync(PSA_FULL, ready);
+                if (ready) {
+                    s.vq[vc + __popc(rb & ((1u << lane) - 1u))] = (int16_t)e;
+                    s.queued[e] = 1;
+                }
+                vc += __popc(rb);
+                if (__any_sync(PSA_FULL, fin_now)) {  // a head stopped: blocks waiting only on it are ready
+                    __syncwarp();
+                    for (int e0 = 0; e0 < e_end; e0 += 32) {
+                        const int ee = e0 + lane;
+                        const bool rd = ee < e_end && s.vmask[ee] != 0u && !s.queued[ee] && ((s.vmask[ee] | stopped) == all);
+                        const unsigned b2 = __ballot_sync(PSA_FULL, rd);
+                        if (rd) {
+                            s.vq[vc + __popc(b2 & ((1u << lane) - 1u))] = (int16_t)ee;
+                            s.queued[ee] = 1;
+                        }
+                        vc += __popc(b2);
+                    }
+                }
+            }
+            if (lane == 0) {
+                s.r_vc[rs] = vc;
+                s.r_live[rs] = (int32_t)lmask;
+                s.r_stop[rs] = done;
+                if (done) {
+                    s.handover = anyho;
+                    if (anyho) b.dense_flag[atomicAdd(b.dense_count, 1)] = u;
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s.rdec[rs]);
+            if (done) break;
+        }
+    } else if (warp < kWV0) {
+        // ================================ SCORERS ================================
+        const int sidx = warp - kWS0;
+        const int gq = lane >> 2, tq = lane & 3;
+        const float fscale = (float)b.scale;
+        uint32_t qg[8][NT][2];  // B fragments: column (head 2t + gq/4, split gq%4), k = dims
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+            const int hq = 2 * t + (gq >> 2), sp = gq & 3;
+            const float* qrow = b.q + ((size_t)u * g + (hq < g ? hq : 0)) * 128;
+#pragma unroll
+            for (int st = 0; st < 8; ++st)
+#pragma unroll
+                for (int hf = 0; hf < 2; ++hf) {
+                    const int d0 = 16 * st + 8 * hf + 2 * tq;
+                    const float a = hq < g ? qrow[d0] : 0.0f, c = hq < g ? qrow[d0 + 1] : 0.0f;
+                    qg[st][t][hf] = pack_split3(a, c, sp);
+                }
+        }
+        for (int k = 0;; ++k) {
+            const int rs = k % kLR;
+            SWAIT(&s.rpub[rs], (k / kLR) & 1, 3, k, 0, 0, 0, 0, 0, 0, 0);
+            const int cnt = s.r_cnt[rs];
+            if (cnt < 0) break;
+            const int e0 = s.r_e0[rs];
+            for (int e = e0 + ((sidx - e0 % kNS) + kNS) % kNS; e < e0 + cnt; e += kNS) {
+                const int st = e % kRK;
+                SWAIT(&s.kfull[st], (e / kRK) & 1, 4, k, e, e0, cnt, 0, 0, 0, 0);
+                const uint32_t kb = smem_u32(s.kring[st]);
+                const int nt = s.entok[e];
+                float c[NT][4];
+#pragma unroll
+                for (int t = 0; t < NT; ++t) c[t][0] = c[t][1] = c[t][2] = c[t][3] = 0.0f;
+#pragma unroll
+                for (int kst = 0; kst < 8; ++kst) {
+                    uint32_t a0, a1, a2, a3;
+                    ldsm4(swz(kb, lane & 15, 2 * kst + (lane >> 4)), a0, a1, a2, a3);
+#pragma unroll
+                    for (int t = 0; t < NT; ++t)
+                        mma_bf16_16816(c[t][0], c[t][1], c[t][2], c[t][3], a0, a1, a2, a3, qg[kst][t][0],
+                                       qg[kst][t][1]);
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&s.kempty[st]);  // the tile is in registers: release it
+                float* we = wg + (size_t)e * 64;
+#pragma unroll
+                for (int t = 0; t < NT; ++t) {
+                    float lo = c[t][0] + c[t][1], hi = c[t][2] + c[t][3];
+                    lo += __shfl_xor_sync(PSA_FULL, lo, 1);  // the 4 split columns of (token, head)
+                    hi += __shfl_xor_sync(PSA_FULL, hi, 1);
+                    const int hq = 2 * t + (tq >> 1);
+                    lo = (gq < nt) ? lo * fscale : -INFINITY;
+                    hi = (gq + 8 < nt) ? hi * fscale : -INFINITY;
+                    float mbv = fmaxf(lo, hi);
+#pragma unroll
+                    for (int o = 4; o < 32; o <<= 1) mbv = fmaxf(mbv, __shfl_xor_sync(PSA_FULL, mbv, o));
+                    const float wlo = (gq < nt) ? expf(lo - mbv) : 0.0f;
+                    const float whi = (gq + 8 < nt) ? expf(hi - mbv) : 0.0f;
+                    float lbv = wlo + whi;
+#pragma unroll
+                    for (int o = 4; o < 32; o <<= 1) lbv += __shfl_xor_sync(PSA_FULL, lbv, o);
+                    if ((tq & 1) == 0) {
+                        we[hq * 16 + gq] = wlo;
+                        we[hq * 16 + gq + 8] = whi;
+                        if (gq == 0) {
+                            s.em[e][hq] = mbv;
+                            s.el[e][hq] = lbv;
+                        }
+                    }
+                }
+            }
+            // the weights are read back by the async proxy (bulk copy beside the V tile)
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s.rscored[rs]);
+        }
+    } else {
+        // ================================== V ==================================
+        const int vidx = warp - kWV0;
+        const int gq = lane >> 2, tq = lane & 3;
+        float O[NT][8], Mh[NT], Lh[NT];
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+            Mh[t] = -INFINITY;
+            Lh[t] = 0.0f;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) O[t][j] = 0.0f;
+        }
+        const int tok = (lane & 7) + ((lane >> 4) << 3);  // ldmatrix.trans row (token) of this lane
+        const int chi = (lane >> 3) & 1;                   // + dim chunk
+        for (int j = vidx;; j += kNV) {
+            const int st = j % kRV;
+            SWAIT(&s.vfull[st], (j / kRV) & 1, 5, j, 0, 0, 0, 0, 0, 0, 0);
+            const int e = s.vq[j];
+            if (e < 0) break;
+            const uint32_t mask = s.vmask[e];
+            const int nt = s.entok[e];
+            uint32_t bw[NT][2];
+#pragma unroll
+            for (int t = 0; t < NT; ++t) {
+                const int hq = 2 * t + (gq >> 2), sp = gq & 3;
+                const bool on = (mask >> hq) & 1u;
+                const float2 wl = on ? *reinterpret_cast<const float2*>(&s.vw[st][hq][2 * tq]) : make_float2(0.f, 0.f);
+                const float2 wh = on ? *reinterpret_cast<const float2*>(&s.vw[st][hq][2 * tq + 8]) : make_float2(0.f, 0.f);
+                bw[t][0] = pack_split3(wl.x, wl.y, sp);
+                bw[t][1] = pack_split3(wh.x, wh.y, sp);
+            }
+            const uint32_t vb = smem_u32(s.vring[st]);
+            float val[NT][8];
+#pragma unroll
+            for (int mt = 0; mt < 8; ++mt) {
+                uint32_t a0, a1, a2, a3;
+                ldsm4t(swz(vb, tok, 2 * mt + chi), a0, a1, a2, a3);
+                if (nt < 16) {  // rows past the block's tokens may hold stale data: zero them
+                    const uint32_t m0 = (2 * tq < nt ? 0x0000FFFFu : 0u) | (2 * tq + 1 < nt ? 0xFFFF0000u : 0u);
+                    const uint32_t m1 = (2 * tq + 8 < nt ? 0x0000FFFFu : 0u) | (2 * tq + 9 < nt ? 0xFFFF0000u : 0u);
+                    a0 &= m0;
+                    a1 &= m0;
+                    a2 &= m1;
+                    a3 &= m1;
+                }
+#pragma unroll
+                for (int t = 0; t < NT; ++t) {
+                    float c0 = 0.f, c1 = 0.f, c2 = 0.f, c3 = 0.f;
+                    mma_bf16_16816(c0, c1, c2, c3, a0, a1, a2, a3, bw[t][0], bw[t][1]);
+                    // lane pair (tq, tq^1) holds the 4 split columns of head 2t + tq/2: the even
+                    // lane keeps dim gq, the odd lane dim gq + 8
+                    const float x = (tq & 1) ? (c0 + c1) : (c2 + c3);
+                    const float y = __shfl_xor_sync(PSA_FULL, x, 1);
+                    val[t][mt] = ((tq & 1) ? (c2 + c3) : (c0 + c1)) + y;
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&s.vempty[st]);
+#pragma unroll
+            for (int t = 0; t < NT; ++t) {
+                const int hq = 2 * t + (tq >> 1);
+                if ((mask >> hq) & 1u) {
+                    const float mb = s.em[e][hq];
+                    const float mnew = fmaxf(Mh[t], mb);
+                    const float a = expf(Mh[t] - mnew);
+                    const float cc = expf(mb - mnew);
+#pragma unroll
+                    for (int mt = 0; mt < 8; ++mt) O[t][mt] = O[t][mt] * a + val[t][mt] * cc;
+                    Lh[t] = Lh[t] * a + s.el[e][hq] * cc;
+                    Mh[t] = mnew;
+                }
+            }
+        }
+        // ---- merge the V warps' states per head (finalize, attention.hpp:104-110) ----
+        asm volatile("bar.sync 1, %0;" ::"r"(kNV * 32) : "memory");  // every V tile consumed
+        float* part = reinterpret_cast<float*>(&s.vring[0][0]);     // [kNV][G][128]
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+            const int hq = 2 * t + (tq >> 1);
+#pragma unroll
+            for (int mt = 0; mt < 8; ++mt) part[(vidx * G + hq) * 128 + 16 * mt + gq + 8 * (tq & 1)] = O[t][mt];
+            if (gq == 0 && (tq & 1) == 0) {
+                s.mpart[vidx][hq] = Mh[t];
+                s.lpart[vidx][hq] = Lh[t];
+            }
+        }
+        asm volatile("bar.sync 1, %0;" ::"r"(kNV * 32) : "memory");
+        if (!s.handover) {
+            for (int idx = tid - kWV0 * 32; idx < g * 128; idx += kNV * 32) {
+                const int hq = idx >> 7, dd = idx & 127;
+                float Mt = -INFINITY;
+#pragma unroll
+                for (int w = 0; w < kNV; ++w) Mt = fmaxf(Mt, s.mpart[w][hq]);
+                float Lt = 0.0f, o = 0.0f;
+#pragma unroll
+                for (int w = 0; w < kNV; ++w) {
+                    const float sc = s.lpart[w][hq] > 0.0f ? expf(s.mpart[w][hq] - Mt) : 0.0f;
+                    Lt += s.lpart[w][hq] * sc;
+                    o += sc > 0.0f ? part[(w * G + hq) * 128 + dd] * sc : 0.0f;
+                }
+                b.out[((size_t)u * g + hq) * 128 + dd] = o / Lt;
+            }
+        }
+    }
+}
+
+}  // namespace stream
+
+bool stream_supported(const PoolView& p, const BatchView& b) {
+    return p.kv_tmap != nullptr && p.loc == nullptr && p.dtype == 1 && p.T == 16 && b.d == 128 && b.g >= 2 &&
+           b.g <= 4 && b.ft_keys != nullptr && b.dense_flag != nullptr && b.stream_w != nullptr;
+}
+
+void launch_stream(const PoolView& p, const BatchView& b, cudaStream_t st) {
+    const CUtensorMap& map = *static_cast<const CUtensorMap*>(p.kv_tmap);
+    auto go = [&](auto kern, size_t smem) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        kern<<<b.n_units, stream::kThreads, smem, st>>>(map, p, b);
+    };
+    if (b.g <= 2) go(stream::psa_stream_kernel<2>, sizeof(stream::Smem<2>) + 1024);
+    else go(stream::psa_stream_kernel<4>, sizeof(stream::Smem<4>) + 1024);
+}
+
+}  // namespace psa
+
+// K tiles fetched, V tiles fetched, rounds decided, units run by the stream kernel since the last
+// call (accumulating device counters; reading zeroes them). Benchmark instrumentation.
+// Development builds: attach a mapped host buffer (int[16 + 16*256]) that collects stuck-wait
+// records; returns its host pointer (nullptr in normal builds).
+extern "C" int* psattn_debug_stream_attach() {
+#ifdef PSA_STREAM_DEBUG
+    static int* host = nullptr;
+    if (!host) {
+        if (cudaHostAlloc((void**)&host, sizeof(int) * (16 + 16 * 256), cudaHostAllocMapped) != cudaSuccess) return nullptr;
+        memset(host, 0, sizeof(int) * (16 + 16 * 256));
+        int* dev = nullptr;
+        if (cudaHostGetDevicePointer((void**)&dev, host, 0) != cudaSuccess) return nullptr;
+        if (cudaMemcpyToSymbol(psa::g_stream_dbg, &dev, sizeof(dev)) != cudaSuccess) return nullptr;
+    }
+    return host;
+#else
+    return nullptr;
+#endif
+}
+
+extern "C" int psattn_debug_stream_stats(unsigned long long* out4) {
+    if (cudaMemcpyFromSymbol(out4, psa::g_stream_stats, sizeof(unsigned long long) * 4) != cudaSuccess) return -1;
+    static const unsigned long long z[4] = {};
+    return cudaMemcpyToSymbol(psa::g_stream_stats, z, sizeof(z)) == cudaSuccess ? 0 : -1;
+}

@@ -33,12 +33,43 @@ def unit_ids(requests: np.ndarray, layers: int, kv_heads: int) -> np.ndarray:
     return ((r * layers + l) * kv_heads + h).reshape(-1)
 
 
+def plan_units(n_requests: int, layers: int, kv_heads: int, world: int, rank: int) -> np.ndarray:
+    """Units (global ids, see unit_ids) owned by `rank` (SURVEY §8e partitioning).
+
+    Primary: whole requests (every layer and kv head of a request on one GPU) when there are at
+    least as many requests as ranks. Secondary, when requests < ranks (config-1-like): the
+    (request, kv-head) pairs are split contiguously, so each rank owns some kv heads of a request
+    with all their layers. Either way every unit is owned by exactly one rank; no collective."""
+    if n_requests >= world:
+        return unit_ids(shard_requests(n_requests, world, rank), layers, kv_heads)
+    pairs = shard_requests(n_requests * kv_heads, world, rank)  # flattened (request, kv head)
+    r, h = pairs // kv_heads, pairs % kv_heads
+    l = np.arange(layers, dtype=np.int64)
+    return ((r[:, None] * layers + l[None, :]) * kv_heads + h[:, None]).reshape(-1)
+
+
+def resident_layers(requests_on_rank: int, layers: int, kv_heads: int, blocks: int, bytes_per_block: int,
+                    budget_bytes: int) -> int:
+    """Config 5 (64 x 128K decodes on 2/4 GPUs exceeds HBM, SURVEY §7 hard part 7): how many layers
+    of every owned request fit the pool budget; a step then runs those resident layers."""
+    per_layer = requests_on_rank * kv_heads * blocks * bytes_per_block
+    return int(max(1, min(layers, budget_bytes // max(per_layer, 1))))
+
+
 def max_over_ranks(x: float, device=None) -> float:
     """Device-timed numbers are reported as the max over ranks."""
     if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
         return float(x)
     t = torch.tensor([float(x)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(x: float, device=None) -> float:
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return float(x)
+    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return float(t.item())
 
 

@@ -1,0 +1,169 @@
+"""The warp-specialised stream kernel (kernels_stream.cu) on the production shape (bf16 pool,
+d = 128, 16-token blocks, GQA 2..4): every head against the C oracle under the parity rule,
+the same processed sets and stop points as the round kernel (psattn_set_progressive_kernel(2)),
+bit-determinism across runs, ragged / tiny lists, Oracle ranking + audit, per-rank estimates,
+and its fetch counters (bounded speculation: V only for committed blocks)."""
+import numpy as np
+import pytest
+
+from helpers import check_parity
+from oracle.pyoracle import BlockSet, make_config
+from workload import synth
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def mods():
+    from paper_2503_00392_b200 import batch, capi
+    return capi, batch
+
+
+def build(mods, tokens, g, planted, cfg, seed=3, want_iter=False):
+    capi, batch = mods
+    d, T = 128, 16
+    p = synth.params(seed=seed, dim=d, block_tokens=T, skew=8.0, planted_prob=planted, round_bf16=1)
+    nb = [(t + T - 1) // T for t in tokens]
+    off = np.zeros(len(tokens) + 1, np.int64)
+    off[1:] = np.cumsum(nb)
+    uids = [100 + i for i in range(len(tokens))]
+    pool = batch.DevicePool(d, T, capi.PSATTN_KV_BF16, int(off[-1]))
+    synth.fill(pool, p, uids, off[:-1], tokens)
+    dev = torch.device("cuda")
+    qs = np.array([[synth.query(p, uid, h) for h in range(g)] for uid in uids], np.float32)
+    run = batch.BatchRun(pool, torch.tensor(qs, device=dev), torch.arange(int(off[-1]), dtype=torch.int32, device=dev),
+                         torch.tensor(off, device=dev), max(nb), batch.BatchConfig(**cfg), want_ranked=True,
+                         want_iter=want_iter)
+    return p, uids, nb, off, qs, run
+
+
+def collect(run, off, nb, g):
+    torch.cuda.synchronize()
+    res = []
+    bp_all = run.bp.cpu().numpy()
+    ranked = run.ranked.cpu().numpy()
+    out = run.out.cpu().numpy()
+    est = run.est.cpu().numpy()
+    term = run.term.cpu().numpy()
+    tcov = run.tcov.cpu().numpy()
+    iest = run.iest.cpu().numpy() if run.iest is not None else None
+    for u in range(len(nb)):
+        for h in range(g):
+            qi = u * g + h
+            bp = int(bp_all[qi])
+            hb = int(off[u]) * g + h * nb[u]
+            res.append(dict(bp=bp, ids=ranked[hb: hb + bp], out=out[u, h].copy(), est=float(est[qi]),
+                            term=int(term[qi]), tcov=float(tcov[qi]),
+                            iest=iest[hb: hb + bp].copy() if iest is not None else None))
+    return res
+
+
+def run_mode(capi, run, mode):
+    assert capi.lib.psattn_set_progressive_kernel(mode) == 0
+    try:
+        run.run()
+    finally:
+        capi.lib.psattn_set_progressive_kernel(0)
+
+
+def blockset(p, uid, tokens, nb):
+    k, v = synth.unit_host(p, uid, tokens)
+    nt = [min(16, tokens - i * 16) for i in range(nb)]
+    return BlockSet([k[i, :nt[i]] for i in range(nb)], [v[i, :nt[i]] for i in range(nb)])
+
+
+CFGS = [dict(epsilon=0.95), dict(epsilon=0.8, microbatch_size=3), dict(epsilon=0.99, estimator=0),
+        dict(epsilon=0.9, estimator=1, microbatch_size=8), dict(topk=100), dict(topk=5), dict(epsilon=0.5),
+        dict(epsilon=1.0)]
+
+
+@pytest.mark.parametrize("g", [4, 3, 2])
+@pytest.mark.parametrize("ci", range(len(CFGS)))
+def test_stream_vs_oracle_and_round_kernel(mods, oracle, g, ci):
+    capi, _ = mods
+    cfg = CFGS[ci]
+    tokens = [16 * 1200 + 5, 16 * 300, 16 * 40 + 1, 7, 16 * 9]  # ragged last blocks, a 1-block list
+    p, uids, nb, off, qs, run = build(mods, tokens, g, 1 / 32, cfg, seed=3 + ci, want_iter=True)
+    run_mode(capi, run, 3)
+    a = collect(run, off, nb, g)
+    run_mode(capi, run, 3)
+    a2 = collect(run, off, nb, g)
+    run_mode(capi, run, 2)
+    r = collect(run, off, nb, g)
+    eps = 1.0 if cfg.get("topk") else cfg.get("epsilon", 0.95)
+    oc = make_config(epsilon=eps, microbatch_size=cfg.get("microbatch_size", 1), estimator=cfg.get("estimator", 2))
+    for u, uid in enumerate(uids):
+        bs = blockset(p, uid, tokens[u], nb[u])
+        for h in range(g):
+            x, y, z = a[u * g + h], a2[u * g + h], r[u * g + h]
+            # deterministic: identical bits run to run
+            assert x["bp"] == y["bp"] and np.array_equal(x["out"], y["out"]) and x["est"] == y["est"]
+            tag = check_parity(oracle, qs[u, h], bs, oc, cfg.get("topk", 0), x["ids"], x["bp"], x["out"], x["est"])
+            if z["bp"] < 384:  # (the round kernel's own hand-over cases differ only in arithmetic order)
+                assert x["bp"] == z["bp"] and x["term"] == z["term"], (u, h, x["bp"], z["bp"])
+                assert np.max(np.abs(x["out"] - z["out"])) <= 1e-5
+                assert abs(x["est"] - z["est"]) <= 1e-5
+            if tag == "exact":
+                o = oracle.psa(qs[u, h], bs, oc, cfg.get("topk", 0))
+                # fp64 decide: the reported estimate is the reference's to ~1e-12 (same masses up
+                # to fp32 q.k summation order)
+                assert abs(x["est"] - o.estimated_coverage) <= 1e-5
+                m = oc.microbatch_size
+                bnd = [i for i in range(x["bp"]) if (i + 1) % m == 0 or i + 1 == x["bp"]]
+                assert np.allclose(x["iest"][bnd], o.iteration_estimates[: len(bnd)], rtol=0, atol=1e-5)
+
+
+@pytest.mark.parametrize("cfg", [dict(epsilon=0.9, ranking_mode=1), dict(epsilon=0.95, audit_coverage=1),
+                                 dict(epsilon=0.9, audit_coverage=1, microbatch_size=2)])
+def test_stream_oracle_masses(mods, oracle, cfg):
+    """Oracle ranking / audit: the decide runs on the fp64 oracle masses (reference engine.cpp:64,
+    118-119); true coverage reported."""
+    capi, _ = mods
+    tokens = [16 * 500 + 3, 16 * 64]
+    g = 4
+    p, uids, nb, off, qs, run = build(mods, tokens, g, 1 / 32, cfg, seed=11)
+    run_mode(capi, run, 3)
+    a = collect(run, off, nb, g)
+    run_mode(capi, run, 2)
+    r = collect(run, off, nb, g)
+    oc = make_config(epsilon=cfg["epsilon"], microbatch_size=cfg.get("microbatch_size", 1),
+                     ranking_mode=cfg.get("ranking_mode", 0), audit_coverage=cfg.get("audit_coverage", 0))
+    for u, uid in enumerate(uids):
+        bs = blockset(p, uid, tokens[u], nb[u])
+        for h in range(g):
+            x, z = a[u * g + h], r[u * g + h]
+            check_parity(oracle, qs[u, h], bs, oc, 0, x["ids"], x["bp"], x["out"], x["est"])
+            assert x["bp"] == z["bp"] and abs(x["est"] - z["est"]) <= 1e-9
+            if cfg.get("audit_coverage"):
+                o = oracle.psa(qs[u, h], bs, oc)
+                assert abs(x["tcov"] - o.true_coverage) <= 1e-9, (x["tcov"], o.true_coverage)
+
+
+def test_stream_many_units_and_counters(mods, oracle):
+    """600 planted units (more than two waves of CTAs): sampled heads vs the oracle; the fetch
+    counters: every processed block's V exactly once per committing round, K fetched ahead by at
+    most the lookahead (bounded speculative waste)."""
+    capi, _ = mods
+    g = 4
+    tokens = [16 * 512] * 600
+    p, uids, nb, off, qs, run = build(mods, tokens, g, 1 / 32, dict(epsilon=0.95), seed=17)
+    stats = np.zeros(4, np.uint64)
+    capi.lib.psattn_debug_stream_stats(stats.ctypes.data)
+    run_mode(capi, run, 3)
+    torch.cuda.synchronize()
+    assert capi.lib.psattn_debug_stream_stats(stats.ctypes.data) == 0
+    k_tiles, v_tiles, rounds, units = (int(x) for x in stats)
+    assert units == 600
+    res = collect(run, off, nb, g)
+    union = int(run.union_blocks().sum())
+    assert v_tiles >= union  # every block of a processed set is read
+    assert v_tiles <= int(sum(x["bp"] for x in res))  # and never more than once per head
+    assert k_tiles >= v_tiles
+    assert k_tiles - union <= units * 3 * 32  # speculation bounded by the lookahead rounds
+    for u in (0, 299, 599):
+        bs = blockset(p, uids[u], tokens[u], nb[u])
+        for h in range(g):
+            x = res[u * g + h]
+            check_parity(oracle, qs[u, h], bs, make_config(epsilon=0.95), 0, x["ids"], x["bp"], x["out"], x["est"])

@@ -59,3 +59,25 @@ def test_shard_balance():
             assert np.array_equal(np.concatenate(parts), np.arange(n))
             sizes = [len(p) for p in parts]
             assert max(sizes) - min(sizes) <= 1
+
+
+def test_plan_units_kv_head_split():
+    """requests < ranks: (request, kv head) pairs split across ranks, all layers of a pair on one rank."""
+    from paper_2503_00392_b200 import shard
+    for reqs, world in ((1, 8), (1, 2), (3, 8), (2, 4), (8, 8), (64, 8), (64, 2)):
+        parts = [shard.plan_units(reqs, 4, 8, world, r) for r in range(world)]
+        allu = np.concatenate(parts)
+        assert np.array_equal(np.sort(allu), np.arange(reqs * 4 * 8))  # every unit exactly once
+        for p in parts:
+            kvh = set(((p // 8) // 4 * 8 + p % 8).tolist())  # (request, kv head) pairs of the rank
+            assert len(p) == len(kvh) * 4                     # each owned pair with all 4 layers
+    one = [shard.plan_units(1, 32, 8, 8, r) for r in range(8)]
+    assert all(set((p % 8).tolist()) == {r} for r, p in enumerate(one))  # config 1 on 8 GPUs: one kv head each
+
+
+def test_resident_layers():
+    from paper_2503_00392_b200 import shard
+    blk = 8192 + 1024
+    assert shard.resident_layers(8, 32, 8, 8192, blk, 150 << 30) == 32
+    l2 = shard.resident_layers(32, 32, 8, 8192, blk, 150 << 30)  # 64 requests on 2 GPUs
+    assert 1 <= l2 < 32 and 32 * 8 * 8192 * blk * l2 <= 150 << 30
