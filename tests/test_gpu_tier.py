@@ -162,11 +162,20 @@ def test_config4_mixed_lengths_uneven_layers(mods, oracle, ref):
     cap = nb // 4
     dev = torch.device("cuda")
     cfg = batch.BatchConfig(epsilon=0.95)
-    # all-HBM reference placement: the plain pool
+    # all-HBM reference placement: the plain pool. Its default progressive kernel on this shape
+    # is the TMA stream kernel (HBM pools only); the host-mapped tier runs the GQA round kernel,
+    # so the placement identity is checked with the round kernel on both sides, and the stream
+    # kernel's own run is checked against the C oracle below.
     pool = batch.DevicePool(d, T, capi.PSATTN_KV_BF16, nb)
     pool.put_blocks(np.arange(nb, dtype=np.int32), ntok, K, V)
-    base_run, off = tier_batch(mods, pool, qs, lists, cfg, dev)
-    base_run.run()
+    stream_run, off = tier_batch(mods, pool, qs, lists, cfg, dev)
+    stream_run.run()
+    capi.check(capi.lib.psattn_set_progressive_kernel(2))
+    try:
+        base_run, off = tier_batch(mods, pool, qs, lists, cfg, dev)
+        base_run.run()
+    finally:
+        capi.check(capi.lib.psattn_set_progressive_kernel(0))
     torch.cuda.synchronize()
     hits = {}
     for policy in (0, 1):
@@ -191,11 +200,12 @@ def test_config4_mixed_lengths_uneven_layers(mods, oracle, ref):
         assert tier.h2d_bytes() > 0
     # uneven budgets: the unified pool serves at least as many loads from HBM
     assert hits[0] >= hits[1], hits
-    # parity of the base run against the C oracle on one head of every unit
+    # parity of both all-HBM runs against the C oracle on one head of every unit
     for u, (k, v, nt) in enumerate(bsets):
         bs = BlockSet([k[i, :nt[i]] for i in range(len(nt))], [v[i, :nt[i]] for i in range(len(nt))])
         h = u % g
-        bpq = int(base_run.bp[u * g + h])
-        ids = ranked_of(base_run, off, u, h)[:bpq]
-        check_parity(oracle, qs[u][h], bs, make_config(epsilon=0.95), 0, ids, bpq,
-                     base_run.out[u, h].cpu().numpy(), float(base_run.est[u * g + h]))
+        for r in (base_run, stream_run):
+            bpq = int(r.bp[u * g + h])
+            ids = ranked_of(r, off, u, h)[:bpq]
+            check_parity(oracle, qs[u][h], bs, make_config(epsilon=0.95), 0, ids, bpq,
+                         r.out[u, h].cpu().numpy(), float(r.est[u * g + h]))
