@@ -403,12 +403,21 @@ def run_ours(args):
     capi.lib.psattn_profile_read(None, None, 1)
     sstats = np.zeros(4, np.uint64)
     capi.lib.psattn_debug_stream_stats(sstats.ctypes.data)  # zero the stream kernel's fetch counters
+    sprof = np.zeros(32, np.uint64)
+    capi.lib.psattn_debug_stream_prof(sprof.ctypes.data)
     capi.lib.psattn_profile_enable(1)
     for _ in range(args.steps):
         run.run()
     torch.cuda.synchronize()
     capi.lib.psattn_profile_enable(0)
     capi.lib.psattn_debug_stream_stats(sstats.ctypes.data)
+    capi.lib.psattn_debug_stream_prof(sprof.ctypes.data)
+    if sprof.any():  # development build with the stream kernel's wait-site cycle counters
+        roles, sites = ["producer", "decider", "scorer", "v"], ["total", "drain", "scored", "pub", "ktile", "vtile"]
+        units = max(1.0, float(sstats[3]))
+        print(json.dumps({"stream_prof_cycles_per_unit": {
+            r: {k: round(float(sprof[8 * i + j]) / units) for j, k in enumerate(sites + ["idle_it", "busy_it"])}
+            for i, r in enumerate(roles)}}), file=sys.stderr)
     stage_ms = np.zeros(4, np.float64)
     stage_n = np.zeros(4, np.int64)
     capi.lib.psattn_profile_read(stage_ms.ctypes.data, stage_n.ctypes.data, 1)

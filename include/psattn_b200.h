@@ -177,6 +177,10 @@ int psattn_set_progressive_kernel(int32_t mode);
  * rounds decided and units run since the last call (device counters; reading zeroes
  * them). Returns 0, or -1 on a CUDA error. */
 int psattn_debug_stream_stats(unsigned long long* out4);
+/* Development builds (make EXTRA=-DPSA_STREAM_PROF) only: per role of the stream kernel (producer,
+ * decider, scorers, V; summed over warps) total cycles, cycles in wait sites 1-5, producer idle /
+ * productive iterations; reading zeroes them. All zero in normal builds. */
+int psattn_debug_stream_prof(unsigned long long* out32);
 /* Development builds (make PROF=1) only: SM cycles per phase of the GQA round kernel
  * (init, order, union, K pass, decide, V pass, advance, finalize, rounds, 3 warp-0
  * counters); reading zeroes them. -1 in normal builds. */

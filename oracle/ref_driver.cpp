@@ -358,6 +358,75 @@ double refdrv_block_log_as_oracle(const float* q, int32_t d, int32_t ntok, const
                                        scale);
 }
 
+// ---- attention.hpp templates (attention.hpp:39-109, attention.cpp:7-63): golden values for
+// the C++ API parity test (tests/golden/make_attention_golden.py).
+namespace {
+psattn::KVBlock make_kv(int32_t ntok, int32_t d, const float* k, const float* v) {
+    psattn::KVBlock b;
+    b.n_tokens = ntok;
+    b.dim = d;
+    b.keys.assign(k, k + static_cast<std::size_t>(ntok) * d);
+    b.values.assign(v, v + static_cast<std::size_t>(ntok) * d);
+    return b;
+}
+}  // namespace
+
+// stats: max score, exp sum, log mass. prec 0 = float, 1 = double (out/stats as double either way).
+int refdrv_block_partial(int32_t prec, const float* q, int32_t d, int32_t ntok, const float* k, const float* v,
+                         double scale, double* out, double* stats) {
+    return guarded([&] {
+        const psattn::KVBlock b = make_kv(ntok, d, k, v);
+        const std::span<const float> qs(q, static_cast<std::size_t>(d));
+        if (prec == 0) {
+            const auto r = psattn::block_partial_attention(qs, b, static_cast<float>(scale));
+            for (int32_t i = 0; i < d; ++i) out[i] = r.out_unnorm[i];
+            stats[0] = r.max_score, stats[1] = r.exp_sum, stats[2] = r.log_as;
+        } else {
+            const auto r = psattn::block_partial_attention_t<double>(qs, b, scale);
+            for (int32_t i = 0; i < d; ++i) out[i] = r.out_unnorm[i];
+            stats[0] = r.max_score, stats[1] = r.exp_sum, stats[2] = r.log_as;
+        }
+        return 0;
+    });
+}
+
+// n blocks of ntok tokens merged in order (merge_partial) then finalize; log_as_acc in stats[0].
+int refdrv_merge_chain(int32_t prec, const float* q, int32_t d, int32_t n, int32_t ntok, const float* k,
+                       const float* v, double scale, double* out, double* stats) {
+    return guarded([&] {
+        const std::span<const float> qs(q, static_cast<std::size_t>(d));
+        const std::size_t per = static_cast<std::size_t>(ntok) * d;
+        auto run = [&](auto zero) {
+            using T = decltype(zero);
+            psattn::SoftmaxAccumulatorT<T> acc;
+            for (int32_t i = 0; i < n; ++i) {
+                const psattn::KVBlock b = make_kv(ntok, d, k + per * i, v + per * i);
+                psattn::merge_partial(acc, psattn::block_partial_attention_t<T>(qs, b, static_cast<T>(scale)));
+            }
+            const auto o = psattn::finalize(acc);
+            for (int32_t i = 0; i < d; ++i) out[i] = o[i];
+            stats[0] = acc.log_as_acc, stats[1] = acc.exp_sum, stats[2] = acc.max_score;
+        };
+        if (prec == 0) run(0.0f);
+        else run(0.0);
+        return 0;
+    });
+}
+
+int refdrv_exact_attention_blocks(const float* q, int32_t d, int32_t n, int32_t ntok, const float* k, const float* v,
+                                  double scale, double* out) {
+    return guarded([&] {
+        const std::size_t per = static_cast<std::size_t>(ntok) * d;
+        std::vector<psattn::KVBlock> bs;
+        for (int32_t i = 0; i < n; ++i) bs.push_back(make_kv(ntok, d, k + per * i, v + per * i));
+        std::vector<const psattn::KVBlock*> ptrs;
+        for (auto& b : bs) ptrs.push_back(&b);
+        const auto o = psattn::exact_attention_blocks(std::span<const float>(q, static_cast<std::size_t>(d)), ptrs, scale);
+        for (int32_t i = 0; i < d; ++i) out[i] = o[i];
+        return 0;
+    });
+}
+
 // ---- Reference workload generator (workload.cpp:49-153), exported so the GPU path can be fed the
 // exact inputs of the reference's own scenarios (tradeoff / serving golden reports in proj/out).
 void* refdrv_workload_create(int32_t n_requests, int32_t dim, int32_t block_size, int32_t n_layers,

@@ -242,18 +242,26 @@ int pool_put(psattn_pool* pool, int64_t n, const int32_t* slots, const int32_t* 
     pack_host(v, n, ntok, keys, values, row_stride_floats, img);
     char* d_img = nullptr;
     int32_t* d_idx = nullptr;
+    // staging buffers are released on every path (stream-ordered frees, then one sync)
+    auto finish = [&](cudaError_t err, const char* what) {
+        if (d_img) cudaFreeAsync(d_img, st);
+        if (d_idx) cudaFreeAsync(d_idx, st);
+        const cudaError_t es = cudaStreamSynchronize(st);
+        if (err != cudaSuccess) return cuda_fail(err, what);
+        return es == cudaSuccess ? PSATTN_OK : cuda_fail(es, "put_blocks");
+    };
     cudaError_t e;
-    if ((e = cudaMallocAsync(&d_img, img.size(), st)) != cudaSuccess) return cuda_fail(e, "put staging");
-    if ((e = cudaMallocAsync(&d_idx, (size_t)n * 8, st)) != cudaSuccess) return cuda_fail(e, "put staging");
-    cudaMemcpyAsync(d_img, img.data(), img.size(), cudaMemcpyHostToDevice, st);
-    cudaMemcpyAsync(d_idx, slots, (size_t)n * 4, cudaMemcpyHostToDevice, st);
-    cudaMemcpyAsync(d_idx + n, ntok, (size_t)n * 4, cudaMemcpyHostToDevice, st);
-    if ((e = launch_scatter(v, d_img, d_idx, d_idx + n, n, st)) != cudaSuccess) return cuda_fail(e, "put scatter");
-    if ((e = launch_meta_build(v, d_idx, 0, n, st)) != cudaSuccess) return cuda_fail(e, "metadata build");
-    cudaFreeAsync(d_img, st);
-    cudaFreeAsync(d_idx, st);
-    if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return cuda_fail(e, "put_blocks");
-    return PSATTN_OK;
+    if ((e = cudaMallocAsync(&d_img, img.size(), st)) != cudaSuccess) return finish(e, "put staging");
+    if ((e = cudaMallocAsync(&d_idx, (size_t)n * 8, st)) != cudaSuccess) return finish(e, "put staging");
+    if ((e = cudaMemcpyAsync(d_img, img.data(), img.size(), cudaMemcpyHostToDevice, st)) != cudaSuccess)
+        return finish(e, "put upload");
+    if ((e = cudaMemcpyAsync(d_idx, slots, (size_t)n * 4, cudaMemcpyHostToDevice, st)) != cudaSuccess)
+        return finish(e, "put upload");
+    if ((e = cudaMemcpyAsync(d_idx + n, ntok, (size_t)n * 4, cudaMemcpyHostToDevice, st)) != cudaSuccess)
+        return finish(e, "put upload");
+    if ((e = launch_scatter(v, d_img, d_idx, d_idx + n, n, st)) != cudaSuccess) return finish(e, "put scatter");
+    if ((e = launch_meta_build(v, d_idx, 0, n, st)) != cudaSuccess) return finish(e, "metadata build");
+    return finish(cudaSuccess, "put_blocks");
 }
 
 int read_slot(const psattn_pool* pool, int64_t slot, int32_t ntok, float* keys, float* values) {

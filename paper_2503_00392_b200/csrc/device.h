@@ -46,4 +46,17 @@ int prun_consume(RunState* s, float scale, int n, const int32_t* ntok, const flo
                  const float* const* values, float* log_as);
 int prun_result(const RunState* s, float* out);
 
+// attention.hpp API (attention_kernels.cu): one token sequence K/V [n][d] (host fp32), the
+// reference's arithmetic order. out [d] (unnormalised unless `normalize`; V may be null),
+// stats [3] = max score, exponent sum, log mass.
+int seq_attention(const float* q, int d, const float* K, const float* V, int64_t n, float scale, int normalize,
+                  float* out, float* stats);
+int seq_attention(const float* q, int d, const float* K, const float* V, int64_t n, double scale, int normalize,
+                  double* out, double* stats);
+// merge_partial on a non-empty accumulator: acc_stats/part_stats [3] = max, exponent sum, log mass.
+int softmax_merge(float* acc_out, float* acc_stats, const float* part_out, const float* part_stats, int d);
+int softmax_merge(double* acc_out, double* acc_stats, const double* part_out, const double* part_stats, int d);
+int softmax_finalize(const float* acc_out, int d, float es, float* out);
+int softmax_finalize(const double* acc_out, int d, double es, double* out);
+
 }  // namespace psa

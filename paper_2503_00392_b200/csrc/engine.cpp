@@ -10,7 +10,10 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <exception>
+#include <semaphore>
 #include <string>
+#include <thread>
 
 #include "device.h"
 #include "engine_internal.h"
@@ -271,29 +274,154 @@ MultiHeadResult psa_attention_multi_head(std::span<const HeadVector> head_querie
     return out;
 }
 
-// ---- pipeline.hpp ----
+// ---- pipeline.hpp (reference pipeline.cpp:32-176) ----
 namespace {
-ExecutionResult run_exec(std::span<const float> q, std::span<const BlockId> ids, const PSAConfig& cfg,
-                         TieredBlockStore& store) {
-    const auto t0 = std::chrono::steady_clock::now();
-    ExecutionResult out;
-    out.result = psa_attention(q, ids, cfg, store);
-    out.timings.total_wall_ms =
-        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
-    out.timings.sequential_equiv_ms = out.timings.total_wall_ms;
-    out.timings.overlap_efficiency = 1.0;
-    return out;
+using WallClock = std::chrono::steady_clock;
+
+double elapsed_ms(WallClock::time_point from, WallClock::time_point to) {
+    return std::chrono::duration<double, std::milli>(to - from).count();
 }
+
+void compute_pad(double ms) {
+    if (ms > 0.0) std::this_thread::sleep_for(std::chrono::duration<double, std::milli>(ms));
+}
+
+void close_timings(PipelineTimings& t, WallClock::time_point start) {
+    t.total_wall_ms = elapsed_ms(start, WallClock::now());
+    double sum = 0.0;
+    for (double x : t.load_ms) sum += x;
+    for (double x : t.compute_ms) sum += x;
+    t.sequential_equiv_ms = sum;
+    t.overlap_efficiency = t.total_wall_ms > 0.0 ? sum / t.total_wall_ms : 1.0;
+}
+
+// Depth-1 hand-off between the loader thread and the computing thread, built on two
+// semaphores: `vacant` (the loader must hold it before it starts a load, so at most one
+// loaded microbatch can be waiting — and be discarded on stop) and `filled`.
+class Handoff {
+public:
+    // loader side
+    bool claim(const StopSignal& stop) {
+        vacant_.acquire();
+        return !stop.raised();
+    }
+    void publish(LoadedBatch&& b, double load_ms) {
+        batch_ = std::move(b);
+        load_ms_ = load_ms;
+        filled_.release();
+    }
+    void fail(std::exception_ptr e) {
+        error_ = e;
+        filled_.release();
+    }
+    // computing side: the next batch (rethrows a loader failure); frees the slot at once
+    LoadedBatch take(double& load_ms) {
+        filled_.acquire();
+        if (error_) std::rethrow_exception(error_);
+        LoadedBatch b = std::move(batch_);
+        load_ms = load_ms_;
+        vacant_.release();
+        return b;
+    }
+    // wake a loader blocked in claim() after the stop was raised
+    void release_loader() { vacant_.release(); }
+
+private:
+    std::counting_semaphore<4> vacant_{1};  // release_loader may add one past a finished loader
+    std::binary_semaphore filled_{0};
+    LoadedBatch batch_;
+    double load_ms_ = 0.0;
+    std::exception_ptr error_;
+};
 }  // namespace
 
 ExecutionResult run_sequential(std::span<const float> q, std::span<const BlockId> block_ids, const PSAConfig& cfg,
-                               TieredBlockStore& store, const PipelineOptions&) {
-    return run_exec(q, block_ids, cfg, store);
+                               TieredBlockStore& store, const PipelineOptions& opts) {
+    const RankedPlan plan = plan_blocks(q, block_ids, cfg, store);
+    ProgressiveRun run(q, plan, cfg);
+    ExecutionResult out;
+    const auto start = WallClock::now();
+    while (!run.finished()) {
+        const auto t0 = WallClock::now();
+        const LoadedBatch lb = load_microbatch(store, plan, run.cursor(), run.next_microbatch_size());
+        const auto t1 = WallClock::now();
+        run.consume(lb.blocks, lb.hits, lb.misses);
+        compute_pad(opts.compute_pad_ms);
+        out.timings.load_ms.push_back(elapsed_ms(t0, t1));
+        out.timings.compute_ms.push_back(elapsed_ms(t1, WallClock::now()));
+    }
+    close_timings(out.timings, start);
+    out.result = run.result();
+    return out;
 }
 
 ExecutionResult run_pipelined(std::span<const float> q, std::span<const BlockId> block_ids, const PSAConfig& cfg,
-                              TieredBlockStore& store, const PipelineOptions&) {
-    return run_exec(q, block_ids, cfg, store);
+                              TieredBlockStore& store, const PipelineOptions& opts) {
+    const RankedPlan plan = plan_blocks(q, block_ids, cfg, store);
+    ProgressiveRun run(q, plan, cfg);
+    const std::size_t n = plan.ranked_ids.size();
+    const std::size_t m = static_cast<std::size_t>(cfg.microbatch_size);
+    Handoff slot;
+    StopSignal stop;
+    ExecutionResult out;
+    const auto start = WallClock::now();
+    // The loader walks the plan in microbatches of m (the sizes ProgressiveRun asks for); a
+    // stop seen after a load completes drops that batch (the one allowed in-flight load).
+    std::thread loader([&] {
+        try {
+            for (std::size_t cur = 0; cur < n;) {
+                if (!slot.claim(stop)) return;
+                const std::size_t cnt = std::min(m, n - cur);
+                const auto t0 = WallClock::now();
+                LoadedBatch lb = load_microbatch(store, plan, cur, cnt);
+                const double ms = elapsed_ms(t0, WallClock::now());
+                cur += cnt;
+                if (stop.raised()) return;
+                slot.publish(std::move(lb), ms);
+            }
+        } catch (...) {
+            slot.fail(std::current_exception());
+        }
+    });
+    try {
+        while (!run.finished()) {
+            double load_ms = 0.0;
+            const LoadedBatch lb = slot.take(load_ms);
+            const auto t0 = WallClock::now();
+            run.consume(lb.blocks, lb.hits, lb.misses);
+            compute_pad(opts.compute_pad_ms);
+            out.timings.load_ms.push_back(load_ms);
+            out.timings.compute_ms.push_back(elapsed_ms(t0, WallClock::now()));
+        }
+    } catch (...) {
+        stop.raise();
+        slot.release_loader();
+        loader.join();
+        throw;
+    }
+    stop.raise();
+    slot.release_loader();
+    loader.join();
+    close_timings(out.timings, start);
+    out.result = run.result();
+    return out;
+}
+
+PipelineModel simulate_pipeline(std::span<const double> load_ms, std::span<const double> compute_ms) {
+    if (load_ms.size() != compute_ms.size()) throw Error("simulate_pipeline: load/compute series length mismatch");
+    PipelineModel pm;
+    // t_take: when compute took the previous batch (the loader may then start the next load);
+    // t_done: when compute finished the previous batch.
+    double t_take = 0.0, t_done = 0.0;
+    for (std::size_t i = 0; i < load_ms.size(); ++i) {
+        const double loaded = t_take + load_ms[i];
+        t_take = std::max(loaded, t_done);
+        t_done = t_take + compute_ms[i];
+        pm.sequential_ms += load_ms[i] + compute_ms[i];
+    }
+    pm.pipelined_ms = t_done;
+    pm.overlap_efficiency = pm.pipelined_ms > 0.0 ? pm.sequential_ms / pm.pipelined_ms : 1.0;
+    return pm;
 }
 
 // ---- ProgressiveRun / load_microbatch (reference engine.cpp:92-160) ----

@@ -3,6 +3,7 @@
 #include <float.h>
 #include <math.h>
 #include <stdlib.h>
+#include <mutex>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -719,6 +720,10 @@ int launch_batch(const PoolView& p, const BatchView& b, cudaStream_t st, cudaEve
         // Two-stream pipeline over sub-batches of units: score(i+1) streams metadata from HBM
         // on `st` while progressive(i) runs on the auxiliary stream. Stream-ordered (events),
         // no host synchronisation; the caller's stream joins the auxiliary one at the end.
+        // The auxiliary stream, its events and the score kernel's smem floor are process-wide:
+        // concurrent callers serialise their enqueues here.
+        static std::mutex pipe_mutex;
+        std::lock_guard<std::mutex> lock(pipe_mutex);
         PipeResources& r = pipe_resources();
         static const size_t floor_env = [] {
             const char* e = getenv("PSA_SCORE_SMEM_FLOOR");

@@ -48,6 +48,7 @@
 namespace psa {
 
 __device__ unsigned long long g_stream_stats[4];  // K tiles, V tiles, rounds, units (accumulating)
+__device__ unsigned long long g_stream_prof[32];  // PSA_STREAM_PROF builds: [role][0 total, wait sites 1-5, idle, busy]
 // Development builds (make STREAM_DEBUG=1): a wait that does not complete within ~2^22 polls
 // writes the stuck warp's state into mapped host memory (readable after the trap) and traps.
 __device__ int* g_stream_dbg = nullptr;
@@ -200,6 +201,14 @@ __device__ __noinline__ void dbg_note(int site, int a0, int a1, int a2, int a3, 
             }                                                                                          \
         }                                                                                              \
     } while (0)
+#elif defined(PSA_STREAM_PROF)
+// development builds (make EXTRA=-DPSA_STREAM_PROF): cycles each warp spends in each wait site
+#define SWAIT(bar, ph, site, a0, a1, a2, a3, a4, a5, a6, a7) \
+    do {                                                      \
+        const long long t0_ = clock64();                      \
+        mbar_wait((bar), (ph));                               \
+        pw[(site)] += clock64() - t0_;                        \
+    } while (0)
 #else
 #define SWAIT(bar, ph, site, a0, a1, a2, a3, a4, a5, a6, a7) mbar_wait((bar), (ph))
 #endif
@@ -219,6 +228,10 @@ __global__ void __launch_bounds__(kThreads, 2) psa_stream_kernel(const __grid_co
     const int64_t n = b.list_off[u + 1] - off;
     const int64_t limit = b.topk > 0 ? (b.topk < n ? b.topk : n) : n;
     const int T2 = 2 * p.T;  // tensor-map rows per slot (K rows then V rows)
+#ifdef PSA_STREAM_PROF
+    long long pw[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const long long t_start = clock64();
+#endif
     float* wg = b.stream_w + (size_t)u * kENT * 64;  // this unit's weights, 64 floats per entry
 
     if (tid == 0) {
@@ -400,6 +413,9 @@ __global__ void __launch_bounds__(kThreads, 2) psa_stream_kernel(const __grid_co
                 }
                 break;
             }
+#ifdef PSA_STREAM_PROF
+            ++pw[progress ? 7 : 6];
+#endif
             if (!progress) {
                 __nanosleep(64);
 #ifdef PSA_STREAM_DEBUG
@@ -739,6 +755,14 @@ __global__ void __launch_bounds__(kThreads, 2) psa_stream_kernel(const __grid_co
             }
         }
     }
+#ifdef PSA_STREAM_PROF
+    {
+        const int role = warp == 0 ? 0 : warp == 1 ? 1 : warp < kWV0 ? 2 : 3;
+        pw[0] = clock64() - t_start;
+        if (lane == 0)
+            for (int i = 0; i < 8; ++i) atomicAdd(&g_stream_prof[role * 8 + i], (unsigned long long)pw[i]);
+    }
+#endif
 }
 
 }  // namespace stream
@@ -784,4 +808,13 @@ extern "C" int psattn_debug_stream_stats(unsigned long long* out4) {
     if (cudaMemcpyFromSymbol(out4, psa::g_stream_stats, sizeof(unsigned long long) * 4) != cudaSuccess) return -1;
     static const unsigned long long z[4] = {};
     return cudaMemcpyToSymbol(psa::g_stream_stats, z, sizeof(z)) == cudaSuccess ? 0 : -1;
+}
+
+// PSA_STREAM_PROF builds: per role (producer, decider, scorers, V) summed over warps: total
+// cycles, cycles waiting at sites 1-5 (1 V-ring drain, 2 round scored, 3 round published,
+// 4 K tile, 5 V tile), producer idle / productive loop iterations. Reading zeroes them.
+extern "C" int psattn_debug_stream_prof(unsigned long long* out32) {
+    if (cudaMemcpyFromSymbol(out32, psa::g_stream_prof, sizeof(unsigned long long) * 32) != cudaSuccess) return -1;
+    static const unsigned long long z[32] = {};
+    return cudaMemcpyToSymbol(psa::g_stream_prof, z, sizeof(z)) == cudaSuccess ? 0 : -1;
 }

@@ -6,12 +6,15 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
+#include <fstream>
 #include <memory>
 #include <random>
 #include <set>
 #include <sstream>
 #include <vector>
 
+#include "psattn/attention.hpp"
 #include "psattn/engine.hpp"
 #include "psattn/pipeline.hpp"
 #include "psattn/store.hpp"
@@ -49,7 +52,106 @@ static StoreOptions opts(std::size_t cap, int layers = 1) {
     return o;
 }
 
-int main() {
+// ---- attention.hpp golden cases (tests/golden/make_attention_golden.py) ----
+static std::vector<float> golden_stream(std::uint64_t seed, std::size_t count) {
+    std::uint64_t x = seed * 0x9E3779B97F4A7C15ull + 1;
+    std::vector<float> out(count);
+    for (auto& o : out) {
+        x ^= x >> 12;
+        x ^= x << 25;
+        x ^= x >> 27;
+        const std::uint64_t v = x * 0x2545F4914F6CDD1Dull;
+        o = static_cast<float>(static_cast<double>(v >> 40) * 0x1p-22 - 2.0);
+    }
+    return out;
+}
+
+static double hex_double(const std::string& h) {
+    std::uint64_t bits = 0;
+    for (int i = 7; i >= 0; --i) bits = (bits << 8) | std::stoull(h.substr(2 * i, 2), nullptr, 16);
+    double d;
+    std::memcpy(&d, &bits, 8);
+    return d;
+}
+
+static void attention_golden(const char* path) {
+    std::ifstream in(path);
+    CHECK(in.good());
+    std::string line;
+    int cases = 0, exact = 0, values = 0;
+    double worst_f = 0.0, worst_d = 0.0;
+    while (std::getline(in, line)) {
+        if (line.empty()) continue;
+        std::istringstream ls(line);
+        std::string kind, qs_hex, sc_hex;
+        int prec, d, n, ntok, cnt;
+        std::uint64_t seed;
+        ls >> kind >> prec >> seed >> d >> n >> ntok >> qs_hex >> sc_hex >> cnt;
+        const double qscale = hex_double(qs_hex), scale = hex_double(sc_hex);
+        std::vector<double> want(cnt);
+        for (auto& w : want) {
+            std::string h;
+            ls >> h;
+            w = hex_double(h);
+        }
+        HeadVector q = golden_stream(seed, d);
+        for (auto& x : q) x *= static_cast<float>(qscale);
+        const auto k = golden_stream(seed + 1, static_cast<std::size_t>(n) * ntok * d);
+        const auto v = golden_stream(seed + 2, static_cast<std::size_t>(n) * ntok * d);
+        std::vector<KVBlock> blocks(n);
+        for (int b = 0; b < n; ++b) {
+            blocks[b].block_id = b;
+            blocks[b].n_tokens = ntok;
+            blocks[b].dim = d;
+            const std::size_t per = static_cast<std::size_t>(ntok) * d;
+            blocks[b].keys.assign(k.begin() + b * per, k.begin() + (b + 1) * per);
+            blocks[b].values.assign(v.begin() + b * per, v.begin() + (b + 1) * per);
+        }
+        std::vector<double> got;
+        auto take = [&](const auto& vec) { for (auto x : vec) got.push_back(static_cast<double>(x)); };
+        if (kind == "partial" && prec == 0) {
+            const auto r = block_partial_attention(q, blocks[0], static_cast<float>(scale));
+            take(r.out_unnorm);
+            got.push_back(r.max_score), got.push_back(r.exp_sum), got.push_back(r.log_as);
+        } else if (kind == "partial") {
+            const auto r = block_partial_attention_t<double>(q, blocks[0], scale);
+            take(r.out_unnorm);
+            got.push_back(r.max_score), got.push_back(r.exp_sum), got.push_back(r.log_as);
+        } else if (kind == "chain" && prec == 0) {
+            SoftmaxAccumulator acc;
+            for (auto& b : blocks) merge_partial(acc, block_partial_attention(q, b, static_cast<float>(scale)));
+            take(finalize(acc));
+            got.push_back(acc.log_as_acc), got.push_back(acc.exp_sum), got.push_back(acc.max_score);
+        } else if (kind == "chain") {
+            SoftmaxAccumulatorT<double> acc;
+            for (auto& b : blocks) merge_partial(acc, block_partial_attention_t<double>(q, b, scale));
+            take(finalize(acc));
+            got.push_back(acc.log_as_acc), got.push_back(acc.exp_sum), got.push_back(acc.max_score);
+        } else if (kind == "exact") {
+            std::vector<const KVBlock*> ptrs;
+            for (auto& b : blocks) ptrs.push_back(&b);
+            take(exact_attention_blocks(q, ptrs, scale));
+        } else {
+            got.push_back(block_log_as_oracle(q, blocks[0], scale));
+        }
+        CHECK(got.size() == want.size());
+        for (std::size_t i = 0; i < got.size(); ++i) {
+            const double err = std::fabs(got[i] - want[i]) / std::max(1.0, std::fabs(want[i]));
+            ++values;
+            if (got[i] == want[i]) ++exact;
+            if (prec == 0) worst_f = std::max(worst_f, err);
+            else worst_d = std::max(worst_d, err);
+            // float: the reference's own rounding order; device expf/logf may differ by ulps
+            CHECK(err < (prec == 0 ? 1e-5 : 1e-12));
+        }
+        ++cases;
+    }
+    std::printf("attention.hpp golden: %d cases, %d/%d values bit-identical, worst rel err f32 %.2e f64 %.2e\n",
+                cases, exact, values, worst_f, worst_d);
+    CHECK(cases > 100);
+}
+
+int main(int argc, char** argv) {
     // --- metadata.hpp scoring / ranking (reference test_core.cpp:363-434) ---
     {
         KVBlock proto;
@@ -315,33 +417,143 @@ int main() {
         }
         CHECK(threw);
     }
-    // --- pipelined == sequential == plain, bitwise (test_pipeline.cpp:48-92) ---
+    // --- pipelined == sequential bitwise; both == plain within tolerance (test_pipeline.cpp:48-92) ---
     {
         std::mt19937_64 rng(77);
-        const int d = 32;
-        TieredBlockStore a(opts(8)), b(opts(8)), c(opts(8));
+        const double epsilons[] = {0.5, 0.7, 0.9, 0.97, 1.0};
+        for (int inst = 0; inst < 10; ++inst) {
+            const int d = 8 + 4 * (inst % 4);
+            const int nb = 12 + (inst % 3) * 6;
+            TieredBlockStore a(opts(8)), b(opts(8)), c(opts(8));
+            std::vector<BlockId> ids;
+            for (int i = 0; i < nb; ++i) {
+                auto blk = make_block(rng, i, 0, 4, d);
+                a.put_block(blk);
+                b.put_block(blk);
+                c.put_block(blk);
+                ids.push_back(i);
+            }
+            std::normal_distribution<float> nd;
+            HeadVector q(d);
+            for (auto& x : q) x = nd(rng);
+            PSAConfig cfg;
+            cfg.epsilon = epsilons[inst % 5];
+            cfg.microbatch_size = 1 + inst % 5;
+            cfg.block_size = 4;
+            cfg.audit_coverage = inst % 2 == 0;
+            const auto p = run_pipelined(q, ids, cfg, a);
+            const auto s = run_sequential(q, ids, cfg, b);
+            const auto plain = psa_attention(q, ids, cfg, c);
+            CHECK(p.result.output == s.result.output);  // same device accumulator, same order: bitwise
+            CHECK(p.result.blocks_processed == s.result.blocks_processed);
+            CHECK(p.result.processed_ids == s.result.processed_ids && s.result.processed_ids == plain.processed_ids);
+            CHECK(p.result.estimated_coverage == s.result.estimated_coverage);
+            CHECK(p.result.true_coverage == s.result.true_coverage);
+            CHECK(p.result.terminated_early == s.result.terminated_early);
+            for (int k = 0; k < d; ++k) CHECK(std::fabs(s.result.output[k] - plain.output[k]) < 1e-4f);
+            CHECK(std::fabs(s.result.estimated_coverage - plain.estimated_coverage) < 1e-6);
+            CHECK(p.result.iterations.size() == s.result.iterations.size());
+            CHECK(s.result.iterations.size() == plain.iterations.size());
+            for (std::size_t i = 0; i < s.result.iterations.size(); ++i) {
+                CHECK(p.result.iterations[i].blocks == s.result.iterations[i].blocks);
+                CHECK(p.result.iterations[i].hits == s.result.iterations[i].hits);
+                CHECK(p.result.iterations[i].misses == s.result.iterations[i].misses);
+                CHECK(p.result.iterations[i].estimated_coverage == s.result.iterations[i].estimated_coverage);
+                CHECK(plain.iterations[i].hits == s.result.iterations[i].hits);
+                CHECK(plain.iterations[i].misses == s.result.iterations[i].misses);
+            }
+            // sequential loads exactly the processed blocks, like psa_attention's replay; the
+            // pipelined loader may have fetched one microbatch past the stop
+            CHECK(b.stats().hits == c.stats().hits && b.stats().misses == c.stats().misses);
+            CHECK(a.stats().accesses() <= c.stats().accesses() + cfg.microbatch_size);
+            CHECK(s.timings.load_ms.size() == s.result.iterations.size());
+            CHECK(p.timings.compute_ms.size() == p.result.iterations.size());
+        }
+        // empty block lists throw from both executors
+        TieredBlockStore e(opts(8));
+        const HeadVector q(8, 1.0f);
+        bool t1 = false, t2 = false;
+        try { (void)run_sequential(q, std::span<const BlockId>{}, PSAConfig{}, e); } catch (const Error&) { t1 = true; }
+        try { (void)run_pipelined(q, std::span<const BlockId>{}, PSAConfig{}, e); } catch (const Error&) { t2 = true; }
+        CHECK(t1 && t2);
+    }
+    // --- loads overlap compute when both cost real time (test_pipeline.cpp:116-148) ---
+    {
+        std::mt19937_64 rng(7);
+        StoreOptions o = opts(0);
+        o.miss_sleep_ms = 2.5;  // every load misses (capacity 0) and sleeps per miss
+        TieredBlockStore a(o), b(o);
         std::vector<BlockId> ids;
-        for (int i = 0; i < 40; ++i) {
-            auto blk = make_block(rng, i, 0, 8, d);
+        for (int i = 0; i < 32; ++i) {
+            auto blk = make_block(rng, i, 0, 2, 8);
             a.put_block(blk);
             b.put_block(blk);
-            c.put_block(blk);
             ids.push_back(i);
         }
-        HeadVector q(d, 0.2f);
+        const HeadVector q(8, 0.3f);
         PSAConfig cfg;
-        cfg.epsilon = 0.9;
-        cfg.microbatch_size = 3;
-        const auto p = run_pipelined(q, ids, cfg, a);
-        const auto s = run_sequential(q, ids, cfg, b);
-        const auto plain = psa_attention(q, ids, cfg, c);
-        CHECK(p.result.output == s.result.output && s.result.output == plain.output);
-        CHECK(p.result.processed_ids == plain.processed_ids);
-        CHECK(a.stats().hits == c.stats().hits && a.stats().misses == c.stats().misses);
-        for (std::size_t i = 0; i < plain.iterations.size(); ++i) {
-            CHECK(p.result.iterations[i].hits == plain.iterations[i].hits);
-            CHECK(p.result.iterations[i].misses == plain.iterations[i].misses);
+        cfg.epsilon = 1.0;
+        cfg.microbatch_size = 4;
+        cfg.block_size = 2;
+        PipelineOptions po;
+        po.compute_pad_ms = 10.0;
+        const auto s = run_sequential(q, ids, cfg, a, po);
+        const auto p = run_pipelined(q, ids, cfg, b, po);
+        CHECK(p.result.output == s.result.output);
+        const double ratio = p.timings.total_wall_ms / s.timings.total_wall_ms;
+        std::printf("pipeline overlap: sequential %.1f ms, pipelined %.1f ms (ratio %.3f, efficiency %.2f)\n",
+                    s.timings.total_wall_ms, p.timings.total_wall_ms, ratio, p.timings.overlap_efficiency);
+        CHECK(ratio < 0.8);
+        CHECK(p.timings.overlap_efficiency > 1.3);
+        CHECK(s.timings.overlap_efficiency > 0.9 && s.timings.overlap_efficiency < 1.01);
+        CHECK(s.timings.load_ms.size() == 8 && p.timings.compute_ms.size() == 8);
+        for (double x : s.timings.load_ms) CHECK(x >= 9.0);  // 4 misses x 2.5 ms, slept per miss
+    }
+    // --- early termination wastes at most one in-flight microbatch (test_pipeline.cpp:150-179) ---
+    {
+        std::mt19937_64 rng(5150);
+        for (int inst = 0; inst < 12; ++inst) {
+            const std::size_t m = 1 + inst % 4;
+            TieredBlockStore a(opts(0)), b(opts(0));
+            std::vector<BlockId> ids;
+            for (int i = 0; i < 20; ++i) {
+                auto blk = make_block(rng, i, 0, 3, 12);
+                a.put_block(blk);
+                b.put_block(blk);
+                ids.push_back(i);
+            }
+            std::normal_distribution<float> nd;
+            HeadVector q(12);
+            for (auto& x : q) x = 2.0f * nd(rng);
+            PSAConfig cfg;
+            cfg.epsilon = 0.55 + 0.02 * (inst % 5);
+            cfg.microbatch_size = static_cast<std::int32_t>(m);
+            cfg.block_size = 3;
+            const auto s = run_sequential(q, ids, cfg, a);
+            CHECK(a.stats().accesses() == s.result.blocks_processed);
+            const auto p = run_pipelined(q, ids, cfg, b);
+            CHECK(p.result.blocks_processed == s.result.blocks_processed);
+            const auto fetched = b.stats().accesses();
+            CHECK(fetched >= p.result.blocks_processed && fetched <= p.result.blocks_processed + m);
         }
+    }
+    // --- simulate_pipeline reproduces hand-walked schedules (test_pipeline.cpp:181-) ---
+    {
+        const std::vector<double> l2 = {2, 2}, c2 = {3, 3};
+        const PipelineModel m2 = simulate_pipeline(l2, c2);
+        CHECK(m2.sequential_ms == 10.0 && m2.pipelined_ms == 8.0);
+        const std::vector<double> l8(8, 4.0), c8(8, 4.0);
+        const PipelineModel m8 = simulate_pipeline(l8, c8);
+        CHECK(m8.sequential_ms == 64.0 && m8.pipelined_ms == 36.0);
+        const std::vector<double> l3 = {10, 10, 10}, c3 = {1, 1, 1};  // load-dominated
+        CHECK(simulate_pipeline(l3, c3).pipelined_ms == 31.0 && simulate_pipeline(l3, c3).sequential_ms == 33.0);
+        CHECK(simulate_pipeline(c3, l3).pipelined_ms == 31.0);  // compute-dominated: first load exposed
+        const PipelineModel m0 = simulate_pipeline({}, {});
+        CHECK(m0.sequential_ms == 0.0 && m0.pipelined_ms == 0.0 && m0.overlap_efficiency == 1.0);
+        const std::vector<double> one = {1.0};
+        bool threw = false;
+        try { (void)simulate_pipeline(l2, one); } catch (const Error&) { threw = true; }
+        CHECK(threw);
     }
     // --- store: hand-walked LRU + exact trace text (test_store.cpp:108-132, 294-309) ---
     {
@@ -445,6 +657,71 @@ int main() {
             const PSAResult run = psa_attention(q, ids, cfg, store);
             for (std::size_t r = 0; r < run.blocks_processed; ++r) CHECK(run.processed_ids[r] == plan.ranked_ids[r]);
         }
+    }
+    // --- attention.hpp: golden values of the compiled reference + the test_core.cpp KATs ---
+    if (argc > 1) attention_golden(argv[1]);
+    {
+        KVBlock b;
+        b.n_tokens = 2;
+        b.dim = 1;
+        b.keys = {0.0f, std::log(3.0f)};
+        b.values = {1.0f, 5.0f};
+        const HeadVector q = {1.0f};
+        const auto part = block_partial_attention(q, b, 1.0f);  // test_core.cpp:104-125
+        CHECK(std::fabs(part.max_score - std::log(3.0)) < 1e-6);
+        CHECK(std::fabs(part.exp_sum - 4.0 / 3.0) < 1e-6);
+        CHECK(std::fabs(part.log_as - std::log(4.0)) < 1e-6);
+        SoftmaxAccumulator acc;
+        CHECK(acc.empty());
+        bool threw = false;
+        try { (void)finalize(acc); } catch (const Error&) { threw = true; }
+        CHECK(threw);
+        merge_partial(acc, part);  // an empty accumulator absorbs the partial
+        CHECK(acc.exp_sum == part.exp_sum && acc.log_as_acc == part.log_as);
+        CHECK(std::fabs(finalize(acc)[0] - 4.0f) < 1e-6f);
+        KVBlock empty;
+        empty.dim = 1;
+        threw = false;
+        try { (void)block_partial_attention(q, empty, 1.0f); } catch (const Error&) { threw = true; }
+        CHECK(threw);
+        threw = false;
+        try { (void)block_log_as_oracle(HeadVector{1.0f, 2.0f}, b, 1.0); } catch (const Error&) { threw = true; }
+        CHECK(threw);
+        // scores around +-300 stay finite in either merge order (test_core.cpp:250-284)
+        KVBlock big, small;
+        for (KVBlock* x : {&big, &small}) {
+            x->n_tokens = 2;
+            x->dim = 4;
+            x->keys.assign(8, 0.0f);
+            x->values.assign(8, 1.0f);
+        }
+        big.keys[0] = 300.0f, big.keys[4] = 299.0f, small.keys[0] = -300.0f, small.keys[4] = -299.0f;
+        const HeadVector q4 = {1.0f, 0.0f, 0.0f, 0.0f};
+        SoftmaxAccumulator a1, a2;
+        merge_partial(a1, block_partial_attention(q4, small, 1.0f));
+        merge_partial(a1, block_partial_attention(q4, big, 1.0f));
+        merge_partial(a2, block_partial_attention(q4, big, 1.0f));
+        merge_partial(a2, block_partial_attention(q4, small, 1.0f));
+        for (float x : finalize(a1)) CHECK(std::isfinite(x) && std::fabs(x - 1.0f) < 1e-6f);
+        CHECK(a1.log_as_acc > 299.0f && std::isfinite(a1.log_as_acc));
+        CHECK(std::fabs(finalize(a2)[0] - finalize(a1)[0]) < 1e-6f);
+        // exact_attention over token vectors == over the same tokens as one block; default_scale
+        std::vector<HeadVector> ks = {{0.5f, -1.0f}, {2.0f, 0.25f}, {-0.5f, 1.5f}}, vs = {{1.0f, 2.0f}, {3.0f, -1.0f}, {0.0f, 4.0f}};
+        KVBlock all;
+        all.n_tokens = 3;
+        all.dim = 2;
+        for (int t = 0; t < 3; ++t) {
+            all.keys.insert(all.keys.end(), ks[t].begin(), ks[t].end());
+            all.values.insert(all.values.end(), vs[t].begin(), vs[t].end());
+        }
+        const HeadVector q2 = {1.0f, -2.0f};
+        const KVBlock* ptr = &all;
+        CHECK(exact_attention(q2, ks, vs, default_scale(2)) ==
+              exact_attention_blocks(q2, std::span<const KVBlock* const>(&ptr, 1), default_scale(2)));
+        CHECK(std::fabs(dot_scaled<double>(q2, ks[0].data(), 0.5) - 1.25) < 1e-15);
+        threw = false;
+        try { (void)exact_attention(q2, std::span<const HeadVector>{}, std::span<const HeadVector>{}, 1.0); } catch (const Error&) { threw = true; }
+        CHECK(threw);
     }
     std::printf("OK %d\n", g_checks);
     return 0;
