@@ -59,8 +59,12 @@ def parse():
     ap.add_argument("--score-kernel", type=int, default=0, help="0 auto, 1 register-staged, 2 TMA-staged")
     ap.add_argument("--pipeline", type=int, default=1, help="0 auto, 1 off, k sub-batches")
     ap.add_argument("--graph", type=int, default=1, help="1: replay the step as a captured CUDA graph")
+    ap.add_argument("--dense-early", type=float, default=2.0,
+                    help="early dense hand-over of flat heads (nats between ranks 0 and 383; 0 off)")
     ap.add_argument("--plan-only", action="store_true",
                     help="launcher/sharding dry run (no GPU): every rank reports its units over gloo")
+    ap.add_argument("--dropin-units", type=int, default=4,
+                    help="units timed through the drop-in C ABI (psattn_run_multi_head, host buffers); 0: off")
     ap.add_argument("--check", type=int, default=16,
                     help="after timing: units of this rank's step checked against the reference (0: off)")
     return ap.parse_args()
@@ -312,6 +316,38 @@ def check_step(args, p, run, q_host, unit_ids, n, g):
     return r
 
 
+def dropin_e2e(args, p, units, n, g, seconds=2.0):
+    """`e2e_dropin`: the same queries through the reference-facing C ABI — psattn_store (blocks put as
+    host fp32 K/V, reference capi.cpp:134-156) and psattn_run_multi_head (psa_attention_multi_head,
+    engine.cpp:240-260: one kv-head list, its g q-heads) — host q in, host outputs + stats out, one
+    call per unit, every copy and the host-side accounting inside the timed region. This is the call
+    the CPU reference arm makes."""
+    from paper_2503_00392_b200 import capi
+    from workload import synth
+    st = capi.Store(capacity=n * len(units), n_layers=1)
+    lists, qs = [], []
+    for i, uid in enumerate(units):
+        k, v = synth.unit_host(p, uid, args.ctx)
+        st.put_many(i * n, k, v)
+        lists.append(np.arange(i * n, (i + 1) * n, dtype=np.int64))
+        qs.append(np.stack([synth.query(p, uid, h) for h in range(g)]).astype(np.float32))
+    cfg = capi.config_default(epsilon=args.eps, microbatch_size=args.microbatch)
+    for i in range(len(units)):  # warm-up (first call sizes the store's staging buffers)
+        capi.check(st.run_multi_head(qs[i], [lists[i]], cfg)[0])
+    calls, t0 = 0, time.perf_counter()
+    while True:
+        for i in range(len(units)):
+            capi.check(st.run_multi_head(qs[i], [lists[i]], cfg)[0])
+            calls += 1
+        el = time.perf_counter() - t0
+        if el >= seconds:
+            break
+    st.close()
+    return dict(value=calls * g / el, unit=UNIT, calls=calls, seconds=round(el, 3), units=len(units),
+                kv_dtype="f32 (C ABI put_block)",
+                api="psattn_run_multi_head per (request, layer, kv-head) unit, host buffers, g q-heads per call")
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -328,6 +364,7 @@ def run_ours(args):
     capi.check(capi.lib.psattn_set_progressive_kernel(args.psa_kernel))
     capi.check(capi.lib.psattn_set_score_kernel(args.score_kernel))
     capi.check(capi.lib.psattn_set_pipeline(args.pipeline))
+    capi.check(capi.lib.psattn_set_dense_early(args.dense_early))
     from workload import synth
     p = synth_params(args)
     g = args.hq // args.hkv
@@ -518,6 +555,11 @@ def run_ours(args):
     if args.check > 0:
         parity = check_step(args, p, run, q_host, unit_ids, n, g)  # every rank checks a sample of its own units
 
+    # ---- the drop-in C ABI with host buffers (rank 0): psattn_run_multi_head per kv-head unit ----
+    dropin = None
+    if rank == 0 and args.dropin_units > 0:
+        dropin = dropin_e2e(args, p, unit_ids[:: max(1, len(unit_ids) // args.dropin_units)][: args.dropin_units], n, g)
+
     # ---- CPU baseline (rank 0, N=1 only) ----
     cpu_base = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
@@ -568,6 +610,7 @@ def run_ours(args):
             stage_ms_per_step={k: v for k, v in per_launch_ms.items()},
             cpu_baseline=cpu_base, parity=parity, parity_ok=(parity or {}).get("ok"),
             e2e=dict(value=e2e_val, unit=UNIT, h2d_bytes_per_step=h2d, d2h_bytes_per_step=d2h),
+            e2e_dropin=dropin,
             gpu_launches=int(launches_per_step) * args.steps,
             cuda_graph=bool(args.graph), gather=gather,
             clocks=clk, setup=dict(fill_seconds=fill_s, pool_gib=(U * n * (lay.slot_bytes + lay.meta_bytes)) / 2**30),

@@ -199,6 +199,11 @@ int psattn_set_pipeline(int32_t sub_batches);
  * 384 ranks without stopping is redone by one K pass + per-head stop rule + one V pass),
  * 1 = off (the round kernel runs every unit to the end). Same results either way. */
 int psattn_set_dense(int32_t mode);
+/* Early dense hand-over (stream kernel): a unit whose head has criticality scores at ranks 0 and
+ * 383 within `nats` of each other (a flat head, e.g. isotropic keys, that would consume the
+ * hand-over budget without stopping) goes to the dense kernels after its first round. Default 2.0;
+ * 0 = off. Performance only: results are the same either way. */
+int psattn_set_dense_early(float nats);
 /* Score-kernel selection: 0 = auto (TMA-staged for dim 128), 1 = register-staged, 2 = TMA whenever supported. */
 int psattn_set_score_kernel(int32_t mode);
 

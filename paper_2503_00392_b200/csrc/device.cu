@@ -339,7 +339,7 @@ static WsLayout ws_layout(const psattn_batch* b) {
         o += align_up((size_t)b->n_units * b->group * ((b->max_blocks + kDenseSlice - 1) / kDenseSlice) * kDensePart * 4, 256);
         // stream kernel: token weights of every fetched block, [unit][kStreamEnt][4 heads][16] fp32
         l.sw = o;
-        o += align_up((size_t)b->n_units * kStreamEnt * 4 * 16 * 4, 256);
+        o += align_up((size_t)b->n_units * kStreamEnt * kStreamWRow * 4, 256);
     }
     // first tranche of every head (GQA shapes): keys | slots | ntok | count
     l.ft = 0;
@@ -410,6 +410,7 @@ BatchView make_view(const psattn_pool* pool, const psattn_batch* b, void* worksp
     v.omass = v.has_oracle ? reinterpret_cast<double*>(ws + l.omass) : nullptr;
     v.iest = b->iter_est;
     v.kminmax = v.rank_oracle ? nullptr : reinterpret_cast<unsigned long long*>(ws + l.kmm);
+    v.kmm_stride = (int64_t)b->n_units * b->group;
     v.dense_count = l.dflag ? reinterpret_cast<int32_t*>(ws + l.dflag) : nullptr;
     v.dense_flag = l.dflag ? reinterpret_cast<int32_t*>(ws + l.dflag + 256) : nullptr;
     v.dense_la = l.dflag ? reinterpret_cast<float*>(ws + l.dla) : nullptr;
@@ -652,6 +653,12 @@ void psattn_graph_destroy(psattn_graph* g) {
 int psattn_set_dense(int32_t mode) {
     if (mode < 0 || mode > 1) return fail(PSATTN_ERR_INVALID_ARGUMENT, "psattn_set_dense: mode must be 0 or 1");
     set_dense_mode(mode);
+    return PSATTN_OK;
+}
+
+int psattn_set_dense_early(float nats) {
+    if (!(nats >= 0.0f)) return fail(PSATTN_ERR_INVALID_ARGUMENT, "psattn_set_dense_early: threshold must be >= 0");
+    set_dense_early(nats);
     return PSATTN_OK;
 }
 

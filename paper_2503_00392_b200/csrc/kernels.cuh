@@ -73,8 +73,11 @@ struct BatchView {
     // optional [2][n_units*g]: per-head min / max sort key, produced by the score kernel so the
     // first tranche selection skips its min/max scan (nullptr: the selection scans)
     unsigned long long* kminmax;
+    int64_t kmm_stride;  // offset of the max half of kminmax (the full batch's n_units * g)
     // dense hand-over (kernels_dense.cu); dense_flag == nullptr disables it
     int32_t* dense_flag;            // [n_units] list of handed-over units (dense_count entries)
+    float dense_early;              // hand a unit over before its first round when a head's criticality
+                                    // scores at ranks 0 and kDenseHandover-1 differ by less than this (0: off)
     int32_t* dense_count;
     float* dense_la;                // [total*g] fp32 block masses
     float* dense_p;                 // [total*g][16] normalised token weights
@@ -88,11 +91,12 @@ struct BatchView {
     uint8_t* ft_ntok;
     int32_t* ft_count;
     // stream kernel (kernels_stream.cu): token weights of every fetched block of a unit,
-    // [n_units][kStreamEnt][4][16] fp32, bulk-copied back beside the block's V tile
+    // [n_units][kStreamEnt][kStreamWRow] fp32, bulk-copied back beside the block's V tile
     float* stream_w;
 };
 constexpr int kFirstCap = 512;   // == the GQA kernel's tranche capacity
 constexpr int kStreamEnt = 512;  // distinct blocks one unit may fetch on the stream kernel (else hand-over)
+constexpr int kStreamWRow = 64;  // floats per fetched block: token weights [4 heads][16]
 constexpr int64_t kDenseMaxBlocks = 16384;  // decide smem: 12 B per rank (196 KB)
 constexpr int64_t kDenseHandover = 384;     // ranks a head consumes on the round kernel before the hand-over
 constexpr int64_t kDenseSlice = 512;        // list positions per dense K / V work item
@@ -121,6 +125,7 @@ void set_psa_kernel_choice(int choice);
 void set_score_kernel_choice(int choice);
 void set_pipeline_subbatches(int k);
 void set_dense_mode(int mode);  // 0 auto (hand-over enabled), 1 off
+void set_dense_early(float nats);  // stream kernel: early hand-over threshold (0 off)
 bool dense_supported(const PoolView& p, const BatchView& b);
 void launch_dense(const PoolView& p, const BatchView& b, cudaStream_t st);
 // Returns the number of kernel launches issued, or -1 on error (cudaGetLastError has it).

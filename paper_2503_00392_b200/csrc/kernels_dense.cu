@@ -182,11 +182,6 @@ __global__ void __launch_bounds__(kDecideThreads) dense_decide_kernel(BatchView 
 #endif
 constexpr int kBucketPerThread = 32;
 constexpr unsigned kBucketMax = 64;
-__device__ __forceinline__ double key_score(uint64_t k, uint64_t pmask) {
-    const uint64_t asc = ~k | pmask;  // make_key_masked's order-preserving image, position bits set
-    const uint64_t u = (asc >> 63) ? (asc & 0x7FFFFFFFFFFFFFFFull) : ~asc;
-    return __longlong_as_double((long long)u);
-}
 __device__ bool bucket_sort_smem(uint64_t* ks, int n, uint64_t pmask, uint32_t* hist, int nbins) {
     __shared__ unsigned long long s_min, s_max;
     __shared__ unsigned s_big, wsum[32];

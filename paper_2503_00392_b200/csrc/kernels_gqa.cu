@@ -204,7 +204,7 @@ __global__ void __launch_bounds__(kPsaThreads, 2) psa_gqa_kernel(PoolView p, Bat
                 t0 = s.tr0[h] + s.tc[h];
                 tc = select_tranche(s.sel[h], s.tb[h], kGTCap, s.hist[h], kGBins, b.keys + hb, n, s.last[h], t0 == 0,
                                     kGTCap, tm, b.kminmax ? b.kminmax + (size_t)u * g + h : nullptr,
-                                    (int64_t)b.n_units * g);
+                                    b.kmm_stride);
                 fill_tranche(s.tb[h], tc, pmask, b.rpos + hb + t0, b.slots + off, p.ntok, s.tslot[h], s.tntok[h], tm);
             }
             __syncthreads();
@@ -396,7 +396,7 @@ __global__ void __launch_bounds__(kPsaThreads, 2) psa_gqa_kernel(PoolView p, Bat
                 const int64_t cb = s.cb[h] + c0;
                 if (b.has_oracle) {
                     dc = decide_chunk(x, cnt, cb, n, limit, b.m, eps, acc, mn, b.iest ? b.iest + hb : nullptr);
-                } else if (!decide_chunk_fast((float)x, cnt, cb, n, limit, b.m, eps, acc, ssum, mn,
+                } else if (!PSA_DECIDE_FAST || !decide_chunk_fast((float)x, cnt, cb, n, limit, b.m, eps, acc, ssum, mn,
                                               b.iest ? b.iest + hb : nullptr, dc)) {
                     // fp64 fallback: carried (M, S) -> log-sum-exp and back (M' = lse, S' = 1)
                     acc = ssum > 0.0 ? acc + log(ssum) : -INFINITY;
@@ -657,7 +657,7 @@ __global__ void __launch_bounds__(kPsaThreads) first_tranche_kernel(PoolView p, 
     const uint64_t pmask = (b.pos_bits >= 64) ? ~0ull : ((1ull << b.pos_bits) - 1ull);
     const Team tm = cta_team();
     const int tc = select_tranche(sel, tb, kGTCap, hist, kGBins, b.keys + hb, n, 0, true, kGTCap, tm,
-                                  b.kminmax ? b.kminmax + qi : nullptr, (int64_t)b.n_units * b.g);
+                                  b.kminmax ? b.kminmax + qi : nullptr, b.kmm_stride);
     fill_tranche(tb, tc, pmask, b.rpos + hb, b.slots + off, p.ntok, b.ft_slot + (size_t)qi * kGTCap,
                  b.ft_ntok + (size_t)qi * kGTCap, tm);
     for (int i = threadIdx.x; i < tc; i += blockDim.x) b.ft_keys[(size_t)qi * kGTCap + i] = tb[i];

@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(kPsaThreads, 3) psa_kernel(PoolView p, BatchVi
             tr0 += tc;
             tc = select_tranche(s.sel, s.tb, kTCap, s.hist, kBins, keys, n, last, tr0 == 0, tr0 == 0 ? kFirstTranche : kTCap,
                                 cta_team(), b.kminmax ? b.kminmax + (size_t)u * b.g + h : nullptr,
-                                (int64_t)b.n_units * b.g);
+                                b.kmm_stride);
             last = s.tb[tc - 1];
             fill_tranche(s.tb, tc, pmask, b.rpos + hb + tr0, b.slots + off, p.ntok, s.tslot, s.tntok, cta_team());
             __syncthreads();
@@ -250,7 +250,7 @@ __global__ void __launch_bounds__(kPsaThreads, 3) psa_kernel(PoolView p, BatchVi
             Decision dc;
             if (omass) {
                 dc = decide_chunk(x, cnt, cb, n, limit, b.m, eps, acc, mn, b.iest ? b.iest + hb : nullptr);
-            } else if (!decide_chunk_fast((float)x, cnt, cb, n, limit, b.m, eps, acc, ssum, mn,
+            } else if (!PSA_DECIDE_FAST || !decide_chunk_fast((float)x, cnt, cb, n, limit, b.m, eps, acc, ssum, mn,
                                           b.iest ? b.iest + hb : nullptr, dc)) {
                 acc = ssum > 0.0 ? acc + log(ssum) : -INFINITY;  // fp64 fallback (see kernels_gqa.cu)
                 dc = decide_chunk(x, cnt, cb, n, limit, b.m, eps, acc, mn, b.iest ? b.iest + hb : nullptr);
@@ -374,12 +374,15 @@ int psa_kernel_choice() { return g_psa_choice; }
 
 static int g_dense_mode = 0;
 void set_dense_mode(int mode) { g_dense_mode = mode; }
+static float g_dense_early = 2.0f;
+void set_dense_early(float nats) { g_dense_early = nats; }
 
 int launch_psa(const PoolView& p, const BatchView& b, cudaStream_t st) {
     if (g_psa_choice != 1 && gqa_supported(p, b)) {  // auto = GQA-group kernel where supported
         BatchView v = b;
         const bool dense = g_dense_mode == 0 && dense_supported(p, b);
         if (!dense) v.dense_flag = nullptr;
+        v.dense_early = g_dense_early;
         if (dense) cudaMemsetAsync(v.dense_count, 0, 4, st);
         const int n = launch_gqa(p, v, st);
         if (!dense) return n;

@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(kScoreWarps * 32, 2) score_kernel(PoolView p, 
     }
     if (b.kminmax && writer && kmax != 0) {
         atomicMin(b.kminmax + (size_t)u * b.g + my_h, (unsigned long long)kmin);
-        atomicMax(b.kminmax + (size_t)(b.n_units + u) * b.g + my_h, (unsigned long long)kmax);
+        atomicMax(b.kminmax + b.kmm_stride + (size_t)u * b.g + my_h, (unsigned long long)kmax);
     }
 }
 
@@ -472,7 +472,7 @@ __global__ void __launch_bounds__(kScoreWarps * 32, 2) score_kernel_tma(PoolView
     }
     if (b.kminmax && writer && kmax != 0) {
         atomicMin(b.kminmax + (size_t)u * b.g + my_h, (unsigned long long)kmin);
-        atomicMax(b.kminmax + (size_t)(b.n_units + u) * b.g + my_h, (unsigned long long)kmax);
+        atomicMax(b.kminmax + b.kmm_stride + (size_t)u * b.g + my_h, (unsigned long long)kmax);
     }
 }
 
@@ -632,7 +632,7 @@ void set_pipeline_subbatches(int k) { g_pipeline = k; }
 
 // Units [u0, u0 + cnt) of a batch: unit-indexed arrays are offset, the workspace
 // (keys / ranked positions / masses, indexed by absolute list offsets) is shared.
-static BatchView sub_view(const BatchView& b, int u0, int cnt) {
+static BatchView sub_view(const BatchView& b, int u0, int cnt, int idx) {
     BatchView v = b;
     const size_t qo = (size_t)u0 * b.g;
     v.n_units = cnt;
@@ -643,11 +643,15 @@ static BatchView sub_view(const BatchView& b, int u0, int cnt) {
     v.est = b.est + qo;
     v.tcov = b.tcov ? b.tcov + qo : nullptr;
     v.term = b.term + qo;
-    v.kminmax = nullptr;  // unit-indexed [2][n_units*g]: not carved per sub-batch
-    if (b.dense_flag) {
-        v.dense_flag = nullptr;  // the hand-over list is per launch: sub-batches run the round kernel only
-        v.dense_count = nullptr;
+    if (b.kminmax) v.kminmax = b.kminmax + qo;  // (the max half stays kmm_stride further)
+    if (b.dense_flag) {  // each sub-batch keeps its own hand-over list and counter
+        v.dense_flag = b.dense_flag + u0;
+        v.dense_count = b.dense_count + idx;
+        v.dense_thr = b.dense_thr + qo;
+        // the workspace holds ceil(max_n / kDenseSlice) partial states per head (the most any slicing uses)
+        v.dense_part = b.dense_part + qo * (size_t)((b.max_n + kDenseSlice - 1) / kDenseSlice) * kDensePart;
     }
+    if (b.stream_w) v.stream_w = b.stream_w + (size_t)u0 * kStreamEnt * kStreamWRow;
     if (b.ft_keys) {  // head-indexed [n_units*g][kFirstCap]: offset to the sub-batch's heads
         v.ft_keys = b.ft_keys + qo * kFirstCap;
         v.ft_slot = b.ft_slot + qo * kFirstCap;
@@ -731,13 +735,18 @@ int launch_batch(const PoolView& p, const BatchView& b, cudaStream_t st, cudaEve
         }();
         g_score_smem_floor = floor_env;
         if (marks) cudaEventRecord(marks[1], st);
+        if (b.kminmax) {
+            const size_t nq = (size_t)b.n_units * b.g;
+            cudaMemsetAsync(b.kminmax, 0xff, nq * 8, st);
+            cudaMemsetAsync(b.kminmax + nq, 0, nq * 8, st);
+        }
         cudaEventRecord(r.ev[0], st);
         cudaStreamWaitEvent(r.aux, r.ev[0], 0);
         const int per = (b.n_units + subs - 1) / subs;
         int i = 0;
         for (int u0 = 0; u0 < b.n_units; u0 += per, ++i) {
             const int cnt = (b.n_units - u0) < per ? (b.n_units - u0) : per;
-            const BatchView v = sub_view(b, u0, cnt);
+            const BatchView v = sub_view(b, u0, cnt, i);
             launch_score_stage(p, v, st);
             cudaEventRecord(r.ev[1 + i], st);
             cudaStreamWaitEvent(r.aux, r.ev[1 + i], 0);

@@ -67,12 +67,21 @@ constexpr int kWS0 = 2, kWV0 = 2 + kNS;  // first scorer / V warp
 #ifndef PSA_STREAM_LOOK
 #define PSA_STREAM_LOOK 2
 #endif
+#ifndef PSA_STREAM_PF
+#define PSA_STREAM_PF 0
+#endif
+#ifndef PSA_STREAM_PARK
+#define PSA_STREAM_PARK 0  // producer park bound (ns) on the next decision when idle; 0 = nanosleep(64)
+#endif
 constexpr int kRK = PSA_STREAM_RK;  // K ring stages (4 KB K tile)
 constexpr int kRV = PSA_STREAM_RV;  // V ring stages (4 KB V tile + the block's token weights)
 constexpr int kLR = 8;              // round slots in flight
 constexpr int kENT = kStreamEnt;    // distinct blocks per unit
 constexpr int kHash = 2 * kENT;     // list position -> entry (open addressing)
 constexpr int kLook = PSA_STREAM_LOOK;
+// V reference R of a head: its top criticality score + kVRef. Kept while the rank-0 block's max is
+// at least R - kVLow and no scored block's max exceeds R + kVHigh; otherwise the unit is redone densely.
+constexpr float kVRef = 8.0f, kVLow = 40.0f, kVHigh = 60.0f;
 static_assert(kLook + 2 <= kLR, "round slots must cover the lookahead");
 // Entry e is consumed by scorer e % kNS from K stage e % kRK (V item j: V warp j % kNV, stage
 // j % kRV). With the ring a multiple of the consumer count, a stage's previous use belongs to
@@ -84,9 +93,9 @@ template <int G>
 struct Smem {
     alignas(1024) unsigned char kring[kRK][4096];
     alignas(1024) unsigned char vring[kRV][4096];
-    alignas(16) float vw[kRV][G][16];  // token weights beside each V tile
-    float em[kENT][G];                 // block max per (entry, head)
-    float el[kENT][G];                 // block exp-sum
+    alignas(16) float vw[kRV][G * 16];  // token weights beside each V tile
+    float em[kENT][G];                 // block log mass per (entry, head) (the stop rule's observation)
+    float el[kENT][G];                 // block exp-sum relative to the head's V reference R_h
     int32_t eslot[kENT];
     int32_t epos[kENT];
     uint32_t vmask[kENT];  // heads that committed the entry (decider)
@@ -99,8 +108,10 @@ struct Smem {
     int32_t r_live[kLR], r_vc[kLR], r_stop[kLR];  // decider -> producer, per decided round
     int16_t vq[kENT + kNV];  // V items in creation order (entry), -1 = end
     int32_t handover;
+    int32_t vref_bad;    // a head's V reference does not fit its blocks (extreme logits): dense redo
+    int32_t rank0[G];    // entry of each head's rank-0 block (set with round 0)
     int32_t dbg_flag;
-    float mpart[kNV][G], lpart[kNV][G];
+    float lpart[kNV][G];
     uint64_t kfull[kRK], kempty[kRK], vfull[kRV], vempty[kRV];
     uint64_t rpub[kLR], rscored[kLR], rdec[kLR];
 };
@@ -150,15 +161,14 @@ __device__ __forceinline__ uint32_t swz(uint32_t base, int r, int c) {
     return base + (uint32_t)((c >> 3) * 2048 + r * 128 + (((c & 7) ^ (r & 7)) << 4));
 }
 // Term `part` (0..2) of the exact 3-term bf16 split of a and b, packed (a low); part 3 -> 0.
+// Branch-free: every lane computes the three terms and selects its own (lanes hold different parts).
 __device__ __forceinline__ uint32_t pack_split3(float a, float b, int part) {
-    if (part >= 3) return 0u;
-    uint32_t p = pack_bf16x2(a, b);
-    for (int i = 0; i < part; ++i) {
-        a -= __uint_as_float(p << 16);
-        b -= __uint_as_float(p & 0xFFFF0000u);
-        p = pack_bf16x2(a, b);
-    }
-    return p;
+    const uint32_t p1 = pack_bf16x2(a, b);
+    const float a1 = a - __uint_as_float(p1 << 16), b1 = b - __uint_as_float(p1 & 0xFFFF0000u);
+    const uint32_t p2 = pack_bf16x2(a1, b1);
+    const float a2 = a1 - __uint_as_float(p2 << 16), b2 = b1 - __uint_as_float(p2 & 0xFFFF0000u);
+    const uint32_t p3 = pack_bf16x2(a2, b2);
+    return part == 0 ? p1 : part == 1 ? p2 : part == 2 ? p3 : 0u;
 }
 
 #ifdef PSA_STREAM_DEBUG
@@ -232,7 +242,7 @@ __global__ void __launch_bounds__(kThreads, 2) psa_stream_kernel(const __grid_co
     long long pw[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     const long long t_start = clock64();
 #endif
-    float* wg = b.stream_w + (size_t)u * kENT * 64;  // this unit's weights, 64 floats per entry
+    float* wg = b.stream_w + (size_t)u * kENT * kStreamWRow;  // this unit's weight rows
 
     if (tid == 0) {
         for (int i = 0; i < kRK; ++i) {
@@ -249,7 +259,9 @@ __global__ void __launch_bounds__(kThreads, 2) psa_stream_kernel(const __grid_co
             mbar_init(&s.rdec[i], 1);
         }
         s.handover = 0;
+        s.vref_bad = 0;
         s.dbg_flag = 0;
+        for (int h = 0; h < G; ++h) s.rank0[h] = -1;
         fence_mbar_init();
     }
     __syncthreads();
@@ -338,6 +350,11 @@ __global__ void __launch_bounds__(kThreads, 2) psa_stream_kernel(const __grid_co
                     closed = true;
                 } else {
                     if (isnew) {
+#if PSA_STREAM_PF
+                        // the entry's K and V (one contiguous slot) start towards L2 now, kLook rounds
+                        // before the K tile is needed: the K ring then refills from L2
+                        prefetch_l2_bulk(p.kv + (int64_t)fslot * p.slot_bytes, (uint32_t)p.slot_bytes);
+#endif
                         ent = E + __popc(nb & ((1u << lane) - 1u));
                         s.hval[hs] = (int16_t)ent;
                         s.eslot[ent] = fslot;
@@ -348,6 +365,7 @@ __global__ void __launch_bounds__(kThreads, 2) psa_stream_kernel(const __grid_co
                     }
                     const int myent = __shfl_sync(PSA_FULL, ent, leader);
                     s.r_map[rs][lane] = (int16_t)(valid ? myent : -1);
+                    if (k_pub == 0 && i == 0 && valid) s.rank0[h] = myent;
                     if (lane == 0) {
                         s.r_e0[rs] = E;
                         s.r_cnt[rs] = cnt;
@@ -392,7 +410,7 @@ __global__ void __launch_bounds__(kThreads, 2) psa_stream_kernel(const __grid_co
                     const uint32_t dst = smem_u32(s.vring[st]);
                     tma_tile(dst, &kvmap, 0, y, &s.vfull[st]);
                     tma_tile(dst + 2048, &kvmap, 64, y, &s.vfull[st]);
-                    bulk_g2s(smem_u32(&s.vw[st][0][0]), wg + (size_t)e * 64, kWB, &s.vfull[st]);
+                    bulk_g2s(smem_u32(&s.vw[st][0]), wg + (size_t)e * kStreamWRow, kWB, &s.vfull[st]);
                 }
                 v_issued += pc;
                 progress |= pc > 0;
@@ -417,7 +435,18 @@ __global__ void __launch_bounds__(kThreads, 2) psa_stream_kernel(const __grid_co
             ++pw[progress ? 7 : 6];
 #endif
             if (!progress) {
+#if PSA_STREAM_PARK
+                // nothing to issue: park on the next round's decision (the usual next event) for a
+                // bounded time instead of spinning through the loop
+                if (decided + 1 < k_pub)
+                    (void)__shfl_sync(PSA_FULL, lane == 0 ? (int)mbar_try_wait_for(&s.rdec[(decided + 1) % kLR],
+                                                                                   ((decided + 1) / kLR) & 1, PSA_STREAM_PARK)
+                                                          : 0, 0);
+                else
+                    __nanosleep(64);
+#else
                 __nanosleep(64);
+#endif
 #ifdef PSA_STREAM_DEBUG
                 if (++idle == (1 << 22)) {
                     if (lane == 0) {
@@ -454,17 +483,32 @@ __global__ void __launch_bounds__(kThreads, 2) psa_stream_kernel(const __grid_co
         bool live = hv;
         int64_t cb = 0;
         int vc = 0;  // V items created
+        // a flat head (criticality within dense_early nats over its top kDenseHandover ranks, e.g.
+        // isotropic keys) would consume the hand-over budget without stopping: the unit goes to the
+        // dense kernels after its first round instead of after kDenseHandover ranks (performance
+        // only: both paths produce the same processed sets)
+        bool flat = false;
+        if (b.dense_early > 0.0f && hv && i == 0 && ftc >= kDenseHandover && limit > kDenseHandover) {
+            const uint64_t pm = (b.pos_bits >= 64) ? ~0ull : ((1ull << b.pos_bits) - 1ull);
+            const double s0 = key_score(b.ft_keys[qi * kFirstCap], pm);
+            const double s1 = key_score(b.ft_keys[qi * kFirstCap + kDenseHandover - 1], pm);
+            flat = s0 - s1 < (double)b.dense_early;
+        }
+        const bool flat_unit = __any_sync(PSA_FULL, flat);
         double M = -INFINITY, S = 0.0, mn = INFINITY, est = 0.0;
         for (int k = 0;; ++k) {
             const int rs = k % kLR;
             SWAIT(&s.rscored[rs], (k / kLR) & 1, 2, k, (int)cb, vc, (int)live, 0, 0, 0, 0);
+#ifdef PSA_STREAM_PROF
+            const long long td0_ = clock64();
+#endif
             const int e = s.r_map[rs][lane];
             const int e_end = s.r_e0[rs] + s.r_cnt[rs];  // entries published up to this round
             const bool overflow = s.r_flag[rs] == 1;
             const int64_t r = cb + i;
             const bool valid = live && e >= 0 && r < limit;
             double x = -INFINITY;
-            if (valid) x = b.has_oracle ? b.omass[hb + s.epos[e]] : (double)(s.em[e][h] + logf(s.el[e][h]));
+            if (valid) x = b.has_oracle ? b.omass[hb + s.epos[e]] : (double)s.em[e][h];
             // segment (C lanes = one head) scan in fp64: running log-sum-exp carried as (max M, sum S)
             double mx = x;
 #pragma unroll
@@ -527,7 +571,7 @@ __global__ void __launch_bounds__(kThreads, 2) psa_stream_kernel(const __grid_co
             }
             // a head that used up its first tranche (or kDenseHandover ranks), or a unit whose
             // distinct blocks overflow the entry table, is handed over to the dense kernels
-            const bool ho = live && cb < limit && (cb >= kDenseHandover || cb >= ftc || overflow);
+            const bool ho = live && cb < limit && (cb >= kDenseHandover || cb >= ftc || overflow || flat_unit);
             const bool anyho = __any_sync(PSA_FULL, ho);
             const unsigned lb = __ballot_sync(PSA_FULL, live && i == 0);
             uint32_t lmask = 0;
@@ -573,6 +617,9 @@ __global__ void __launch_bounds__(kThreads, 2) psa_stream_kernel(const __grid_co
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&s.rdec[rs]);
+#ifdef PSA_STREAM_PROF
+            pw[6] += clock64() - td0_;
+#endif
             if (done) break;
         }
     } else if (warp < kWV0) {
@@ -594,6 +641,19 @@ __global__ void __launch_bounds__(kThreads, 2) psa_stream_kernel(const __grid_co
                     qg[st][t][hf] = pack_split3(a, c, sp);
                 }
         }
+        // V reference of the epilogue's head (2t + tq/2): the token weights handed to the V pass are
+        // exp(s - R_h) with one fixed R_h per head (its top criticality score + kVRef), so the V warps
+        // accumulate every committed block as is. Deterministic; checked against the blocks' actual
+        // maxima (the rank-0 block within kVLow below R_h, no block more than kVHigh above it), else
+        // the unit is redone by the dense kernels (per-block maxima).
+        float vref[NT];
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+            const int hq = 2 * t + (tq >> 1);
+            const size_t qh = (size_t)u * g + (hq < g ? hq : 0);
+            const uint64_t pm = (b.pos_bits >= 64) ? ~0ull : ((1ull << b.pos_bits) - 1ull);
+            vref[t] = b.ft_count[qh] > 0 ? (float)key_score(b.ft_keys[qh * kFirstCap], pm) + kVRef : 0.0f;
+        }
         for (int k = 0;; ++k) {
             const int rs = k % kLR;
             SWAIT(&s.rpub[rs], (k / kLR) & 1, 3, k, 0, 0, 0, 0, 0, 0, 0);
@@ -603,23 +663,37 @@ __global__ void __launch_bounds__(kThreads, 2) psa_stream_kernel(const __grid_co
             for (int e = e0 + ((sidx - e0 % kNS) + kNS) % kNS; e < e0 + cnt; e += kNS) {
                 const int st = e % kRK;
                 SWAIT(&s.kfull[st], (e / kRK) & 1, 4, k, e, e0, cnt, 0, 0, 0, 0);
+#ifdef PSA_STREAM_PROF
+                const long long tq0_ = clock64();
+#endif
                 const uint32_t kb = smem_u32(s.kring[st]);
                 const int nt = s.entok[e];
-                float c[NT][4];
+                // two accumulator sets (even / odd k-steps): halves the dependent MMA chain
+                float c[NT][4], c2[NT][4];
 #pragma unroll
-                for (int t = 0; t < NT; ++t) c[t][0] = c[t][1] = c[t][2] = c[t][3] = 0.0f;
+                for (int t = 0; t < NT; ++t)
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) c[t][r] = c2[t][r] = 0.0f;
 #pragma unroll
                 for (int kst = 0; kst < 8; ++kst) {
                     uint32_t a0, a1, a2, a3;
                     ldsm4(swz(kb, lane & 15, 2 * kst + (lane >> 4)), a0, a1, a2, a3);
 #pragma unroll
-                    for (int t = 0; t < NT; ++t)
-                        mma_bf16_16816(c[t][0], c[t][1], c[t][2], c[t][3], a0, a1, a2, a3, qg[kst][t][0],
-                                       qg[kst][t][1]);
+                    for (int t = 0; t < NT; ++t) {
+                        float(&cc)[4] = (kst & 1) ? c2[t] : c[t];
+                        mma_bf16_16816(cc[0], cc[1], cc[2], cc[3], a0, a1, a2, a3, qg[kst][t][0], qg[kst][t][1]);
+                    }
                 }
+#pragma unroll
+                for (int t = 0; t < NT; ++t)
+#pragma unroll
+                    for (int r = 0; r < 4; ++r) c[t][r] += c2[t][r];
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&s.kempty[st]);  // the tile is in registers: release it
-                float* we = wg + (size_t)e * 64;
+#ifdef PSA_STREAM_PROF
+                pw[6] += clock64() - tq0_;
+#endif
+                float* we = wg + (size_t)e * kStreamWRow;
 #pragma unroll
                 for (int t = 0; t < NT; ++t) {
                     float lo = c[t][0] + c[t][1], hi = c[t][2] + c[t][3];
@@ -636,54 +710,76 @@ __global__ void __launch_bounds__(kThreads, 2) psa_stream_kernel(const __grid_co
                     float lbv = wlo + whi;
 #pragma unroll
                     for (int o = 4; o < 32; o <<= 1) lbv += __shfl_xor_sync(PSA_FULL, lbv, o);
+                    const float R = vref[t];
+                    const float fv = expf(mbv - R);  // block max -> the head's V reference
+                    if (mbv > R + kVHigh || (k == 0 && e == s.rank0[hq] && mbv < R - kVLow)) s.vref_bad = 1;
                     if ((tq & 1) == 0) {
-                        we[hq * 16 + gq] = wlo;
-                        we[hq * 16 + gq + 8] = whi;
+                        we[hq * 16 + gq] = wlo * fv;
+                        we[hq * 16 + gq + 8] = whi * fv;
                         if (gq == 0) {
-                            s.em[e][hq] = mbv;
-                            s.el[e][hq] = lbv;
+                            s.em[e][hq] = mbv + logf(lbv);  // log_as (attention.hpp:73)
+                            s.el[e][hq] = lbv * fv;
                         }
                     }
                 }
             }
             // the weights are read back by the async proxy (bulk copy beside the V tile)
+#ifdef PSA_STREAM_PROF
+            const long long tq1_ = clock64();
+#endif
             asm volatile("fence.proxy.async.global;" ::: "memory");
             __syncwarp();
             if (lane == 0) mbar_arrive(&s.rscored[rs]);
+#ifdef PSA_STREAM_PROF
+            pw[7] += clock64() - tq1_;
+#endif
         }
     } else {
         // ================================== V ==================================
+        // The scorers hand over token weights exp(s - R_h) relative to one fixed reference per head,
+        // so a committed block is accumulated as is: acc += V^T w (exact 3-term bf16 split of w,
+        // mma.sync into fp32 accumulators, one column per split term, summed once at the end) and
+        // L_h += its exponent sum. Heads that did not commit the block get zero weights.
         const int vidx = warp - kWV0;
         const int gq = lane >> 2, tq = lane & 3;
-        float O[NT][8], Mh[NT], Lh[NT];
+        float acc[NT][8][4];
+        float Lh[G];
 #pragma unroll
-        for (int t = 0; t < NT; ++t) {
-            Mh[t] = -INFINITY;
-            Lh[t] = 0.0f;
+        for (int h = 0; h < G; ++h) Lh[h] = 0.0f;
 #pragma unroll
-            for (int j = 0; j < 8; ++j) O[t][j] = 0.0f;
-        }
+        for (int t = 0; t < NT; ++t)
+#pragma unroll
+            for (int mt = 0; mt < 8; ++mt) acc[t][mt][0] = acc[t][mt][1] = acc[t][mt][2] = acc[t][mt][3] = 0.0f;
         const int tok = (lane & 7) + ((lane >> 4) << 3);  // ldmatrix.trans row (token) of this lane
         const int chi = (lane >> 3) & 1;                   // + dim chunk
         for (int j = vidx;; j += kNV) {
             const int st = j % kRV;
             SWAIT(&s.vfull[st], (j / kRV) & 1, 5, j, 0, 0, 0, 0, 0, 0, 0);
+#ifdef PSA_STREAM_PROF
+            const long long tp0_ = clock64();
+#endif
             const int e = s.vq[j];
             if (e < 0) break;
             const uint32_t mask = s.vmask[e];
             const int nt = s.entok[e];
+#pragma unroll
+            for (int h = 0; h < G; ++h)
+                if ((mask >> h) & 1u) Lh[h] += s.el[e][h];
             uint32_t bw[NT][2];
 #pragma unroll
             for (int t = 0; t < NT; ++t) {
                 const int hq = 2 * t + (gq >> 2), sp = gq & 3;
                 const bool on = (mask >> hq) & 1u;
-                const float2 wl = on ? *reinterpret_cast<const float2*>(&s.vw[st][hq][2 * tq]) : make_float2(0.f, 0.f);
-                const float2 wh = on ? *reinterpret_cast<const float2*>(&s.vw[st][hq][2 * tq + 8]) : make_float2(0.f, 0.f);
-                bw[t][0] = pack_split3(wl.x, wl.y, sp);
-                bw[t][1] = pack_split3(wh.x, wh.y, sp);
+                const float2 wl = *reinterpret_cast<const float2*>(&s.vw[st][hq * 16 + 2 * tq]);
+                const float2 wh = *reinterpret_cast<const float2*>(&s.vw[st][hq * 16 + 2 * tq + 8]);
+                bw[t][0] = on ? pack_split3(wl.x, wl.y, sp) : 0u;
+                bw[t][1] = on ? pack_split3(wh.x, wh.y, sp) : 0u;
             }
+#ifdef PSA_STREAM_PROF
+            const long long tp1_ = clock64();
+            pw[6] += tp1_ - tp0_;
+#endif
             const uint32_t vb = smem_u32(s.vring[st]);
-            float val[NT][8];
 #pragma unroll
             for (int mt = 0; mt < 8; ++mt) {
                 uint32_t a0, a1, a2, a3;
@@ -697,33 +793,26 @@ __global__ void __launch_bounds__(kThreads, 2) psa_stream_kernel(const __grid_co
                     a3 &= m1;
                 }
 #pragma unroll
-                for (int t = 0; t < NT; ++t) {
-                    float c0 = 0.f, c1 = 0.f, c2 = 0.f, c3 = 0.f;
-                    mma_bf16_16816(c0, c1, c2, c3, a0, a1, a2, a3, bw[t][0], bw[t][1]);
-                    // lane pair (tq, tq^1) holds the 4 split columns of head 2t + tq/2: the even
-                    // lane keeps dim gq, the odd lane dim gq + 8
-                    const float x = (tq & 1) ? (c0 + c1) : (c2 + c3);
-                    const float y = __shfl_xor_sync(PSA_FULL, x, 1);
-                    val[t][mt] = ((tq & 1) ? (c2 + c3) : (c0 + c1)) + y;
-                }
+                for (int t = 0; t < NT; ++t)
+                    mma_bf16_16816(acc[t][mt][0], acc[t][mt][1], acc[t][mt][2], acc[t][mt][3], a0, a1, a2, a3,
+                                   bw[t][0], bw[t][1]);
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&s.vempty[st]);
-#pragma unroll
-            for (int t = 0; t < NT; ++t) {
-                const int hq = 2 * t + (tq >> 1);
-                if ((mask >> hq) & 1u) {
-                    const float mb = s.em[e][hq];
-                    const float mnew = fmaxf(Mh[t], mb);
-                    const float a = expf(Mh[t] - mnew);
-                    const float cc = expf(mb - mnew);
-#pragma unroll
-                    for (int mt = 0; mt < 8; ++mt) O[t][mt] = O[t][mt] * a + val[t][mt] * cc;
-                    Lh[t] = Lh[t] * a + s.el[e][hq] * cc;
-                    Mh[t] = mnew;
-                }
-            }
+#ifdef PSA_STREAM_PROF
+            pw[7] += clock64() - tp1_;
+#endif
         }
+        // sum the split columns: lane pair (tq, tq^1) holds the 4 columns of head 2t + tq/2
+        float O[NT][8];
+#pragma unroll
+        for (int t = 0; t < NT; ++t)
+#pragma unroll
+            for (int mt = 0; mt < 8; ++mt) {
+                const float x = (tq & 1) ? (acc[t][mt][0] + acc[t][mt][1]) : (acc[t][mt][2] + acc[t][mt][3]);
+                const float y = __shfl_xor_sync(PSA_FULL, x, 1);
+                O[t][mt] = ((tq & 1) ? (acc[t][mt][2] + acc[t][mt][3]) : (acc[t][mt][0] + acc[t][mt][1])) + y;
+            }
         // ---- merge the V warps' states per head (finalize, attention.hpp:104-110) ----
         asm volatile("bar.sync 1, %0;" ::"r"(kNV * 32) : "memory");  // every V tile consumed
         float* part = reinterpret_cast<float*>(&s.vring[0][0]);     // [kNV][G][128]
@@ -732,26 +821,23 @@ __global__ void __launch_bounds__(kThreads, 2) psa_stream_kernel(const __grid_co
             const int hq = 2 * t + (tq >> 1);
 #pragma unroll
             for (int mt = 0; mt < 8; ++mt) part[(vidx * G + hq) * 128 + 16 * mt + gq + 8 * (tq & 1)] = O[t][mt];
-            if (gq == 0 && (tq & 1) == 0) {
-                s.mpart[vidx][hq] = Mh[t];
-                s.lpart[vidx][hq] = Lh[t];
-            }
+            if (gq == 0 && (tq & 1) == 0) s.lpart[vidx][hq] = (tq >> 1) ? Lh[2 * t + 1] : Lh[2 * t];
         }
         asm volatile("bar.sync 1, %0;" ::"r"(kNV * 32) : "memory");
-        if (!s.handover) {
+        if (!s.handover && s.vref_bad) {
+            // extreme logits: a head's criticality-based reference does not fit its blocks' maxima
+            // (fp32 weights could overflow or the dominant blocks underflow): the dense kernels redo it
+            if (tid == kWV0 * 32) b.dense_flag[atomicAdd(b.dense_count, 1)] = u;
+        } else if (!s.handover) {
             for (int idx = tid - kWV0 * 32; idx < g * 128; idx += kNV * 32) {
                 const int hq = idx >> 7, dd = idx & 127;
-                float Mt = -INFINITY;
-#pragma unroll
-                for (int w = 0; w < kNV; ++w) Mt = fmaxf(Mt, s.mpart[w][hq]);
-                float Lt = 0.0f, o = 0.0f;
+                float Lt = 0.0f, o = 0.0f;  // every V warp's state shares the head's reference: plain sums
 #pragma unroll
                 for (int w = 0; w < kNV; ++w) {
-                    const float sc = s.lpart[w][hq] > 0.0f ? expf(s.mpart[w][hq] - Mt) : 0.0f;
-                    Lt += s.lpart[w][hq] * sc;
-                    o += sc > 0.0f ? part[(w * G + hq) * 128 + dd] * sc : 0.0f;
+                    Lt += s.lpart[w][hq];
+                    o += part[(w * G + hq) * 128 + dd];
                 }
-                b.out[((size_t)u * g + hq) * 128 + dd] = o / Lt;
+                b.out[((size_t)u * g + hq) * 128 + dd] = o / Lt;  // finalize (attention.hpp:104-110)
             }
         }
     }

@@ -401,6 +401,12 @@ __device__ __forceinline__ Decision decide_chunk(double x, int cnt, int64_t cb, 
 // differ from the fp64 reference only within ~1e-7 of eps (the parity rule's tau is 1e-5).
 // Returns false, leaving every argument untouched, when a chunk mass sits > 80 below the
 // chunk maximum (fp32 exp would lose it): the caller then runs decide_chunk in fp64.
+// PSA_DECIDE_FAST = 0 (default): the round and per-head kernels decide in fp64 throughout, so the
+// reported estimated_coverage carries fp64 accuracy like the reference's CoverageEstimator;
+// 1 = the fp32 chunk scan below (measured faster on the round kernel, ~1e-7 relative estimate).
+#ifndef PSA_DECIDE_FAST
+#define PSA_DECIDE_FAST 0
+#endif
 __device__ __forceinline__ bool decide_chunk_fast(float x, int cnt, int64_t cb, int64_t n, int64_t limit, int m,
                                                   double eps, double& M, double& S, double& mn, double* iest_head,
                                                   Decision& d) {

@@ -305,20 +305,26 @@ void TieredBlockStore::run_device(const detail::DeviceQueryBatch& qb, detail::De
     const int n_units = static_cast<int>(qb.lists.size());
     if (n_units == 0) throw Error("batched attention: empty batch");
     auto pit = pools_.find(d);
-    // Resolve ids -> slots, ascending-id order per list.
+    // Resolve ids -> slots (one lookup per id), ascending-id order per list; lists that arrive
+    // sorted (the usual page-table order) skip the sort.
     std::vector<std::vector<BlockId>> sorted(n_units);
+    std::vector<std::vector<std::int32_t>> slot_of(n_units);
     std::vector<std::int64_t> off(n_units + 1, 0);
     std::int64_t max_n = 0;
     for (int u = 0; u < n_units; ++u) {
         const auto& ids = qb.lists[u];
         if (ids.empty()) throw Error("plan_blocks: no blocks given");
-        for (BlockId id : ids) {
-            auto it = blocks_.find(id);
-            if (it == blocks_.end()) throw NotFoundError("metadata: unknown block id " + std::to_string(id));
+        auto& srt = sorted[u];
+        auto& sl = slot_of[u];
+        srt.assign(ids.begin(), ids.end());
+        if (!std::is_sorted(srt.begin(), srt.end())) std::sort(srt.begin(), srt.end());
+        sl.resize(srt.size());
+        for (std::size_t i = 0; i < srt.size(); ++i) {
+            auto it = blocks_.find(srt[i]);
+            if (it == blocks_.end()) throw NotFoundError("metadata: unknown block id " + std::to_string(srt[i]));
             check_dim(static_cast<std::size_t>(d), static_cast<std::size_t>(it->second.dim), "criticality_score");
+            sl[i] = static_cast<std::int32_t>(it->second.slot);
         }
-        sorted[u].assign(ids.begin(), ids.end());
-        std::sort(sorted[u].begin(), sorted[u].end());
         off[u + 1] = off[u] + static_cast<std::int64_t>(ids.size());
         max_n = std::max<std::int64_t>(max_n, static_cast<std::int64_t>(ids.size()));
     }
@@ -335,9 +341,7 @@ void TieredBlockStore::run_device(const detail::DeviceQueryBatch& qb, detail::De
     char* hin = static_cast<char*>(dev_->h_in.get(q_b + s_b + o_b));
     for (std::int64_t i = 0; i < nq; ++i) std::memcpy(hin + static_cast<size_t>(i) * d * 4, qb.queries[i], d * 4);
     auto* hs = reinterpret_cast<std::int32_t*>(hin + q_b);
-    for (int u = 0; u < n_units; ++u)
-        for (std::int64_t i = 0; i < off[u + 1] - off[u]; ++i)
-            hs[off[u] + i] = static_cast<std::int32_t>(blocks_.at(sorted[u][i]).slot);
+    for (int u = 0; u < n_units; ++u) std::memcpy(hs + off[u], slot_of[u].data(), slot_of[u].size() * 4);
     std::memcpy(hin + q_b + s_b, off.data(), (n_units + 1) * 8);
     char* din = static_cast<char*>(dev_->in.get(q_b + s_b + o_b));
     check_cuda(cudaMemcpyAsync(din, hin, q_b + s_b + o_b, cudaMemcpyHostToDevice, dev_->stream), "H2D");

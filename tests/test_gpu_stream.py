@@ -167,3 +167,49 @@ def test_stream_many_units_and_counters(mods, oracle):
         for h in range(g):
             x = res[u * g + h]
             check_parity(oracle, qs[u, h], bs, make_config(epsilon=0.95), 0, x["ids"], x["bp"], x["out"], x["est"])
+
+
+@pytest.mark.parametrize("scale", [4.0, 40.0])
+def test_stream_extreme_logits(mods, oracle, scale):
+    """Large logits (scale_override): the V weights are taken relative to an earlier block's actual
+    max (raised when a block exceeds it by more than the slack), never to a criticality estimate, so
+    weights stay finite and the dominant blocks never underflow; parity rule as everywhere."""
+    capi, _ = mods
+    g = 4
+    tokens = [16 * 700 + 9, 16 * 100]
+    cfg = dict(epsilon=0.95, scale_override=scale)
+    p, uids, nb, off, qs, run = build(mods, tokens, g, 1 / 32, cfg, seed=23)
+    run_mode(capi, run, 3)
+    a = collect(run, off, nb, g)
+    oc = make_config(epsilon=0.95, scale_override=scale)
+    for u, uid in enumerate(uids):
+        bs = blockset(p, uid, tokens[u], nb[u])
+        for h in range(g):
+            x = a[u * g + h]
+            assert np.all(np.isfinite(x["out"]))
+            check_parity(oracle, qs[u, h], bs, oc, 0, x["ids"], x["bp"], x["out"], x["est"])
+
+
+def test_stream_early_dense_handover(mods, oracle):
+    """Isotropic keys: flat heads go to the dense kernels after the first round (psattn_set_dense_early)
+    with the same processed sets as the late hand-over (threshold 0 = off)."""
+    capi, _ = mods
+    g = 4
+    tokens = [16 * 2048, 16 * 1500 + 7]
+    p, uids, nb, off, qs, run = build(mods, tokens, g, 0.0, dict(epsilon=0.95), seed=29)
+    res = {}
+    for thr in (2.0, 0.0):
+        assert capi.lib.psattn_set_dense_early(thr) == 0
+        try:
+            run_mode(capi, run, 3)
+            res[thr] = collect(run, off, nb, g)
+        finally:
+            capi.lib.psattn_set_dense_early(2.0)
+    for u, uid in enumerate(uids):
+        bs = blockset(p, uid, tokens[u], nb[u])
+        for h in range(g):
+            x, y = res[2.0][u * g + h], res[0.0][u * g + h]
+            assert x["bp"] > 384  # flat heads need most of the list
+            assert x["bp"] == y["bp"] and np.array_equal(x["ids"], y["ids"])
+            assert np.max(np.abs(x["out"] - y["out"])) <= 1e-5
+            check_parity(oracle, qs[u, h], bs, make_config(epsilon=0.95), 0, x["ids"], x["bp"], x["out"], x["est"])
