@@ -186,6 +186,7 @@ EXPORTED = [
     "psattn_last_error", "psattn_version", "psattn_store_options_default", "psattn_store_create",
     "psattn_store_destroy", "psattn_store_put_block", "psattn_store_release_request", "psattn_store_contains",
     "psattn_store_stats", "psattn_config_default", "psattn_run_query", "psattn_run_topk",
+    "psattn_cmd_run", "psattn_cmd_tradeoff", "psattn_cmd_equivalence",
     "psattn_pool_create", "psattn_pool_destroy", "psattn_pool_get_desc", "psattn_pool_get_layout",
     "psattn_pool_put_blocks", "psattn_pool_build_metadata", "psattn_pool_read_metadata",
     "psattn_pool_append_tokens",

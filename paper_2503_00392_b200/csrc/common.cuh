@@ -86,6 +86,11 @@ __device__ __forceinline__ float warp_max(float x) {
     for (int o = 16; o >= 1; o >>= 1) x = fmaxf(x, __shfl_xor_sync(PSA_FULL, x, o));
     return x;
 }
+__device__ __forceinline__ float warp_sum(float x) {
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) x += __shfl_xor_sync(PSA_FULL, x, o);
+    return x;
+}
 __device__ __forceinline__ double warp_max_d(double x) {
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) x = fmax(x, __shfl_xor_sync(PSA_FULL, x, o));

@@ -443,8 +443,8 @@ int psattn_pool_create(const psattn_pool_desc* desc, psattn_pool** out_pool) {
     if (!desc || !out_pool) return fail(PSATTN_ERR_INVALID_ARGUMENT, "psattn_pool_create: null argument");
     if (desc->dim < 1 || desc->dim > 256)
         return fail(PSATTN_ERR_INVALID_ARGUMENT, "psattn_pool_create: dim must be in [1, 256]");
-    if (desc->block_tokens < 1 || desc->block_tokens > 32)
-        return fail(PSATTN_ERR_INVALID_ARGUMENT, "psattn_pool_create: block_tokens must be in [1, 32]");
+    if (desc->block_tokens < 1 || desc->block_tokens > kMaxBlockTokens)
+        return fail(PSATTN_ERR_INVALID_ARGUMENT, "psattn_pool_create: block_tokens must be in [1, 128]");
     if (desc->kv_dtype != PSATTN_KV_F32 && desc->kv_dtype != PSATTN_KV_BF16)
         return fail(PSATTN_ERR_INVALID_ARGUMENT, "psattn_pool_create: unknown kv dtype");
     if (desc->n_slots < 0) return fail(PSATTN_ERR_INVALID_ARGUMENT, "psattn_pool_create: n_slots must be >= 0");

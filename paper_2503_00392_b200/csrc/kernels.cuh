@@ -94,6 +94,7 @@ struct BatchView {
     // [n_units][kStreamEnt][kStreamWRow] fp32, bulk-copied back beside the block's V tile
     float* stream_w;
 };
+constexpr int kMaxBlockTokens = 128;  // longest block (tokens) a pool slot holds; > 32 runs the chunked per-head kernel
 constexpr int kFirstCap = 512;   // == the GQA kernel's tranche capacity
 constexpr int kStreamEnt = 512;  // distinct blocks one unit may fetch on the stream kernel (else hand-over)
 constexpr int kStreamWRow = 64;  // floats per fetched block: token weights [4 heads][16]

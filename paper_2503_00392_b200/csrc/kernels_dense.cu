@@ -445,23 +445,32 @@ __device__ __forceinline__ void dense_v_unit(const PoolView& p, const BatchView&
     float Oreg[16], Mreg = -INFINITY, Lreg = 0.0f;
 #pragma unroll
     for (int j = 0; j < 16; ++j) Oreg[j] = 0.0f;
-    // membership mask, slot and prefetch target of the NEXT block are loaded one iteration ahead
-    constexpr int64_t kPfd = (int64_t)kDensePf * kDenseWarps;
+    // membership masks and slots run kDensePf iterations ahead of the V reads: the L2 prefetch (same
+    // distance) touches only blocks of the union, so no V byte outside it is fetched
+    constexpr int kD = kDensePf;
+    constexpr int64_t kW = kDenseWarps;
     int64_t e = e_begin + warp;
-    uint32_t mask_n = e < e_end ? mask_of(e) : 0u;
-    int32_t slot_n = e < e_end ? b.slots[off + e] : 0;
-    int32_t sf_n = e + kPfd < e_end ? b.slots[off + e + kPfd] : -1;
-    for (; e < e_end; e += kDenseWarps) {
-        const uint32_t mask = mask_n;
-        const int32_t slot = slot_n, sf = sf_n;
-        const int64_t en = e + kDenseWarps;
-        if (en < e_end) {
-            mask_n = mask_of(en);
-            slot_n = b.slots[off + en];
+    auto slot_or = [&](int64_t f) { return f < e_end ? b.slots[off + f] : 0; };
+    auto mask_or = [&](int64_t f) { return f < e_end ? mask_of(f) : 0u; };
+    uint32_t mq[kD + 1];
+    int32_t sq[kD + 1];
+#pragma unroll
+    for (int i = 0; i <= kD; ++i) {
+        mq[i] = mask_or(e + i * kW);
+        sq[i] = slot_or(e + i * kW);
+    }
+    for (; e < e_end; e += kW) {
+        const uint32_t mask = mq[0];
+        const int32_t slot = sq[0];
+        if (lane == 0 && mq[kD] && kv_resident(p, sq[kD]))  // block e + kD*W, kD iterations ahead
+            prefetch_l2_bulk(kv_block<__nv_bfloat16>(p, sq[kD]) + v_off, (uint32_t)(T * 128 * 2));
+#pragma unroll
+        for (int i = 0; i < kD; ++i) {
+            mq[i] = mq[i + 1];
+            sq[i] = sq[i + 1];
         }
-        sf_n = en + kPfd < e_end ? b.slots[off + en + kPfd] : -1;
-        if (lane == 0 && sf >= 0 && kv_resident(p, sf))
-            prefetch_l2_bulk(kv_block<__nv_bfloat16>(p, sf) + v_off, (uint32_t)(T * 128 * 2));
+        mq[kD] = mask_or(e + (kD + 1) * kW);
+        sq[kD] = slot_or(e + (kD + 1) * kW);
         if (!mask) continue;
         const __nv_bfloat16* vblk = kv_block<__nv_bfloat16>(p, slot) + v_off;
         uint32_t vw[4][8];

@@ -11,7 +11,7 @@ namespace psa {
 // Specialised lane mappings for d = 64 and d = 128; every other d <= 256 runs
 // the masked 8-dims-per-lane variant.
 int dpl_for(int d) { return d == 128 ? 4 : d == 64 ? 2 : 8; }
-int tok_for(int T) { return T <= 16 ? 16 : 32; }
+int tok_for(int T) { return T <= 16 ? 16 : T <= 32 ? 32 : kMaxBlockTokens; }
 int g_for(int g) { return g <= 4 ? 4 : 8; }
 
 // =============================================================================

@@ -132,7 +132,7 @@ __global__ void __launch_bounds__(kPsaThreads, 3) psa_kernel(PoolView p, BatchVi
     const int lim = d - base;
     constexpr bool full = FULL;  // d == 32*DPL: vector loads, no bounds
     const float fscale = (float)b.scale;  // engine.cpp:113
-    constexpr int TSH = 5 - Log2<TOK>::v;  // lanes per token after reduce-scatter = 1 << TSH
+    constexpr int TSH = TOK <= 32 ? 5 - Log2<TOK <= 32 ? TOK : 32>::v : 0;  // lanes per token after reduce-scatter = 1 << TSH
     const int my_tok = lane >> TSH;
     const uint64_t pmask = (b.pos_bits >= 64) ? ~0ull : ((1ull << b.pos_bits) - 1ull);
 
@@ -199,6 +199,49 @@ __global__ void __launch_bounds__(kPsaThreads, 3) psa_kernel(PoolView p, BatchVi
                     s.mb[warp][j] = mb;
                     s.lb[warp][j] = lb;
                     s.la[rl] = mb + logf(lb);
+                }
+                continue;
+            }
+            if constexpr (TOK > 32) {
+                // long blocks (32 < T <= TOK): 32-token chunks, each scored like a 32-token block,
+                // folded into the block's (max, exp-sum) online; the token weights end up relative
+                // to the block max (attention.hpp:55-73 over all the block's tokens)
+                const KV* kp = kv_block<KV>(p, slot) + base;
+                float mbk = -INFINITY, lbk = 0.0f, wc[TOK / 32], mc[TOK / 32];
+#pragma unroll
+                for (int c = 0; c < TOK / 32; ++c) {
+                    wc[c] = 0.0f;
+                    mc[c] = -INFINITY;
+                    if (c * 32 >= nt) continue;
+                    float part[32];
+#pragma unroll
+                    for (int t = 0; t < 32; ++t) {
+                        const int row = c * 32 + t < T ? c * 32 + t : T - 1;
+                        float kr[DPL];
+                        load_row<DPL>(kp + (size_t)row * d, full, lim, kr);
+                        float a = 0.0f;
+#pragma unroll
+                        for (int jj = 0; jj < DPL; ++jj) a = fmaf(q[jj], kr[jj], a);
+                        part[t] = a;
+                    }
+                    float sc = reduce_scatter<32>(part, lane) * fscale;  // token c*32 + lane
+                    sc = c * 32 + lane < nt ? sc : -INFINITY;
+                    const float m = warp_max(sc);
+                    const float w = c * 32 + lane < nt ? expf(sc - m) : 0.0f;
+                    const float l = warp_sum(w);
+                    const float mnew = fmaxf(mbk, m);
+                    lbk = lbk * expf(mbk - mnew) + l * expf(m - mnew);
+                    mbk = mnew;
+                    wc[c] = w;
+                    mc[c] = m;
+                }
+#pragma unroll
+                for (int c = 0; c < TOK / 32; ++c)
+                    if (c * 32 < nt) s.w[warp][j][c * 32 + lane] = wc[c] * expf(mc[c] - mbk);
+                if (lane == 0) {
+                    s.mb[warp][j] = mbk;
+                    s.lb[warp][j] = lbk;
+                    s.la[rl] = mbk + logf(lbk);
                 }
                 continue;
             }
@@ -277,7 +320,15 @@ __global__ void __launch_bounds__(kPsaThreads, 3) psa_kernel(PoolView p, BatchVi
             float ob[DPL];
 #pragma unroll
             for (int jj = 0; jj < DPL; ++jj) ob[jj] = 0.0f;
-            if (T == TOK) {
+            if constexpr (TOK > 32) {
+                for (int t = 0; t < nt; ++t) {
+                    const float wt = s.w[warp][j][t];
+                    float vr[DPL];
+                    load_row<DPL>(vp + (size_t)t * d, full, lim, vr);
+#pragma unroll
+                    for (int jj = 0; jj < DPL; ++jj) ob[jj] = fmaf(wt, vr[jj], ob[jj]);
+                }
+            } else if (T == TOK) {
 #pragma unroll
                 for (int t = 0; t < TOK; ++t) {
                     const float wt = s.w[warp][j][t];  // 0 for t >= ntok
@@ -392,10 +443,12 @@ int launch_psa(const PoolView& p, const BatchView& b, cudaStream_t st) {
     const int nq = b.n_units * b.g;
     if (p.dtype == 0) {
         if (tok_for(p.T) == 16) launch_psa_t<float, 16>(p, b, nq, st);
-        else launch_psa_t<float, 32>(p, b, nq, st);
+        else if (tok_for(p.T) == 32) launch_psa_t<float, 32>(p, b, nq, st);
+        else launch_psa_t<float, kMaxBlockTokens>(p, b, nq, st);
     } else {
         if (tok_for(p.T) == 16) launch_psa_t<__nv_bfloat16, 16>(p, b, nq, st);
-        else launch_psa_t<__nv_bfloat16, 32>(p, b, nq, st);
+        else if (tok_for(p.T) == 32) launch_psa_t<__nv_bfloat16, 32>(p, b, nq, st);
+        else launch_psa_t<__nv_bfloat16, kMaxBlockTokens>(p, b, nq, st);
     }
     return 1;
 }

@@ -288,6 +288,9 @@ __global__ void __launch_bounds__(kScoreWarps * 32, 2) score_kernel(PoolView p, 
 // ahead of the math, so memory-level parallelism no longer costs registers.
 // -----------------------------------------------------------------------------
 constexpr int kTmaBarBytes = 256;  // kScoreWarps x (<= 4 stages) x 8 B mbarriers
+#ifndef PSA_SCORE_CHUNKED
+#define PSA_SCORE_CHUNKED 1  // contiguous group runs per warp + windowed slot loads
+#endif
 
 template <typename KV, int G, int EST>
 __global__ void __launch_bounds__(kScoreWarps * 32, 2) score_kernel_tma(PoolView p, BatchView b) {
@@ -344,7 +347,29 @@ __global__ void __launch_bounds__(kScoreWarps * 32, 2) score_kernel_tma(PoolView
 
     const int64_t ngroups = (n + kRecs - 1) / kRecs;
     const int64_t nwarps = (int64_t)gridDim.x * kScoreWarps;
+#if PSA_SCORE_CHUNKED
+    // each warp owns a contiguous run of groups; the page-table slots of 32 consecutive records
+    // (a window) arrive in one coalesced load, one window ahead, and reach the issuing lanes by shuffle
+    const int64_t gpw = (ngroups + nwarps - 1) / nwarps;
+    const int64_t g_begin = ((int64_t)blockIdx.x * kScoreWarps + warp) * gpw;
+    const int64_t g_end = g_begin + gpw < ngroups ? g_begin + gpw : ngroups;
+    constexpr int kWinGroups = 32 / kRecs;
+    const int64_t rec_end = g_end * kRecs < n ? g_end * kRecs : n;
+    auto win_load = [&](int64_t w) -> int32_t {
+        const int64_t r = g_begin * kRecs + w * 32 + lane;
+        return r < rec_end ? b.slots[off + r] : 0;
+    };
+    int32_t wcur = win_load(0), wnext = win_load(1);
+    int64_t wi = 0;  // window held in wcur
+    auto slot_at = [&](int64_t g) -> int32_t {  // lanes < kRecs: slots of group g (all lanes call)
+        const int64_t k = g - g_begin;
+        const int src = (int)(k % kWinGroups) * kRecs + (lane < kRecs ? lane : 0);
+        const int32_t a = __shfl_sync(PSA_FULL, wcur, src), c = __shfl_sync(PSA_FULL, wnext, src);
+        return (k / kWinGroups) == wi ? a : c;
+    };
+#else
     const int64_t grp0 = (int64_t)blockIdx.x * kScoreWarps + warp;
+#endif
     auto issue = [&](int64_t grp, int stage, int32_t slot) {
         const int64_t p0 = grp * kRecs;
         const int cnt = (int)((n - p0) < kRecs ? (n - p0) : kRecs);
@@ -359,6 +384,26 @@ __global__ void __launch_bounds__(kScoreWarps * 32, 2) score_kernel_tma(PoolView
             tma_load_1d(wbuf + stage * STAGE + lane * MB, p.meta + (int64_t)slot * MB, MB, &wbar[stage], pol);
         }
     };
+#if PSA_SCORE_CHUNKED
+    // prologue: S groups in flight
+#pragma unroll 1
+    for (int st = 0; st < S; ++st) {
+        const int64_t g = g_begin + st;
+        const int32_t sl = slot_at(g);
+        if (g < g_end) issue(g, st, sl);
+    }
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int64_t grp = g_begin; grp < g_end; ++grp) {
+        const int64_t gn = grp + S;  // group that refills this stage
+        if ((gn - g_begin) / kWinGroups != wi) {  // the refill enters the next window: slide
+            wcur = wnext;
+            ++wi;
+            wnext = win_load(wi + 1);
+        }
+        const int32_t nslot = slot_at(gn);
+        mbar_wait(&wbar[stage], phase);
+#else
     // prologue: S groups in flight
 #pragma unroll 1
     for (int st = 0; st < S; ++st) {
@@ -381,6 +426,7 @@ __global__ void __launch_bounds__(kScoreWarps * 32, 2) score_kernel_tma(PoolView
         pf0 = pf1;
         pf1 = slot_of(grp + (S + 2) * nwarps);
         mbar_wait(&wbar[stage], phase);
+#endif
         const unsigned char* sb = wbuf + stage * STAGE;
         double acc[N];
 #pragma unroll
@@ -457,7 +503,11 @@ __global__ void __launch_bounds__(kScoreWarps * 32, 2) score_kernel_tma(PoolView
         // every lane's shared-memory accesses of this stage precede the refill (generic -> async proxy)
         fence_proxy_async();
         __syncwarp();
+#if PSA_SCORE_CHUNKED
+        if (gn < g_end) issue(gn, stage, nslot);
+#else
         if (gn < ngroups) issue(gn, stage, nslot);
+#endif
         const int64_t p0 = grp * kRecs;
         if (writer && p0 + my_j < n) {
             const uint64_t key = make_key_masked(tot * kscale, (uint32_t)(p0 + my_j), kmask);

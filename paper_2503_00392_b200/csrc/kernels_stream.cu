@@ -495,7 +495,10 @@ __global__ void __launch_bounds__(kThreads, 2) psa_stream_kernel(const __grid_co
             flat = s0 - s1 < (double)b.dense_early;
         }
         const bool flat_unit = __any_sync(PSA_FULL, flat);
-        double M = -INFINITY, S = 0.0, mn = INFINITY, est = 0.0;
+        // CoverageEstimator state (engine.cpp:38-55) in fp64 about the running max M of the observed
+        // masses: S = sum exp(mass - M), E = exp(min mass - M) (+inf before the first block)
+        double M = -INFINITY, S = 0.0, E = INFINITY, est = 0.0;
+        const double one_m_eps = 1.0 - eps;
         for (int k = 0;; ++k) {
             const int rs = k % kLR;
             SWAIT(&s.rscored[rs], (k / kLR) & 1, 2, k, (int)cb, vc, (int)live, 0, 0, 0, 0);
@@ -507,30 +510,52 @@ __global__ void __launch_bounds__(kThreads, 2) psa_stream_kernel(const __grid_co
             const bool overflow = s.r_flag[rs] == 1;
             const int64_t r = cb + i;
             const bool valid = live && e >= 0 && r < limit;
-            double x = -INFINITY;
-            if (valid) x = b.has_oracle ? b.omass[hb + s.epos[e]] : (double)s.em[e][h];
-            // segment (C lanes = one head) scan in fp64: running log-sum-exp carried as (max M, sum S)
-            double mx = x;
+            double x = -INFINITY, mx;
+            if (!b.has_oracle) {  // fp32 masses: the segment max is exact in fp32
+                float xf = valid ? s.em[e][h] : -INFINITY;
+                x = (double)xf;
 #pragma unroll
-            for (int o = C / 2; o >= 1; o >>= 1) mx = fmax(mx, __shfl_xor_sync(PSA_FULL, mx, o));
+                for (int o = C / 2; o >= 1; o >>= 1) xf = fmaxf(xf, __shfl_xor_sync(PSA_FULL, xf, o));
+                mx = (double)xf;
+            } else {
+                if (valid) x = b.omass[hb + s.epos[e]];
+                mx = x;
+#pragma unroll
+                for (int o = C / 2; o >= 1; o >>= 1) mx = fmax(mx, __shfl_xor_sync(PSA_FULL, mx, o));
+            }
             mx = fmax(mx, M);
+            // carried state re-expressed about the new max (only when it moved: rare after round 0)
+            double Sc = S, Ec = E;  // (M = -inf: S = 0, E = +inf, nothing to rescale)
+            const bool moved = M != -INFINITY && mx != M;
+            if (__any_sync(PSA_FULL, moved)) {
+                const double fct = moved ? exp(M - mx) : 1.0;
+                Sc = S * fct;
+                Ec = E * fct;
+            }
+            // segment scans: prefix sum and prefix min of exp(mass - mx); exp(min - mx) is the min of
+            // the exponentials (monotone), so one fp64 exp per rank
             double ev = valid ? exp(x - mx) : 0.0;
-            double mnv = valid ? x : INFINITY;
+            double em_ = valid ? ev : INFINITY;
 #pragma unroll
             for (int o = 1; o < C; o <<= 1) {
                 const double ye = __shfl_up_sync(PSA_FULL, ev, o, C);
-                const double ym = __shfl_up_sync(PSA_FULL, mnv, o, C);
+                const double ym = __shfl_up_sync(PSA_FULL, em_, o, C);
                 if (i >= o) {
                     ev += ye;
-                    mnv = fmin(mnv, ym);
+                    em_ = fmin(em_, ym);
                 }
             }
-            const double Si = (M == -INFINITY ? 0.0 : S * exp(M - mx)) + ev;  // sum exp(mass - mx) so far
-            const double mn_i = fmin(mnv, mn);
+            const double Si = Sc + ev;        // sum exp(mass - mx) observed up to this rank
+            const double Ei = fmin(Ec, em_);  // exp(min mass - mx)
             const int64_t nl = n - (r + 1);
-            const double est_i = nl == 0 ? 1.0 : (Si > 0.0 ? Si / fma((double)nl, exp(mn_i - mx), Si) : 0.0);
+            const double D = (double)nl * Ei;
+            // est = Si / (Si + n_left exp(min - mx)) = 1 / (1 + n_left exp(min - acc)) (engine.cpp:48-55);
+            // est > eps  <=>  Si (1 - eps) > eps D: the division runs only when a head may stop
             const bool boundary = valid && (b.m == 1 || ((r + 1) % b.m) == 0 || r + 1 == limit);
-            const bool stop = boundary && (est_i > eps || r + 1 == limit);
+            const bool over = nl == 0 ? eps < 1.0 : (Si > 0.0 && Si * one_m_eps > eps * D);
+            const bool stop = boundary && (over || r + 1 == limit);
+            double est_i = 0.0;
+            if (b.iest || __any_sync(PSA_FULL, stop)) est_i = nl == 0 ? 1.0 : (Si > 0.0 ? Si / (Si + D) : 0.0);
             const unsigned sb = __ballot_sync(PSA_FULL, stop) & seg;
             const unsigned vb = __ballot_sync(PSA_FULL, valid) & seg;
             const int nvalid = __popc(vb);
@@ -539,12 +564,12 @@ __global__ void __launch_bounds__(kThreads, 2) psa_stream_kernel(const __grid_co
             if (b.iest && boundary && i <= f) b.iest[hb + r] = est_i;  // IterationStats::estimated_coverage
             if (committed) atomicOr(&s.vmask[e], 1u << h);
             const int src = h * C + (f > 0 ? f : 0);
-            const double Sf = __shfl_sync(PSA_FULL, Si, src), mnf = __shfl_sync(PSA_FULL, mn_i, src);
+            const double Sf = __shfl_sync(PSA_FULL, Si, src), Ef = __shfl_sync(PSA_FULL, Ei, src);
             const double estf = __shfl_sync(PSA_FULL, est_i, src);
             if (nvalid > 0) {
                 M = mx;
                 S = Sf;
-                mn = mnf;
+                E = Ef;
                 est = estf;
                 cb += f + 1;
             }
@@ -702,23 +727,35 @@ __global__ void __launch_bounds__(kThreads, 2) psa_stream_kernel(const __grid_co
                     const int hq = 2 * t + (tq >> 1);
                     lo = (gq < nt) ? lo * fscale : -INFINITY;
                     hi = (gq + 8 < nt) ? hi * fscale : -INFINITY;
-                    float mbv = fmaxf(lo, hi);
-#pragma unroll
-                    for (int o = 4; o < 32; o <<= 1) mbv = fmaxf(mbv, __shfl_xor_sync(PSA_FULL, mbv, o));
-                    const float wlo = (gq < nt) ? expf(lo - mbv) : 0.0f;
-                    const float whi = (gq + 8 < nt) ? expf(hi - mbv) : 0.0f;
+                    // token weights straight against the head's V reference R (no block-max pass):
+                    // w = exp(s - R), block exponent sum L = sum w, log mass = R + ln L (the reference's
+                    // m + ln sum exp(s - m), attention.hpp:55-73, taken about R instead of m)
+                    const float R = vref[t];
+                    float wlo = expf(lo - R), whi = expf(hi - R);
                     float lbv = wlo + whi;
 #pragma unroll
                     for (int o = 4; o < 32; o <<= 1) lbv += __shfl_xor_sync(PSA_FULL, lbv, o);
-                    const float R = vref[t];
-                    const float fv = expf(mbv - R);  // block max -> the head's V reference
-                    if (mbv > R + kVHigh || (k == 0 && e == s.rank0[hq] && mbv < R - kVLow)) s.vref_bad = 1;
+                    float la = R + __logf(lbv);  // MUFU lg2: ~1e-7 absolute, below fp32 ulp(la) at these magnitudes
+                    if (__any_sync(PSA_FULL, !(lbv >= 1e-30f && lbv <= 1e30f))) {
+                        // a block far below R (its fp32 terms would lose precision) or above it (could
+                        // overflow): exact mass about its own max; above-R blocks flag the unit (dense redo)
+                        float mbv = fmaxf(lo, hi);
+#pragma unroll
+                        for (int o = 4; o < 32; o <<= 1) mbv = fmaxf(mbv, __shfl_xor_sync(PSA_FULL, mbv, o));
+                        float l2 = ((gq < nt) ? expf(lo - mbv) : 0.0f) + ((gq + 8 < nt) ? expf(hi - mbv) : 0.0f);
+#pragma unroll
+                        for (int o = 4; o < 32; o <<= 1) l2 += __shfl_xor_sync(PSA_FULL, l2, o);
+                        la = mbv + logf(l2);
+                        if (mbv > R + kVHigh) s.vref_bad = 1;
+                        if (!(lbv <= 1e30f)) wlo = whi = lbv = 0.0f;
+                    }
+                    if (k == 0 && e == s.rank0[hq] && la < R - kVLow) s.vref_bad = 1;  // R far above the top block
                     if ((tq & 1) == 0) {
-                        we[hq * 16 + gq] = wlo * fv;
-                        we[hq * 16 + gq + 8] = whi * fv;
+                        we[hq * 16 + gq] = wlo;
+                        we[hq * 16 + gq + 8] = whi;
                         if (gq == 0) {
-                            s.em[e][hq] = mbv + logf(lbv);  // log_as (attention.hpp:73)
-                            s.el[e][hq] = lbv * fv;
+                            s.em[e][hq] = la;  // log_as (attention.hpp:73)
+                            s.el[e][hq] = lbv;
                         }
                     }
                 }

@@ -17,6 +17,7 @@
 #include <vector>
 
 #include "device.h"
+#include "kernels.cuh"
 
 namespace psa {
 
@@ -34,7 +35,7 @@ struct RunState {
 
 namespace {
 
-constexpr int kThreads = 256;  // >= d (<= 256) and >= tokens per block (<= 32)
+constexpr int kThreads = 256;  // >= d (<= 256) and >= tokens per block (<= kMaxBlockTokens)
 
 // One CTA; blocks strictly in order like the reference. Token scores: one thread per token,
 // dims in order with explicit rounding (the reference's dot_scaled<float>); max / exp-sum by
@@ -43,7 +44,7 @@ __global__ void __launch_bounds__(kThreads) consume_kernel(const float* __restri
                                                            const float* __restrict__ kv, const int32_t* __restrict__ ntok,
                                                            int n, int T, float* __restrict__ acc,
                                                            float* __restrict__ las) {
-    __shared__ float sc[32], w[32];
+    __shared__ float sc[kMaxBlockTokens], w[kMaxBlockTokens];
     __shared__ float fa, fp;
     const int i = threadIdx.x;
     float* mx = acc + d;
@@ -133,8 +134,8 @@ int prun_consume(RunState* s, float scale, int n, const int32_t* ntok, const flo
                  const float* const* values, float* log_as) {
     int T = 1;
     for (int b = 0; b < n; ++b) {
-        if (ntok[b] <= 0 || ntok[b] > 32)
-            return fail(PSATTN_ERR_INVALID_ARGUMENT, "progressive run: blocks must hold 1..32 tokens");
+        if (ntok[b] <= 0 || ntok[b] > kMaxBlockTokens)
+            return fail(PSATTN_ERR_INVALID_ARGUMENT, "progressive run: blocks must hold 1..128 tokens");
         T = ntok[b] > T ? ntok[b] : T;
     }
     const int64_t need = (int64_t)n * 2 * T * s->d;

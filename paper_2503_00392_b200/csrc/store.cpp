@@ -133,7 +133,7 @@ void TieredBlockStore::put_block(std::shared_ptr<const KVBlock> block, RequestId
     if (!block) throw Error("put_block: null block");
     if (block->n_tokens <= 0) throw Error("build_metadata: empty block");
     if (block->dim <= 0 || block->dim > 256) throw Error("put_block: dim must be in [1, 256] on the device pool");
-    if (block->n_tokens > 32) throw Error("put_block: blocks of more than 32 tokens are not supported by the device pool");
+    if (block->n_tokens > 128) throw Error("put_block: blocks of more than 128 tokens are not supported by the device pool");
     const std::size_t nelem = static_cast<std::size_t>(block->n_tokens) * static_cast<std::size_t>(block->dim);
     if (block->keys.size() < nelem || block->values.size() < nelem) throw Error("put_block: short key/value arrays");
     std::lock_guard lock(mutex_);

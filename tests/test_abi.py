@@ -97,3 +97,17 @@ def test_synthetic_generator_host_properties():
     # ragged tail: tokens past the end are zero
     kr, _ = synth.unit_host(p, 3, 16 * 3 + 5)
     assert kr.shape == (4, 16, 128) and np.all(kr[3, 5:] == 0) and np.any(kr[3, :5] != 0)
+
+
+def test_cli_commands_link_and_refuse():
+    """psattn_cmd_* (reference psattn.h:107-121) link for CLI callers and refuse with a clear error
+    (the scenario drivers are outside this path) — no GPU needed."""
+    import ctypes as C
+    from paper_2503_00392_b200 import capi
+    lib = capi.lib
+    lib.psattn_cmd_run.argtypes = [C.c_char_p]
+    lib.psattn_cmd_tradeoff.argtypes = [C.c_char_p]
+    assert lib.psattn_cmd_run(b"x.ini") == 1
+    assert b"not part of the B200 build" in C.c_char_p(lib.psattn_last_error()).value
+    assert lib.psattn_cmd_tradeoff(b"x.ini") == 1
+    assert lib.psattn_cmd_equivalence(None) == 1

@@ -176,3 +176,32 @@ def test_store_accounting_matches_reference(capi, ref):
         for i in range(bs.n):
             assert mine.contains(int(bs.ids[i]))[1] == theirs.contains(int(bs.ids[i]))
         assert mine.release(1) == 0 and theirs.release(1) == 0
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_long_blocks_parity(capi, oracle, seed):
+    """Blocks of 33..128 tokens (the reference accepts any n_tokens, types.hpp:29-48): the chunked
+    per-head kernel scores them in 32-token chunks folded online; parity with the oracle."""
+    rng = np.random.default_rng(500 + seed)
+    d = int(rng.choice([16, 64, 128, 256]))
+    n = int(rng.integers(2, 80))
+    ids = rng.permutation(5_000)[:n]
+    bs = random_blockset(rng, n, d, 1, 128, planted_frac=0.1, ids=ids)
+    s = capi.Store(capacity=64)
+    s.put_blockset(bs)
+    q = (rng.standard_normal(d) * 2).astype(np.float32)
+    kw = dict(epsilon=float(rng.choice([0.8, 0.95, 1.0])), microbatch_size=int(rng.integers(1, 4)),
+              audit_coverage=int(seed % 2))
+    rc, r = s.run_query(q, ids, capi.config_default(**kw))
+    assert rc == 0, capi.last_error()
+    o = oracle.psa(q, bs, make_config(**kw))
+    if r.blocks_processed == o.blocks_processed:
+        assert max_abs(r.output, o.output) <= OUT_TOL
+        assert r.estimated_coverage == pytest.approx(o.estimated_coverage, abs=1e-4)
+    else:
+        m = kw["microbatch_size"]
+        k = min(r.blocks_processed, o.blocks_processed)
+        assert abs(o.iteration_estimates[(k + m - 1) // m - 1] - kw["epsilon"]) <= 1e-5
+    # > 128 tokens is refused with a clear error (not silently truncated)
+    big = rng.standard_normal((129, d)).astype(np.float32)
+    assert s.put(99_999, big, big) == capi.PSATTN_ERR_RUNTIME
