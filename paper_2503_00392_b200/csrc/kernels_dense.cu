@@ -442,9 +442,15 @@ __device__ __forceinline__ void dense_v_unit(const PoolView& p, const BatchView&
             if (h < g && b.keys[off * g + (int64_t)h * n + e] <= thr[h]) m |= 1u << h;
         return m;
     };
-    float Oreg[16], Mreg = -INFINITY, Lreg = 0.0f;
+    constexpr int NTV = G > 2 ? 2 : 1;  // n-tiles of (head, split) columns: 2 heads x 4 per tile
+    float Oreg[NTV][8], Mreg[NTV], Lreg[NTV];
 #pragma unroll
-    for (int j = 0; j < 16; ++j) Oreg[j] = 0.0f;
+    for (int t = 0; t < NTV; ++t) {
+        Mreg[t] = -INFINITY;
+        Lreg[t] = 0.0f;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) Oreg[t][i] = 0.0f;
+    }
     // membership masks and slots run kDensePf iterations ahead of the V reads: the L2 prefetch (same
     // distance) touches only blocks of the union, so no V byte outside it is fetched
     constexpr int kD = kDensePf;
@@ -483,42 +489,62 @@ __device__ __forceinline__ void dense_v_unit(const PoolView& p, const BatchView&
             vw[r][0] = x0.x; vw[r][1] = x0.y; vw[r][2] = x0.z; vw[r][3] = x0.w;
             vw[r][4] = x1.x; vw[r][5] = x1.y; vw[r][6] = x1.z; vw[r][7] = x1.w;
         }
-        // B columns = (head, split): weights p_t of head hb (2-term bf16 split), zero if not committed
-        const int hbq = gq >> 1, sb = gq & 1;
-        const bool hon = hbq < g && (mask >> hbq) & 1u;
-        uint32_t bfr[2];
+        // B columns of n-tile t = (head 2t + c/4, split c%4): weights p_t of the head as an exact 3-term
+        // bf16 split (fp32 weights; the 4th column is zero), zero if the head did not commit the block
+        uint32_t bfr[NTV][2];
 #pragma unroll
-        for (int hf = 0; hf < 2; ++hf) {
-            float2 wv = make_float2(0.0f, 0.0f);
-            if (hon) wv = *reinterpret_cast<const float2*>(b.dense_p + ((off * g + (int64_t)hbq * n) + e) * 16 + 2 * tq + 8 * hf);
-            bfr[hf] = pack_bf16x2_split(wv.x, wv.y, sb);
+        for (int t = 0; t < NTV; ++t) {
+            const int hq = 2 * t + (gq >> 2), sp = gq & 3;
+            const bool hon = hq < g && (mask >> hq) & 1u;
+#pragma unroll
+            for (int hf = 0; hf < 2; ++hf) {
+                float2 wv = make_float2(0.0f, 0.0f);
+                if (hon)
+                    wv = *reinterpret_cast<const float2*>(b.dense_p + ((off * g + (int64_t)hq * n) + e) * 16 + 2 * tq + 8 * hf);
+                bfr[t][hf] = pack_split3(wv.x, wv.y, sp);
+            }
         }
-        float ob[16];
+        // A = V^T with the dims permuted by the loads above: m-tile i row gq is dim 16gq + 2i, row gq+8 is
+        // dim 16gq + 2i + 1; lane (gq, tq) of tile t ends with head 2t + tq/2 at dim 16gq + 2i + (tq & 1)
+        float ob[NTV][8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-            float c0 = 0.f, c1 = 0.f, c2 = 0.f, c3 = 0.f;
-            mma_bf16_16816(c0, c1, c2, c3, __byte_perm(vw[0][i], vw[1][i], 0x5410), __byte_perm(vw[0][i], vw[1][i], 0x7632),
-                           __byte_perm(vw[2][i], vw[3][i], 0x5410), __byte_perm(vw[2][i], vw[3][i], 0x7632), bfr[0], bfr[1]);
-            ob[2 * i] = c0 + c1;
-            ob[2 * i + 1] = c2 + c3;
-        }
-        if (tq < g && ((mask >> tq) & 1u)) {
-            const float la = b.dense_la[off * g + (int64_t)tq * n + e];  // block weight exp(la - M), sum_t p_t = 1
-            const float mnew = fmaxf(Mreg, la);
-            const float a = expf(Mreg - mnew);
-            const float cc = expf(la - mnew);
+            const uint32_t a0 = __byte_perm(vw[0][i], vw[1][i], 0x5410), a1 = __byte_perm(vw[0][i], vw[1][i], 0x7632);
+            const uint32_t a2 = __byte_perm(vw[2][i], vw[3][i], 0x5410), a3 = __byte_perm(vw[2][i], vw[3][i], 0x7632);
 #pragma unroll
-            for (int j = 0; j < 16; ++j) Oreg[j] = Oreg[j] * a + ob[j] * cc;
-            Lreg = Lreg * a + cc;
-            Mreg = mnew;
+            for (int t = 0; t < NTV; ++t) {
+                float c0 = 0.f, c1 = 0.f, c2 = 0.f, c3 = 0.f;
+                mma_bf16_16816(c0, c1, c2, c3, a0, a1, a2, a3, bfr[t][0], bfr[t][1]);
+                const float x = (tq & 1) ? (c0 + c1) : (c2 + c3);
+                const float y = __shfl_xor_sync(PSA_FULL, x, 1);
+                ob[t][i] = ((tq & 1) ? (c2 + c3) : (c0 + c1)) + y;
+            }
+        }
+#pragma unroll
+        for (int t = 0; t < NTV; ++t) {
+            const int hq = 2 * t + (tq >> 1);
+            if (hq < g && ((mask >> hq) & 1u)) {
+                const float la = b.dense_la[off * g + (int64_t)hq * n + e];  // block weight exp(la - M), sum_t p_t = 1
+                const float mnew = fmaxf(Mreg[t], la);
+                const float a = expf(Mreg[t] - mnew);
+                const float cc = expf(la - mnew);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) Oreg[t][i] = Oreg[t][i] * a + ob[t][i] * cc;
+                Lreg[t] = Lreg[t] * a + cc;
+                Mreg[t] = mnew;
+            }
         }
     }
-    if (tq < G) {
 #pragma unroll
-        for (int j = 0; j < 16; ++j) so[warp][tq][16 * gq + j] = Oreg[j];
-        if (gq == 0) {
-            som[warp][tq] = Mreg;
-            sol[warp][tq] = Lreg;
+    for (int t = 0; t < NTV; ++t) {
+        const int hq = 2 * t + (tq >> 1);
+        if (hq < G) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) so[warp][hq][16 * gq + 2 * i + (tq & 1)] = Oreg[t][i];
+            if (gq == 0 && (tq & 1) == 0) {
+                som[warp][hq] = Mreg[t];
+                sol[warp][hq] = Lreg[t];
+            }
         }
     }
     __syncthreads();

@@ -160,16 +160,6 @@ __device__ __forceinline__ void ldsm4t(uint32_t addr, uint32_t& a0, uint32_t& a1
 __device__ __forceinline__ uint32_t swz(uint32_t base, int r, int c) {
     return base + (uint32_t)((c >> 3) * 2048 + r * 128 + (((c & 7) ^ (r & 7)) << 4));
 }
-// Term `part` (0..2) of the exact 3-term bf16 split of a and b, packed (a low); part 3 -> 0.
-// Branch-free: every lane computes the three terms and selects its own (lanes hold different parts).
-__device__ __forceinline__ uint32_t pack_split3(float a, float b, int part) {
-    const uint32_t p1 = pack_bf16x2(a, b);
-    const float a1 = a - __uint_as_float(p1 << 16), b1 = b - __uint_as_float(p1 & 0xFFFF0000u);
-    const uint32_t p2 = pack_bf16x2(a1, b1);
-    const float a2 = a1 - __uint_as_float(p2 << 16), b2 = b1 - __uint_as_float(p2 & 0xFFFF0000u);
-    const uint32_t p3 = pack_bf16x2(a2, b2);
-    return part == 0 ? p1 : part == 1 ? p2 : part == 2 ? p3 : 0u;
-}
 
 #ifdef PSA_STREAM_DEBUG
 __device__ __noinline__ void dbg_stuck(int site, int a0, int a1, int a2, int a3, int a4, int a5, int a6, int a7) {
@@ -351,9 +341,10 @@ __global__ void __launch_bounds__(kThreads, 2) psa_stream_kernel(const __grid_co
                 } else {
                     if (isnew) {
 #if PSA_STREAM_PF
-                        // the entry's K and V (one contiguous slot) start towards L2 now, kLook rounds
-                        // before the K tile is needed: the K ring then refills from L2
-                        prefetch_l2_bulk(p.kv + (int64_t)fslot * p.slot_bytes, (uint32_t)p.slot_bytes);
+                        // the entry's K (PF=2) or K and V (PF=1, one contiguous slot) start towards L2 now,
+                        // kLook rounds before the K tile is needed: the K ring then refills from L2
+                        prefetch_l2_bulk(p.kv + (int64_t)fslot * p.slot_bytes,
+                                         (uint32_t)(PSA_STREAM_PF == 2 ? p.slot_bytes / 2 : p.slot_bytes));
 #endif
                         ent = E + __popc(nb & ((1u << lane) - 1u));
                         s.hval[hs] = (int16_t)ent;

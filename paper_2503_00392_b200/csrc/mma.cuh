@@ -30,6 +30,17 @@ __device__ __forceinline__ uint32_t pack_bf16x2_split(float a, float b, int part
 }
 
 
+// Term `part` (0..2) of the exact 3-term bf16 split of a and b, packed (a low); part 3 -> 0.
+// Branch-free: every lane computes the three terms and selects its own (lanes hold different parts).
+__device__ __forceinline__ uint32_t pack_split3(float a, float b, int part) {
+    const uint32_t p1 = pack_bf16x2(a, b);
+    const float a1 = a - __uint_as_float(p1 << 16), b1 = b - __uint_as_float(p1 & 0xFFFF0000u);
+    const uint32_t p2 = pack_bf16x2(a1, b1);
+    const float a2 = a1 - __uint_as_float(p2 << 16), b2 = b1 - __uint_as_float(p2 & 0xFFFF0000u);
+    const uint32_t p3 = pack_bf16x2(a2, b2);
+    return part == 0 ? p1 : part == 1 ? p2 : part == 2 ? p3 : 0u;
+}
+
 // Exact 3-term bf16 split of an fp32 value: x == x1 + x2 + x3 (split index 0..2; 3+ -> 0).
 __device__ __forceinline__ float bf16_split(float x, int part) {
     const float x1 = __bfloat162float(__float2bfloat16_rn(x));

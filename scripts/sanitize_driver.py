@@ -37,6 +37,9 @@ def synth_run(tokens, planted, cfg, kv=capi.PSATTN_KV_BF16, kernel=0):
 synth_run([16 * 900 + 3, 16 * 300], 1 / 32, dict(epsilon=0.95))            # score + first tranche + GQA
 synth_run([16 * 700 + 5], 0.0, dict(epsilon=0.95))                          # dense hand-over
 synth_run([16 * 500], 0.0, dict(epsilon=0.9), kernel=1)                     # per-head kernel
+synth_run([16 * 600 + 7, 16 * 90], 1 / 32, dict(epsilon=0.95), kernel=2)     # GQA round kernel
+synth_run([16 * 400], 1 / 32, dict(epsilon=0.95, scale_override=4.0))        # stream kernel -> dense redo (extreme logits)
+synth_run([16 * 300, 16 * 77 + 2], 1 / 32, dict(epsilon=0.8, microbatch_size=3, topk=40))  # stream kernel, top-k
 synth_run([16 * 400 + 1], 0.05, dict(topk=64, microbatch_size=3), kv=capi.PSATTN_KV_F32)
 pool, run = synth_run([16 * 300], 0.05, dict(epsilon=0.9, audit_coverage=1, microbatch_size=2))
 run.exact_attention()
@@ -62,5 +65,14 @@ torch.cuda.synchronize()
 mk = rng.standard_normal((50, T, 40)).astype(np.float32)
 sc = capi.criticality_scores(rng.standard_normal(40).astype(np.float32), mk.mean(1), mk.min(1), mk.max(1), 2)
 capi.rank_by_scores(np.round(sc, 1), np.arange(50))
+torch.cuda.synchronize()
+# drop-in store with long blocks (33..128 tokens: chunked per-head kernel)
+st = capi.Store(capacity=32)
+rng2 = np.random.default_rng(3)
+for i in range(24):
+    nt = int(rng2.integers(1, 129))
+    kk = rng2.standard_normal((nt, 64)).astype(np.float32)
+    capi.check(st.put(i, kk, kk))
+capi.check(st.run_query(rng2.standard_normal(64).astype(np.float32), np.arange(24), capi.config_default(epsilon=0.9))[0])
 torch.cuda.synchronize()
 print("sanitize driver ok")
