@@ -96,7 +96,10 @@ struct BatchView {
 };
 constexpr int kMaxBlockTokens = 128;  // longest block (tokens) a pool slot holds; > 32 runs the chunked per-head kernel
 constexpr int kFirstCap = 512;   // == the GQA kernel's tranche capacity
-constexpr int kStreamEnt = 512;  // distinct blocks one unit may fetch on the stream kernel (else hand-over)
+#ifndef PSA_STREAM_ENT
+#define PSA_STREAM_ENT 512
+#endif
+constexpr int kStreamEnt = PSA_STREAM_ENT;  // distinct blocks one unit may fetch on the stream kernel (else hand-over)
 constexpr int kStreamWRow = 64;  // floats per fetched block: token weights [4 heads][16]
 constexpr int64_t kDenseMaxBlocks = 16384;  // decide smem: 12 B per rank (196 KB)
 constexpr int64_t kDenseHandover = 384;     // ranks a head consumes on the round kernel before the hand-over

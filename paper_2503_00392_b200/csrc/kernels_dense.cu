@@ -339,6 +339,7 @@ __device__ __forceinline__ void dense_decide_head(const BatchView& b, int u, int
     const int tid = threadIdx.x;
     const int64_t seg = (limit + kDecideThreads - 1) / kDecideThreads;
     const int64_t r0 = (int64_t)tid * seg, r1 = r0 + seg < limit ? r0 + seg : limit;
+    // (the walk uses fp32 exponentials; the reported estimate is recomputed in fp64 below)
     auto absorb = [](float x, float& M, double& S, float& mn) {
         if (x > M) {
             S = (M == -INFINITY) ? 1.0 : fma(S, (double)expf(M - x), 1.0);
@@ -365,6 +366,7 @@ __device__ __forceinline__ void dense_decide_head(const BatchView& b, int u, int
     tmn[tid] = mn;
     if (tid == 0) first_stop = ~0ull;
     __syncthreads();
+
     float PM = -INFINITY, Pmn = INFINITY;
     double PS = 0.0;
     for (int t = 0; t < tid; ++t) {
@@ -377,27 +379,54 @@ __device__ __forceinline__ void dense_decide_head(const BatchView& b, int u, int
     }
     // walk again from the prefix
     int64_t stop_r = -1;
-    float stop_est = 0.0f;
     for (int64_t r = r0; r < r1; ++r) {
         absorb(xs[r], PM, PS, Pmn);
         const bool boundary = b.m == 1 || ((r + 1) % b.m) == 0 || (r + 1 == limit);
         if (!boundary) continue;
         const int64_t nl = n - (r + 1);
-        const float sf = (float)PS;
-        const float est = nl == 0 ? 1.0f : sf / fmaf((float)nl, expf(Pmn - PM), sf);
-        if (b.iest) b.iest[hb + r] = (double)est;
-        if ((double)est > eps || r + 1 == limit) {
+        const double est = nl == 0 ? 1.0 : PS / fma((double)nl, (double)expf(Pmn - PM), PS);
+        if (b.iest) b.iest[hb + r] = est;
+        if (est > eps || r + 1 == limit) {
             stop_r = r;
-            stop_est = est;
             break;
         }
     }
     if (stop_r >= 0) atomicMin(&first_stop, (unsigned long long)stop_r);
     __syncthreads();
+    // The reported estimate at the stop rank, recomputed in fp64 over the processed ranks (the
+    // reference's CoverageEstimator precision, engine.cpp:38-55): max, then sum exp(x - max) and min.
+    const int64_t last = (int64_t)first_stop;  // every head stops (at the limit at the latest)
+    const int64_t q1 = r1 < last + 1 ? r1 : last + 1;
+    float pm = -INFINITY, pmn = INFINITY;
+    for (int64_t r = r0; r < q1; ++r) {
+        pm = fmaxf(pm, xs[r]);
+        pmn = fminf(pmn, xs[r]);
+    }
+    tM[tid] = pm;
+    tmn[tid] = pmn;
+    __syncthreads();
+    __shared__ float Mfin, mnfin;
+    if (tid == 0) {
+        float a = -INFINITY, c = INFINITY;
+        for (int t = 0; t < kDecideThreads; ++t) {
+            a = fmaxf(a, tM[t]);
+            c = fminf(c, tmn[t]);
+        }
+        Mfin = a;
+        mnfin = c;
+    }
+    __syncthreads();
+    double ps = 0.0;
+    for (int64_t r = r0; r < q1; ++r) ps += exp((double)xs[r] - (double)Mfin);
+    tS[tid] = ps;
+    __syncthreads();
     if (stop_r >= 0 && (unsigned long long)stop_r == first_stop) {
         const int64_t cb = stop_r + 1;
+        double S64 = 0.0;
+        for (int t = 0; t < kDecideThreads; ++t) S64 += tS[t];
+        const int64_t nl = n - cb;
         b.bp[qi] = cb;
-        b.est[qi] = (double)stop_est;
+        b.est[qi] = nl == 0 ? 1.0 : S64 / fma((double)nl, exp((double)mnfin - (double)Mfin), S64);
         b.term[qi] = b.topk > 0 ? (limit < n) : (cb < n);
         b.dense_thr[qi] = ks[stop_r];
     }
@@ -442,15 +471,9 @@ __device__ __forceinline__ void dense_v_unit(const PoolView& p, const BatchView&
             if (h < g && b.keys[off * g + (int64_t)h * n + e] <= thr[h]) m |= 1u << h;
         return m;
     };
-    constexpr int NTV = G > 2 ? 2 : 1;  // n-tiles of (head, split) columns: 2 heads x 4 per tile
-    float Oreg[NTV][8], Mreg[NTV], Lreg[NTV];
+    float Oreg[16], Mreg = -INFINITY, Lreg = 0.0f;
 #pragma unroll
-    for (int t = 0; t < NTV; ++t) {
-        Mreg[t] = -INFINITY;
-        Lreg[t] = 0.0f;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) Oreg[t][i] = 0.0f;
-    }
+    for (int j = 0; j < 16; ++j) Oreg[j] = 0.0f;
     // membership masks and slots run kDensePf iterations ahead of the V reads: the L2 prefetch (same
     // distance) touches only blocks of the union, so no V byte outside it is fetched
     constexpr int kD = kDensePf;
@@ -489,62 +512,42 @@ __device__ __forceinline__ void dense_v_unit(const PoolView& p, const BatchView&
             vw[r][0] = x0.x; vw[r][1] = x0.y; vw[r][2] = x0.z; vw[r][3] = x0.w;
             vw[r][4] = x1.x; vw[r][5] = x1.y; vw[r][6] = x1.z; vw[r][7] = x1.w;
         }
-        // B columns of n-tile t = (head 2t + c/4, split c%4): weights p_t of the head as an exact 3-term
-        // bf16 split (fp32 weights; the 4th column is zero), zero if the head did not commit the block
-        uint32_t bfr[NTV][2];
+        // B columns = (head, split): weights p_t of head hb (2-term bf16 split), zero if not committed
+        const int hbq = gq >> 1, sb = gq & 1;
+        const bool hon = hbq < g && (mask >> hbq) & 1u;
+        uint32_t bfr[2];
 #pragma unroll
-        for (int t = 0; t < NTV; ++t) {
-            const int hq = 2 * t + (gq >> 2), sp = gq & 3;
-            const bool hon = hq < g && (mask >> hq) & 1u;
-#pragma unroll
-            for (int hf = 0; hf < 2; ++hf) {
-                float2 wv = make_float2(0.0f, 0.0f);
-                if (hon)
-                    wv = *reinterpret_cast<const float2*>(b.dense_p + ((off * g + (int64_t)hq * n) + e) * 16 + 2 * tq + 8 * hf);
-                bfr[t][hf] = pack_split3(wv.x, wv.y, sp);
-            }
+        for (int hf = 0; hf < 2; ++hf) {
+            float2 wv = make_float2(0.0f, 0.0f);
+            if (hon) wv = *reinterpret_cast<const float2*>(b.dense_p + ((off * g + (int64_t)hbq * n) + e) * 16 + 2 * tq + 8 * hf);
+            bfr[hf] = pack_bf16x2_split(wv.x, wv.y, sb);
         }
-        // A = V^T with the dims permuted by the loads above: m-tile i row gq is dim 16gq + 2i, row gq+8 is
-        // dim 16gq + 2i + 1; lane (gq, tq) of tile t ends with head 2t + tq/2 at dim 16gq + 2i + (tq & 1)
-        float ob[NTV][8];
+        float ob[16];
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-            const uint32_t a0 = __byte_perm(vw[0][i], vw[1][i], 0x5410), a1 = __byte_perm(vw[0][i], vw[1][i], 0x7632);
-            const uint32_t a2 = __byte_perm(vw[2][i], vw[3][i], 0x5410), a3 = __byte_perm(vw[2][i], vw[3][i], 0x7632);
-#pragma unroll
-            for (int t = 0; t < NTV; ++t) {
-                float c0 = 0.f, c1 = 0.f, c2 = 0.f, c3 = 0.f;
-                mma_bf16_16816(c0, c1, c2, c3, a0, a1, a2, a3, bfr[t][0], bfr[t][1]);
-                const float x = (tq & 1) ? (c0 + c1) : (c2 + c3);
-                const float y = __shfl_xor_sync(PSA_FULL, x, 1);
-                ob[t][i] = ((tq & 1) ? (c2 + c3) : (c0 + c1)) + y;
-            }
+            float c0 = 0.f, c1 = 0.f, c2 = 0.f, c3 = 0.f;
+            mma_bf16_16816(c0, c1, c2, c3, __byte_perm(vw[0][i], vw[1][i], 0x5410), __byte_perm(vw[0][i], vw[1][i], 0x7632),
+                           __byte_perm(vw[2][i], vw[3][i], 0x5410), __byte_perm(vw[2][i], vw[3][i], 0x7632), bfr[0], bfr[1]);
+            ob[2 * i] = c0 + c1;
+            ob[2 * i + 1] = c2 + c3;
         }
+        if (tq < g && ((mask >> tq) & 1u)) {
+            const float la = b.dense_la[off * g + (int64_t)tq * n + e];  // block weight exp(la - M), sum_t p_t = 1
+            const float mnew = fmaxf(Mreg, la);
+            const float a = expf(Mreg - mnew);
+            const float cc = expf(la - mnew);
 #pragma unroll
-        for (int t = 0; t < NTV; ++t) {
-            const int hq = 2 * t + (tq >> 1);
-            if (hq < g && ((mask >> hq) & 1u)) {
-                const float la = b.dense_la[off * g + (int64_t)hq * n + e];  // block weight exp(la - M), sum_t p_t = 1
-                const float mnew = fmaxf(Mreg[t], la);
-                const float a = expf(Mreg[t] - mnew);
-                const float cc = expf(la - mnew);
-#pragma unroll
-                for (int i = 0; i < 8; ++i) Oreg[t][i] = Oreg[t][i] * a + ob[t][i] * cc;
-                Lreg[t] = Lreg[t] * a + cc;
-                Mreg[t] = mnew;
-            }
+            for (int j = 0; j < 16; ++j) Oreg[j] = Oreg[j] * a + ob[j] * cc;
+            Lreg = Lreg * a + cc;
+            Mreg = mnew;
         }
     }
+    if (tq < G) {
 #pragma unroll
-    for (int t = 0; t < NTV; ++t) {
-        const int hq = 2 * t + (tq >> 1);
-        if (hq < G) {
-#pragma unroll
-            for (int i = 0; i < 8; ++i) so[warp][hq][16 * gq + 2 * i + (tq & 1)] = Oreg[t][i];
-            if (gq == 0 && (tq & 1) == 0) {
-                som[warp][hq] = Mreg[t];
-                sol[warp][hq] = Lreg[t];
-            }
+        for (int j = 0; j < 16; ++j) so[warp][tq][16 * gq + j] = Oreg[j];
+        if (gq == 0) {
+            som[warp][tq] = Mreg;
+            sol[warp][tq] = Lreg;
         }
     }
     __syncthreads();

@@ -44,6 +44,7 @@
 #include "common.cuh"
 #include "kernels.cuh"
 #include "mma.cuh"
+#include "tma.cuh"
 
 namespace psa {
 
@@ -55,8 +56,17 @@ __device__ int* g_stream_dbg = nullptr;
 
 namespace stream {
 
-constexpr int kThreads = 256;
-constexpr int kNS = 3, kNV = 3;          // scorer / V warps
+#ifndef PSA_STREAM_NS
+#define PSA_STREAM_NS 3
+#endif
+#ifndef PSA_STREAM_NV
+#define PSA_STREAM_NV 3
+#endif
+#ifndef PSA_STREAM_MINB
+#define PSA_STREAM_MINB 2
+#endif
+constexpr int kNS = PSA_STREAM_NS, kNV = PSA_STREAM_NV;  // scorer / V warps
+constexpr int kThreads = (2 + kNS + kNV) * 32;
 constexpr int kWS0 = 2, kWV0 = 2 + kNS;  // first scorer / V warp
 #ifndef PSA_STREAM_RK
 #define PSA_STREAM_RK 9
@@ -77,7 +87,11 @@ constexpr int kRK = PSA_STREAM_RK;  // K ring stages (4 KB K tile)
 constexpr int kRV = PSA_STREAM_RV;  // V ring stages (4 KB V tile + the block's token weights)
 constexpr int kLR = 8;              // round slots in flight
 constexpr int kENT = kStreamEnt;    // distinct blocks per unit
-constexpr int kHash = 2 * kENT;     // list position -> entry (open addressing)
+#ifndef PSA_STREAM_HASH
+#define PSA_STREAM_HASH (2 * kStreamEnt)
+#endif
+constexpr int kHash = PSA_STREAM_HASH;  // list position -> entry (open addressing), a power of two
+static_assert((kHash & (kHash - 1)) == 0 && kHash >= kENT && kHash <= 2048, "hash size");
 constexpr int kLook = PSA_STREAM_LOOK;
 // V reference R of a head: its top criticality score + kVRef. Kept while the rank-0 block's max is
 // at least R - kVLow and no scored block's max exceeds R + kVHigh; otherwise the unit is redone densely.
@@ -115,51 +129,6 @@ struct Smem {
     uint64_t kfull[kRK], kempty[kRK], vfull[kRV], vempty[kRV];
     uint64_t rpub[kLR], rscored[kLR], rdec[kLR];
 };
-
-__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t phase) {
-    uint32_t ok;
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-        "selp.u32 %0, 1, 0, p;\n"
-        "}\n"
-        : "=r"(ok)
-        : "r"(smem_u32(bar)), "r"(phase)
-        : "memory");
-    return ok != 0;
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-// 2-D tiled TMA load (box 64 dims x 16 tokens, 128-byte swizzle) completing on `bar`.
-__device__ __forceinline__ void tma_tile(uint32_t dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-            dst),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
-        : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
-                 : "memory");
-}
-__device__ __forceinline__ void ldsm4(uint32_t addr, uint32_t& a0, uint32_t& a1, uint32_t& a2, uint32_t& a3) {
-    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(a0), "=r"(a1), "=r"(a2), "=r"(a3)
-                 : "r"(addr));
-}
-__device__ __forceinline__ void ldsm4t(uint32_t addr, uint32_t& a0, uint32_t& a1, uint32_t& a2, uint32_t& a3) {
-    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(a0), "=r"(a1), "=r"(a2), "=r"(a3)
-                 : "r"(addr));
-}
-// Byte address of the 16-byte chunk c (0..15, 8 dims each) of token row r (0..15) in a tile
-// loaded as two 64-dim boxes with the 128-byte swizzle (chunk index XOR row % 8).
-__device__ __forceinline__ uint32_t swz(uint32_t base, int r, int c) {
-    return base + (uint32_t)((c >> 3) * 2048 + r * 128 + (((c & 7) ^ (r & 7)) << 4));
-}
 
 #ifdef PSA_STREAM_DEBUG
 __device__ __noinline__ void dbg_stuck(int site, int a0, int a1, int a2, int a3, int a4, int a5, int a6, int a7) {
@@ -214,7 +183,7 @@ __device__ __noinline__ void dbg_note(int site, int a0, int a1, int a2, int a3, 
 #endif
 
 template <int G>
-__global__ void __launch_bounds__(kThreads, 2) psa_stream_kernel(const __grid_constant__ CUtensorMap kvmap,
+__global__ void __launch_bounds__(kThreads, PSA_STREAM_MINB) psa_stream_kernel(const __grid_constant__ CUtensorMap kvmap,
                                                                 PoolView p, BatchView b) {
     constexpr int C = 32 / G;  // ranks per head per round
     constexpr int NT = G / 2;  // n8 tiles (4 columns per head: 3 split terms + 0)
@@ -298,6 +267,8 @@ __global__ void __launch_bounds__(kThreads, 2) psa_stream_kernel(const __grid_co
                 if (s.r_stop[rs]) stopped = true;
                 progress = true;
             }
+            // lane 0 acquired the decisions; order the warp's later shared reads (vq, r_*) after it
+            if (progress) __syncwarp();
             // (2) publish the next round (speculative: heads live as of the last decided round)
             if (!stopped && !closed && k_pub <= decided + kLook) {
                 const int rs = k_pub % kLR;
