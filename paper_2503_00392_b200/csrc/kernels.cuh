@@ -100,7 +100,7 @@ constexpr int kFirstCap = 512;   // == the GQA kernel's tranche capacity
 #define PSA_STREAM_ENT 512
 #endif
 constexpr int kStreamEnt = PSA_STREAM_ENT;  // distinct blocks one unit may fetch on the stream kernel (else hand-over)
-constexpr int kStreamWRow = 64;  // floats per fetched block: token weights [4 heads][16]
+constexpr int kStreamWRow = 68;  // floats per fetched block: token weights [4 heads][16] + 4 exponent sums
 constexpr int64_t kDenseMaxBlocks = 16384;  // decide smem: 12 B per rank (196 KB)
 constexpr int64_t kDenseHandover = 384;     // ranks a head consumes on the round kernel before the hand-over
 constexpr int64_t kDenseSlice = 512;        // list positions per dense K / V work item

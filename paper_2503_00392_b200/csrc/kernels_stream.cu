@@ -93,6 +93,11 @@ constexpr int kENT = kStreamEnt;    // distinct blocks per unit
 constexpr int kHash = PSA_STREAM_HASH;  // list position -> entry (open addressing), a power of two
 static_assert((kHash & (kHash - 1)) == 0 && kHash >= kENT && kHash <= 2048, "hash size");
 constexpr int kLook = PSA_STREAM_LOOK;
+#ifndef PSA_STREAM_SPL
+#define PSA_STREAM_SPL 1
+#endif
+constexpr int kSPL = PSA_STREAM_SPL;  // rank slots per lane in a round: a round is 32*kSPL/G ranks per head
+static_assert(kSPL == 1 || kSPL == 2, "1 or 2 rank slots per lane");
 // V reference R of a head: its top criticality score + kVRef. Kept while the rank-0 block's max is
 // at least R - kVLow and no scored block's max exceeds R + kVHigh; otherwise the unit is redone densely.
 constexpr float kVRef = 8.0f, kVLow = 40.0f, kVHigh = 60.0f;
@@ -107,9 +112,8 @@ template <int G>
 struct Smem {
     alignas(1024) unsigned char kring[kRK][4096];
     alignas(1024) unsigned char vring[kRV][4096];
-    alignas(16) float vw[kRV][G * 16];  // token weights beside each V tile
+    alignas(16) float vw[kRV][G * 16 + 4];  // token weights beside each V tile, then the heads' exponent sums
     float em[kENT][G];                 // block log mass per (entry, head) (the stop rule's observation)
-    float el[kENT][G];                 // block exp-sum relative to the head's V reference R_h
     int32_t eslot[kENT];
     int32_t epos[kENT];
     uint32_t vmask[kENT];  // heads that committed the entry (decider)
@@ -117,7 +121,7 @@ struct Smem {
     uint8_t queued[kENT];
     int32_t hkey[kHash];
     int16_t hval[kHash];
-    int16_t r_map[kLR][32];  // (head, rank-in-round) lane -> entry, -1 none
+    int16_t r_map[kLR][32 * kSPL];  // (head, rank-in-round) slot lane*kSPL+s -> entry, -1 none
     int32_t r_e0[kLR], r_cnt[kLR], r_flag[kLR];
     int32_t r_live[kLR], r_vc[kLR], r_stop[kLR];  // decider -> producer, per decided round
     int16_t vq[kENT + kNV];  // V items in creation order (entry), -1 = end
@@ -185,9 +189,10 @@ __device__ __noinline__ void dbg_note(int site, int a0, int a1, int a2, int a3, 
 template <int G>
 __global__ void __launch_bounds__(kThreads, PSA_STREAM_MINB) psa_stream_kernel(const __grid_constant__ CUtensorMap kvmap,
                                                                 PoolView p, BatchView b) {
-    constexpr int C = 32 / G;  // ranks per head per round
+    constexpr int LPH = 32 / G;    // lanes per head (producer / decider)
+    constexpr int C = LPH * kSPL;  // ranks per head per round
     constexpr int NT = G / 2;  // n8 tiles (4 columns per head: 3 split terms + 0)
-    constexpr uint32_t kWB = G * 16 * 4;  // weight bytes per entry
+    constexpr uint32_t kWB = (G * 16 + 4) * 4;  // weight bytes per entry (+ exponent sums)
     extern __shared__ unsigned char smem_raw[];
     Smem<G>& s = *reinterpret_cast<Smem<G>*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -230,27 +235,30 @@ __global__ void __launch_bounds__(kThreads, PSA_STREAM_MINB) psa_stream_kernel(c
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&kvmap)) : "memory");
         for (int i = lane; i < kHash; i += 32) s.hkey[i] = -1;
         __syncwarp();
-        const int h = lane / C, i = lane % C;
+        const int h = lane / LPH, il = lane % LPH;  // head; the lane's slots are ranks il*kSPL + s of a round
         const bool hv = h < g;
         const size_t qi = (size_t)u * g + (hv ? h : 0);
         const int ftc = hv ? b.ft_count[qi] : 0;
         const uint64_t pmask = (b.pos_bits >= 64) ? ~0ull : ((1ull << b.pos_bits) - 1ull);
         int k_pub = 0, E = 0, k_issue = 0, v_seen = 0, v_issued = 0, decided = -1, lm = (1 << g) - 1;
         bool stopped = false, closed = false;  // closed: no more rounds (entry table full)
-        auto fetch = [&](int k, int32_t& pos, int32_t& slot, int32_t& nt) {
-            const int64_t r = (int64_t)k * C + i;
-            if (hv && r < ftc && r < limit) {
-                pos = (int32_t)(b.ft_keys[qi * kFirstCap + r] & pmask);
-                slot = b.ft_slot[qi * kFirstCap + r];
-                nt = b.ft_ntok[qi * kFirstCap + r];
-            } else {
-                pos = -1;
-                slot = 0;
-                nt = 0;
+        int32_t fpos[kSPL], fslot[kSPL], fnt[kSPL];
+        auto fetch = [&](int k) {
+#pragma unroll
+            for (int sl = 0; sl < kSPL; ++sl) {
+                const int64_t r = (int64_t)k * C + il * kSPL + sl;
+                if (hv && r < ftc && r < limit) {
+                    fpos[sl] = (int32_t)(b.ft_keys[qi * kFirstCap + r] & pmask);
+                    fslot[sl] = b.ft_slot[qi * kFirstCap + r];
+                    fnt[sl] = b.ft_ntok[qi * kFirstCap + r];
+                } else {
+                    fpos[sl] = -1;
+                    fslot[sl] = 0;
+                    fnt[sl] = 0;
+                }
             }
         };
-        int32_t fpos, fslot, fnt;
-        fetch(0, fpos, fslot, fnt);
+        fetch(0);
 #ifdef PSA_STREAM_DEBUG
         int idle = 0;
 #endif
@@ -272,73 +280,72 @@ __global__ void __launch_bounds__(kThreads, PSA_STREAM_MINB) psa_stream_kernel(c
             // (2) publish the next round (speculative: heads live as of the last decided round)
             if (!stopped && !closed && k_pub <= decided + kLook) {
                 const int rs = k_pub % kLR;
-                const bool valid = fpos >= 0 && ((lm >> h) & 1);
-                const unsigned peers = __match_any_sync(PSA_FULL, valid ? fpos : -1 - lane);
-                const int leader = __ffs(peers) - 1;
-                const bool lead = valid && leader == lane;
-                int hs = 0, ent = -1;
-                bool isnew = false;
-                if (lead) {  // unit-wide dedup: a block fetched in an earlier round is not fetched again
-                    hs = (int)(((uint32_t)fpos * 2654435761u) >> 21) & (kHash - 1);
-                    for (;;) {
-                        const int kk = s.hkey[hs];
-                        if (kk == fpos) {
-                            ent = s.hval[hs];
-                            break;
-                        }
-                        if (kk == -1) {
-                            const int old = atomicCAS(&s.hkey[hs], -1, fpos);
-                            if (old == -1) {
-                                isnew = true;
+                const int e_round0 = E;
+#pragma unroll
+                for (int sl = 0; sl < kSPL; ++sl) {  // one pass per rank slot of the lanes
+                    const bool valid = !closed && fpos[sl] >= 0 && ((lm >> h) & 1);
+                    const unsigned peers = __match_any_sync(PSA_FULL, valid ? fpos[sl] : -1 - lane);
+                    const int leader = __ffs(peers) - 1;
+                    const bool lead = valid && leader == lane;
+                    int hs = 0, ent = -1;
+                    bool isnew = false;
+                    if (lead) {  // unit-wide dedup: a block fetched in an earlier round is not fetched again
+                        hs = (int)(((uint32_t)fpos[sl] * 2654435761u) >> 21) & (kHash - 1);
+                        for (;;) {
+                            const int kk = s.hkey[hs];
+                            if (kk == fpos[sl]) {
+                                ent = s.hval[hs];
                                 break;
                             }
-                            continue;  // another lane took the slot: look at it again
+                            if (kk == -1) {
+                                const int old = atomicCAS(&s.hkey[hs], -1, fpos[sl]);
+                                if (old == -1) {
+                                    isnew = true;
+                                    break;
+                                }
+                                continue;  // another lane took the slot: look at it again
+                            }
+                            hs = (hs + 1) & (kHash - 1);
                         }
-                        hs = (hs + 1) & (kHash - 1);
+                    }
+                    const unsigned nb = __ballot_sync(PSA_FULL, isnew);
+                    const int cnt = __popc(nb);
+                    if (closed || E + cnt > kENT) {
+                        // more distinct blocks than the entry table holds: the decider hands the unit
+                        // over (dense path) at this round; nothing more is published
+                        s.r_map[rs][lane * kSPL + sl] = -1;
+                        closed = true;
+                    } else {
+                        if (isnew) {
+#if PSA_STREAM_PF
+                            // the entry's K (PF=2) or K and V (PF=1, one contiguous slot) start towards L2
+                            // now, kLook rounds before the K tile is needed: the K ring refills from L2
+                            prefetch_l2_bulk(p.kv + (int64_t)fslot[sl] * p.slot_bytes,
+                                             (uint32_t)(PSA_STREAM_PF == 2 ? p.slot_bytes / 2 : p.slot_bytes));
+#endif
+                            ent = E + __popc(nb & ((1u << lane) - 1u));
+                            s.hval[hs] = (int16_t)ent;
+                            s.eslot[ent] = fslot[sl];
+                            s.epos[ent] = fpos[sl];
+                            s.entok[ent] = (uint8_t)fnt[sl];
+                            s.vmask[ent] = 0u;
+                            s.queued[ent] = 0;
+                        }
+                        const int myent = __shfl_sync(PSA_FULL, ent, leader);
+                        s.r_map[rs][lane * kSPL + sl] = (int16_t)(valid ? myent : -1);
+                        if (k_pub == 0 && il == 0 && sl == 0 && valid) s.rank0[h] = myent;
+                        E += cnt;
                     }
                 }
-                const unsigned nb = __ballot_sync(PSA_FULL, isnew);
-                const int cnt = __popc(nb);
-                if (E + cnt > kENT) {
-                    // more distinct blocks than the entry table holds: the decider hands the unit
-                    // over (dense path) at this round; nothing more is published
-                    if (lane == 0) {
-                        s.r_e0[rs] = E;
-                        s.r_cnt[rs] = 0;
-                        s.r_flag[rs] = 1;
-                    }
-                    s.r_map[rs][lane] = -1;
-                    closed = true;
-                } else {
-                    if (isnew) {
-#if PSA_STREAM_PF
-                        // the entry's K (PF=2) or K and V (PF=1, one contiguous slot) start towards L2 now,
-                        // kLook rounds before the K tile is needed: the K ring then refills from L2
-                        prefetch_l2_bulk(p.kv + (int64_t)fslot * p.slot_bytes,
-                                         (uint32_t)(PSA_STREAM_PF == 2 ? p.slot_bytes / 2 : p.slot_bytes));
-#endif
-                        ent = E + __popc(nb & ((1u << lane) - 1u));
-                        s.hval[hs] = (int16_t)ent;
-                        s.eslot[ent] = fslot;
-                        s.epos[ent] = fpos;
-                        s.entok[ent] = (uint8_t)fnt;
-                        s.vmask[ent] = 0u;
-                        s.queued[ent] = 0;
-                    }
-                    const int myent = __shfl_sync(PSA_FULL, ent, leader);
-                    s.r_map[rs][lane] = (int16_t)(valid ? myent : -1);
-                    if (k_pub == 0 && i == 0 && valid) s.rank0[h] = myent;
-                    if (lane == 0) {
-                        s.r_e0[rs] = E;
-                        s.r_cnt[rs] = cnt;
-                        s.r_flag[rs] = 0;
-                    }
-                    E += cnt;
+                if (lane == 0) {
+                    s.r_e0[rs] = e_round0;
+                    s.r_cnt[rs] = E - e_round0;
+                    s.r_flag[rs] = closed ? 1 : 0;
                 }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&s.rpub[rs]);
                 ++k_pub;
-                if (!closed) fetch(k_pub, fpos, fslot, fnt);
+                if (!closed) fetch(k_pub);
                 progress = true;
             }
             // (3) K tiles of new entries, while K stages are free
@@ -434,13 +441,13 @@ __global__ void __launch_bounds__(kThreads, PSA_STREAM_MINB) psa_stream_kernel(c
         }
     } else if (warp == 1) {
         // ================================ DECIDER ================================
-        const int h = lane / C, i = lane % C;
+        const int h = lane / LPH, il = lane % LPH;  // head; the lane's slots are ranks il*kSPL + sl
         const bool hv = h < g;
         const int64_t qi = (int64_t)u * g + (hv ? h : 0);
         const int64_t hb = off * g + (int64_t)(hv ? h : 0) * n;
         const int ftc = hv ? b.ft_count[qi] : 0;
         const double eps = b.topk > 0 ? 1.0 : b.eps;
-        const unsigned seg = (C == 32 ? PSA_FULL : ((1u << C) - 1u)) << (h * C);
+        const unsigned seg = (LPH == 32 ? PSA_FULL : ((1u << LPH) - 1u)) << (h * LPH);
         const uint32_t all = (1u << g) - 1u;
         bool live = hv;
         int64_t cb = 0;
@@ -450,7 +457,7 @@ __global__ void __launch_bounds__(kThreads, PSA_STREAM_MINB) psa_stream_kernel(c
         // dense kernels after its first round instead of after kDenseHandover ranks (performance
         // only: both paths produce the same processed sets)
         bool flat = false;
-        if (b.dense_early > 0.0f && hv && i == 0 && ftc >= kDenseHandover && limit > kDenseHandover) {
+        if (b.dense_early > 0.0f && hv && il == 0 && ftc >= kDenseHandover && limit > kDenseHandover) {
             const uint64_t pm = (b.pos_bits >= 64) ? ~0ull : ((1ull << b.pos_bits) - 1ull);
             const double s0 = key_score(b.ft_keys[qi * kFirstCap], pm);
             const double s1 = key_score(b.ft_keys[qi * kFirstCap + kDenseHandover - 1], pm);
@@ -467,23 +474,40 @@ __global__ void __launch_bounds__(kThreads, PSA_STREAM_MINB) psa_stream_kernel(c
 #ifdef PSA_STREAM_PROF
             const long long td0_ = clock64();
 #endif
-            const int e = s.r_map[rs][lane];
             const int e_end = s.r_e0[rs] + s.r_cnt[rs];  // entries published up to this round
             const bool overflow = s.r_flag[rs] == 1;
-            const int64_t r = cb + i;
-            const bool valid = live && e >= 0 && r < limit;
-            double x = -INFINITY, mx;
+            int e[kSPL];
+            int64_t r[kSPL];
+            bool valid[kSPL];
+            double x[kSPL];
+            float xmax = -INFINITY;
+            double xmaxd = -INFINITY;
+#pragma unroll
+            for (int sl = 0; sl < kSPL; ++sl) {
+                e[sl] = s.r_map[rs][lane * kSPL + sl];
+                r[sl] = cb + il * kSPL + sl;
+                valid[sl] = live && e[sl] >= 0 && r[sl] < limit;
+                x[sl] = -INFINITY;
+                if (valid[sl]) {
+                    if (!b.has_oracle) {
+                        const float xf = s.em[e[sl]][h];
+                        x[sl] = (double)xf;
+                        xmax = fmaxf(xmax, xf);
+                    } else {
+                        x[sl] = b.omass[hb + s.epos[e[sl]]];
+                        xmaxd = fmax(xmaxd, x[sl]);
+                    }
+                }
+            }
+            double mx;
             if (!b.has_oracle) {  // fp32 masses: the segment max is exact in fp32
-                float xf = valid ? s.em[e][h] : -INFINITY;
-                x = (double)xf;
 #pragma unroll
-                for (int o = C / 2; o >= 1; o >>= 1) xf = fmaxf(xf, __shfl_xor_sync(PSA_FULL, xf, o));
-                mx = (double)xf;
+                for (int o = LPH / 2; o >= 1; o >>= 1) xmax = fmaxf(xmax, __shfl_xor_sync(PSA_FULL, xmax, o));
+                mx = (double)xmax;
             } else {
-                if (valid) x = b.omass[hb + s.epos[e]];
-                mx = x;
+                mx = xmaxd;
 #pragma unroll
-                for (int o = C / 2; o >= 1; o >>= 1) mx = fmax(mx, __shfl_xor_sync(PSA_FULL, mx, o));
+                for (int o = LPH / 2; o >= 1; o >>= 1) mx = fmax(mx, __shfl_xor_sync(PSA_FULL, mx, o));
             }
             mx = fmax(mx, M);
             // carried state re-expressed about the new max (only when it moved: rare after round 0)
@@ -494,40 +518,87 @@ __global__ void __launch_bounds__(kThreads, PSA_STREAM_MINB) psa_stream_kernel(c
                 Sc = S * fct;
                 Ec = E * fct;
             }
-            // segment scans: prefix sum and prefix min of exp(mass - mx); exp(min - mx) is the min of
-            // the exponentials (monotone), so one fp64 exp per rank
-            double ev = valid ? exp(x - mx) : 0.0;
-            double em_ = valid ? ev : INFINITY;
+            // prefix sums / prefix mins of exp(mass - mx) in rank order: within the lane's slots, then a
+            // segmented scan over the head's lanes; exp(min - mx) is the min of the exponentials (monotone)
+            double ps[kSPL], pm_[kSPL];
+            double run = 0.0, runm = INFINITY;
 #pragma unroll
-            for (int o = 1; o < C; o <<= 1) {
-                const double ye = __shfl_up_sync(PSA_FULL, ev, o, C);
-                const double ym = __shfl_up_sync(PSA_FULL, em_, o, C);
-                if (i >= o) {
-                    ev += ye;
-                    em_ = fmin(em_, ym);
+            for (int sl = 0; sl < kSPL; ++sl) {
+                const double ev = valid[sl] ? exp(x[sl] - mx) : 0.0;
+                run += ev;
+                runm = fmin(runm, valid[sl] ? ev : INFINITY);
+                ps[sl] = run;
+                pm_[sl] = runm;
+            }
+            double incl = run, inclm = runm;
+#pragma unroll
+            for (int o = 1; o < LPH; o <<= 1) {
+                const double ye = __shfl_up_sync(PSA_FULL, incl, o, LPH);
+                const double ym = __shfl_up_sync(PSA_FULL, inclm, o, LPH);
+                if (il >= o) {
+                    incl += ye;
+                    inclm = fmin(inclm, ym);
                 }
             }
-            const double Si = Sc + ev;        // sum exp(mass - mx) observed up to this rank
-            const double Ei = fmin(Ec, em_);  // exp(min mass - mx)
-            const int64_t nl = n - (r + 1);
-            const double D = (double)nl * Ei;
-            // est = Si / (Si + n_left exp(min - mx)) = 1 / (1 + n_left exp(min - acc)) (engine.cpp:48-55);
-            // est > eps  <=>  Si (1 - eps) > eps D: the division runs only when a head may stop
-            const bool boundary = valid && (b.m == 1 || ((r + 1) % b.m) == 0 || r + 1 == limit);
-            const bool over = nl == 0 ? eps < 1.0 : (Si > 0.0 && Si * one_m_eps > eps * D);
-            const bool stop = boundary && (over || r + 1 == limit);
-            double est_i = 0.0;
-            if (b.iest || __any_sync(PSA_FULL, stop)) est_i = nl == 0 ? 1.0 : (Si > 0.0 ? Si / (Si + D) : 0.0);
-            const unsigned sb = __ballot_sync(PSA_FULL, stop) & seg;
-            const unsigned vb = __ballot_sync(PSA_FULL, valid) & seg;
-            const int nvalid = __popc(vb);
-            const int f = sb ? (__ffs(sb) - 1 - h * C) : nvalid - 1;  // last committed lane of the head
-            const bool committed = valid && i <= f;
-            if (b.iest && boundary && i <= f) b.iest[hb + r] = est_i;  // IterationStats::estimated_coverage
-            if (committed) atomicOr(&s.vmask[e], 1u << h);
-            const int src = h * C + (f > 0 ? f : 0);
-            const double Sf = __shfl_sync(PSA_FULL, Si, src), Ef = __shfl_sync(PSA_FULL, Ei, src);
-            const double estf = __shfl_sync(PSA_FULL, est_i, src);
+            const double excl = incl - run;  // sum over the head's earlier lanes
+            double exclm = __shfl_up_sync(PSA_FULL, inclm, 1, LPH);
+            if (il == 0) exclm = INFINITY;
+            double Si[kSPL], Ei[kSPL], est_i[kSPL];
+            bool boundary[kSPL], stop[kSPL];
+            bool anystop = false;
+#pragma unroll
+            for (int sl = 0; sl < kSPL; ++sl) {
+                Si[sl] = Sc + (excl + ps[sl]);        // sum exp(mass - mx) observed up to this rank
+                Ei[sl] = fmin(Ec, fmin(exclm, pm_[sl]));  // exp(min mass - mx)
+                const int64_t nl = n - (r[sl] + 1);
+                const double D = (double)nl * Ei[sl];
+                // est = Si / (Si + n_left exp(min - mx)) = 1 / (1 + n_left exp(min - acc)) (engine.cpp:48-55);
+                // est > eps  <=>  Si (1 - eps) > eps D: the division runs only when a head may stop
+                boundary[sl] = valid[sl] && (b.m == 1 || ((r[sl] + 1) % b.m) == 0 || r[sl] + 1 == limit);
+                const bool over = nl == 0 ? eps < 1.0 : (Si[sl] > 0.0 && Si[sl] * one_m_eps > eps * D);
+                stop[sl] = boundary[sl] && (over || r[sl] + 1 == limit);
+                anystop |= stop[sl];
+                est_i[sl] = 0.0;
+            }
+            if (b.iest || __any_sync(PSA_FULL, anystop)) {
+#pragma unroll
+                for (int sl = 0; sl < kSPL; ++sl) {
+                    const int64_t nl = n - (r[sl] + 1);
+                    est_i[sl] = nl == 0 ? 1.0 : (Si[sl] > 0.0 ? Si[sl] / (Si[sl] + (double)nl * Ei[sl]) : 0.0);
+                }
+            }
+            // first stop in rank order (lane-major, slot-minor) and the head's valid ranks
+            int f_stop = 1 << 30, nvalid = 0;
+#pragma unroll
+            for (int sl = 0; sl < kSPL; ++sl) {
+                const unsigned sb_s = __ballot_sync(PSA_FULL, stop[sl]) & seg;
+                const unsigned vb_s = __ballot_sync(PSA_FULL, valid[sl]) & seg;
+                nvalid += __popc(vb_s);
+                if (sb_s) f_stop = min(f_stop, (__ffs(sb_s) - 1 - h * LPH) * kSPL + sl);
+            }
+            const unsigned sb = f_stop < (1 << 30) ? 1u : 0u;  // (head stops in this round)
+            const int f = sb ? f_stop : nvalid - 1;  // last committed rank of the head in this round
+            bool committed[kSPL];
+#pragma unroll
+            for (int sl = 0; sl < kSPL; ++sl) {
+                const int ri = il * kSPL + sl;
+                committed[sl] = valid[sl] && ri <= f;
+                if (b.iest && boundary[sl] && ri <= f) b.iest[hb + r[sl]] = est_i[sl];  // IterationStats
+                if (committed[sl]) atomicOr(&s.vmask[e[sl]], 1u << h);
+            }
+            const int fr = f > 0 ? f : 0;
+            const int src = h * LPH + fr / kSPL, fsl = fr % kSPL;
+            double Sf = 0.0, Ef = 0.0, estf = 0.0;
+#pragma unroll
+            for (int sl = 0; sl < kSPL; ++sl) {
+                const double a1 = __shfl_sync(PSA_FULL, Si[sl], src), a2 = __shfl_sync(PSA_FULL, Ei[sl], src);
+                const double a3 = __shfl_sync(PSA_FULL, est_i[sl], src);
+                if (sl == fsl) {
+                    Sf = a1;
+                    Ef = a2;
+                    estf = a3;
+                }
+            }
             if (nvalid > 0) {
                 M = mx;
                 S = Sf;
@@ -538,7 +609,7 @@ __global__ void __launch_bounds__(kThreads, PSA_STREAM_MINB) psa_stream_kernel(c
             const bool fin_now = live && sb != 0;
             if (fin_now) {
                 live = false;
-                if (i == 0) {
+                if (il == 0) {
                     b.bp[qi] = cb;
                     b.est[qi] = est;
                     b.term[qi] = b.topk > 0 ? (limit < n) : (cb < n);
@@ -560,25 +631,29 @@ __global__ void __launch_bounds__(kThreads, PSA_STREAM_MINB) psa_stream_kernel(c
             // distinct blocks overflow the entry table, is handed over to the dense kernels
             const bool ho = live && cb < limit && (cb >= kDenseHandover || cb >= ftc || overflow || flat_unit);
             const bool anyho = __any_sync(PSA_FULL, ho);
-            const unsigned lb = __ballot_sync(PSA_FULL, live && i == 0);
+            const unsigned lb = __ballot_sync(PSA_FULL, live && il == 0);
             uint32_t lmask = 0;
 #pragma unroll
-            for (int hh = 0; hh < G; ++hh) lmask |= ((lb >> (hh * C)) & 1u) << hh;
+            for (int hh = 0; hh < G; ++hh) lmask |= ((lb >> (hh * LPH)) & 1u) << hh;
             const bool done = anyho || lmask == 0;
             __syncwarp();  // this round's vmask bits are visible to every lane
             if (!anyho) {
                 // V items: a block goes to the V pass once every head has decided it (committed it,
                 // or stopped before reaching it), in a deterministic order
                 const uint32_t stopped = all & ~lmask;
-                const unsigned peers = __match_any_sync(PSA_FULL, committed ? e : -1 - lane);
-                const bool cand = committed && (__ffs(peers) - 1) == lane;
-                const bool ready = cand && ((s.vmask[e] | stopped) == all) && !s.queued[e];
-                const unsigned rb = __ballot_sync(PSA_FULL, ready);
-                if (ready) {
-                    s.vq[vc + __popc(rb & ((1u << lane) - 1u))] = (int16_t)e;
-                    s.queued[e] = 1;
+#pragma unroll
+                for (int sl = 0; sl < kSPL; ++sl) {
+                    const unsigned peers = __match_any_sync(PSA_FULL, committed[sl] ? e[sl] : -1 - lane);
+                    const bool cand = committed[sl] && (__ffs(peers) - 1) == lane;
+                    const bool ready = cand && ((s.vmask[e[sl]] | stopped) == all) && !s.queued[e[sl]];
+                    const unsigned rb = __ballot_sync(PSA_FULL, ready);
+                    if (ready) {
+                        s.vq[vc + __popc(rb & ((1u << lane) - 1u))] = (int16_t)e[sl];
+                        s.queued[e[sl]] = 1;
+                    }
+                    vc += __popc(rb);
+                    __syncwarp();  // queued flags of this pass before the next slot's
                 }
-                vc += __popc(rb);
                 if (__any_sync(PSA_FULL, fin_now)) {  // a head stopped: blocks waiting only on it are ready
                     __syncwarp();
                     for (int e0 = 0; e0 < e_end; e0 += 32) {
@@ -717,7 +792,7 @@ __global__ void __launch_bounds__(kThreads, PSA_STREAM_MINB) psa_stream_kernel(c
                         we[hq * 16 + gq + 8] = whi;
                         if (gq == 0) {
                             s.em[e][hq] = la;  // log_as (attention.hpp:73)
-                            s.el[e][hq] = lbv;
+                            we[G * 16 + hq] = lbv;  // exponent sum about R_h (travels with the weights)
                         }
                     }
                 }
@@ -763,7 +838,7 @@ __global__ void __launch_bounds__(kThreads, PSA_STREAM_MINB) psa_stream_kernel(c
             const int nt = s.entok[e];
 #pragma unroll
             for (int h = 0; h < G; ++h)
-                if ((mask >> h) & 1u) Lh[h] += s.el[e][h];
+                if ((mask >> h) & 1u) Lh[h] += s.vw[st][G * 16 + h];
             uint32_t bw[NT][2];
 #pragma unroll
             for (int t = 0; t < NT; ++t) {
