@@ -8,9 +8,10 @@
 // admits it (evicting the oldest entry of a full domain; the eviction is charged to the
 // victim's layer), release drops entries without counting evictions.
 //
-// Representation: each domain is an intrusive doubly linked recency chain stored in one hash
-// map (id -> {older, newer} neighbour ids), with the newest / oldest ids at the ends — one
-// lookup per access, no per-entry list nodes.
+// Representation: each domain is an intrusive doubly linked recency chain (id -> {older, newer}
+// neighbour ids) with the newest / oldest ids at the ends, no per-entry list nodes: in a hash map
+// for arbitrary ids (the C/C++ store), in two flat arrays for dense ids (the two-tier store's
+// block indices: no hashing on the per-step accounting replay).
 #pragma once
 
 #include <cstdint>
@@ -25,18 +26,29 @@ class RecencyChain {
 public:
     static constexpr std::int64_t kNone = INT64_MIN;
 
-    explicit RecencyChain(std::size_t capacity = 0) : cap_(capacity) {}
+    // dense_ids > 0: ids are known to lie in [0, dense_ids) (the two-tier store's block indices):
+    // the links live in two flat arrays indexed by id instead of a hash map (no hashing per access).
+    explicit RecencyChain(std::size_t capacity = 0, std::size_t dense_ids = 0)
+        : cap_(capacity), dense_(dense_ids > 0) {
+        if (dense_) {
+            older_.assign(dense_ids, kNone);
+            newer_.assign(dense_ids, kNone);
+            in_.assign(dense_ids, 0);
+        }
+    }
     std::size_t capacity() const { return cap_; }
-    std::size_t size() const { return links_.size(); }
-    bool contains(std::int64_t id) const { return links_.count(id) != 0; }
+    std::size_t size() const { return dense_ ? count_ : links_.size(); }
+    bool contains(std::int64_t id) const {
+        if (dense_) return id >= 0 && static_cast<std::size_t>(id) < in_.size() && in_[static_cast<std::size_t>(id)];
+        return links_.count(id) != 0;
+    }
 
     // Moves a present id to the newest end. Returns false when absent.
     bool refresh(std::int64_t id) {
-        auto it = links_.find(id);
-        if (it == links_.end()) return false;
+        if (!contains(id)) return false;
         if (newest_ != id) {
-            unlink(it->second);
-            link_newest(id, it->second);
+            unlink(id);
+            link_newest(id);
         }
         return true;
     }
@@ -45,19 +57,28 @@ public:
     std::optional<std::int64_t> admit(std::int64_t id) {
         if (cap_ == 0) return std::nullopt;
         std::optional<std::int64_t> victim;
-        if (links_.size() == cap_) {
+        if (size() == cap_) {
             victim = oldest_;
             erase(oldest_);
         }
-        Link& l = links_[id];
-        link_newest(id, l);
+        if (dense_) {
+            in_[static_cast<std::size_t>(id)] = 1;
+            ++count_;
+        } else {
+            links_[id] = Link{};
+        }
+        link_newest(id);
         return victim;
     }
     bool erase(std::int64_t id) {
-        auto it = links_.find(id);
-        if (it == links_.end()) return false;
-        unlink(it->second);
-        links_.erase(it);
+        if (!contains(id)) return false;
+        unlink(id);
+        if (dense_) {
+            in_[static_cast<std::size_t>(id)] = 0;
+            --count_;
+        } else {
+            links_.erase(id);
+        }
         return true;
     }
 
@@ -65,23 +86,35 @@ private:
     struct Link {
         std::int64_t older = kNone, newer = kNone;
     };
-    void unlink(Link& l) {
-        if (l.older != kNone) links_[l.older].newer = l.newer;
-        else oldest_ = l.newer;
-        if (l.newer != kNone) links_[l.newer].older = l.older;
-        else newest_ = l.older;
-        l.older = l.newer = kNone;
+    std::int64_t& older(std::int64_t id) {
+        return dense_ ? older_[static_cast<std::size_t>(id)] : links_.find(id)->second.older;
     }
-    void link_newest(std::int64_t id, Link& l) {
-        l.older = newest_;
-        l.newer = kNone;
-        if (newest_ != kNone) links_[newest_].newer = id;
+    std::int64_t& newer(std::int64_t id) {
+        return dense_ ? newer_[static_cast<std::size_t>(id)] : links_.find(id)->second.newer;
+    }
+    void unlink(std::int64_t id) {
+        std::int64_t& o = older(id);
+        std::int64_t& w = newer(id);
+        if (o != kNone) newer(o) = w;
+        else oldest_ = w;
+        if (w != kNone) older(w) = o;
+        else newest_ = o;
+        o = w = kNone;
+    }
+    void link_newest(std::int64_t id) {
+        older(id) = newest_;
+        newer(id) = kNone;
+        if (newest_ != kNone) newer(newest_) = id;
         newest_ = id;
         if (oldest_ == kNone) oldest_ = id;
     }
 
     std::size_t cap_;
+    bool dense_;
     std::unordered_map<std::int64_t, Link> links_;
+    std::vector<std::int64_t> older_, newer_;
+    std::vector<std::uint8_t> in_;
+    std::size_t count_ = 0;
     std::int64_t newest_ = kNone, oldest_ = kNone;
 };
 
@@ -97,11 +130,12 @@ public:
         std::optional<std::int64_t> evicted;  // victim of the admission (misses only)
     };
 
-    FastTier(std::size_t capacity, std::int32_t n_layers, bool per_layer_domains, bool lru)
+    // dense_ids > 0: every id lies in [0, dense_ids) (array-backed recency chains)
+    FastTier(std::size_t capacity, std::int32_t n_layers, bool per_layer_domains, bool lru, std::size_t dense_ids = 0)
         : per_layer_domains_(per_layer_domains), lru_(lru), layers_(static_cast<std::size_t>(n_layers)) {
         if (n_layers <= 0) throw std::invalid_argument("fast tier: n_layers must be positive");
-        if (per_layer_domains) domains_.assign(layers_.size(), RecencyChain(capacity / layers_.size()));
-        else domains_.assign(1, RecencyChain(capacity));
+        if (per_layer_domains) domains_.assign(layers_.size(), RecencyChain(capacity / layers_.size(), dense_ids));
+        else domains_.assign(1, RecencyChain(capacity, dense_ids));
     }
 
     // put_block's write-allocate (no hit/miss). `layer_of` resolves a victim's layer.

@@ -151,7 +151,7 @@ int psattn_tier_create(const psattn_tier_desc* desc, psattn_tier** out) {
     t->owner.assign(nb, 0);
     const bool per_layer = desc->pool_policy != PSATTN_POOL_UNIFIED;
     t->fast = std::make_unique<psa::FastTier>((size_t)desc->fast_slots, desc->n_layers, per_layer,
-                                              desc->eviction_policy == PSATTN_EVICT_LRU);
+                                              desc->eviction_policy == PSATTN_EVICT_LRU, (size_t)nb);
     // HBM slots: [0, cap) for the unified domain, [l*per, (l+1)*per) for layer l
     const size_t n_dom = per_layer ? (size_t)desc->n_layers : 1;
     const size_t per = per_layer ? (size_t)desc->fast_slots / (size_t)desc->n_layers : (size_t)desc->fast_slots;

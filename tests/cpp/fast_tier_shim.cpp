@@ -8,13 +8,14 @@ namespace {
 struct Shim {
     psa::FastTier tier;
     std::unordered_map<std::int64_t, std::int32_t> layer;
-    Shim(std::size_t cap, int layers, bool per_layer, bool lru) : tier(cap, layers, per_layer, lru) {}
+    Shim(std::size_t cap, int layers, bool per_layer, bool lru, std::size_t dense)
+        : tier(cap, layers, per_layer, lru, dense) {}
 };
 }  // namespace
 
 extern "C" {
-void* ft_create(std::uint64_t cap, int n_layers, int per_layer, int lru) {
-    return new Shim(cap, n_layers, per_layer != 0, lru != 0);
+void* ft_create(std::uint64_t cap, int n_layers, int per_layer, int lru, std::uint64_t dense_ids) {
+    return new Shim(cap, n_layers, per_layer != 0, lru != 0, dense_ids);
 }
 void ft_destroy(void* h) { delete static_cast<Shim*>(h); }
 std::int64_t ft_put(void* h, std::int64_t id, int layer) {

@@ -21,7 +21,7 @@ def shim(tmp_path_factory):
                     os.path.join(ROOT, "tests", "cpp", "fast_tier_shim.cpp"), "-o", so], check=True)
     L = C.CDLL(so)
     L.ft_create.restype = C.c_void_p
-    L.ft_create.argtypes = [C.c_uint64, C.c_int, C.c_int, C.c_int]
+    L.ft_create.argtypes = [C.c_uint64, C.c_int, C.c_int, C.c_int, C.c_uint64]
     L.ft_destroy.argtypes = [C.c_void_p]
     L.ft_put.restype = C.c_int64
     L.ft_put.argtypes = [C.c_void_p, C.c_int64, C.c_int]
@@ -38,11 +38,12 @@ NONE = -(2 ** 63)
 @pytest.mark.parametrize("partitioned", [0, 1])
 @pytest.mark.parametrize("fifo", [0, 1])
 @pytest.mark.parametrize("cap", [0, 5, 12])
-def test_fast_tier_matches_reference_store(shim, ref, partitioned, fifo, cap):
+@pytest.mark.parametrize("dense", [0, 1000])  # hash-map chains (C/C++ store) / flat arrays (two-tier store)
+def test_fast_tier_matches_reference_store(shim, ref, partitioned, fifo, cap, dense):
     rng = np.random.default_rng(100 * cap + 10 * partitioned + fifo)
     layers, d = 3, 4
     st = ref.store(capacity=cap, n_layers=layers, partitioned=partitioned, fifo=fifo)
-    h = shim.ft_create(cap, layers, partitioned, 1 - fifo)
+    h = shim.ft_create(cap, layers, partitioned, 1 - fifo, dense)
     layer_of, ntok, owner_of, live = {}, {}, {}, []
     next_id = 0
     n_loads = 0
