@@ -16,6 +16,9 @@
 // reference counts them — and the blocks that entered the fast tier are installed into
 // their HBM slots by one copy kernel on the caller's stream.
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <limits>
@@ -237,8 +240,12 @@ struct TierIter {
 // query like consecutive psa_attention / topk_attention calls (one TierIter per microbatch).
 int tier_run_account(psattn_tier* t, const psattn_batch* b, void* workspace, cudaStream_t st, bool lockstep,
                      std::vector<TierIter>* iters) {
+    static const bool prof = getenv("PSA_TIER_PROF") != nullptr;  // development: phase times to stderr
+    const auto c0 = std::chrono::steady_clock::now();
     int rc = psattn_run_batch(t->pool, b, workspace, st);
     if (rc) return rc;
+    if (prof) cudaStreamSynchronize(st);
+    const auto c1 = std::chrono::steady_clock::now();
     const int64_t nq = (int64_t)b->n_units * b->group;
     const int64_t hbt = b->total_blocks * b->group;
     std::vector<int64_t> bp((size_t)nq), off((size_t)b->n_units + 1);
@@ -271,11 +278,18 @@ int tier_run_account(psattn_tier* t, const psattn_batch* b, void* workspace, cud
         return end < bp[(size_t)qi];
     };
     if (lockstep) {
-        for (bool live = true; live;) {
-            live = false;
+        // rounds over the live queries in query order (psa_attention_batched, engine.cpp:188-207);
+        // finished queries leave the list, so a round costs only its loads
+        std::vector<int64_t> act;
+        act.reserve((size_t)nq);
+        for (int64_t qi = 0; qi < nq; ++qi)
+            if (cur[(size_t)qi] < bp[(size_t)qi]) act.push_back(qi);
+        while (!act.empty()) {
             TierIter round;
-            for (int64_t qi = 0; qi < nq; ++qi)
-                if (cur[(size_t)qi] < bp[(size_t)qi]) live |= load_mb(qi, round);
+            size_t w = 0;
+            for (size_t k = 0; k < act.size(); ++k)
+                if (load_mb(act[k], round)) act[w++] = act[k];
+            act.resize(w);
             if (iters && round.blocks > 0) iters->push_back(round);
         }
     } else {
@@ -286,7 +300,14 @@ int tier_run_account(psattn_tier* t, const psattn_batch* b, void* workspace, cud
                 if (iters) iters->push_back(it);
             }
     }
-    return install_pending(t, st);
+    const auto c2 = std::chrono::steady_clock::now();
+    rc = install_pending(t, st);
+    if (prof) {
+        const auto c3 = std::chrono::steady_clock::now();
+        auto ms = [](auto a, auto b2) { return std::chrono::duration<double, std::milli>(b2 - a).count(); };
+        fprintf(stderr, "tier phases ms: batch %.3f  d2h+replay %.3f  install %.3f\n", ms(c0, c1), ms(c1, c2), ms(c2, c3));
+    }
+    return rc;
 }
 
 }  // namespace psa
