@@ -293,7 +293,13 @@ constexpr int kTmaBarBytes = 256;  // kScoreWarps x (<= 4 stages) x 8 B mbarrier
 #endif
 
 template <typename KV, int G, int EST>
-__global__ void __launch_bounds__(kScoreWarps * 32, 2) score_kernel_tma(PoolView p, BatchView b) {
+#ifndef PSA_SCORE_MINB
+#define PSA_SCORE_MINB 2
+#endif
+#ifndef PSA_SCORE_SB
+#define PSA_SCORE_SB 12288  // bytes of TMA stages per warp (3 x 4 KB records groups)
+#endif
+__global__ void __launch_bounds__(kScoreWarps * 32, PSA_SCORE_MINB) score_kernel_tma(PoolView p, BatchView b) {
     constexpr int DPL = 4, D = 128;
     constexpr int kRecs = RecsPer<G, DPL>::v;
     constexpr int N = G * kRecs;
@@ -301,7 +307,7 @@ __global__ void __launch_bounds__(kScoreWarps * 32, 2) score_kernel_tma(PoolView
     constexpr int MB = D * 4 + 2 * D * (int)sizeof(KV);  // metadata record bytes (meta_bytes)
     constexpr int STAGE = kRecs * MB;
     constexpr bool kReuse = (N == 16 && STAGE >= 4096);  // reduction scratch lives in the consumed stage
-    constexpr int SB = kReuse ? 12288 : 8192;
+    constexpr int SB = kReuse ? PSA_SCORE_SB : 8192;
     constexpr int S = (SB / STAGE) < 2 ? 2 : ((SB / STAGE) > 4 ? 4 : (SB / STAGE));  // 2 CTAs/SM
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
@@ -532,7 +538,7 @@ static size_t tma_smem_bytes() {
     constexpr int STAGE = kRecs * (128 * 4 + 2 * 128 * (int)sizeof(KV));
     constexpr int N = G * kRecs;
     constexpr bool kReuse = (N == 16 && STAGE >= 4096);
-    constexpr int SB = kReuse ? 12288 : 8192;
+    constexpr int SB = kReuse ? PSA_SCORE_SB : 8192;
     constexpr int S = (SB / STAGE) < 2 ? 2 : ((SB / STAGE) > 4 ? 4 : (SB / STAGE));
     return kTmaBarBytes + (size_t)kScoreWarps * S * STAGE + (kReuse ? 0 : (size_t)kScoreWarps * 32 * (N + 1) * 8);
 }

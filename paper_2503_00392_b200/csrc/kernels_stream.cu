@@ -96,7 +96,14 @@ constexpr int kLook = PSA_STREAM_LOOK;
 #ifndef PSA_STREAM_SPL
 #define PSA_STREAM_SPL 1
 #endif
-constexpr int kSPL = PSA_STREAM_SPL;  // rank slots per lane in a round: a round is 32*kSPL/G ranks per head
+constexpr int kSPL = PSA_STREAM_SPL;
+#ifndef PSA_STREAM_SLEEP
+#define PSA_STREAM_SLEEP 64  // producer back-off (ns) when nothing can be issued
+#endif
+#ifndef PSA_STREAM_PAIR
+#define PSA_STREAM_PAIR 1
+#endif
+constexpr int kPair = PSA_STREAM_PAIR;  // entries a scorer warp handles together (1 or 2)  // rank slots per lane in a round: a round is 32*kSPL/G ranks per head
 static_assert(kSPL == 1 || kSPL == 2, "1 or 2 rank slots per lane");
 // V reference R of a head: its top criticality score + kVRef. Kept while the rank-0 block's max is
 // at least R - kVLow and no scored block's max exceeds R + kVHigh; otherwise the unit is redone densely.
@@ -412,9 +419,9 @@ __global__ void __launch_bounds__(kThreads, PSA_STREAM_MINB) psa_stream_kernel(c
                                                                                    ((decided + 1) / kLR) & 1, PSA_STREAM_PARK)
                                                           : 0, 0);
                 else
-                    __nanosleep(64);
+                    __nanosleep(PSA_STREAM_SLEEP);
 #else
-                __nanosleep(64);
+                __nanosleep(PSA_STREAM_SLEEP);
 #endif
 #ifdef PSA_STREAM_DEBUG
                 if (++idle == (1 << 22)) {
@@ -722,16 +729,14 @@ __global__ void __launch_bounds__(kThreads, PSA_STREAM_MINB) psa_stream_kernel(c
             const int cnt = s.r_cnt[rs];
             if (cnt < 0) break;
             const int e0 = s.r_e0[rs];
-            for (int e = e0 + ((sidx - e0 % kNS) + kNS) % kNS; e < e0 + cnt; e += kNS) {
+            // entries of this round owned by this scorer, kPair at a time: the MMA chains and the
+            // epilogues of the pair are independent (latency overlap)
+            auto score_tile = [&](int e, float (&c)[NT][4]) {
                 const int st = e % kRK;
                 SWAIT(&s.kfull[st], (e / kRK) & 1, 4, k, e, e0, cnt, 0, 0, 0, 0);
-#ifdef PSA_STREAM_PROF
-                const long long tq0_ = clock64();
-#endif
                 const uint32_t kb = smem_u32(s.kring[st]);
-                const int nt = s.entok[e];
                 // two accumulator sets (even / odd k-steps): halves the dependent MMA chain
-                float c[NT][4], c2[NT][4];
+                float c2[NT][4];
 #pragma unroll
                 for (int t = 0; t < NT; ++t)
 #pragma unroll
@@ -752,9 +757,9 @@ __global__ void __launch_bounds__(kThreads, PSA_STREAM_MINB) psa_stream_kernel(c
                     for (int r = 0; r < 4; ++r) c[t][r] += c2[t][r];
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&s.kempty[st]);  // the tile is in registers: release it
-#ifdef PSA_STREAM_PROF
-                pw[6] += clock64() - tq0_;
-#endif
+            };
+            auto epilogue = [&](int e, float (&c)[NT][4]) {
+                const int nt = s.entok[e];
                 float* we = wg + (size_t)e * kStreamWRow;
 #pragma unroll
                 for (int t = 0; t < NT; ++t) {
@@ -796,6 +801,22 @@ __global__ void __launch_bounds__(kThreads, PSA_STREAM_MINB) psa_stream_kernel(c
                         }
                     }
                 }
+            };
+            for (int e = e0 + ((sidx - e0 % kNS) + kNS) % kNS; e < e0 + cnt; e += kNS * kPair) {
+#ifdef PSA_STREAM_PROF
+                const long long tq0_ = clock64();
+#endif
+                float c[kPair][NT][4];
+                const bool two = kPair == 2 && e + kNS < e0 + cnt;
+                score_tile(e, c[0]);
+                if constexpr (kPair == 2)
+                    if (two) score_tile(e + kNS, c[kPair - 1]);
+#ifdef PSA_STREAM_PROF
+                pw[6] += clock64() - tq0_;
+#endif
+                epilogue(e, c[0]);
+                if constexpr (kPair == 2)
+                    if (two) epilogue(e + kNS, c[kPair - 1]);
             }
             // the weights are read back by the async proxy (bulk copy beside the V tile)
 #ifdef PSA_STREAM_PROF
