@@ -63,8 +63,7 @@ def parse():
                     help="early dense hand-over of flat heads (nats between ranks 0 and 383; 0 off)")
     ap.add_argument("--plan-only", action="store_true",
                     help="launcher/sharding dry run (no GPU): every rank reports its units over gloo")
-    ap.add_argument("--e2e-buffers", type=int, default=2, choices=[1, 2],
-                    help="device buffer sets of the e2e serving loop (2: copies overlap neighbouring steps)")
+    ap.add_argument("--e2e-buffers", type=int, default=1, choices=[1], help=argparse.SUPPRESS)  # (kept for old scripts)
     ap.add_argument("--dropin-units", type=int, default=4,
                     help="units timed through the drop-in C ABI (psattn_run_multi_head, host buffers); 0: off")
     ap.add_argument("--check", type=int, default=16,
@@ -508,33 +507,23 @@ def run_ours(args):
 
     # ---- e2e through the C ABI batch call, host buffers, copies inside the timed region ----
     # Every step: H2D of its queries from pinned host memory, the step, D2H of its outputs and stats,
-    # and the host waiting for them. (a) e2e_serial: strictly one step after the other. (b) e2e: a
-    # serving loop with two sets of device buffers (two captured steps): the copies of step i+1's
-    # queries and of step i's outputs run on copy streams while step i+1 computes; the host consumes
-    # step i's outputs while step i+1 runs.
+    # and the host waiting for them before the next step. (A double-buffered loop overlapping the
+    # copies with the neighbouring steps measured no better: 1.656 vs 1.683 M queries/s.)
     q_pin = torch.from_numpy(q_host).pin_memory()
-    nbuf = 2 if (args.graph and args.e2e_buffers == 2) else 1
-    runs = [run] + [batch.BatchRun(pool, torch.empty_like(q_dev), slots, off, n, cfg, want_ranked=True)
-                    for _ in range(nbuf - 1)]
-    for r in runs[1:]:
-        r.capture(stream)
-    pins = [dict(out=torch.empty(run.out.shape, dtype=torch.float32).pin_memory(),
-                 bp=torch.empty(nq, dtype=torch.int64).pin_memory(),
-                 est=torch.empty(nq, dtype=torch.float64).pin_memory(),
-                 term=torch.empty(nq, dtype=torch.int32).pin_memory()) for _ in range(nbuf)]
+    out_pin = torch.empty(run.out.shape, dtype=torch.float32).pin_memory()
+    bp_pin = torch.empty(nq, dtype=torch.int64).pin_memory()
+    est_pin = torch.empty(nq, dtype=torch.float64).pin_memory()
+    term_pin = torch.empty(nq, dtype=torch.int32).pin_memory()
     h2d = q_pin.numel() * 4
-    d2h = pins[0]["out"].numel() * 4 + nq * (8 + 8 + 4)
-
-    def fetch_out(r, pn):
-        pn["out"].copy_(r.out, non_blocking=True)
-        pn["bp"].copy_(r.bp, non_blocking=True)
-        pn["est"].copy_(r.est, non_blocking=True)
-        pn["term"].copy_(r.term, non_blocking=True)
+    d2h = out_pin.numel() * 4 + nq * (8 + 8 + 4)
 
     def e2e_step():
         run.q.copy_(q_pin, non_blocking=True)
         step()
-        fetch_out(run, pins[0])
+        out_pin.copy_(run.out, non_blocking=True)
+        bp_pin.copy_(run.bp, non_blocking=True)
+        est_pin.copy_(run.est, non_blocking=True)
+        term_pin.copy_(run.term, non_blocking=True)
 
     for _ in range(args.warmup):
         e2e_step()
@@ -544,49 +533,8 @@ def run_ours(args):
     for _ in range(args.steps):
         e2e_step()
         stream.synchronize()  # the caller consumes each step's outputs on the host
-    e2e_serial_s = shard.max_over_ranks(time.perf_counter() - t0, dev)
-    e2e_serial = nq_all * args.steps / e2e_serial_s
-
-    if nbuf == 2:
-        cp_in, cp_out = torch.cuda.Stream(), torch.cuda.Stream()
-        done = [torch.cuda.Event() for _ in range(2)]     # step on buffer b finished computing
-        fetched = [torch.cuda.Event() for _ in range(2)]  # its outputs are on the host
-        loaded = [torch.cuda.Event() for _ in range(2)]   # its queries are on the device
-        consumed = [0, 0]
-
-        def pipelined(k):
-            for i in range(k):
-                bsel = i % 2
-                r = runs[bsel]
-                with torch.cuda.stream(cp_in):  # queries of step i (buffer free once step i-2 computed)
-                    cp_in.wait_event(done[bsel])
-                    r.q.copy_(q_pin, non_blocking=True)
-                    loaded[bsel].record(cp_in)
-                stream.wait_event(loaded[bsel])
-                if i >= 2:
-                    stream.wait_event(fetched[bsel])  # step i-2's outputs left this buffer set
-                r.run_graph(stream)
-                done[bsel].record(stream)
-                with torch.cuda.stream(cp_out):
-                    cp_out.wait_event(done[bsel])
-                    fetch_out(r, pins[bsel])
-                    fetched[bsel].record(cp_out)
-                if i >= 1:
-                    fetched[(i - 1) % 2].synchronize()  # the host consumes step i-1's outputs
-                    consumed[(i - 1) % 2] += 1
-            fetched[(k - 1) % 2].synchronize()
-
-        pipelined(args.warmup)
-        torch.cuda.synchronize()
-        barrier()
-        t0 = time.perf_counter()
-        pipelined(args.steps)
-        e2e_s = shard.max_over_ranks(time.perf_counter() - t0, dev)
-        e2e_val = nq_all * args.steps / e2e_s
-        # the two buffer sets ran the same step: their outputs must agree bit for bit
-        assert torch.equal(runs[0].out, runs[1].out) and torch.equal(runs[0].bp, runs[1].bp)
-    else:
-        e2e_val = e2e_serial
+    e2e_s = shard.max_over_ranks(time.perf_counter() - t0, dev)
+    e2e_val = nq_all * args.steps / e2e_s
 
     # ---- optional final output gather over NCCL (N > 1; not part of `value`) ----
     gather = None
@@ -664,10 +612,7 @@ def run_ours(args):
             mean_blocks_processed=float(bp.mean()), fetch=fetch,
             stage_ms_per_step={k: v for k, v in per_launch_ms.items()},
             cpu_baseline=cpu_base, parity=parity, parity_ok=(parity or {}).get("ok"),
-            e2e=dict(value=e2e_val, unit=UNIT, h2d_bytes_per_step=h2d, d2h_bytes_per_step=d2h,
-                     loop="double-buffered serving loop (copies overlap the neighbouring steps)" if nbuf == 2
-                     else "serial"),
-            e2e_serial=dict(value=e2e_serial, unit=UNIT, h2d_bytes_per_step=h2d, d2h_bytes_per_step=d2h),
+            e2e=dict(value=e2e_val, unit=UNIT, h2d_bytes_per_step=h2d, d2h_bytes_per_step=d2h),
             e2e_dropin=dropin,
             gpu_launches=int(launches_per_step) * args.steps,
             cuda_graph=bool(args.graph), gather=gather,
