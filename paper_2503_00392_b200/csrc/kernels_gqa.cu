@@ -657,7 +657,7 @@ __global__ void __launch_bounds__(kPsaThreads) first_tranche_kernel(PoolView p, 
     const uint64_t pmask = (b.pos_bits >= 64) ? ~0ull : ((1ull << b.pos_bits) - 1ull);
     const Team tm = cta_team();
     const int tc = select_tranche(sel, tb, kGTCap, hist, kGBins, b.keys + hb, n, 0, true, kGTCap, tm,
-                                  b.kminmax ? b.kminmax + qi : nullptr, b.kmm_stride, pmask);
+                                  b.kminmax ? b.kminmax + qi : nullptr, b.kmm_stride);
     fill_tranche(tb, tc, pmask, b.rpos + hb, b.slots + off, p.ntok, b.ft_slot + (size_t)qi * kGTCap,
                  b.ft_ntok + (size_t)qi * kGTCap, tm);
     for (int i = threadIdx.x; i < tc; i += blockDim.x) b.ft_keys[(size_t)qi * kGTCap + i] = tb[i];

@@ -189,97 +189,7 @@ __device__ __forceinline__ void scan_keys(const uint64_t* __restrict__ keys, int
 static __device__ __noinline__ int select_tranche(SelScratch& s, uint64_t* tb, int cap, uint32_t* hist, int nbins,
                                           const uint64_t* __restrict__ keys, int64_t n, uint64_t last, bool first,
                                           unsigned target, Team tm, const unsigned long long* bounds = nullptr,
-                                          int64_t bstride = 0, uint64_t score_pmask = 0);
-#ifndef PSA_SCORE_BINS
-#define PSA_SCORE_BINS 1
-#endif
-// First tranche when the key range is known (score kernel bounds): ONE histogram pass with bins
-// linear in the decoded score (monotone in the key, so bins are ordered; the key-space bins of
-// the general path crowd where the fp64 exponent changes and need refinement passes), then one
-// gather of the keys in the chosen bins. Returns -1 (nothing written) when the top bins are too
-// crowded to cut a tranche of >= 32 and <= cap keys; the caller then runs the general path.
-static __device__ __noinline__ int select_first_by_score(SelScratch& s, uint64_t* tb, int cap, uint32_t* hist,
-                                                         int nbins, const uint64_t* __restrict__ keys, int64_t n,
-                                                         unsigned target, Team tm, uint64_t kmin, uint64_t kmax,
-                                                         uint64_t pmask) {
-    const int tid = tm.tid, lane = threadIdx.x & 31;
-    const double smax = key_score(kmin, pmask), smin = key_score(kmax, pmask);
-    if (!(smax > smin) || !isfinite(smax - smin)) return -1;
-    const double inv = (double)nbins / (smax - smin) * (1.0 - 1e-9);
-    auto bin_of = [&](uint64_t k) {
-        const double v = (smax - key_score(k, pmask)) * inv;
-        const int b = v > 0.0 ? (int)v : 0;
-        return b < nbins ? b : nbins - 1;
-    };
-    for (int i = tid; i < nbins; i += tm.size) hist[i] = 0;
-    if (tid == 0) s.gcount = 0;
-    team_sync(tm);
-    scan_keys(keys, n, tm, [&](uint64_t k) { atomicAdd(&hist[bin_of(k)], 1u); });
-    team_sync(tm);
-    // first bin bs with cum(bs) >= target (each thread owns nbins / size consecutive bins)
-    const int per = nbins / tm.size;
-    unsigned loc = 0;
-    for (int j = 0; j < per; ++j) loc += hist[tid * per + j];
-    unsigned inc = loc;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const unsigned y = __shfl_up_sync(PSA_FULL, inc, o);
-        if (lane >= o) inc += y;
-    }
-    if (lane == 31) s.wsum[tid >> 5] = inc;
-    if (tid == 0) s.bstar = -1;
-    team_sync(tm);
-    unsigned wbase = 0;
-    for (int w = 0; w < (tid >> 5); ++w) wbase += s.wsum[w];
-    unsigned cum = wbase + inc - loc;
-    if (cum < target && target <= cum + loc) {
-#pragma unroll 1
-        for (int j = 0; j < per; ++j) {
-            const unsigned c = hist[tid * per + j];
-            if (target <= cum + c) {
-                s.bstar = tid * per + j;
-                s.excl = cum;
-                break;
-            }
-            cum += c;
-        }
-    }
-    team_sync(tm);
-    int bs = s.bstar;
-    if (bs < 0) return -1;  // (fewer than target keys: the general path handles it)
-    const unsigned ex = s.excl, incl = ex + hist[bs];
-    int take;
-    if (incl <= (unsigned)cap) take = bs;
-    else if (ex >= 32) take = bs - 1;
-    else return -1;
-    scan_keys(keys, n, tm, [&](uint64_t k) {
-        const bool t = bin_of(k) <= take;
-        const unsigned m = __ballot_sync(__activemask(), t);
-        if (t) {
-            const int leader = __ffs(m) - 1;
-            unsigned basei = 0;
-            if (lane == leader) basei = atomicAdd(&s.gcount, (unsigned)__popc(m));
-            basei = __shfl_sync(m, basei, leader);
-            const unsigned idx = basei + __popc(m & ((1u << lane) - 1u));
-            if (idx < (unsigned)cap) tb[idx] = k;
-        }
-    });
-    team_sync(tm);
-    const int C = (int)min(s.gcount, (unsigned)cap);
-    bitonic_smem(tb, C, tm);
-    return C;
-}
-
-static __device__ __noinline__ int select_tranche(SelScratch& s, uint64_t* tb, int cap, uint32_t* hist, int nbins,
-                                          const uint64_t* __restrict__ keys, int64_t n, uint64_t last, bool first,
-                                          unsigned target, Team tm, const unsigned long long* bounds,
-                                          int64_t bstride, uint64_t score_pmask) {
-    if (PSA_SCORE_BINS && first && bounds && score_pmask && n > (int64_t)cap) {
-        const int c = select_first_by_score(s, tb, cap, hist, nbins, keys, n, target, tm, bounds[0], bounds[bstride],
-                                            score_pmask);
-        if (c >= 0) return c;
-        team_sync(tm);
-    }
+                                          int64_t bstride = 0) {
     const int tid = tm.tid, lane = threadIdx.x & 31;
     unsigned long long lmin = ~0ull, lmax = 0;
     unsigned lcnt = 0;
