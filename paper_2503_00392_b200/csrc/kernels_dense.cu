@@ -406,24 +406,38 @@ __device__ __forceinline__ void dense_decide_head(const BatchView& b, int u, int
     tmn[tid] = pmn;
     __syncthreads();
     __shared__ float Mfin, mnfin;
-    if (tid == 0) {
+    __shared__ double S64s;
+    if (tid < 32) {  // warp 0 reduces the per-thread max / min
         float a = -INFINITY, c = INFINITY;
-        for (int t = 0; t < kDecideThreads; ++t) {
+        for (int t = tid; t < kDecideThreads; t += 32) {
             a = fmaxf(a, tM[t]);
             c = fminf(c, tmn[t]);
         }
-        Mfin = a;
-        mnfin = c;
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) {
+            a = fmaxf(a, __shfl_xor_sync(PSA_FULL, a, o));
+            c = fminf(c, __shfl_xor_sync(PSA_FULL, c, o));
+        }
+        if (tid == 0) {
+            Mfin = a;
+            mnfin = c;
+        }
     }
     __syncthreads();
     double ps = 0.0;
     for (int64_t r = r0; r < q1; ++r) ps += exp((double)xs[r] - (double)Mfin);
     tS[tid] = ps;
     __syncthreads();
+    if (tid < 32) {
+        double a = 0.0;
+        for (int t = tid; t < kDecideThreads; t += 32) a += tS[t];
+        a = warp_sum_d(a);
+        if (tid == 0) S64s = a;
+    }
+    __syncthreads();
     if (stop_r >= 0 && (unsigned long long)stop_r == first_stop) {
         const int64_t cb = stop_r + 1;
-        double S64 = 0.0;
-        for (int t = 0; t < kDecideThreads; ++t) S64 += tS[t];
+        const double S64 = S64s;
         const int64_t nl = n - cb;
         b.bp[qi] = cb;
         b.est[qi] = nl == 0 ? 1.0 : S64 / fma((double)nl, exp((double)mnfin - (double)Mfin), S64);
