@@ -101,7 +101,7 @@ class ReferenceCPU:
         drv = RefDriver()
         p = synth_params(args)
         self.g = args.hq // args.hkv
-        self.n = args.ctx // args.block
+        self.n = -(-args.ctx // args.block)
         self.threads = max(1, min(os.cpu_count() or 1, 64))
         self.stores, self.qs = [None] * self.threads, [None] * self.threads
         self.cfg = make_config(epsilon=args.eps, microbatch_size=args.microbatch)
@@ -112,7 +112,9 @@ class ReferenceCPU:
             uid = 10_000_000 + rank_offset + t
             k, v = synth.unit_host(p, uid, args.ctx)
             st = drv.store(capacity=0)
-            st.put_many(0, k, v)
+            r = args.ctx - (self.n - 1) * args.block  # tokens of the (possibly ragged) last block
+            st.put_many(0, k[:-1], v[:-1])
+            st.put(self.n - 1, k[-1, :r], v[-1, :r])
             self.stores[t] = st
             self.qs[t] = np.array([synth.query(p, uid, h) for h in range(self.g)], np.float32)
             st.multi_head(self.qs[t], self.ids, self.cfg, want_ids=False)  # warm
@@ -156,7 +158,7 @@ class PortCPU(ReferenceCPU):
         self.orc = COracle()
         p = synth_params(args)
         self.g = args.hq // args.hkv
-        self.n = args.ctx // args.block
+        self.n = -(-args.ctx // args.block)
         self.threads = max(1, min(os.cpu_count() or 1, 64))
         self.cfg = make_config(epsilon=args.eps, microbatch_size=args.microbatch)
         self.args = args
@@ -165,7 +167,8 @@ class PortCPU(ReferenceCPU):
         def setup(t):
             uid = 10_000_000 + rank_offset + t
             k, v = synth.unit_host(p, uid, args.ctx)
-            self.units[t] = BlockSet(list(k), list(v))
+            r = args.ctx - (self.n - 1) * args.block
+            self.units[t] = BlockSet(list(k[:-1]) + [k[-1, :r]], list(v[:-1]) + [v[-1, :r]])
             self.qs[t] = np.array([synth.query(p, uid, h) for h in range(self.g)], np.float32)
 
         ths = [threading.Thread(target=setup, args=(t,)) for t in range(self.threads)]
@@ -329,7 +332,9 @@ def dropin_e2e(args, p, units, n, g, seconds=2.0):
     lists, qs = [], []
     for i, uid in enumerate(units):
         k, v = synth.unit_host(p, uid, args.ctx)
-        st.put_many(i * n, k, v)
+        r = args.ctx - (n - 1) * args.block  # ragged last block keeps its own token count
+        st.put_many(i * n, k[:-1], v[:-1])
+        capi.check(st.put(i * n + n - 1, k[-1, :r], v[-1, :r]))
         lists.append(np.arange(i * n, (i + 1) * n, dtype=np.int64))
         qs.append(np.stack([synth.query(p, uid, h) for h in range(g)]).astype(np.float32))
     cfg = capi.config_default(epsilon=args.eps, microbatch_size=args.microbatch)
@@ -369,15 +374,18 @@ def run_ours(args):
     from workload import synth
     p = synth_params(args)
     g = args.hq // args.hkv
-    n = args.ctx // args.block
+    n = -(-args.ctx // args.block)
     # ---- units of this rank: weak scaling (requests per GPU fixed) or a fixed total (strong) ----
     strong = args.total_requests > 0
     total_req = args.total_requests if strong else args.requests * ws
     unit_ids = shard.plan_units(total_req, args.layers, args.hkv, ws, rank)
     layers_resident = args.layers
-    if strong:
-        slot_b = 2 * args.block * args.dim * 2
-        meta_b1 = args.dim * (4 + 2 * 2)
+    slot_b = 2 * args.block * args.dim * 2
+    meta_b1 = args.dim * (4 + 2 * 2)
+    overflow = unit_ids.size * n * (slot_b + meta_b1) > torch.cuda.mem_get_info(dev)[0] - (10 << 30)
+    if overflow and not strong:  # the weak-scaling shape does not fit one GPU: the resident layers (in config)
+        print(f"bench: {unit_ids.size} units x {n} blocks exceed HBM; running the resident layers", file=sys.stderr)
+    if strong or overflow:
         budget = torch.cuda.mem_get_info(dev)[0] - (10 << 30)
         reqs_here = max(1, len(np.unique(unit_ids // (args.layers * args.hkv))))
         layers_resident = shard.resident_layers(reqs_here, args.layers, args.hkv, n, slot_b + meta_b1, budget)
