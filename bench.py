@@ -599,7 +599,7 @@ def run_ours(args):
             wl = (f"config5: {total_req} concurrent 128K-context decodes (Llama-3.1-8B shape) over {ws} GPU(s), "
                   f"{layers_resident} of {args.layers} layers resident per step, eps {args.eps}")
         else:
-            wl = "config2: Llama-3.1-8B shape, 32 layers, batch 8 decode, 128K ctx, eps 0.95"
+            wl = f"config2: Llama-3.1-8B shape, {args.layers} layers, batch {args.requests} decode, ctx {args.ctx}, eps {args.eps}"
         line = dict(
             metric=METRIC, value=value, unit=UNIT, n_gpus=ws, steps=args.steps, warmup=args.warmup,
             ms_per_step=ms_per_step, higher_is_better=True, scaling="strong" if strong else "weak",

@@ -180,6 +180,12 @@ __global__ void __launch_bounds__(kDecideThreads) dense_decide_kernel(BatchView 
 #ifndef PSA_DECIDE_BUCKET
 #define PSA_DECIDE_BUCKET 1
 #endif
+#ifndef PSA_DECIDE_BINS
+#define PSA_DECIDE_BINS 2048
+#endif
+#ifndef PSA_DECIDE_SCAN
+#define PSA_DECIDE_SCAN 1
+#endif
 constexpr int kBucketPerThread = 32;
 constexpr unsigned kBucketMax = 64;
 __device__ bool bucket_sort_smem(uint64_t* ks, int n, uint64_t pmask, uint32_t* hist, int nbins) {
@@ -299,7 +305,7 @@ __device__ __forceinline__ void dense_decide_head(const BatchView& b, int u, int
     __syncthreads();
     {
         // bins: the rank-order mass array's space (n2 floats) before it is filled
-        const int nbins = n2 < 2048 ? n2 : 2048;
+        const int nbins = n2 < PSA_DECIDE_BINS ? n2 : PSA_DECIDE_BINS;
         if (!(PSA_DECIDE_BUCKET && n <= (int64_t)kBucketPerThread * blockDim.x &&
               bucket_sort_smem(ks, (int)n, pmask, reinterpret_cast<uint32_t*>(ks + n2), nbins)))
             bitonic_smem(ks, (int)n, cta_team());
@@ -360,15 +366,55 @@ __device__ __forceinline__ void dense_decide_head(const BatchView& b, int u, int
     float M = -INFINITY, mn = INFINITY;
     double S = 0.0;
     for (int64_t r = r0; r < r1; ++r) absorb(xs[r], M, S, mn);
+    float PM = -INFINITY, Pmn = INFINITY;
+    double PS = 0.0;
+#if PSA_DECIDE_SCAN
+    // exclusive prefix of this thread (the triples of threads 0 .. tid-1): a shuffle scan inside
+    // the warp, the totals of the earlier warps folded in order
+    const int lane = tid & 31, wid = tid >> 5;
+    {
+        float wM = M, wmn = mn;
+        double wS = S;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const float Mo = __shfl_up_sync(PSA_FULL, wM, o), mno = __shfl_up_sync(PSA_FULL, wmn, o);
+            const double So = __shfl_up_sync(PSA_FULL, wS, o);
+            if (lane >= o) combine(Mo, So, mno, wM, wS, wmn);
+        }
+        if (lane == 31) {
+            tM[wid] = wM;
+            tS[wid] = wS;
+            tmn[wid] = wmn;
+        }
+        if (tid == 0) first_stop = ~0ull;
+        float eM = __shfl_up_sync(PSA_FULL, wM, 1), emn = __shfl_up_sync(PSA_FULL, wmn, 1);
+        double eS = __shfl_up_sync(PSA_FULL, wS, 1);
+        if (lane == 0) {
+            eM = -INFINITY;
+            eS = 0.0;
+            emn = INFINITY;
+        }
+        __syncthreads();
+        for (int w = 0; w < wid; ++w) {
+            float m2 = tM[w], n2v = tmn[w];
+            double s2 = tS[w];
+            combine(PM, PS, Pmn, m2, s2, n2v);
+            PM = m2;
+            PS = s2;
+            Pmn = n2v;
+        }
+        combine(PM, PS, Pmn, eM, eS, emn);
+        PM = eM;
+        PS = eS;
+        Pmn = emn;
+    }
+#else
     // exclusive prefix of this thread: the triples of threads 0 .. tid-1, combined in order
     tM[tid] = M;
     tS[tid] = S;
     tmn[tid] = mn;
     if (tid == 0) first_stop = ~0ull;
     __syncthreads();
-
-    float PM = -INFINITY, Pmn = INFINITY;
-    double PS = 0.0;
     for (int t = 0; t < tid; ++t) {
         float m2 = tM[t], n2v = tmn[t];
         double s2 = tS[t];
@@ -377,6 +423,7 @@ __device__ __forceinline__ void dense_decide_head(const BatchView& b, int u, int
         PS = s2;
         Pmn = n2v;
     }
+#endif
     // walk again from the prefix
     int64_t stop_r = -1;
     for (int64_t r = r0; r < r1; ++r) {

@@ -1,7 +1,7 @@
 # robustness sweep of bench configurations (each re-checks sampled units of its own step against the reference)
 run() {
   timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --dropin-units 0 --check 4 "$@" > gpurun_out/sweep.log 2>&1
-  python -c "import json,sys;d=json.loads(open('gpurun_out/sweep.log').read().strip().splitlines()[-1]);print('$*', round(d['value']), round(d['ms_per_step'],3), d['parity_ok'], d['parity']['exact'], d['parity']['tie'], round(d['kv_fraction_read'],4))" || tail -3 gpurun_out/sweep.log
+  python -c "import json,sys;d=json.loads(open('gpurun_out/sweep.log').read().strip().splitlines()[-1]);print('$*', round(d['value']), round(d['ms_per_step'],3), d['parity_ok'], d['parity'].get('exact'), d['parity'].get('tie'), d['parity'].get('error'), round(d['kv_fraction_read'],4))" || tail -3 gpurun_out/sweep.log
 }
 run --total-requests 64
 run --microbatch 4
