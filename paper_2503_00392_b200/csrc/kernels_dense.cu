@@ -39,6 +39,9 @@ constexpr int kDenseWarps = 8;
 #define PSA_DENSE_PF 2
 #endif
 constexpr int kDensePf = PSA_DENSE_PF;  // L2 prefetch distance (warp iterations)
+#ifndef PSA_DENSE_VPF
+#define PSA_DENSE_VPF 1  // V pass: L2 prefetch of the weights / masses with the V block
+#endif
 
 // q fragments of the K pass (see psa_gqa_kernel): columns = (head, split), 4 per head.
 template <int G>
@@ -554,6 +557,19 @@ __device__ __forceinline__ void dense_v_unit(const PoolView& p, const BatchView&
         const int32_t slot = sq[0];
         if (lane == 0 && mq[kD] && kv_resident(p, sq[kD]))  // block e + kD*W, kD iterations ahead
             prefetch_l2_bulk(kv_block<__nv_bfloat16>(p, sq[kD]) + v_off, (uint32_t)(T * 128 * 2));
+#if PSA_DENSE_VPF
+        // ... with the committed heads' token weights (lanes 0..g-1, one 64 B row each) and block
+        // masses (lanes 8..8+g-1): both come from dense_k's write-back in HBM, and loading them
+        // cold would put two DRAM round trips on every block's critical path
+        if (mq[kD]) {
+            const int64_t ef = e + kD * kW;
+            const int hl = lane & 7;
+            if (lane < 16 && hl < g && ((mq[kD] >> hl) & 1u)) {
+                const int64_t row = off * g + (int64_t)hl * n + ef;
+                prefetch_l2_line(lane < 8 ? (const void*)(b.dense_p + row * 16) : (const void*)(b.dense_la + row));
+            }
+        }
+#endif
 #pragma unroll
         for (int i = 0; i < kD; ++i) {
             mq[i] = mq[i + 1];
@@ -562,6 +578,8 @@ __device__ __forceinline__ void dense_v_unit(const PoolView& p, const BatchView&
         mq[kD] = mask_or(e + (kD + 1) * kW);
         sq[kD] = slot_or(e + (kD + 1) * kW);
         if (!mask) continue;
+        const bool mine = tq < g && ((mask >> tq) & 1u);  // this lane's merge head (tq) is committed
+        const float la = mine ? __ldg(b.dense_la + off * g + (int64_t)tq * n + e) : 0.0f;  // exp(la - M) weight
         const __nv_bfloat16* vblk = kv_block<__nv_bfloat16>(p, slot) + v_off;
         uint32_t vw[4][8];
 #pragma unroll
@@ -592,8 +610,7 @@ __device__ __forceinline__ void dense_v_unit(const PoolView& p, const BatchView&
             ob[2 * i] = c0 + c1;
             ob[2 * i + 1] = c2 + c3;
         }
-        if (tq < g && ((mask >> tq) & 1u)) {
-            const float la = b.dense_la[off * g + (int64_t)tq * n + e];  // block weight exp(la - M), sum_t p_t = 1
+        if (mine) {  // block weight exp(la - M), sum_t p_t = 1
             const float mnew = fmaxf(Mreg, la);
             const float a = expf(Mreg - mnew);
             const float cc = expf(la - mnew);
