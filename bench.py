@@ -61,6 +61,8 @@ def parse():
     ap.add_argument("--graph", type=int, default=1, help="1: replay the step as a captured CUDA graph")
     ap.add_argument("--dense-early", type=float, default=2.0,
                     help="early dense hand-over of flat heads (nats between ranks 0 and 383; 0 off)")
+    ap.add_argument("--dense-partial", type=int, default=1024,
+                    help="dense hand-over: ranks of each head's first-round candidate prefix (0: whole lists)")
     ap.add_argument("--plan-only", action="store_true",
                     help="launcher/sharding dry run (no GPU): every rank reports its units over gloo")
     ap.add_argument("--e2e-buffers", type=int, default=1, choices=[1], help=argparse.SUPPRESS)  # (kept for old scripts)
@@ -371,6 +373,7 @@ def run_ours(args):
     capi.check(capi.lib.psattn_set_score_kernel(args.score_kernel))
     capi.check(capi.lib.psattn_set_pipeline(args.pipeline))
     capi.check(capi.lib.psattn_set_dense_early(args.dense_early))
+    capi.check(capi.lib.psattn_set_dense_partial(args.dense_partial))
     from workload import synth
     p = synth_params(args)
     g = args.hq // args.hkv

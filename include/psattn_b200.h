@@ -204,6 +204,12 @@ int psattn_set_dense(int32_t mode);
  * hand-over budget without stopping) goes to the dense kernels after its first round. Default 2.0;
  * 0 = off. Performance only: results are the same either way. */
 int psattn_set_dense_early(float nats);
+/* Partial dense mode: a handed-over unit first computes the block masses of each head's top
+ * ~`ranks` ranks only (a key-space threshold between ranks/2 and 2*ranks keys) and decides on
+ * them; a head that does not stop inside that prefix sends its unit to a second round over the
+ * rest of the list. Default 1024; 0 = off (every handed-over unit reads its whole list). Flat
+ * units (see psattn_set_dense_early) always take the whole list. Results are the same either way. */
+int psattn_set_dense_partial(int32_t ranks);
 /* Score-kernel selection: 0 = auto (TMA-staged for dim 128), 1 = register-staged, 2 = TMA whenever supported. */
 int psattn_set_score_kernel(int32_t mode);
 

@@ -147,6 +147,7 @@ def _load() -> C.CDLL:
     L.psattn_debug_stream_stats.argtypes = [vp]
     L.psattn_debug_stream_prof.argtypes = [vp]
     L.psattn_set_dense_early.argtypes = [C.c_float]
+    L.psattn_set_dense_partial.argtypes = [i32]
     L.psattn_debug_gqa_phases.argtypes = [vp]
     L.psattn_debug_stream_attach.argtypes = []
     L.psattn_debug_stream_attach.restype = C.POINTER(C.c_int)
@@ -192,7 +193,7 @@ EXPORTED = [
     "psattn_pool_append_tokens",
     "psattn_batch_workspace_bytes", "psattn_run_batch", "psattn_batch_union_blocks", "psattn_batch_last_launches",
     "psattn_profile_enable", "psattn_profile_read", "psattn_set_progressive_kernel",
-    "psattn_debug_stream_stats", "psattn_debug_stream_prof", "psattn_set_dense_early", "psattn_debug_gqa_phases", "psattn_debug_stream_attach",
+    "psattn_debug_stream_stats", "psattn_debug_stream_prof", "psattn_set_dense_early", "psattn_set_dense_partial", "psattn_debug_gqa_phases", "psattn_debug_stream_attach",
     "psattn_set_score_kernel", "psattn_set_pipeline", "psattn_set_dense",
     "psattn_graph_create", "psattn_graph_launch", "psattn_graph_destroy",
     "psattn_exact_attention", "psattn_tradeoff", "psattn_rank_batch", "psattn_run_multi_head",

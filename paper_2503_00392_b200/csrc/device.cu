@@ -308,7 +308,7 @@ int read_meta(const psattn_pool* pool, int64_t slot, float* mean, float* lo, flo
 
 // ---- workspace carving ----
 struct WsLayout {
-    size_t keys, rpos, omass, kmm, dflag, dla, dp, dthr, dpart, ft, sw, total;
+    size_t keys, rpos, omass, kmm, dflag, dla, dp, dthr, dpart, dsel, ft, sw, total;
 };
 
 static WsLayout ws_layout(const psattn_batch* b) {
@@ -324,11 +324,13 @@ static WsLayout ws_layout(const psattn_batch* b) {
     l.kmm = o;
     o += align_up((size_t)b->n_units * b->group * 16, 256);
     // dense hand-over scratch (GQA shapes with the estimated ranking: d = 128, group 2..4)
-    l.dflag = l.dla = l.dp = l.dthr = l.dpart = 0;
+    l.dflag = l.dla = l.dp = l.dthr = l.dpart = l.dsel = 0;
     if (b->dim == 128 && b->group >= 2 && b->group <= 4 && b->ranking_mode != PSATTN_RANK_ORACLE &&
         !b->audit_coverage && b->max_blocks <= kDenseMaxBlocks) {
         l.dflag = o;
-        o += 256 + align_up((size_t)b->n_units * 4, 256);  // count | unit list
+        o += 256 + align_up((size_t)b->n_units * 4, 256);  // counts (hand-over [0,32), escalated [32,64)) | unit list
+        l.dsel = o;  // candidate thresholds | escalated list | escalation marks
+        o += align_up((size_t)b->n_units * b->group * 8, 256) + 2 * align_up((size_t)b->n_units * 4, 256);
         l.dla = o;
         o += align_up(hb * 4, 256);
         l.dp = o;
@@ -417,6 +419,11 @@ BatchView make_view(const psattn_pool* pool, const psattn_batch* b, void* worksp
     v.dense_p = l.dflag ? reinterpret_cast<float*>(ws + l.dp) : nullptr;
     v.dense_thr = l.dflag ? reinterpret_cast<unsigned long long*>(ws + l.dthr) : nullptr;
     v.dense_part = l.dflag ? reinterpret_cast<float*>(ws + l.dpart) : nullptr;
+    v.dense_esc_count = l.dflag ? reinterpret_cast<int32_t*>(ws + l.dflag) + 32 : nullptr;
+    v.dense_sel = l.dflag ? reinterpret_cast<unsigned long long*>(ws + l.dsel) : nullptr;
+    v.dense_esc = l.dflag ? reinterpret_cast<int32_t*>(ws + l.dsel + align_up((size_t)b->n_units * b->group * 8, 256))
+                          : nullptr;
+    v.dense_esc_mark = l.dflag ? v.dense_esc + align_up((size_t)b->n_units * 4, 256) / 4 : nullptr;
     v.stream_w = l.sw ? reinterpret_cast<float*>(ws + l.sw) : nullptr;
     if (l.ft) {
         const size_t hq = (size_t)b->n_units * b->group;
@@ -659,6 +666,12 @@ int psattn_set_dense(int32_t mode) {
 int psattn_set_dense_early(float nats) {
     if (!(nats >= 0.0f)) return fail(PSATTN_ERR_INVALID_ARGUMENT, "psattn_set_dense_early: threshold must be >= 0");
     set_dense_early(nats);
+    return PSATTN_OK;
+}
+
+int psattn_set_dense_partial(int32_t ranks) {
+    if (ranks < 0) return fail(PSATTN_ERR_INVALID_ARGUMENT, "psattn_set_dense_partial: ranks must be >= 0");
+    set_dense_partial(ranks);
     return PSATTN_OK;
 }
 

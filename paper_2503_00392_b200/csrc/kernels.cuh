@@ -84,6 +84,15 @@ struct BatchView {
     unsigned long long* dense_thr;  // [n_units*g] rank-threshold key of each head's processed set
     float* dense_part;              // [n_units*g][slices][kDensePart] per-slice V-pass partial states
     int64_t dense_slice;            // list positions per dense work item (set by launch_dense)
+    // partial dense mode: round 0 computes the masses of each head's candidate prefix only (keys <=
+    // dense_sel, about dense_sel_ranks ranks) and decides on it; heads that do not stop inside it send
+    // their unit to round 1 (dense_esc list), which completes the K pass on the rest and decides in full
+    unsigned long long* dense_sel;  // [n_units*g] candidate threshold key per head (~0: every block)
+    int32_t* dense_esc;             // [n_units] escalated units (dense_esc_count entries)
+    int32_t* dense_esc_count;
+    int32_t* dense_esc_mark;        // [n_units] per unit: > 0 once a head escalated it
+    int32_t dense_sel_ranks;        // candidate prefix size (0: partial mode off)
+    int32_t dense_round;            // 0: the hand-over list, 1: the escalated list (set by launch_dense)
     // first tranche of every head, selected up front by first_tranche_kernel (nullptr: the
     // progressive kernel selects it itself): [n_units*g][kFirstCap] sorted keys, slots, ntok, count
     unsigned long long* ft_keys;
@@ -129,6 +138,7 @@ void set_psa_kernel_choice(int choice);
 void set_score_kernel_choice(int choice);
 void set_pipeline_subbatches(int k);
 void set_dense_mode(int mode);  // 0 auto (hand-over enabled), 1 off
+void set_dense_partial(int ranks);  // dense hand-over: candidate prefix of round 0 (0: off)
 void set_dense_early(float nats);  // stream kernel: early hand-over threshold (0 off)
 bool dense_supported(const PoolView& p, const BatchView& b);
 void launch_dense(const PoolView& p, const BatchView& b, cudaStream_t st);

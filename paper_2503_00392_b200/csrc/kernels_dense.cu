@@ -70,6 +70,17 @@ __device__ __forceinline__ void load_qg(const BatchView& b, int u, int lane, uin
 // Work items of the K and V passes: (handed-over unit, slice of kDenseSlice list positions), so a
 // few long units still spread over every SM (the V pass merges the slices' partial states).
 __device__ __forceinline__ int dense_slices(const BatchView& b) { return (int)((b.max_n + b.dense_slice - 1) / b.dense_slice); }
+// The round's unit list: round 0 the hand-over list, round 1 the escalated units.
+__device__ __forceinline__ const int32_t* dense_list(const BatchView& b) {
+    return b.dense_round == 0 ? b.dense_flag : b.dense_esc;
+}
+__device__ __forceinline__ int dense_list_count(const BatchView& b) {
+    return *(b.dense_round == 0 ? b.dense_count : b.dense_esc_count);
+}
+// Round 0 skips, after its decide, the units a head escalated (round 1 redoes them).
+__device__ __forceinline__ bool dense_skip(const BatchView& b, int u) {
+    return b.dense_round == 0 && b.dense_esc_mark[u] > 0;
+}
 
 template <int G>
 __device__ __forceinline__ void dense_k_unit(const PoolView& p, const BatchView& b, int u, int64_t e_begin, int64_t e_end) {
@@ -84,21 +95,27 @@ __device__ __forceinline__ void dense_k_unit(const PoolView& p, const BatchView&
     // the small dependent loads (page-table slot, its ntok, the prefetch target's slot) are
     // issued one iteration ahead so they never sit on the block's critical path
     constexpr int64_t kPfd = (int64_t)kDensePf * kDenseWarps;
-    int64_t e = e_begin + warp;
-    int32_t slot_n = e < e_end ? b.slots[off + e] : 0;
-    int nt_n = e < e_end ? p.ntok[slot_n] : 0;
-    int32_t sf_n = e + kPfd < e_end ? b.slots[off + e + kPfd] : -1;
-    for (; e < e_end; e += kDenseWarps) {
-        const int32_t slot = slot_n, sf = sf_n;
-        const int nt = nt_n;
-        const int64_t en = e + kDenseWarps;
-        if (en < e_end) {
-            slot_n = b.slots[off + en];
-            nt_n = p.ntok[slot_n];
-        }
-        sf_n = en + kPfd < e_end ? b.slots[off + en + kPfd] : -1;
-        if (lane == 0 && sf >= 0 && kv_resident(p, sf))
-            prefetch_l2_bulk(kv_block<__nv_bfloat16>(p, sf), (uint32_t)(T * 128 * 2));
+    // blocks this round computes: round 0 = the heads' candidate prefixes (key <= dense_sel), round 1
+    // = the rest; every block when a head's candidate threshold is ~0 (no key test)
+    uint64_t sel[G];
+    bool all_sel = true;
+#pragma unroll
+    for (int h = 0; h < G; ++h) {
+        sel[h] = h < b.g ? b.dense_sel[(size_t)u * b.g + h] : 0ull;
+        all_sel = all_sel && (h >= b.g || sel[h] == ~0ull);
+    }
+    const bool every = all_sel && b.dense_round == 0;
+    auto wanted = [&](int64_t f) -> bool {
+        if (f >= e_end) return false;
+        if (every) return true;
+        bool cand = false;
+#pragma unroll
+        for (int h = 0; h < G; ++h)
+            if (h < b.g) cand = cand || b.keys[off * b.g + (int64_t)h * n + f] <= sel[h];
+        return b.dense_round == 0 ? cand : !cand;
+    };
+    // one block: K tile -> tensor-core scores of every head -> mass la and token weights p_t
+    auto block = [&](int64_t e, int32_t slot, int nt) {
         const __nv_bfloat16* kblk = kv_block<__nv_bfloat16>(p, slot);
         const int r0 = gq < T ? gq : T - 1, r1 = (gq + 8) < T ? (gq + 8) : T - 1;
         const uint4* p0 = reinterpret_cast<const uint4*>(kblk + (size_t)r0 * 128 + 32 * tq);
@@ -144,14 +161,73 @@ __device__ __forceinline__ void dense_k_unit(const PoolView& p, const BatchView&
                 if (gq == 0) b.dense_la[hb + e] = mbv + logf(lbv);
             }
         }
+    };
+    int64_t e = e_begin + warp;
+    if (every) {  // whole list: the page-table loads one iteration ahead, L2 prefetch kDensePf ahead
+        int32_t slot_n = e < e_end ? b.slots[off + e] : 0;
+        int nt_n = e < e_end ? p.ntok[slot_n] : 0;
+        int32_t sf_n = e + kPfd < e_end ? b.slots[off + e + kPfd] : -1;
+        for (; e < e_end; e += kDenseWarps) {
+            const int32_t slot = slot_n, sf = sf_n;
+            const int nt = nt_n;
+            const int64_t en = e + kDenseWarps;
+            if (en < e_end) {
+                slot_n = b.slots[off + en];
+                nt_n = p.ntok[slot_n];
+            }
+            sf_n = en + kPfd < e_end ? b.slots[off + en + kPfd] : -1;
+            if (lane == 0 && sf >= 0 && kv_resident(p, sf))
+                prefetch_l2_bulk(kv_block<__nv_bfloat16>(p, sf), (uint32_t)(T * 128 * 2));
+            block(e, slot, nt);
+        }
+        return;
+    }
+    // a subset of the list: the warp's positions e + 8j are tested 32 at a time (one lane each: keys,
+    // then slot and token count of the wanted ones), a ballot gives the window's wanted blocks, and
+    // the L2 prefetch runs kDensePf wanted blocks ahead across the window boundary
+    constexpr int64_t kWin = 32 * (int64_t)kDenseWarps;
+    auto window = [&](int64_t wb, uint32_t& m, int32_t& sl, int& ntk) {
+        const int64_t f = wb + (int64_t)kDenseWarps * lane;
+        const bool ok = wanted(f);
+        sl = ok ? b.slots[off + f] : 0;
+        ntk = ok ? p.ntok[sl] : 0;
+        m = __ballot_sync(PSA_FULL, ok);
+    };
+    uint32_t mc, mn;
+    int32_t sc, sn;
+    int tc, tn;
+    window(e, mc, sc, tc);
+    window(e + kWin, mn, sn, tn);
+    for (int64_t wb = e; wb < e_end; wb += kWin) {
+        const uint64_t comb = (uint64_t)mc | ((uint64_t)mn << 32);
+        uint32_t rem = mc;
+        while (rem) {
+            const int i = __ffs(rem) - 1;
+            rem &= rem - 1;
+            uint64_t ahead = comb & ~((2ull << i) - 1ull);  // wanted blocks after i
+#pragma unroll
+            for (int k = 1; k < kDensePf; ++k) ahead &= ahead - 1;
+            if (ahead) {
+                const int j = __ffsll((long long)ahead) - 1;
+                const int32_t sf = __shfl_sync(PSA_FULL, j < 32 ? sc : sn, j & 31);
+                if (lane == 0 && kv_resident(p, sf))
+                    prefetch_l2_bulk(kv_block<__nv_bfloat16>(p, sf), (uint32_t)(T * 128 * 2));
+            }
+            block(wb + (int64_t)kDenseWarps * i, __shfl_sync(PSA_FULL, sc, i), __shfl_sync(PSA_FULL, tc, i));
+        }
+        mc = mn;
+        sc = sn;
+        tc = tn;
+        window(wb + 2 * kWin, mn, sn, tn);
     }
 }
 
 template <int G>
 __global__ void __launch_bounds__(kDenseWarps * 32) dense_k_kernel(PoolView p, BatchView b) {
     const int S = dense_slices(b);
-    for (int item = blockIdx.x; item < *b.dense_count * S; item += gridDim.x) {
-        const int u = b.dense_flag[item / S];
+    const int32_t* list = dense_list(b);
+    for (int item = blockIdx.x; item < dense_list_count(b) * S; item += gridDim.x) {
+        const int u = list[item / S];
         const int64_t n = b.list_off[u + 1] - b.list_off[u];
         const int64_t e0 = (int64_t)(item % S) * b.dense_slice, e1 = e0 + b.dense_slice < n ? e0 + b.dense_slice : n;
         if (e0 < n) dense_k_unit<G>(p, b, u, e0, e1);
@@ -169,8 +245,9 @@ constexpr int kDecideThreads = PSA_DECIDE_THREADS;
 __global__ void __launch_bounds__(kDecideThreads) dense_decide_kernel(BatchView b) {
     extern __shared__ __align__(16) unsigned char dsm[];
     uint64_t* ks = reinterpret_cast<uint64_t*>(dsm);
-    for (int item = blockIdx.x; item < *b.dense_count * b.g; item += gridDim.x) {
-        dense_decide_head(b, b.dense_flag[item / b.g], item % b.g, ks);
+    const int32_t* list = dense_list(b);
+    for (int item = blockIdx.x; item < dense_list_count(b) * b.g; item += gridDim.x) {
+        dense_decide_head(b, list[item / b.g], item % b.g, ks);
         __syncthreads();
     }
 }
@@ -289,7 +366,12 @@ __device__ __forceinline__ void dense_decide_head(const BatchView& b, int u, int
     const double eps = b.topk > 0 ? 1.0 : b.eps;
     int n2 = 1;
     while (n2 < n) n2 <<= 1;
-    {  // 8 loads in flight per thread (the loop is latency-bound otherwise)
+    // round 0 decides on the head's candidate prefix (keys <= sel: the top ranks, whatever their
+    // order) and escalates the unit when the head does not stop inside it
+    const uint64_t sel = b.dense_round == 0 ? b.dense_sel[qi] : ~0ull;
+    __shared__ int s_nsel;
+    int64_t ns = n;  // keys sorted and walked
+    if (sel == ~0ull) {  // 8 loads in flight per thread (the loop is latency-bound otherwise)
         constexpr int U = 8;
         for (int64_t i0 = threadIdx.x; i0 < n2; i0 += (int64_t)U * blockDim.x) {
             uint64_t v[U];
@@ -304,31 +386,56 @@ __device__ __forceinline__ void dense_decide_head(const BatchView& b, int u, int
                 if (i < n2) ks[i] = v[k];
             }
         }
+    } else {  // compaction of the candidates (any order: they are sorted next)
+        if (threadIdx.x == 0) s_nsel = 0;
+        __syncthreads();
+        const int lane = threadIdx.x & 31;
+        constexpr int U = 8;
+        for (int64_t i0 = threadIdx.x; i0 < n; i0 += (int64_t)U * blockDim.x) {
+            uint64_t v[U];
+#pragma unroll
+            for (int k = 0; k < U; ++k) {
+                const int64_t i = i0 + (int64_t)k * blockDim.x;
+                v[k] = i < n ? __ldg(reinterpret_cast<const unsigned long long*>(b.keys) + hb + i) : ~0ull;
+            }
+#pragma unroll
+            for (int k = 0; k < U; ++k) {
+                const bool take = v[k] <= sel;  // (~0 padding never passes: sel < ~0)
+                const unsigned m = __ballot_sync(PSA_FULL, take);
+                int base = 0;
+                if (lane == 0 && m) base = atomicAdd(&s_nsel, __popc(m));
+                base = __shfl_sync(PSA_FULL, base, 0);
+                if (take) ks[base + __popc(m & ((1u << lane) - 1u))] = v[k];
+            }
+        }
+        __syncthreads();
+        ns = s_nsel;
     }
     __syncthreads();
     {
         // bins: the rank-order mass array's space (n2 floats) before it is filled
         const int nbins = n2 < PSA_DECIDE_BINS ? n2 : PSA_DECIDE_BINS;
-        if (!(PSA_DECIDE_BUCKET && n <= (int64_t)kBucketPerThread * blockDim.x &&
-              bucket_sort_smem(ks, (int)n, pmask, reinterpret_cast<uint32_t*>(ks + n2), nbins)))
-            bitonic_smem(ks, (int)n, cta_team());
+        if (!(PSA_DECIDE_BUCKET && ns <= (int64_t)kBucketPerThread * blockDim.x &&
+              bucket_sort_smem(ks, (int)ns, pmask, reinterpret_cast<uint32_t*>(ks + n2), nbins)))
+            bitonic_smem(ks, (int)ns, cta_team());
     }
+    const int64_t wl = limit < ns ? limit : ns;  // ranks walked: the budget, or the candidate prefix
     // every rank's list position (ranked_pos output) and mass, gathered by the whole CTA so the
     // sequential walk below reads shared memory only
     float* xs = reinterpret_cast<float*>(ks + n2);
     {
         constexpr int U = 8;
-        for (int64_t r0 = threadIdx.x; r0 < limit; r0 += (int64_t)U * blockDim.x) {
+        for (int64_t r0 = threadIdx.x; r0 < wl; r0 += (int64_t)U * blockDim.x) {
             float v[U];
 #pragma unroll
             for (int k = 0; k < U; ++k) {
                 const int64_t r = r0 + (int64_t)k * blockDim.x;
-                v[k] = r < limit ? __ldg(b.dense_la + hb + (int64_t)(ks[r] & pmask)) : 0.0f;
+                v[k] = r < wl ? __ldg(b.dense_la + hb + (int64_t)(ks[r] & pmask)) : 0.0f;
             }
 #pragma unroll
             for (int k = 0; k < U; ++k) {
                 const int64_t r = r0 + (int64_t)k * blockDim.x;
-                if (r < limit) {
+                if (r < wl) {
                     b.rpos[hb + r] = (int32_t)(ks[r] & pmask);
                     xs[r] = v[k];
                 }
@@ -346,8 +453,8 @@ __device__ __forceinline__ void dense_decide_head(const BatchView& b, int u, int
     __shared__ double tS[kDecideThreads];
     __shared__ unsigned long long first_stop;
     const int tid = threadIdx.x;
-    const int64_t seg = (limit + kDecideThreads - 1) / kDecideThreads;
-    const int64_t r0 = (int64_t)tid * seg, r1 = r0 + seg < limit ? r0 + seg : limit;
+    const int64_t seg = (wl + kDecideThreads - 1) / kDecideThreads;
+    const int64_t r0 = (int64_t)tid * seg, r1 = r0 + seg < wl ? r0 + seg : wl;
     // (the walk uses fp32 exponentials; the reported estimate is recomputed in fp64 below)
     auto absorb = [](float x, float& M, double& S, float& mn) {
         if (x > M) {
@@ -443,6 +550,10 @@ __device__ __forceinline__ void dense_decide_head(const BatchView& b, int u, int
     }
     if (stop_r >= 0) atomicMin(&first_stop, (unsigned long long)stop_r);
     __syncthreads();
+    if (first_stop == ~0ull) {  // no stop inside the candidate prefix (wl < limit): round 1 redoes the unit
+        if (tid == 0 && atomicAdd(&b.dense_esc_mark[u], 1) == 0) b.dense_esc[atomicAdd(b.dense_esc_count, 1)] = u;
+        return;
+    }
     // The reported estimate at the stop rank, recomputed in fp64 over the processed ranks (the
     // reference's CoverageEstimator precision, engine.cpp:38-55): max, then sum exp(x - max) and min.
     const int64_t last = (int64_t)first_stop;  // every head stops (at the limit at the latest)
@@ -506,11 +617,12 @@ __global__ void __launch_bounds__(kDenseWarps * 32) dense_v_kernel(PoolView p, B
     __shared__ float so[kDenseWarps][G][128];
     __shared__ float som[kDenseWarps][G], sol[kDenseWarps][G];
     const int S = dense_slices(b);
-    for (int item = blockIdx.x; item < *b.dense_count * S; item += gridDim.x) {
-        const int u = b.dense_flag[item / S];
+    const int32_t* list = dense_list(b);
+    for (int item = blockIdx.x; item < dense_list_count(b) * S; item += gridDim.x) {
+        const int u = list[item / S];
         const int64_t n = b.list_off[u + 1] - b.list_off[u];
         const int64_t e0 = (int64_t)(item % S) * b.dense_slice, e1 = e0 + b.dense_slice < n ? e0 + b.dense_slice : n;
-        if (e0 < n) dense_v_unit<G>(p, b, u, item % S, e0, e1, so, som, sol);
+        if (e0 < n && !dense_skip(b, u)) dense_v_unit<G>(p, b, u, item % S, e0, e1, so, som, sol);
         __syncthreads();
     }
 }
@@ -538,46 +650,27 @@ __device__ __forceinline__ void dense_v_unit(const PoolView& p, const BatchView&
     float Oreg[16], Mreg = -INFINITY, Lreg = 0.0f;
 #pragma unroll
     for (int j = 0; j < 16; ++j) Oreg[j] = 0.0f;
-    // membership masks and slots run kDensePf iterations ahead of the V reads: the L2 prefetch (same
-    // distance) touches only blocks of the union, so no V byte outside it is fetched
     constexpr int kD = kDensePf;
     constexpr int64_t kW = kDenseWarps;
-    int64_t e = e_begin + warp;
-    auto slot_or = [&](int64_t f) { return f < e_end ? b.slots[off + f] : 0; };
-    auto mask_or = [&](int64_t f) { return f < e_end ? mask_of(f) : 0u; };
-    uint32_t mq[kD + 1];
-    int32_t sq[kD + 1];
-#pragma unroll
-    for (int i = 0; i <= kD; ++i) {
-        mq[i] = mask_or(e + i * kW);
-        sq[i] = slot_or(e + i * kW);
-    }
-    for (; e < e_end; e += kW) {
-        const uint32_t mask = mq[0];
-        const int32_t slot = sq[0];
-        if (lane == 0 && mq[kD] && kv_resident(p, sq[kD]))  // block e + kD*W, kD iterations ahead
-            prefetch_l2_bulk(kv_block<__nv_bfloat16>(p, sq[kD]) + v_off, (uint32_t)(T * 128 * 2));
+    // L2 prefetch of a union block's V tile ...
+    auto prefetch = [&](int64_t ef, uint32_t mf, int32_t sf) {
+        if (lane == 0 && mf && kv_resident(p, sf))
+            prefetch_l2_bulk(kv_block<__nv_bfloat16>(p, sf) + v_off, (uint32_t)(T * 128 * 2));
 #if PSA_DENSE_VPF
         // ... with the committed heads' token weights (lanes 0..g-1, one 64 B row each) and block
         // masses (lanes 8..8+g-1): both come from dense_k's write-back in HBM, and loading them
         // cold would put two DRAM round trips on every block's critical path
-        if (mq[kD]) {
-            const int64_t ef = e + kD * kW;
+        if (mf) {
             const int hl = lane & 7;
-            if (lane < 16 && hl < g && ((mq[kD] >> hl) & 1u)) {
+            if (lane < 16 && hl < g && ((mf >> hl) & 1u)) {
                 const int64_t row = off * g + (int64_t)hl * n + ef;
                 prefetch_l2_line(lane < 8 ? (const void*)(b.dense_p + row * 16) : (const void*)(b.dense_la + row));
             }
         }
 #endif
-#pragma unroll
-        for (int i = 0; i < kD; ++i) {
-            mq[i] = mq[i + 1];
-            sq[i] = sq[i + 1];
-        }
-        mq[kD] = mask_or(e + (kD + 1) * kW);
-        sq[kD] = slot_or(e + (kD + 1) * kW);
-        if (!mask) continue;
+    };
+    // one union block: V tile x the committed heads' weights (tensor cores), merged per head
+    auto block = [&](int64_t e, int32_t slot, uint32_t mask) {
         const bool mine = tq < g && ((mask >> tq) & 1u);  // this lane's merge head (tq) is committed
         const float la = mine ? __ldg(b.dense_la + off * g + (int64_t)tq * n + e) : 0.0f;  // exp(la - M) weight
         const __nv_bfloat16* vblk = kv_block<__nv_bfloat16>(p, slot) + v_off;
@@ -619,6 +712,71 @@ __device__ __forceinline__ void dense_v_unit(const PoolView& p, const BatchView&
             Lreg = Lreg * a + cc;
             Mreg = mnew;
         }
+    };
+    int64_t e = e_begin + warp;
+    int64_t most = 0;  // the heads' processed counts: a sparse union takes the windowed walk
+    for (int h = 0; h < g; ++h) most = b.bp[(int64_t)u * g + h] > most ? b.bp[(int64_t)u * g + h] : most;
+    if (4 * most >= n) {
+        // membership masks and slots run kDensePf iterations ahead of the V reads: the L2 prefetch (same
+        // distance) touches only blocks of the union, so no V byte outside it is fetched
+        auto slot_or = [&](int64_t f) { return f < e_end ? b.slots[off + f] : 0; };
+        auto mask_or = [&](int64_t f) { return f < e_end ? mask_of(f) : 0u; };
+        uint32_t mq[kD + 1];
+        int32_t sq[kD + 1];
+#pragma unroll
+        for (int i = 0; i <= kD; ++i) {
+            mq[i] = mask_or(e + i * kW);
+            sq[i] = slot_or(e + i * kW);
+        }
+        for (; e < e_end; e += kW) {
+            const uint32_t mask = mq[0];
+            const int32_t slot = sq[0];
+            if (mq[kD]) prefetch(e + kD * kW, mq[kD], sq[kD]);  // block e + kD*W, kD iterations ahead
+#pragma unroll
+            for (int i = 0; i < kD; ++i) {
+                mq[i] = mq[i + 1];
+                sq[i] = sq[i + 1];
+            }
+            mq[kD] = mask_or(e + (kD + 1) * kW);
+            sq[kD] = slot_or(e + (kD + 1) * kW);
+            if (mask) block(e, slot, mask);
+        }
+    } else {
+        // sparse union: the warp's positions tested 32 at a time (one lane each), a ballot gives the
+        // window's union blocks, the prefetch runs kDensePf union blocks ahead across windows
+        constexpr int64_t kWin = 32 * kW;
+        auto window = [&](int64_t wb, uint32_t& bal, uint32_t& ml, int32_t& sl) {
+            const int64_t f = wb + kW * lane;
+            ml = f < e_end ? mask_of(f) : 0u;
+            sl = ml ? b.slots[off + f] : 0;
+            bal = __ballot_sync(PSA_FULL, ml != 0u);
+        };
+        uint32_t bc, bn, mc, mn;
+        int32_t sc, sn;
+        window(e, bc, mc, sc);
+        window(e + kWin, bn, mn, sn);
+        for (int64_t wb = e; wb < e_end; wb += kWin) {
+            const uint64_t comb = (uint64_t)bc | ((uint64_t)bn << 32);
+            uint32_t rem = bc;
+            while (rem) {
+                const int i = __ffs(rem) - 1;
+                rem &= rem - 1;
+                uint64_t ahead = comb & ~((2ull << i) - 1ull);
+#pragma unroll
+                for (int k = 1; k < kD; ++k) ahead &= ahead - 1;
+                if (ahead) {
+                    const int j = __ffsll((long long)ahead) - 1;
+                    const uint32_t mf = __shfl_sync(PSA_FULL, j < 32 ? mc : mn, j & 31);
+                    const int32_t sf = __shfl_sync(PSA_FULL, j < 32 ? sc : sn, j & 31);
+                    prefetch(wb + kW * j, mf, sf);
+                }
+                block(wb + kW * i, __shfl_sync(PSA_FULL, sc, i), __shfl_sync(PSA_FULL, mc, i));
+            }
+            bc = bn;
+            mc = mn;
+            sc = sn;
+            window(wb + 2 * kWin, bn, mn, sn);
+        }
     }
     if (tq < G) {
 #pragma unroll
@@ -655,11 +813,118 @@ __device__ __forceinline__ void dense_v_unit(const PoolView& p, const BatchView&
     }
 }
 
+// Round 0's candidate prefix of every (handed-over unit, head): a key threshold tau with between
+// dense_sel_ranks / 2 and 2 * dense_sel_ranks keys <= tau (a prefix of the head's rank order, since
+// keys order the ranking), found by histogram refinement in key space between the head's min and
+// max key (from the score kernel). ~0 (every block) for short lists, partial mode off, and flat
+// units (criticality within dense_early nats over the first tranche: they stop near the end of
+// their lists). Also clears the unit's escalation mark.
+constexpr int kSelBins = 1024;
+constexpr int kSelThreads = 256;
+__global__ void __launch_bounds__(kSelThreads) dense_select_kernel(BatchView b) {
+    __shared__ uint32_t hist[kSelBins];
+    __shared__ unsigned wsum[kSelThreads / 32];
+    __shared__ int s_bstar;
+    __shared__ unsigned s_excl;
+    const int tid = threadIdx.x, lane = tid & 31;
+    const uint64_t pm = (b.pos_bits >= 64) ? ~0ull : ((1ull << b.pos_bits) - 1ull);
+    const int64_t N = b.dense_sel_ranks;
+    for (int item = blockIdx.x; item < *b.dense_count * b.g; item += gridDim.x) {
+        const int u = b.dense_flag[item / b.g], h = item % b.g;
+        const int64_t off = b.list_off[u], n = b.list_off[u + 1] - off;
+        const int64_t qi = (int64_t)u * b.g + h;
+        if (h == 0 && tid == 0) b.dense_esc_mark[u] = 0;
+        bool full = N <= 0 || n <= 2 * N;
+        if (!full && b.dense_early > 0.0f && b.ft_keys) {
+            for (int h2 = 0; h2 < b.g; ++h2) {
+                const int64_t q2 = (int64_t)u * b.g + h2;
+                if (b.ft_count[q2] >= kDenseHandover) {
+                    const double s0 = key_score(b.ft_keys[q2 * kFirstCap], pm);
+                    const double s1 = key_score(b.ft_keys[q2 * kFirstCap + kDenseHandover - 1], pm);
+                    full = full || s0 - s1 < (double)b.dense_early;
+                }
+            }
+        }
+        if (full) {
+            if (tid == 0) b.dense_sel[qi] = ~0ull;
+            continue;
+        }
+        const uint64_t* keys = b.keys + off * b.g + (int64_t)h * n;
+        uint64_t lo = 0, hi = ~0ull;
+        if (b.kminmax) {
+            lo = b.kminmax[qi];
+            hi = b.kminmax[qi + b.kmm_stride];
+        }
+        uint64_t tau = ~0ull;
+        unsigned before = 0, need = (unsigned)N;
+        for (int it = 0; it < 8; ++it) {
+            const uint64_t span = hi - lo;
+            const int bits = span ? 64 - __clzll((long long)span) : 0;
+            constexpr int kLog = 10;  // log2(kSelBins)
+            const int sh = bits > kLog ? bits - kLog : 0;
+            for (int i = tid; i < kSelBins; i += kSelThreads) hist[i] = 0;
+            __syncthreads();
+            scan_keys(keys, n, cta_team(), [&](uint64_t k) {
+                if (k >= lo && k <= hi) atomicAdd(&hist[(k - lo) >> sh], 1u);
+            });
+            __syncthreads();
+            constexpr int per = kSelBins / kSelThreads;
+            unsigned loc = 0;
+#pragma unroll
+            for (int j = 0; j < per; ++j) loc += hist[tid * per + j];
+            unsigned inc = loc;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned y = __shfl_up_sync(PSA_FULL, inc, o);
+                if (lane >= o) inc += y;
+            }
+            if (lane == 31) wsum[tid >> 5] = inc;
+            __syncthreads();
+            unsigned cum = inc - loc;
+            for (int w = 0; w < (tid >> 5); ++w) cum += wsum[w];
+            if (cum < need && need <= cum + loc) {
+#pragma unroll 1
+                for (int j = 0; j < per; ++j) {
+                    const unsigned c = hist[tid * per + j];
+                    if (need <= cum + c) {
+                        s_bstar = tid * per + j;
+                        s_excl = cum;
+                        break;
+                    }
+                    cum += c;
+                }
+            }
+            __syncthreads();
+            const int bs = s_bstar;
+            const unsigned ex = s_excl, c = hist[bs];
+            const uint64_t width_m1 = (sh >= 64) ? ~0ull : ((1ull << sh) - 1ull);
+            const uint64_t bin_lo = lo + ((uint64_t)bs << sh);
+            const uint64_t bin_hi = (hi - bin_lo <= width_m1) ? hi : bin_lo + width_m1;
+            __syncthreads();  // (s_bstar / hist reused by the next pass)
+            if (before + ex + c <= (unsigned)(2 * N)) {
+                tau = bin_hi;
+                break;
+            }
+            if (before + ex >= (unsigned)(N / 2)) {
+                tau = bin_lo - 1;  // the bins below bs (bin_lo > lo: before < N / 2 keys lie below lo)
+                break;
+            }
+            before += ex;
+            need -= ex;
+            lo = bin_lo;
+            hi = bin_hi;
+        }
+        if (tid == 0) b.dense_sel[qi] = tau;
+    }
+}
+
 // Per (handed-over unit, head): the slices' partial states merged (finalize, attention.hpp:104-110).
 __global__ void __launch_bounds__(128) dense_merge_kernel(BatchView b) {
     const int S = dense_slices(b);
-    for (int item = blockIdx.x; item < *b.dense_count * b.g; item += gridDim.x) {
-        const int u = b.dense_flag[item / b.g], h = item % b.g;
+    const int32_t* list = dense_list(b);
+    for (int item = blockIdx.x; item < dense_list_count(b) * b.g; item += gridDim.x) {
+        const int u = list[item / b.g], h = item % b.g;
+        if (dense_skip(b, u)) continue;
         const int64_t n = b.list_off[u + 1] - b.list_off[u];
         const int ns = (int)((n + b.dense_slice - 1) / b.dense_slice);
         const int64_t qi = (int64_t)u * b.g + h;
@@ -696,10 +961,26 @@ static int dense_sms() {
 }
 
 // Persistent grids over the hand-over list (sized to the SMs: no cost when the list is empty).
+static void launch_dense_round(const PoolView& p, const BatchView& b, cudaStream_t st);
+static int g_dense_sel = 1024;
+void set_dense_partial(int ranks) { g_dense_sel = ranks; }
+
 void launch_dense(const PoolView& p, const BatchView& b_in, cudaStream_t st) {
     // a whole list per work item when the batch alone fills the GPU, else kDenseSlice positions
     BatchView b = b_in;
     b.dense_slice = b.n_units >= 2 * dense_sms() ? (b.max_n > 0 ? b.max_n : 1) : kDenseSlice;
+    b.dense_sel_ranks = g_dense_sel;
+    b.dense_round = 0;
+    {
+        const int items = b.n_units * b.g < 2 * dense_sms() ? b.n_units * b.g : 2 * dense_sms();
+        dense_select_kernel<<<items, kSelThreads, 0, st>>>(b);
+    }
+    launch_dense_round(p, b, st);
+    b.dense_round = 1;  // units a head escalated: the rest of the K pass, full decide, V
+    launch_dense_round(p, b, st);
+}
+
+static void launch_dense_round(const PoolView& p, const BatchView& b, cudaStream_t st) {
     const int G = b.g <= 2 ? 2 : 4;
     const int64_t slices = (b.max_n + b.dense_slice - 1) / b.dense_slice;
     const int units = b.n_units * slices < 2 * dense_sms() ? (int)(b.n_units * slices) : 2 * dense_sms();

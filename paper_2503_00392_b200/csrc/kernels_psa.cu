@@ -434,11 +434,14 @@ int launch_psa(const PoolView& p, const BatchView& b, cudaStream_t st) {
         const bool dense = g_dense_mode == 0 && dense_supported(p, b);
         if (!dense) v.dense_flag = nullptr;
         v.dense_early = g_dense_early;
-        if (dense) cudaMemsetAsync(v.dense_count, 0, 4, st);
+        if (dense) {
+            cudaMemsetAsync(v.dense_count, 0, 4, st);
+            cudaMemsetAsync(v.dense_esc_count, 0, 4, st);
+        }
         const int n = launch_gqa(p, v, st);
         if (!dense) return n;
         launch_dense(p, v, st);  // units the GQA kernel handed over (others exit at once)
-        return n + 4;
+        return n + 9;  // select + two rounds of K / decide / V / merge
     }
     const int nq = b.n_units * b.g;
     if (p.dtype == 0) {

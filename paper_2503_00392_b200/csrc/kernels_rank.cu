@@ -704,6 +704,10 @@ static BatchView sub_view(const BatchView& b, int u0, int cnt, int idx) {
         v.dense_flag = b.dense_flag + u0;
         v.dense_count = b.dense_count + idx;
         v.dense_thr = b.dense_thr + qo;
+        v.dense_sel = b.dense_sel + qo;
+        v.dense_esc = b.dense_esc + u0;
+        v.dense_esc_count = b.dense_esc_count + idx;
+        v.dense_esc_mark = b.dense_esc_mark + u0;
         // the workspace holds ceil(max_n / kDenseSlice) partial states per head (the most any slicing uses)
         v.dense_part = b.dense_part + qo * (size_t)((b.max_n + kDenseSlice - 1) / kDenseSlice) * kDensePart;
     }

@@ -160,3 +160,42 @@ def test_dense_decide_crowded_bins(mods, oracle, cfg):
         assert a["bp"] == b["bp"] and np.array_equal(a["ids"], b["ids"]) and a["term"] == b["term"]
         assert np.max(np.abs(a["out"] - b["out"])) <= 1e-4
         check_parity(oracle, qs[0, h], bs, oc, cfg.get("topk", 0), a["ids"], a["bp"], a["out"], a["est"])
+
+
+@pytest.mark.parametrize("cfg", [dict(epsilon=0.99), dict(epsilon=0.99, microbatch_size=4), dict(topk=1500)])
+def test_dense_partial_prefix(mods, oracle, cfg):
+    """Partial dense mode: round 0 computes only each head's candidate prefix (~ranks keys) and
+    decides on it, heads that do not stop inside it send their unit to round 1 (rest of the K
+    pass, full decide). Every prefix size gives the same processed sets, stop points and
+    outputs (bit for bit) as the whole-list pass, and parity with the oracle."""
+    capi, _ = mods
+    g = 4
+    tokens = [16 * 6000 + 5, 16 * 9000, 16 * 5000 + 11]  # planted 1/32 at eps 0.99: heads need 400+ ranks
+    p, uids, nb, off, qs, run = synth_batch(mods, tokens, g, 1 / 32, cfg, seed=9)
+    got = {}
+    try:
+        for ranks in (0, 64, 700, 1024, 2048):
+            assert capi.lib.psattn_set_dense_partial(ranks) == 0
+            run.run()
+            got[ranks] = results(run, off, nb, g)
+    finally:
+        capi.lib.psattn_set_dense_partial(1024)
+    assert max(r["bp"] for r in got[0]) > 384  # the hand-over was exercised
+    for ranks in (64, 700, 1024, 2048):
+        for a, b in zip(got[ranks], got[0]):
+            assert a["bp"] == b["bp"] and np.array_equal(a["ids"], b["ids"]) and a["term"] == b["term"]
+            assert np.array_equal(a["out"], b["out"]) and a["est"] == b["est"]
+    oc = make_config(epsilon=cfg.get("epsilon", 1.0), microbatch_size=cfg.get("microbatch_size", 1))
+    for u, uid in enumerate(uids):
+        k, v = synth.unit_host(p, uid, tokens[u])
+        nt = [min(16, tokens[u] - i * 16) for i in range(nb[u])]
+        bs = BlockSet([k[i, :nt[i]] for i in range(nb[u])], [v[i, :nt[i]] for i in range(nb[u])])
+        for h in range(g):
+            a = got[1024][u * g + h]
+            check_parity(oracle, qs[u, h], bs, oc, cfg.get("topk", 0), a["ids"], a["bp"], a["out"], a["est"])
+
+
+def test_dense_partial_setter(mods):
+    capi, _ = mods
+    assert capi.lib.psattn_set_dense_partial(-1) != 0
+    assert capi.lib.psattn_set_dense_partial(1024) == 0
