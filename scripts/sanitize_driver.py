@@ -36,6 +36,10 @@ def synth_run(tokens, planted, cfg, kv=capi.PSATTN_KV_BF16, kernel=0):
 
 synth_run([16 * 900 + 3, 16 * 300], 1 / 32, dict(epsilon=0.95))            # score + first tranche + GQA
 synth_run([16 * 700 + 5], 0.0, dict(epsilon=0.95))                          # dense hand-over
+for ranks in (256, 32):  # partial dense: candidate prefix select, windowed K / V walks (32: escalations)
+    capi.check(capi.lib.psattn_set_dense_partial(ranks))
+    synth_run([16 * 3000 + 9, 16 * 1200], 1 / 32, dict(epsilon=0.99))
+capi.check(capi.lib.psattn_set_dense_partial(1024))
 synth_run([16 * 500], 0.0, dict(epsilon=0.9), kernel=1)                     # per-head kernel
 synth_run([16 * 600 + 7, 16 * 90], 1 / 32, dict(epsilon=0.95), kernel=2)     # GQA round kernel
 synth_run([16 * 400], 1 / 32, dict(epsilon=0.95, scale_override=4.0))        # stream kernel -> dense redo (extreme logits)
