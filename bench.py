@@ -66,8 +66,10 @@ def parse():
     ap.add_argument("--plan-only", action="store_true",
                     help="launcher/sharding dry run (no GPU): every rank reports its units over gloo")
     ap.add_argument("--e2e-buffers", type=int, default=1, choices=[1], help=argparse.SUPPRESS)  # (kept for old scripts)
-    ap.add_argument("--dropin-units", type=int, default=4,
-                    help="units timed through the drop-in C ABI (psattn_run_multi_head, host buffers); 0: off")
+    ap.add_argument("--dropin-groups", type=int, default=2,
+                    help="(request, layer) groups timed through the drop-in C ABI (psattn_run_multi_head, "
+                         "host buffers); 0: off")
+    ap.add_argument("--dropin-units", dest="dropin_groups", type=int, help=argparse.SUPPRESS)  # old scripts
     ap.add_argument("--check", type=int, default=16,
                     help="after timing: units of this rank's step checked against the reference (0: off)")
     return ap.parse_args()
@@ -322,14 +324,18 @@ def check_step(args, p, run, q_host, unit_ids, n, g):
     return r
 
 
-def dropin_e2e(args, p, units, n, g, seconds=2.0):
+def dropin_e2e(args, p, groups, n, g, seconds=2.0):
     """`e2e_dropin`: the same queries through the reference-facing C ABI — psattn_store (blocks put as
     host fp32 K/V, reference capi.cpp:134-156) and psattn_run_multi_head (psa_attention_multi_head,
-    engine.cpp:240-260: one kv-head list, its g q-heads) — host q in, host outputs + stats out, one
-    call per unit, every copy and the host-side accounting inside the timed region. This is the call
-    the CPU reference arm makes."""
+    engine.cpp:240-260) — host q in, host outputs + stats out, every copy and the host-side
+    accounting inside the timed region. One call per (request, layer): its hq q-heads over its hkv
+    kv-head lists, the call a decode step makes for one layer of one request (the multi-head API's
+    shape). `per_kv_head` times the same store one kv-head list (g q-heads) per call — the unit the
+    CPU reference arm's threads run."""
     from paper_2503_00392_b200 import capi
     from workload import synth
+    hkv = args.hkv
+    units = [(int(r) * args.layers + int(l)) * hkv + h for r, l in groups for h in range(hkv)]
     st = capi.Store(capacity=n * len(units), n_layers=1)
     lists, qs = [], []
     for i, uid in enumerate(units):
@@ -337,23 +343,36 @@ def dropin_e2e(args, p, units, n, g, seconds=2.0):
         r = args.ctx - (n - 1) * args.block  # ragged last block keeps its own token count
         st.put_many(i * n, k[:-1], v[:-1])
         capi.check(st.put(i * n + n - 1, k[-1, :r], v[-1, :r]))
+        del k, v
         lists.append(np.arange(i * n, (i + 1) * n, dtype=np.int64))
         qs.append(np.stack([synth.query(p, uid, h) for h in range(g)]).astype(np.float32))
     cfg = capi.config_default(epsilon=args.eps, microbatch_size=args.microbatch)
-    for i in range(len(units)):  # warm-up (first call sizes the store's staging buffers)
-        capi.check(st.run_multi_head(qs[i], [lists[i]], cfg)[0])
-    calls, t0 = 0, time.perf_counter()
-    while True:
-        for i in range(len(units)):
-            capi.check(st.run_multi_head(qs[i], [lists[i]], cfg)[0])
-            calls += 1
-        el = time.perf_counter() - t0
-        if el >= seconds:
-            break
+    calls_layer = [(np.concatenate(qs[j * hkv:(j + 1) * hkv]), lists[j * hkv:(j + 1) * hkv])
+                   for j in range(len(groups))]
+    calls_unit = [(qs[i], [lists[i]]) for i in range(len(units))]
+
+    def timed(calls):
+        for q, ls in calls:  # warm-up (the first call sizes the store's staging buffers)
+            capi.check(st.run_multi_head(q, ls, cfg)[0])
+        ncall, nq, t0 = 0, 0, time.perf_counter()
+        while True:
+            for q, ls in calls:
+                capi.check(st.run_multi_head(q, ls, cfg)[0])
+                ncall += 1
+                nq += q.shape[0]
+            el = time.perf_counter() - t0
+            if el >= seconds:
+                return nq / el, ncall, el
+
+    v_layer, c_layer, s_layer = timed(calls_layer)
+    v_unit, c_unit, s_unit = timed(calls_unit)
     st.close()
-    return dict(value=calls * g / el, unit=UNIT, calls=calls, seconds=round(el, 3), units=len(units),
-                kv_dtype="f32 (C ABI put_block)",
-                api="psattn_run_multi_head per (request, layer, kv-head) unit, host buffers, g q-heads per call")
+    return dict(value=v_layer, unit=UNIT, calls=c_layer, seconds=round(s_layer, 3),
+                groups=[[int(r), int(l)] for r, l in groups], kv_dtype="f32 (C ABI put_block)",
+                api=f"psattn_run_multi_head per (request, layer): {args.hq} q-heads over {hkv} kv-head lists of "
+                    f"{n} blocks, host buffers",
+                per_kv_head=dict(value=v_unit, unit=UNIT, calls=c_unit, seconds=round(s_unit, 3),
+                                 api=f"psattn_run_multi_head per kv-head unit: {g} q-heads, one list"))
 
 
 def run_ours(args):
@@ -569,10 +588,12 @@ def run_ours(args):
     if args.check > 0:
         parity = check_step(args, p, run, q_host, unit_ids, n, g)  # every rank checks a sample of its own units
 
-    # ---- the drop-in C ABI with host buffers (rank 0): psattn_run_multi_head per kv-head unit ----
+    # ---- the drop-in C ABI with host buffers (rank 0): psattn_run_multi_head per (request, layer) ----
     dropin = None
-    if rank == 0 and args.dropin_units > 0:
-        dropin = dropin_e2e(args, p, unit_ids[:: max(1, len(unit_ids) // args.dropin_units)][: args.dropin_units], n, g)
+    if rank == 0 and args.dropin_groups > 0:
+        rl = np.unique(unit_ids // args.hkv)  # this rank's (request, layer) pairs
+        pick = rl[np.linspace(0, len(rl) - 1, min(args.dropin_groups, len(rl))).astype(np.int64)]
+        dropin = dropin_e2e(args, p, [(x // args.layers, x % args.layers) for x in pick], n, g)
 
     # ---- CPU baseline (rank 0, N=1 only) ----
     cpu_base = None

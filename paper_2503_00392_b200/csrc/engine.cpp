@@ -10,6 +10,8 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <exception>
 #include <semaphore>
 #include <string>
@@ -63,6 +65,7 @@ Built assemble(const detail::DeviceQueryResult& r, std::size_t qi, std::size_t n
     res.terminated_early = r.terminated[qi] != 0;
     res.processed_ids.assign(r.ranked_ids[qi].begin(), r.ranked_ids[qi].begin() + res.blocks_processed);
     b.mbs = microbatches(res.blocks_processed, n, static_cast<std::size_t>(cfg.microbatch_size), take);
+    res.iterations.reserve(b.mbs.size());
     std::size_t cur = 0;
     for (std::size_t c : b.mbs) {
         cur += c;
@@ -84,12 +87,15 @@ std::uint64_t account_mb(TieredBlockStore& store, Built& b, std::size_t k, std::
     return hm.second;
 }
 
+// Replays every microbatch of a result (one store lock for the whole list).
 std::uint64_t account_all(TieredBlockStore& store, Built& b) {
+    std::vector<std::pair<std::uint64_t, std::uint64_t>> hm;
+    store.account_runs(b.res.processed_ids, b.mbs, hm);
     std::uint64_t misses = 0;
-    std::size_t start = 0;
     for (std::size_t k = 0; k < b.mbs.size(); ++k) {
-        misses += account_mb(store, b, k, start);
-        start += b.mbs[k];
+        b.res.iterations[k].hits = hm[k].first;
+        b.res.iterations[k].misses = hm[k].second;
+        misses += hm[k].second;
     }
     return misses;
 }
@@ -243,6 +249,7 @@ MultiHeadResult psa_attention_multi_head(std::span<const HeadVector> head_querie
         qb.group = static_cast<std::int32_t>(group);
         qb.dim = static_cast<std::int32_t>(head_queries[0].size());
         qb.cfg = cfg;
+        qb.want_union = true;
         for (const auto& l : kv_head_blocks) qb.lists.emplace_back(l);
         for (const auto& q : head_queries) {
             check_dim(q.size(), static_cast<std::size_t>(qb.dim), "multi-head attention");
@@ -255,24 +262,86 @@ MultiHeadResult psa_attention_multi_head(std::span<const HeadVector> head_querie
         qb.group = 1;
         qb.dim = static_cast<std::int32_t>(head_queries[0].size());
         qb.cfg = cfg;
+        qb.want_union = true;
         for (std::size_t h = 0; h < head_queries.size(); ++h) {
             qb.lists.emplace_back(kv_head_blocks[h / group]);
             qb.queries.push_back(head_queries[h].data());
         }
         store.run_device(qb, r);
     }
+    static const bool prof = std::getenv("PSA_RUN_PROF") != nullptr;  // development: host post-processing time
+    const auto t_post = std::chrono::steady_clock::now();
     std::uint64_t misses = 0;
+    double t_asm = 0.0, t_acc = 0.0;
+    auto lap = [](std::chrono::steady_clock::time_point& t) {
+        const auto now = std::chrono::steady_clock::now();
+        const double us = std::chrono::duration<double, std::micro>(now - t).count();
+        t = now;
+        return us;
+    };
+    auto t_lap = t_post;
+    out.per_head.reserve(head_queries.size());
     for (std::size_t h = 0; h < head_queries.size(); ++h) {
         Built b = assemble(r, h, kv_head_blocks[h / group].size(), cfg, 0);
+        if (prof) t_asm += lap(t_lap);
         misses += account_all(store, b);
-        for (BlockId id : b.res.processed_ids) out.fetched_union.push_back(id);
+        if (prof) t_acc += lap(t_lap);
         out.per_head.push_back(std::move(b.res));
     }
-    std::sort(out.fetched_union.begin(), out.fetched_union.end());
-    out.fetched_union.erase(std::unique(out.fetched_union.begin(), out.fetched_union.end()), out.fetched_union.end());
+    out.fetched_union = std::move(r.union_ids);  // sorted, distinct (reference engine.cpp:255-258)
+    if (prof)
+        std::fprintf(stderr, "multi_head_prof post_us=%.1f assemble_us=%.1f account_us=%.1f\n",
+                     std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t_post).count(),
+                     t_asm, t_acc);
     store.inject_miss_latency(misses);
     return out;
 }
+
+namespace detail {
+
+std::size_t multi_head_into(const float* q, std::int32_t n_q_heads, std::int32_t dim, const BlockId* ids,
+                            const std::int64_t* list_off, std::int32_t n_kv_heads, const PSAConfig& cfg,
+                            TieredBlockStore& store, float* out, HeadStats* stats) {
+    // the checks of psa_attention_multi_head above (reference engine.cpp:243-247)
+    if (n_q_heads <= 0) throw Error("multi-head attention: no query heads");
+    if (n_kv_heads <= 0) throw Error("multi-head attention: no kv heads");
+    if (n_q_heads % n_kv_heads != 0)
+        throw Error("multi-head attention: query head count must be a multiple of kv head count");
+    cfg.validate();
+    const int group = n_q_heads / n_kv_heads;
+    DeviceQueryBatch qb;
+    qb.dim = dim;
+    qb.cfg = cfg;
+    qb.want_union = true;
+    auto list = [&](int k) {
+        if (list_off[k + 1] < list_off[k]) throw ConfigError("psattn_run_multi_head: bad list offsets");
+        return std::span<const BlockId>(ids + list_off[k], static_cast<std::size_t>(list_off[k + 1] - list_off[k]));
+    };
+    qb.group = group <= 8 ? group : 1;  // wider groups run as independent lists (one per q-head)
+    for (int h = 0; h < n_q_heads; ++h) {
+        if (group > 8 || h % group == 0) qb.lists.push_back(list(h / group));
+        qb.queries.push_back(q + static_cast<std::size_t>(h) * dim);
+    }
+    DeviceQueryResult r;
+    store.run_device(qb, r);
+    std::uint64_t misses = 0;
+    std::vector<std::pair<std::uint64_t, std::uint64_t>> hm;
+    for (int h = 0; h < n_q_heads; ++h) {
+        const std::size_t n = qb.lists[static_cast<std::size_t>(group > 8 ? h : h / group)].size();
+        const auto bp = static_cast<std::size_t>(r.blocks_processed[h]);
+        const auto mbs = microbatches(bp, n, static_cast<std::size_t>(cfg.microbatch_size), 0);
+        store.account_runs(r.ranked_ids[h], mbs, hm);  // load_microbatch of every microbatch, in order
+        for (const auto& x : hm) misses += x.second;
+        std::copy(r.out.begin() + static_cast<std::ptrdiff_t>(h) * dim,
+                  r.out.begin() + static_cast<std::ptrdiff_t>(h + 1) * dim, out + static_cast<std::size_t>(h) * dim);
+        if (stats)
+            stats[h] = HeadStats{bp, n, r.est[h], cfg.audit_coverage ? r.true_cov[h] : -1.0, r.terminated[h] != 0};
+    }
+    store.inject_miss_latency(misses);
+    return r.union_ids.size();
+}
+
+}  // namespace detail
 
 // ---- pipeline.hpp (reference pipeline.cpp:32-176) ----
 namespace {

@@ -17,6 +17,7 @@
 #include <cstdint>
 #include <optional>
 #include <stdexcept>
+#include <algorithm>
 #include <unordered_map>
 #include <vector>
 
@@ -37,6 +38,14 @@ public:
         }
     }
     std::size_t capacity() const { return cap_; }
+    // dense chains: extends the id range to at least [0, n) (geometric growth)
+    void grow(std::size_t n) {
+        if (!dense_ || n <= in_.size()) return;
+        const std::size_t m = std::max(n, 2 * in_.size());
+        older_.resize(m, kNone);
+        newer_.resize(m, kNone);
+        in_.resize(m, 0);
+    }
     std::size_t size() const { return dense_ ? count_ : links_.size(); }
     bool contains(std::int64_t id) const {
         if (dense_) return id >= 0 && static_cast<std::size_t>(id) < in_.size() && in_[static_cast<std::size_t>(id)];
@@ -166,6 +175,9 @@ public:
         return a;
     }
     bool release(std::int64_t id, std::int32_t layer) { return domain(layer).erase(id); }
+    void grow(std::size_t dense_ids) {
+        for (auto& d : domains_) d.grow(dense_ids);
+    }
     bool resident(std::int64_t id, std::int32_t layer) const { return domain(layer).contains(id); }
 
     std::size_t capacity(std::int32_t layer) const { return domain(layer).capacity(); }

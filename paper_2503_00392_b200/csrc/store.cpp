@@ -8,6 +8,8 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <thread>
@@ -16,6 +18,7 @@
 
 #include "device.h"
 #include "engine_internal.h"
+#include "block_table.h"
 #include "fast_tier.h"
 #include "psattn_b200.h"
 
@@ -95,7 +98,8 @@ TieredBlockStore::TieredBlockStore(const StoreOptions& options) : options_(optio
     if (options_.n_layers <= 0) throw Error("TieredBlockStore: n_layers must be positive");
     tier_ = std::make_unique<psa::FastTier>(options_.fast_capacity_slots, options_.n_layers,
                                             options_.policy == PoolPolicy::LayerPartitioned,
-                                            options_.eviction == EvictionPolicy::LRU);
+                                            options_.eviction == EvictionPolicy::LRU, /*dense_ids=*/1);
+    blocks_ = std::make_unique<psa::BlockTable<BlockRec>>();
     int n = 0;
     if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
         throw Error("TieredBlockStore: no CUDA device (the B200 PSA path has no CPU fallback)");
@@ -105,9 +109,8 @@ TieredBlockStore::TieredBlockStore(const StoreOptions& options) : options_(optio
 
 TieredBlockStore::~TieredBlockStore() = default;
 
-std::int32_t TieredBlockStore::layer_of(BlockId id) const {
-    auto it = blocks_.find(id);
-    return it == blocks_.end() ? -1 : it->second.layer;
+std::int32_t TieredBlockStore::layer_of_handle(std::int64_t handle) const {
+    return blocks_->at(handle).layer;
 }
 
 TieredBlockStore::DevicePool& TieredBlockStore::pool_for(std::int32_t dim, std::int32_t n_tokens) {
@@ -138,7 +141,7 @@ void TieredBlockStore::put_block(std::shared_ptr<const KVBlock> block, RequestId
     if (block->keys.size() < nelem || block->values.size() < nelem) throw Error("put_block: short key/value arrays");
     std::lock_guard lock(mutex_);
     if (block->layer_id < 0 || block->layer_id >= options_.n_layers) throw Error("put_block: layer_id out of range");
-    if (blocks_.count(block->block_id))
+    if (blocks_->contains(block->block_id))
         throw Error("put_block: duplicate block id " + std::to_string(block->block_id));
     DevicePool& dp = pool_for(block->dim, block->n_tokens);
     std::int64_t slot;
@@ -154,30 +157,43 @@ void TieredBlockStore::put_block(std::shared_ptr<const KVBlock> block, RequestId
     const std::int32_t s32 = static_cast<std::int32_t>(slot);
     const std::int32_t nt = block->n_tokens;
     check_rc(psa::pool_put(dp.pool, 1, &s32, &nt, block->keys.data(), block->values.data(), 0, dev_->stream));
-    blocks_.emplace(block->block_id, BlockRec{block->dim, block->layer_id, block->n_tokens, slot, owner});
+    const std::int64_t h =
+        blocks_->insert(block->block_id, BlockRec{block->dim, block->layer_id, block->n_tokens, slot, owner});
     owned_[owner].push_back(block->block_id);
-    tier_->put(block->block_id, block->layer_id, [this](BlockId v) { return layer_of(v); });
+    tier_->grow(blocks_->handles());
+    tier_->put(h, block->layer_id, [this](std::int64_t v) { return layer_of_handle(v); });
 }
 
-bool TieredBlockStore::account_locked(BlockId id, const BlockRec& rec) {
+bool TieredBlockStore::account_locked(BlockId id, std::int64_t handle, const BlockRec& rec) {
     const std::uint64_t payload = 2ull * static_cast<std::uint64_t>(rec.n_tokens) * rec.dim * sizeof(float);
-    const auto a = tier_->access(id, rec.layer, payload, [this](BlockId v) { return layer_of(v); });
+    const auto a = tier_->access(handle, rec.layer, payload, [this](std::int64_t v) { return layer_of_handle(v); });
     if (trace_)  // seq,layer_id,block_id,hit|miss,evicted_id|-
         *trace_ << trace_seq_++ << ',' << rec.layer << ',' << id << ',' << (a.hit ? "hit," : "miss,")
-                << (a.evicted ? std::to_string(*a.evicted) : std::string("-")) << '\n';
+                << (a.evicted ? std::to_string(blocks_->id_of(*a.evicted)) : std::string("-")) << '\n';
     return !a.hit;
 }
 
 std::pair<std::uint64_t, std::uint64_t> TieredBlockStore::account_loads(std::span<const BlockId> ids) {
+    std::vector<std::pair<std::uint64_t, std::uint64_t>> hm;
+    const std::size_t run = ids.size();
+    account_runs(ids, std::span<const std::size_t>(&run, 1), hm);
+    return hm[0];
+}
+
+void TieredBlockStore::account_runs(std::span<const BlockId> ids, std::span<const std::size_t> runs,
+                                    std::vector<std::pair<std::uint64_t, std::uint64_t>>& hits_misses) {
     std::lock_guard lock(mutex_);
-    std::uint64_t h = 0, m = 0;
-    for (BlockId id : ids) {
-        auto it = blocks_.find(id);
-        if (it == blocks_.end()) throw NotFoundError("load_block: unknown block id " + std::to_string(id));
-        if (account_locked(id, it->second)) ++m;
-        else ++h;
+    hits_misses.assign(runs.size(), {0, 0});
+    std::size_t i = 0;
+    for (std::size_t k = 0; k < runs.size(); ++k) {
+        for (std::size_t e = i + runs[k]; i < e && i < ids.size(); ++i) {
+            const BlockId id = ids[i];
+            const std::int64_t h = blocks_->handle(id);
+            if (h < 0) throw NotFoundError("load_block: unknown block id " + std::to_string(id));
+            if (account_locked(id, h, blocks_->at(h))) ++hits_misses[k].second;
+            else ++hits_misses[k].first;
+        }
     }
-    return {h, m};
 }
 
 void TieredBlockStore::inject_miss_latency(std::uint64_t misses) const {
@@ -203,11 +219,12 @@ std::shared_ptr<const KVBlock> TieredBlockStore::load_block(BlockId block_id, st
     bool miss = false;
     {
         std::lock_guard lock(mutex_);
-        auto it = blocks_.find(block_id);
-        if (it == blocks_.end()) throw NotFoundError("load_block: unknown block id " + std::to_string(block_id));
-        if (layer_id >= 0 && it->second.layer != layer_id) throw Error("load_block: layer_id does not match block");
-        miss = account_locked(block_id, it->second);
-        out = copy_out(block_id, it->second);
+        const std::int64_t h = blocks_->handle(block_id);
+        if (h < 0) throw NotFoundError("load_block: unknown block id " + std::to_string(block_id));
+        const BlockRec& rec = blocks_->at(h);
+        if (layer_id >= 0 && rec.layer != layer_id) throw Error("load_block: layer_id does not match block");
+        miss = account_locked(block_id, h, rec);
+        out = copy_out(block_id, rec);
     }
     if (miss) inject_miss_latency(1);
     return out;
@@ -215,16 +232,16 @@ std::shared_ptr<const KVBlock> TieredBlockStore::load_block(BlockId block_id, st
 
 std::shared_ptr<const KVBlock> TieredBlockStore::peek_block(BlockId block_id) const {
     std::lock_guard lock(mutex_);
-    auto it = blocks_.find(block_id);
-    if (it == blocks_.end()) throw NotFoundError("peek_block: unknown block id " + std::to_string(block_id));
-    return copy_out(block_id, it->second);
+    const BlockRec* rec = blocks_->find(block_id);
+    if (!rec) throw NotFoundError("peek_block: unknown block id " + std::to_string(block_id));
+    return copy_out(block_id, *rec);
 }
 
 BlockMetadata TieredBlockStore::metadata(BlockId block_id) const {
     std::lock_guard lock(mutex_);
-    auto it = blocks_.find(block_id);
-    if (it == blocks_.end()) throw NotFoundError("metadata: unknown block id " + std::to_string(block_id));
-    const BlockRec& r = it->second;
+    const BlockRec* rp = blocks_->find(block_id);
+    if (!rp) throw NotFoundError("metadata: unknown block id " + std::to_string(block_id));
+    const BlockRec& r = *rp;
     BlockMetadata m;
     m.block_id = block_id;
     m.layer_id = r.layer;
@@ -248,25 +265,26 @@ void TieredBlockStore::release_request(RequestId request_id) {
     auto it = owned_.find(request_id);
     if (it == owned_.end()) throw NotFoundError("release_request: unknown request " + std::to_string(request_id));
     for (BlockId id : it->second) {
-        auto b = blocks_.find(id);
-        if (b == blocks_.end()) continue;
-        tier_->release(id, b->second.layer);
-        pools_.at(b->second.dim)->free_slots.push_back(b->second.slot);
-        blocks_.erase(b);
+        const std::int64_t h = blocks_->handle(id);
+        if (h < 0) continue;
+        const BlockRec& rec = blocks_->at(h);
+        tier_->release(h, rec.layer);
+        pools_.at(rec.dim)->free_slots.push_back(rec.slot);
+        blocks_->erase(id);
     }
     owned_.erase(it);
 }
 
 bool TieredBlockStore::contains(BlockId block_id) const {
     std::lock_guard lock(mutex_);
-    return blocks_.count(block_id) > 0;
+    return blocks_->contains(block_id);
 }
 
 bool TieredBlockStore::resident_fast(BlockId block_id) const {
     std::lock_guard lock(mutex_);
-    auto it = blocks_.find(block_id);
-    if (it == blocks_.end()) return false;
-    return tier_->resident(block_id, it->second.layer);
+    const std::int64_t h = blocks_->handle(block_id);
+    if (h < 0) return false;
+    return tier_->resident(h, blocks_->at(h).layer);
 }
 
 CacheStats TieredBlockStore::stats() const {
@@ -301,35 +319,24 @@ void TieredBlockStore::enable_trace(std::ostream* sink) {
 // -----------------------------------------------------------------------------
 void TieredBlockStore::run_device(const detail::DeviceQueryBatch& qb, detail::DeviceQueryResult& res) {
     std::lock_guard lock(mutex_);
+    static const bool prof = getenv("PSA_RUN_PROF") != nullptr;  // development: phase times to stderr
+    using PClock = std::chrono::steady_clock;
+    const auto t_begin = PClock::now();
+    auto us_since = [](PClock::time_point a) {
+        return std::chrono::duration<double, std::micro>(PClock::now() - a).count();
+    };
     const int g = qb.group, d = qb.dim;
     const int n_units = static_cast<int>(qb.lists.size());
     if (n_units == 0) throw Error("batched attention: empty batch");
     auto pit = pools_.find(d);
-    // Resolve ids -> slots (one lookup per id), ascending-id order per list; lists that arrive
-    // sorted (the usual page-table order) skip the sort.
-    std::vector<std::vector<BlockId>> sorted(n_units);
-    std::vector<std::vector<std::int32_t>> slot_of(n_units);
     std::vector<std::int64_t> off(n_units + 1, 0);
     std::int64_t max_n = 0;
     for (int u = 0; u < n_units; ++u) {
-        const auto& ids = qb.lists[u];
-        if (ids.empty()) throw Error("plan_blocks: no blocks given");
-        auto& srt = sorted[u];
-        auto& sl = slot_of[u];
-        srt.assign(ids.begin(), ids.end());
-        if (!std::is_sorted(srt.begin(), srt.end())) std::sort(srt.begin(), srt.end());
-        sl.resize(srt.size());
-        for (std::size_t i = 0; i < srt.size(); ++i) {
-            auto it = blocks_.find(srt[i]);
-            if (it == blocks_.end()) throw NotFoundError("metadata: unknown block id " + std::to_string(srt[i]));
-            check_dim(static_cast<std::size_t>(d), static_cast<std::size_t>(it->second.dim), "criticality_score");
-            sl[i] = static_cast<std::int32_t>(it->second.slot);
-        }
-        off[u + 1] = off[u] + static_cast<std::int64_t>(ids.size());
-        max_n = std::max<std::int64_t>(max_n, static_cast<std::int64_t>(ids.size()));
+        const auto m = static_cast<std::int64_t>(qb.lists[u].size());
+        if (m == 0) throw Error("plan_blocks: no blocks given");
+        off[u + 1] = off[u] + m;
+        max_n = std::max(max_n, m);
     }
-    if (pit == pools_.end()) throw Error("no blocks of this dimension");
-    psattn_pool* pool = pit->second->pool;
     const std::int64_t total = off[n_units];
     const std::int64_t nq = static_cast<std::int64_t>(n_units) * g;
     const std::int64_t hbt = total * g;
@@ -339,10 +346,34 @@ void TieredBlockStore::run_device(const detail::DeviceQueryBatch& qb, detail::De
     const size_t s_b = align256(static_cast<size_t>(total) * 4);
     const size_t o_b = align256(static_cast<size_t>(n_units + 1) * 8);
     char* hin = static_cast<char*>(dev_->h_in.get(q_b + s_b + o_b));
-    for (std::int64_t i = 0; i < nq; ++i) std::memcpy(hin + static_cast<size_t>(i) * d * 4, qb.queries[i], d * 4);
     auto* hs = reinterpret_cast<std::int32_t*>(hin + q_b);
-    for (int u = 0; u < n_units; ++u) std::memcpy(hs + off[u], slot_of[u].data(), slot_of[u].size() * 4);
+    // Resolve ids -> slots straight into the staging buffer (one table index per id), ascending-id
+    // order per list; lists that arrive sorted (the usual page-table order) are used in place.
+    std::vector<std::vector<BlockId>> sorted_copy(n_units);
+    std::vector<const BlockId*> sorted(n_units);
+    for (int u = 0; u < n_units; ++u) {
+        const auto& ids = qb.lists[u];
+        if (std::is_sorted(ids.begin(), ids.end())) {
+            sorted[u] = ids.data();
+        } else {
+            sorted_copy[u].assign(ids.begin(), ids.end());
+            std::sort(sorted_copy[u].begin(), sorted_copy[u].end());
+            sorted[u] = sorted_copy[u].data();
+        }
+        const BlockId* src = sorted[u];
+        std::int32_t* dst = hs + off[u];
+        for (std::int64_t i = 0, m = off[u + 1] - off[u]; i < m; ++i) {
+            const BlockRec* rec = blocks_->find(src[i]);
+            if (!rec) throw NotFoundError("metadata: unknown block id " + std::to_string(src[i]));
+            if (rec->dim != d) check_dim(static_cast<std::size_t>(d), static_cast<std::size_t>(rec->dim), "criticality_score");
+            dst[i] = static_cast<std::int32_t>(rec->slot);
+        }
+    }
+    if (pit == pools_.end()) throw Error("no blocks of this dimension");
+    psattn_pool* pool = pit->second->pool;
+    for (std::int64_t i = 0; i < nq; ++i) std::memcpy(hin + static_cast<size_t>(i) * d * 4, qb.queries[i], d * 4);
     std::memcpy(hin + q_b + s_b, off.data(), (n_units + 1) * 8);
+    const double t_resolve = prof ? us_since(t_begin) : 0.0;
     char* din = static_cast<char*>(dev_->in.get(q_b + s_b + o_b));
     check_cuda(cudaMemcpyAsync(din, hin, q_b + s_b + o_b, cudaMemcpyHostToDevice, dev_->stream), "H2D");
 
@@ -379,7 +410,13 @@ void TieredBlockStore::run_device(const detail::DeviceQueryBatch& qb, detail::De
     b.iter_est = reinterpret_cast<double*>(dout + o); o += ob_iest;
     const size_t wsb = psattn_batch_workspace_bytes(&b);
     void* ws = dev_->ws.get(wsb);
+    cudaEvent_t pev[3] = {nullptr, nullptr, nullptr};
+    if (prof) {
+        for (auto& e : pev) cudaEventCreate(&e);
+        cudaEventRecord(pev[0], dev_->stream);
+    }
     check_rc(qb.rank_only ? psattn_rank_batch(pool, &b, ws, dev_->stream) : psattn_run_batch(pool, &b, ws, dev_->stream));
+    if (prof) cudaEventRecord(pev[1], dev_->stream);
 
     const bool has_oracle = b.ranking_mode == PSATTN_RANK_ORACLE || b.audit_coverage;
     const size_t om_b = has_oracle ? static_cast<size_t>(hbt) * 8 : 0;
@@ -392,7 +429,10 @@ void TieredBlockStore::run_device(const detail::DeviceQueryBatch& qb, detail::De
                                    dev_->stream),
                    "D2H");
     }
+    if (prof) cudaEventRecord(pev[2], dev_->stream);
+    const double t_launched = prof ? us_since(t_begin) : 0.0;
     check_cuda(cudaStreamSynchronize(dev_->stream), "PSA device launch");
+    const double t_synced = prof ? us_since(t_begin) : 0.0;
 
     // ---- unpack ----
     res.dim = d;
@@ -413,8 +453,11 @@ void TieredBlockStore::run_device(const detail::DeviceQueryBatch& qb, detail::De
     res.ranked_ids.assign(nq, {});
     res.iter_est.assign(nq, {});
     res.oracle_ranked.assign(nq, {});
+    res.union_ids.clear();
+    std::vector<std::uint8_t> seen;  // want_union: list positions processed by any head of the unit
     for (int u = 0; u < n_units; ++u) {
         const std::int64_t n = off[u + 1] - off[u];
+        if (qb.want_union) seen.assign(static_cast<std::size_t>(n), 0);
         for (int h = 0; h < g; ++h) {
             const std::int64_t qi = static_cast<std::int64_t>(u) * g + h;
             const std::int64_t hb = off[u] * g + h * n;
@@ -426,6 +469,7 @@ void TieredBlockStore::run_device(const detail::DeviceQueryBatch& qb, detail::De
                 const std::int32_t pos = rpos[hb + r];
                 if (pos < 0 || pos >= n) throw Error("device ranking: position out of range");
                 ids[r] = sorted[u][pos];
+                if (qb.want_union) seen[static_cast<std::size_t>(pos)] = 1;
             }
             if (!qb.rank_only) res.iter_est[qi].assign(iest + hb, iest + hb + nr);
             if (has_oracle) {
@@ -434,6 +478,24 @@ void TieredBlockStore::run_device(const detail::DeviceQueryBatch& qb, detail::De
                 for (std::int64_t r = 0; r < nr; ++r) orr[r] = om[hb + rpos[hb + r]];
             }
         }
+        if (qb.want_union)  // positions ascend with ids: the unit's union comes out sorted
+            for (std::int64_t i = 0; i < n; ++i)
+                if (seen[static_cast<std::size_t>(i)]) res.union_ids.push_back(sorted[u][i]);
+    }
+    if (qb.want_union && !std::is_sorted(res.union_ids.begin(), res.union_ids.end()))
+        std::sort(res.union_ids.begin(), res.union_ids.end());  // lists sharing ids: merge the runs
+    if (qb.want_union)
+        res.union_ids.erase(std::unique(res.union_ids.begin(), res.union_ids.end()), res.union_ids.end());
+    if (prof) {
+        float kms = 0.0f, cms = 0.0f;
+        cudaEventElapsedTime(&kms, pev[0], pev[1]);
+        cudaEventElapsedTime(&cms, pev[1], pev[2]);
+        for (auto& e : pev) cudaEventDestroy(e);
+        fprintf(stderr,
+                "run_device_prof units=%d blocks=%lld resolve_us=%.1f launch_us=%.1f sync_us=%.1f unpack_us=%.1f "
+                "device_kernels_us=%.1f d2h_us=%.1f\n",
+                n_units, static_cast<long long>(total), t_resolve, t_launched - t_resolve, t_synced - t_launched,
+                us_since(t_begin) - t_synced, kms * 1e3, cms * 1e3);
     }
 }
 

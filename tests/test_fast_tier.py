@@ -22,6 +22,8 @@ def shim(tmp_path_factory):
     L = C.CDLL(so)
     L.ft_create.restype = C.c_void_p
     L.ft_create.argtypes = [C.c_uint64, C.c_int, C.c_int, C.c_int, C.c_uint64]
+    L.ft_create_table.restype = C.c_void_p
+    L.ft_create_table.argtypes = [C.c_uint64, C.c_int, C.c_int, C.c_int]
     L.ft_destroy.argtypes = [C.c_void_p]
     L.ft_put.restype = C.c_int64
     L.ft_put.argtypes = [C.c_void_p, C.c_int64, C.c_int]
@@ -38,19 +40,27 @@ NONE = -(2 ** 63)
 @pytest.mark.parametrize("partitioned", [0, 1])
 @pytest.mark.parametrize("fifo", [0, 1])
 @pytest.mark.parametrize("cap", [0, 5, 12])
-@pytest.mark.parametrize("dense", [0, 1000])  # hash-map chains (C/C++ store) / flat arrays (two-tier store)
+# hash-map chains / flat arrays over ids (two-tier store) / ids -> handles through BlockTable with
+# chains over handles (the C/C++ store), ids spread over the direct range, negatives and huge values
+@pytest.mark.parametrize("dense", [0, 1000, "table"])
 def test_fast_tier_matches_reference_store(shim, ref, partitioned, fifo, cap, dense):
     rng = np.random.default_rng(100 * cap + 10 * partitioned + fifo)
     layers, d = 3, 4
     st = ref.store(capacity=cap, n_layers=layers, partitioned=partitioned, fifo=fifo)
-    h = shim.ft_create(cap, layers, partitioned, 1 - fifo, dense)
+    if dense == "table":
+        h = shim.ft_create_table(cap, layers, partitioned, 1 - fifo)
+        idmap = {0: lambda i: i, 1: lambda i: -1 - 3 * i, 2: lambda i: (1 << 40) + i, 3: lambda i: (1 << 24) + i}
+        ids = [idmap[i % 4](i) for i in range(400)]
+    else:
+        h = shim.ft_create(cap, layers, partitioned, 1 - fifo, dense)
+        ids = list(range(400))
     layer_of, ntok, owner_of, live = {}, {}, {}, []
     next_id = 0
     n_loads = 0
     for step in range(400):
         op = rng.random()
         if op < 0.3 or not live:
-            bid, lay, nt, own = next_id, int(rng.integers(layers)), int(rng.integers(1, 5)), int(rng.integers(4))
+            bid, lay, nt, own = ids[next_id], int(rng.integers(layers)), int(rng.integers(1, 5)), int(rng.integers(4))
             next_id += 1
             k = rng.standard_normal((nt, d)).astype(np.float32)
             st.put(bid, k, k, layer=lay, owner=own)
