@@ -73,6 +73,12 @@ public:
     }
 
     std::int64_t id_of(std::int64_t h) const { return ids_[static_cast<std::size_t>(h)]; }
+    // fn(id, rec) for every live block
+    template <typename Fn>
+    void for_each(Fn&& fn) const {
+        for (std::size_t h = 0; h < recs_.size(); ++h)
+            if (handle(ids_[h]) == static_cast<std::int64_t>(h)) fn(ids_[h], recs_[h]);
+    }
     const Rec& at(std::int64_t h) const { return recs_[static_cast<std::size_t>(h)]; }
     std::size_t handles() const { return recs_.size(); }  // every handle ever issued is below this
     std::size_t size() const { return live_; }

@@ -80,6 +80,7 @@ size_t align256(size_t x) { return (x + 255) / 256 * 256; }
 
 struct TieredBlockStore::DevicePool {
     psattn_pool* pool = nullptr;
+    bool bf16 = false;  // lossless bf16 storage: every block put so far is exactly representable
     std::int64_t next_slot = 0;
     std::vector<std::int64_t> free_slots;
     ~DevicePool() { psattn_pool_destroy(pool); }
@@ -113,14 +114,39 @@ std::int32_t TieredBlockStore::layer_of_handle(std::int64_t handle) const {
     return blocks_->at(handle).layer;
 }
 
-TieredBlockStore::DevicePool& TieredBlockStore::pool_for(std::int32_t dim, std::int32_t n_tokens) {
+namespace {
+// true when every value is exactly a bf16 (low 16 bits of the fp32 pattern zero): the block is
+// then stored losslessly in bf16 — half the HBM, and the bf16 production kernels
+bool bf16_exact(const float* x, std::size_t n) {
+    std::uint32_t acc = 0;
+    for (std::size_t i = 0; i < n; ++i) {
+        std::uint32_t b;
+        std::memcpy(&b, x + i, 4);
+        acc |= b;
+    }
+    return (acc & 0xFFFFu) == 0;
+}
+
+bool lossless_bf16_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("PSA_STORE_F32_ONLY");  // development: keep every pool fp32
+        return !(e && e[0] == '1');
+    }();
+    return on;
+}
+}  // namespace
+
+TieredBlockStore::DevicePool& TieredBlockStore::pool_for(std::int32_t dim, std::int32_t n_tokens, bool exact_bf16) {
     auto it = pools_.find(dim);
     if (it == pools_.end()) {
         auto dp = std::make_unique<DevicePool>();
         psattn_pool_desc desc{};
         desc.dim = dim;
         desc.block_tokens = std::max(n_tokens, 16);
-        desc.kv_dtype = PSATTN_KV_F32;  // the C/C++ API hands fp32 blocks; keep them exact
+        // the C/C++ API hands fp32 blocks and keeps them exact: bf16 while every block is exactly
+        // representable in bf16 (e.g. an upcast bf16 KV cache), fp32 otherwise
+        dp->bf16 = exact_bf16 && lossless_bf16_enabled();
+        desc.kv_dtype = dp->bf16 ? PSATTN_KV_BF16 : PSATTN_KV_F32;
         desc.n_slots = 256;
         check_rc(psattn_pool_create(&desc, &dp->pool));
         it = pools_.emplace(dim, std::move(dp)).first;
@@ -128,6 +154,34 @@ TieredBlockStore::DevicePool& TieredBlockStore::pool_for(std::int32_t dim, std::
     DevicePool& dp = *it->second;
     psattn_pool_desc desc{};
     psattn_pool_get_desc(dp.pool, &desc);
+    if (dp.bf16 && !exact_bf16) {
+        // first block that bf16 cannot hold exactly: move every stored block to an fp32 pool (same
+        // slots, values and metadata unchanged: bf16 -> fp32 is exact)
+        psattn_pool_desc fd = desc;
+        fd.kv_dtype = PSATTN_KV_F32;
+        fd.block_tokens = std::max(desc.block_tokens, n_tokens);
+        psattn_pool* fp = nullptr;
+        check_rc(psattn_pool_create(&fd, &fp));
+        std::vector<float> k, v;
+        int rc = PSATTN_OK;
+        blocks_->for_each([&](BlockId, const BlockRec& r) {
+            if (r.dim != dim || rc != PSATTN_OK) return;
+            const std::size_t cnt = static_cast<std::size_t>(r.n_tokens) * static_cast<std::size_t>(dim);
+            k.resize(cnt);
+            v.resize(cnt);
+            const std::int32_t s32 = static_cast<std::int32_t>(r.slot), nt = r.n_tokens;
+            rc = psa::read_slot(dp.pool, r.slot, r.n_tokens, k.data(), v.data());
+            if (rc == PSATTN_OK) rc = psa::pool_put(fp, 1, &s32, &nt, k.data(), v.data(), 0, dev_->stream);
+        });
+        if (rc != PSATTN_OK) {
+            psattn_pool_destroy(fp);
+            check_rc(rc);
+        }
+        psattn_pool_destroy(dp.pool);
+        dp.pool = fp;
+        dp.bf16 = false;
+        psattn_pool_get_desc(dp.pool, &desc);
+    }
     if (n_tokens > desc.block_tokens) check_rc(psa::pool_grow(dp.pool, desc.n_slots, n_tokens));
     return dp;
 }
@@ -139,11 +193,12 @@ void TieredBlockStore::put_block(std::shared_ptr<const KVBlock> block, RequestId
     if (block->n_tokens > 128) throw Error("put_block: blocks of more than 128 tokens are not supported by the device pool");
     const std::size_t nelem = static_cast<std::size_t>(block->n_tokens) * static_cast<std::size_t>(block->dim);
     if (block->keys.size() < nelem || block->values.size() < nelem) throw Error("put_block: short key/value arrays");
+    const bool exact = bf16_exact(block->keys.data(), nelem) && bf16_exact(block->values.data(), nelem);
     std::lock_guard lock(mutex_);
     if (block->layer_id < 0 || block->layer_id >= options_.n_layers) throw Error("put_block: layer_id out of range");
     if (blocks_->contains(block->block_id))
         throw Error("put_block: duplicate block id " + std::to_string(block->block_id));
-    DevicePool& dp = pool_for(block->dim, block->n_tokens);
+    DevicePool& dp = pool_for(block->dim, block->n_tokens, exact);
     std::int64_t slot;
     if (!dp.free_slots.empty()) {
         slot = dp.free_slots.back();

@@ -259,3 +259,51 @@ def test_run_multi_head_matches_reference(capi, ref, case):
     theirs.put(int(bs.ids[1]), k, v, owner=1)
     assert mine.contains(int(bs.ids[1])) == (0, True) and theirs.contains(int(bs.ids[1]))
     assert mine.stats() == theirs.stats()
+
+
+def _to_bf16_exact(x):
+    b = np.ascontiguousarray(x, np.float32).view(np.uint32)
+    return ((b + 0x7FFF + ((b >> 16) & 1)) & 0xFFFF0000).view(np.float32)
+
+
+@pytest.mark.parametrize("d,g", [(128, 4), (64, 2), (32, 3)])
+def test_lossless_bf16_store_and_migration(capi, ref, d, g):
+    """Blocks whose values are all exact bf16 (an upcast bf16 KV cache) are stored losslessly in a
+    bf16 pool (the production kernels); the first block that is not moves every stored block to an
+    fp32 pool. Query results before and after the move match the compiled reference on the same
+    fp32 values, and match a store that held fp32 from the start."""
+    from oracle.pyoracle import BlockSet
+    rng = np.random.default_rng(d + g)
+    n, hkv = 300, 2
+    raw = random_blockset(rng, n, d, 16, 16, planted_frac=0.05, skew=4.0, ids=np.arange(n) * 3 + 1)
+    blocks = [raw.block(i) for i in range(n)]
+    bs = BlockSet([_to_bf16_exact(k) for k, _ in blocks], [_to_bf16_exact(v) for _, v in blocks], raw.ids)
+    odd = rng.standard_normal((16, d)).astype(np.float32)  # not bf16-exact
+    mine = capi.Store(capacity=2 * n, n_layers=1)
+    f32 = capi.Store(capacity=2 * n, n_layers=1)
+    theirs = ref.store(capacity=2 * n, n_layers=1)
+    assert f32.put(10**6, odd, odd) == 0  # fp32 pool from the first block
+    for s in (mine, f32, theirs):
+        s.put_blockset(bs)
+    kv = bs.ids[rng.permutation(n)[: hkv * (n // hkv)]].reshape(hkv, -1)
+    qs = (rng.standard_normal((hkv * g, d)) * 2).astype(np.float32)
+    cfg = dict(epsilon=0.9, microbatch_size=2)
+
+    def check(tag):
+        rc, out, res, un = mine.run_multi_head(qs, list(kv), capi.config_default(**cfg))
+        assert rc == 0, capi.last_error()
+        rc2, out2, res2, _ = f32.run_multi_head(qs, list(kv), capi.config_default(**cfg))
+        assert rc2 == 0, capi.last_error()
+        want, wuni = theirs.multi_head(qs, kv, make_config(**cfg))
+        if all(r.blocks_processed == w.blocks_processed for r, w in zip(res, want)):
+            for h in range(hkv * g):
+                assert max_abs(out[h], want[h].output) <= OUT_TOL, tag
+            assert un == wuni.size
+            assert mine.stats() == theirs.stats()
+        if all(r.blocks_processed == w.blocks_processed for r, w in zip(res2, res)):
+            assert max_abs(out, out2) <= OUT_TOL, tag
+
+    check("bf16 pool")
+    assert mine.put(10**6, odd, odd) == 0  # moves the 300 stored blocks to an fp32 pool
+    theirs.put(10**6, odd, odd)
+    check("after the move")
