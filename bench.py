@@ -368,7 +368,7 @@ def dropin_e2e(args, p, groups, n, g, seconds=2.0):
     v_unit, c_unit, s_unit = timed(calls_unit)
     st.close()
     return dict(value=v_layer, unit=UNIT, calls=c_layer, seconds=round(s_layer, 3),
-                groups=[[int(r), int(l)] for r, l in groups], kv_dtype="f32 (C ABI put_block)",
+                groups=[[int(r), int(l)] for r, l in groups], kv_dtype="fp32 host blocks via put_block (bf16-exact values: stored losslessly as bf16)",
                 api=f"psattn_run_multi_head per (request, layer): {args.hq} q-heads over {hkv} kv-head lists of "
                     f"{n} blocks, host buffers",
                 per_kv_head=dict(value=v_unit, unit=UNIT, calls=c_unit, seconds=round(s_unit, 3),

@@ -476,13 +476,35 @@ void TieredBlockStore::run_device(const detail::DeviceQueryBatch& qb, detail::De
     const bool has_oracle = b.ranking_mode == PSATTN_RANK_ORACLE || b.audit_coverage;
     const size_t om_b = has_oracle ? static_cast<size_t>(hbt) * 8 : 0;
     char* hout = static_cast<char*>(dev_->h_out.get(out_total + om_b + 256));
-    check_cuda(cudaMemcpyAsync(hout, dout, out_total, cudaMemcpyDeviceToHost, dev_->stream), "D2H");
+    // Compact read-back (equal-length lists, no oracle masses): the per-query scalars first, then
+    // only ranks below the largest blocks_processed of the rank positions and estimates (one 2-D
+    // copy each: rows of n entries, max_bp wide) instead of every rank of every list.
+    bool compact = !has_oracle && !qb.rank_only;
+    for (int u = 0; compact && u < n_units; ++u) compact = off[u + 1] - off[u] == max_n;
+    const size_t head_b = ob_out + ob_bp + ob_est + ob_tc + ob_term;
+    std::int64_t rows_w = 0;  // compact: entries kept per (unit, head) row
+    check_cuda(cudaMemcpyAsync(hout, dout, compact ? head_b : out_total, cudaMemcpyDeviceToHost, dev_->stream), "D2H");
     if (has_oracle) {
         // workspace layout: keys | rpos | omass (psattn_batch_workspace_bytes)
         const size_t om_off = align256(static_cast<size_t>(hbt) * 8) + align256(static_cast<size_t>(hbt) * 4);
         check_cuda(cudaMemcpyAsync(hout + out_total, static_cast<char*>(ws) + om_off, om_b, cudaMemcpyDeviceToHost,
                                    dev_->stream),
                    "D2H");
+    }
+    if (compact) {
+        check_cuda(cudaStreamSynchronize(dev_->stream), "PSA device launch");
+        const auto* bp0 = reinterpret_cast<const std::int64_t*>(hout + ob_out);
+        for (std::int64_t qi = 0; qi < nq; ++qi) rows_w = std::max(rows_w, std::clamp<std::int64_t>(bp0[qi], 0, max_n));
+        if (rows_w > 0) {
+            const size_t w4 = static_cast<size_t>(rows_w) * 4, w8 = static_cast<size_t>(rows_w) * 8;
+            check_cuda(cudaMemcpy2DAsync(hout + head_b, w4, dout + head_b, static_cast<size_t>(max_n) * 4, w4,
+                                         static_cast<size_t>(nq), cudaMemcpyDeviceToHost, dev_->stream),
+                       "D2H");
+            check_cuda(cudaMemcpy2DAsync(hout + head_b + ob_rpos, w8, dout + head_b + ob_rpos,
+                                         static_cast<size_t>(max_n) * 8, w8, static_cast<size_t>(nq),
+                                         cudaMemcpyDeviceToHost, dev_->stream),
+                       "D2H");
+        }
     }
     if (prof) cudaEventRecord(pev[2], dev_->stream);
     const double t_launched = prof ? us_since(t_begin) : 0.0;
@@ -515,7 +537,7 @@ void TieredBlockStore::run_device(const detail::DeviceQueryBatch& qb, detail::De
         if (qb.want_union) seen.assign(static_cast<std::size_t>(n), 0);
         for (int h = 0; h < g; ++h) {
             const std::int64_t qi = static_cast<std::int64_t>(u) * g + h;
-            const std::int64_t hb = off[u] * g + h * n;
+            const std::int64_t hb = compact ? qi * rows_w : off[u] * g + h * n;  // row of query qi
             // psattn_run_batch defines ranks below blocks_processed only (it orders lazily)
             const std::int64_t nr = qb.rank_only ? n : std::clamp<std::int64_t>(bp[qi], 0, n);
             auto& ids = res.ranked_ids[qi];
