@@ -20,20 +20,20 @@ if [[ $what == all || $what == bench ]]; then
 fi
 if [[ $what == all || $what == ncu ]]; then
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
-     --log-file gpurun_out/launches_$tag.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline \
+     --log-file gpurun_out/launches_$tag.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --dropin-groups 0 --check 0 \
      > gpurun_out/ncu_launch_bench_$tag.log 2>&1; echo "ncu launches rc=$?"
-  for k in score_kernel psa_gqa_kernel first_tranche_kernel; do
+  for k in score_kernel psa_stream_kernel first_tranche_kernel; do
     timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k --launch-skip 2 -c 1 \
-       -o gpurun_out/${tag}_$k -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline \
+       -o gpurun_out/${tag}_$k -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline --dropin-groups 0 --check 0 \
        > gpurun_out/ncu_full_${k}_$tag.log 2>&1; echo "ncu $k rc=$?"
   done
   # isotropic keys: the dense hand-over kernels carry the step
   timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
      -k regex:"psa|score|dense|first" --launch-skip 7 -c 7 --csv --log-file gpurun_out/launches_iso_$tag.csv \
-     python bench.py --steps 1 --warmup 3 --no-cpu-baseline --dist iso > /dev/null 2>&1; echo "ncu iso rc=$?"
+     python bench.py --steps 1 --warmup 3 --no-cpu-baseline --dropin-groups 0 --check 0 --dist iso > /dev/null 2>&1; echo "ncu iso rc=$?"
   for k in dense_k_kernel dense_v_kernel dense_decide_kernel; do
     timeout 900 ncu --set full --clock-control none --import-source on -k regex:$k --launch-skip 1 -c 1 \
-       -o gpurun_out/${tag}_$k -f python bench.py --steps 1 --warmup 1 --no-cpu-baseline --dist iso \
+       -o gpurun_out/${tag}_$k -f python bench.py --steps 1 --warmup 1 --no-cpu-baseline --dropin-groups 0 --check 0 --dist iso \
        > gpurun_out/ncu_full_${k}_$tag.log 2>&1; echo "ncu $k rc=$?"
   done
 fi
