@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <array>
+#include <atomic>
 #include <mutex>
 #include <cmath>
 #include <string>
@@ -42,6 +43,7 @@ struct Profiler {
     int64_t count[4] = {0, 0, 0, 0};
 };
 Profiler g_prof;
+std::atomic<uint64_t> g_knob_gen{0};  // bumped by every psattn_set_* / psattn_profile_enable
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 }  // namespace
@@ -600,10 +602,18 @@ int psattn_rank_batch(psattn_pool* pool, const psattn_batch* b, void* workspace,
 int psattn_set_progressive_kernel(int32_t mode) {
     if (mode < 0 || mode > 3) return fail(PSATTN_ERR_INVALID_ARGUMENT, "progressive kernel mode must be 0, 1, 2 or 3");
     set_psa_kernel_choice(mode);
+    g_knob_gen.fetch_add(1);
     return PSATTN_OK;
 }
 
 }  // extern "C"
+
+namespace psa {
+uint64_t launch_config_generation() {
+    std::lock_guard<std::mutex> lk(g_prof.mu);
+    return g_prof.on ? ~0ull : g_knob_gen.load();  // ~0: profiling (no graph reuse)
+}
+}  // namespace psa
 
 struct psattn_graph {
     cudaGraph_t graph = nullptr;
@@ -660,34 +670,40 @@ void psattn_graph_destroy(psattn_graph* g) {
 int psattn_set_dense(int32_t mode) {
     if (mode < 0 || mode > 1) return fail(PSATTN_ERR_INVALID_ARGUMENT, "psattn_set_dense: mode must be 0 or 1");
     set_dense_mode(mode);
+    g_knob_gen.fetch_add(1);
     return PSATTN_OK;
 }
 
 int psattn_set_dense_early(float nats) {
     if (!(nats >= 0.0f)) return fail(PSATTN_ERR_INVALID_ARGUMENT, "psattn_set_dense_early: threshold must be >= 0");
     set_dense_early(nats);
+    g_knob_gen.fetch_add(1);
     return PSATTN_OK;
 }
 
 int psattn_set_dense_partial(int32_t ranks) {
     if (ranks < 0) return fail(PSATTN_ERR_INVALID_ARGUMENT, "psattn_set_dense_partial: ranks must be >= 0");
     set_dense_partial(ranks);
+    g_knob_gen.fetch_add(1);
     return PSATTN_OK;
 }
 
 int psattn_set_score_kernel(int32_t mode) {
     if (mode < 0 || mode > 3) return fail(PSATTN_ERR_INVALID_ARGUMENT, "score kernel mode must be 0..3");
     set_score_kernel_choice(mode);
+    g_knob_gen.fetch_add(1);
     return PSATTN_OK;
 }
 
 int psattn_set_pipeline(int32_t sub_batches) {
     if (sub_batches < 0 || sub_batches > 16) return fail(PSATTN_ERR_INVALID_ARGUMENT, "sub_batches must be in [0, 16]");
     set_pipeline_subbatches(sub_batches);
+    g_knob_gen.fetch_add(1);
     return PSATTN_OK;
 }
 
 int psattn_profile_enable(int32_t enable) {
+    g_knob_gen.fetch_add(1);
     std::lock_guard<std::mutex> lk(g_prof.mu);
     g_prof.on = enable != 0;
     return PSATTN_OK;

@@ -25,6 +25,9 @@ int pool_put(psattn_pool* pool, int64_t n, const int32_t* slots, const int32_t* 
 int read_slot(const psattn_pool* pool, int64_t slot, int32_t ntok, float* keys, float* values);
 int read_meta(const psattn_pool* pool, int64_t slot, float* mean, float* lo, float* hi);
 int cuda_fail(cudaError_t e, const char* what);
+// Changes whenever a launch-shaping knob (psattn_set_*) changes; ~0 while profiling is on. A
+// captured launch sequence is reusable while this and its inputs are unchanged.
+uint64_t launch_config_generation();
 // psattn_run_batch internals shared with the audit/tradeoff tooling (tradeoff.cu).
 int validate_batch(const psattn_pool* pool, const psattn_batch* b);
 size_t ws_omass_offset(const psattn_batch* b);

@@ -307,3 +307,52 @@ def test_lossless_bf16_store_and_migration(capi, ref, d, g):
     assert mine.put(10**6, odd, odd) == 0  # moves the 300 stored blocks to an fp32 pool
     theirs.put(10**6, odd, odd)
     check("after the move")
+
+
+def test_repeated_queries_across_pool_growth_and_knobs(capi, ref):
+    """The store replays a captured launch sequence for a repeated query shape: it
+    must see blocks put since (contents), a pool that grew (new device buffers), and launch knobs
+    changed in between (psattn_set_*), each time matching the compiled reference."""
+    import ctypes as C
+    rng = np.random.default_rng(77)
+    from oracle.pyoracle import BlockSet
+    d, g = 128, 4  # bf16-exact values: the bf16 pool, stream kernel and dense hand-over
+
+    def exact(b):
+        blocks = [b.block(i) for i in range(b.ids.size)]
+        return BlockSet([_to_bf16_exact(k) for k, _ in blocks], [_to_bf16_exact(v) for _, v in blocks], b.ids)
+    mine = capi.Store(capacity=4096, n_layers=1)
+    theirs = ref.store(capacity=4096, n_layers=1)
+    ids = np.arange(200, dtype=np.int64)
+    bs = exact(random_blockset(rng, ids.size, d, 16, 16, planted_frac=0.1, ids=ids))
+    for s in (mine, theirs):
+        s.put_blockset(bs)
+    qs = (rng.standard_normal((g, d)) * 2).astype(np.float32)
+    cfg = dict(epsilon=0.9, microbatch_size=1)
+
+    def run(lst):
+        rc, out, res, un = mine.run_multi_head(qs, [lst], capi.config_default(**cfg))
+        assert rc == 0, capi.last_error()
+        want, wuni = theirs.multi_head(qs, lst[None, :], make_config(**cfg))
+        if all(r.blocks_processed == w.blocks_processed for r, w in zip(res, want)):
+            assert max_abs(out, np.stack([w.output for w in want])) <= OUT_TOL
+            assert un == wuni.size
+            assert mine.stats() == theirs.stats()
+
+    for _ in range(3):
+        run(ids)
+    # overwrite nothing, but put 600 more blocks: the pool doubles (new device buffers)
+    more = np.arange(1000, 1600, dtype=np.int64)
+    bs2 = exact(random_blockset(rng, more.size, d, 16, 16, planted_frac=0.2, ids=more))
+    for s in (mine, theirs):
+        s.put_blockset(bs2)
+    for _ in range(2):
+        run(ids)
+    both = np.concatenate([ids, more[:56]])  # a new shape
+    run(both)
+    try:
+        assert capi.lib.psattn_set_dense_partial(C.c_int32(0)) == 0
+        run(ids)
+        run(both)
+    finally:
+        capi.lib.psattn_set_dense_partial(C.c_int32(1024))
