@@ -79,4 +79,20 @@ for i in range(24):
     capi.check(st.put(i, kk, kk))
 capi.check(st.run_query(rng2.standard_normal(64).astype(np.float32), np.arange(24), capi.config_default(epsilon=0.9))[0])
 torch.cuda.synchronize()
+# drop-in store, bf16-exact values: lossless bf16 pool (stream kernel), run_multi_head over two
+# kv-head lists twice (the second replays the captured graph; compact read-back), then a block
+# that is not bf16-exact moves the pool to fp32 and the query runs again
+st2 = capi.Store(capacity=1024)
+n2 = 600
+kb = rng2.standard_normal((n2, 16, 128)).astype(np.float32)
+kb = (kb.view(np.uint32) & 0xFFFF0000).view(np.float32)
+st2.put_many(0, kb, kb)
+q2 = rng2.standard_normal((8, 128)).astype(np.float32)
+lists2 = [np.arange(0, 300, dtype=np.int64), np.arange(300, 600, dtype=np.int64)]
+for _ in range(2):
+    capi.check(st2.run_multi_head(q2, lists2, capi.config_default(epsilon=0.95))[0])
+odd = rng2.standard_normal((16, 128)).astype(np.float32)
+capi.check(st2.put(10_000, odd, odd))
+capi.check(st2.run_multi_head(q2, lists2, capi.config_default(epsilon=0.95))[0])
+torch.cuda.synchronize()
 print("sanitize driver ok")
